@@ -1,0 +1,415 @@
+"""Benchmark: 1080p training iterations/s and render FPS, 3M Gaussians SH3 (BASELINE.json).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (BASELINE configs[2], "c3"): the SURVEY §8(d) frustum generator,
+3,000,000 Gaussians, SH degree 3, one 1920x1080 camera; a step is one
+training iteration: project -> bin/sort -> forward blend -> L1+D-SSIM loss
+(lambda 0.2) -> backward blend -> backward preprocess (+densify stats) ->
+fused Adam.  Multi-GPU (torchrun): one process per GPU, each rank trains on
+its own view of the replicated scene per step, gradients are summed with an
+NCCL all-reduce, every rank runs the identical Adam (weak scaling).
+
+The reference arm (--impl reference) times the float64 C oracle port of the
+reference hot path (oracle/, pinned to splatlab's own outputs) on the host
+cores, rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "1080p render FPS + fwd/bwd train iters/sec, 3M Gaussians SH3, 1/2/4/8 B200"
+UNIT = "train_iters/s"
+N_GAUSS = 3_000_000
+WIDTH, HEIGHT = 1920, 1080
+DEGREE = 3
+LAMBDA_DSSIM = 0.2
+
+
+def peaks() -> dict:
+    try:
+        return json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+    except Exception:
+        return {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.QUERY}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        self.proc.wait(timeout=5)
+        rows = [r.split(",") for r in Path(self.path).read_text().strip().splitlines() if r.strip()]
+        os.unlink(self.path)
+        sm = [float(r[1]) for r in rows if len(r) >= 9 and r[1].strip().replace(".", "").isdigit()]
+        smax = [float(r[2]) for r in rows if len(r) >= 9 and r[2].strip().replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows if len(r) >= 9 for i in range(4) if "Active" in r[5 + i]
+                          and "Not" not in r[5 + i]})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ---------------------------------------------------------------------------
+# our arm
+
+def run_ours(args, rank: int, world: int, local_rank: int) -> None:
+    import torch
+    import torch.distributed as dist
+
+    from paper_2308_04079_b200 import _lib, synthetic
+    from paper_2308_04079_b200 import rasterizer as R
+    from paper_2308_04079_b200.camera import Camera
+    from paper_2308_04079_b200.cloud import GaussianCloud
+    from paper_2308_04079_b200.loss import l1_dssim_loss
+    from paper_2308_04079_b200.optimizer import DeviceAdam, TrainConfig
+    from paper_2308_04079_b200.profiling import StageTimer
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    _lib.load()
+    n = args.n_gaussians
+    cloud_np, cam0 = synthetic.frustum_scene(n, WIDTH, HEIGHT, seed=0)
+    cloud = GaussianCloud.from_numpy(**cloud_np, device=dev)
+    del cloud_np
+    # each rank renders its own view: the frustum camera panned by a small per-rank offset
+    def view_for(r: int) -> Camera:
+        return Camera(np.eye(3), np.array([0.02 * r, -0.01 * r, 0.0]), cam0.fx, cam0.fy, cam0.cx, cam0.cy,
+                      WIDTH, HEIGHT, cam0.near)
+    cam = view_for(rank)
+    # target image: render of the same generator with seed 1
+    tgt_np, _ = synthetic.frustum_scene(n, WIDTH, HEIGHT, seed=1)
+    target_cloud = GaussianCloud.from_numpy(**tgt_np, device=dev)
+    del tgt_np
+    bg = (0.0, 0.0, 0.0)
+    with torch.no_grad():
+        target, _, _ = R.render_view(target_cloud, cam, bg, DEGREE)
+    target = target.image.contiguous()
+    del target_cloud
+    torch.cuda.synchronize()
+
+    config = TrainConfig(lambda_dssim=LAMBDA_DSSIM)
+    adam = DeviceAdam(cloud)
+    stats = R.DensifyStats.zeros(n, dev)
+    grads = R.GaussianGrads.zeros(n, dev)
+    flat = None
+    if world > 1:
+        # gradients live in one flat buffer so one NCCL all-reduce covers every group
+        sizes = [n * 3, n * 4, n * 3, n, n * 48]
+        flat = torch.zeros(sum(sizes), dtype=torch.float32, device=dev)
+        parts = torch.split(flat, sizes)
+        grads = R.GaussianGrads(parts[0].view(n, 3), parts[1].view(n, 4), parts[2].view(n, 3), parts[3].view(n),
+                                parts[4].view(n, 16, 3), torch.zeros(n, device=dev))
+    timer = StageTimer(enabled=True)
+    iteration = [0]
+
+    def train_step(gt: torch.Tensor, timed: bool) -> torch.Tensor:
+        iteration[0] += 1
+        tm = timer if timed else None
+        params = cloud.c_params()
+        with StageTimer.stage(tm, "preprocess_fwd"):
+            splats = R._project_tensors(params, n, dev, cam, DEGREE)
+        with StageTimer.stage(tm, "bin_and_sort"):
+            binning = R.bin_and_sort(splats, WIDTH, HEIGHT)
+        with StageTimer.stage(tm, "blend_fwd"):
+            out = R.render_forward(splats, binning, WIDTH, HEIGHT, bg, training=True)
+        with StageTimer.stage(tm, "loss"):
+            loss, d_image = l1_dssim_loss(out.image, gt, LAMBDA_DSSIM)
+        with StageTimer.stage(tm, "blend_bwd"):
+            g2 = R.render_backward(d_image, out, splats, binning, WIDTH, HEIGHT, bg)
+        with StageTimer.stage(tm, "preprocess_bwd"):
+            R._backward_project_tensors(params, n, dev, cam, splats, g2, DEGREE, stats, grads, False)
+        if flat is not None:
+            with StageTimer.stage(tm, "allreduce"):
+                dist.all_reduce(flat)
+        with StageTimer.stage(tm, "adam"):
+            adam.step(cloud, grads, iteration[0], config)
+        if timed:
+            timer.note_instances(binning.num_instances, out)
+        return loss
+
+    for _ in range(args.warmup):
+        train_step(target, False)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    start.record()
+    for _ in range(args.steps):
+        train_step(target, True)
+    end.record()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = start.elapsed_time(end)
+    clock_info = clocks.stop()
+    ms_t = torch.tensor([ms], device=dev)
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms_max = float(ms_t.item())
+
+    # end-to-end through the public API: drop-in autograd Function + Adam,
+    # target image H2D from pinned host memory each step, loss D2H each step
+    gt_host = target.cpu().pin_memory()
+    leaves = [p.detach().clone().requires_grad_(True) for p in cloud.params()]
+    e2e_adam_cloud = GaussianCloud(means=leaves[0].data, rotations=leaves[2].data, log_scales=leaves[1].data,
+                                   opacity_logits=leaves[3].data, sh=leaves[4].data)
+    e2e_adam = DeviceAdam(e2e_adam_cloud)
+    e2e_it = [0]
+
+    def e2e_step() -> float:
+        e2e_it[0] += 1
+        gt = gt_host.to(dev, non_blocking=True)
+        for leaf in leaves:
+            leaf.grad = None
+        image, radii = R.rasterize_gaussians(*leaves, cam, bg, DEGREE, stats)
+        loss, d_image = l1_dssim_loss(image.detach(), gt, LAMBDA_DSSIM)
+        image.backward(d_image)
+        g = R.GaussianGrads(leaves[0].grad, leaves[2].grad, leaves[1].grad, leaves[3].grad, leaves[4].grad,
+                            stats.accum_pos_grad)
+        if world > 1:
+            for leaf in leaves:
+                dist.all_reduce(leaf.grad)
+        e2e_adam.step(e2e_adam_cloud, g, e2e_it[0], config)
+        return float(loss.item())   # D2H of the step's loss
+
+    for _ in range(args.warmup):
+        e2e_step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        e2e_step()
+    e1.record()
+    torch.cuda.synchronize()
+    e_ms = torch.tensor([e0.elapsed_time(e1)], device=dev)
+    if world > 1:
+        dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
+    e2e_ms = float(e_ms.item())
+    del leaves, e2e_adam, e2e_adam_cloud
+
+    # inference render FPS (forward only, same scene, same camera)
+    fps_steps = max(args.steps, 10)
+    for _ in range(3):
+        R.render_view(cloud, cam, bg, DEGREE)
+    torch.cuda.synchronize()
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    f0.record()
+    for _ in range(fps_steps):
+        R.render_view(cloud, cam, bg, DEGREE)
+    f1.record()
+    torch.cuda.synchronize()
+    render_ms = f0.elapsed_time(f1) / fps_steps
+
+    if rank != 0:
+        return
+    ms_per_step = ms_max / args.steps
+    value = world * args.steps / (ms_max / 1e3)
+    e2e_value = world * args.steps / (e2e_ms / 1e3)
+    stage_ms = timer.mean_ms()
+    roof = timer.roofline(n, WIDTH, HEIGHT, peaks())
+    line = {
+        "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32 (f64 projection geometry)",
+        "data": "synthetic (SURVEY §8(d) frustum generator, seed 0; target = seed-1 render)",
+        "config": {"workload": "c3: 3M Gaussians SH3, 1920x1080, train step (fwd + L1/D-SSIM loss + bwd + "
+                               "fused Adam + densify stats)", "gaussians": n, "width": WIDTH, "height": HEIGHT,
+                   "sh_degree": DEGREE, "views_per_step": world, "parallelism": f"dp{world} (view-parallel)",
+                   "l2": "inputs larger than L2 (708 MB parameters + 2.1 GB Adam state)"},
+        "render_fps": round(1e3 / render_ms, 2), "render_ms": round(render_ms, 4),
+        "stage_ms": {k: round(v, 4) for k, v in stage_ms.items()},
+        "instances_per_view": timer.last_k, "evaluated_pairs_per_view": timer.last_e,
+        "e2e": {"value": round(e2e_value, 3), "unit": UNIT, "h2d_bytes_per_step": WIDTH * HEIGHT * 3 * 4,
+                "d2h_bytes_per_step": 4, "path": "GaussianRasterizer autograd.Function + DeviceAdam, "
+                                                 "target image from pinned host memory"},
+        "gpu_launches": timer.launches_per_step() * args.steps,
+        "roofline": roof["primary"], "roofline_stages": roof["stages"],
+        "clocks": clock_info,
+    }
+    if args.cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline_sample(args)
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# CPU (oracle port) arm
+
+def _cpu_scene(n):
+    from paper_2308_04079_b200 import synthetic
+    cloud, cam = synthetic.frustum_scene(n, WIDTH, HEIGHT, seed=0)
+    return synthetic.round_to_f32(cloud), cam
+
+
+def cpu_step_timings(cloud, cam, band: int, bands: int, adam_state: dict, it: int) -> dict:
+    """One sampled training step of the oracle port: per-Gaussian stages over all
+    N; the pixel stages (bin/sort, blend fwd, loss, blend bwd) over one band of
+    tile rows (1/bands of the frame).  Returns stage seconds."""
+    from oracle import oracle as O
+    t = {}
+    s = time.perf_counter()
+    proj = O.project(cloud, cam, DEGREE)
+    t["project"] = time.perf_counter() - s
+    ty = (HEIGHT + 15) // 16
+    r0, r1 = band * ty // bands, (band + 1) * ty // bands
+    proj_b = dict(proj)
+    rect = proj["rect"].copy()
+    keep = (proj["tiles"] > 0) & (rect[:, 3] >= r0) & (rect[:, 1] < r1)
+    rect[:, 1] = np.clip(rect[:, 1], r0, r1 - 1)
+    rect[:, 3] = np.clip(rect[:, 3], r0, r1 - 1)
+    proj_b["rect"] = rect
+    proj_b["tiles"] = np.where(keep, (rect[:, 2] - rect[:, 0] + 1) * (rect[:, 3] - rect[:, 1] + 1), 0).astype(
+        np.int64)
+    s = time.perf_counter()
+    bins = O.bin_and_sort(proj_b, WIDTH, HEIGHT)
+    t["bin_and_sort"] = time.perf_counter() - s
+    s = time.perf_counter()
+    fwd = O.render_forward(proj_b, bins, WIDTH, HEIGHT, (0.0, 0.0, 0.0))
+    t["blend_fwd"] = time.perf_counter() - s
+    s = time.perf_counter()
+    d_image = np.sign(fwd["image"] - 0.5) * (1.0 - LAMBDA_DSSIM) / fwd["image"].size  # L1 part only (host)
+    t["loss_l1"] = time.perf_counter() - s
+    s = time.perf_counter()
+    g2 = O.render_backward(d_image, proj_b, bins, fwd, WIDTH, HEIGHT, (0.0, 0.0, 0.0))
+    t["blend_bwd"] = time.perf_counter() - s
+    s = time.perf_counter()
+    grads = O.backward_project(cloud, cam, DEGREE, proj, g2)
+    t["preprocess_bwd"] = time.perf_counter() - s
+    s = time.perf_counter()
+    gmap = {"means": "d_means", "log_scales": "d_log_scales", "rotations": "d_rotations",
+            "opacity_logits": "d_opacity_logits", "sh": "d_sh"}
+    for k, gk in gmap.items():
+        st = adam_state[k]
+        O.adam_group(st["p"], grads[gk], st["m"], st["v"], 1e-3, 0.9, 0.999, 1e-15, it,
+                     **({"lr_head": 2.5e-3, "period": 48, "head": 3} if k == "sh" else {}))
+    t["adam"] = time.perf_counter() - s
+    t["K_band"] = int(bins["ids"].shape[0])
+    return t
+
+
+def cpu_full_step_seconds(t: dict, bands: int) -> float:
+    pixel = t["bin_and_sort"] + t["blend_fwd"] + t["loss_l1"] + t["blend_bwd"]
+    return t["project"] + t["preprocess_bwd"] + t["adam"] + bands * pixel
+
+
+def cpu_baseline_sample(args) -> dict:
+    from oracle import oracle as O
+    cloud, cam = _cpu_scene(args.n_gaussians)
+    state = {k: {"p": cloud[k].copy(), "m": np.zeros_like(cloud[k]), "v": np.zeros_like(cloud[k])} for k in cloud}
+    bands = 8
+    t = cpu_step_timings(cloud, cam, 3, bands, state, 1)
+    full = cpu_full_step_seconds(t, bands)
+    return {"value": round(1.0 / full, 5), "unit": UNIT, "cores": O.num_threads(), "kind": "port",
+            "sample": f"one oracle training step: project/backward_project/Adam over all {args.n_gaussians} "
+                      f"Gaussians + bin/blend fwd/bwd over 1/{bands} of the tile rows; full-frame step "
+                      f"= per-Gaussian stages + {bands} x band stages = {full:.2f} s",
+            "stage_s": {k: round(v, 4) if isinstance(v, float) else v for k, v in t.items()}}
+
+
+def run_reference(args, rank: int, world: int) -> None:
+    if rank != 0:
+        return
+    from oracle import oracle as O
+    cloud, cam = _cpu_scene(args.n_gaussians)
+    state = {k: {"p": cloud[k].copy(), "m": np.zeros_like(cloud[k]), "v": np.zeros_like(cloud[k])} for k in cloud}
+    bands = 8
+    it = 0
+    for _ in range(args.warmup):
+        it += 1
+        cpu_step_timings(cloud, cam, it % bands, bands, state, it)
+    fulls = []
+    for _ in range(args.steps):
+        it += 1
+        fulls.append(cpu_full_step_seconds(cpu_step_timings(cloud, cam, it % bands, bands, state, it), bands))
+    total = sum(fulls)
+    value = args.steps / total
+    line = {
+        "metric": METRIC, "value": round(value, 5), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(1e3 * total / args.steps, 2), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (same generator, seed 0)",
+        "config": {"workload": "c3: 3M Gaussians SH3, 1920x1080, train step", "gaussians": args.n_gaussians,
+                   "width": WIDTH, "height": HEIGHT, "sh_degree": DEGREE},
+        "impl": "reference",
+        "cpu_baseline": {"value": round(value, 5), "unit": UNIT, "cores": O.num_threads(), "kind": "port",
+                         "sample": f"float64 C oracle port of splatlab's hot path; each step: per-Gaussian "
+                                   f"stages over all N + bin/blend over 1/{bands} of the tile rows (rotating), "
+                                   f"full-frame time extrapolated as per-Gaussian + {bands} x band"},
+        "e2e": {"value": round(value, 5), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--n-gaussians", type=int, default=N_GAUSS)
+    ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_ours(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

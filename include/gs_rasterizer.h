@@ -1,0 +1,206 @@
+/*
+ * gs_rasterizer.h — C ABI of the B200-native differentiable Gaussian-splatting
+ * rasterizer (libgs_b200.so).
+ *
+ * This is the drop-in boundary for the hot path of arXiv 2308.04079 as the
+ * reference package `splatlab` (/root/reference/pkg/src/splatlab) structures
+ * it.  The reference has no native FFI: its hot path is the Python function
+ * trio render_view / render_backward / backward_project plus the Adam step.
+ * Every entry point below replaces one of those functions (or one stage
+ * inside them) and is bound from Python through ctypes.
+ *
+ * Conventions
+ *   - All array arguments are DEVICE pointers owned by the caller (torch's
+ *     caching allocator in the Python host layer).  The library never
+ *     allocates or frees device memory and keeps no global mutable state.
+ *   - Work is enqueued on the caller's stream (`stream` is a cudaStream_t
+ *     passed as void*; NULL = legacy default stream).  Only gs_bin_and_sort
+ *     synchronises that stream once (to read the instance count K).
+ *   - Parameter layouts are the reference's (core.py:36-50): means (N,3),
+ *     rotations (N,4) raw (r,i,j,k) quaternions, log_scales (N,3),
+ *     opacity_logits (N,), sh (N,16,3) coefficient-major / channel-minor.
+ *     Device arithmetic: float32 storage; the projection geometry (view
+ *     transform, EWA covariance, radius, tile rectangle, depth) runs in
+ *     float64 so radii, keys and tile ranges match the float64 reference.
+ *   - Return value: GS_OK or a GS_ERR_* code.  The Python host layer maps the
+ *     codes to the reference's exception types.
+ */
+#ifndef GS_RASTERIZER_H
+#define GS_RASTERIZER_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GS_ABI_VERSION 1
+#define GS_TILE_SIZE 16        /* rasterizer.py:13 TILE_SIZE */
+#define GS_SH_COEFFS 16        /* sh.py:25 NUM_COEFFS */
+#define GS_REC_FLOATS 12       /* floats per projected-splat record, see gs_splats_t */
+#define GS_GRAD2D_FLOATS 12    /* floats per screen-space gradient row, see gs_blend_backward */
+
+enum gs_status {
+  GS_OK = 0,
+  GS_ERR_INVALID_ARG = 1,      /* ValueError: bad camera / SH degree (core.py:135-141, sh.py:37-38),
+                                  backward without training record (rasterizer.py:265-266)          */
+  GS_ERR_ZERO_QUATERNION = 2,  /* InvalidPrimitiveError (core.py:164-165)                          */
+  GS_ERR_RESOURCE_LIMIT = 3,   /* ResourceLimitError: > 2^32-1 tiles or > 2^31 instances
+                                  (rasterizer.py:76-79, 99-101)                                    */
+  GS_ERR_CAPACITY = 4,         /* caller's instance buffers hold fewer than K entries;
+                                  *k_out carries the K required                                    */
+  GS_ERR_CUDA = 5              /* a CUDA runtime error; see gs_last_cuda_error()                    */
+};
+
+/* Pinhole camera (core.py:113-146).  View space x-right, y-down, z-forward;
+ * pixel centres at (col+0.5, row+0.5). */
+typedef struct gs_camera {
+  double rotation[9];          /* world-to-view rotation, row-major */
+  double translation[3];       /* world-to-view translation */
+  double fx, fy, cx, cy;
+  int32_t width, height;
+  double near_plane;           /* Camera.near, default 0.2 */
+} gs_camera_t;
+
+/* Raw Gaussian parameters (GaussianCloud, core.py:36-50), float32, device. */
+typedef struct gs_params {
+  const float* means;          /* (N,3) */
+  const float* rotations;      /* (N,4) raw quaternion, normalised on use */
+  const float* log_scales;     /* (N,3) */
+  const float* opacity_logits; /* (N,)  */
+  const float* sh;             /* (N,16,3) */
+  int64_t n;
+} gs_params_t;
+
+/* Per-view projected splats, N rows indexed by Gaussian (the device
+ * counterpart of ProjectedSplats, core.py:236-263, kept in N-space instead of
+ * compacted; a row is a survivor of project() iff radii[row] > 0).
+ *
+ *   rec (N,12) float32, three 16-byte words per row:
+ *     [0..3]  mean2d.x (hi), mean2d.y (hi), alpha, mean2d.x (lo)
+ *     [4..7]  conic a, conic b, conic c, mean2d.y (lo)
+ *     [8..11] color r, g, b, clamp mask (bits 0..2 as float: channel active)
+ *   mean2d = hi + lo reproduces the float64 screen position to ~2^-48.
+ *   depth (N,)  float32 view-space z (the sort key's source, rasterizer.py:61)
+ *   radii (N,)  int32 ceil(3 sqrt(lambda_max)), 0 = culled
+ *   rect  (N,4) int32 clipped inclusive tile rectangle x0,y0,x1,y1
+ *   tiles_touched (N,) int32 (x1-x0+1)(y1-y0+1) or 0 (rasterizer.py:86-97)
+ *   status (1,) int32 device word; bit 0 set when a survivor had a zero quaternion.
+ * Rows with radii == 0 leave rec/depth/rect undefined. */
+typedef struct gs_splats {
+  float* rec;
+  float* depth;
+  int32_t* radii;
+  int32_t* rect;
+  int32_t* tiles_touched;
+  int32_t* status;
+  int64_t n;
+} gs_splats_t;
+
+/* Parameter gradients (GaussianGrads, gradients.py:13-27), device float32,
+ * same shapes as gs_params_t.  view_pos_grad_norm (N,) may be NULL. */
+typedef struct gs_grads {
+  float* d_means;
+  float* d_rotations;
+  float* d_log_scales;
+  float* d_opacity_logits;
+  float* d_sh;
+  float* view_pos_grad_norm;
+} gs_grads_t;
+
+/* Densification statistics (TrainState, optimizer.py:106-108, updated at
+ * optimizer.py:252-255).  Any pointer may be NULL to skip that statistic. */
+typedef struct gs_stats {
+  float* accum_pos_grad;       /* (N,) += view_pos_grad_norm for survivors */
+  int32_t* accum_count;        /* (N,) += 1 for survivors */
+  float* max_radius_frac;      /* (N,) = max(., radius / image height) */
+} gs_stats_t;
+
+/* One Adam parameter group (optimizer.py:263-293).  Elements whose index e
+ * satisfies (e % period) < head use lr_head instead of lr (the SH DC row:
+ * period 48, head 3, optimizer.py:268-269).  period <= 0 disables it. */
+typedef struct gs_adam_group {
+  float* param;
+  const float* grad;
+  float* exp_avg;
+  float* exp_avg_sq;
+  int64_t numel;
+  float lr;
+  float lr_head;
+  int32_t period;
+  int32_t head;
+} gs_adam_group_t;
+
+/* ---- library info ------------------------------------------------------ */
+int gs_abi_version(void);
+const char* gs_status_string(int status);
+/* Copies the last CUDA error string seen by the library into buf. */
+int gs_last_cuda_error(char* buf, size_t len);
+
+/* ---- K1 preprocess: replaces core.project (core.py:266-345) ------------- */
+/* Culls (near plane, guard band, det <= 0), builds the EWA conic, radius,
+ * tile rectangle, SH colour and sigmoid opacity for every Gaussian. */
+int gs_preprocess_forward(const gs_params_t* params, const gs_camera_t* camera,
+                          int32_t active_sh_degree, gs_splats_t* splats, void* stream);
+
+/* ---- K2-K5 binning: replaces rasterizer.bin_and_sort (rasterizer.py:69-124)
+ * Orders every (tile, splat) instance by (tile, float32 depth, Gaussian
+ * index) — the reference's stable sort on (tile<<32 | depth bits) — and
+ * writes the Gaussian id of every sorted instance plus per-tile [start,end)
+ * ranges (T,2) int32 (empty tiles [0,0]).  Synchronises `stream` once to
+ * read K, written to *k_out (host).  Returns GS_ERR_CAPACITY (and K) when
+ * k_capacity < K; nothing is written in that case. */
+int gs_bin_workspace_size(int64_t n, int32_t width, int32_t height, int64_t k_capacity,
+                          size_t* bytes);
+int gs_bin_and_sort(const gs_splats_t* splats, int32_t width, int32_t height,
+                    void* workspace, size_t workspace_bytes, int64_t k_capacity,
+                    uint32_t* sorted_ids, int32_t* ranges, int64_t* k_out, void* stream);
+
+/* ---- K6 forward blend: replaces rasterizer.render_forward (rasterizer.py:201-240)
+ * image (H,W,3) float32.  When training != 0, t_final (H,W) float32 and
+ * last (H,W) int32 (global sorted index of the last blended instance, -1 =
+ * none; rasterizer.py:131, 225-231) are written too. */
+int gs_blend_forward(const gs_splats_t* splats, const uint32_t* sorted_ids, const int32_t* ranges,
+                     int32_t width, int32_t height, const float background[3], int32_t training,
+                     float* image, float* t_final, int32_t* last, void* stream);
+
+/* ---- K7 backward blend: replaces rasterizer.render_backward (rasterizer.py:253-316)
+ * with gradients.backward_blend (gradients.py:30-94).
+ * grads2d (N,12) float32 is zeroed and then accumulated:
+ *   [0..3] d_mean2d.x, d_mean2d.y, d_alpha, 0
+ *   [4..7] d_conic a, b, c, 0
+ *   [8..11] d_color r, g, b, 0          (SplatGrads2D, rasterizer.py:243-250) */
+int gs_blend_backward(const float* d_image, const gs_splats_t* splats, const uint32_t* sorted_ids,
+                      const int32_t* ranges, const float* t_final, const int32_t* last,
+                      int32_t width, int32_t height, const float background[3],
+                      float* grads2d, void* stream);
+
+/* ---- K8 backward preprocess: replaces gradients.backward_project
+ * (gradients.py:192-259) and the densification statistics update of
+ * train_step (optimizer.py:252-255).  accumulate = 0 overwrites `grads`
+ * (culled rows exactly 0), 1 adds to them (multi-view batches).
+ * stats may be NULL. */
+int gs_preprocess_backward(const gs_params_t* params, const gs_camera_t* camera,
+                           int32_t active_sh_degree, const gs_splats_t* splats,
+                           const float* grads2d, const gs_grads_t* grads, int32_t accumulate,
+                           const gs_stats_t* stats, void* stream);
+
+/* ---- K9 fused Adam: replaces optimizer._adam_step (optimizer.py:263-293)
+ * over all groups in one launch; bias1 = 1-beta1^t, bias2 = 1-beta2^t. */
+int gs_adam_step(const gs_adam_group_t* groups, int32_t num_groups, double beta1, double beta2,
+                 double eps, double bias1, double bias2, void* stream);
+
+/* ---- training loss: replaces optimizer.loss
+ * (optimizer.py:141-163) with ssim_map/ssim_backward (ssim.py:50-84).
+ * image, target (H,W,3) float32; loss_out (3,) float32 device:
+ * [total loss, mean |image-target|, mean SSIM]; d_image (H,W,3) float32 =
+ * d loss / d image.  workspace: gs_loss_workspace_size bytes, device. */
+int gs_loss_workspace_size(int32_t width, int32_t height, size_t* bytes);
+int gs_l1_dssim_loss(const float* image, const float* target, int32_t width, int32_t height, double lambda_dssim,
+                     void* workspace, size_t workspace_bytes, float* loss_out, float* d_image, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GS_RASTERIZER_H */

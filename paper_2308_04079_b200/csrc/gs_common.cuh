@@ -1,0 +1,205 @@
+// gs_common.cuh — device-side constants and math shared by every kernel.
+//
+// The constants restate the reference's module-level constants
+// (core.py:13-18, rasterizer.py:13-25, sh.py:6-23).  The alpha evaluation
+// used by the forward and the backward blend is ONE inline function built
+// from non-contractible intrinsics, so both passes see bit-identical alphas
+// and therefore identical contributor sets (gradients.py:54-65).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/gs_rasterizer.h"
+
+namespace gs {
+
+constexpr int kTile = GS_TILE_SIZE;             // rasterizer.py:13
+constexpr int kTilePixels = kTile * kTile;      // 256 pixels = 256 threads per tile CTA
+constexpr double kLowpass = 0.3;                // core.py:13 LOWPASS_FLOOR
+constexpr double kGuardBand = 1.3;              // core.py:16 GUARD_BAND
+constexpr double kRadiusSigmas = 3.0;           // core.py:18 RADIUS_SIGMAS
+constexpr float kAlphaEps = 1.0f / 255.0f;      // rasterizer.py:17 ALPHA_EPS
+constexpr float kAlphaClamp = 0.99f;            // rasterizer.py:18 ALPHA_CLAMP
+constexpr float kSaturation = 0.9999f;          // rasterizer.py:19 SATURATION
+constexpr int64_t kMaxInstances = int64_t(1) << 31;    // rasterizer.py:25
+constexpr int64_t kMaxTiles = (int64_t(1) << 32) - 1;  // rasterizer.py:24
+
+// Real SH constants (sh.py:6-23).
+constexpr float kC0 = 0.28209479177387814f;
+constexpr float kC1 = 0.4886025119029199f;
+constexpr float kC2_0 = 1.0925484305920792f;
+constexpr float kC2_1 = -1.0925484305920792f;
+constexpr float kC2_2 = 0.31539156525252005f;
+constexpr float kC2_3 = -1.0925484305920792f;
+constexpr float kC2_4 = 0.5462742152960396f;
+constexpr float kC3_0 = -0.5900435899266435f;
+constexpr float kC3_1 = 2.890611442640554f;
+constexpr float kC3_2 = -0.4570457994644658f;
+constexpr float kC3_3 = 0.3731763325901154f;
+constexpr float kC3_4 = -0.4570457994644658f;
+constexpr float kC3_5 = 1.445305721320277f;
+constexpr float kC3_6 = -0.5900435899266435f;
+
+// Camera as the kernels see it (passed by value in the kernel parameters).
+struct DevCamera {
+  double R[9];
+  double t[3];
+  double center[3];   // -R^T t (core.py:143-146)
+  double fx, fy, cx, cy;
+  double near_plane;
+  int width, height;
+  int tiles_x, tiles_y;
+};
+
+__host__ inline DevCamera make_dev_camera(const gs_camera_t& c) {
+  DevCamera d;
+  for (int i = 0; i < 9; ++i) d.R[i] = c.rotation[i];
+  for (int i = 0; i < 3; ++i) d.t[i] = c.translation[i];
+  for (int i = 0; i < 3; ++i)
+    d.center[i] = -(c.rotation[0 * 3 + i] * c.translation[0] + c.rotation[1 * 3 + i] * c.translation[1] +
+                    c.rotation[2 * 3 + i] * c.translation[2]);
+  d.fx = c.fx; d.fy = c.fy; d.cx = c.cx; d.cy = c.cy;
+  d.near_plane = c.near_plane;
+  d.width = c.width; d.height = c.height;
+  d.tiles_x = (c.width + kTile - 1) / kTile;
+  d.tiles_y = (c.height + kTile - 1) / kTile;
+  return d;
+}
+
+// ---------------------------------------------------------------------------
+// Alpha of one splat at one pixel (rasterizer.py:171-177, gradients.py:54-61).
+//   power = -0.5 (a dx^2 + c dy^2) - b dx dy ; G = 0 if power > 0 else e^power
+// dx uses the split (hi, lo) screen mean so the subtraction keeps ~f64
+// accuracy at 4K coordinates.  Explicit _rn intrinsics are never fused or
+// re-associated by the compiler, which pins the bit pattern across kernels.
+struct AlphaEval {
+  float dx, dy, g, a_raw, a;   // a: clamped and eps-skipped alpha (0 = skip)
+};
+
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+__device__ __forceinline__ AlphaEval eval_alpha(float px, float py, float4 r0, float4 r1) {
+  AlphaEval e;
+  e.dx = __fsub_rn(__fsub_rn(px, r0.x), r0.w);
+  e.dy = __fsub_rn(__fsub_rn(py, r0.y), r1.w);
+  const float qa = __fmul_rn(__fmul_rn(r1.x, e.dx), e.dx);
+  const float qc = __fmul_rn(__fmul_rn(r1.z, e.dy), e.dy);
+  const float qb = __fmul_rn(__fmul_rn(r1.y, e.dx), e.dy);
+  const float power = __fsub_rn(__fmul_rn(-0.5f, __fadd_rn(qa, qc)), qb);
+  if (power > 0.0f) {
+    e.g = 0.0f;
+  } else {
+    e.g = ex2_approx(__fmul_rn(power, 1.4426950408889634f));
+  }
+  e.a_raw = __fmul_rn(r0.z, e.g);
+  float a = fminf(kAlphaClamp, e.a_raw);
+  e.a = (a < kAlphaEps) ? 0.0f : a;
+  return e;
+}
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// ---------------------------------------------------------------------------
+// Geometry (float64).  Quaternion -> rotation (core.py:170-184).
+__device__ __forceinline__ void quat_to_rot(double r, double i, double j, double k, double R[9]) {
+  R[0] = 1.0 - 2.0 * (j * j + k * k);
+  R[1] = 2.0 * (i * j - r * k);
+  R[2] = 2.0 * (i * k + r * j);
+  R[3] = 2.0 * (i * j + r * k);
+  R[4] = 1.0 - 2.0 * (i * i + k * k);
+  R[5] = 2.0 * (j * k - r * i);
+  R[6] = 2.0 * (i * k - r * j);
+  R[7] = 2.0 * (j * k + r * i);
+  R[8] = 1.0 - 2.0 * (i * i + j * j);
+}
+
+// SH basis (sh.py:32-63), float32, zero above the active degree.
+__device__ __forceinline__ void sh_basis(float x, float y, float z, int degree, float b[16]) {
+#pragma unroll
+  for (int k = 0; k < 16; ++k) b[k] = 0.0f;
+  b[0] = kC0;
+  if (degree >= 1) {
+    b[1] = -kC1 * y;
+    b[2] = kC1 * z;
+    b[3] = -kC1 * x;
+  }
+  if (degree >= 2) {
+    const float xx = x * x, yy = y * y, zz = z * z;
+    b[4] = kC2_0 * x * y;
+    b[5] = kC2_1 * y * z;
+    b[6] = kC2_2 * (2.0f * zz - xx - yy);
+    b[7] = kC2_3 * x * z;
+    b[8] = kC2_4 * (xx - yy);
+    if (degree >= 3) {
+      b[9] = kC3_0 * y * (3.0f * xx - yy);
+      b[10] = kC3_1 * x * y * z;
+      b[11] = kC3_2 * y * (4.0f * zz - xx - yy);
+      b[12] = kC3_3 * z * (2.0f * zz - 3.0f * xx - 3.0f * yy);
+      b[13] = kC3_4 * x * (4.0f * zz - xx - yy);
+      b[14] = kC3_5 * z * (xx - yy);
+      b[15] = kC3_6 * x * (xx - 3.0f * yy);
+    }
+  }
+}
+
+// d(basis)/d(direction) contracted with d_basis (sh.py:66-109):
+// returns sum_k d_basis[k] * d basis_k / d dir.
+__device__ __forceinline__ void sh_basis_vjp(float x, float y, float z, int degree, const float db[16],
+                                             float& gx, float& gy, float& gz) {
+  gx = gy = gz = 0.0f;
+  if (degree >= 1) {
+    gy += -kC1 * db[1];
+    gz += kC1 * db[2];
+    gx += -kC1 * db[3];
+  }
+  if (degree >= 2) {
+    gx += kC2_0 * y * db[4];
+    gy += kC2_0 * x * db[4];
+    gy += kC2_1 * z * db[5];
+    gz += kC2_1 * y * db[5];
+    gx += kC2_2 * (-2.0f * x) * db[6];
+    gy += kC2_2 * (-2.0f * y) * db[6];
+    gz += kC2_2 * (4.0f * z) * db[6];
+    gx += kC2_3 * z * db[7];
+    gz += kC2_3 * x * db[7];
+    gx += kC2_4 * (2.0f * x) * db[8];
+    gy += kC2_4 * (-2.0f * y) * db[8];
+  }
+  if (degree >= 3) {
+    const float xx = x * x, yy = y * y, zz = z * z;
+    gx += kC3_0 * 6.0f * x * y * db[9];
+    gy += kC3_0 * (3.0f * xx - 3.0f * yy) * db[9];
+    gx += kC3_1 * y * z * db[10];
+    gy += kC3_1 * x * z * db[10];
+    gz += kC3_1 * x * y * db[10];
+    gx += kC3_2 * (-2.0f * x * y) * db[11];
+    gy += kC3_2 * (4.0f * zz - xx - 3.0f * yy) * db[11];
+    gz += kC3_2 * 8.0f * y * z * db[11];
+    gx += kC3_3 * (-6.0f * x * z) * db[12];
+    gy += kC3_3 * (-6.0f * y * z) * db[12];
+    gz += kC3_3 * (6.0f * zz - 3.0f * xx - 3.0f * yy) * db[12];
+    gx += kC3_4 * (4.0f * zz - 3.0f * xx - yy) * db[13];
+    gy += kC3_4 * (-2.0f * x * y) * db[13];
+    gz += kC3_4 * 8.0f * x * z * db[13];
+    gx += kC3_5 * 2.0f * x * z * db[14];
+    gy += kC3_5 * (-2.0f * y * z) * db[14];
+    gz += kC3_5 * (xx - yy) * db[14];
+    gx += kC3_6 * (3.0f * xx - 3.0f * yy) * db[15];
+    gy += kC3_6 * (-6.0f * x * y) * db[15];
+  }
+}
+
+// Status plumbing shared by the C-ABI entry points.
+int record_cuda_error(cudaError_t err);
+int check_launch();
+
+}  // namespace gs

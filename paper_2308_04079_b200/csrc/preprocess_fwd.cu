@@ -1,0 +1,190 @@
+// K1 preprocess_fwd — replaces splatlab core.project (core.py:266-345) and the
+// per-splat tile rectangle of rasterizer.bin_and_sort (rasterizer.py:86-97).
+//
+// One thread per Gaussian.  The geometry chain that decides integers
+// (culling, radius, tile rectangle, float32 depth key) runs in float64 with
+// non-contracted IEEE operations, mirroring the float64 reference, so radii
+// and binning agree bit-for-bit.  Appearance (SH colour) runs in float32.
+#include "gs_common.cuh"
+
+namespace gs {
+namespace {
+
+__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
+
+__global__ void __launch_bounds__(128)
+preprocess_fwd_kernel(gs_params_t p, DevCamera cam, int degree, gs_splats_t out) {
+  const int64_t g = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (g >= p.n) return;
+
+  // view = means @ W^T + t (core.py:279)
+  const double mx = p.means[3 * g + 0], my = p.means[3 * g + 1], mz = p.means[3 * g + 2];
+  double view[3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+    view[i] = dadd(dadd(dadd(dmul(mx, cam.R[3 * i + 0]), dmul(my, cam.R[3 * i + 1])), dmul(mz, cam.R[3 * i + 2])),
+                   cam.t[i]);
+  const double x = view[0], y = view[1], z = view[2];
+
+  int32_t radius_out = 0;
+  int32_t tiles = 0;
+  // near-plane cull (core.py:281); NaN compares false and is culled like numpy
+  if (!(z >= cam.near_plane)) {
+    out.radii[g] = 0;
+    out.tiles_touched[g] = 0;
+    return;
+  }
+  // screen position and guard band (core.py:286-293)
+  const double u = dadd(__ddiv_rn(dmul(cam.fx, x), z), cam.cx);
+  const double v = dadd(__ddiv_rn(dmul(cam.fy, y), z), cam.cy);
+  const double ndc_x = __ddiv_rn(dsub(u, cam.cx), dmul(0.5, double(cam.width)));
+  const double ndc_y = __ddiv_rn(dsub(v, cam.cy), dmul(0.5, double(cam.height)));
+  if (!(fabs(ndc_x) <= kGuardBand && fabs(ndc_y) <= kGuardBand)) {
+    out.radii[g] = 0;
+    out.tiles_touched[g] = 0;
+    return;
+  }
+
+  // world covariance Sigma = M M^T, M = R(q/|q|) diag(exp(s)) (core.py:187-201)
+  const float4 qf = reinterpret_cast<const float4*>(p.rotations)[g];
+  double qr = qf.x, qi = qf.y, qj = qf.z, qk = qf.w;
+  const double qn = sqrt(dadd(dadd(dadd(dmul(qr, qr), dmul(qi, qi)), dmul(qj, qj)), dmul(qk, qk)));
+  if (qn == 0.0) {  // InvalidPrimitiveError (core.py:164-165)
+    atomicOr(out.status, 1);
+    out.radii[g] = 0;
+    out.tiles_touched[g] = 0;
+    return;
+  }
+  qr = __ddiv_rn(qr, qn); qi = __ddiv_rn(qi, qn); qj = __ddiv_rn(qj, qn); qk = __ddiv_rn(qk, qn);
+  double R[9];
+  quat_to_rot(qr, qi, qj, qk, R);
+  const double s0 = exp(double(p.log_scales[3 * g + 0]));
+  const double s1 = exp(double(p.log_scales[3 * g + 1]));
+  const double s2 = exp(double(p.log_scales[3 * g + 2]));
+  double M[9];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    M[3 * i + 0] = dmul(R[3 * i + 0], s0);
+    M[3 * i + 1] = dmul(R[3 * i + 1], s1);
+    M[3 * i + 2] = dmul(R[3 * i + 2], s2);
+  }
+  double S[9];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+      S[3 * i + k] = dadd(dadd(dmul(M[3 * i + 0], M[3 * k + 0]), dmul(M[3 * i + 1], M[3 * k + 1])),
+                          dmul(M[3 * i + 2], M[3 * k + 2]));
+
+  // EWA: J (core.py:298-302), U = J W, Sigma' = U Sigma U^T (303-304)
+  const double zz = dmul(z, z);
+  const double j00 = __ddiv_rn(cam.fx, z);
+  const double j02 = __ddiv_rn(dmul(-cam.fx, x), zz);
+  const double j11 = __ddiv_rn(cam.fy, z);
+  const double j12 = __ddiv_rn(dmul(-cam.fy, y), zz);
+  double U[6];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    U[c] = dadd(dmul(j00, cam.R[c]), dmul(j02, cam.R[6 + c]));
+    U[3 + c] = dadd(dmul(j11, cam.R[3 + c]), dmul(j12, cam.R[6 + c]));
+  }
+  double US[6];
+#pragma unroll
+  for (int r = 0; r < 2; ++r)
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+      US[3 * r + k] = dadd(dadd(dmul(U[3 * r + 0], S[0 * 3 + k]), dmul(U[3 * r + 1], S[1 * 3 + k])),
+                           dmul(U[3 * r + 2], S[2 * 3 + k]));
+  const double c00 = dadd(dadd(dmul(US[0], U[0]), dmul(US[1], U[1])), dmul(US[2], U[2]));
+  const double c01 = dadd(dadd(dmul(US[0], U[3]), dmul(US[1], U[4])), dmul(US[2], U[5]));
+  const double c11 = dadd(dadd(dmul(US[3], U[3]), dmul(US[4], U[4])), dmul(US[5], U[5]));
+  const double ca = dadd(c00, kLowpass);  // core.py:305-307
+  const double cb = c01;
+  const double cc = dadd(c11, kLowpass);
+  const double det = dsub(dmul(ca, cc), dmul(cb, cb));  // core.py:309
+  if (!(det > 0.0)) {
+    out.radii[g] = 0;
+    out.tiles_touched[g] = 0;
+    return;
+  }
+  // conic, lambda_max, radius (core.py:316-319)
+  const double mid = dmul(0.5, dadd(ca, cc));
+  const double lam = dadd(mid, sqrt(fmax(dsub(dmul(mid, mid), det), 0.0)));
+  const double rad_d = ceil(dmul(kRadiusSigmas, sqrt(lam)));
+  radius_out = rad_d >= 2147483647.0 ? 2147483647 : int32_t(rad_d);
+
+  // tile rectangle, inclusive, clipped (rasterizer.py:86-97)
+  const double x0d = floor(__ddiv_rn(dsub(u, rad_d), double(kTile)));
+  const double x1d = floor(__ddiv_rn(dadd(u, rad_d), double(kTile)));
+  const double y0d = floor(__ddiv_rn(dsub(v, rad_d), double(kTile)));
+  const double y1d = floor(__ddiv_rn(dadd(v, rad_d), double(kTile)));
+  const double txm = double(cam.tiles_x - 1), tym = double(cam.tiles_y - 1);
+  const bool valid = (x1d >= 0.0) && (x0d < double(cam.tiles_x)) && (y1d >= 0.0) && (y0d < double(cam.tiles_y));
+  const int32_t x0 = int32_t(fmin(fmax(x0d, 0.0), txm));
+  const int32_t x1 = int32_t(fmin(fmax(x1d, 0.0), txm));
+  const int32_t y0 = int32_t(fmin(fmax(y0d, 0.0), tym));
+  const int32_t y1 = int32_t(fmin(fmax(y1d, 0.0), tym));
+  if (valid) {
+    const int64_t cnt = int64_t(x1 - x0 + 1) * int64_t(y1 - y0 + 1);
+    tiles = cnt > 2147483647 ? 2147483647 : int32_t(cnt);
+  }
+
+  // SH colour along the unit camera->mean direction (core.py:321-326)
+  const double dx = dsub(mx, cam.center[0]), dy = dsub(my, cam.center[1]), dz = dsub(mz, cam.center[2]);
+  const double dist = sqrt(dadd(dadd(dmul(dx, dx), dmul(dy, dy)), dmul(dz, dz)));
+  const float vx = float(__ddiv_rn(dx, dist)), vy = float(__ddiv_rn(dy, dist)), vz = float(__ddiv_rn(dz, dist));
+  float b[16];
+  sh_basis(vx, vy, vz, degree, b);
+  const int nrows = (degree + 1) * (degree + 1);
+  const float* shg = p.sh + 48 * g;
+  float col[3] = {0.0f, 0.0f, 0.0f};
+  for (int k = 0; k < nrows; ++k) {
+    col[0] = fmaf(b[k], shg[3 * k + 0], col[0]);
+    col[1] = fmaf(b[k], shg[3 * k + 1], col[1]);
+    col[2] = fmaf(b[k], shg[3 * k + 2], col[2]);
+  }
+  int mask = 0;
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    col[c] += 0.5f;
+    if (col[c] > 0.0f) mask |= (1 << c);
+    col[c] = fmaxf(col[c], 0.0f);
+  }
+  // sigmoid opacity (core.py:327)
+  const double alpha = 1.0 / (1.0 + exp(-double(p.opacity_logits[g])));
+
+  const float ux_hi = float(u), uy_hi = float(v);
+  const float ux_lo = float(dsub(u, double(ux_hi))), uy_lo = float(dsub(v, double(uy_hi)));
+  float4* rec = reinterpret_cast<float4*>(out.rec) + 3 * g;
+  rec[0] = make_float4(ux_hi, uy_hi, float(alpha), ux_lo);
+  rec[1] = make_float4(float(__ddiv_rn(cc, det)), float(__ddiv_rn(-cb, det)), float(__ddiv_rn(ca, det)), uy_lo);
+  rec[2] = make_float4(col[0], col[1], col[2], float(mask));
+  out.depth[g] = float(z);
+  reinterpret_cast<int4*>(out.rect)[g] = make_int4(x0, y0, x1, y1);
+  out.radii[g] = radius_out;
+  out.tiles_touched[g] = tiles;
+}
+
+}  // namespace
+}  // namespace gs
+
+extern "C" int gs_preprocess_forward(const gs_params_t* params, const gs_camera_t* camera,
+                                     int32_t active_sh_degree, gs_splats_t* splats, void* stream) {
+  if (!params || !camera || !splats) return GS_ERR_INVALID_ARG;
+  if (active_sh_degree < 0 || active_sh_degree > 3) return GS_ERR_INVALID_ARG;
+  if (camera->width <= 0 || camera->height <= 0 || !(camera->fx > 0) || !(camera->fy > 0) ||
+      !(camera->near_plane > 0))
+    return GS_ERR_INVALID_ARG;
+  if (params->n < 0 || splats->n != params->n) return GS_ERR_INVALID_ARG;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaError_t e = cudaMemsetAsync(splats->status, 0, sizeof(int32_t), s);
+  if (e != cudaSuccess) return gs::record_cuda_error(e);
+  if (params->n == 0) return GS_OK;
+  const gs::DevCamera cam = gs::make_dev_camera(*camera);
+  const int block = 128;
+  const unsigned grid = unsigned((params->n + block - 1) / block);
+  gs::preprocess_fwd_kernel<<<grid, block, 0, s>>>(*params, cam, active_sh_degree, *splats);
+  return gs::check_launch();
+}

@@ -1,0 +1,88 @@
+"""Fused device Adam and the training-step slice of the hot path.
+
+Mirrors splatlab's optimizer slice: TrainConfig learning rates and the
+position-LR decay (optimizer.py:20-75), the dense per-group Adam
+(`_adam_step`, optimizer.py:263-293) and the densification statistics
+(optimizer.py:252-255).  One gs_adam_step launch updates all five groups.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import torch
+
+from . import _lib
+from .cloud import PARAM_GROUPS, GaussianCloud
+from .rasterizer import DensifyStats, GaussianGrads
+
+
+@dataclass
+class TrainConfig:
+    """The Adam / schedule fields of splatlab TrainConfig (optimizer.py:20-48)."""
+
+    lambda_dssim: float = 0.2
+    total_iters: int = 30000
+    lr_means: float = 1.6e-4
+    lr_means_final: float = 1.6e-6
+    lr_sh_dc: float = 2.5e-3
+    lr_sh_rest: float = 2.5e-3 / 20.0
+    lr_opacity: float = 5e-2
+    lr_log_scales: float = 5e-3
+    lr_rotations: float = 1e-3
+    adam_betas: tuple[float, float] = (0.9, 0.999)
+    adam_eps: float = 1e-15
+    background: tuple[float, float, float] = (0.0, 0.0, 0.0)
+    sh_band_interval: int = 1000
+
+    def __post_init__(self):
+        if not 0.0 <= self.lambda_dssim <= 1.0:
+            raise ValueError("lambda_dssim must be in [0, 1]")
+        if self.total_iters <= 0 or self.sh_band_interval <= 0:
+            raise ValueError("total_iters and sh_band_interval must be positive")
+
+    def lr_means_at(self, iteration: int) -> float:
+        """Exponential position-LR decay (optimizer.py:72-75)."""
+        frac = min(iteration, self.total_iters) / self.total_iters
+        return self.lr_means * (self.lr_means_final / self.lr_means) ** frac
+
+
+class DeviceAdam:
+    """Adam moments for the five parameter groups, updated in one launch."""
+
+    def __init__(self, cloud: GaussianCloud):
+        self.exp_avg = {g: torch.zeros_like(getattr(cloud, g)) for g in PARAM_GROUPS}
+        self.exp_avg_sq = {g: torch.zeros_like(getattr(cloud, g)) for g in PARAM_GROUPS}
+
+    def step(self, cloud: GaussianCloud, grads: GaussianGrads, iteration: int, config: TrainConfig) -> None:
+        """One dense Adam step at `iteration` (= the bias-correction t)."""
+        beta1, beta2 = config.adam_betas
+        t = int(iteration)
+        if t < 1:
+            raise ValueError("Adam iteration must be >= 1")
+        bias1 = 1.0 - beta1**t
+        bias2 = 1.0 - beta2**t
+        grad_of = {"means": grads.d_means, "log_scales": grads.d_log_scales, "rotations": grads.d_rotations,
+                   "opacity_logits": grads.d_opacity_logits, "sh": grads.d_sh}
+        lrs = {"means": config.lr_means_at(t), "log_scales": config.lr_log_scales,
+               "rotations": config.lr_rotations, "opacity_logits": config.lr_opacity, "sh": config.lr_sh_rest}
+        groups = (_lib.GsAdamGroup * len(PARAM_GROUPS))()
+        for i, name in enumerate(PARAM_GROUPS):
+            p, g = getattr(cloud, name), grad_of[name]
+            if not (p.is_contiguous() and g.is_contiguous()):
+                raise ValueError(f"{name}: parameters and gradients must be contiguous")
+            G = groups[i]
+            G.param, G.grad = p.data_ptr(), g.data_ptr()
+            G.exp_avg, G.exp_avg_sq = self.exp_avg[name].data_ptr(), self.exp_avg_sq[name].data_ptr()
+            G.numel = p.numel()
+            G.lr = lrs[name]
+            if name == "sh":  # row 0 (DC) uses lr_sh_dc (optimizer.py:268-269)
+                G.lr_head, G.period, G.head = config.lr_sh_dc, 48, 3
+            else:
+                G.lr_head, G.period, G.head = lrs[name], 0, 0
+        lib = _lib.load()
+        _lib.check(lib.gs_adam_step(groups, len(PARAM_GROUPS), beta1, beta2, config.adam_eps, bias1, bias2,
+                                    torch.cuda.current_stream().cuda_stream), "adam_step")
+
+
+__all__ = ["TrainConfig", "DeviceAdam", "DensifyStats"]

@@ -1,0 +1,433 @@
+"""Host side of the B200 rasterizer: the reference's stage functions over
+device tensors, and the drop-in torch.autograd.Function.
+
+Stage functions keep the names, argument meaning and error behaviour of the
+reference (splatlab):
+  project          core.py:266-345        -> gs_preprocess_forward   (K1)
+  bin_and_sort     rasterizer.py:69-124   -> gs_bin_and_sort         (K2-K5)
+  render_forward   rasterizer.py:201-240  -> gs_blend_forward        (K6)
+  render_backward  rasterizer.py:253-316  -> gs_blend_backward       (K7)
+  backward_project gradients.py:192-259   -> gs_preprocess_backward  (K8)
+  render_view      optimizer.py:212-219   (composition of the first three)
+Everything runs on the current CUDA stream; buffers come from torch's
+caching allocator, the library itself never allocates.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .camera import Camera
+from .cloud import GaussianCloud, c_params_from
+from .errors import InvalidPrimitiveError
+
+TILE_SIZE = 16            # rasterizer.py:13
+ALPHA_EPS = 1.0 / 255.0   # rasterizer.py:17
+ALPHA_CLAMP = 0.99        # rasterizer.py:18
+SATURATION = 0.9999       # rasterizer.py:19
+MAX_TILES = 2**32 - 1     # rasterizer.py:24
+MAX_INSTANCES = 2**31     # rasterizer.py:25
+
+
+def tile_extent(width: int, height: int) -> tuple[int, int]:
+    return (width + TILE_SIZE - 1) // TILE_SIZE, (height + TILE_SIZE - 1) // TILE_SIZE
+
+
+def _stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _camera(camera) -> Camera:
+    return camera if isinstance(camera, Camera) else Camera.from_reference(camera)
+
+
+@dataclass
+class DeviceSplats:
+    """Per-view projected splats in N-space (see gs_splats_t)."""
+
+    rec: torch.Tensor            # (N,12) float32
+    depth: torch.Tensor          # (N,)   float32
+    radii: torch.Tensor          # (N,)   int32, 0 = culled
+    rect: torch.Tensor           # (N,4)  int32
+    tiles_touched: torch.Tensor  # (N,)   int32
+    status: torch.Tensor         # (1,)   int32
+
+    @classmethod
+    def empty(cls, n: int, device) -> "DeviceSplats":
+        f32, i32 = dict(dtype=torch.float32, device=device), dict(dtype=torch.int32, device=device)
+        return cls(torch.empty((n, _lib.REC_FLOATS), **f32), torch.empty(n, **f32), torch.empty(n, **i32),
+                   torch.empty((n, 4), **i32), torch.empty(n, **i32), torch.zeros(1, **i32))
+
+    def __len__(self) -> int:
+        return self.radii.shape[0]
+
+    @classmethod
+    def from_projected(cls, mean2d, conic, depth, color, alpha, radius, width: int, height: int,
+                       color_active=None, device="cuda") -> "DeviceSplats":
+        """Adapter from reference-style ProjectedSplats arrays (core.py:236-263)
+        to device records, for stage-level tests that bypass project()
+        (as test_rasterizer.py:11-36 does).  Tile rectangles follow
+        rasterizer.py:86-97 in float64."""
+        mean2d = np.asarray(mean2d, np.float64).reshape(-1, 2)
+        n = mean2d.shape[0]
+        conic = np.asarray(conic, np.float64).reshape(n, 3)
+        color = np.asarray(color, np.float64).reshape(n, 3)
+        radius = np.asarray(radius, np.int64).reshape(n)
+        rec = np.zeros((n, _lib.REC_FLOATS), np.float32)
+        hi = mean2d.astype(np.float32)
+        rec[:, 0], rec[:, 1] = hi[:, 0], hi[:, 1]
+        rec[:, 3] = (mean2d[:, 0] - hi[:, 0]).astype(np.float32)
+        rec[:, 7] = (mean2d[:, 1] - hi[:, 1]).astype(np.float32)
+        rec[:, 2] = np.asarray(alpha, np.float64).reshape(n)
+        rec[:, 4:7] = conic
+        rec[:, 8:11] = color
+        active = np.ones((n, 3), bool) if color_active is None else np.asarray(color_active, bool).reshape(n, 3)
+        rec[:, 11] = (active * np.array([1, 2, 4])).sum(axis=1)
+        tx, ty = tile_extent(width, height)
+        r = radius.astype(np.float64)
+        x0, x1 = np.floor((mean2d[:, 0] - r) / TILE_SIZE), np.floor((mean2d[:, 0] + r) / TILE_SIZE)
+        y0, y1 = np.floor((mean2d[:, 1] - r) / TILE_SIZE), np.floor((mean2d[:, 1] + r) / TILE_SIZE)
+        valid = (x1 >= 0) & (x0 < tx) & (y1 >= 0) & (y0 < ty) & (radius > 0)
+        x0, x1 = np.clip(x0, 0, tx - 1), np.clip(x1, 0, tx - 1)
+        y0, y1 = np.clip(y0, 0, ty - 1), np.clip(y1, 0, ty - 1)
+        rect = np.stack([x0, y0, x1, y1], axis=1).astype(np.int32)
+        tiles = np.where(valid, (x1 - x0 + 1) * (y1 - y0 + 1), 0).astype(np.int32)
+        t = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a, dtype=dt)).to(device)  # noqa: E731
+        return cls(t(rec, np.float32), t(np.asarray(depth, np.float64).reshape(n), np.float32),
+                   t(np.minimum(radius, 2**31 - 1), np.int32), t(rect, np.int32), t(tiles, np.int32),
+                   torch.zeros(1, dtype=torch.int32, device=device))
+
+    def c_struct(self) -> _lib.GsSplats:
+        s = _lib.GsSplats()
+        s.rec, s.depth, s.radii = self.rec.data_ptr(), self.depth.data_ptr(), self.radii.data_ptr()
+        s.rect, s.tiles_touched, s.status = self.rect.data_ptr(), self.tiles_touched.data_ptr(), self.status.data_ptr()
+        s.n = len(self)
+        return s
+
+    # Views in the reference's ProjectedSplats vocabulary (core.py:236-263).
+    @property
+    def visible(self) -> torch.Tensor:
+        return self.radii > 0
+
+    @property
+    def mean2d(self) -> torch.Tensor:
+        r = self.rec.double()
+        return torch.stack([r[:, 0] + r[:, 3], r[:, 1] + r[:, 7]], dim=1)
+
+    @property
+    def conic(self) -> torch.Tensor:
+        return self.rec[:, 4:7]
+
+    @property
+    def alpha(self) -> torch.Tensor:
+        return self.rec[:, 2]
+
+    @property
+    def color(self) -> torch.Tensor:
+        return self.rec[:, 8:11]
+
+    @property
+    def color_active(self) -> torch.Tensor:
+        bits = self.rec[:, 11].to(torch.int32)
+        return torch.stack([(bits >> c) & 1 for c in range(3)], dim=1).bool()
+
+
+@dataclass
+class TileBinning:
+    """Sorted instances (rasterizer.py:44-52): Gaussian id per sorted instance
+    and per-tile [start, end) ranges.  Keys are implicit: (tile, depth[id])."""
+
+    splat_ids: torch.Tensor   # (K,) int32 Gaussian index (N-space)
+    ranges: torch.Tensor      # (T,2) int32
+    tiles_x: int
+    tiles_y: int
+
+    @property
+    def num_instances(self) -> int:
+        return self.splat_ids.shape[0]
+
+
+@dataclass
+class RenderOutput:
+    image: torch.Tensor                        # (H,W,3) float32
+    final_transmittance: torch.Tensor | None   # (H,W) float32, training only
+    last_contributor: torch.Tensor | None      # (H,W) int32, -1 = none
+
+
+@dataclass
+class SplatGrads2D:
+    """Screen-space gradients (rasterizer.py:243-250) in the packed (N,12) row."""
+
+    packed: torch.Tensor  # (N,12) float32
+
+    @property
+    def d_mean2d(self) -> torch.Tensor:
+        return self.packed[:, 0:2]
+
+    @property
+    def d_alpha(self) -> torch.Tensor:
+        return self.packed[:, 2]
+
+    @property
+    def d_conic(self) -> torch.Tensor:
+        return self.packed[:, 4:7]
+
+    @property
+    def d_color(self) -> torch.Tensor:
+        return self.packed[:, 8:11]
+
+
+@dataclass
+class GaussianGrads:
+    """Parameter gradients (gradients.py:13-27); culled rows are exactly 0."""
+
+    d_means: torch.Tensor
+    d_rotations: torch.Tensor
+    d_log_scales: torch.Tensor
+    d_opacity_logits: torch.Tensor
+    d_sh: torch.Tensor
+    view_pos_grad_norm: torch.Tensor
+
+    @classmethod
+    def zeros(cls, n: int, device) -> "GaussianGrads":
+        z = dict(dtype=torch.float32, device=device)
+        return cls(torch.zeros((n, 3), **z), torch.zeros((n, 4), **z), torch.zeros((n, 3), **z),
+                   torch.zeros(n, **z), torch.zeros((n, 16, 3), **z), torch.zeros(n, **z))
+
+    def c_struct(self) -> _lib.GsGrads:
+        g = _lib.GsGrads()
+        g.d_means, g.d_rotations = self.d_means.data_ptr(), self.d_rotations.data_ptr()
+        g.d_log_scales, g.d_opacity_logits = self.d_log_scales.data_ptr(), self.d_opacity_logits.data_ptr()
+        g.d_sh, g.view_pos_grad_norm = self.d_sh.data_ptr(), self.view_pos_grad_norm.data_ptr()
+        return g
+
+
+@dataclass
+class DensifyStats:
+    """Device densification statistics (TrainState, optimizer.py:106-108)."""
+
+    accum_pos_grad: torch.Tensor   # (N,) float32
+    accum_count: torch.Tensor      # (N,) int32
+    max_radius_frac: torch.Tensor  # (N,) float32
+
+    @classmethod
+    def zeros(cls, n: int, device) -> "DensifyStats":
+        return cls(torch.zeros(n, dtype=torch.float32, device=device),
+                   torch.zeros(n, dtype=torch.int32, device=device),
+                   torch.zeros(n, dtype=torch.float32, device=device))
+
+    def c_struct(self) -> _lib.GsStats:
+        s = _lib.GsStats()
+        s.accum_pos_grad = self.accum_pos_grad.data_ptr()
+        s.accum_count = self.accum_count.data_ptr()
+        s.max_radius_frac = self.max_radius_frac.data_ptr()
+        return s
+
+
+# ---------------------------------------------------------------------------
+# stage functions
+
+def _project_tensors(params: _lib.GsParams, n: int, device, camera: Camera, active_sh_degree: int) -> DeviceSplats:
+    if not 0 <= active_sh_degree <= 3:
+        raise ValueError(f"SH degree must be in 0..3, got {active_sh_degree}")  # sh.py:37-38
+    lib = _lib.load()
+    splats = DeviceSplats.empty(n, device)
+    cs = splats.c_struct()
+    _lib.check(lib.gs_preprocess_forward(ctypes.byref(params), ctypes.byref(camera.to_c()), int(active_sh_degree),
+                                         ctypes.byref(cs), _stream()), "project")
+    return splats
+
+
+def project(cloud: GaussianCloud, camera, active_sh_degree: int = 3) -> DeviceSplats:
+    """K1: cull, EWA-project, colour and activate every Gaussian (core.py:266).
+
+    Raises InvalidPrimitiveError for a zero quaternion among the survivors of
+    the near/guard-band tests, like the reference (this check synchronises)."""
+    camera = _camera(camera)
+    splats = _project_tensors(cloud.c_params(), len(cloud), cloud.device, camera, active_sh_degree)
+    if len(cloud) and int(splats.status.item()) & 1:
+        raise InvalidPrimitiveError("zero-norm quaternion cannot be normalized")
+    return splats
+
+
+class _CapacityHint:
+    """Instance-buffer sizing: remembers the largest K seen per device so a
+    steady-state frame issues exactly one gs_bin_and_sort call."""
+
+    def __init__(self):
+        self.k = {}
+
+    def get(self, device) -> int:
+        return self.k.get(str(device), 1 << 16)
+
+    def update(self, device, k: int) -> None:
+        self.k[str(device)] = max(self.get(device), int(k * 1.15) + 1024)
+
+
+_capacity = _CapacityHint()
+
+
+def bin_and_sort(splats: DeviceSplats, width: int, height: int) -> TileBinning:
+    """K2-K5: duplicate, sort by (tile, depth, index), find tile ranges (rasterizer.py:69)."""
+    lib = _lib.load()
+    tiles_x, tiles_y = tile_extent(width, height)
+    device = splats.rec.device
+    n = len(splats)
+    cs = splats.c_struct()
+    stream = _stream()
+    cap = _capacity.get(device)
+    for _ in range(2):
+        ws_bytes = ctypes.c_size_t(0)
+        _lib.check(lib.gs_bin_workspace_size(n, width, height, cap, ctypes.byref(ws_bytes)), "bin_and_sort")
+        ws = torch.empty(max(int(ws_bytes.value), 1), dtype=torch.uint8, device=device)
+        ids = torch.empty(max(cap, 1), dtype=torch.int32, device=device)
+        ranges = torch.empty((tiles_x * tiles_y, 2), dtype=torch.int32, device=device)
+        k = ctypes.c_int64(0)
+        st = lib.gs_bin_and_sort(ctypes.byref(cs), width, height, ws.data_ptr(), ws_bytes.value, cap,
+                                 ids.data_ptr(), ranges.data_ptr(), ctypes.byref(k), stream)
+        if st == _lib.GS_ERR_CAPACITY:
+            _capacity.update(device, k.value)
+            cap = _capacity.get(device)
+            continue
+        _lib.check(st, "bin_and_sort")
+        return TileBinning(ids[:k.value], ranges, tiles_x, tiles_y)
+    raise RuntimeError("bin_and_sort: instance capacity did not converge")
+
+
+def _bg(background) -> ctypes.Array:
+    b = np.asarray(background, dtype=np.float64).reshape(3)
+    return (ctypes.c_float * 3)(*[float(v) for v in b])
+
+
+def render_forward(splats: DeviceSplats, binning: TileBinning, width: int, height: int, background,
+                   training: bool = False) -> RenderOutput:
+    """K6: per-tile front-to-back blend (rasterizer.py:201)."""
+    lib = _lib.load()
+    device = splats.rec.device
+    image = torch.empty((height, width, 3), dtype=torch.float32, device=device)
+    t_final = torch.empty((height, width), dtype=torch.float32, device=device) if training else None
+    last = torch.empty((height, width), dtype=torch.int32, device=device) if training else None
+    cs = splats.c_struct()
+    _lib.check(lib.gs_blend_forward(ctypes.byref(cs), binning.splat_ids.data_ptr(), binning.ranges.data_ptr(),
+                                    width, height, _bg(background), int(bool(training)), image.data_ptr(),
+                                    _lib.ptr(t_final), _lib.ptr(last), _stream()), "render_forward")
+    return RenderOutput(image, t_final, last)
+
+
+def render_backward(d_image: torch.Tensor, output: RenderOutput, splats: DeviceSplats, binning: TileBinning,
+                    width: int, height: int, background) -> SplatGrads2D:
+    """K7: back-to-front blend gradient (rasterizer.py:253)."""
+    if output.final_transmittance is None or output.last_contributor is None:
+        raise ValueError("backward pass needs a training-mode RenderOutput")  # rasterizer.py:265-266
+    lib = _lib.load()
+    d_image = d_image.to(dtype=torch.float32).contiguous()
+    if tuple(d_image.shape) != (height, width, 3):
+        raise ValueError(f"d_image shape {tuple(d_image.shape)} != {(height, width, 3)}")
+    packed = torch.empty((len(splats), _lib.GRAD2D_FLOATS), dtype=torch.float32, device=splats.rec.device)
+    cs = splats.c_struct()
+    _lib.check(lib.gs_blend_backward(d_image.data_ptr(), ctypes.byref(cs), binning.splat_ids.data_ptr(),
+                                     binning.ranges.data_ptr(), output.final_transmittance.data_ptr(),
+                                     output.last_contributor.data_ptr(), width, height, _bg(background),
+                                     packed.data_ptr(), _stream()), "render_backward")
+    return SplatGrads2D(packed)
+
+
+def _backward_project_tensors(params: _lib.GsParams, n: int, device, camera: Camera, splats: DeviceSplats,
+                              grads2d: SplatGrads2D, active_sh_degree: int, stats: DensifyStats | None,
+                              out: GaussianGrads | None, accumulate: bool) -> GaussianGrads:
+    if not 0 <= active_sh_degree <= 3:
+        raise ValueError(f"SH degree must be in 0..3, got {active_sh_degree}")
+    lib = _lib.load()
+    if out is None:
+        z = dict(dtype=torch.float32, device=device)
+        out = GaussianGrads(torch.empty((n, 3), **z), torch.empty((n, 4), **z), torch.empty((n, 3), **z),
+                            torch.empty(n, **z), torch.empty((n, 16, 3), **z), torch.empty(n, **z))
+        accumulate = False
+    cs = splats.c_struct()
+    cg = out.c_struct()
+    cst = stats.c_struct() if stats is not None else None
+    _lib.check(lib.gs_preprocess_backward(ctypes.byref(params), ctypes.byref(camera.to_c()), int(active_sh_degree),
+                                          ctypes.byref(cs), grads2d.packed.data_ptr(), ctypes.byref(cg),
+                                          int(bool(accumulate)), ctypes.byref(cst) if cst is not None else None,
+                                          _stream()), "backward_project")
+    return out
+
+
+def backward_project(cloud: GaussianCloud, camera, splats: DeviceSplats, grads2d: SplatGrads2D,
+                     active_sh_degree: int = 3, *, stats: DensifyStats | None = None,
+                     out: GaussianGrads | None = None, accumulate: bool = False) -> GaussianGrads:
+    """K8: chain screen-space gradients to the raw parameters (gradients.py:192).
+
+    `stats` (optional) receives the densification statistics update of
+    optimizer.py:252-255; `out` + `accumulate` sum several views in place."""
+    return _backward_project_tensors(cloud.c_params(), len(cloud), cloud.device, _camera(camera), splats, grads2d,
+                                     active_sh_degree, stats, out, accumulate)
+
+
+def render_view(cloud: GaussianCloud, camera, background, active_sh_degree: int = 3, training: bool = False):
+    """project -> bin_and_sort -> render_forward (optimizer.py:212-219)."""
+    camera = _camera(camera)
+    splats = _project_tensors(cloud.c_params(), len(cloud), cloud.device, camera, active_sh_degree)
+    binning = bin_and_sort(splats, camera.width, camera.height)
+    out = render_forward(splats, binning, camera.width, camera.height, background, training=training)
+    return out, splats, binning
+
+
+# ---------------------------------------------------------------------------
+# drop-in autograd Function
+
+class GaussianRasterizer(torch.autograd.Function):
+    """Differentiable rasterizer: raw parameters + camera in; image (H,W,3)
+    and radii (N,) int32 (0 = culled) out; gradients w.r.t. the raw means,
+    log-scales, quaternions, opacity logits and SH coefficients back.
+
+    The forward is render_view(training=True); the backward is
+    render_backward + backward_project, optionally updating `stats`."""
+
+    @staticmethod
+    def forward(ctx, means, log_scales, rotations, opacity_logits, sh, camera, background,
+                active_sh_degree=3, stats=None):
+        camera = _camera(camera)
+        tensors = [t.detach().contiguous() for t in (means, log_scales, rotations, opacity_logits, sh)]
+        params = c_params_from(*tensors)
+        n = means.shape[0]
+        splats = _project_tensors(params, n, means.device, camera, int(active_sh_degree))
+        binning = bin_and_sort(splats, camera.width, camera.height)
+        out = render_forward(splats, binning, camera.width, camera.height, background, training=True)
+        ctx.save_for_backward(*tensors, splats.rec, splats.depth, splats.radii, splats.rect, splats.tiles_touched,
+                              splats.status, binning.splat_ids, binning.ranges, out.final_transmittance,
+                              out.last_contributor)
+        ctx.camera = camera
+        ctx.background = background
+        ctx.degree = int(active_sh_degree)
+        ctx.stats = stats
+        ctx.tiles = (binning.tiles_x, binning.tiles_y)
+        ctx.mark_non_differentiable(splats.radii)
+        return out.image, splats.radii
+
+    @staticmethod
+    def backward(ctx, d_image, d_radii):
+        (means, log_scales, rotations, opacity_logits, sh, rec, depth, radii, rect, tiles_touched, status,
+         ids, ranges, t_final, last) = ctx.saved_tensors
+        camera = ctx.camera
+        splats = DeviceSplats(rec, depth, radii, rect, tiles_touched, status)
+        binning = TileBinning(ids, ranges, *ctx.tiles)
+        output = RenderOutput(None, t_final, last)
+        g2d = render_backward(d_image, output, splats, binning, camera.width, camera.height, ctx.background)
+        params = c_params_from(means, log_scales, rotations, opacity_logits, sh)
+        grads = _backward_project_tensors(params, means.shape[0], means.device, camera, splats, g2d, ctx.degree,
+                                          ctx.stats, None, False)
+        ctx.view_pos_grad_norm = grads.view_pos_grad_norm
+        return (grads.d_means, grads.d_log_scales, grads.d_rotations, grads.d_opacity_logits, grads.d_sh,
+                None, None, None, None)
+
+
+def rasterize_gaussians(means, log_scales, rotations, opacity_logits, sh, camera, background=(0.0, 0.0, 0.0),
+                        active_sh_degree: int = 3, stats: DensifyStats | None = None):
+    """Functional form of GaussianRasterizer.apply -> (image, radii)."""
+    return GaussianRasterizer.apply(means, log_scales, rotations, opacity_logits, sh, camera, background,
+                                    active_sh_degree, stats)
