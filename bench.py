@@ -211,7 +211,7 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
             for leaf in leaves:
                 dist.all_reduce(leaf.grad)
         e2e_adam.step(e2e_adam_cloud, g, e2e_it[0], config)
-        return float(loss.item())   # D2H of the step's loss
+        return float(loss[0].item())   # D2H of the step's loss
 
     for _ in range(args.warmup):
         e2e_step()

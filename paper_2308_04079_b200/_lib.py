@@ -20,7 +20,7 @@ GS_ERR_RESOURCE_LIMIT = 3
 GS_ERR_CAPACITY = 4
 GS_ERR_CUDA = 5
 
-REC_FLOATS = 12
+REC_FLOATS = 16
 GRAD2D_FLOATS = 12
 
 

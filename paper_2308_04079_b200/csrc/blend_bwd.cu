@@ -66,9 +66,9 @@ blend_bwd_kernel(const float* __restrict__ d_image, const float4* __restrict__ r
     if (i < top) {
       const uint32_t g = ids[i];
       s_id[t] = g;
-      s_r0[t] = rec[3 * size_t(g) + 0];
-      s_r1[t] = rec[3 * size_t(g) + 1];
-      s_col[t] = rec[3 * size_t(g) + 2];
+      s_r0[t] = rec[4 * size_t(g) + 0];
+      s_r1[t] = rec[4 * size_t(g) + 1];
+      s_col[t] = rec[4 * size_t(g) + 2];
     }
     __syncthreads();
     for (int j = top - lo - 1; j >= 0; --j) {
@@ -77,7 +77,7 @@ blend_bwd_kernel(const float* __restrict__ d_image, const float4* __restrict__ r
       bool contrib = false;
       if (gi <= last_idx) {
         const float4 r1 = s_r1[j];
-        const AlphaEval e = eval_alpha(fx, fy, s_r0[j], r1);
+        const AlphaEval e = eval_alpha(fx, fy, s_r0[j], r1, rec, s_id[j]);
         if (e.a > 0.0f) {
           contrib = true;
           const float inv = __frcp_rn(1.0f - e.a);
@@ -90,7 +90,7 @@ blend_bwd_kernel(const float* __restrict__ d_image, const float4* __restrict__ r
           g_r = w * dlx;
           g_g = w * dly;
           g_b = w * dlz;
-          if (e.a_raw < kAlphaClamp) {  // clamped alphas pass no gradient (gradients.py:83-84)
+          if (e.live) {  // clamped alphas pass no gradient (gradients.py:83-84)
             g_al = d_a * e.g;
             const float dp = d_a * e.a_raw;
             g_mx = dp * (r1.x * e.dx + r1.y * e.dy);

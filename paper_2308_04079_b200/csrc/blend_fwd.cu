@@ -3,7 +3,7 @@
 //
 // One 256-thread CTA per 16x16 tile, one pixel per thread.  The tile's sorted
 // instance list is walked front to back in batches of 256: every thread
-// gathers one splat record (48 B) into shared memory, then each pixel blends
+// gathers one splat record (48 of its 64 B) into shared memory, then each pixel blends
 // the batch sequentially.  A pixel stops before its accumulated opacity
 // would exceed 0.9999 (rasterizer.py:179-180); the CTA leaves the list as
 // soon as __syncthreads_count says every pixel is done (rasterizer.py:194-195).
@@ -21,6 +21,7 @@ blend_fwd_kernel(const float4* __restrict__ rec, const uint32_t* __restrict__ id
   __shared__ float4 s_r0[kTilePixels];
   __shared__ float4 s_r1[kTilePixels];
   __shared__ float4 s_col[kTilePixels];
+  __shared__ uint32_t s_id[kTilePixels];
 
   const int tile = blockIdx.x;
   const int t = threadIdx.x;
@@ -41,15 +42,16 @@ blend_fwd_kernel(const float4* __restrict__ rec, const uint32_t* __restrict__ id
     const int i = base + t;
     if (i < range.y) {
       const uint32_t g = ids[i];
-      s_r0[t] = rec[3 * size_t(g) + 0];
-      s_r1[t] = rec[3 * size_t(g) + 1];
-      s_col[t] = rec[3 * size_t(g) + 2];
+      s_id[t] = g;
+      s_r0[t] = rec[4 * size_t(g) + 0];
+      s_r1[t] = rec[4 * size_t(g) + 1];
+      s_col[t] = rec[4 * size_t(g) + 2];
     }
     __syncthreads();
     if (!done) {
       const int cnt = min(kTilePixels, range.y - base);
       for (int j = 0; j < cnt; ++j) {
-        const AlphaEval e = eval_alpha(fx, fy, s_r0[j], s_r1[j]);
+        const AlphaEval e = eval_alpha(fx, fy, s_r0[j], s_r1[j], rec, s_id[j]);
         if (e.a == 0.0f) continue;
         const float t_new = T * (1.0f - e.a);
         if (1.0f - t_new > kSaturation) {

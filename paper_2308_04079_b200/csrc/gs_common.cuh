@@ -70,12 +70,22 @@ __host__ inline DevCamera make_dev_camera(const gs_camera_t& c) {
 // ---------------------------------------------------------------------------
 // Alpha of one splat at one pixel (rasterizer.py:171-177, gradients.py:54-61).
 //   power = -0.5 (a dx^2 + c dy^2) - b dx dy ; G = 0 if power > 0 else e^power
-// dx uses the split (hi, lo) screen mean so the subtraction keeps ~f64
-// accuracy at 4K coordinates.  Explicit _rn intrinsics are never fused or
-// re-associated by the compiler, which pins the bit pattern across kernels.
+//   a_raw = alpha G ; a = min(0.99, a_raw) ; a < 1/255 -> skipped
+// Fast path in float32: dx uses the split (hi, lo) screen mean so the
+// subtraction keeps ~f64 accuracy at 4K coordinates, and explicit _rn
+// intrinsics are never fused or re-associated, so the forward and the
+// backward see bit-identical alphas (identical contributor sets).
+// Threshold guard: when a_raw lies within kGuard (relative) of 1/255 or of
+// 0.99 the pair is re-evaluated in float64 from the split records
+// (mean, conic and opacity hi + lo), so the skip / clamp decisions agree with
+// the float64 reference.  The float32 fast path is accurate to < 5e-6
+// relative, kGuard = 1e-5 covers it; about 4e-5 of pairs take the slow path.
 struct AlphaEval {
   float dx, dy, g, a_raw, a;   // a: clamped and eps-skipped alpha (0 = skip)
+  bool live;                   // a_raw < 0.99: the pair passes gradient to alpha/power
 };
+
+constexpr float kGuard = 1e-5f;
 
 __device__ __forceinline__ float ex2_approx(float x) {
   float y;
@@ -83,7 +93,26 @@ __device__ __forceinline__ float ex2_approx(float x) {
   return y;
 }
 
-__device__ __forceinline__ AlphaEval eval_alpha(float px, float py, float4 r0, float4 r1) {
+// Record layout (gs_splats_t.rec, 4 x float4 per Gaussian):
+//   r0 = (mx_hi, my_hi, alpha_hi, mx_lo)   r1 = (ca_hi, cb_hi, cc_hi, my_lo)
+//   r2 = (r, g, b, mask)                   r3 = (ca_lo, cb_lo, cc_lo, alpha_lo)
+static __device__ __noinline__ void eval_alpha_f64(float px, float py, float4 r0, float4 r1, float4 r3, AlphaEval& e) {
+  const double dx = double(px) - (double(r0.x) + double(r0.w));
+  const double dy = double(py) - (double(r0.y) + double(r1.w));
+  const double ca = double(r1.x) + double(r3.x), cb = double(r1.y) + double(r3.y), cc = double(r1.z) + double(r3.z);
+  const double al = double(r0.z) + double(r3.w);
+  const double power = -0.5 * (ca * dx * dx + cc * dy * dy) - cb * dx * dy;
+  const double g = power > 0.0 ? 0.0 : exp(power);
+  const double ar = al * g;
+  const double a = ar < 0.99 ? ar : 0.99;
+  e.g = float(g);
+  e.a_raw = float(ar);
+  e.live = ar < 0.99;
+  e.a = (a < 1.0 / 255.0) ? 0.0f : float(a);
+}
+
+__device__ __forceinline__ AlphaEval eval_alpha(float px, float py, float4 r0, float4 r1,
+                                                const float4* __restrict__ rec, uint32_t gid) {
   AlphaEval e;
   e.dx = __fsub_rn(__fsub_rn(px, r0.x), r0.w);
   e.dy = __fsub_rn(__fsub_rn(py, r0.y), r1.w);
@@ -91,13 +120,14 @@ __device__ __forceinline__ AlphaEval eval_alpha(float px, float py, float4 r0, f
   const float qc = __fmul_rn(__fmul_rn(r1.z, e.dy), e.dy);
   const float qb = __fmul_rn(__fmul_rn(r1.y, e.dx), e.dy);
   const float power = __fsub_rn(__fmul_rn(-0.5f, __fadd_rn(qa, qc)), qb);
-  if (power > 0.0f) {
-    e.g = 0.0f;
-  } else {
-    e.g = ex2_approx(__fmul_rn(power, 1.4426950408889634f));
-  }
+  e.g = (power > 0.0f) ? 0.0f : ex2_approx(__fmul_rn(power, 1.4426950408889634f));
   e.a_raw = __fmul_rn(r0.z, e.g);
-  float a = fminf(kAlphaClamp, e.a_raw);
+  if (fabsf(e.a_raw - kAlphaEps) <= kGuard * kAlphaEps || fabsf(e.a_raw - kAlphaClamp) <= kGuard) {
+    eval_alpha_f64(px, py, r0, r1, rec[4 * size_t(gid) + 3], e);
+    return e;
+  }
+  e.live = e.a_raw < kAlphaClamp;
+  const float a = fminf(kAlphaClamp, e.a_raw);
   e.a = (a < kAlphaEps) ? 0.0f : a;
   return e;
 }

@@ -37,7 +37,7 @@ preprocess_bwd_kernel(gs_params_t p, DevCamera cam, int degree, const float4* __
   const float4 ga = g2d[3 * g + 0];  // d_mean2d.x, d_mean2d.y, d_alpha
   const float4 gb = g2d[3 * g + 1];  // d_conic a, b, c
   const float4 gc = g2d[3 * g + 2];  // d_color r, g, b
-  const float4 r2 = rec[3 * g + 2];
+  const float4 r2 = rec[4 * g + 2];
   const int mask = int(r2.w);
 
   // --- opacity through the sigmoid (gradients.py:217)

@@ -157,10 +157,15 @@ preprocess_fwd_kernel(gs_params_t p, DevCamera cam, int degree, gs_splats_t out)
 
   const float ux_hi = float(u), uy_hi = float(v);
   const float ux_lo = float(dsub(u, double(ux_hi))), uy_lo = float(dsub(v, double(uy_hi)));
-  float4* rec = reinterpret_cast<float4*>(out.rec) + 3 * g;
-  rec[0] = make_float4(ux_hi, uy_hi, float(alpha), ux_lo);
-  rec[1] = make_float4(float(__ddiv_rn(cc, det)), float(__ddiv_rn(-cb, det)), float(__ddiv_rn(ca, det)), uy_lo);
+  // split float64 -> (hi, lo) float32 pairs for the blend's threshold guard
+  const double c0 = __ddiv_rn(cc, det), c1 = __ddiv_rn(-cb, det), c2 = __ddiv_rn(ca, det);
+  const float c0h = float(c0), c1h = float(c1), c2h = float(c2), ah = float(alpha);
+  float4* rec = reinterpret_cast<float4*>(out.rec) + 4 * g;
+  rec[0] = make_float4(ux_hi, uy_hi, ah, ux_lo);
+  rec[1] = make_float4(c0h, c1h, c2h, uy_lo);
   rec[2] = make_float4(col[0], col[1], col[2], float(mask));
+  rec[3] = make_float4(float(dsub(c0, double(c0h))), float(dsub(c1, double(c1h))), float(dsub(c2, double(c2h))),
+                       float(dsub(alpha, double(ah))));
   out.depth[g] = float(z);
   reinterpret_cast<int4*>(out.rect)[g] = make_int4(x0, y0, x1, y1);
   out.radii[g] = radius_out;

@@ -82,8 +82,11 @@ class DeviceSplats:
         rec[:, 0], rec[:, 1] = hi[:, 0], hi[:, 1]
         rec[:, 3] = (mean2d[:, 0] - hi[:, 0]).astype(np.float32)
         rec[:, 7] = (mean2d[:, 1] - hi[:, 1]).astype(np.float32)
-        rec[:, 2] = np.asarray(alpha, np.float64).reshape(n)
+        alpha = np.asarray(alpha, np.float64).reshape(n)
+        rec[:, 2] = alpha
         rec[:, 4:7] = conic
+        rec[:, 12:15] = conic - rec[:, 4:7].astype(np.float64)
+        rec[:, 15] = alpha - rec[:, 2].astype(np.float64)
         rec[:, 8:11] = color
         active = np.ones((n, 3), bool) if color_active is None else np.asarray(color_active, bool).reshape(n, 3)
         rec[:, 11] = (active * np.array([1, 2, 4])).sum(axis=1)
