@@ -54,7 +54,7 @@ blend_fwd_kernel(const float4* __restrict__ rec, const uint32_t* __restrict__ id
         const AlphaEval e = eval_alpha(fx, fy, s_r0[j], s_r1[j], rec, s_id[j]);
         if (e.a == 0.0f) continue;
         const float t_new = T * (1.0f - e.a);
-        if (1.0f - t_new > kSaturation) {
+        if (t_new < kTransSat) {  // 1 - T_new > 0.9999
           done = true;
           break;
         }

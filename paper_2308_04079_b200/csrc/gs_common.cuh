@@ -21,7 +21,10 @@ constexpr double kGuardBand = 1.3;              // core.py:16 GUARD_BAND
 constexpr double kRadiusSigmas = 3.0;           // core.py:18 RADIUS_SIGMAS
 constexpr float kAlphaEps = 1.0f / 255.0f;      // rasterizer.py:17 ALPHA_EPS
 constexpr float kAlphaClamp = 0.99f;            // rasterizer.py:18 ALPHA_CLAMP
-constexpr float kSaturation = 0.9999f;          // rasterizer.py:19 SATURATION
+// rasterizer.py:19 SATURATION = 0.9999; "1 - T_new > 0.9999" is evaluated as
+// T_new < 1 - 0.9999 so float32 keeps full relative precision near T = 1e-4
+// (1.0f - T would quantise T to ulp(1) = 6e-8, i.e. 6e-4 relative).
+constexpr float kTransSat = float(1.0 - 0.9999);
 constexpr int64_t kMaxInstances = int64_t(1) << 31;    // rasterizer.py:25
 constexpr int64_t kMaxTiles = (int64_t(1) << 32) - 1;  // rasterizer.py:24
 
