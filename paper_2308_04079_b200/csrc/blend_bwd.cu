@@ -1,18 +1,72 @@
 // K7 blend_bwd — replaces splatlab rasterizer.render_backward
 // (rasterizer.py:253-316) and gradients.backward_blend (gradients.py:30-94).
 //
-// Same CTA-per-tile layout as the forward.  Each tile walks its list back to
-// front from the largest last contributor of its pixels (gradients.py:48-52),
-// re-evaluating alpha with the forward's exact code so the contributor sets
-// coincide.  Each pixel rebuilds T_before by dividing out (1 - a)
-// (gradients.py:67-70) and carries the composited tail (gradients.py:75-78)
-// as a running sum.  The nine per-splat partial gradients of a warp are
-// summed with xor shuffles and committed with three float4 atomics per warp,
-// only when at least one lane contributed.
+// Same CTA-per-tile layout as the forward (warp = 8x4 pixel block).  Each
+// tile walks its list back to front from the largest last contributor of its
+// pixels (gradients.py:48-52), re-evaluating alpha with the forward's exact
+// code so the contributor sets coincide.  Each pixel rebuilds T_before by
+// dividing out (1 - a) (gradients.py:67-70) and carries the composited tail
+// (gradients.py:75-78) as a running sum.
+//
+// Reduction: a warp processes the splats of its coverage mask in groups of
+// four; the 4 x 9 per-lane partial gradients are summed across the warp by a
+// transposed (reduce-scatter) butterfly — 37 shuffles per group instead of
+// 4 x 45 — leaving each of 8 lanes one summed component, which is added to a
+// per-CTA shared-memory accumulator.  At the end of each 256-splat batch one
+// thread per splat commits the tile's sums with three float4 atomics, so the
+// global atomic traffic is one set per (splat, tile), not per (splat, warp).
 #include "gs_common.cuh"
 
 namespace gs {
 namespace {
+
+constexpr int kG = 4;    // splats per reduction group
+constexpr int kC = 9;    // gradient components per splat
+
+// Sum v[0..35] over the warp.  On return lane l holds, in `out`, component
+// (l & 7) of splat (l >> 3) of the group, and `out8` holds component 8 of
+// that splat (valid in every lane of the 8-lane group).
+__device__ __forceinline__ void group_reduce(float (&v)[kG * kC], int lane, float& out, float& out8) {
+  const bool b16 = lane & 16, b8 = lane & 8, b4 = lane & 4, b2 = lane & 2, b1 = lane & 1;
+  float w[18];
+#pragma unroll
+  for (int i = 0; i < 18; ++i) {
+    const float send = b16 ? v[i] : v[i + 18];
+    const float keep = b16 ? v[i + 18] : v[i];
+    w[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+  }
+  float x[9];
+#pragma unroll
+  for (int i = 0; i < 9; ++i) {
+    const float send = b8 ? w[i] : w[i + 9];
+    const float keep = b8 ? w[i + 9] : w[i];
+    x[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+  }
+  // component 8: full butterfly over the 8-lane group
+  float c8 = x[8];
+  c8 += __shfl_xor_sync(0xffffffffu, c8, 4);
+  c8 += __shfl_xor_sync(0xffffffffu, c8, 2);
+  c8 += __shfl_xor_sync(0xffffffffu, c8, 1);
+  out8 = c8;
+  // components 0..7: recursive halving, lane ends with component (lane & 7)
+  float y[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float send = b4 ? x[i] : x[i + 4];
+    const float keep = b4 ? x[i + 4] : x[i];
+    y[i] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+  }
+  float z[2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const float send = b2 ? y[i] : y[i + 2];
+    const float keep = b2 ? y[i + 2] : y[i];
+    z[i] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+  }
+  const float send = b1 ? z[0] : z[1];
+  const float keep = b1 ? z[1] : z[0];
+  out = keep + __shfl_xor_sync(0xffffffffu, send, 1);
+}
 
 __global__ void __launch_bounds__(kTilePixels)
 blend_bwd_kernel(const float* __restrict__ d_image, const float4* __restrict__ rec, const uint32_t* __restrict__ ids,
@@ -22,16 +76,19 @@ blend_bwd_kernel(const float* __restrict__ d_image, const float4* __restrict__ r
   __shared__ float4 s_r1[kTilePixels];
   __shared__ float4 s_col[kTilePixels];
   __shared__ uint32_t s_id[kTilePixels];
+  __shared__ uint8_t s_mask[kTilePixels];
+  __shared__ float s_grad[kTilePixels][kC];
   __shared__ int s_warp_max[kTilePixels / 32];
 
   const int tile = blockIdx.x;
   const int t = threadIdx.x;
   const int lane = t & 31, warp = t >> 5;
   const int tx = tile % tiles_x, ty = tile / tiles_x;
-  const int px = tx * kTile + (t & (kTile - 1));
-  const int py = ty * kTile + (t >> 4);
+  const int px = tx * kTile + tile_px(t);
+  const int py = ty * kTile + tile_py(t);
   const bool inside = (px < width) && (py < height);
   const float fx = float(px) + 0.5f, fy = float(py) + 0.5f;
+  const float tile_x0 = float(tx * kTile), tile_y0 = float(ty * kTile);
   const int2 range = ranges[tile];
 
   float T = 1.0f, dlx = 0.0f, dly = 0.0f, dlz = 0.0f;
@@ -48,8 +105,9 @@ blend_bwd_kernel(const float* __restrict__ d_image, const float4* __restrict__ r
   const bool nonzero = (dlx != 0.0f) || (dly != 0.0f) || (dlz != 0.0f);
   if (!__syncthreads_or(nonzero)) return;
   // needed = max(last_local) + 1 (gradients.py:48-52)
-  int wmax = __reduce_max_sync(0xffffffffu, last_idx);
-  if (lane == 0) s_warp_max[warp] = wmax;
+  const int warp_last = __reduce_max_sync(0xffffffffu, last_idx);
+  if (lane == 0) s_warp_max[warp] = warp_last;
+  for (int i = t; i < kTilePixels * kC; i += kTilePixels) (&s_grad[0][0])[i] = 0.0f;
   __syncthreads();
   int tile_last = s_warp_max[0];
 #pragma unroll
@@ -61,64 +119,88 @@ blend_bwd_kernel(const float* __restrict__ d_image, const float4* __restrict__ r
 
   for (int top = tile_last + 1; top > range.x; top -= kTilePixels) {
     const int lo = max(range.x, top - kTilePixels);
+    const int cnt = top - lo;
     __syncthreads();
-    const int i = lo + t;
-    if (i < top) {
-      const uint32_t g = ids[i];
+    if (t < cnt) {
+      const uint32_t g = ids[lo + t];
+      const float4 r0 = rec[4 * size_t(g) + 0];
+      const float4 r1 = rec[4 * size_t(g) + 1];
       s_id[t] = g;
-      s_r0[t] = rec[4 * size_t(g) + 0];
-      s_r1[t] = rec[4 * size_t(g) + 1];
+      s_r0[t] = r0;
+      s_r1[t] = r1;
       s_col[t] = rec[4 * size_t(g) + 2];
+      s_mask[t] = uint8_t(warp_cover_mask(r0, r1, tile_x0, tile_y0));
     }
     __syncthreads();
-    for (int j = top - lo - 1; j >= 0; --j) {
-      const int gi = lo + j;
-      float g_mx = 0.f, g_my = 0.f, g_al = 0.f, g_ca = 0.f, g_cb = 0.f, g_cc = 0.f, g_r = 0.f, g_g = 0.f, g_b = 0.f;
-      bool contrib = false;
-      if (gi <= last_idx) {
-        const float4 r1 = s_r1[j];
-        const AlphaEval e = eval_alpha(fx, fy, s_r0[j], r1, rec, s_id[j]);
-        if (e.a > 0.0f) {
-          contrib = true;
-          const float inv = __frcp_rn(1.0f - e.a);
-          T = T * inv;  // transmittance just before this splat
-          const float w = T * e.a;
-          const float4 c = s_col[j];
-          const float dc = c.x * dlx + c.y * dly + c.z * dlz;
-          const float d_a = T * dc - S * inv;  // gradients.py:81
-          S = fmaf(w, dc, S);
-          g_r = w * dlx;
-          g_g = w * dly;
-          g_b = w * dlz;
-          if (e.live) {  // clamped alphas pass no gradient (gradients.py:83-84)
-            g_al = d_a * e.g;
-            const float dp = d_a * e.a_raw;
-            g_mx = dp * (r1.x * e.dx + r1.y * e.dy);
-            g_my = dp * (r1.y * e.dx + r1.z * e.dy);
-            g_ca = -0.5f * dp * e.dx * e.dx;
-            g_cb = -dp * e.dx * e.dy;
-            g_cc = -0.5f * dp * e.dy * e.dy;
+    if (lo <= warp_last) {
+      const int jmax = min(cnt - 1, warp_last - lo);
+      for (int c = jmax; c >= 0; c -= 32) {
+        const int jl = c - lane;  // lane l looks at splat c - l: ascending lanes = back to front
+        unsigned live = __ballot_sync(0xffffffffu, jl >= 0 && ((s_mask[jl] >> warp) & 1u));
+        while (live) {
+          int js[kG];
+#pragma unroll
+          for (int u = 0; u < kG; ++u) {
+            js[u] = live ? c - (__ffs(live) - 1) : -1;
+            live &= live - 1;
+          }
+          float v[kG * kC];
+          bool any = false;
+#pragma unroll
+          for (int u = 0; u < kG; ++u) {
+#pragma unroll
+            for (int k = 0; k < kC; ++k) v[u * kC + k] = 0.0f;
+            const int j = js[u];
+            if (j < 0 || lo + j > last_idx) continue;
+            const float4 r1 = s_r1[j];
+            const AlphaEval e = eval_alpha(fx, fy, s_r0[j], r1, rec, s_id[j]);
+            if (e.a == 0.0f) continue;
+            any = true;
+            const float inv = __frcp_rn(1.0f - e.a);
+            T = T * inv;  // transmittance just before this splat
+            const float w = T * e.a;
+            const float4 col = s_col[j];
+            const float dc = col.x * dlx + col.y * dly + col.z * dlz;
+            const float d_a = T * dc - S * inv;  // gradients.py:81
+            S = fmaf(w, dc, S);
+            v[u * kC + 6] = w * dlx;
+            v[u * kC + 7] = w * dly;
+            v[u * kC + 8] = w * dlz;
+            if (e.live) {  // clamped alphas pass no gradient (gradients.py:83-84)
+              const float dp = d_a * e.a_raw;
+              v[u * kC + 0] = dp * (r1.x * e.dx + r1.y * e.dy);   // d_mean2d.x
+              v[u * kC + 1] = dp * (r1.y * e.dx + r1.z * e.dy);   // d_mean2d.y
+              v[u * kC + 2] = d_a * e.g;                          // d_alpha
+              v[u * kC + 3] = -0.5f * dp * e.dx * e.dx;           // d_conic a
+              v[u * kC + 4] = -dp * e.dx * e.dy;                  // d_conic b
+              v[u * kC + 5] = -0.5f * dp * e.dy * e.dy;           // d_conic c
+            }
+          }
+          if (!__any_sync(0xffffffffu, any)) continue;
+          float out, out8;
+          group_reduce(v, lane, out, out8);
+          const int j = js[lane >> 3];
+          if (j >= 0) {
+            atomicAdd(&s_grad[j][lane & 7], out);
+            if ((lane & 7) == 0) atomicAdd(&s_grad[j][8], out8);
           }
         }
       }
-      if (__any_sync(0xffffffffu, contrib)) {
-        g_mx = warp_sum(g_mx);
-        g_my = warp_sum(g_my);
-        g_al = warp_sum(g_al);
-        g_ca = warp_sum(g_ca);
-        g_cb = warp_sum(g_cb);
-        g_cc = warp_sum(g_cc);
-        g_r = warp_sum(g_r);
-        g_g = warp_sum(g_g);
-        g_b = warp_sum(g_b);
-        if (lane < 3) {
-          float4* row = grads2d + 3 * size_t(s_id[j]);
-          float4 v;
-          if (lane == 0) v = make_float4(g_mx, g_my, g_al, 0.0f);
-          else if (lane == 1) v = make_float4(g_ca, g_cb, g_cc, 0.0f);
-          else v = make_float4(g_r, g_g, g_b, 0.0f);
-          atomicAdd(row + lane, v);
-        }
+    }
+    __syncthreads();
+    // commit the tile's sums: one set of atomics per splat per tile
+    if (t < cnt) {
+      float* gr = s_grad[t];
+      const float g0 = gr[0], g1 = gr[1], g2 = gr[2], g3 = gr[3], g4 = gr[4], g5 = gr[5], g6 = gr[6],
+                  g7 = gr[7], g8 = gr[8];
+      if (g0 != 0.f || g1 != 0.f || g2 != 0.f || g3 != 0.f || g4 != 0.f || g5 != 0.f || g6 != 0.f || g7 != 0.f ||
+          g8 != 0.f) {
+        float4* row = grads2d + 3 * size_t(s_id[t]);
+        atomicAdd(row + 0, make_float4(g0, g1, g2, 0.0f));
+        atomicAdd(row + 1, make_float4(g3, g4, g5, 0.0f));
+        atomicAdd(row + 2, make_float4(g6, g7, g8, 0.0f));
+#pragma unroll
+        for (int k = 0; k < kC; ++k) gr[k] = 0.0f;
       }
     }
   }

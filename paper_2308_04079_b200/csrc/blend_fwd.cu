@@ -1,13 +1,16 @@
 // K6 blend_fwd — replaces splatlab rasterizer.render_forward / _blend_tile
 // (rasterizer.py:152-240).
 //
-// One 256-thread CTA per 16x16 tile, one pixel per thread.  The tile's sorted
-// instance list is walked front to back in batches of 256: every thread
-// gathers one splat record (48 of its 64 B) into shared memory, then each pixel blends
-// the batch sequentially.  A pixel stops before its accumulated opacity
-// would exceed 0.9999 (rasterizer.py:179-180); the CTA leaves the list as
-// soon as __syncthreads_count says every pixel is done (rasterizer.py:194-195).
-// Warps whose 32 pixels are all done skip the batch body but keep loading.
+// One 256-thread CTA per 16x16 tile, one pixel per thread, each warp an 8x4
+// pixel block.  The tile's sorted instance list is walked front to back in
+// batches of 256: every thread gathers one splat record (48 of its 64 B)
+// into shared memory and computes the splat's 8-bit warp coverage mask
+// (warp_cover_mask).  Each warp then visits, in order, only the splats whose
+// mask bit is set (a ballot over 32 mask bits at a time), so splats that
+// cannot reach alpha >= 1/255 anywhere in its block cost no pixel work.
+// A pixel stops before its accumulated opacity would exceed 0.9999
+// (rasterizer.py:179-180); the CTA leaves the list as soon as
+// __syncthreads_count says every pixel is done (rasterizer.py:194-195).
 #include "gs_common.cuh"
 
 namespace gs {
@@ -22,14 +25,17 @@ blend_fwd_kernel(const float4* __restrict__ rec, const uint32_t* __restrict__ id
   __shared__ float4 s_r1[kTilePixels];
   __shared__ float4 s_col[kTilePixels];
   __shared__ uint32_t s_id[kTilePixels];
+  __shared__ uint8_t s_mask[kTilePixels];
 
   const int tile = blockIdx.x;
   const int t = threadIdx.x;
+  const int lane = t & 31, warp = t >> 5;
   const int tx = tile % tiles_x, ty = tile / tiles_x;
-  const int px = tx * kTile + (t & (kTile - 1));
-  const int py = ty * kTile + (t >> 4);
+  const int px = tx * kTile + tile_px(t);
+  const int py = ty * kTile + tile_py(t);
   const bool inside = (px < width) && (py < height);
   const float fx = float(px) + 0.5f, fy = float(py) + 0.5f;  // rasterizer.py:142
+  const float tile_x0 = float(tx * kTile), tile_y0 = float(ty * kTile);
 
   const int2 range = ranges[tile];
   float T = 1.0f;
@@ -42,21 +48,30 @@ blend_fwd_kernel(const float4* __restrict__ rec, const uint32_t* __restrict__ id
     const int i = base + t;
     if (i < range.y) {
       const uint32_t g = ids[i];
+      const float4 r0 = rec[4 * size_t(g) + 0];
+      const float4 r1 = rec[4 * size_t(g) + 1];
       s_id[t] = g;
-      s_r0[t] = rec[4 * size_t(g) + 0];
-      s_r1[t] = rec[4 * size_t(g) + 1];
+      s_r0[t] = r0;
+      s_r1[t] = r1;
       s_col[t] = rec[4 * size_t(g) + 2];
+      s_mask[t] = uint8_t(warp_cover_mask(r0, r1, tile_x0, tile_y0));
     }
     __syncthreads();
-    if (!done) {
-      const int cnt = min(kTilePixels, range.y - base);
-      for (int j = 0; j < cnt; ++j) {
+    if (__all_sync(0xffffffffu, done)) continue;
+    const int cnt = min(kTilePixels, range.y - base);
+    for (int c0 = 0; c0 < cnt; c0 += 32) {
+      const int jl = c0 + lane;
+      unsigned live = __ballot_sync(0xffffffffu, jl < cnt && ((s_mask[jl] >> warp) & 1u));
+      while (live) {
+        const int j = c0 + __ffs(live) - 1;
+        live &= live - 1;
+        if (done) continue;
         const AlphaEval e = eval_alpha(fx, fy, s_r0[j], s_r1[j], rec, s_id[j]);
         if (e.a == 0.0f) continue;
         const float t_new = T * (1.0f - e.a);
         if (t_new < kTransSat) {  // 1 - T_new > 0.9999
           done = true;
-          break;
+          continue;
         }
         const float4 c = s_col[j];
         const float w = T * e.a;
@@ -66,6 +81,7 @@ blend_fwd_kernel(const float4* __restrict__ rec, const uint32_t* __restrict__ id
         T = t_new;
         if (kTraining) last_idx = base + j;
       }
+      if (__all_sync(0xffffffffu, done)) break;
     }
   }
   if (!inside) return;

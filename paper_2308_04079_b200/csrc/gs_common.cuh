@@ -135,6 +135,40 @@ __device__ __forceinline__ AlphaEval eval_alpha(float px, float py, float4 r0, f
   return e;
 }
 
+// ---------------------------------------------------------------------------
+// Tile CTA pixel layout: warp w covers the 8x4 pixel block at
+// ((w & 1) * 8, (w >> 1) * 4) of the 16x16 tile; lane l covers pixel
+// (l & 7, l >> 3) of that block.
+__device__ __forceinline__ int tile_px(int t) { return ((t >> 5) & 1) * 8 + (t & 7); }
+__device__ __forceinline__ int tile_py(int t) { return (t >> 6) * 4 + ((t & 31) >> 3); }
+
+// Warp coverage mask of one splat: bit w is set when the splat can reach
+// alpha >= 1/255 at some pixel centre of warp w's block.  The set
+// {alpha * exp(-Q/2) >= 1/255} is the ellipse Q(d) = d^T conic d <= 2 tau,
+// tau = ln(255 alpha); its axis-aligned box has half-extents
+// sqrt(2 tau Sigma'_xx), sqrt(2 tau Sigma'_yy).  tau and the box are
+// inflated so the test is conservative against float32 rounding: a pair is
+// skipped only if the reference would skip it (a < 1/255), so culling never
+// changes a result bit.
+__device__ __forceinline__ uint32_t warp_cover_mask(float4 r0, float4 r1, float tile_x0, float tile_y0) {
+  const float alpha = r0.z;
+  if (alpha < kAlphaEps * (1.0f - 1e-5f)) return 0u;
+  const float tau = fmaxf(__logf(255.0f * alpha), 0.0f) * 1.0001f + 1e-4f;
+  const float det = r1.x * r1.z - r1.y * r1.y;
+  if (!(det > 0.0f)) return 0xffu;  // degenerate conic: never cull
+  const float inv = 2.0f * tau / det;
+  const float hx = sqrtf(inv * r1.z) * 1.001f + 0.05f;
+  const float hy = sqrtf(inv * r1.x) * 1.001f + 0.05f;
+  const float mx = r0.x + r0.w, my = r0.y + r1.w;
+  uint32_t m = 0u;
+#pragma unroll
+  for (int w = 0; w < 8; ++w) {
+    const float x0 = tile_x0 + float((w & 1) * 8) + 0.5f, y0 = tile_y0 + float((w >> 1) * 4) + 0.5f;
+    if (mx + hx >= x0 && mx - hx <= x0 + 7.0f && my + hy >= y0 && my - hy <= y0 + 3.0f) m |= 1u << w;
+  }
+  return m;
+}
+
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
