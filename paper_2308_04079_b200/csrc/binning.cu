@@ -9,13 +9,14 @@
 //      (ties keep index order, exactly like the reference's stable sort);
 //   2. per-Gaussian instance counts gathered in depth order, exclusive scan
 //      -> instance offsets and K (one D2H read);
-//   3. emission: each Gaussian writes (tile id, gaussian id) for every tile
-//      of its rectangle, in depth-sorted Gaussian order;
+//   3. emission: warps write (tile id, gaussian id) for 32 depth-ranked
+//      Gaussians at a time into their contiguous output range, coalesced;
 //   4. stable radix sort of the instances on the tile id only
-//      (ceil(log2 T) bits = 2 passes at 1080p and 4K);
-//   5. tile ranges from neighbouring tile ids (rasterizer.py:118-123).
-// HBM traffic per instance: 8 B written by emission + 2 x 16 B per tile pass,
-// against 6 x 24 B for a 64-bit key sort.
+//      (16-bit keys and ceil(log2 T) bits = 2 passes at 1080p and 4K);
+//   5. tile ranges from neighbouring tile ids, 8 keys per thread
+//      (rasterizer.py:118-123).
+// HBM traffic per instance: 6 B written by emission + 2 x 12 B per tile
+// pass + 2 B for ranges, against 6 x 24 B for a 64-bit key sort.
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
@@ -48,35 +49,83 @@ __global__ void total_kernel(const uint64_t* __restrict__ offsets, const uint64_
   out[1] = uint64_t(status[0]);
 }
 
-// One thread per depth-ranked Gaussian; instances of one Gaussian are emitted
-// in row-major tile order (rasterizer.py:105-111).
-__global__ void emit_instances_kernel(const uint32_t* __restrict__ order, const uint64_t* __restrict__ offsets,
-                                      const uint64_t* __restrict__ counts, const int4* __restrict__ rect,
-                                      int tiles_x, uint32_t* __restrict__ tile_keys, uint32_t* __restrict__ ids,
-                                      int64_t n) {
+// Warp-cooperative emission.  A warp owns 32 consecutive depth-ranked
+// Gaussians whose instances occupy one contiguous output range (K < 2^31 is
+// checked by the host before launch).  The warp sweeps that range 32
+// positions at a time: each lane finds the Gaussian owning its position by a
+// binary search over the lanes' offsets (shuffles) and derives the tile from
+// the local index, row-major over the rectangle (rasterizer.py:105-111).
+template <typename KeyT>
+__global__ void __launch_bounds__(256)
+emit_instances_kernel(const uint32_t* __restrict__ order, const uint64_t* __restrict__ offsets,
+                      const uint64_t* __restrict__ counts, const int4* __restrict__ rect, int tiles_x,
+                      KeyT* __restrict__ tile_keys, uint32_t* __restrict__ ids, int64_t n) {
   const int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (r >= n) return;
-  const uint64_t cnt = counts[r];
-  if (cnt == 0) return;
-  const uint32_t g = order[r];
-  const int4 rc = rect[g];
-  uint64_t o = offsets[r];
-  for (int ty = rc.y; ty <= rc.w; ++ty) {
-    const uint32_t row = uint32_t(ty) * uint32_t(tiles_x);
-    for (int tx = rc.x; tx <= rc.z; ++tx) {
-      tile_keys[o] = row + uint32_t(tx);
-      ids[o] = g;
-      ++o;
+  const int lane = threadIdx.x & 31;
+  uint32_t off = 0xFFFFFFFFu, end = 0u, g = 0u;
+  int4 rc = make_int4(0, 0, 0, 0);
+  if (r < n) {
+    const uint32_t cnt = uint32_t(counts[r]);
+    off = uint32_t(offsets[r]);
+    end = off + cnt;
+    if (cnt) {
+      g = order[r];
+      rc = rect[g];
+    }
+  }
+  const uint32_t base = __shfl_sync(0xffffffffu, off, 0);
+  const uint32_t warp_end = __reduce_max_sync(0xffffffffu, end);
+  const int w = rc.z - rc.x + 1;
+  for (uint32_t ob = base; ob < warp_end; ob += 32) {
+    const uint32_t o = ob + lane;
+    int owner = 0;
+#pragma unroll
+    for (int step = 16; step >= 1; step >>= 1) {
+      const int cand = owner + step;
+      const uint32_t co = __shfl_sync(0xffffffffu, off, cand);
+      if (co <= o) owner = cand;
+    }
+    const uint32_t k = o - __shfl_sync(0xffffffffu, off, owner);
+    const int ow = __shfl_sync(0xffffffffu, w, owner);
+    const int ox = __shfl_sync(0xffffffffu, rc.x, owner);
+    const int oy = __shfl_sync(0xffffffffu, rc.y, owner);
+    const uint32_t og = __shfl_sync(0xffffffffu, g, owner);
+    if (o < warp_end) {
+      const uint32_t row = k / uint32_t(ow);
+      const uint32_t col = k - row * uint32_t(ow);
+      tile_keys[o] = KeyT((uint32_t(oy) + row) * uint32_t(tiles_x) + uint32_t(ox) + col);
+      ids[o] = og;
     }
   }
 }
 
-__global__ void tile_ranges_kernel(const uint32_t* __restrict__ tile_keys, int64_t k, int2* __restrict__ ranges) {
-  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= k) return;
-  const uint32_t t = tile_keys[i];
-  if (i == 0 || tile_keys[i - 1] != t) ranges[t].x = int(i);
-  if (i == k - 1 || tile_keys[i + 1] != t) ranges[t].y = int(i + 1);
+// Tile ranges: each thread inspects 16 bytes of sorted keys plus its two
+// neighbours and records [start, end) where the tile id changes.
+template <typename KeyT>
+__global__ void tile_ranges_kernel(const KeyT* __restrict__ keys, int64_t k, int2* __restrict__ ranges) {
+  constexpr int kPer = 16 / sizeof(KeyT);
+  const int64_t i0 = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) * kPer;
+  if (i0 >= k) return;
+  KeyT v[kPer];
+  if (i0 + kPer <= k) {
+    const uint4 raw = *reinterpret_cast<const uint4*>(keys + i0);
+    const KeyT* rv = reinterpret_cast<const KeyT*>(&raw);
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) v[j] = rv[j];
+  } else {
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) v[j] = (i0 + j < k) ? keys[i0 + j] : KeyT(0);
+  }
+  KeyT prev = i0 > 0 ? keys[i0 - 1] : KeyT(0);
+#pragma unroll
+  for (int j = 0; j < kPer; ++j) {
+    const int64_t i = i0 + j;
+    if (i >= k) break;
+    if (i == 0 || v[j] != prev) ranges[v[j]].x = int(i);
+    const bool last = (i == k - 1) || (j + 1 < kPer ? v[j + 1] != v[j] : keys[i + 1] != v[j]);
+    if (last) ranges[v[j]].y = int(i + 1);
+    prev = v[j];
+  }
 }
 
 inline size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
@@ -92,6 +141,14 @@ int bits_for(int64_t tiles) {
   return b;
 }
 
+bool small_keys(int64_t tiles) { return tiles <= 65536; }
+
+template <typename KeyT>
+cudaError_t tile_sort(void* temp, size_t& temp_bytes, const KeyT* kin, KeyT* kout, const uint32_t* vin, uint32_t* vout,
+                      int k, int bits, cudaStream_t s) {
+  return cub::DeviceRadixSort::SortPairs(temp, temp_bytes, kin, kout, vin, vout, k, 0, bits, s);
+}
+
 int make_layout(int64_t n, int64_t tiles, int64_t kcap, Layout* L) {
   size_t temp_depth = 0, temp_scan = 0, temp_tiles = 0;
   const int nn = int(n > 0 ? n : 1);
@@ -101,8 +158,11 @@ int make_layout(int64_t n, int64_t tiles, int64_t kcap, Layout* L) {
   e = cub::DeviceScan::ExclusiveSum(nullptr, temp_scan, (const uint64_t*)nullptr, (uint64_t*)nullptr, nn);
   if (e != cudaSuccess) return record_cuda_error(e);
   const int kk = int(kcap > 0 ? kcap : 1);
-  e = cub::DeviceRadixSort::SortPairs(nullptr, temp_tiles, (const uint32_t*)nullptr, (uint32_t*)nullptr,
-                                      (const uint32_t*)nullptr, (uint32_t*)nullptr, kk, 0, bits_for(tiles));
+  const size_t key_bytes = small_keys(tiles) ? 2 : 4;
+  if (small_keys(tiles))
+    e = tile_sort<uint16_t>(nullptr, temp_tiles, nullptr, nullptr, nullptr, nullptr, kk, bits_for(tiles), nullptr);
+  else
+    e = tile_sort<uint32_t>(nullptr, temp_tiles, nullptr, nullptr, nullptr, nullptr, kk, bits_for(tiles), nullptr);
   if (e != cudaSuccess) return record_cuda_error(e);
   size_t off = 0;
   auto take = [&](size_t bytes) {
@@ -118,8 +178,8 @@ int make_layout(int64_t n, int64_t tiles, int64_t kcap, Layout* L) {
   L->counts = take(8 * un);
   L->offsets = take(8 * un);
   L->total = take(16);
-  L->tile_keys_in = take(4 * uk);
-  L->tile_keys_out = take(4 * uk);
+  L->tile_keys_in = take(key_bytes * uk + 16);
+  L->tile_keys_out = take(key_bytes * uk + 16);
   L->inst_ids_in = take(4 * uk);
   size_t temp = temp_depth;
   if (temp_scan > temp) temp = temp_scan;
@@ -127,6 +187,27 @@ int make_layout(int64_t n, int64_t tiles, int64_t kcap, Layout* L) {
   L->cub_temp = take(temp);
   L->bytes = off;
   return GS_OK;
+}
+
+template <typename KeyT>
+int emit_sort_ranges(const uint32_t* order, const uint64_t* offsets, const uint64_t* counts, const int4* rect,
+                     int tiles_x, int64_t tiles, int64_t n, int64_t K, char* ws, const Layout& L, size_t temp_bytes,
+                     uint32_t* sorted_ids, int2* ranges, cudaStream_t s) {
+  auto* tk_in = reinterpret_cast<KeyT*>(ws + L.tile_keys_in);
+  auto* tk_out = reinterpret_cast<KeyT*>(ws + L.tile_keys_out);
+  auto* iid_in = reinterpret_cast<uint32_t*>(ws + L.inst_ids_in);
+  const int block = 256;
+  emit_instances_kernel<KeyT><<<unsigned((n + block - 1) / block), block, 0, s>>>(order, offsets, counts, rect,
+                                                                                   tiles_x, tk_in, iid_in, n);
+  int st = check_launch();
+  if (st != GS_OK) return st;
+  cudaError_t e = tile_sort<KeyT>(ws + L.cub_temp, temp_bytes, tk_in, tk_out, iid_in, sorted_ids, int(K),
+                                  bits_for(tiles), s);
+  if (e != cudaSuccess) return record_cuda_error(e);
+  constexpr int kPer = 16 / sizeof(KeyT);
+  const int64_t threads = (K + kPer - 1) / kPer;
+  tile_ranges_kernel<KeyT><<<unsigned((threads + block - 1) / block), block, 0, s>>>(tk_out, K, ranges);
+  return check_launch();
 }
 
 }  // namespace
@@ -174,9 +255,6 @@ extern "C" int gs_bin_and_sort(const gs_splats_t* splats, int32_t width, int32_t
   auto* counts = reinterpret_cast<uint64_t*>(ws + L.counts);
   auto* offsets = reinterpret_cast<uint64_t*>(ws + L.offsets);
   auto* total = reinterpret_cast<uint64_t*>(ws + L.total);
-  auto* tk_in = reinterpret_cast<uint32_t*>(ws + L.tile_keys_in);
-  auto* tk_out = reinterpret_cast<uint32_t*>(ws + L.tile_keys_out);
-  auto* iid_in = reinterpret_cast<uint32_t*>(ws + L.inst_ids_in);
   void* temp = ws + L.cub_temp;
   size_t temp_bytes = workspace_bytes - L.cub_temp;
 
@@ -205,14 +283,10 @@ extern "C" int gs_bin_and_sort(const gs_splats_t* splats, int32_t width, int32_t
   if (int64_t(K) > k_capacity) return GS_ERR_CAPACITY;
   if (K == 0) return GS_OK;
   if (!sorted_ids || !ranges) return GS_ERR_INVALID_ARG;
-
-  emit_instances_kernel<<<gn, block, 0, s>>>(id_out, offsets, counts, reinterpret_cast<const int4*>(splats->rect),
-                                             tiles_x, tk_in, iid_in, n);
-  if ((st = check_launch()) != GS_OK) return st;
-  e = cub::DeviceRadixSort::SortPairs(temp, temp_bytes, tk_in, tk_out, iid_in, sorted_ids, int(K), 0,
-                                      bits_for(tiles), s);
-  if (e != cudaSuccess) return record_cuda_error(e);
-  const unsigned gk = unsigned((K + block - 1) / block);
-  tile_ranges_kernel<<<gk, block, 0, s>>>(tk_out, int64_t(K), reinterpret_cast<int2*>(ranges));
-  return check_launch();
+  const int4* rect = reinterpret_cast<const int4*>(splats->rect);
+  if (small_keys(tiles))
+    return emit_sort_ranges<uint16_t>(id_out, offsets, counts, rect, tiles_x, tiles, n, int64_t(K), ws, L,
+                                      temp_bytes, sorted_ids, reinterpret_cast<int2*>(ranges), s);
+  return emit_sort_ranges<uint32_t>(id_out, offsets, counts, rect, tiles_x, tiles, n, int64_t(K), ws, L, temp_bytes,
+                                    sorted_ids, reinterpret_cast<int2*>(ranges), s);
 }

@@ -136,6 +136,36 @@ __device__ __forceinline__ AlphaEval eval_alpha(float px, float py, float4 r0, f
 }
 
 // ---------------------------------------------------------------------------
+// SH coefficient staging for the per-Gaussian kernels.  A block of B threads
+// owns B consecutive Gaussians whose (B,16,3) coefficients are one
+// contiguous 192*B-byte span: it is read with consecutive float4 loads
+// (coalesced) into shared memory rows padded to 13 float4, so each thread's
+// 12 float4 row reads are bank-conflict free (row stride 52 words).
+constexpr int kShStride = 13;
+
+__device__ __forceinline__ void stage_sh_rows(const float* __restrict__ src_rows, int64_t n, int64_t g0,
+                                              float4* __restrict__ s) {
+  const int64_t left = n - g0;
+  const int nb = left < int64_t(blockDim.x) ? int(left) : int(blockDim.x);
+  const float4* src = reinterpret_cast<const float4*>(src_rows) + g0 * 12;
+  for (int f = threadIdx.x; f < nb * 12; f += blockDim.x) {
+    const int j = f / 12;
+    s[j * kShStride + (f - j * 12)] = __ldg(src + f);
+  }
+}
+
+__device__ __forceinline__ void store_sh_rows(const float4* __restrict__ s, int64_t n, int64_t g0,
+                                              float* __restrict__ dst_rows) {
+  const int64_t left = n - g0;
+  const int nb = left < int64_t(blockDim.x) ? int(left) : int(blockDim.x);
+  float4* dst = reinterpret_cast<float4*>(dst_rows) + g0 * 12;
+  for (int f = threadIdx.x; f < nb * 12; f += blockDim.x) {
+    const int j = f / 12;
+    dst[f] = s[j * kShStride + (f - j * 12)];
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Tile CTA pixel layout: warp w covers the 8x4 pixel block at
 // ((w & 1) * 8, (w >> 1) * 4) of the 16x16 tile; lane l covers pixel
 // (l & 7, l >> 3) of that block.

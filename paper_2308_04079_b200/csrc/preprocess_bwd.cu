@@ -14,26 +14,15 @@
 namespace gs {
 namespace {
 
-__global__ void __launch_bounds__(128)
-preprocess_bwd_kernel(gs_params_t p, DevCamera cam, int degree, const float4* __restrict__ rec,
-                      const int32_t* __restrict__ radii, const float4* __restrict__ g2d, gs_grads_t out,
-                      int accumulate, gs_stats_t stats) {
-  const int64_t g = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (g >= p.n) return;
-  const int32_t radius = radii[g];
-  float* dsh = out.d_sh + 48 * g;
-  if (radius <= 0) {  // culled: exactly zero gradient (gradients.py:13-27)
-    if (!accumulate) {
-      for (int k = 0; k < 3; ++k) out.d_means[3 * g + k] = 0.0f;
-      for (int k = 0; k < 3; ++k) out.d_log_scales[3 * g + k] = 0.0f;
-      reinterpret_cast<float4*>(out.d_rotations)[g] = make_float4(0.f, 0.f, 0.f, 0.f);
-      out.d_opacity_logits[g] = 0.0f;
-      float4* d4 = reinterpret_cast<float4*>(dsh);
-      for (int k = 0; k < 12; ++k) d4[k] = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (out.view_pos_grad_norm) out.view_pos_grad_norm[g] = 0.0f;
-    }
-    return;
-  }
+// Gradients of one surviving Gaussian g.  Writes the non-SH outputs and the
+// statistics; returns the SH basis b and the masked colour gradient dcol,
+// whose outer product is the (16,3) d_sh row (written by the caller through
+// shared memory).  shrow: the Gaussian's staged SH coefficients.
+__device__ __forceinline__ void grad_one(const gs_params_t& p, const DevCamera& cam, int degree,
+                                         const float4* __restrict__ rec, const float4* __restrict__ g2d,
+                                         const gs_grads_t& out, int accumulate, const gs_stats_t& stats,
+                                         int64_t g, int32_t radius, const float4* shrow, float (&b)[16],
+                                         float (&dcol)[3]) {
   const float4 ga = g2d[3 * g + 0];  // d_mean2d.x, d_mean2d.y, d_alpha
   const float4 gb = g2d[3 * g + 1];  // d_conic a, b, c
   const float4 gc = g2d[3 * g + 2];  // d_color r, g, b
@@ -166,16 +155,21 @@ preprocess_bwd_kernel(gs_params_t p, DevCamera cam, int degree, const float4* __
   const double ddx = mx - cam.center[0], ddy = my - cam.center[1], ddz = mz - cam.center[2];
   const double dist = sqrt(ddx * ddx + ddy * ddy + ddz * ddz);
   const float vx = float(ddx / dist), vy = float(ddy / dist), vz = float(ddz / dist);
-  float b[16];
   sh_basis(vx, vy, vz, degree, b);
-  const float dcol[3] = {(mask & 1) ? gc.x : 0.0f, (mask & 2) ? gc.y : 0.0f, (mask & 4) ? gc.z : 0.0f};
-  const float* shg = p.sh + 48 * g;
+  dcol[0] = (mask & 1) ? gc.x : 0.0f;
+  dcol[1] = (mask & 2) ? gc.y : 0.0f;
+  dcol[2] = (mask & 4) ? gc.z : 0.0f;
+  float shv[48];
+#pragma unroll
+  for (int k = 0; k < 12; ++k) {
+    const float4 q4 = shrow[k];
+    shv[4 * k + 0] = q4.x; shv[4 * k + 1] = q4.y; shv[4 * k + 2] = q4.z; shv[4 * k + 3] = q4.w;
+  }
   float db[16];
   const int nrows = (degree + 1) * (degree + 1);
 #pragma unroll
-  for (int k = 0; k < 16; ++k) db[k] = 0.0f;
-  for (int k = 0; k < nrows; ++k)
-    db[k] = dcol[0] * shg[3 * k + 0] + dcol[1] * shg[3 * k + 1] + dcol[2] * shg[3 * k + 2];
+  for (int k = 0; k < 16; ++k)
+    db[k] = k < nrows ? dcol[0] * shv[3 * k + 0] + dcol[1] * shv[3 * k + 1] + dcol[2] * shv[3 * k + 2] : 0.0f;
   float gdx, gdy, gdz;
   sh_basis_vjp(vx, vy, vz, degree, db, gdx, gdy, gdz);
   const float vdot = vx * gdx + vy * gdy + vz * gdz;
@@ -189,7 +183,6 @@ preprocess_bwd_kernel(gs_params_t p, DevCamera cam, int degree, const float4* __
     dmean[j] = float(dt[0] * cam.R[j] + dt[1] * cam.R[3 + j] + dt[2] * cam.R[6 + j]) + dms[j];
   const float norm = sqrtf(ga.x * ga.x + ga.y * ga.y);  // gradients.py:258
 
-  float4* d4 = reinterpret_cast<float4*>(dsh);
   if (accumulate) {
     for (int k = 0; k < 3; ++k) out.d_means[3 * g + k] += dmean[k];
     for (int k = 0; k < 3; ++k) out.d_log_scales[3 * g + k] += float(d_logs[k]);
@@ -197,28 +190,13 @@ preprocess_bwd_kernel(gs_params_t p, DevCamera cam, int degree, const float4* __
     r.x += d_rot.x; r.y += d_rot.y; r.z += d_rot.z; r.w += d_rot.w;
     reinterpret_cast<float4*>(out.d_rotations)[g] = r;
     out.d_opacity_logits[g] += d_logit;
-    for (int k = 0; k < 12; ++k) {
-      float4 v = d4[k];
-      const int e0 = 4 * k;
-      float* pv = &v.x;
-#pragma unroll
-      for (int m = 0; m < 4; ++m) pv[m] += b[(e0 + m) / 3] * dcol[(e0 + m) % 3];
-      d4[k] = v;
-    }
-    if (out.view_pos_grad_norm) out.view_pos_grad_norm[g] = norm;
   } else {
     for (int k = 0; k < 3; ++k) out.d_means[3 * g + k] = dmean[k];
     for (int k = 0; k < 3; ++k) out.d_log_scales[3 * g + k] = float(d_logs[k]);
     reinterpret_cast<float4*>(out.d_rotations)[g] = d_rot;
     out.d_opacity_logits[g] = d_logit;
-#pragma unroll
-    for (int k = 0; k < 12; ++k) {
-      const int e0 = 4 * k;
-      d4[k] = make_float4(b[(e0 + 0) / 3] * dcol[(e0 + 0) % 3], b[(e0 + 1) / 3] * dcol[(e0 + 1) % 3],
-                          b[(e0 + 2) / 3] * dcol[(e0 + 2) % 3], b[(e0 + 3) / 3] * dcol[(e0 + 3) % 3]);
-    }
-    if (out.view_pos_grad_norm) out.view_pos_grad_norm[g] = norm;
   }
+  if (out.view_pos_grad_norm) out.view_pos_grad_norm[g] = norm;
   // densification statistics over every survivor (optimizer.py:252-255)
   if (stats.accum_pos_grad) stats.accum_pos_grad[g] += norm;
   if (stats.accum_count) stats.accum_count[g] += 1;
@@ -226,6 +204,54 @@ preprocess_bwd_kernel(gs_params_t p, DevCamera cam, int degree, const float4* __
     const float frac = float(double(radius) / double(cam.height));
     stats.max_radius_frac[g] = fmaxf(stats.max_radius_frac[g], frac);
   }
+}
+
+__global__ void __launch_bounds__(128, 4)
+preprocess_bwd_kernel(gs_params_t p, DevCamera cam, int degree, const float4* __restrict__ rec,
+                      const int32_t* __restrict__ radii, const float4* __restrict__ g2d, gs_grads_t out,
+                      int accumulate, gs_stats_t stats) {
+  __shared__ float4 s_sh[128 * kShStride];
+  const int64_t g0 = int64_t(blockIdx.x) * blockDim.x;
+  stage_sh_rows(p.sh, p.n, g0, s_sh);
+  __syncthreads();
+  const int64_t g = g0 + threadIdx.x;
+  const bool valid = g < p.n;
+  const int32_t radius = valid ? radii[g] : 0;
+  float b[16], dcol[3] = {0.0f, 0.0f, 0.0f};
+#pragma unroll
+  for (int k = 0; k < 16; ++k) b[k] = 0.0f;
+  if (radius > 0) {
+    grad_one(p, cam, degree, rec, g2d, out, accumulate, stats, g, radius, s_sh + threadIdx.x * kShStride, b, dcol);
+  } else if (valid && !accumulate) {  // culled: exactly zero gradient (gradients.py:13-27)
+    for (int k = 0; k < 3; ++k) out.d_means[3 * g + k] = 0.0f;
+    for (int k = 0; k < 3; ++k) out.d_log_scales[3 * g + k] = 0.0f;
+    reinterpret_cast<float4*>(out.d_rotations)[g] = make_float4(0.f, 0.f, 0.f, 0.f);
+    out.d_opacity_logits[g] = 0.0f;
+    if (out.view_pos_grad_norm) out.view_pos_grad_norm[g] = 0.0f;
+  }
+  // d_sh = basis (x) masked d_color (gradients.py:221), written through shared
+  // memory so the (N,16,3) stores are coalesced
+  __syncthreads();
+  if (accumulate) {
+    stage_sh_rows(out.d_sh, p.n, g0, s_sh);
+    __syncthreads();
+  }
+  if (valid) {
+    float4* row = s_sh + threadIdx.x * kShStride;
+#pragma unroll
+    for (int k = 0; k < 12; ++k) {
+      const int e0 = 4 * k;
+      float4 v = make_float4(b[(e0 + 0) / 3] * dcol[(e0 + 0) % 3], b[(e0 + 1) / 3] * dcol[(e0 + 1) % 3],
+                             b[(e0 + 2) / 3] * dcol[(e0 + 2) % 3], b[(e0 + 3) / 3] * dcol[(e0 + 3) % 3]);
+      if (accumulate) {
+        const float4 o = row[k];
+        v.x += o.x; v.y += o.y; v.z += o.z; v.w += o.w;
+      }
+      row[k] = v;
+    }
+  }
+  __syncthreads();
+  store_sh_rows(s_sh, p.n, g0, out.d_sh);
 }
 
 }  // namespace

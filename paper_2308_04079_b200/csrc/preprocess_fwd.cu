@@ -16,7 +16,11 @@ __device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a,
 
 __global__ void __launch_bounds__(128)
 preprocess_fwd_kernel(gs_params_t p, DevCamera cam, int degree, gs_splats_t out) {
-  const int64_t g = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  __shared__ float4 s_sh[128 * kShStride];
+  const int64_t g0 = int64_t(blockIdx.x) * blockDim.x;
+  stage_sh_rows(p.sh, p.n, g0, s_sh);
+  __syncthreads();
+  const int64_t g = g0 + threadIdx.x;
   if (g >= p.n) return;
 
   // view = means @ W^T + t (core.py:279)
@@ -138,12 +142,20 @@ preprocess_fwd_kernel(gs_params_t p, DevCamera cam, int degree, gs_splats_t out)
   float b[16];
   sh_basis(vx, vy, vz, degree, b);
   const int nrows = (degree + 1) * (degree + 1);
-  const float* shg = p.sh + 48 * g;
+  float shv[48];
+#pragma unroll
+  for (int k = 0; k < 12; ++k) {
+    const float4 q4 = s_sh[threadIdx.x * kShStride + k];
+    shv[4 * k + 0] = q4.x; shv[4 * k + 1] = q4.y; shv[4 * k + 2] = q4.z; shv[4 * k + 3] = q4.w;
+  }
   float col[3] = {0.0f, 0.0f, 0.0f};
-  for (int k = 0; k < nrows; ++k) {
-    col[0] = fmaf(b[k], shg[3 * k + 0], col[0]);
-    col[1] = fmaf(b[k], shg[3 * k + 1], col[1]);
-    col[2] = fmaf(b[k], shg[3 * k + 2], col[2]);
+#pragma unroll
+  for (int k = 0; k < 16; ++k) {
+    if (k < nrows) {
+      col[0] = fmaf(b[k], shv[3 * k + 0], col[0]);
+      col[1] = fmaf(b[k], shv[3 * k + 1], col[1]);
+      col[2] = fmaf(b[k], shv[3 * k + 2], col[2]);
+    }
   }
   int mask = 0;
 #pragma unroll
