@@ -137,11 +137,9 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
     flat = None
     if world > 1:
         # gradients live in one flat buffer so one NCCL all-reduce covers every group
-        sizes = [n * 3, n * 4, n * 3, n, n * 48]
-        flat = torch.zeros(sum(sizes), dtype=torch.float32, device=dev)
-        parts = torch.split(flat, sizes)
-        grads = R.GaussianGrads(parts[0].view(n, 3), parts[1].view(n, 4), parts[2].view(n, 3), parts[3].view(n),
-                                parts[4].view(n, 16, 3), torch.zeros(n, device=dev))
+        from paper_2308_04079_b200.distributed import GradientBucket
+        bucket = GradientBucket(n, dev)
+        flat, grads = bucket.flat, bucket.grads
     timer = StageTimer(enabled=True)
     iteration = [0]
 

@@ -60,7 +60,7 @@ class DeviceSplats:
     def empty(cls, n: int, device) -> "DeviceSplats":
         f32, i32 = dict(dtype=torch.float32, device=device), dict(dtype=torch.int32, device=device)
         return cls(torch.empty((n, _lib.REC_FLOATS), **f32), torch.empty(n, **f32), torch.empty(n, **i32),
-                   torch.empty((n, 4), **i32), torch.empty(n, **i32), torch.zeros(1, **i32))
+                   torch.empty((n, 4), **i32), torch.empty(n, **i32), torch.empty(1, **i32))
 
     def __len__(self) -> int:
         return self.radii.shape[0]

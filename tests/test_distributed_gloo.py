@@ -1,0 +1,82 @@
+"""Multi-process (gloo, world size 2, CPU) tests of the view-parallel plumbing:
+view sharding, the flat gradient bucket and its all-reduce, and the
+cross-rank densification statistics."""
+import os
+import socket
+
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2308_04079_b200.distributed import (FLOATS_PER_GAUSSIAN, GradientBucket, reduce_stats_,
+                                                shard_views)
+from paper_2308_04079_b200.rasterizer import DensifyStats
+
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, results):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        n = 5
+        bucket = GradientBucket(n, "cpu")
+        g = bucket.grads
+        # each rank writes a distinct per-view gradient through the group views
+        g.d_means.fill_(rank + 1.0)
+        g.d_sh[:, 0, 0] = 10.0 * (rank + 1)
+        g.d_opacity_logits[2] = -1.0
+        bucket.allreduce_()
+        stats = DensifyStats(torch.full((n,), float(rank + 1)), torch.full((n,), rank + 1, dtype=torch.int32),
+                             torch.tensor([0.1 * (rank + 1)] * n))
+        reduce_stats_(stats)
+        results[rank] = {
+            "means": g.d_means.clone(), "sh00": g.d_sh[:, 0, 0].clone(), "opac": g.d_opacity_logits.clone(),
+            "flat_is_view": g.d_means.data_ptr() == bucket.flat.data_ptr(),
+            "accum": stats.accum_pos_grad.clone(), "count": stats.accum_count.clone(),
+            "maxr": stats.max_radius_frac.clone(),
+        }
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gradient_bucket_and_stats_allreduce_world2():
+    world = 2
+    port = _free_port()
+    with mp.Manager() as mgr:
+        results = mgr.dict()
+        mp.spawn(_worker, args=(world, port, results), nprocs=world, join=True)
+        res = dict(results)
+    for rank in range(world):
+        r = res[rank]
+        assert r["flat_is_view"]
+        assert torch.all(r["means"] == 3.0)             # 1 + 2
+        assert torch.all(r["sh00"] == 30.0)             # 10 + 20
+        assert float(r["opac"][2]) == -2.0 and float(r["opac"][0]) == 0.0
+        assert torch.all(r["accum"] == 3.0)
+        assert torch.all(r["count"] == 3)
+        assert torch.allclose(r["maxr"], torch.full((5,), 0.2))
+    # replicas hold bit-identical reduced gradients
+    assert torch.equal(res[0]["means"], res[1]["means"])
+
+
+def test_bucket_layout():
+    b = GradientBucket(7, "cpu")
+    assert b.flat.numel() == 7 * FLOATS_PER_GAUSSIAN == 7 * 59
+    assert b.grads.d_sh.shape == (7, 16, 3) and b.grads.d_rotations.shape == (7, 4)
+    b.grads.d_sh.fill_(1.0)
+    assert float(b.flat.sum()) == 7 * 48
+
+
+@pytest.mark.parametrize("views,world", [(32, 2), (32, 4), (32, 8), (7, 3), (1, 2)])
+def test_shard_views_partition(views, world):
+    shards = [shard_views(views, world, r) for r in range(world)]
+    flat = [v for s in shards for v in s]
+    assert flat == list(range(views))
+    assert max(map(len, shards)) - min(map(len, shards)) <= 1
