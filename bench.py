@@ -105,7 +105,7 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
     from paper_2308_04079_b200.cloud import GaussianCloud
     from paper_2308_04079_b200.loss import l1_dssim_loss
     from paper_2308_04079_b200.optimizer import DeviceAdam, TrainConfig
-    from paper_2308_04079_b200.profiling import StageTimer
+    from paper_2308_04079_b200.profiling import StageTimer, evaluated_pairs, measure_fp32_peak
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
@@ -255,13 +255,26 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
     torch.cuda.synchronize()
     render_ms = f0.elapsed_time(f1) / fps_steps
 
+    # evaluated (pixel, splat) pairs E from the forward's own training record, and
+    # the FP32 FMA peak of this GPU (the blend kernels' roofline denominator)
+    with torch.no_grad():
+        out_e, splats_e, binning_e = R.render_view(cloud, cam, bg, DEGREE, training=True)
+        e_pairs = evaluated_pairs(out_e, binning_e, WIDTH)
+        visible = int((splats_e.radii > 0).sum().item())
+    fp32_peak = measure_fp32_peak(dev) / 1e12
+
     if rank != 0:
         return
     ms_per_step = ms_max / args.steps
     value = world * args.steps / (ms_max / 1e3)
     e2e_value = world * args.steps / (e2e_ms / 1e3)
     stage_ms = timer.mean_ms()
-    roof = timer.roofline(n, WIDTH, HEIGHT, peaks())
+    pk = dict(peaks())
+    pk["fp32_tflops"] = fp32_peak
+    traffic_file = ROOT / "profiles" / "traffic_bytes.json"
+    if traffic_file.exists():
+        pk["traffic_bytes"] = json.loads(traffic_file.read_text()).get("per_launch", {})
+    roof = timer.roofline(n, WIDTH, HEIGHT, pk, visible=visible, e_pairs=e_pairs)
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
@@ -273,12 +286,13 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
                    "l2": "inputs larger than L2 (708 MB parameters + 2.1 GB Adam state)"},
         "render_fps": round(1e3 / render_ms, 2), "render_ms": round(render_ms, 4),
         "stage_ms": {k: round(v, 4) for k, v in stage_ms.items()},
-        "instances_per_view": timer.last_k, "evaluated_pairs_per_view": timer.last_e,
+        "instances_per_view": timer.last_k, "evaluated_pairs_per_view": e_pairs, "visible_gaussians": visible,
         "e2e": {"value": round(e2e_value, 3), "unit": UNIT, "h2d_bytes_per_step": WIDTH * HEIGHT * 3 * 4,
                 "d2h_bytes_per_step": 4, "path": "GaussianRasterizer autograd.Function + DeviceAdam, "
                                                  "target image from pinned host memory"},
         "gpu_launches": timer.launches_per_step() * args.steps,
-        "roofline": roof["primary"], "roofline_stages": roof["stages"],
+        "roofline": roof["primary"], "roofline_hbm": roof["hbm"], "roofline_stages": roof["stages"],
+        "fp32_peak_tflops_measured": round(fp32_peak, 2),
         "clocks": clock_info,
     }
     if args.cpu_baseline:

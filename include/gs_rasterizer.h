@@ -139,6 +139,10 @@ int gs_abi_version(void);
 const char* gs_status_string(int status);
 /* Copies the last CUDA error string seen by the library into buf. */
 int gs_last_cuda_error(char* buf, size_t len);
+/* Diagnostics: FP32 FMA throughput probe used by bench.py as the roofline
+ * denominator of the blend kernels (blocks x 256 threads x iters x 8 FMAs;
+ * scratch: >= blocks floats, device). */
+int gs_fp32_fma_probe(float* scratch, int32_t blocks, int32_t iters, void* stream);
 
 /* ---- K1 preprocess: replaces core.project (core.py:266-345) ------------- */
 /* Culls (near plane, guard band, det <= 0), builds the EWA conic, radius,

@@ -69,6 +69,7 @@ SIGNATURES = [
     ("gs_abi_version", c_int32, []),
     ("gs_status_string", ctypes.c_char_p, [c_int32]),
     ("gs_last_cuda_error", c_int32, [ctypes.c_char_p, c_size_t]),
+    ("gs_fp32_fma_probe", c_int32, [c_void_p, c_int32, c_int32, c_void_p]),
     ("gs_preprocess_forward", c_int32, [POINTER(GsParams), POINTER(GsCamera), c_int32, POINTER(GsSplats), c_void_p]),
     ("gs_bin_workspace_size", c_int32, [c_int64, c_int32, c_int32, c_int64, POINTER(c_size_t)]),
     ("gs_bin_and_sort", c_int32, [POINTER(GsSplats), c_int32, c_int32, c_void_p, c_size_t, c_int64, c_void_p,

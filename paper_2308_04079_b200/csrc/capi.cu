@@ -21,6 +21,33 @@ int check_launch() {
 
 }  // namespace gs
 
+namespace gs {
+namespace {
+// FP32 FMA throughput probe: 8 independent FMA chains per thread, enough
+// resident warps to saturate every SM's FMA pipes.
+__global__ void __launch_bounds__(256) fma_probe_kernel(float* out, int iters) {
+  float a[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) a[k] = float(threadIdx.x + k) * 1e-3f;
+  const float b = 0.999f, c = 1e-4f;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a[k] = fmaf(a[k], b, c);
+  }
+  float s = 0.0f;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) s += a[k];
+  if (s == -1.0f) out[blockIdx.x] = s;  // never true; keeps the chains alive
+}
+}  // namespace
+}  // namespace gs
+
+extern "C" int gs_fp32_fma_probe(float* scratch, int32_t blocks, int32_t iters, void* stream) {
+  if (!scratch || blocks <= 0 || iters <= 0) return GS_ERR_INVALID_ARG;
+  gs::fma_probe_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(scratch, iters);
+  return gs::check_launch();
+}
+
 extern "C" int gs_abi_version(void) { return GS_ABI_VERSION; }
 
 extern "C" const char* gs_status_string(int status) {

@@ -82,17 +82,75 @@ class StageTimer:
             "loss": 132 * P,
         }
         hbm = float(peaks.get("hbm_gbs", 6650.0))
+        fp32 = peaks.get("fp32_tflops")  # measured in-run by measure_fp32_peak
+        flops = {}
+        if e_pairs:
+            flops = {"blend_fwd": 25.0 * e_pairs, "blend_bwd": 60.0 * e_pairs}
+        traffic = peaks.get("traffic_bytes", {})
         stages = {}
         for k, t in ms.items():
             if k in bytes_ and t > 0:
                 gbs = bytes_[k] / (t * 1e-3) / 1e9
-                stages[k] = {"ms": round(t, 4), "algorithmic_bytes": bytes_[k], "achieved_gbs": round(gbs, 1),
-                             "frac_hbm": round(gbs / hbm, 4)}
+                st = {"ms": round(t, 4), "algorithmic_bytes": bytes_[k], "achieved_gbs": round(gbs, 1),
+                      "frac_hbm": round(gbs / hbm, 4)}
+                if k in flops and fp32:
+                    tf = flops[k] / (t * 1e-3) / 1e12
+                    st.update({"algorithmic_flops": flops[k], "achieved_tflops": round(tf, 2),
+                               "frac_fp32": round(tf / fp32, 4)})
+                stages[k] = st
         dom = max(ms, key=lambda k: ms[k]) if ms else None
         primary = None
         if dom in stages:
             st = stages[dom]
-            primary = {"kernel": dom, "bound": "hbm", "achieved": st["achieved_gbs"], "peak": hbm, "unit": "GB/s",
-                       "frac": st["frac_hbm"], "traffic": None,
-                       "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6650"}
-        return {"primary": primary, "stages": stages}
+            if "frac_fp32" in st:
+                primary = {"kernel": dom, "bound": "fp32", "achieved": st["achieved_tflops"], "peak": round(fp32, 2),
+                           "unit": "TFLOP/s", "frac": st["frac_fp32"], "traffic": traffic.get(dom),
+                           "peak_source": "in-run FP32 FMA probe (gs_fp32_fma_probe); MEASURED_PEAKS.json has "
+                                          "no FP32 figure and this kernel is FP32-issue-bound, not HBM/tensor",
+                           "algorithmic": f"{st['algorithmic_flops']:.4g} FLOP per launch "
+                                          f"(25|60 FP32 ops x E={e_pairs} evaluated pairs)"}
+            else:
+                primary = {"kernel": dom, "bound": "hbm", "achieved": st["achieved_gbs"], "peak": hbm,
+                           "unit": "GB/s", "frac": st["frac_hbm"], "traffic": traffic.get(dom),
+                           "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6650"}
+        hbm_stages = {k: v for k, v in stages.items() if k not in flops}
+        top_hbm = max(hbm_stages, key=lambda k: hbm_stages[k]["ms"]) if hbm_stages else None
+        secondary = None
+        if top_hbm:
+            st = hbm_stages[top_hbm]
+            secondary = {"kernel": top_hbm, "bound": "hbm", "achieved": st["achieved_gbs"], "peak": hbm,
+                         "unit": "GB/s", "frac": st["frac_hbm"], "traffic": traffic.get(top_hbm),
+                         "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6650"}
+        return {"primary": primary, "hbm": secondary, "stages": stages}
+
+
+def measure_fp32_peak(device=None, iters: int = 4096) -> float:
+    """FP32 FMA throughput (FLOP/s, FMA = 2) of this GPU, from gs_fp32_fma_probe."""
+    from . import _lib
+    lib = _lib.load()
+    props = torch.cuda.get_device_properties(device)
+    blocks = props.multi_processor_count * 8
+    scratch = torch.empty(blocks, dtype=torch.float32, device=device)
+    stream = torch.cuda.current_stream(device).cuda_stream
+    for _ in range(2):
+        _lib.check(lib.gs_fp32_fma_probe(scratch.data_ptr(), blocks, iters, stream), "fma_probe")
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    reps = 5
+    for _ in range(reps):
+        _lib.check(lib.gs_fp32_fma_probe(scratch.data_ptr(), blocks, iters, stream), "fma_probe")
+    e.record()
+    torch.cuda.synchronize(device)
+    secs = s.elapsed_time(e) / 1e3 / reps
+    return blocks * 256 * iters * 8 * 2 / secs
+
+
+def evaluated_pairs(out, binning, width: int) -> int:
+    """E = sum over pixels of (last_contributor - tile_start + 1)."""
+    last = out.last_contributor.long()
+    h, w = last.shape
+    ty = torch.arange(h, device=last.device) // 16
+    tx = torch.arange(w, device=last.device) // 16
+    tiles = ty[:, None] * binning.tiles_x + tx[None, :]
+    start = binning.ranges[:, 0].long()[tiles]
+    return int(torch.where(last >= 0, last - start + 1, torch.zeros_like(last)).sum().item())
