@@ -208,14 +208,34 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
                                    opacity_logits=leaves[3].data, sh=leaves[4].data)
     e2e_adam = DeviceAdam(e2e_adam_cloud)
     e2e_it = [0]
+    # each step's target image is copied H2D from pinned memory on a copy stream,
+    # double-buffered so step i+1's copy overlaps step i's compute
+    copy_stream = torch.cuda.Stream(dev)
+    gt_bufs = [torch.empty_like(target) for _ in range(2)]
+    ready = [torch.cuda.Event() for _ in range(2)]
+    consumed = [torch.cuda.Event() for _ in range(2)]
 
-    def e2e_step() -> float:
+    def prefetch(i: int) -> None:
+        b = i % 2
+        with torch.cuda.stream(copy_stream):
+            copy_stream.wait_event(consumed[b])
+            gt_bufs[b].copy_(gt_host, non_blocking=True)
+            ready[b].record(copy_stream)
+
+    def e2e_step(i: int, count: int) -> float:
         e2e_it[0] += 1
-        gt = gt_host.to(dev, non_blocking=True)
+        if i == 0:
+            prefetch(0)
+        if i + 1 < count:
+            prefetch(i + 1)
+        b = i % 2
+        torch.cuda.current_stream().wait_event(ready[b])
+        gt = gt_bufs[b]
         for leaf in leaves:
             leaf.grad = None
         image, radii = R.rasterize_gaussians(*leaves, cam, bg, DEGREE, stats)
         loss, d_image = l1_dssim_loss(image.detach(), gt, LAMBDA_DSSIM)
+        consumed[b].record()
         image.backward(d_image)
         g = R.GaussianGrads(leaves[0].grad, leaves[2].grad, leaves[1].grad, leaves[3].grad, leaves[4].grad,
                             stats.accum_pos_grad)
@@ -225,15 +245,15 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
         e2e_adam.step(e2e_adam_cloud, g, e2e_it[0], config)
         return float(loss[0].item())   # D2H of the step's loss
 
-    for _ in range(args.warmup):
-        e2e_step()
+    for i in range(args.warmup):
+        e2e_step(i, args.warmup)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    for _ in range(args.steps):
-        e2e_step()
+    for i in range(args.steps):
+        e2e_step(i, args.steps)
     e1.record()
     torch.cuda.synchronize()
     e_ms = torch.tensor([e0.elapsed_time(e1)], device=dev)

@@ -1,27 +1,42 @@
 // K7 blend_bwd — replaces splatlab rasterizer.render_backward
 // (rasterizer.py:253-316) and gradients.backward_blend (gradients.py:30-94).
 //
-// Same CTA-per-tile layout as the forward (warp = 8x4 pixel block).  Each
-// tile walks its list back to front from the largest last contributor of its
-// pixels (gradients.py:48-52), re-evaluating alpha with the forward's exact
-// code so the contributor sets coincide.  Each pixel rebuilds T_before by
-// dividing out (1 - a) (gradients.py:67-70) and carries the composited tail
-// (gradients.py:75-78) as a running sum.
+// Same tiling as the forward (8 consumer warps = 8x4 pixel blocks + 1
+// producer warp, kStages-deep ring of shared-memory batches with mbarriers).
+// Each tile walks its list back to front from the largest last contributor
+// of its pixels (gradients.py:48-52), re-evaluating alpha with the forward's
+// exact code so the contributor sets coincide.  Each pixel rebuilds T_before
+// by dividing out (1 - a) (gradients.py:67-70) and carries the composited
+// tail (gradients.py:75-78) as a running sum.
 //
 // Reduction: a warp processes the splats of its coverage mask in groups of
 // four; the 4 x 9 per-lane partial gradients are summed across the warp by a
 // transposed (reduce-scatter) butterfly — 37 shuffles per group instead of
-// 4 x 45 — leaving each of 8 lanes one summed component, which is added to a
-// per-CTA shared-memory accumulator.  At the end of each 256-splat batch one
-// thread per splat commits the tile's sums with three float4 atomics, so the
-// global atomic traffic is one set per (splat, tile), not per (splat, warp).
+// 4 x 45 — leaving each of 8 lanes one summed component, which is added to
+// the stage's shared-memory accumulator.  When every consumer is done with a
+// stage the producer commits the tile's sums with three float4 atomics per
+// splat (one set per (splat, tile)) before refilling the stage.
 #include "gs_common.cuh"
 
 namespace gs {
 namespace {
 
+constexpr int kBatch = 256;
+constexpr int kStages = 3;
+constexpr int kConsumerWarps = 8;
+constexpr int kThreads = (kConsumerWarps + 1) * 32;
 constexpr int kG = 4;    // splats per reduction group
 constexpr int kC = 9;    // gradient components per splat
+
+struct BwdStage {
+  float4 r0[kBatch];
+  float4 r1[kBatch];
+  float4 col[kBatch];
+  float grad[kBatch][kC];
+  uint32_t id[kBatch];
+  uint8_t mask[kBatch];
+};
+constexpr size_t kSmemBytes = sizeof(BwdStage) * kStages;
 
 // Sum v[0..35] over the warp.  On return lane l holds, in `out`, component
 // (l & 7) of splat (l >> 3) of the group, and `out8` holds component 8 of
@@ -42,13 +57,11 @@ __device__ __forceinline__ void group_reduce(float (&v)[kG * kC], int lane, floa
     const float keep = b8 ? w[i + 9] : w[i];
     x[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
   }
-  // component 8: full butterfly over the 8-lane group
   float c8 = x[8];
   c8 += __shfl_xor_sync(0xffffffffu, c8, 4);
   c8 += __shfl_xor_sync(0xffffffffu, c8, 2);
   c8 += __shfl_xor_sync(0xffffffffu, c8, 1);
   out8 = c8;
-  // components 0..7: recursive halving, lane ends with component (lane & 7)
   float y[4];
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
@@ -68,25 +81,47 @@ __device__ __forceinline__ void group_reduce(float (&v)[kG * kC], int lane, floa
   out = keep + __shfl_xor_sync(0xffffffffu, send, 1);
 }
 
-__global__ void __launch_bounds__(kTilePixels)
+// batch b covers sorted positions [lo, top) counted back from the tile's end
+__device__ __forceinline__ void batch_bounds(int b, int tile_top, int range_lo, int& lo, int& cnt) {
+  const int top = tile_top - b * kBatch;
+  lo = max(range_lo, top - kBatch);
+  cnt = top - lo;
+}
+
+__device__ __forceinline__ void flush_stage(BwdStage& st, int cnt, int lane, float4* __restrict__ grads2d) {
+  for (int e = lane; e < cnt; e += 32) {
+    float* gr = st.grad[e];
+    const float g0 = gr[0], g1 = gr[1], g2 = gr[2], g3 = gr[3], g4 = gr[4], g5 = gr[5], g6 = gr[6], g7 = gr[7],
+                g8 = gr[8];
+    if (g0 != 0.f || g1 != 0.f || g2 != 0.f || g3 != 0.f || g4 != 0.f || g5 != 0.f || g6 != 0.f || g7 != 0.f ||
+        g8 != 0.f) {
+      float4* row = grads2d + 3 * size_t(st.id[e]);
+      atomicAdd(row + 0, make_float4(g0, g1, g2, 0.0f));
+      atomicAdd(row + 1, make_float4(g3, g4, g5, 0.0f));
+      atomicAdd(row + 2, make_float4(g6, g7, g8, 0.0f));
+#pragma unroll
+      for (int k = 0; k < kC; ++k) gr[k] = 0.0f;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kThreads, 3)
 blend_bwd_kernel(const float* __restrict__ d_image, const float4* __restrict__ rec, const uint32_t* __restrict__ ids,
                  const int2* __restrict__ ranges, const float* __restrict__ t_final, const int32_t* __restrict__ last,
                  int width, int height, int tiles_x, float3 bg, float4* __restrict__ grads2d) {
-  __shared__ float4 s_r0[kTilePixels];
-  __shared__ float4 s_r1[kTilePixels];
-  __shared__ float4 s_col[kTilePixels];
-  __shared__ uint32_t s_id[kTilePixels];
-  __shared__ uint8_t s_mask[kTilePixels];
-  __shared__ float s_grad[kTilePixels][kC];
-  __shared__ int s_warp_max[kTilePixels / 32];
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  BwdStage* stages = reinterpret_cast<BwdStage*>(smem_raw);
+  __shared__ uint64_t full_bar[kStages], empty_bar[kStages];
+  __shared__ int s_warp_max[kConsumerWarps + 1];
 
   const int tile = blockIdx.x;
   const int t = threadIdx.x;
   const int lane = t & 31, warp = t >> 5;
+  const bool consumer = warp < kConsumerWarps;
   const int tx = tile % tiles_x, ty = tile / tiles_x;
   const int px = tx * kTile + tile_px(t);
   const int py = ty * kTile + tile_py(t);
-  const bool inside = (px < width) && (py < height);
+  const bool inside = consumer && (px < width) && (py < height);
   const float fx = float(px) + 0.5f, fy = float(py) + 0.5f;
   const float tile_x0 = float(tx * kTile), tile_y0 = float(ty * kTile);
   const int2 range = ranges[tile];
@@ -107,36 +142,82 @@ blend_bwd_kernel(const float* __restrict__ d_image, const float4* __restrict__ r
   // needed = max(last_local) + 1 (gradients.py:48-52)
   const int warp_last = __reduce_max_sync(0xffffffffu, last_idx);
   if (lane == 0) s_warp_max[warp] = warp_last;
-  for (int i = t; i < kTilePixels * kC; i += kTilePixels) (&s_grad[0][0])[i] = 0.0f;
+  if (t == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full_bar[s], 32);
+      mbar_init(&empty_bar[s], kConsumerWarps);
+    }
+  }
+  for (int i = t; i < kStages * kBatch * kC; i += kThreads) {
+    const int s = i / (kBatch * kC), r = i - s * (kBatch * kC);
+    (&stages[s].grad[0][0])[r] = 0.0f;
+  }
   __syncthreads();
   int tile_last = s_warp_max[0];
 #pragma unroll
-  for (int w = 1; w < kTilePixels / 32; ++w) tile_last = max(tile_last, s_warp_max[w]);
+  for (int w = 1; w < kConsumerWarps; ++w) tile_last = max(tile_last, s_warp_max[w]);
   if (tile_last < range.x) return;
+  const int tile_top = tile_last + 1;
+  const int nb = (tile_top - range.x + kBatch - 1) / kBatch;
 
+  if (!consumer) {  // ---------------- producer warp: load, then flush behind the consumers
+    for (int b = 0; b < nb + kStages; ++b) {
+      const int s = b % kStages;
+      if (b >= kStages) {
+        while (!mbar_try_wait(&empty_bar[s], uint32_t((b / kStages) - 1) & 1u)) {
+        }
+        int plo, pcnt;
+        batch_bounds(b - kStages, tile_top, range.x, plo, pcnt);
+        flush_stage(stages[s], pcnt, lane, grads2d);
+      }
+      if (b < nb) {
+        int lo, cnt;
+        batch_bounds(b, tile_top, range.x, lo, cnt);
+        BwdStage& st = stages[s];
+        uint32_t gid[kBatch / 32];
+#pragma unroll
+        for (int u = 0; u < kBatch / 32; ++u) {
+          const int e = lane + 32 * u;
+          gid[u] = e < cnt ? __ldg(ids + lo + e) : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < kBatch / 32; ++u) {
+          const int e = lane + 32 * u;
+          if (e < cnt) {
+            const float4* src = rec + 4 * size_t(gid[u]);
+            st.id[e] = gid[u];
+            cp_async16(&st.r0[e], src + 0);
+            cp_async16(&st.r1[e], src + 1);
+            cp_async16(&st.col[e], src + 2);
+          }
+        }
+        cp_async_wait_all();
+#pragma unroll
+        for (int u = 0; u < kBatch / 32; ++u) {
+          const int e = lane + 32 * u;
+          if (e < cnt) st.mask[e] = uint8_t(warp_cover_mask(st.r0[e], st.r1[e], tile_x0, tile_y0));
+        }
+        mbar_arrive(&full_bar[s]);
+      }
+    }
+    return;
+  }
+
+  // ---------------- consumer warps
   // composited tail behind the current splat, starts at the background term
   float S = T * (dlx * bg.x + dly * bg.y + dlz * bg.z);
-
-  for (int top = tile_last + 1; top > range.x; top -= kTilePixels) {
-    const int lo = max(range.x, top - kTilePixels);
-    const int cnt = top - lo;
-    __syncthreads();
-    if (t < cnt) {
-      const uint32_t g = ids[lo + t];
-      const float4 r0 = rec[4 * size_t(g) + 0];
-      const float4 r1 = rec[4 * size_t(g) + 1];
-      s_id[t] = g;
-      s_r0[t] = r0;
-      s_r1[t] = r1;
-      s_col[t] = rec[4 * size_t(g) + 2];
-      s_mask[t] = uint8_t(warp_cover_mask(r0, r1, tile_x0, tile_y0));
+  for (int b = 0; b < nb; ++b) {
+    const int s = b % kStages;
+    while (!mbar_try_wait(&full_bar[s], uint32_t(b / kStages) & 1u)) {
     }
-    __syncthreads();
+    int lo, cnt;
+    batch_bounds(b, tile_top, range.x, lo, cnt);
+    BwdStage& st = stages[s];
     if (lo <= warp_last) {
       const int jmax = min(cnt - 1, warp_last - lo);
       for (int c = jmax; c >= 0; c -= 32) {
         const int jl = c - lane;  // lane l looks at splat c - l: ascending lanes = back to front
-        unsigned live = __ballot_sync(0xffffffffu, jl >= 0 && ((s_mask[jl] >> warp) & 1u));
+        unsigned live = __ballot_sync(0xffffffffu, jl >= 0 && ((st.mask[jl] >> warp) & 1u));
         while (live) {
           int js[kG];
 #pragma unroll
@@ -152,14 +233,14 @@ blend_bwd_kernel(const float* __restrict__ d_image, const float4* __restrict__ r
             for (int k = 0; k < kC; ++k) v[u * kC + k] = 0.0f;
             const int j = js[u];
             if (j < 0 || lo + j > last_idx) continue;
-            const float4 r1 = s_r1[j];
-            const AlphaEval e = eval_alpha(fx, fy, s_r0[j], r1, rec, s_id[j]);
+            const float4 r1 = st.r1[j];
+            const AlphaEval e = eval_alpha(fx, fy, st.r0[j], r1, rec, st.id[j]);
             if (e.a == 0.0f) continue;
             any = true;
             const float inv = __frcp_rn(1.0f - e.a);
             T = T * inv;  // transmittance just before this splat
             const float w = T * e.a;
-            const float4 col = s_col[j];
+            const float4 col = st.col[j];
             const float dc = col.x * dlx + col.y * dly + col.z * dlz;
             const float d_a = T * dc - S * inv;  // gradients.py:81
             S = fmaf(w, dc, S);
@@ -181,28 +262,14 @@ blend_bwd_kernel(const float* __restrict__ d_image, const float4* __restrict__ r
           group_reduce(v, lane, out, out8);
           const int j = js[lane >> 3];
           if (j >= 0) {
-            atomicAdd(&s_grad[j][lane & 7], out);
-            if ((lane & 7) == 0) atomicAdd(&s_grad[j][8], out8);
+            atomicAdd(&st.grad[j][lane & 7], out);
+            if ((lane & 7) == 0) atomicAdd(&st.grad[j][8], out8);
           }
         }
       }
     }
-    __syncthreads();
-    // commit the tile's sums: one set of atomics per splat per tile
-    if (t < cnt) {
-      float* gr = s_grad[t];
-      const float g0 = gr[0], g1 = gr[1], g2 = gr[2], g3 = gr[3], g4 = gr[4], g5 = gr[5], g6 = gr[6],
-                  g7 = gr[7], g8 = gr[8];
-      if (g0 != 0.f || g1 != 0.f || g2 != 0.f || g3 != 0.f || g4 != 0.f || g5 != 0.f || g6 != 0.f || g7 != 0.f ||
-          g8 != 0.f) {
-        float4* row = grads2d + 3 * size_t(s_id[t]);
-        atomicAdd(row + 0, make_float4(g0, g1, g2, 0.0f));
-        atomicAdd(row + 1, make_float4(g3, g4, g5, 0.0f));
-        atomicAdd(row + 2, make_float4(g6, g7, g8, 0.0f));
-#pragma unroll
-        for (int k = 0; k < kC; ++k) gr[k] = 0.0f;
-      }
-    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty_bar[s]);
   }
 }
 
@@ -223,8 +290,14 @@ extern "C" int gs_blend_backward(const float* d_image, const gs_splats_t* splats
   cudaError_t e = cudaMemsetAsync(grads2d, 0, size_t(splats->n) * GS_GRAD2D_FLOATS * sizeof(float), s);
   if (e != cudaSuccess) return record_cuda_error(e);
   if (splats->n == 0) return GS_OK;
+  static bool configured = false;
+  if (!configured) {
+    e = cudaFuncSetAttribute(blend_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmemBytes));
+    if (e != cudaSuccess) return record_cuda_error(e);
+    configured = true;
+  }
   const float3 bg = make_float3(background[0], background[1], background[2]);
-  blend_bwd_kernel<<<unsigned(tiles), kTilePixels, 0, s>>>(
+  blend_bwd_kernel<<<unsigned(tiles), kThreads, kSmemBytes, s>>>(
       d_image, reinterpret_cast<const float4*>(splats->rec), sorted_ids, reinterpret_cast<const int2*>(ranges),
       t_final, last, width, height, tiles_x, bg, reinterpret_cast<float4*>(grads2d));
   return check_launch();

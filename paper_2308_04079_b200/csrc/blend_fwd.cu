@@ -1,89 +1,171 @@
 // K6 blend_fwd — replaces splatlab rasterizer.render_forward / _blend_tile
 // (rasterizer.py:152-240).
 //
-// One 256-thread CTA per 16x16 tile, one pixel per thread, each warp an 8x4
-// pixel block.  The tile's sorted instance list is walked front to back in
-// batches of 256: every thread gathers one splat record (48 of its 64 B)
-// into shared memory and computes the splat's 8-bit warp coverage mask
-// (warp_cover_mask).  Each warp then visits, in order, only the splats whose
-// mask bit is set (a ballot over 32 mask bits at a time), so splats that
-// cannot reach alpha >= 1/255 anywhere in its block cost no pixel work.
+// One CTA per 16x16 tile: 8 consumer warps (one pixel per thread, each warp
+// an 8x4 pixel block) + 1 producer warp, warp-specialised over a ring of
+// kStages shared-memory batch buffers guarded by mbarriers:
+//   producer: for each 256-entry batch of the tile's sorted instance list,
+//     loads the Gaussian ids, gathers the 48-byte splat records with
+//     cp.async, computes each splat's 8-bit warp coverage mask
+//     (warp_cover_mask) and arrives on full[stage];
+//   consumers: wait on full[stage], visit (front to back, by ballot over the
+//     mask bits) only the splats that can reach alpha >= 1/255 in their
+//     block, then arrive on empty[stage].
+// Warps therefore drift apart by up to kStages-1 batches instead of meeting
+// at a CTA barrier after every batch (the v1 kernel's dominant stall).
 // A pixel stops before its accumulated opacity would exceed 0.9999
-// (rasterizer.py:179-180); the CTA leaves the list as soon as
-// __syncthreads_count says every pixel is done (rasterizer.py:194-195).
+// (rasterizer.py:179-180); once every consumer warp is done the CTA stops
+// (rasterizer.py:194-195): the last warp to finish raises s_stop, which the
+// producer and any waiting consumer poll.
 #include "gs_common.cuh"
 
 namespace gs {
 namespace {
 
+constexpr int kBatch = 256;
+constexpr int kStages = 4;
+constexpr int kConsumerWarps = 8;
+constexpr int kThreads = (kConsumerWarps + 1) * 32;
+
+struct FwdStage {
+  float4 r0[kBatch];
+  float4 r1[kBatch];
+  float4 col[kBatch];
+  uint32_t id[kBatch];
+  uint8_t mask[kBatch];
+};
+constexpr size_t kSmemBytes = sizeof(FwdStage) * kStages;
+
+__device__ __forceinline__ void produce_batch(FwdStage& st, const float4* __restrict__ rec,
+                                              const uint32_t* __restrict__ ids, int base, int cnt, int lane,
+                                              float tile_x0, float tile_y0) {
+  uint32_t gid[kBatch / 32];
+#pragma unroll
+  for (int u = 0; u < kBatch / 32; ++u) {
+    const int e = lane + 32 * u;
+    gid[u] = e < cnt ? __ldg(ids + base + e) : 0u;
+  }
+#pragma unroll
+  for (int u = 0; u < kBatch / 32; ++u) {
+    const int e = lane + 32 * u;
+    if (e < cnt) {
+      const float4* src = rec + 4 * size_t(gid[u]);
+      st.id[e] = gid[u];
+      cp_async16(&st.r0[e], src + 0);
+      cp_async16(&st.r1[e], src + 1);
+      cp_async16(&st.col[e], src + 2);
+    }
+  }
+  cp_async_wait_all();
+#pragma unroll
+  for (int u = 0; u < kBatch / 32; ++u) {
+    const int e = lane + 32 * u;
+    if (e < cnt) st.mask[e] = uint8_t(warp_cover_mask(st.r0[e], st.r1[e], tile_x0, tile_y0));
+  }
+}
+
 template <bool kTraining>
-__global__ void __launch_bounds__(kTilePixels)
+__global__ void __launch_bounds__(kThreads)
 blend_fwd_kernel(const float4* __restrict__ rec, const uint32_t* __restrict__ ids, const int2* __restrict__ ranges,
                  int width, int height, int tiles_x, float3 bg, float* __restrict__ image,
                  float* __restrict__ t_final, int32_t* __restrict__ last) {
-  __shared__ float4 s_r0[kTilePixels];
-  __shared__ float4 s_r1[kTilePixels];
-  __shared__ float4 s_col[kTilePixels];
-  __shared__ uint32_t s_id[kTilePixels];
-  __shared__ uint8_t s_mask[kTilePixels];
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  FwdStage* stages = reinterpret_cast<FwdStage*>(smem_raw);
+  __shared__ uint64_t full_bar[kStages], empty_bar[kStages];
+  __shared__ int s_done, s_stop;
 
   const int tile = blockIdx.x;
   const int t = threadIdx.x;
   const int lane = t & 31, warp = t >> 5;
   const int tx = tile % tiles_x, ty = tile / tiles_x;
+  const float tile_x0 = float(tx * kTile), tile_y0 = float(ty * kTile);
+  const int2 range = ranges[tile];
+  const int nb = (range.y - range.x + kBatch - 1) / kBatch;
+
+  if (t == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full_bar[s], 32);
+      mbar_init(&empty_bar[s], kConsumerWarps);
+    }
+    s_done = 0;
+    s_stop = 0;
+  }
+  __syncthreads();
+
+  if (warp == kConsumerWarps) {  // ---------------- producer warp
+    for (int b = 0; b < nb; ++b) {
+      const int s = b % kStages;
+      if (b >= kStages) {
+        while (!mbar_try_wait(&empty_bar[s], uint32_t((b / kStages) - 1) & 1u))
+          if (ld_volatile(&s_stop)) return;
+      }
+      if (ld_volatile(&s_stop)) return;
+      const int base = range.x + b * kBatch;
+      produce_batch(stages[s], rec, ids, base, min(kBatch, range.y - base), lane, tile_x0, tile_y0);
+      mbar_arrive(&full_bar[s]);
+    }
+    return;
+  }
+
+  // ---------------- consumer warps
   const int px = tx * kTile + tile_px(t);
   const int py = ty * kTile + tile_py(t);
   const bool inside = (px < width) && (py < height);
   const float fx = float(px) + 0.5f, fy = float(py) + 0.5f;  // rasterizer.py:142
-  const float tile_x0 = float(tx * kTile), tile_y0 = float(ty * kTile);
-
-  const int2 range = ranges[tile];
   float T = 1.0f;
   float cr = 0.0f, cg = 0.0f, cb = 0.0f;
   int32_t last_idx = -1;
   bool done = !inside;
+  bool warp_done = __all_sync(0xffffffffu, done);
+  if (warp_done && lane == 0 && atomicAdd(&s_done, 1) == kConsumerWarps - 1) s_stop = 1;
 
-  for (int base = range.x; base < range.y; base += kTilePixels) {
-    if (__syncthreads_count(done) == kTilePixels) break;
-    const int i = base + t;
-    if (i < range.y) {
-      const uint32_t g = ids[i];
-      const float4 r0 = rec[4 * size_t(g) + 0];
-      const float4 r1 = rec[4 * size_t(g) + 1];
-      s_id[t] = g;
-      s_r0[t] = r0;
-      s_r1[t] = r1;
-      s_col[t] = rec[4 * size_t(g) + 2];
-      s_mask[t] = uint8_t(warp_cover_mask(r0, r1, tile_x0, tile_y0));
-    }
-    __syncthreads();
-    if (__all_sync(0xffffffffu, done)) continue;
-    const int cnt = min(kTilePixels, range.y - base);
-    for (int c0 = 0; c0 < cnt; c0 += 32) {
-      const int jl = c0 + lane;
-      unsigned live = __ballot_sync(0xffffffffu, jl < cnt && ((s_mask[jl] >> warp) & 1u));
-      while (live) {
-        const int j = c0 + __ffs(live) - 1;
-        live &= live - 1;
-        if (done) continue;
-        const AlphaEval e = eval_alpha(fx, fy, s_r0[j], s_r1[j], rec, s_id[j]);
-        if (e.a == 0.0f) continue;
-        const float t_new = T * (1.0f - e.a);
-        if (t_new < kTransSat) {  // 1 - T_new > 0.9999
-          done = true;
-          continue;
-        }
-        const float4 c = s_col[j];
-        const float w = T * e.a;
-        cr = fmaf(w, c.x, cr);
-        cg = fmaf(w, c.y, cg);
-        cb = fmaf(w, c.z, cb);
-        T = t_new;
-        if (kTraining) last_idx = base + j;
+  for (int b = 0; b < nb; ++b) {
+    const int s = b % kStages;
+    bool stop = false;
+    while (!mbar_try_wait(&full_bar[s], uint32_t(b / kStages) & 1u)) {
+      if (ld_volatile(&s_stop)) {
+        stop = true;
+        break;
       }
-      if (__all_sync(0xffffffffu, done)) break;
     }
+    if (__any_sync(0xffffffffu, stop)) break;
+    if (!warp_done) {
+      const FwdStage& st = stages[s];
+      const int base = range.x + b * kBatch;
+      const int cnt = min(kBatch, range.y - base);
+      for (int c0 = 0; c0 < cnt; c0 += 32) {
+        const int jl = c0 + lane;
+        unsigned live = __ballot_sync(0xffffffffu, jl < cnt && ((st.mask[jl] >> warp) & 1u));
+        while (live) {
+          const int j = c0 + __ffs(live) - 1;
+          live &= live - 1;
+          if (done) continue;
+          const AlphaEval e = eval_alpha(fx, fy, st.r0[j], st.r1[j], rec, st.id[j]);
+          if (e.a == 0.0f) continue;
+          const float t_new = T * (1.0f - e.a);
+          if (t_new < kTransSat) {  // 1 - T_new > 0.9999
+            done = true;
+            continue;
+          }
+          const float4 c = st.col[j];
+          const float w = T * e.a;
+          cr = fmaf(w, c.x, cr);
+          cg = fmaf(w, c.y, cg);
+          cb = fmaf(w, c.z, cb);
+          T = t_new;
+          if (kTraining) last_idx = base + j;
+        }
+        if (__all_sync(0xffffffffu, done)) break;
+      }
+      if (__all_sync(0xffffffffu, done)) {
+        warp_done = true;
+        if (lane == 0 && atomicAdd(&s_done, 1) == kConsumerWarps - 1) s_stop = 1;
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty_bar[s]);
   }
+
   if (!inside) return;
   const size_t p = size_t(py) * width + px;
   image[3 * p + 0] = fmaf(T, bg.x, cr);  // rasterizer.py:197
@@ -93,6 +175,21 @@ blend_fwd_kernel(const float4* __restrict__ rec, const uint32_t* __restrict__ id
     t_final[p] = T;
     last[p] = last_idx;
   }
+}
+
+template <bool kTraining>
+int launch(const float4* rec, const uint32_t* ids, const int2* rg, int width, int height, int tiles_x, int64_t tiles,
+           float3 bg, float* image, float* t_final, int32_t* last, cudaStream_t s) {
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(blend_fwd_kernel<kTraining>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(kSmemBytes));
+    if (e != cudaSuccess) return record_cuda_error(e);
+    configured = true;
+  }
+  blend_fwd_kernel<kTraining><<<unsigned(tiles), kThreads, kSmemBytes, s>>>(rec, ids, rg, width, height, tiles_x, bg,
+                                                                            image, t_final, last);
+  return check_launch();
 }
 
 }  // namespace
@@ -111,11 +208,6 @@ extern "C" int gs_blend_forward(const gs_splats_t* splats, const uint32_t* sorte
   const float3 bg = make_float3(background[0], background[1], background[2]);
   const float4* rec = reinterpret_cast<const float4*>(splats->rec);
   const int2* rg = reinterpret_cast<const int2*>(ranges);
-  if (training)
-    blend_fwd_kernel<true><<<unsigned(tiles), kTilePixels, 0, s>>>(rec, sorted_ids, rg, width, height, tiles_x, bg,
-                                                                  image, t_final, last);
-  else
-    blend_fwd_kernel<false><<<unsigned(tiles), kTilePixels, 0, s>>>(rec, sorted_ids, rg, width, height, tiles_x, bg,
-                                                                   image, nullptr, nullptr);
-  return check_launch();
+  if (training) return launch<true>(rec, sorted_ids, rg, width, height, tiles_x, tiles, bg, image, t_final, last, s);
+  return launch<false>(rec, sorted_ids, rg, width, height, tiles_x, tiles, bg, image, nullptr, nullptr, s);
 }

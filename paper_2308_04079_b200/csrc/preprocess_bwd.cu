@@ -18,23 +18,40 @@ namespace {
 // statistics; returns the SH basis b and the masked colour gradient dcol,
 // whose outer product is the (16,3) d_sh row (written by the caller through
 // shared memory).  shrow: the Gaussian's staged SH coefficients.
-__device__ __forceinline__ void grad_one(const gs_params_t& p, const DevCamera& cam, int degree,
-                                         const float4* __restrict__ rec, const float4* __restrict__ g2d,
+// Per-Gaussian inputs, loaded before the block's SH staging so their
+// latency overlaps it.
+struct GradInputs {
+  float4 ga, gb, gc;   // grads2d row: (d_mx, d_my, d_alpha), (d_ca, d_cb, d_cc), (d_r, d_g, d_b)
+  float4 q;            // raw quaternion
+  float m0, m1, m2, l0, l1, l2, op, mask;
+};
+
+__device__ __forceinline__ void load_inputs(const gs_params_t& p, const float4* __restrict__ rec,
+                                            const float4* __restrict__ g2d, int64_t g, GradInputs& in) {
+  in.ga = __ldg(g2d + 3 * g + 0);
+  in.gb = __ldg(g2d + 3 * g + 1);
+  in.gc = __ldg(g2d + 3 * g + 2);
+  in.mask = __ldg(rec + 4 * g + 2).w;
+  in.q = __ldg(reinterpret_cast<const float4*>(p.rotations) + g);
+  in.m0 = __ldg(p.means + 3 * g + 0); in.m1 = __ldg(p.means + 3 * g + 1); in.m2 = __ldg(p.means + 3 * g + 2);
+  in.l0 = __ldg(p.log_scales + 3 * g + 0); in.l1 = __ldg(p.log_scales + 3 * g + 1);
+  in.l2 = __ldg(p.log_scales + 3 * g + 2);
+  in.op = __ldg(p.opacity_logits + g);
+}
+
+__device__ __forceinline__ void grad_one(const GradInputs& in, const DevCamera& cam, int degree,
                                          const gs_grads_t& out, int accumulate, const gs_stats_t& stats,
                                          int64_t g, int32_t radius, const float4* shrow, float (&b)[16],
                                          float (&dcol)[3]) {
-  const float4 ga = g2d[3 * g + 0];  // d_mean2d.x, d_mean2d.y, d_alpha
-  const float4 gb = g2d[3 * g + 1];  // d_conic a, b, c
-  const float4 gc = g2d[3 * g + 2];  // d_color r, g, b
-  const float4 r2 = rec[4 * g + 2];
-  const int mask = int(r2.w);
+  const float4 ga = in.ga, gb = in.gb, gc = in.gc;
+  const int mask = int(in.mask);
 
   // --- opacity through the sigmoid (gradients.py:217)
-  const double alpha = 1.0 / (1.0 + exp(-double(p.opacity_logits[g])));
+  const double alpha = 1.0 / (1.0 + exp(-double(in.op)));
   const float d_logit = float(double(ga.z) * alpha * (1.0 - alpha));
 
   // --- view position, Jacobian, U = J W (core.py:279, 298-303)
-  const double mx = p.means[3 * g + 0], my = p.means[3 * g + 1], mz = p.means[3 * g + 2];
+  const double mx = in.m0, my = in.m1, mz = in.m2;
   double view[3];
 #pragma unroll
   for (int i = 0; i < 3; ++i)
@@ -50,13 +67,12 @@ __device__ __forceinline__ void grad_one(const gs_params_t& p, const DevCamera& 
   }
 
   // --- covariance from the raw quaternion and log scales (core.py:187-201)
-  const float4 qf = reinterpret_cast<const float4*>(p.rotations)[g];
+  const float4 qf = in.q;
   const double qn = sqrt(double(qf.x) * qf.x + double(qf.y) * qf.y + double(qf.z) * qf.z + double(qf.w) * qf.w);
   const double q[4] = {qf.x / qn, qf.y / qn, qf.z / qn, qf.w / qn};
   double R[9];
   quat_to_rot(q[0], q[1], q[2], q[3], R);
-  const double s[3] = {exp(double(p.log_scales[3 * g + 0])), exp(double(p.log_scales[3 * g + 1])),
-                       exp(double(p.log_scales[3 * g + 2]))};
+  const double s[3] = {exp(double(in.l0)), exp(double(in.l1)), exp(double(in.l2))};
   double M[9], S[9];
 #pragma unroll
   for (int i = 0; i < 3; ++i)
@@ -212,16 +228,18 @@ preprocess_bwd_kernel(gs_params_t p, DevCamera cam, int degree, const float4* __
                       int accumulate, gs_stats_t stats) {
   __shared__ float4 s_sh[128 * kShStride];
   const int64_t g0 = int64_t(blockIdx.x) * blockDim.x;
-  stage_sh_rows(p.sh, p.n, g0, s_sh);
-  __syncthreads();
   const int64_t g = g0 + threadIdx.x;
   const bool valid = g < p.n;
   const int32_t radius = valid ? radii[g] : 0;
+  GradInputs in;
+  if (valid) load_inputs(p, rec, g2d, g, in);
+  stage_sh_rows(p.sh, p.n, g0, s_sh);
+  __syncthreads();
   float b[16], dcol[3] = {0.0f, 0.0f, 0.0f};
 #pragma unroll
   for (int k = 0; k < 16; ++k) b[k] = 0.0f;
   if (radius > 0) {
-    grad_one(p, cam, degree, rec, g2d, out, accumulate, stats, g, radius, s_sh + threadIdx.x * kShStride, b, dcol);
+    grad_one(in, cam, degree, out, accumulate, stats, g, radius, s_sh + threadIdx.x * kShStride, b, dcol);
   } else if (valid && !accumulate) {  // culled: exactly zero gradient (gradients.py:13-27)
     for (int k = 0; k < 3; ++k) out.d_means[3 * g + k] = 0.0f;
     for (int k = 0; k < 3; ++k) out.d_log_scales[3 * g + k] = 0.0f;

@@ -18,13 +18,24 @@ __global__ void __launch_bounds__(128)
 preprocess_fwd_kernel(gs_params_t p, DevCamera cam, int degree, gs_splats_t out) {
   __shared__ float4 s_sh[128 * kShStride];
   const int64_t g0 = int64_t(blockIdx.x) * blockDim.x;
+  const int64_t g = g0 + threadIdx.x;
+  // this thread's parameter loads are issued first so their latency overlaps
+  // the block's SH staging
+  float pm0 = 0.f, pm1 = 0.f, pm2 = 0.f, pl0 = 0.f, pl1 = 0.f, pl2 = 0.f, pop = 0.f;
+  float4 qf = make_float4(1.f, 0.f, 0.f, 0.f);
+  if (g < p.n) {
+    pm0 = __ldg(p.means + 3 * g + 0); pm1 = __ldg(p.means + 3 * g + 1); pm2 = __ldg(p.means + 3 * g + 2);
+    qf = __ldg(reinterpret_cast<const float4*>(p.rotations) + g);
+    pl0 = __ldg(p.log_scales + 3 * g + 0); pl1 = __ldg(p.log_scales + 3 * g + 1);
+    pl2 = __ldg(p.log_scales + 3 * g + 2);
+    pop = __ldg(p.opacity_logits + g);
+  }
   stage_sh_rows(p.sh, p.n, g0, s_sh);
   __syncthreads();
-  const int64_t g = g0 + threadIdx.x;
   if (g >= p.n) return;
 
   // view = means @ W^T + t (core.py:279)
-  const double mx = p.means[3 * g + 0], my = p.means[3 * g + 1], mz = p.means[3 * g + 2];
+  const double mx = pm0, my = pm1, mz = pm2;
   double view[3];
 #pragma unroll
   for (int i = 0; i < 3; ++i)
@@ -52,7 +63,7 @@ preprocess_fwd_kernel(gs_params_t p, DevCamera cam, int degree, gs_splats_t out)
   }
 
   // world covariance Sigma = M M^T, M = R(q/|q|) diag(exp(s)) (core.py:187-201)
-  const float4 qf = reinterpret_cast<const float4*>(p.rotations)[g];
+
   double qr = qf.x, qi = qf.y, qj = qf.z, qk = qf.w;
   const double qn = sqrt(dadd(dadd(dadd(dmul(qr, qr), dmul(qi, qi)), dmul(qj, qj)), dmul(qk, qk)));
   if (qn == 0.0) {  // InvalidPrimitiveError (core.py:164-165)
@@ -64,9 +75,9 @@ preprocess_fwd_kernel(gs_params_t p, DevCamera cam, int degree, gs_splats_t out)
   qr = __ddiv_rn(qr, qn); qi = __ddiv_rn(qi, qn); qj = __ddiv_rn(qj, qn); qk = __ddiv_rn(qk, qn);
   double R[9];
   quat_to_rot(qr, qi, qj, qk, R);
-  const double s0 = exp(double(p.log_scales[3 * g + 0]));
-  const double s1 = exp(double(p.log_scales[3 * g + 1]));
-  const double s2 = exp(double(p.log_scales[3 * g + 2]));
+  const double s0 = exp(double(pl0));
+  const double s1 = exp(double(pl1));
+  const double s2 = exp(double(pl2));
   double M[9];
 #pragma unroll
   for (int i = 0; i < 3; ++i) {
@@ -165,7 +176,7 @@ preprocess_fwd_kernel(gs_params_t p, DevCamera cam, int degree, gs_splats_t out)
     col[c] = fmaxf(col[c], 0.0f);
   }
   // sigmoid opacity (core.py:327)
-  const double alpha = 1.0 / (1.0 + exp(-double(p.opacity_logits[g])));
+  const double alpha = 1.0 / (1.0 + exp(-double(pop)));
 
   const float ux_hi = float(u), uy_hi = float(v);
   const float ux_lo = float(dsub(u, double(ux_hi))), uy_lo = float(dsub(v, double(uy_hi)));
