@@ -192,6 +192,20 @@ int gs_preprocess_backward(const gs_params_t* params, const gs_camera_t* camera,
                            const float* grads2d, const gs_grads_t* grads, int32_t accumulate,
                            const gs_stats_t* stats, void* stream);
 
+/* ---- K8+K9 fused: backward_project + densify statistics + dense Adam in one
+ * pass (gradients.py:192-259, optimizer.py:252-257 and 263-293 back to back,
+ * as train_step runs them).  The parameters in *params are UPDATED IN PLACE.
+ * groups[5] in PARAM_GROUPS order (means, log_scales, rotations,
+ * opacity_logits, sh; optimizer.py:85): exp_avg / exp_avg_sq / lr are used
+ * (groups[4].lr_head = SH DC learning rate); param / grad fields are ignored.
+ * grads_out (nullable, any member nullable) additionally receives the
+ * gradients.  Bit-identical to gs_preprocess_backward + gs_adam_step. */
+int gs_preprocess_backward_adam(const gs_params_t* params, const gs_camera_t* camera,
+                                int32_t active_sh_degree, const gs_splats_t* splats, const float* grads2d,
+                                const gs_adam_group_t* groups, double beta1, double beta2, double eps,
+                                double bias1, double bias2, const gs_stats_t* stats,
+                                const gs_grads_t* grads_out, void* stream);
+
 /* ---- K9 fused Adam: replaces optimizer._adam_step (optimizer.py:263-293)
  * over all groups in one launch; bias1 = 1-beta1^t, bias2 = 1-beta2^t. */
 int gs_adam_step(const gs_adam_group_t* groups, int32_t num_groups, double beta1, double beta2,

@@ -80,6 +80,9 @@ SIGNATURES = [
                                     c_int32, POINTER(c_float), c_void_p, c_void_p]),
     ("gs_preprocess_backward", c_int32, [POINTER(GsParams), POINTER(GsCamera), c_int32, POINTER(GsSplats),
                                          c_void_p, POINTER(GsGrads), c_int32, POINTER(GsStats), c_void_p]),
+    ("gs_preprocess_backward_adam", c_int32, [POINTER(GsParams), POINTER(GsCamera), c_int32, POINTER(GsSplats),
+                                              c_void_p, POINTER(GsAdamGroup), c_double, c_double, c_double,
+                                              c_double, c_double, POINTER(GsStats), POINTER(GsGrads), c_void_p]),
     ("gs_loss_workspace_size", c_int32, [c_int32, c_int32, POINTER(c_size_t)]),
     ("gs_l1_dssim_loss", c_int32, [c_void_p, c_void_p, c_int32, c_int32, c_double, c_void_p, c_size_t, c_void_p,
                                    c_void_p, c_void_p]),

@@ -20,11 +20,8 @@ struct AdamArgs {
 };
 
 __device__ __forceinline__ void adam_elem(float& p, float gr, float& m, float& v, float lr, const AdamArgs& a) {
-  // m = b1 m + (1-b1) g ; v = b2 v + (1-b2) g^2 ; p -= lr (m/bias1) / (sqrt(v/bias2) + eps)
-  m = a.beta1 * m + a.one_m_beta1 * gr;
-  v = a.beta2 * v + a.one_m_beta2 * gr * gr;
-  const float denom = sqrtf(v * a.inv_bias2) + a.eps;
-  p -= lr * (m * a.inv_bias1) / denom;
+  adam_update(p, gr, m, v, lr, AdamCoef{a.beta1, a.beta2, a.one_m_beta1, a.one_m_beta2, a.eps, a.inv_bias1,
+                                        a.inv_bias2});
 }
 
 __global__ void __launch_bounds__(256) adam_kernel(AdamArgs a) {

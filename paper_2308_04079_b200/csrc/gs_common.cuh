@@ -200,6 +200,22 @@ __device__ __forceinline__ uint32_t warp_cover_mask(float4 r0, float4 r1, float 
 }
 
 // ---------------------------------------------------------------------------
+// Adam update of one element (optimizer.py:288-293), shared by the standalone
+// Adam kernel and the fused backward+Adam kernel; explicit _rn intrinsics so
+// both produce bit-identical parameters and moments.
+//   m = b1 m + (1-b1) g ; v = b2 v + (1-b2) g^2 ; p -= lr (m/bias1) / (sqrt(v/bias2) + eps)
+struct AdamCoef {
+  float beta1, beta2, one_m_beta1, one_m_beta2, eps, inv_bias1, inv_bias2;
+};
+
+__device__ __forceinline__ void adam_update(float& p, float g, float& m, float& v, float lr, const AdamCoef& c) {
+  m = __fadd_rn(__fmul_rn(c.beta1, m), __fmul_rn(c.one_m_beta1, g));
+  v = __fadd_rn(__fmul_rn(c.beta2, v), __fmul_rn(__fmul_rn(c.one_m_beta2, g), g));
+  const float denom = __fadd_rn(__fsqrt_rn(__fmul_rn(v, c.inv_bias2)), c.eps);
+  p = __fsub_rn(p, __fdiv_rn(__fmul_rn(lr, __fmul_rn(m, c.inv_bias1)), denom));
+}
+
+// ---------------------------------------------------------------------------
 // mbarrier / cp.async helpers (sm_90+ PTX) for the pipelined blend kernels.
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));

@@ -39,10 +39,25 @@ __device__ __forceinline__ void load_inputs(const gs_params_t& p, const float4* 
   in.op = __ldg(p.opacity_logits + g);
 }
 
+// Non-SH gradients of one Gaussian (the SH row is b (x) dcol).
+struct GradOut {
+  float dmean[3];
+  float dlogs[3];
+  float4 drot;
+  float dlogit;
+  float norm;   // view_pos_grad_norm = |d_mean2d| (gradients.py:258)
+};
+
+__device__ __forceinline__ void zero_grads(GradOut& o) {
+  o.dmean[0] = o.dmean[1] = o.dmean[2] = 0.0f;
+  o.dlogs[0] = o.dlogs[1] = o.dlogs[2] = 0.0f;
+  o.drot = make_float4(0.f, 0.f, 0.f, 0.f);
+  o.dlogit = 0.0f;
+  o.norm = 0.0f;
+}
+
 __device__ __forceinline__ void grad_one(const GradInputs& in, const DevCamera& cam, int degree,
-                                         const gs_grads_t& out, int accumulate, const gs_stats_t& stats,
-                                         int64_t g, int32_t radius, const float4* shrow, float (&b)[16],
-                                         float (&dcol)[3]) {
+                                         const float4* shrow, GradOut& o, float (&b)[16], float (&dcol)[3]) {
   const float4 ga = in.ga, gb = in.gb, gc = in.gc;
   const int mask = int(in.mask);
 
@@ -197,29 +212,49 @@ __device__ __forceinline__ void grad_one(const GradInputs& in, const DevCamera& 
 #pragma unroll
   for (int j = 0; j < 3; ++j)
     dmean[j] = float(dt[0] * cam.R[j] + dt[1] * cam.R[3 + j] + dt[2] * cam.R[6 + j]) + dms[j];
-  const float norm = sqrtf(ga.x * ga.x + ga.y * ga.y);  // gradients.py:258
-
-  if (accumulate) {
-    for (int k = 0; k < 3; ++k) out.d_means[3 * g + k] += dmean[k];
-    for (int k = 0; k < 3; ++k) out.d_log_scales[3 * g + k] += float(d_logs[k]);
-    float4 r = reinterpret_cast<float4*>(out.d_rotations)[g];
-    r.x += d_rot.x; r.y += d_rot.y; r.z += d_rot.z; r.w += d_rot.w;
-    reinterpret_cast<float4*>(out.d_rotations)[g] = r;
-    out.d_opacity_logits[g] += d_logit;
-  } else {
-    for (int k = 0; k < 3; ++k) out.d_means[3 * g + k] = dmean[k];
-    for (int k = 0; k < 3; ++k) out.d_log_scales[3 * g + k] = float(d_logs[k]);
-    reinterpret_cast<float4*>(out.d_rotations)[g] = d_rot;
-    out.d_opacity_logits[g] = d_logit;
+  o.norm = sqrtf(ga.x * ga.x + ga.y * ga.y);  // gradients.py:258
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    o.dmean[k] = dmean[k];
+    o.dlogs[k] = float(d_logs[k]);
   }
-  if (out.view_pos_grad_norm) out.view_pos_grad_norm[g] = norm;
-  // densification statistics over every survivor (optimizer.py:252-255)
+  o.drot = d_rot;
+  o.dlogit = d_logit;
+}
+
+__device__ __forceinline__ void store_grads(const gs_grads_t& out, int64_t g, const GradOut& o, bool accumulate) {
+  if (accumulate) {
+    for (int k = 0; k < 3; ++k) out.d_means[3 * g + k] += o.dmean[k];
+    for (int k = 0; k < 3; ++k) out.d_log_scales[3 * g + k] += o.dlogs[k];
+    float4 r = reinterpret_cast<float4*>(out.d_rotations)[g];
+    r.x += o.drot.x; r.y += o.drot.y; r.z += o.drot.z; r.w += o.drot.w;
+    reinterpret_cast<float4*>(out.d_rotations)[g] = r;
+    out.d_opacity_logits[g] += o.dlogit;
+  } else {
+    for (int k = 0; k < 3; ++k) out.d_means[3 * g + k] = o.dmean[k];
+    for (int k = 0; k < 3; ++k) out.d_log_scales[3 * g + k] = o.dlogs[k];
+    reinterpret_cast<float4*>(out.d_rotations)[g] = o.drot;
+    out.d_opacity_logits[g] = o.dlogit;
+  }
+  if (out.view_pos_grad_norm) out.view_pos_grad_norm[g] = o.norm;
+}
+
+// densification statistics over every survivor (optimizer.py:252-255)
+__device__ __forceinline__ void update_stats(const gs_stats_t& stats, int64_t g, float norm, int32_t radius,
+                                             int height) {
   if (stats.accum_pos_grad) stats.accum_pos_grad[g] += norm;
   if (stats.accum_count) stats.accum_count[g] += 1;
   if (stats.max_radius_frac) {
-    const float frac = float(double(radius) / double(cam.height));
+    const float frac = float(double(radius) / double(height));
     stats.max_radius_frac[g] = fmaxf(stats.max_radius_frac[g], frac);
   }
+}
+
+// d_sh row (gradients.py:221) as float4 k of the (16,3) row: basis (x) dcol
+__device__ __forceinline__ float4 dsh_quad(const float (&b)[16], const float (&dcol)[3], int k) {
+  const int e0 = 4 * k;
+  return make_float4(b[(e0 + 0) / 3] * dcol[(e0 + 0) % 3], b[(e0 + 1) / 3] * dcol[(e0 + 1) % 3],
+                     b[(e0 + 2) / 3] * dcol[(e0 + 2) % 3], b[(e0 + 3) / 3] * dcol[(e0 + 3) % 3]);
 }
 
 __global__ void __launch_bounds__(128, 4)
@@ -238,14 +273,14 @@ preprocess_bwd_kernel(gs_params_t p, DevCamera cam, int degree, const float4* __
   float b[16], dcol[3] = {0.0f, 0.0f, 0.0f};
 #pragma unroll
   for (int k = 0; k < 16; ++k) b[k] = 0.0f;
+  GradOut o;
   if (radius > 0) {
-    grad_one(in, cam, degree, out, accumulate, stats, g, radius, s_sh + threadIdx.x * kShStride, b, dcol);
+    grad_one(in, cam, degree, s_sh + threadIdx.x * kShStride, o, b, dcol);
+    store_grads(out, g, o, accumulate);
+    update_stats(stats, g, o.norm, radius, cam.height);
   } else if (valid && !accumulate) {  // culled: exactly zero gradient (gradients.py:13-27)
-    for (int k = 0; k < 3; ++k) out.d_means[3 * g + k] = 0.0f;
-    for (int k = 0; k < 3; ++k) out.d_log_scales[3 * g + k] = 0.0f;
-    reinterpret_cast<float4*>(out.d_rotations)[g] = make_float4(0.f, 0.f, 0.f, 0.f);
-    out.d_opacity_logits[g] = 0.0f;
-    if (out.view_pos_grad_norm) out.view_pos_grad_norm[g] = 0.0f;
+    zero_grads(o);
+    store_grads(out, g, o, false);
   }
   // d_sh = basis (x) masked d_color (gradients.py:221), written through shared
   // memory so the (N,16,3) stores are coalesced
@@ -258,9 +293,7 @@ preprocess_bwd_kernel(gs_params_t p, DevCamera cam, int degree, const float4* __
     float4* row = s_sh + threadIdx.x * kShStride;
 #pragma unroll
     for (int k = 0; k < 12; ++k) {
-      const int e0 = 4 * k;
-      float4 v = make_float4(b[(e0 + 0) / 3] * dcol[(e0 + 0) % 3], b[(e0 + 1) / 3] * dcol[(e0 + 1) % 3],
-                             b[(e0 + 2) / 3] * dcol[(e0 + 2) % 3], b[(e0 + 3) / 3] * dcol[(e0 + 3) % 3]);
+      float4 v = dsh_quad(b, dcol, k);
       if (accumulate) {
         const float4 o = row[k];
         v.x += o.x; v.y += o.y; v.z += o.z; v.w += o.w;
@@ -272,8 +305,156 @@ preprocess_bwd_kernel(gs_params_t p, DevCamera cam, int degree, const float4* __
   store_sh_rows(s_sh, p.n, g0, out.d_sh);
 }
 
+// ---------------------------------------------------------------------------
+// Fused backward preprocess + densify statistics + dense Adam: the same
+// per-Gaussian gradient as preprocess_bwd_kernel, consumed in registers /
+// shared memory by the Adam update (optimizer.py:263-293) instead of being
+// written to HBM and re-read by a second kernel (saves 472 B per Gaussian).
+// Bit-identical to preprocess_bwd_kernel followed by adam_kernel.
+struct FusedAdam {
+  float* m[5];   // exp_avg:    means, log_scales, rotations, opacity_logits, sh
+  float* v[5];   // exp_avg_sq: same order (optimizer.py:85 PARAM_GROUPS)
+  float lr[5];
+  float lr_sh_dc;
+  AdamCoef c;
+};
+
+__global__ void __launch_bounds__(128, 4)
+preprocess_bwd_adam_kernel(gs_params_t p, DevCamera cam, int degree, const float4* __restrict__ rec,
+                           const int32_t* __restrict__ radii, const float4* __restrict__ g2d, gs_grads_t out,
+                           gs_stats_t stats, FusedAdam A) {
+  extern __shared__ __align__(16) float4 smem4[];
+  float4* s_sh = smem4;                      // staged SH coefficients (the SH parameters)
+  float4* s_dsh = smem4 + 128 * kShStride;   // d_sh rows
+  const int64_t g0 = int64_t(blockIdx.x) * blockDim.x;
+  const int64_t g = g0 + threadIdx.x;
+  const bool valid = g < p.n;
+  const int32_t radius = valid ? radii[g] : 0;
+  GradInputs in;
+  if (valid) load_inputs(p, rec, g2d, g, in);
+  stage_sh_rows(p.sh, p.n, g0, s_sh);
+  __syncthreads();
+  float b[16], dcol[3] = {0.0f, 0.0f, 0.0f};
+#pragma unroll
+  for (int k = 0; k < 16; ++k) b[k] = 0.0f;
+  GradOut o;
+  zero_grads(o);
+  if (radius > 0) {
+    grad_one(in, cam, degree, s_sh + threadIdx.x * kShStride, o, b, dcol);
+    update_stats(stats, g, o.norm, radius, cam.height);
+  }
+  if (valid) {
+    if (out.d_means) store_grads(out, g, o, false);
+    // dense Adam on the 11 non-SH parameters of this Gaussian
+    float* means = const_cast<float*>(p.means);
+    float* logs = const_cast<float*>(p.log_scales);
+    float pm[3] = {in.m0, in.m1, in.m2}, pl[3] = {in.l0, in.l1, in.l2};
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      float m = A.m[0][3 * g + k], v = A.v[0][3 * g + k];
+      adam_update(pm[k], o.dmean[k], m, v, A.lr[0], A.c);
+      means[3 * g + k] = pm[k];
+      A.m[0][3 * g + k] = m;
+      A.v[0][3 * g + k] = v;
+    }
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      float m = A.m[1][3 * g + k], v = A.v[1][3 * g + k];
+      adam_update(pl[k], o.dlogs[k], m, v, A.lr[1], A.c);
+      logs[3 * g + k] = pl[k];
+      A.m[1][3 * g + k] = m;
+      A.v[1][3 * g + k] = v;
+    }
+    {
+      float4 q = in.q, m = reinterpret_cast<float4*>(A.m[2])[g], v = reinterpret_cast<float4*>(A.v[2])[g];
+      adam_update(q.x, o.drot.x, m.x, v.x, A.lr[2], A.c);
+      adam_update(q.y, o.drot.y, m.y, v.y, A.lr[2], A.c);
+      adam_update(q.z, o.drot.z, m.z, v.z, A.lr[2], A.c);
+      adam_update(q.w, o.drot.w, m.w, v.w, A.lr[2], A.c);
+      reinterpret_cast<float4*>(const_cast<float*>(p.rotations))[g] = q;
+      reinterpret_cast<float4*>(A.m[2])[g] = m;
+      reinterpret_cast<float4*>(A.v[2])[g] = v;
+    }
+    {
+      float op = in.op, m = A.m[3][g], v = A.v[3][g];
+      adam_update(op, o.dlogit, m, v, A.lr[3], A.c);
+      const_cast<float*>(p.opacity_logits)[g] = op;
+      A.m[3][g] = m;
+      A.v[3][g] = v;
+    }
+    float4* row = s_dsh + threadIdx.x * kShStride;
+#pragma unroll
+    for (int k = 0; k < 12; ++k) row[k] = dsh_quad(b, dcol, k);
+  }
+  __syncthreads();
+  if (out.d_sh) store_sh_rows(s_dsh, p.n, g0, out.d_sh);
+  // dense Adam on the SH rows: coalesced float4 sweep over the block's span;
+  // element 0..2 of each 48-float row (the DC band) uses lr_sh_dc
+  const int64_t left = p.n - g0;
+  const int nb = left < int64_t(blockDim.x) ? int(left) : int(blockDim.x);
+  float4* shp = reinterpret_cast<float4*>(const_cast<float*>(p.sh)) + g0 * 12;
+  float4* m4 = reinterpret_cast<float4*>(A.m[4]) + g0 * 12;
+  float4* v4 = reinterpret_cast<float4*>(A.v[4]) + g0 * 12;
+  for (int f = threadIdx.x; f < nb * 12; f += blockDim.x) {
+    const int j = f / 12, k = f - j * 12;
+    float4 pq = s_sh[j * kShStride + k];
+    const float4 gq = s_dsh[j * kShStride + k];
+    float4 mq = m4[f], vq = v4[f];
+    const float lr0 = (k == 0) ? A.lr_sh_dc : A.lr[4];
+    adam_update(pq.x, gq.x, mq.x, vq.x, lr0, A.c);
+    adam_update(pq.y, gq.y, mq.y, vq.y, lr0, A.c);
+    adam_update(pq.z, gq.z, mq.z, vq.z, lr0, A.c);
+    adam_update(pq.w, gq.w, mq.w, vq.w, A.lr[4], A.c);
+    shp[f] = pq;
+    m4[f] = mq;
+    v4[f] = vq;
+  }
+}
+
 }  // namespace
 }  // namespace gs
+
+extern "C" int gs_preprocess_backward_adam(const gs_params_t* params, const gs_camera_t* camera,
+                                           int32_t active_sh_degree, const gs_splats_t* splats,
+                                           const float* grads2d, const gs_adam_group_t* groups, double beta1,
+                                           double beta2, double eps, double bias1, double bias2,
+                                           const gs_stats_t* stats, const gs_grads_t* grads_out, void* stream) {
+  if (!params || !camera || !splats || !grads2d || !groups) return GS_ERR_INVALID_ARG;
+  if (active_sh_degree < 0 || active_sh_degree > 3) return GS_ERR_INVALID_ARG;
+  if (splats->n != params->n || !(bias1 > 0) || !(bias2 > 0)) return GS_ERR_INVALID_ARG;
+  if (params->n == 0) return GS_OK;
+  for (int i = 0; i < 5; ++i)
+    if (!groups[i].exp_avg || !groups[i].exp_avg_sq) return GS_ERR_INVALID_ARG;
+  gs::FusedAdam A;
+  for (int i = 0; i < 5; ++i) {
+    A.m[i] = groups[i].exp_avg;
+    A.v[i] = groups[i].exp_avg_sq;
+    A.lr[i] = groups[i].lr;
+  }
+  A.lr_sh_dc = groups[4].lr_head;
+  A.c = gs::AdamCoef{float(beta1), float(beta2), float(1.0 - beta1), float(1.0 - beta2), float(eps),
+                     float(1.0 / bias1), float(1.0 / bias2)};
+  gs_stats_t st = {nullptr, nullptr, nullptr};
+  if (stats) st = *stats;
+  gs_grads_t go = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+  if (grads_out) go = *grads_out;
+  const size_t smem = 2 * 128 * gs::kShStride * sizeof(float4);
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(gs::preprocess_bwd_adam_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(smem));
+    if (e != cudaSuccess) return gs::record_cuda_error(e);
+    configured = true;
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const gs::DevCamera cam = gs::make_dev_camera(*camera);
+  const unsigned grid = unsigned((params->n + 127) / 128);
+  gs::preprocess_bwd_adam_kernel<<<grid, 128, smem, s>>>(*params, cam, active_sh_degree,
+                                                         reinterpret_cast<const float4*>(splats->rec),
+                                                         splats->radii, reinterpret_cast<const float4*>(grads2d),
+                                                         go, st, A);
+  return gs::check_launch();
+}
 
 extern "C" int gs_preprocess_backward(const gs_params_t* params, const gs_camera_t* camera, int32_t active_sh_degree,
                                       const gs_splats_t* splats, const float* grads2d, const gs_grads_t* grads,

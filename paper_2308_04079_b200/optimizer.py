@@ -54,25 +54,19 @@ class DeviceAdam:
         self.exp_avg = {g: torch.zeros_like(getattr(cloud, g)) for g in PARAM_GROUPS}
         self.exp_avg_sq = {g: torch.zeros_like(getattr(cloud, g)) for g in PARAM_GROUPS}
 
-    def step(self, cloud: GaussianCloud, grads: GaussianGrads, iteration: int, config: TrainConfig) -> None:
-        """One dense Adam step at `iteration` (= the bias-correction t)."""
-        beta1, beta2 = config.adam_betas
-        t = int(iteration)
-        if t < 1:
-            raise ValueError("Adam iteration must be >= 1")
-        bias1 = 1.0 - beta1**t
-        bias2 = 1.0 - beta2**t
-        grad_of = {"means": grads.d_means, "log_scales": grads.d_log_scales, "rotations": grads.d_rotations,
-                   "opacity_logits": grads.d_opacity_logits, "sh": grads.d_sh}
+    def _groups(self, cloud: GaussianCloud, grads: GaussianGrads | None, t: int, config: TrainConfig):
+        grad_of = {} if grads is None else {
+            "means": grads.d_means, "log_scales": grads.d_log_scales, "rotations": grads.d_rotations,
+            "opacity_logits": grads.d_opacity_logits, "sh": grads.d_sh}
         lrs = {"means": config.lr_means_at(t), "log_scales": config.lr_log_scales,
                "rotations": config.lr_rotations, "opacity_logits": config.lr_opacity, "sh": config.lr_sh_rest}
         groups = (_lib.GsAdamGroup * len(PARAM_GROUPS))()
         for i, name in enumerate(PARAM_GROUPS):
-            p, g = getattr(cloud, name), grad_of[name]
-            if not (p.is_contiguous() and g.is_contiguous()):
+            p, g = getattr(cloud, name), grad_of.get(name)
+            if not p.is_contiguous() or (g is not None and not g.is_contiguous()):
                 raise ValueError(f"{name}: parameters and gradients must be contiguous")
             G = groups[i]
-            G.param, G.grad = p.data_ptr(), g.data_ptr()
+            G.param, G.grad = p.data_ptr(), (g.data_ptr() if g is not None else None)
             G.exp_avg, G.exp_avg_sq = self.exp_avg[name].data_ptr(), self.exp_avg_sq[name].data_ptr()
             G.numel = p.numel()
             G.lr = lrs[name]
@@ -80,9 +74,44 @@ class DeviceAdam:
                 G.lr_head, G.period, G.head = config.lr_sh_dc, 48, 3
             else:
                 G.lr_head, G.period, G.head = lrs[name], 0, 0
-        lib = _lib.load()
-        _lib.check(lib.gs_adam_step(groups, len(PARAM_GROUPS), beta1, beta2, config.adam_eps, bias1, bias2,
-                                    torch.cuda.current_stream().cuda_stream), "adam_step")
+        return groups
+
+    @staticmethod
+    def _bias(t: int, config: TrainConfig) -> tuple[float, float]:
+        if t < 1:
+            raise ValueError("Adam iteration must be >= 1")
+        beta1, beta2 = config.adam_betas
+        return 1.0 - beta1**t, 1.0 - beta2**t
+
+    def step(self, cloud: GaussianCloud, grads: GaussianGrads, iteration: int, config: TrainConfig) -> None:
+        """One dense Adam step at `iteration` (= the bias-correction t)."""
+        t = int(iteration)
+        bias1, bias2 = self._bias(t, config)
+        groups = self._groups(cloud, grads, t, config)
+        beta1, beta2 = config.adam_betas
+        _lib.check(_lib.load().gs_adam_step(groups, len(PARAM_GROUPS), beta1, beta2, config.adam_eps, bias1, bias2,
+                                            torch.cuda.current_stream().cuda_stream), "adam_step")
+
+    def backward_step(self, cloud: GaussianCloud, camera, splats, grads2d, active_sh_degree: int, iteration: int,
+                      config: TrainConfig, stats=None, grads_out: GaussianGrads | None = None) -> None:
+        """backward_project + densify statistics + Adam fused in one kernel
+        (gs_preprocess_backward_adam): parameters are updated in place, the
+        raw gradients never round-trip through HBM unless `grads_out` is given."""
+        from .rasterizer import _camera
+        if not 0 <= active_sh_degree <= 3:
+            raise ValueError(f"SH degree must be in 0..3, got {active_sh_degree}")
+        t = int(iteration)
+        bias1, bias2 = self._bias(t, config)
+        groups = self._groups(cloud, None, t, config)
+        beta1, beta2 = config.adam_betas
+        cs = splats.c_struct()
+        cst = stats.c_struct() if stats is not None else None
+        cg = grads_out.c_struct() if grads_out is not None else None
+        _lib.check(_lib.load().gs_preprocess_backward_adam(
+            ctypes.byref(cloud.c_params()), ctypes.byref(_camera(camera).to_c()), int(active_sh_degree),
+            ctypes.byref(cs), grads2d.packed.data_ptr(), groups, beta1, beta2, config.adam_eps, bias1, bias2,
+            ctypes.byref(cst) if cst is not None else None, ctypes.byref(cg) if cg is not None else None,
+            torch.cuda.current_stream().cuda_stream), "backward_adam")
 
 
 __all__ = ["TrainConfig", "DeviceAdam", "DensifyStats"]

@@ -21,7 +21,7 @@ import torch
 # our own __global__ kernels launched per training step (CUB's radix-sort and scan
 # kernels, compiled into the same library, are counted separately in DESIGN.md)
 KERNELS_PER_STEP = {"preprocess_fwd": 1, "bin_and_sort": 5, "blend_fwd": 1, "loss": 3, "blend_bwd": 1,
-                    "preprocess_bwd": 1, "adam": 1}
+                    "preprocess_bwd": 1, "adam": 1, "preprocess_bwd_adam": 1}
 
 
 class StageTimer:
@@ -79,6 +79,8 @@ class StageTimer:
             "blend_bwd": 40 * K + 20 * P + 36 * V,
             "preprocess_bwd": 276 * V + 240 * n + 20 * n,
             "adam": 1652 * n,
+            # fused K8+K9: the 236 B/Gaussian gradient write and re-read are gone
+            "preprocess_bwd_adam": 276 * V + 260 * n + 1652 * n - 472 * n,
             "loss": 132 * P,
         }
         hbm = float(peaks.get("hbm_gbs", 6650.0))

@@ -293,3 +293,37 @@ def test_backward_run_to_run_within_contract(cuda_device):
     b = device_pipeline(cloud_np, cam, 3, (0, 0, 0), d_image)[5]
     for key in ("d_means", "d_log_scales", "d_opacity_logits", "d_sh"):
         assert rel(getattr(a, key).cpu().numpy(), getattr(b, key).cpu().numpy()) < 1e-5
+
+
+def test_fused_backward_adam_bit_identical(cuda_device):
+    """gs_preprocess_backward_adam == gs_preprocess_backward + gs_adam_step, bit for bit."""
+    from paper_2308_04079_b200.optimizer import DeviceAdam, TrainConfig
+    g, cloud_np, cam = golden_scenes.load("scene_c")
+    degree, bg = int(g["degree"]), g["background"]
+    d_image = torch.from_numpy(golden_scenes.d_image_for(13, cam.width, cam.height).astype(np.float32)).cuda()
+    cfg = TrainConfig(total_iters=1000)
+    a = GaussianCloud.from_numpy(**cloud_np)
+    b = GaussianCloud.from_numpy(**cloud_np)
+    opt_a, opt_b = DeviceAdam(a), DeviceAdam(b)
+    st_a, st_b = R.DensifyStats.zeros(len(a), "cuda"), R.DensifyStats.zeros(len(b), "cuda")
+    for it in (1, 2, 3):
+        out, splats, binning = R.render_view(a, cam, bg, degree, training=True)
+        g2 = R.render_backward(d_image, out, splats, binning, cam.width, cam.height, bg)
+        grads = R.backward_project(a, cam, splats, g2, degree, stats=st_a)
+        opt_a.step(a, grads, it, cfg)
+        grads_b = R.GaussianGrads.zeros(len(b), "cuda")
+        opt_b.backward_step(b, cam, splats, g2, degree, it, cfg, stats=st_b, grads_out=grads_b)
+        torch.cuda.synchronize()
+        for key in ("d_means", "d_rotations", "d_log_scales", "d_opacity_logits", "d_sh"):
+            assert torch.equal(getattr(grads, key), getattr(grads_b, key)), key
+        for k in ("means", "log_scales", "rotations", "opacity_logits", "sh"):
+            assert torch.equal(getattr(a, k), getattr(b, k)), (it, k)
+            assert torch.equal(opt_a.exp_avg[k], opt_b.exp_avg[k]) and torch.equal(opt_a.exp_avg_sq[k],
+                                                                                   opt_b.exp_avg_sq[k])
+        b = GaussianCloud(*(getattr(a, k).clone() for k in ("means", "rotations", "log_scales", "opacity_logits",
+                                                            "sh")))
+        b.means.copy_(a.means)
+        opt_b.exp_avg = {k: v.clone() for k, v in opt_a.exp_avg.items()}
+        opt_b.exp_avg_sq = {k: v.clone() for k, v in opt_a.exp_avg_sq.items()}
+    assert torch.equal(st_a.accum_pos_grad, st_b.accum_pos_grad) and torch.equal(st_a.accum_count,
+                                                                                   st_b.accum_count)
