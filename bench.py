@@ -157,15 +157,16 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
             loss, d_image = l1_dssim_loss(out.image, gt, LAMBDA_DSSIM)
         with StageTimer.stage(tm, "blend_bwd"):
             g2 = R.render_backward(d_image, out, splats, binning, WIDTH, HEIGHT, bg)
-        if flat is None:
+        if flat is None and os.environ.get("GS_BENCH_UNFUSED") != "1":
             # single GPU: backward_project + stats + Adam fused (no gradient round trip)
             with StageTimer.stage(tm, "preprocess_bwd_adam"):
                 adam.backward_step(cloud, cam, splats, g2, DEGREE, iteration[0], config, stats=stats)
         else:
             with StageTimer.stage(tm, "preprocess_bwd"):
                 R._backward_project_tensors(params, n, dev, cam, splats, g2, DEGREE, stats, grads, False)
-            with StageTimer.stage(tm, "allreduce"):
-                dist.all_reduce(flat)
+            if flat is not None:
+                with StageTimer.stage(tm, "allreduce"):
+                    dist.all_reduce(flat)
             with StageTimer.stage(tm, "adam"):
                 adam.step(cloud, grads, iteration[0], config)
         if timed:

@@ -120,7 +120,8 @@ typedef struct gs_stats {
 } gs_stats_t;
 
 /* One Adam parameter group (optimizer.py:263-293).  Elements whose index e
- * satisfies (e % period) < head use lr_head instead of lr (the SH DC row:
+ * satisfies (e % period) < head use lr_head instead of lr (period a multiple
+ * of 4, head <= 4; the SH DC row:
  * period 48, head 3, optimizer.py:268-269).  period <= 0 disables it. */
 typedef struct gs_adam_group {
   float* param;

@@ -31,6 +31,9 @@ __global__ void __launch_bounds__(256) adam_kernel(AdamArgs a) {
   while (gi + 1 < a.num_groups && q >= a.quad_start[gi + 1]) ++gi;
   const gs_adam_group_t& G = a.g[gi];
   const int64_t e0 = (q - a.quad_start[gi]) * 4;
+  // period % 4 == 0 (checked on the host): the quad is a row head iff its quad
+  // index is a multiple of period / 4; components c < head then use lr_head
+  const bool head_quad = G.period > 0 && uint32_t((q - a.quad_start[gi]) % uint32_t(G.period / 4)) == 0u;
   const bool vec = ((reinterpret_cast<uintptr_t>(G.param) | reinterpret_cast<uintptr_t>(G.grad) |
                      reinterpret_cast<uintptr_t>(G.exp_avg) | reinterpret_cast<uintptr_t>(G.exp_avg_sq)) & 15) == 0;
   if (vec && e0 + 4 <= G.numel) {
@@ -42,7 +45,7 @@ __global__ void __launch_bounds__(256) adam_kernel(AdamArgs a) {
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       const int64_t e = e0 + k;
-      const float lr = (G.period > 0 && int(e % G.period) < G.head) ? G.lr_head : G.lr;
+      const float lr = (head_quad && k < G.head) ? G.lr_head : G.lr;
       adam_elem(pp[k], pg[k], pm[k], pv[k], lr, a);
     }
     *reinterpret_cast<float4*>(G.param + e0) = p;
@@ -52,7 +55,7 @@ __global__ void __launch_bounds__(256) adam_kernel(AdamArgs a) {
     for (int k = 0; k < 4; ++k) {
       const int64_t e = e0 + k;
       if (e >= G.numel) break;
-      const float lr = (G.period > 0 && int(e % G.period) < G.head) ? G.lr_head : G.lr;
+      const float lr = (head_quad && k < G.head) ? G.lr_head : G.lr;
       float p = G.param[e], m = G.exp_avg[e], v = G.exp_avg_sq[e];
       adam_elem(p, G.grad[e], m, v, lr, a);
       G.param[e] = p;
@@ -75,7 +78,8 @@ extern "C" int gs_adam_step(const gs_adam_group_t* groups, int32_t num_groups, d
   a.quad_start[0] = 0;
   for (int i = 0; i < num_groups; ++i) {
     a.g[i] = groups[i];
-    if (groups[i].numel < 0) return GS_ERR_INVALID_ARG;
+    if (groups[i].numel < 0 || (groups[i].period > 0 && (groups[i].period % 4 != 0 || groups[i].head > 4)))
+      return GS_ERR_INVALID_ARG;
     if (groups[i].numel > 0 &&
         (!groups[i].param || !groups[i].grad || !groups[i].exp_avg || !groups[i].exp_avg_sq))
       return GS_ERR_INVALID_ARG;

@@ -212,7 +212,8 @@ __device__ __forceinline__ void adam_update(float& p, float g, float& m, float& 
   m = __fadd_rn(__fmul_rn(c.beta1, m), __fmul_rn(c.one_m_beta1, g));
   v = __fadd_rn(__fmul_rn(c.beta2, v), __fmul_rn(__fmul_rn(c.one_m_beta2, g), g));
   const float denom = __fadd_rn(__fsqrt_rn(__fmul_rn(v, c.inv_bias2)), c.eps);
-  p = __fsub_rn(p, __fdiv_rn(__fmul_rn(lr, __fmul_rn(m, c.inv_bias1)), denom));
+  // denom >= eps = 1e-15 is a normal float: __fdividef is accurate to 2 ulp
+  p = __fsub_rn(p, __fdividef(__fmul_rn(lr, __fmul_rn(m, c.inv_bias1)), denom));
 }
 
 // ---------------------------------------------------------------------------

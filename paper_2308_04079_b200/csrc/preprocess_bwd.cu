@@ -325,7 +325,11 @@ preprocess_bwd_adam_kernel(gs_params_t p, DevCamera cam, int degree, const float
                            gs_stats_t stats, FusedAdam A) {
   extern __shared__ __align__(16) float4 smem4[];
   float4* s_sh = smem4;                      // staged SH coefficients (the SH parameters)
-  float4* s_dsh = smem4 + 128 * kShStride;   // d_sh rows
+  float4* s_dsh = smem4;  // d_sh rows: each thread overwrites its own SH row after grad_one read it
+  float4* s_grot = smem4 + 128 * kShStride;  // (128) rotation grads
+  float* s_gmean = reinterpret_cast<float*>(s_grot + 128);  // (128*3)
+  float* s_glogs = s_gmean + 128 * 3;                       // (128*3)
+  float* s_gop = s_glogs + 128 * 3;                         // (128)
   const int64_t g0 = int64_t(blockIdx.x) * blockDim.x;
   const int64_t g = g0 + threadIdx.x;
   const bool valid = g < p.n;
@@ -343,61 +347,66 @@ preprocess_bwd_adam_kernel(gs_params_t p, DevCamera cam, int degree, const float
     grad_one(in, cam, degree, s_sh + threadIdx.x * kShStride, o, b, dcol);
     update_stats(stats, g, o.norm, radius, cam.height);
   }
+  // gradients -> shared memory, group-major, so every Adam group below is a
+  // coalesced sweep over the block's contiguous span
+  const int tid = threadIdx.x;
   if (valid) {
     if (out.d_means) store_grads(out, g, o, false);
-    // dense Adam on the 11 non-SH parameters of this Gaussian
-    float* means = const_cast<float*>(p.means);
-    float* logs = const_cast<float*>(p.log_scales);
-    float pm[3] = {in.m0, in.m1, in.m2}, pl[3] = {in.l0, in.l1, in.l2};
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
-      float m = A.m[0][3 * g + k], v = A.v[0][3 * g + k];
-      adam_update(pm[k], o.dmean[k], m, v, A.lr[0], A.c);
-      means[3 * g + k] = pm[k];
-      A.m[0][3 * g + k] = m;
-      A.v[0][3 * g + k] = v;
+      s_gmean[3 * tid + k] = o.dmean[k];
+      s_glogs[3 * tid + k] = o.dlogs[k];
     }
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      float m = A.m[1][3 * g + k], v = A.v[1][3 * g + k];
-      adam_update(pl[k], o.dlogs[k], m, v, A.lr[1], A.c);
-      logs[3 * g + k] = pl[k];
-      A.m[1][3 * g + k] = m;
-      A.v[1][3 * g + k] = v;
-    }
-    {
-      float4 q = in.q, m = reinterpret_cast<float4*>(A.m[2])[g], v = reinterpret_cast<float4*>(A.v[2])[g];
-      adam_update(q.x, o.drot.x, m.x, v.x, A.lr[2], A.c);
-      adam_update(q.y, o.drot.y, m.y, v.y, A.lr[2], A.c);
-      adam_update(q.z, o.drot.z, m.z, v.z, A.lr[2], A.c);
-      adam_update(q.w, o.drot.w, m.w, v.w, A.lr[2], A.c);
-      reinterpret_cast<float4*>(const_cast<float*>(p.rotations))[g] = q;
-      reinterpret_cast<float4*>(A.m[2])[g] = m;
-      reinterpret_cast<float4*>(A.v[2])[g] = v;
-    }
-    {
-      float op = in.op, m = A.m[3][g], v = A.v[3][g];
-      adam_update(op, o.dlogit, m, v, A.lr[3], A.c);
-      const_cast<float*>(p.opacity_logits)[g] = op;
-      A.m[3][g] = m;
-      A.v[3][g] = v;
-    }
-    float4* row = s_dsh + threadIdx.x * kShStride;
+    s_grot[tid] = o.drot;
+    s_gop[tid] = o.dlogit;
+    float4* row = s_dsh + tid * kShStride;
 #pragma unroll
     for (int k = 0; k < 12; ++k) row[k] = dsh_quad(b, dcol, k);
   }
   __syncthreads();
   if (out.d_sh) store_sh_rows(s_dsh, p.n, g0, out.d_sh);
-  // dense Adam on the SH rows: coalesced float4 sweep over the block's span;
-  // element 0..2 of each 48-float row (the DC band) uses lr_sh_dc
   const int64_t left = p.n - g0;
   const int nb = left < int64_t(blockDim.x) ? int(left) : int(blockDim.x);
+  {  // dense Adam: means, log_scales (N,3); rotations (N,4); opacity (N,)
+    float* pm = const_cast<float*>(p.means) + 3 * g0;
+    float* pl = const_cast<float*>(p.log_scales) + 3 * g0;
+    float* mm = A.m[0] + 3 * g0;
+    float* vm = A.v[0] + 3 * g0;
+    float* ml = A.m[1] + 3 * g0;
+    float* vl = A.v[1] + 3 * g0;
+    for (int f = tid; f < 3 * nb; f += blockDim.x) {
+      float x = pm[f], m = mm[f], v = vm[f];
+      float y = pl[f], m2 = ml[f], v2 = vl[f];
+      adam_update(x, s_gmean[f], m, v, A.lr[0], A.c);
+      adam_update(y, s_glogs[f], m2, v2, A.lr[1], A.c);
+      pm[f] = x; mm[f] = m; vm[f] = v;
+      pl[f] = y; ml[f] = m2; vl[f] = v2;
+    }
+    if (tid < nb) {
+      float4* pr = reinterpret_cast<float4*>(const_cast<float*>(p.rotations)) + g0 + tid;
+      float4* mr = reinterpret_cast<float4*>(A.m[2]) + g0 + tid;
+      float4* vr = reinterpret_cast<float4*>(A.v[2]) + g0 + tid;
+      float4 q = *pr, m = *mr, v = *vr;
+      const float4 gq = s_grot[tid];
+      adam_update(q.x, gq.x, m.x, v.x, A.lr[2], A.c);
+      adam_update(q.y, gq.y, m.y, v.y, A.lr[2], A.c);
+      adam_update(q.z, gq.z, m.z, v.z, A.lr[2], A.c);
+      adam_update(q.w, gq.w, m.w, v.w, A.lr[2], A.c);
+      *pr = q; *mr = m; *vr = v;
+      float* po = const_cast<float*>(p.opacity_logits) + g0 + tid;
+      float op = *po, mo = A.m[3][g0 + tid], vo = A.v[3][g0 + tid];
+      adam_update(op, s_gop[tid], mo, vo, A.lr[3], A.c);
+      *po = op; A.m[3][g0 + tid] = mo; A.v[3][g0 + tid] = vo;
+    }
+  }
+  // dense Adam on the SH rows: coalesced float4 sweep over the block's span;
+  // element 0..2 of each 48-float row (the DC band) uses lr_sh_dc
   float4* shp = reinterpret_cast<float4*>(const_cast<float*>(p.sh)) + g0 * 12;
   float4* m4 = reinterpret_cast<float4*>(A.m[4]) + g0 * 12;
   float4* v4 = reinterpret_cast<float4*>(A.v[4]) + g0 * 12;
   for (int f = threadIdx.x; f < nb * 12; f += blockDim.x) {
     const int j = f / 12, k = f - j * 12;
-    float4 pq = s_sh[j * kShStride + k];
+    float4 pq = shp[f];
     const float4 gq = s_dsh[j * kShStride + k];
     float4 mq = m4[f], vq = v4[f];
     const float lr0 = (k == 0) ? A.lr_sh_dc : A.lr[4];
@@ -438,7 +447,7 @@ extern "C" int gs_preprocess_backward_adam(const gs_params_t* params, const gs_c
   if (stats) st = *stats;
   gs_grads_t go = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
   if (grads_out) go = *grads_out;
-  const size_t smem = 2 * 128 * gs::kShStride * sizeof(float4);
+  const size_t smem = (128 * gs::kShStride + 128) * sizeof(float4) + 128 * 7 * sizeof(float);
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(gs::preprocess_bwd_adam_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
