@@ -518,3 +518,80 @@ void or_adam(int64_t numel, double* p, const double* grad, double* m, double* v,
     p[e] -= l * (m[e] / b1) / (sqrt(v[e] / b2) + eps);
   }
 }
+
+/* ---- L1 + D-SSIM loss and image gradient (optimizer.py:141-163; ssim.py:50-84)
+ * 11-tap Gaussian window (sigma 1.5), separable, zero padding, per channel.
+ * out[0] = loss, out[1] = mean |x-y|, out[2] = mean SSIM; d_image (H,W,3). */
+static void filt(const double* in, double* out, double* tmp, int H, int W, const double* w) {
+  /* rows then columns; in/out (H,W,3) */
+#pragma omp parallel for schedule(static)
+  for (int r = 0; r < H; ++r)
+    for (int c = 0; c < W; ++c)
+      for (int ch = 0; ch < 3; ++ch) {
+        double acc = 0.0;
+        for (int k = -5; k <= 5; ++k) {
+          int rr = r + k;
+          if (rr < 0 || rr >= H) continue;
+          acc += w[k + 5] * in[((int64_t)rr * W + c) * 3 + ch];
+        }
+        tmp[((int64_t)r * W + c) * 3 + ch] = acc;
+      }
+#pragma omp parallel for schedule(static)
+  for (int r = 0; r < H; ++r)
+    for (int c = 0; c < W; ++c)
+      for (int ch = 0; ch < 3; ++ch) {
+        double acc = 0.0;
+        for (int k = -5; k <= 5; ++k) {
+          int cc = c + k;
+          if (cc < 0 || cc >= W) continue;
+          acc += w[k + 5] * tmp[((int64_t)r * W + cc) * 3 + ch];
+        }
+        out[((int64_t)r * W + c) * 3 + ch] = acc;
+      }
+}
+
+void or_l1_dssim(const double* x, const double* y, int H, int W, double lambda, double* out, double* d_image) {
+  const int64_t n = (int64_t)H * W * 3;
+  double w[11], s = 0.0;
+  for (int i = 0; i < 11; ++i) { double t = i - 5.0; w[i] = exp(-(t * t) / (2.0 * 1.5 * 1.5)); s += w[i]; }
+  for (int i = 0; i < 11; ++i) w[i] /= s;
+  double* buf = (double*)malloc(sizeof(double) * (size_t)n * 10);
+  double *mx = buf, *my = buf + n, *sxx = buf + 2 * n, *syy = buf + 3 * n, *sxy = buf + 4 * n;
+  double *tmp = buf + 5 * n, *prod = buf + 6 * n, *a = buf + 7 * n, *b = buf + 8 * n, *c = buf + 9 * n;
+  filt(x, mx, tmp, H, W, w);
+  filt(y, my, tmp, H, W, w);
+  for (int64_t i = 0; i < n; ++i) prod[i] = x[i] * x[i];
+  filt(prod, sxx, tmp, H, W, w);
+  for (int64_t i = 0; i < n; ++i) prod[i] = y[i] * y[i];
+  filt(prod, syy, tmp, H, W, w);
+  for (int64_t i = 0; i < n; ++i) prod[i] = x[i] * y[i];
+  filt(prod, sxy, tmp, H, W, w);
+  const double C1 = 0.01 * 0.01, C2 = 0.03 * 0.03, d_map = -lambda / (2.0 * (double)n);
+  double ssum = 0.0, l1 = 0.0;
+  for (int64_t i = 0; i < n; ++i) {
+    double vx = sxx[i] - mx[i] * mx[i], vy = syy[i] - my[i] * my[i], cxy = sxy[i] - mx[i] * my[i];
+    double a1 = 2.0 * mx[i] * my[i] + C1, a2 = 2.0 * cxy + C2;
+    double b1 = mx[i] * mx[i] + my[i] * my[i] + C1, b2 = vx + vy + C2;
+    ssum += (a1 * a2) / (b1 * b2);
+    l1 += fabs(x[i] - y[i]);
+    /* ssim_backward (ssim.py:67-84) */
+    double den = b1 * b2, da1 = d_map * a2 / den, da2 = d_map * a1 / den;
+    double db1 = -da1 * (a1 / b1), db2 = -da2 * (a2 / b2);
+    a[i] = 2.0 * my[i] * da1 + 2.0 * mx[i] * db1 - 2.0 * my[i] * da2 - 2.0 * mx[i] * db2;
+    b[i] = db2;
+    c[i] = 2.0 * da2;
+  }
+  double *fa = mx, *fb = my, *fc = sxx;  /* reuse */
+  filt(a, fa, tmp, H, W, w);
+  filt(b, fb, tmp, H, W, w);
+  filt(c, fc, tmp, H, W, w);
+  for (int64_t i = 0; i < n; ++i) {
+    double diff = x[i] - y[i];
+    double sg = diff > 0 ? 1.0 : (diff < 0 ? -1.0 : 0.0);
+    d_image[i] = (1.0 - lambda) * sg / (double)n + fa[i] + 2.0 * x[i] * fb[i] + y[i] * fc[i];
+  }
+  out[1] = l1 / (double)n;
+  out[2] = ssum / (double)n;
+  out[0] = (1.0 - lambda) * out[1] + lambda * (1.0 - out[2]) / 2.0;
+  free(buf);
+}

@@ -185,3 +185,16 @@ def to_reference_order(proj: dict, bins: dict) -> dict:
 __all__ = ["project", "bin_and_sort", "render_forward", "render_backward", "backward_project", "stats_update",
            "adam_group", "render_view", "params_f64", "to_reference_order", "set_threads", "num_threads"]
 _here = Path(__file__).resolve().parent
+
+
+def l1_dssim_loss(render, ground_truth, lambda_dssim: float = 0.2) -> tuple[np.ndarray, np.ndarray]:
+    """optimizer.loss (optimizer.py:141-163): ([loss, mean L1, mean SSIM], d_image)."""
+    x = np.ascontiguousarray(np.asarray(render, dtype=np.float64))
+    y = np.ascontiguousarray(np.asarray(ground_truth, dtype=np.float64))
+    if x.shape != y.shape:
+        raise ValueError(f"resolution mismatch: {x.shape} vs {y.shape}")
+    h, w = x.shape[0], x.shape[1]
+    out = np.zeros(3)
+    d = np.zeros_like(x)
+    lib().or_l1_dssim(_p(x), _p(y), c_int(h), c_int(w), c_double(lambda_dssim), _p(out), _p(d))
+    return out, d

@@ -29,14 +29,18 @@ constexpr int kG = 4;    // splats per reduction group
 constexpr int kC = 9;    // gradient components per splat
 
 struct BwdStage {
-  float4 r0[kBatch];
-  float4 r1[kBatch];
+  float4 geo[kBatch];    // (mx - tile_x0, my - tile_y0, A, B), see make_tile_splat
   float4 col[kBatch];
+  float2 geo2[kBatch];   // (C, alpha)
   float grad[kBatch][kC];
   uint32_t id[kBatch];
   uint8_t mask[kBatch];
 };
-constexpr size_t kSmemBytes = sizeof(BwdStage) * kStages;
+struct RawRec {          // the producer's landing buffer for the cp.async gathers
+  float4 r0[kBatch];
+  float4 r1[kBatch];
+};
+constexpr size_t kSmemBytes = sizeof(BwdStage) * kStages + sizeof(RawRec);
 
 // Sum v[0..35] over the warp.  On return lane l holds, in `out`, component
 // (l & 7) of splat (l >> 3) of the group, and `out8` holds component 8 of
@@ -111,6 +115,7 @@ blend_bwd_kernel(const float* __restrict__ d_image, const float4* __restrict__ r
                  int width, int height, int tiles_x, float3 bg, float4* __restrict__ grads2d) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   BwdStage* stages = reinterpret_cast<BwdStage*>(smem_raw);
+  RawRec* raw = reinterpret_cast<RawRec*>(smem_raw + sizeof(BwdStage) * kStages);
   __shared__ uint64_t full_bar[kStages], empty_bar[kStages];
   __shared__ int s_warp_max[kConsumerWarps + 1];
 
@@ -123,6 +128,7 @@ blend_bwd_kernel(const float* __restrict__ d_image, const float4* __restrict__ r
   const int py = ty * kTile + tile_py(t);
   const bool inside = consumer && (px < width) && (py < height);
   const float fx = float(px) + 0.5f, fy = float(py) + 0.5f;
+  const float lx = float(tile_px(t)) + 0.5f, ly = float(tile_py(t)) + 0.5f;
   const float tile_x0 = float(tx * kTile), tile_y0 = float(ty * kTile);
   const int2 range = ranges[tile];
 
@@ -186,8 +192,8 @@ blend_bwd_kernel(const float* __restrict__ d_image, const float4* __restrict__ r
           if (e < cnt) {
             const float4* src = rec + 4 * size_t(gid[u]);
             st.id[e] = gid[u];
-            cp_async16(&st.r0[e], src + 0);
-            cp_async16(&st.r1[e], src + 1);
+            cp_async16(&raw->r0[e], src + 0);
+            cp_async16(&raw->r1[e], src + 1);
             cp_async16(&st.col[e], src + 2);
           }
         }
@@ -195,7 +201,11 @@ blend_bwd_kernel(const float* __restrict__ d_image, const float4* __restrict__ r
 #pragma unroll
         for (int u = 0; u < kBatch / 32; ++u) {
           const int e = lane + 32 * u;
-          if (e < cnt) st.mask[e] = uint8_t(warp_cover_mask(st.r0[e], st.r1[e], tile_x0, tile_y0));
+          if (e < cnt) {
+            const float4 r0 = raw->r0[e], r1 = raw->r1[e];
+            make_tile_splat(r0, r1, tile_x0, tile_y0, st.geo[e], st.geo2[e]);
+            st.mask[e] = uint8_t(warp_cover_mask(r0, r1, tile_x0, tile_y0));
+          }
         }
         mbar_arrive(&full_bar[s]);
       }
@@ -231,30 +241,36 @@ blend_bwd_kernel(const float* __restrict__ d_image, const float4* __restrict__ r
           for (int u = 0; u < kG; ++u) {
 #pragma unroll
             for (int k = 0; k < kC; ++k) v[u * kC + k] = 0.0f;
-            const int j = js[u];
-            if (j < 0 || lo + j > last_idx) continue;
-            const float4 r1 = st.r1[j];
-            const AlphaEval e = eval_alpha(fx, fy, st.r0[j], r1, rec, st.id[j]);
-            if (e.a == 0.0f) continue;
-            any = true;
-            const float inv = __frcp_rn(1.0f - e.a);
-            T = T * inv;  // transmittance just before this splat
-            const float w = T * e.a;
-            const float4 col = st.col[j];
-            const float dc = col.x * dlx + col.y * dly + col.z * dlz;
-            const float d_a = T * dc - S * inv;  // gradients.py:81
-            S = fmaf(w, dc, S);
-            v[u * kC + 6] = w * dlx;
-            v[u * kC + 7] = w * dly;
-            v[u * kC + 8] = w * dlz;
-            if (e.live) {  // clamped alphas pass no gradient (gradients.py:83-84)
-              const float dp = d_a * e.a_raw;
-              v[u * kC + 0] = dp * (r1.x * e.dx + r1.y * e.dy);   // d_mean2d.x
-              v[u * kC + 1] = dp * (r1.y * e.dx + r1.z * e.dy);   // d_mean2d.y
-              v[u * kC + 2] = d_a * e.g;                          // d_alpha
-              v[u * kC + 3] = -0.5f * dp * e.dx * e.dx;           // d_conic a
-              v[u * kC + 4] = -dp * e.dx * e.dy;                  // d_conic b
-              v[u * kC + 5] = -0.5f * dp * e.dy * e.dy;           // d_conic c
+            const int j = max(js[u], 0);
+            const float4 geo = st.geo[j];
+            const AlphaEval e = eval_alpha_tile(lx, ly, fx, fy, geo, st.geo2[j], rec, st.id, j);
+            // branch-light body: lanes past their last contributor (or the
+            // padding slots of a short group) evaluate but are masked by `use`
+            const bool use = (js[u] >= 0) && (lo + j <= last_idx) && (e.a > 0.0f);
+            if (use) {
+              any = true;
+              const float inv = __frcp_rn(1.0f - e.a);
+              T = T * inv;  // transmittance just before this splat
+              const float w = T * e.a;
+              const float4 col = st.col[j];
+              const float dc = col.x * dlx + col.y * dly + col.z * dlz;
+              const float d_a = T * dc - S * inv;  // gradients.py:81
+              S = fmaf(w, dc, S);
+              v[u * kC + 6] = w * dlx;
+              v[u * kC + 7] = w * dly;
+              v[u * kC + 8] = w * dlz;
+              if (e.live) {  // clamped alphas pass no gradient (gradients.py:83-84)
+                const float dp = d_a * e.a_raw;
+                // d power / d mean = (a dx + b dy, b dx + c dy) = -(2A dx + B dy, B dx + 2C dy) / log2(e)
+                const float q = dp * (-1.0f / kLog2e);
+                const float C = st.geo2[j].x;
+                v[u * kC + 0] = q * (2.0f * geo.z * e.dx + geo.w * e.dy);   // d_mean2d.x
+                v[u * kC + 1] = q * (geo.w * e.dx + 2.0f * C * e.dy);       // d_mean2d.y
+                v[u * kC + 2] = d_a * e.g;                                  // d_alpha
+                v[u * kC + 3] = -0.5f * dp * e.dx * e.dx;                   // d_conic a
+                v[u * kC + 4] = -dp * e.dx * e.dy;                          // d_conic b
+                v[u * kC + 5] = -0.5f * dp * e.dy * e.dy;                   // d_conic c
+              }
             }
           }
           if (!__any_sync(0xffffffffu, any)) continue;

@@ -28,15 +28,19 @@ constexpr int kConsumerWarps = 8;
 constexpr int kThreads = (kConsumerWarps + 1) * 32;
 
 struct FwdStage {
-  float4 r0[kBatch];
-  float4 r1[kBatch];
+  float4 geo[kBatch];    // (mx - tile_x0, my - tile_y0, A, B), see make_tile_splat
   float4 col[kBatch];
+  float2 geo2[kBatch];   // (C, alpha)
   uint32_t id[kBatch];
   uint8_t mask[kBatch];
 };
-constexpr size_t kSmemBytes = sizeof(FwdStage) * kStages;
+struct RawRec {          // the producer's landing buffer for the cp.async gathers
+  float4 r0[kBatch];
+  float4 r1[kBatch];
+};
+constexpr size_t kSmemBytes = sizeof(FwdStage) * kStages + sizeof(RawRec);
 
-__device__ __forceinline__ void produce_batch(FwdStage& st, const float4* __restrict__ rec,
+__device__ __forceinline__ void produce_batch(FwdStage& st, RawRec& raw, const float4* __restrict__ rec,
                                               const uint32_t* __restrict__ ids, int base, int cnt, int lane,
                                               float tile_x0, float tile_y0) {
   uint32_t gid[kBatch / 32];
@@ -51,8 +55,8 @@ __device__ __forceinline__ void produce_batch(FwdStage& st, const float4* __rest
     if (e < cnt) {
       const float4* src = rec + 4 * size_t(gid[u]);
       st.id[e] = gid[u];
-      cp_async16(&st.r0[e], src + 0);
-      cp_async16(&st.r1[e], src + 1);
+      cp_async16(&raw.r0[e], src + 0);
+      cp_async16(&raw.r1[e], src + 1);
       cp_async16(&st.col[e], src + 2);
     }
   }
@@ -60,7 +64,11 @@ __device__ __forceinline__ void produce_batch(FwdStage& st, const float4* __rest
 #pragma unroll
   for (int u = 0; u < kBatch / 32; ++u) {
     const int e = lane + 32 * u;
-    if (e < cnt) st.mask[e] = uint8_t(warp_cover_mask(st.r0[e], st.r1[e], tile_x0, tile_y0));
+    if (e < cnt) {
+      const float4 r0 = raw.r0[e], r1 = raw.r1[e];
+      make_tile_splat(r0, r1, tile_x0, tile_y0, st.geo[e], st.geo2[e]);
+      st.mask[e] = uint8_t(warp_cover_mask(r0, r1, tile_x0, tile_y0));
+    }
   }
 }
 
@@ -71,6 +79,7 @@ blend_fwd_kernel(const float4* __restrict__ rec, const uint32_t* __restrict__ id
                  float* __restrict__ t_final, int32_t* __restrict__ last) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   FwdStage* stages = reinterpret_cast<FwdStage*>(smem_raw);
+  RawRec* raw = reinterpret_cast<RawRec*>(smem_raw + sizeof(FwdStage) * kStages);
   __shared__ uint64_t full_bar[kStages], empty_bar[kStages];
   __shared__ int s_done, s_stop;
 
@@ -101,7 +110,7 @@ blend_fwd_kernel(const float4* __restrict__ rec, const uint32_t* __restrict__ id
       }
       if (ld_volatile(&s_stop)) return;
       const int base = range.x + b * kBatch;
-      produce_batch(stages[s], rec, ids, base, min(kBatch, range.y - base), lane, tile_x0, tile_y0);
+      produce_batch(stages[s], *raw, rec, ids, base, min(kBatch, range.y - base), lane, tile_x0, tile_y0);
       mbar_arrive(&full_bar[s]);
     }
     return;
@@ -112,6 +121,7 @@ blend_fwd_kernel(const float4* __restrict__ rec, const uint32_t* __restrict__ id
   const int py = ty * kTile + tile_py(t);
   const bool inside = (px < width) && (py < height);
   const float fx = float(px) + 0.5f, fy = float(py) + 0.5f;  // rasterizer.py:142
+  const float lx = float(tile_px(t)) + 0.5f, ly = float(tile_py(t)) + 0.5f;
   float T = 1.0f;
   float cr = 0.0f, cg = 0.0f, cb = 0.0f;
   int32_t last_idx = -1;
@@ -139,21 +149,22 @@ blend_fwd_kernel(const float4* __restrict__ rec, const uint32_t* __restrict__ id
         while (live) {
           const int j = c0 + __ffs(live) - 1;
           live &= live - 1;
-          if (done) continue;
-          const AlphaEval e = eval_alpha(fx, fy, st.r0[j], st.r1[j], rec, st.id[j]);
-          if (e.a == 0.0f) continue;
+          // branch-light body: finished lanes evaluate too (free under SIMT)
+          // and are masked by `take`
+          const AlphaEval e = eval_alpha_tile(lx, ly, fx, fy, st.geo[j], st.geo2[j], rec, st.id, j);
           const float t_new = T * (1.0f - e.a);
-          if (t_new < kTransSat) {  // 1 - T_new > 0.9999
-            done = true;
-            continue;
+          const bool blend = !done && e.a > 0.0f;
+          const bool sat = t_new < kTransSat;  // 1 - T_new > 0.9999
+          done = done || (blend && sat);
+          if (blend && !sat) {
+            const float4 c = st.col[j];
+            const float w = T * e.a;
+            cr = fmaf(w, c.x, cr);
+            cg = fmaf(w, c.y, cg);
+            cb = fmaf(w, c.z, cb);
+            T = t_new;
+            if (kTraining) last_idx = base + j;
           }
-          const float4 c = st.col[j];
-          const float w = T * e.a;
-          cr = fmaf(w, c.x, cr);
-          cg = fmaf(w, c.y, cg);
-          cb = fmaf(w, c.z, cb);
-          T = t_new;
-          if (kTraining) last_idx = base + j;
         }
         if (__all_sync(0xffffffffu, done)) break;
       }

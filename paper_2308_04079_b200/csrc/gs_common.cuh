@@ -99,7 +99,8 @@ __device__ __forceinline__ float ex2_approx(float x) {
 // Record layout (gs_splats_t.rec, 4 x float4 per Gaussian):
 //   r0 = (mx_hi, my_hi, alpha_hi, mx_lo)   r1 = (ca_hi, cb_hi, cc_hi, my_lo)
 //   r2 = (r, g, b, mask)                   r3 = (ca_lo, cb_lo, cc_lo, alpha_lo)
-static __device__ __noinline__ void eval_alpha_f64(float px, float py, float4 r0, float4 r1, float4 r3, AlphaEval& e) {
+// Returns (G, a_raw, a, live) by value (registers, no local memory).
+static __device__ __noinline__ float4 alpha_f64(float px, float py, float4 r0, float4 r1, float4 r3) {
   const double dx = double(px) - (double(r0.x) + double(r0.w));
   const double dy = double(py) - (double(r0.y) + double(r1.w));
   const double ca = double(r1.x) + double(r3.x), cb = double(r1.y) + double(r3.y), cc = double(r1.z) + double(r3.z);
@@ -108,10 +109,15 @@ static __device__ __noinline__ void eval_alpha_f64(float px, float py, float4 r0
   const double g = power > 0.0 ? 0.0 : exp(power);
   const double ar = al * g;
   const double a = ar < 0.99 ? ar : 0.99;
-  e.g = float(g);
-  e.a_raw = float(ar);
-  e.live = ar < 0.99;
-  e.a = (a < 1.0 / 255.0) ? 0.0f : float(a);
+  return make_float4(float(g), float(ar), (a < 1.0 / 255.0) ? 0.0f : float(a), ar < 0.99 ? 1.0f : 0.0f);
+}
+
+__device__ __forceinline__ void eval_alpha_f64(float px, float py, float4 r0, float4 r1, float4 r3, AlphaEval& e) {
+  const float4 v = alpha_f64(px, py, r0, r1, r3);
+  e.g = v.x;
+  e.a_raw = v.y;
+  e.a = v.z;
+  e.live = v.w != 0.0f;
 }
 
 __device__ __forceinline__ AlphaEval eval_alpha(float px, float py, float4 r0, float4 r1,
@@ -244,6 +250,49 @@ __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src)
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 __device__ __forceinline__ int ld_volatile(const int* p) { return *reinterpret_cast<const volatile int*>(p); }
+
+// ---------------------------------------------------------------------------
+// Per-(splat, tile) blend record, built once by the producer warp:
+//   geo  = (mx - tile_x0, my - tile_y0, A, B)     (tile-relative mean, from hi+lo in f64)
+//   geo2 = (C, alpha)
+// with (A, B, C) = -log2(e) * (a/2, b, c/2): the exponent in log2 units is
+//   p2 = A dx^2 + B dx dy + C dy^2 = log2(e) * power,  G = 2^p2
+// so the per-pixel evaluation needs no constant multiplies.  Both blend
+// kernels evaluate from the same records with the same intrinsics, so their
+// alphas (and contributor sets) are bit-identical; near the 1/255 and 0.99
+// thresholds the float64 slow path (eval_alpha_f64) decides from the global
+// hi/lo record.
+constexpr float kLog2e = 1.4426950408889634f;
+
+__device__ __forceinline__ void make_tile_splat(float4 r0, float4 r1, float tile_x0, float tile_y0, float4& geo,
+                                                float2& geo2) {
+  const double mx = (double(r0.x) + double(r0.w)) - double(tile_x0);
+  const double my = (double(r0.y) + double(r1.w)) - double(tile_y0);
+  geo = make_float4(float(mx), float(my), -0.5f * kLog2e * r1.x, -kLog2e * r1.y);
+  geo2 = make_float2(-0.5f * kLog2e * r1.z, r0.z);
+}
+
+// lx, ly: tile-local pixel centre (col + 0.5); px, py: absolute pixel centre
+__device__ __forceinline__ AlphaEval eval_alpha_tile(float lx, float ly, float px, float py, float4 geo,
+                                                     float2 geo2, const float4* __restrict__ rec,
+                                                     const uint32_t* s_id, int j) {
+  AlphaEval e;
+  e.dx = __fsub_rn(lx, geo.x);
+  e.dy = __fsub_rn(ly, geo.y);
+  const float p2 = __fmaf_rn(e.dx, __fmaf_rn(geo.z, e.dx, __fmul_rn(geo.w, e.dy)),
+                             __fmul_rn(__fmul_rn(geo2.x, e.dy), e.dy));
+  e.g = (p2 > 0.0f) ? 0.0f : ex2_approx(p2);
+  e.a_raw = __fmul_rn(geo2.y, e.g);
+  if (fabsf(e.a_raw - kAlphaEps) <= kGuard * kAlphaEps || fabsf(e.a_raw - kAlphaClamp) <= kGuard) {
+    const uint32_t gid = s_id[j];
+    eval_alpha_f64(px, py, rec[4 * size_t(gid) + 0], rec[4 * size_t(gid) + 1], rec[4 * size_t(gid) + 3], e);
+    return e;
+  }
+  e.live = e.a_raw < kAlphaClamp;
+  const float a = fminf(kAlphaClamp, e.a_raw);
+  e.a = (a < kAlphaEps) ? 0.0f : a;
+  return e;
+}
 
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll

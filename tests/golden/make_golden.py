@@ -25,7 +25,7 @@ sys.path.insert(0, "/root/reference/pkg/src")
 
 from splatlab.core import Camera as RefCamera, GaussianCloud, project  # noqa: E402
 from splatlab.gradients import backward_project  # noqa: E402
-from splatlab.optimizer import TrainConfig, TrainState, _adam_step  # noqa: E402
+from splatlab.optimizer import TrainConfig, TrainState, _adam_step, loss  # noqa: E402
 from splatlab.rasterizer import bin_and_sort, render_backward, render_forward  # noqa: E402
 
 sys.path.insert(0, str(REPO / "tests"))
@@ -95,6 +95,13 @@ def run_scene(name: str, cloud: dict, cam, degree: int, background, seed: int, c
     else:
         data.update(inputs)
         data.update(adam)
+        # L1 + D-SSIM loss (optimizer.py:141-163) of the float32-rounded render
+        # against a seeded float32 target image
+        render32 = out.image.astype(np.float32).astype(np.float64)
+        target = np.random.default_rng(seed + 100).uniform(0, 1, render32.shape).astype(np.float32)
+        value, d_loss = loss(render32, target.astype(np.float64), 0.2)
+        data.update({"loss_render": render32.astype(np.float32), "loss_target": target,
+                     "loss_value": np.array(value), "loss_d_image": d_loss})
     np.savez_compressed(HERE / f"{name}.npz", **data)
     print(f"{name}: N={n} V={len(sp)} K={len(b.keys)} {W}x{H} deg={degree}")
 
