@@ -9,11 +9,11 @@
 // by dividing out (1 - a) (gradients.py:67-70) and carries the composited
 // tail (gradients.py:75-78) as a running sum.
 //
-// Reduction: a warp processes the splats of its coverage mask in groups of
-// four; the 4 x 9 per-lane partial gradients are summed across the warp by a
-// transposed (reduce-scatter) butterfly — 37 shuffles per group instead of
-// 4 x 45 — leaving each of 8 lanes one summed component, which is added to
-// the stage's shared-memory accumulator.  When every consumer is done with a
+// Reduction: a warp processes the splats of its coverage mask in pairs; the
+// 2 x 9 per-lane partial gradients are summed across the warp by a
+// transposed (reduce-scatter) butterfly — 22 shuffles per pair instead of
+// 2 x 45 — leaving each of 8 lane pairs one summed component, which is added
+// to the stage's shared-memory accumulator.  When every consumer is done with a
 // stage the producer commits the tile's sums with three float4 atomics per
 // splat (one set per (splat, tile)) before refilling the stage.
 #include "gs_common.cuh"
@@ -21,11 +21,14 @@
 namespace gs {
 namespace {
 
+#ifndef GS_BWD_MIN_BLOCKS
+#define GS_BWD_MIN_BLOCKS 3  // 72 registers (small spill) beats 2 blocks at 96 (measured 1.69 vs 1.99 ms)
+#endif
 constexpr int kBatch = 256;
 constexpr int kStages = 3;
 constexpr int kConsumerWarps = 8;
 constexpr int kThreads = (kConsumerWarps + 1) * 32;
-constexpr int kG = 4;    // splats per reduction group
+constexpr int kG = 2;    // splats per reduction group (group_reduce2)
 constexpr int kC = 9;    // gradient components per splat
 
 struct BwdStage {
@@ -42,26 +45,21 @@ struct RawRec {          // the producer's landing buffer for the cp.async gathe
 };
 constexpr size_t kSmemBytes = sizeof(BwdStage) * kStages + sizeof(RawRec);
 
-// Sum v[0..35] over the warp.  On return lane l holds, in `out`, component
-// (l & 7) of splat (l >> 3) of the group, and `out8` holds component 8 of
-// that splat (valid in every lane of the 8-lane group).
-__device__ __forceinline__ void group_reduce(float (&v)[kG * kC], int lane, float& out, float& out8) {
-  const bool b16 = lane & 16, b8 = lane & 8, b4 = lane & 4, b2 = lane & 2, b1 = lane & 1;
-  float w[18];
-#pragma unroll
-  for (int i = 0; i < 18; ++i) {
-    const float send = b16 ? v[i] : v[i + 18];
-    const float keep = b16 ? v[i + 18] : v[i];
-    w[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
-  }
+// Two-splat variant: sum v[0..17] over the warp.  On return lane l holds, in
+// `out`, component ((l >> 1) & 7) of splat (l >> 4) (lanes l and l^1 hold the
+// same value) and `out8` holds component 8 of splat (l >> 4).
+// 37 instructions per splat with 18 live floats.
+__device__ __forceinline__ void group_reduce2(float (&v)[2 * kC], int lane, float& out, float& out8) {
+  const bool b16 = lane & 16, b8 = lane & 8, b4 = lane & 4, b2 = lane & 2;
   float x[9];
 #pragma unroll
   for (int i = 0; i < 9; ++i) {
-    const float send = b8 ? w[i] : w[i + 9];
-    const float keep = b8 ? w[i + 9] : w[i];
-    x[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+    const float send = b16 ? v[i] : v[i + 9];
+    const float keep = b16 ? v[i + 9] : v[i];
+    x[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
   }
   float c8 = x[8];
+  c8 += __shfl_xor_sync(0xffffffffu, c8, 8);
   c8 += __shfl_xor_sync(0xffffffffu, c8, 4);
   c8 += __shfl_xor_sync(0xffffffffu, c8, 2);
   c8 += __shfl_xor_sync(0xffffffffu, c8, 1);
@@ -69,20 +67,20 @@ __device__ __forceinline__ void group_reduce(float (&v)[kG * kC], int lane, floa
   float y[4];
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    const float send = b4 ? x[i] : x[i + 4];
-    const float keep = b4 ? x[i + 4] : x[i];
-    y[i] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+    const float send = b8 ? x[i] : x[i + 4];
+    const float keep = b8 ? x[i + 4] : x[i];
+    y[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
   }
   float z[2];
 #pragma unroll
   for (int i = 0; i < 2; ++i) {
-    const float send = b2 ? y[i] : y[i + 2];
-    const float keep = b2 ? y[i + 2] : y[i];
-    z[i] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+    const float send = b4 ? y[i] : y[i + 2];
+    const float keep = b4 ? y[i + 2] : y[i];
+    z[i] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
   }
-  const float send = b1 ? z[0] : z[1];
-  const float keep = b1 ? z[1] : z[0];
-  out = keep + __shfl_xor_sync(0xffffffffu, send, 1);
+  const float send = b2 ? z[0] : z[1];
+  float w = (b2 ? z[1] : z[0]) + __shfl_xor_sync(0xffffffffu, send, 2);
+  out = w + __shfl_xor_sync(0xffffffffu, w, 1);
 }
 
 // batch b covers sorted positions [lo, top) counted back from the tile's end
@@ -109,7 +107,7 @@ __device__ __forceinline__ void flush_stage(BwdStage& st, int cnt, int lane, flo
   }
 }
 
-__global__ void __launch_bounds__(kThreads, 3)
+__global__ void __launch_bounds__(kThreads, GS_BWD_MIN_BLOCKS)
 blend_bwd_kernel(const float* __restrict__ d_image, const float4* __restrict__ rec, const uint32_t* __restrict__ ids,
                  const int2* __restrict__ ranges, const float* __restrict__ t_final, const int32_t* __restrict__ last,
                  int width, int height, int tiles_x, float3 bg, float4* __restrict__ grads2d) {
@@ -249,7 +247,8 @@ blend_bwd_kernel(const float* __restrict__ d_image, const float4* __restrict__ r
             const bool use = (js[u] >= 0) && (lo + j <= last_idx) && (e.a > 0.0f);
             if (use) {
               any = true;
-              const float inv = __frcp_rn(1.0f - e.a);
+              // 1 - a >= 0.01: MUFU reciprocal (~1 ulp) instead of the IEEE sequence
+              const float inv = __fdividef(1.0f, 1.0f - e.a);
               T = T * inv;  // transmittance just before this splat
               const float w = T * e.a;
               const float4 col = st.col[j];
@@ -275,11 +274,12 @@ blend_bwd_kernel(const float* __restrict__ d_image, const float4* __restrict__ r
           }
           if (!__any_sync(0xffffffffu, any)) continue;
           float out, out8;
-          group_reduce(v, lane, out, out8);
-          const int j = js[lane >> 3];
-          if (j >= 0) {
-            atomicAdd(&st.grad[j][lane & 7], out);
-            if ((lane & 7) == 0) atomicAdd(&st.grad[j][8], out8);
+          group_reduce2(v, lane, out, out8);
+          const int j = js[lane >> 4];
+          const int comp = (lane >> 1) & 7;
+          if (j >= 0 && (lane & 1) == 0) {
+            atomicAdd(&st.grad[j][comp], out);
+            if (comp == 0) atomicAdd(&st.grad[j][8], out8);
           }
         }
       }
