@@ -154,7 +154,20 @@ __device__ __forceinline__ void stage_sh_rows(const float* __restrict__ src_rows
   const int64_t left = n - g0;
   const int nb = left < int64_t(blockDim.x) ? int(left) : int(blockDim.x);
   const float4* src = reinterpret_cast<const float4*>(src_rows) + g0 * 12;
-  for (int f = threadIdx.x; f < nb * 12; f += blockDim.x) {
+  const int total = nb * 12, step = blockDim.x;
+  int f = threadIdx.x;
+  // four loads in flight per thread before the shared-memory stores
+  for (; f + 3 * step < total; f += 4 * step) {
+    float4 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = __ldg(src + f + u * step);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int ff = f + u * step, j = ff / 12;
+      s[j * kShStride + (ff - j * 12)] = v[u];
+    }
+  }
+  for (; f < total; f += step) {
     const int j = f / 12;
     s[j * kShStride + (f - j * 12)] = __ldg(src + f);
   }

@@ -368,19 +368,31 @@ preprocess_bwd_adam_kernel(gs_params_t p, DevCamera cam, int degree, const float
   const int64_t left = p.n - g0;
   const int nb = left < int64_t(blockDim.x) ? int(left) : int(blockDim.x);
   {  // dense Adam: means, log_scales (N,3); rotations (N,4); opacity (N,)
-    float* pm = const_cast<float*>(p.means) + 3 * g0;
-    float* pl = const_cast<float*>(p.log_scales) + 3 * g0;
-    float* mm = A.m[0] + 3 * g0;
-    float* vm = A.v[0] + 3 * g0;
-    float* ml = A.m[1] + 3 * g0;
-    float* vl = A.v[1] + 3 * g0;
-    for (int f = tid; f < 3 * nb; f += blockDim.x) {
-      float x = pm[f], m = mm[f], v = vm[f];
-      float y = pl[f], m2 = ml[f], v2 = vl[f];
-      adam_update(x, s_gmean[f], m, v, A.lr[0], A.c);
-      adam_update(y, s_glogs[f], m2, v2, A.lr[1], A.c);
-      pm[f] = x; mm[f] = m; vm[f] = v;
-      pl[f] = y; ml[f] = m2; vl[f] = v2;
+    float* __restrict__ pm = const_cast<float*>(p.means) + 3 * g0;
+    float* __restrict__ pl = const_cast<float*>(p.log_scales) + 3 * g0;
+    float* __restrict__ mm = A.m[0] + 3 * g0;
+    float* __restrict__ vm = A.v[0] + 3 * g0;
+    float* __restrict__ ml = A.m[1] + 3 * g0;
+    float* __restrict__ vl = A.v[1] + 3 * g0;
+    // 3 * nb <= 3 * blockDim.x: at most 3 iterations, all loads issued first
+    float x[3], m[3], v[3], y[3], m2[3], v2[3];
+#pragma unroll
+    for (int u = 0; u < 3; ++u) {
+      const int f = tid + u * int(blockDim.x);
+      if (f < 3 * nb) {
+        x[u] = pm[f]; m[u] = mm[f]; v[u] = vm[f];
+        y[u] = pl[f]; m2[u] = ml[f]; v2[u] = vl[f];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 3; ++u) {
+      const int f = tid + u * int(blockDim.x);
+      if (f < 3 * nb) {
+        adam_update(x[u], s_gmean[f], m[u], v[u], A.lr[0], A.c);
+        adam_update(y[u], s_glogs[f], m2[u], v2[u], A.lr[1], A.c);
+        pm[f] = x[u]; mm[f] = m[u]; vm[f] = v[u];
+        pl[f] = y[u]; ml[f] = m2[u]; vl[f] = v2[u];
+      }
     }
     if (tid < nb) {
       float4* pr = reinterpret_cast<float4*>(const_cast<float*>(p.rotations)) + g0 + tid;
@@ -401,22 +413,37 @@ preprocess_bwd_adam_kernel(gs_params_t p, DevCamera cam, int degree, const float
   }
   // dense Adam on the SH rows: coalesced float4 sweep over the block's span;
   // element 0..2 of each 48-float row (the DC band) uses lr_sh_dc
-  float4* shp = reinterpret_cast<float4*>(const_cast<float*>(p.sh)) + g0 * 12;
-  float4* m4 = reinterpret_cast<float4*>(A.m[4]) + g0 * 12;
-  float4* v4 = reinterpret_cast<float4*>(A.v[4]) + g0 * 12;
-  for (int f = threadIdx.x; f < nb * 12; f += blockDim.x) {
-    const int j = f / 12, k = f - j * 12;
-    float4 pq = shp[f];
-    const float4 gq = s_dsh[j * kShStride + k];
-    float4 mq = m4[f], vq = v4[f];
-    const float lr0 = (k == 0) ? A.lr_sh_dc : A.lr[4];
-    adam_update(pq.x, gq.x, mq.x, vq.x, lr0, A.c);
-    adam_update(pq.y, gq.y, mq.y, vq.y, lr0, A.c);
-    adam_update(pq.z, gq.z, mq.z, vq.z, lr0, A.c);
-    adam_update(pq.w, gq.w, mq.w, vq.w, A.lr[4], A.c);
-    shp[f] = pq;
-    m4[f] = mq;
-    v4[f] = vq;
+  float4* __restrict__ shp = reinterpret_cast<float4*>(const_cast<float*>(p.sh)) + g0 * 12;
+  float4* __restrict__ m4 = reinterpret_cast<float4*>(A.m[4]) + g0 * 12;
+  float4* __restrict__ v4 = reinterpret_cast<float4*>(A.v[4]) + g0 * 12;
+  const int total = nb * 12, step = blockDim.x;
+  constexpr int kU = 3;  // 3 x 3 float4 loads in flight per thread
+  for (int f0 = threadIdx.x; f0 < total; f0 += kU * step) {
+    float4 pq[kU], mq[kU], vq[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int f = f0 + u * step;
+      if (f < total) {
+        pq[u] = shp[f];
+        mq[u] = m4[f];
+        vq[u] = v4[f];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int f = f0 + u * step;
+      if (f >= total) break;
+      const int j = f / 12, k = f - j * 12;
+      const float4 gq = s_dsh[j * kShStride + k];
+      const float lr0 = (k == 0) ? A.lr_sh_dc : A.lr[4];
+      adam_update(pq[u].x, gq.x, mq[u].x, vq[u].x, lr0, A.c);
+      adam_update(pq[u].y, gq.y, mq[u].y, vq[u].y, lr0, A.c);
+      adam_update(pq[u].z, gq.z, mq[u].z, vq[u].z, lr0, A.c);
+      adam_update(pq[u].w, gq.w, mq[u].w, vq[u].w, A.lr[4], A.c);
+      shp[f] = pq[u];
+      m4[f] = mq[u];
+      v4[f] = vq[u];
+    }
   }
 }
 
