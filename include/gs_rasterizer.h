@@ -135,6 +135,30 @@ typedef struct gs_adam_group {
   int32_t head;
 } gs_adam_group_t;
 
+/* Parameters + Adam moments of a cloud, PARAM_GROUPS order (optimizer.py:85):
+ * means (N,3), log_scales (N,3), rotations (N,4), opacity_logits (N,),
+ * sh (N,16,3); float32, device. */
+typedef struct gs_cloud_state {
+  float* param[5];
+  float* exp_avg[5];
+  float* exp_avg_sq[5];
+  int64_t n;
+} gs_cloud_state_t;
+
+/* densify_and_prune settings (TrainConfig, optimizer.py:20-70), resolved
+ * for one call. */
+typedef struct gs_densify_config {
+  double grad_threshold;         /* densify_grad_threshold                       */
+  double split_scale_threshold;  /* resolve_split_threshold(scene_extent)        */
+  double split_log_factor;       /* log(split_factor)                            */
+  double prune_alpha;            /* prune_alpha_threshold                        */
+  double prune_world_scale;      /* prune_world_percent * scene_extent           */
+  double prune_screen_fraction;  /* prune_screen_fraction                        */
+  int32_t prune_big;             /* iteration > opacity_reset_interval           */
+  int32_t reset_opacity;         /* iteration > 0 && iteration % interval == 0   */
+  float reset_logit;             /* logit(opacity_reset_alpha)                   */
+} gs_densify_config_t;
+
 /* ---- library info ------------------------------------------------------ */
 int gs_abi_version(void);
 const char* gs_status_string(int status);
@@ -211,6 +235,23 @@ int gs_preprocess_backward_adam(const gs_params_t* params, const gs_camera_t* ca
  * over all groups in one launch; bias1 = 1-beta1^t, bias2 = 1-beta2^t. */
 int gs_adam_step(const gs_adam_group_t* groups, int32_t num_groups, double beta1, double beta2,
                  double eps, double bias1, double bias2, void* stream);
+
+/* ---- adaptive density control: replaces
+ * optimizer.densify_and_prune (optimizer.py:304-374).
+ * gs_densify_classify counts clones and splits (synchronises `stream`);
+ * the caller then draws z = rng.standard_normal((2*n_split, 3)) from the
+ * training RNG (optimizer.py:335), uploads it (float32, device) and calls
+ * gs_densify_apply, which writes the densified, pruned, (opacity-reset)
+ * cloud and its moments into `out` (capacity >= N - n_split + n_clone +
+ * 2 n_split rows) in the reference's row order and reports the surviving
+ * row count (synchronises).  Densify statistics are left to the caller to
+ * reset (optimizer.py:372). */
+int gs_densify_workspace_size(int64_t n, size_t* bytes);
+int gs_densify_classify(const gs_cloud_state_t* cloud, const gs_stats_t* stats, const gs_densify_config_t* cfg,
+                        void* workspace, size_t workspace_bytes, int64_t* n_clone, int64_t* n_split, void* stream);
+int gs_densify_apply(const gs_cloud_state_t* cloud, const gs_stats_t* stats, const gs_densify_config_t* cfg,
+                     int64_t n_clone, int64_t n_split, const float* z, void* workspace, size_t workspace_bytes,
+                     gs_cloud_state_t* out, int64_t* n_out, void* stream);
 
 /* ---- training loss: replaces optimizer.loss
  * (optimizer.py:141-163) with ssim_map/ssim_backward (ssim.py:50-84).

@@ -64,6 +64,16 @@ class GsAdamGroup(ctypes.Structure):
     ]
 
 
+class GsCloudState(ctypes.Structure):
+    _fields_ = [("param", c_void_p * 5), ("exp_avg", c_void_p * 5), ("exp_avg_sq", c_void_p * 5), ("n", c_int64)]
+
+
+class GsDensifyConfig(ctypes.Structure):
+    _fields_ = [("grad_threshold", c_double), ("split_scale_threshold", c_double), ("split_log_factor", c_double),
+                ("prune_alpha", c_double), ("prune_world_scale", c_double), ("prune_screen_fraction", c_double),
+                ("prune_big", c_int32), ("reset_opacity", c_int32), ("reset_logit", c_float)]
+
+
 # (name, restype, argtypes) — the full exported surface of gs_rasterizer.h
 SIGNATURES = [
     ("gs_abi_version", c_int32, []),
@@ -83,6 +93,12 @@ SIGNATURES = [
     ("gs_preprocess_backward_adam", c_int32, [POINTER(GsParams), POINTER(GsCamera), c_int32, POINTER(GsSplats),
                                               c_void_p, POINTER(GsAdamGroup), c_double, c_double, c_double,
                                               c_double, c_double, POINTER(GsStats), POINTER(GsGrads), c_void_p]),
+    ("gs_densify_workspace_size", c_int32, [c_int64, POINTER(c_size_t)]),
+    ("gs_densify_classify", c_int32, [POINTER(GsCloudState), POINTER(GsStats), POINTER(GsDensifyConfig), c_void_p,
+                                      c_size_t, POINTER(c_int64), POINTER(c_int64), c_void_p]),
+    ("gs_densify_apply", c_int32, [POINTER(GsCloudState), POINTER(GsStats), POINTER(GsDensifyConfig), c_int64,
+                                   c_int64, c_void_p, c_void_p, c_size_t, POINTER(GsCloudState), POINTER(c_int64),
+                                   c_void_p]),
     ("gs_loss_workspace_size", c_int32, [c_int32, c_int32, POINTER(c_size_t)]),
     ("gs_l1_dssim_loss", c_int32, [c_void_p, c_void_p, c_int32, c_int32, c_double, c_void_p, c_size_t, c_void_p,
                                    c_void_p, c_void_p]),

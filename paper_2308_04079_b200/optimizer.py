@@ -22,6 +22,18 @@ class TrainConfig:
     """The Adam / schedule fields of splatlab TrainConfig (optimizer.py:20-48)."""
 
     lambda_dssim: float = 0.2
+    densify_interval: int = 100
+    densify_start: int = 500
+    densify_until: int | None = None   # default: half the schedule
+    densify_grad_threshold: float = 0.0002
+    split_scale_threshold: float | None = None   # world units; default 1% of scene extent
+    split_scale_percent: float = 0.01
+    split_factor: float = 1.6
+    opacity_reset_interval: int = 3000
+    opacity_reset_alpha: float = 0.01
+    prune_alpha_threshold: float = 0.005
+    prune_world_percent: float = 0.10
+    prune_screen_fraction: float = 0.5           # of image height
     total_iters: int = 30000
     lr_means: float = 1.6e-4
     lr_means_final: float = 1.6e-6
@@ -38,8 +50,20 @@ class TrainConfig:
     def __post_init__(self):
         if not 0.0 <= self.lambda_dssim <= 1.0:
             raise ValueError("lambda_dssim must be in [0, 1]")
-        if self.total_iters <= 0 or self.sh_band_interval <= 0:
-            raise ValueError("total_iters and sh_band_interval must be positive")
+        for name in ("densify_interval", "opacity_reset_interval", "sh_band_interval", "total_iters"):
+            if getattr(self, name) <= 0:
+                raise ValueError(f"{name} must be positive")
+        for name in ("densify_grad_threshold", "split_factor", "prune_alpha_threshold"):
+            if getattr(self, name) <= 0:
+                raise ValueError(f"{name} must be positive")
+
+    def resolve_split_threshold(self, scene_extent: float) -> float:
+        if self.split_scale_threshold is not None:
+            return self.split_scale_threshold
+        return self.split_scale_percent * scene_extent
+
+    def resolve_densify_until(self) -> int:
+        return self.densify_until if self.densify_until is not None else self.total_iters // 2
 
     def lr_means_at(self, iteration: int) -> float:
         """Exponential position-LR decay (optimizer.py:72-75)."""

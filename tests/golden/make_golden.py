@@ -106,10 +106,46 @@ def run_scene(name: str, cloud: dict, cam, degree: int, background, seed: int, c
     print(f"{name}: N={n} V={len(sp)} K={len(b.keys)} {W}x{H} deg={degree}")
 
 
+def run_densify(name: str, iteration: int, extent: float, seed: int) -> None:
+    """densify_and_prune (optimizer.py:304-374) on the scene_c cloud with
+    seeded float32-representable statistics and moments."""
+    from splatlab.optimizer import densify_and_prune
+    cloud, cam, *_ = build("scene_c")
+    gc = GaussianCloud(cloud["means"], cloud["rotations"], cloud["log_scales"], cloud["opacity_logits"], cloud["sh"])
+    n = len(gc)
+    rng = np.random.default_rng(seed)
+    f32 = lambda a: np.asarray(a, np.float32).astype(np.float64)  # noqa: E731
+    state = TrainState(gc, extent, seed=seed)
+    state.iteration = iteration
+    state.accum_count = rng.integers(0, 4, n).astype(np.int64)
+    state.accum_pos_grad = f32(rng.uniform(0.0, 0.0006, n) * state.accum_count)
+    state.max_radius_frac = f32(rng.uniform(0.0, 0.7, n))
+    moments = {}
+    for g in ("means", "log_scales", "rotations", "opacity_logits", "sh"):
+        state.exp_avg[g] = f32(rng.normal(size=getattr(gc, g).shape))
+        state.exp_avg_sq[g] = f32(rng.uniform(0, 1, getattr(gc, g).shape))
+        moments[f"in_m_{g}"], moments[f"in_v_{g}"] = state.exp_avg[g].copy(), state.exp_avg_sq[g].copy()
+    stats_in = {"in_accum": state.accum_pos_grad.copy(), "in_count": state.accum_count.copy(),
+                "in_maxr": state.max_radius_frac.copy()}
+    rep = densify_and_prune(state, TrainConfig(total_iters=30000))
+    out = {"iteration": np.array(iteration), "extent": np.array(extent), "seed": np.array(seed),
+           "cloned": np.array(rep.cloned), "split": np.array(rep.split), "pruned": np.array(rep.pruned),
+           "opacity_reset": np.array(rep.opacity_reset), **stats_in, **moments}
+    for g in ("means", "log_scales", "rotations", "opacity_logits", "sh"):
+        out[f"out_{g}"] = getattr(state.cloud, g)
+        out[f"out_m_{g}"] = state.exp_avg[g]
+        out[f"out_v_{g}"] = state.exp_avg_sq[g]
+    np.savez_compressed(HERE / f"{name}.npz", **out)
+    print(f"{name}: N={n} -> {len(state.cloud)} cloned={rep.cloned} split={rep.split} pruned={rep.pruned} "
+          f"reset={rep.opacity_reset}")
+
+
 def main() -> None:
     for name in SCENES:
         cloud, cam, degree, bg, seed, compact = build(name)
         run_scene(name, cloud, cam, degree, bg, seed, compact=compact)
+    run_densify("densify_a", iteration=600, extent=10.0, seed=21)
+    run_densify("densify_b", iteration=6000, extent=6.0, seed=22)
 
 
 if __name__ == "__main__":
