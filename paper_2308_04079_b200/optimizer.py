@@ -34,6 +34,7 @@ class TrainConfig:
     prune_alpha_threshold: float = 0.005
     prune_world_percent: float = 0.10
     prune_screen_fraction: float = 0.5           # of image height
+    warmup_upsample_iters: tuple[int, int] = (250, 500)
     total_iters: int = 30000
     lr_means: float = 1.6e-4
     lr_means_final: float = 1.6e-6

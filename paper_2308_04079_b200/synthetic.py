@@ -88,6 +88,67 @@ def toy_scene(n: int = 10_000, resolution: int = 256) -> tuple[dict, Camera]:
     return _cloud(points, rotations, log_scales, opacity, sh), cam
 
 
+# --------------------------------------------------------------------------
+# the reference's procedural toy problem (toydata.py), used by the
+# toy-recovery acceptance run (test_acceptance.py:104-116)
+
+TOY_COLORS = np.array([[0.85, 0.15, 0.10], [0.10, 0.75, 0.20], [0.15, 0.25, 0.90], [0.90, 0.80, 0.10],
+                       [0.80, 0.15, 0.80], [0.10, 0.80, 0.80], [0.95, 0.55, 0.15], [0.60, 0.60, 0.60]])
+SH_C0 = 0.28209479177387814
+
+
+def make_toy_cloud(seed: int = 7, count: int = 8) -> dict:
+    """Well-separated isotropic coloured blobs on a jittered sphere (toydata.py:26-47)."""
+    rng = np.random.default_rng(seed)
+    phi = np.linspace(0.0, 2.0 * np.pi, count, endpoint=False)
+    zs = np.linspace(-0.7, 0.7, count)
+    ring = np.sqrt(1 - zs**2)
+    means = np.stack([1.1 * np.cos(phi) * ring, 1.1 * np.sin(phi) * ring, 1.1 * zs], axis=1)
+    means = means + rng.normal(scale=0.08, size=means.shape)
+    q = np.zeros((count, 4))
+    q[:, 0] = 1.0
+    sigma = rng.uniform(0.25, 0.35, size=(count, 1))
+    alphas = rng.uniform(0.65, 0.9, size=count)
+    sh = np.zeros((count, 16, 3))
+    sh[:, 0, :] = (TOY_COLORS[:count] - 0.5) / SH_C0
+    return _cloud(means, q, np.log(np.repeat(sigma, 3, axis=1)), np.log(alphas / (1 - alphas)), sh)
+
+
+def make_toy_cameras(n_train: int = 24, n_test: int = 3, distance: float = 4.0, resolution: int = 128,
+                     focal: float | None = None) -> tuple[list[Camera], list[Camera]]:
+    """Golden-angle training band plus held-out in-betweens (toydata.py:71-90)."""
+    if focal is None:
+        focal = resolution * distance / 4.0
+    golden = np.pi * (3.0 - np.sqrt(5.0))
+    train = [orbit_camera(i * golden, np.arcsin(-0.75 + 1.5 * (i + 0.5) / n_train), distance, resolution, focal)
+             for i in range(n_train)]
+    test = [orbit_camera((i + 0.5) * golden, np.arcsin(-0.5 + 1.0 * (i + 0.5) / max(n_test, 1)), distance,
+                         resolution, focal) for i in range(n_test)]
+    return train, test
+
+
+def compute_scene_extent(cameras) -> float:
+    """Bounding-sphere radius of the camera centres (scene_io.py:236-248)."""
+    if cameras:
+        centers = np.stack([c.center for c in cameras])
+        extent = float(np.linalg.norm(centers - centers.mean(axis=0), axis=1).max())
+        if extent > 0:
+            return extent
+    return 1.0
+
+
+def init_random(count: int, bounds, rng) -> dict:
+    """Uniform points with isotropic kNN scales, opacity 0.1, zero SH (scene_io.py:339-366)."""
+    lo, hi = (np.asarray(b, dtype=np.float64) for b in bounds)
+    points = rng.uniform(lo, hi, size=(count, 3))
+    dist = (np.maximum(_mean_knn_distance(points), 1e-7) if count >= 4
+            else np.full(count, np.linalg.norm(hi - lo) / 10.0))
+    q = np.zeros((count, 4))
+    q[:, 0] = 1.0
+    return _cloud(points, q, np.repeat(np.log(dist)[:, None], 3, axis=1), np.full(count, np.log(0.1 / 0.9)),
+                  np.zeros((count, 16, 3)))
+
+
 def ball_cameras(count: int = 32, width: int = 1920, height: int = 1080, distance: float = 4.0) -> list[Camera]:
     """Golden-angle band of look-at cameras (toydata.py:79-83) at 1080p."""
     from .camera import look_at
