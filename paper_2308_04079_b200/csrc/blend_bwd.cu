@@ -237,45 +237,42 @@ blend_bwd_kernel(const float* __restrict__ d_image, const float4* __restrict__ r
           bool any = false;
 #pragma unroll
           for (int u = 0; u < kG; ++u) {
-#pragma unroll
-            for (int k = 0; k < kC; ++k) v[u * kC + k] = 0.0f;
             const int j = max(js[u], 0);
             const float4 geo = st.geo[j];
-            const AlphaEval e = eval_alpha_tile(lx, ly, fx, fy, geo, st.geo2[j], rec, st.id, j);
-            // branch-light body: lanes past their last contributor (or the
-            // padding slots of a short group) evaluate but are masked by `use`
+            const float2 geo2 = st.geo2[j];
+            const AlphaEval e = eval_alpha_tile(lx, ly, fx, fy, geo, geo2, rec, st.id, j);
+            // branch-free body: lanes past their last contributor (or the
+            // padding slots of a short group) evaluate with a = 0, which
+            // leaves T and S unchanged and zeroes every gradient term
             const bool use = (js[u] >= 0) && (lo + j <= last_idx) && (e.a > 0.0f);
-            if (use) {
-              any = true;
-              // 1 - a >= 0.01: MUFU reciprocal (~1 ulp) instead of the IEEE sequence
-              const float inv = __fdividef(1.0f, 1.0f - e.a);
-              T = T * inv;  // transmittance just before this splat
-              const float w = T * e.a;
-              const float4 col = st.col[j];
-              const float dc = col.x * dlx + col.y * dly + col.z * dlz;
-              const float d_a = T * dc - S * inv;  // gradients.py:81
-              S = fmaf(w, dc, S);
-              v[u * kC + 6] = w * dlx;
-              v[u * kC + 7] = w * dly;
-              v[u * kC + 8] = w * dlz;
-              if (e.live) {  // clamped alphas pass no gradient (gradients.py:83-84)
-                const float dp = d_a * e.a_raw;
-                // d power / d mean = (a dx + b dy, b dx + c dy) = -(2A dx + B dy, B dx + 2C dy) / log2(e)
-                const float q = dp * (-1.0f / kLog2e);
-                const float C = st.geo2[j].x;
-                v[u * kC + 0] = q * (2.0f * geo.z * e.dx + geo.w * e.dy);   // d_mean2d.x
-                v[u * kC + 1] = q * (geo.w * e.dx + 2.0f * C * e.dy);       // d_mean2d.y
-                v[u * kC + 2] = d_a * e.g;                                  // d_alpha
-                v[u * kC + 3] = -0.5f * dp * e.dx * e.dx;                   // d_conic a
-                v[u * kC + 4] = -dp * e.dx * e.dy;                          // d_conic b
-                v[u * kC + 5] = -0.5f * dp * e.dy * e.dy;                   // d_conic c
-              }
-            }
+            any |= use;
+            const float a = use ? e.a : 0.0f;
+            // 1 - a >= 0.01: MUFU reciprocal (~1 ulp), no IEEE/denormal sequence
+            const float inv = rcp_approx(1.0f - a);
+            T = use ? T * inv : T;  // transmittance just before this splat
+            const float w = T * a;
+            const float4 col = st.col[j];
+            const float dc = col.x * dlx + col.y * dly + col.z * dlz;
+            // clamped alphas pass no gradient (gradients.py:83-84)
+            const float d_a = (use && e.live) ? T * dc - S * inv : 0.0f;  // gradients.py:81
+            S = fmaf(w, dc, S);
+            v[u * kC + 6] = w * dlx;
+            v[u * kC + 7] = w * dly;
+            v[u * kC + 8] = w * dlz;
+            const float dp = d_a * e.a_raw;
+            // d power / d mean = (a dx + b dy, b dx + c dy) = -(2A dx + B dy, B dx + 2C dy) / log2(e)
+            const float q = dp * (-1.0f / kLog2e);
+            v[u * kC + 0] = q * (2.0f * geo.z * e.dx + geo.w * e.dy);   // d_mean2d.x
+            v[u * kC + 1] = q * (geo.w * e.dx + 2.0f * geo2.x * e.dy);  // d_mean2d.y
+            v[u * kC + 2] = d_a * e.g;                                  // d_alpha
+            v[u * kC + 3] = -0.5f * dp * e.dx * e.dx;                   // d_conic a
+            v[u * kC + 4] = -dp * e.dx * e.dy;                          // d_conic b
+            v[u * kC + 5] = -0.5f * dp * e.dy * e.dy;                   // d_conic c
           }
           if (!__any_sync(0xffffffffu, any)) continue;
           float out, out8;
           group_reduce2(v, lane, out, out8);
-          const int j = js[lane >> 4];
+          const int j = (lane & 16) ? js[1] : js[0];
           const int comp = (lane >> 1) & 7;
           if (j >= 0 && (lane & 1) == 0) {
             atomicAdd(&st.grad[j][comp], out);

@@ -96,6 +96,14 @@ __device__ __forceinline__ float ex2_approx(float x) {
   return y;
 }
 
+// one MUFU.RCP (the value __fdividef(1, x) computes for normal x, without
+// its denormal-range rescaling sequence)
+__device__ __forceinline__ float rcp_approx(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 // Record layout (gs_splats_t.rec, 4 x float4 per Gaussian):
 //   r0 = (mx_hi, my_hi, alpha_hi, mx_lo)   r1 = (ca_hi, cb_hi, cc_hi, my_lo)
 //   r2 = (r, g, b, mask)                   r3 = (ca_lo, cb_lo, cc_lo, alpha_lo)
