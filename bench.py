@@ -95,6 +95,17 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 # our arm
 
+def check_binned(k_infos: list) -> None:
+    """Every async binning of the run stayed within its instance capacity and
+    raised no error flag (K and flags stay on the device until here)."""
+    import torch
+    if k_infos:
+        flags = torch.stack(k_infos)[:, 1]
+        if bool((flags != 0).any()):
+            raise RuntimeError(f"async binning flagged an error/overflow: flags {flags.unique().tolist()}")
+    k_infos.clear()
+
+
 def run_ours(args, rank: int, world: int, local_rank: int) -> None:
     import torch
     import torch.distributed as dist
@@ -150,7 +161,9 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
         with StageTimer.stage(tm, "preprocess_fwd"):
             splats = R._project_tensors(params, n, dev, cam, DEGREE)
         with StageTimer.stage(tm, "bin_and_sort"):
-            binning = R.bin_and_sort(splats, WIDTH, HEIGHT)
+            # sync-free binning: K stays on the device, checked after the loop
+            binning = R.bin_and_sort_async(splats, WIDTH, HEIGHT)
+        binnings.append(binning.k_info)
         with StageTimer.stage(tm, "blend_fwd"):
             out = R.render_forward(splats, binning, WIDTH, HEIGHT, bg, training=True)
         with StageTimer.stage(tm, "loss"):
@@ -170,12 +183,16 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
             with StageTimer.stage(tm, "adam"):
                 adam.step(cloud, grads, iteration[0], config)
         if timed:
-            timer.note_instances(binning.num_instances, out)
+            timer.note_instances(binning, out)
         return loss
 
+    binnings = []
+    # size the instance buffers once from a synchronous binning of the first view
+    R.bin_and_sort(R._project_tensors(cloud.c_params(), n, dev, cam, DEGREE), WIDTH, HEIGHT)
     for _ in range(args.warmup):
         train_step(target, False)
     torch.cuda.synchronize()
+    check_binned(binnings)
     if world > 1:
         dist.barrier()
     clocks = ClockSampler(local_rank)
@@ -193,6 +210,7 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
         dist.barrier()
     ms = start.elapsed_time(end)
     clock_info = clocks.stop()
+    check_binned(binnings)   # every timed step binned within capacity (else the step is invalid)
     ms_t = torch.tensor([ms], device=dev)
     if world > 1:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
@@ -205,67 +223,39 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
                               "stage_ms": timer.mean_ms(), "instances": timer.last_k}), flush=True)
         return
 
-    # end-to-end through the public API: drop-in autograd Function + Adam,
-    # target image H2D from pinned host memory each step, loss D2H each step
+    # end-to-end through the public API: training.train_step, the mirror of the
+    # reference's train_step (optimizer.py:222-260) -- render, L1+D-SSIM loss,
+    # backward, fused Adam + densify statistics -- on a view whose target image
+    # lives in pinned HOST memory and is copied H2D inside every step; the
+    # step's result (loss, MSE for the PSNR, instance count) is read D2H.
+    from paper_2308_04079_b200.densify import TrainState
+    from paper_2308_04079_b200.training import TrainView, train_step
     gt_host = target.cpu().pin_memory()
-    leaves = [p.detach().clone().requires_grad_(True) for p in cloud.params()]
-    e2e_adam_cloud = GaussianCloud(means=leaves[0].data, rotations=leaves[2].data, log_scales=leaves[1].data,
-                                   opacity_logits=leaves[3].data, sh=leaves[4].data)
-    e2e_adam = DeviceAdam(e2e_adam_cloud)
-    e2e_it = [0]
-    # each step's target image is copied H2D from pinned memory on a copy stream,
-    # double-buffered so step i+1's copy overlaps step i's compute
-    copy_stream = torch.cuda.Stream(dev)
-    gt_bufs = [torch.empty_like(target) for _ in range(2)]
-    ready = [torch.cuda.Event() for _ in range(2)]
-    consumed = [torch.cuda.Event() for _ in range(2)]
-
-    def prefetch(i: int) -> None:
-        b = i % 2
-        with torch.cuda.stream(copy_stream):
-            copy_stream.wait_event(consumed[b])
-            gt_bufs[b].copy_(gt_host, non_blocking=True)
-            ready[b].record(copy_stream)
-
-    def e2e_step(i: int, count: int) -> float:
-        e2e_it[0] += 1
-        if i == 0:
-            prefetch(0)
-        if i + 1 < count:
-            prefetch(i + 1)
-        b = i % 2
-        torch.cuda.current_stream().wait_event(ready[b])
-        gt = gt_bufs[b]
-        for leaf in leaves:
-            leaf.grad = None
-        image, radii = R.rasterize_gaussians(*leaves, cam, bg, DEGREE, stats)
-        loss, d_image = l1_dssim_loss(image.detach(), gt, LAMBDA_DSSIM)
-        consumed[b].record()
-        image.backward(d_image)
-        g = R.GaussianGrads(leaves[0].grad, leaves[2].grad, leaves[1].grad, leaves[3].grad, leaves[4].grad,
-                            stats.accum_pos_grad)
-        if world > 1:
-            for leaf in leaves:
-                dist.all_reduce(leaf.grad)
-        e2e_adam.step(e2e_adam_cloud, g, e2e_it[0], config)
-        return float(loss[0].item())   # D2H of the step's loss
+    e2e_cloud = GaussianCloud(**{g: getattr(cloud, g).clone() for g in
+                                 ("means", "rotations", "log_scales", "opacity_logits", "sh")})
+    state = TrainState(e2e_cloud, scene_extent=10.0, seed=rank)
+    state.active_sh_degree = DEGREE
+    e2e_config = TrainConfig(lambda_dssim=LAMBDA_DSSIM, warmup_upsample_iters=(0, 0), sh_band_interval=10**9)
+    # one view per rank (each rank trains on its own shard of the view list)
+    views = [TrainView(view_for(r), gt_host) for r in range(world)]
 
     for i in range(args.warmup):
-        e2e_step(i, args.warmup)
+        train_step(state, views, e2e_config)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for i in range(args.steps):
-        e2e_step(i, args.steps)
+        report = train_step(state, views, e2e_config)
     e1.record()
     torch.cuda.synchronize()
     e_ms = torch.tensor([e0.elapsed_time(e1)], device=dev)
     if world > 1:
         dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
     e2e_ms = float(e_ms.item())
-    del leaves, e2e_adam, e2e_adam_cloud
+    e2e_loss = report.loss
+    del state, e2e_cloud
 
     # inference render FPS (forward only, same scene, same camera)
     fps_steps = max(args.steps, 10)
@@ -313,8 +303,10 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
         "stage_ms": {k: round(v, 4) for k, v in stage_ms.items()},
         "instances_per_view": timer.last_k, "evaluated_pairs_per_view": e_pairs, "visible_gaussians": visible,
         "e2e": {"value": round(e2e_value, 3), "unit": UNIT, "h2d_bytes_per_step": WIDTH * HEIGHT * 3 * 4,
-                "d2h_bytes_per_step": 4, "path": "GaussianRasterizer autograd.Function + DeviceAdam, "
-                                                 "target image from pinned host memory"},
+                "d2h_bytes_per_step": 4 * 4 + 3 * 8,
+                "path": "training.train_step (mirror of splatlab optimizer.train_step): target image H2D from "
+                        "pinned host memory every step, [loss, L1, SSIM, MSE] + [K, flags, K] read D2H",
+                "last_loss": round(e2e_loss, 6)},
         "gpu_launches": timer.launches_per_step() * args.steps,
         "roofline": roof["primary"], "roofline_hbm": roof["hbm"], "roofline_stages": roof["stages"],
         "fp32_peak_tflops_measured": round(fp32_peak, 2),

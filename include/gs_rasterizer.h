@@ -15,7 +15,8 @@
  *     allocates or frees device memory and keeps no global mutable state.
  *   - Work is enqueued on the caller's stream (`stream` is a cudaStream_t
  *     passed as void*; NULL = legacy default stream).  Only gs_bin_and_sort
- *     synchronises that stream once (to read the instance count K).
+ *     synchronises that stream once (to read the instance count K);
+ *     gs_bin_and_sort_async keeps K on the device.
  *   - Parameter layouts are the reference's (core.py:36-50): means (N,3),
  *     rotations (N,4) raw (r,i,j,k) quaternions, log_scales (N,3),
  *     opacity_logits (N,), sh (N,16,3) coefficient-major / channel-minor.
@@ -181,12 +182,21 @@ int gs_preprocess_forward(const gs_params_t* params, const gs_camera_t* camera,
  * writes the Gaussian id of every sorted instance plus per-tile [start,end)
  * ranges (T,2) int32 (empty tiles [0,0]).  Synchronises `stream` once to
  * read K, written to *k_out (host).  Returns GS_ERR_CAPACITY (and K) when
- * k_capacity < K; nothing is written in that case. */
+ * k_capacity < K; the instance buffers then hold unspecified values. */
 int gs_bin_workspace_size(int64_t n, int32_t width, int32_t height, int64_t k_capacity,
                           size_t* bytes);
 int gs_bin_and_sort(const gs_splats_t* splats, int32_t width, int32_t height,
                     void* workspace, size_t workspace_bytes, int64_t k_capacity,
                     uint32_t* sorted_ids, int32_t* ranges, int64_t* k_out, void* stream);
+/* Same binning, enqueued without any host synchronisation (CUDA-graph
+ * capturable): K never leaves the device.  k_info is a caller-owned DEVICE
+ * int64[3]: [0] = K, [1] = flags (1: zero quaternion among the survivors,
+ * 2: K > k_capacity, 4: K > 2^31 instances), [2] = min(K, k_capacity).
+ * When flags != 0 the ranges stay empty and the caller must check k_info
+ * (e.g. one step later) and re-run with a larger capacity / raise. */
+int gs_bin_and_sort_async(const gs_splats_t* splats, int32_t width, int32_t height,
+                          void* workspace, size_t workspace_bytes, int64_t k_capacity,
+                          uint32_t* sorted_ids, int32_t* ranges, int64_t* k_info, void* stream);
 
 /* ---- K6 forward blend: replaces rasterizer.render_forward (rasterizer.py:201-240)
  * image (H,W,3) float32.  When training != 0, t_final (H,W) float32 and
@@ -255,8 +265,9 @@ int gs_densify_apply(const gs_cloud_state_t* cloud, const gs_stats_t* stats, con
 
 /* ---- training loss: replaces optimizer.loss
  * (optimizer.py:141-163) with ssim_map/ssim_backward (ssim.py:50-84).
- * image, target (H,W,3) float32; loss_out (3,) float32 device:
- * [total loss, mean |image-target|, mean SSIM]; d_image (H,W,3) float32 =
+ * image, target (H,W,3) float32; loss_out (4,) float32 device:
+ * [total loss, mean |image-target|, mean SSIM, mean squared error (the
+ * step's PSNR, optimizer.py:257-259)]; d_image (H,W,3) float32 =
  * d loss / d image.  workspace: gs_loss_workspace_size bytes, device. */
 int gs_loss_workspace_size(int32_t width, int32_t height, size_t* bytes);
 int gs_l1_dssim_loss(const float* image, const float* target, int32_t width, int32_t height, double lambda_dssim,

@@ -8,15 +8,21 @@
 //   1. depth sort: stable radix sort of (depth bits, gaussian id) over N
 //      (ties keep index order, exactly like the reference's stable sort);
 //   2. per-Gaussian instance counts gathered in depth order, exclusive scan
-//      -> instance offsets and K (one D2H read);
+//      -> instance offsets and K, kept on the device (no host round trip);
 //   3. emission: warps write (tile id, gaussian id) for 32 depth-ranked
 //      Gaussians at a time into their contiguous output range, coalesced;
-//   4. stable radix sort of the instances on the tile id only
-//      (16-bit keys and ceil(log2 T) bits = 2 passes at 1080p and 4K);
-//   5. tile ranges from neighbouring tile ids, 8 keys per thread
+//      slots [K, capacity) are padded with the largest tile key;
+//   4. stable radix sort of the capacity-sized instance list on the tile id
+//      only (16-bit keys and ceil(log2 T) bits = 2 passes at 1080p and 4K);
+//   5. tile ranges from neighbouring tile ids over the first K sorted keys
 //      (rasterizer.py:118-123).
 // HBM traffic per instance: 6 B written by emission + 2 x 12 B per tile
-// pass + 2 B for ranges, against 6 x 24 B for a 64-bit key sort.
+// pass + 2 B for ranges, against 6 x 24 B for a 64-bit key sort.  Every
+// kernel after the scan reads K from device memory, so the whole binning is
+// enqueued without synchronising (CUDA-graph capturable); the grids and the
+// sort length are the caller's instance capacity and K > capacity is
+// reported through a device flag (gs_bin_and_sort_async) or, in the
+// synchronous entry point, as GS_ERR_CAPACITY after one stream sync.
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
@@ -26,6 +32,10 @@ namespace gs {
 namespace {
 
 constexpr uint32_t kCulledKey = 0xFFFFFFFFu;
+
+// kinfo[] (device, int64): [0] K, [1] flags, [2] K clamped to the capacity
+constexpr int64_t kFlagZeroQuat = 1, kFlagCapacity = 2, kFlagLimit = 4;
+
 
 __global__ void depth_keys_kernel(const float* __restrict__ depth, const int32_t* __restrict__ tiles,
                                   uint32_t* __restrict__ keys, uint32_t* __restrict__ ids, int64_t n) {
@@ -44,14 +54,19 @@ __global__ void gather_counts_kernel(const uint32_t* __restrict__ order, const i
 }
 
 __global__ void total_kernel(const uint64_t* __restrict__ offsets, const uint64_t* __restrict__ counts, int64_t n,
-                             const int32_t* __restrict__ status, uint64_t* __restrict__ out) {
-  out[0] = offsets[n - 1] + counts[n - 1];
-  out[1] = uint64_t(status[0]);
+                             int64_t capacity, const int32_t* __restrict__ status, int64_t* __restrict__ kinfo) {
+  const uint64_t K = offsets[n - 1] + counts[n - 1];
+  int64_t flags = (status[0] & 1) ? kFlagZeroQuat : 0;
+  if (K > uint64_t(kMaxInstances) || K > uint64_t(INT32_MAX)) flags |= kFlagLimit;  // rasterizer.py:99-101
+  if (K > uint64_t(capacity)) flags |= kFlagCapacity;
+  kinfo[0] = int64_t(K);
+  kinfo[1] = flags;
+  kinfo[2] = int64_t(K < uint64_t(capacity) ? K : uint64_t(capacity));
 }
 
 // Warp-cooperative emission.  A warp owns 32 consecutive depth-ranked
-// Gaussians whose instances occupy one contiguous output range (K < 2^31 is
-// checked by the host before launch).  The warp sweeps that range 32
+// Gaussians whose instances occupy one contiguous output range (32-bit
+// positions: the capacity is < 2^31, and positions past it are dropped).  The warp sweeps that range 32
 // positions at a time: each lane finds the Gaussian owning its position by a
 // binary search over the lanes' offsets (shuffles) and derives the tile from
 // the local index, row-major over the rectangle (rasterizer.py:105-111).
@@ -59,7 +74,7 @@ template <typename KeyT>
 __global__ void __launch_bounds__(256)
 emit_instances_kernel(const uint32_t* __restrict__ order, const uint64_t* __restrict__ offsets,
                       const uint64_t* __restrict__ counts, const int4* __restrict__ rect, int tiles_x,
-                      KeyT* __restrict__ tile_keys, uint32_t* __restrict__ ids, int64_t n) {
+                      KeyT* __restrict__ tile_keys, uint32_t* __restrict__ ids, int64_t n, int64_t capacity) {
   const int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31;
   uint32_t off = 0xFFFFFFFFu, end = 0u, g = 0u;
@@ -90,7 +105,7 @@ emit_instances_kernel(const uint32_t* __restrict__ order, const uint64_t* __rest
     const int ox = __shfl_sync(0xffffffffu, rc.x, owner);
     const int oy = __shfl_sync(0xffffffffu, rc.y, owner);
     const uint32_t og = __shfl_sync(0xffffffffu, g, owner);
-    if (o < warp_end) {
+    if (o < warp_end && int64_t(o) < capacity) {
       const uint32_t row = k / uint32_t(ow);
       const uint32_t col = k - row * uint32_t(ow);
       tile_keys[o] = KeyT((uint32_t(oy) + row) * uint32_t(tiles_x) + uint32_t(ox) + col);
@@ -99,13 +114,28 @@ emit_instances_kernel(const uint32_t* __restrict__ order, const uint64_t* __rest
   }
 }
 
+// Instance slots [K, capacity) get the largest key (all tile bits set) so the
+// capacity-sized sort leaves them behind every real instance (a stable sort
+// keeps them after the real instances of the last tile too).
+template <typename KeyT>
+__global__ void pad_instances_kernel(const int64_t* __restrict__ kinfo, int64_t capacity, KeyT* __restrict__ keys,
+                                     uint32_t* __restrict__ ids) {
+  for (int64_t i = kinfo[2] + int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < capacity;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    keys[i] = KeyT(~KeyT(0));
+    ids[i] = 0u;
+  }
+}
+
 // Tile ranges: each thread inspects 16 bytes of sorted keys plus its two
 // neighbours and records [start, end) where the tile id changes.
 template <typename KeyT>
-__global__ void tile_ranges_kernel(const KeyT* __restrict__ keys, int64_t k, int2* __restrict__ ranges) {
+__global__ void tile_ranges_kernel(const KeyT* __restrict__ keys, const int64_t* __restrict__ kinfo,
+                                   int2* __restrict__ ranges) {
   constexpr int kPer = 16 / sizeof(KeyT);
+  const int64_t k = kinfo[2];
   const int64_t i0 = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) * kPer;
-  if (i0 >= k) return;
+  if (i0 >= k || kinfo[1] != 0) return;
   KeyT v[kPer];
   if (i0 + kPer <= k) {
     const uint4 raw = *reinterpret_cast<const uint4*>(keys + i0);
@@ -130,11 +160,6 @@ __global__ void tile_ranges_kernel(const KeyT* __restrict__ keys, int64_t k, int
 
 inline size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
-struct Layout {
-  size_t depth_keys_in, depth_keys_out, ids_in, ids_out, counts, offsets, total, tile_keys_in, tile_keys_out,
-      inst_ids_in, cub_temp, bytes;
-};
-
 int bits_for(int64_t tiles) {
   int b = 1;
   while ((int64_t(1) << b) < tiles) ++b;
@@ -143,10 +168,15 @@ int bits_for(int64_t tiles) {
 
 bool small_keys(int64_t tiles) { return tiles <= 65536; }
 
+struct Layout {
+  size_t depth_keys_in, depth_keys_out, ids_in, ids_out, counts, offsets, kinfo, tile_keys_in, tile_keys_out,
+      inst_ids_in, cub_temp, bytes;
+};
+
 template <typename KeyT>
-cudaError_t tile_sort(void* temp, size_t& temp_bytes, const KeyT* kin, KeyT* kout, const uint32_t* vin, uint32_t* vout,
-                      int k, int bits, cudaStream_t s) {
-  return cub::DeviceRadixSort::SortPairs(temp, temp_bytes, kin, kout, vin, vout, k, 0, bits, s);
+cudaError_t sort_tiles(void* temp, size_t& temp_bytes, const KeyT* kin, KeyT* kout, const uint32_t* vin,
+                       uint32_t* vout, int64_t count, int bits, cudaStream_t s) {
+  return cub::DeviceRadixSort::SortPairs(temp, temp_bytes, kin, kout, vin, vout, int(count), 0, bits, s);
 }
 
 int make_layout(int64_t n, int64_t tiles, int64_t kcap, Layout* L) {
@@ -157,12 +187,13 @@ int make_layout(int64_t n, int64_t tiles, int64_t kcap, Layout* L) {
   if (e != cudaSuccess) return record_cuda_error(e);
   e = cub::DeviceScan::ExclusiveSum(nullptr, temp_scan, (const uint64_t*)nullptr, (uint64_t*)nullptr, nn);
   if (e != cudaSuccess) return record_cuda_error(e);
-  const int kk = int(kcap > 0 ? kcap : 1);
+  if (kcap > int64_t(INT32_MAX)) return GS_ERR_RESOURCE_LIMIT;
+  const int64_t kk = kcap > 0 ? kcap : 1;
   const size_t key_bytes = small_keys(tiles) ? 2 : 4;
   if (small_keys(tiles))
-    e = tile_sort<uint16_t>(nullptr, temp_tiles, nullptr, nullptr, nullptr, nullptr, kk, bits_for(tiles), nullptr);
+    e = sort_tiles<uint16_t>(nullptr, temp_tiles, nullptr, nullptr, nullptr, nullptr, kk, bits_for(tiles), nullptr);
   else
-    e = tile_sort<uint32_t>(nullptr, temp_tiles, nullptr, nullptr, nullptr, nullptr, kk, bits_for(tiles), nullptr);
+    e = sort_tiles<uint32_t>(nullptr, temp_tiles, nullptr, nullptr, nullptr, nullptr, kk, bits_for(tiles), nullptr);
   if (e != cudaSuccess) return record_cuda_error(e);
   size_t off = 0;
   auto take = [&](size_t bytes) {
@@ -177,7 +208,7 @@ int make_layout(int64_t n, int64_t tiles, int64_t kcap, Layout* L) {
   L->ids_out = take(4 * un);
   L->counts = take(8 * un);
   L->offsets = take(8 * un);
-  L->total = take(16);
+  L->kinfo = take(4 * sizeof(int64_t));
   L->tile_keys_in = take(key_bytes * uk + 16);
   L->tile_keys_out = take(key_bytes * uk + 16);
   L->inst_ids_in = take(4 * uk);
@@ -189,60 +220,50 @@ int make_layout(int64_t n, int64_t tiles, int64_t kcap, Layout* L) {
   return GS_OK;
 }
 
+// Emission in depth order, padding to the capacity, a stable sort of the
+// capacity-sized instance list on the tile bits only (ceil(log2 T): 2 radix
+// passes at 1080p and 4K) and the tile ranges — all sized by the host-known
+// capacity, with K itself read on the device.
 template <typename KeyT>
-int emit_sort_ranges(const uint32_t* order, const uint64_t* offsets, const uint64_t* counts, const int4* rect,
-                     int tiles_x, int64_t tiles, int64_t n, int64_t K, char* ws, const Layout& L, size_t temp_bytes,
-                     uint32_t* sorted_ids, int2* ranges, cudaStream_t s) {
+int tile_sort(const uint32_t* order, const uint64_t* offsets, const uint64_t* counts, const int4* rect, int tiles_x,
+              int64_t tiles, int64_t n, int64_t cap, const int64_t* kinfo, char* ws, const Layout& L,
+              size_t temp_bytes, uint32_t* sorted_ids, int2* ranges, cudaStream_t s) {
   auto* tk_in = reinterpret_cast<KeyT*>(ws + L.tile_keys_in);
   auto* tk_out = reinterpret_cast<KeyT*>(ws + L.tile_keys_out);
   auto* iid_in = reinterpret_cast<uint32_t*>(ws + L.inst_ids_in);
   const int block = 256;
   emit_instances_kernel<KeyT><<<unsigned((n + block - 1) / block), block, 0, s>>>(order, offsets, counts, rect,
-                                                                                   tiles_x, tk_in, iid_in, n);
+                                                                                   tiles_x, tk_in, iid_in, n, cap);
   int st = check_launch();
   if (st != GS_OK) return st;
-  cudaError_t e = tile_sort<KeyT>(ws + L.cub_temp, temp_bytes, tk_in, tk_out, iid_in, sorted_ids, int(K),
-                                  bits_for(tiles), s);
+  pad_instances_kernel<KeyT><<<4 * 148, block, 0, s>>>(kinfo, cap, tk_in, iid_in);
+  if ((st = check_launch()) != GS_OK) return st;
+  cudaError_t e = sort_tiles<KeyT>(ws + L.cub_temp, temp_bytes, tk_in, tk_out, iid_in, sorted_ids, cap,
+                                   bits_for(tiles), s);
   if (e != cudaSuccess) return record_cuda_error(e);
   constexpr int kPer = 16 / sizeof(KeyT);
-  const int64_t threads = (K + kPer - 1) / kPer;
-  tile_ranges_kernel<KeyT><<<unsigned((threads + block - 1) / block), block, 0, s>>>(tk_out, K, ranges);
+  const int64_t threads = (cap + kPer - 1) / kPer;
+  tile_ranges_kernel<KeyT><<<unsigned((threads + block - 1) / block), block, 0, s>>>(tk_out, kinfo, ranges);
   return check_launch();
 }
 
-}  // namespace
-}  // namespace gs
-
-extern "C" int gs_bin_workspace_size(int64_t n, int32_t width, int32_t height, int64_t k_capacity, size_t* bytes) {
-  if (!bytes || n < 0 || width <= 0 || height <= 0 || k_capacity < 0) return GS_ERR_INVALID_ARG;
-  const int64_t tiles = int64_t((width + gs::kTile - 1) / gs::kTile) * int64_t((height + gs::kTile - 1) / gs::kTile);
-  if (tiles > gs::kMaxTiles) return GS_ERR_RESOURCE_LIMIT;
-  gs::Layout L;
-  int st = gs::make_layout(n, tiles, k_capacity, &L);
-  if (st != GS_OK) return st;
-  *bytes = L.bytes;
-  return GS_OK;
-}
-
-extern "C" int gs_bin_and_sort(const gs_splats_t* splats, int32_t width, int32_t height, void* workspace,
-                               size_t workspace_bytes, int64_t k_capacity, uint32_t* sorted_ids, int32_t* ranges,
-                               int64_t* k_out, void* stream) {
-  using namespace gs;
-  if (!splats || !k_out || width <= 0 || height <= 0 || k_capacity < 0) return GS_ERR_INVALID_ARG;
+// Enqueues the whole binning; K and the flags land in kinfo (device).
+int bin_enqueue(const gs_splats_t* splats, int32_t width, int32_t height, void* workspace, size_t workspace_bytes,
+                int64_t k_capacity, uint32_t* sorted_ids, int32_t* ranges, int64_t* kinfo, cudaStream_t s) {
   const int tiles_x = (width + kTile - 1) / kTile, tiles_y = (height + kTile - 1) / kTile;
   const int64_t tiles = int64_t(tiles_x) * int64_t(tiles_y);
-  if (tiles > kMaxTiles) return GS_ERR_RESOURCE_LIMIT;  // rasterizer.py:76-79
-  if (tiles > int64_t(INT32_MAX)) return GS_ERR_RESOURCE_LIMIT;
   const int64_t n = splats->n;
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  *k_out = 0;
   cudaError_t e;
   if (ranges) {
     e = cudaMemsetAsync(ranges, 0, size_t(tiles) * 2 * sizeof(int32_t), s);
     if (e != cudaSuccess) return record_cuda_error(e);
   }
-  if (n == 0) return GS_OK;
+  if (n == 0) {
+    e = cudaMemsetAsync(kinfo, 0, 3 * sizeof(int64_t), s);
+    return e == cudaSuccess ? GS_OK : record_cuda_error(e);
+  }
   if (n > int64_t(INT32_MAX)) return GS_ERR_RESOURCE_LIMIT;
+  if (k_capacity > 0 && (!sorted_ids || !ranges)) return GS_ERR_INVALID_ARG;
   Layout L;
   int st = make_layout(n, tiles, k_capacity, &L);
   if (st != GS_OK) return st;
@@ -254,7 +275,6 @@ extern "C" int gs_bin_and_sort(const gs_splats_t* splats, int32_t width, int32_t
   auto* id_out = reinterpret_cast<uint32_t*>(ws + L.ids_out);
   auto* counts = reinterpret_cast<uint64_t*>(ws + L.counts);
   auto* offsets = reinterpret_cast<uint64_t*>(ws + L.offsets);
-  auto* total = reinterpret_cast<uint64_t*>(ws + L.total);
   void* temp = ws + L.cub_temp;
   size_t temp_bytes = workspace_bytes - L.cub_temp;
 
@@ -268,25 +288,88 @@ extern "C" int gs_bin_and_sort(const gs_splats_t* splats, int32_t width, int32_t
   if ((st = check_launch()) != GS_OK) return st;
   e = cub::DeviceScan::ExclusiveSum(temp, temp_bytes, counts, offsets, int(n), s);
   if (e != cudaSuccess) return record_cuda_error(e);
-  total_kernel<<<1, 1, 0, s>>>(offsets, counts, n, splats->status, total);
+  total_kernel<<<1, 1, 0, s>>>(offsets, counts, n, k_capacity, splats->status, kinfo);
   if ((st = check_launch()) != GS_OK) return st;
-  uint64_t host_total[2] = {0, 0};
-  e = cudaMemcpyAsync(host_total, total, sizeof(host_total), cudaMemcpyDeviceToHost, s);
+  if (k_capacity == 0) return GS_OK;
+  const int4* rect = reinterpret_cast<const int4*>(splats->rect);
+  if (small_keys(tiles))
+    return tile_sort<uint16_t>(id_out, offsets, counts, rect, tiles_x, tiles, n, k_capacity, kinfo, ws, L,
+                               temp_bytes, sorted_ids, reinterpret_cast<int2*>(ranges), s);
+  return tile_sort<uint32_t>(id_out, offsets, counts, rect, tiles_x, tiles, n, k_capacity, kinfo, ws, L, temp_bytes,
+                             sorted_ids, reinterpret_cast<int2*>(ranges), s);
+}
+
+int check_dims(int32_t width, int32_t height) {
+  if (width <= 0 || height <= 0) return GS_ERR_INVALID_ARG;
+  const int64_t tiles = int64_t((width + kTile - 1) / kTile) * int64_t((height + kTile - 1) / kTile);
+  if (tiles > kMaxTiles) return GS_ERR_RESOURCE_LIMIT;  // rasterizer.py:76-79
+  if (tiles > int64_t(INT32_MAX)) return GS_ERR_RESOURCE_LIMIT;
+  return GS_OK;
+}
+
+}  // namespace
+}  // namespace gs
+
+extern "C" int gs_bin_workspace_size(int64_t n, int32_t width, int32_t height, int64_t k_capacity, size_t* bytes) {
+  if (!bytes || n < 0 || k_capacity < 0) return GS_ERR_INVALID_ARG;
+  int st = gs::check_dims(width, height);
+  if (st != GS_OK) return st;
+  const int64_t tiles = int64_t((width + gs::kTile - 1) / gs::kTile) * int64_t((height + gs::kTile - 1) / gs::kTile);
+  gs::Layout L;
+  st = gs::make_layout(n, tiles, k_capacity, &L);
+  if (st != GS_OK) return st;
+  *bytes = L.bytes;
+  return GS_OK;
+}
+
+extern "C" int gs_bin_and_sort_async(const gs_splats_t* splats, int32_t width, int32_t height, void* workspace,
+                                     size_t workspace_bytes, int64_t k_capacity, uint32_t* sorted_ids,
+                                     int32_t* ranges, int64_t* k_info, void* stream) {
+  using namespace gs;
+  if (!splats || !k_info || k_capacity < 0) return GS_ERR_INVALID_ARG;
+  int st = check_dims(width, height);
+  if (st != GS_OK) return st;
+  return bin_enqueue(splats, width, height, workspace, workspace_bytes, k_capacity, sorted_ids, ranges, k_info,
+                     static_cast<cudaStream_t>(stream));
+}
+
+extern "C" int gs_bin_and_sort(const gs_splats_t* splats, int32_t width, int32_t height, void* workspace,
+                               size_t workspace_bytes, int64_t k_capacity, uint32_t* sorted_ids, int32_t* ranges,
+                               int64_t* k_out, void* stream) {
+  using namespace gs;
+  if (!splats || !k_out || k_capacity < 0) return GS_ERR_INVALID_ARG;
+  int st = check_dims(width, height);
+  if (st != GS_OK) return st;
+  *k_out = 0;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (splats->n == 0) {
+    if (ranges) {
+      const int64_t tiles = int64_t((width + kTile - 1) / kTile) * int64_t((height + kTile - 1) / kTile);
+      cudaError_t e = cudaMemsetAsync(ranges, 0, size_t(tiles) * 2 * sizeof(int32_t), s);
+      if (e != cudaSuccess) return record_cuda_error(e);
+    }
+    return GS_OK;
+  }
+  if (!workspace) return GS_ERR_INVALID_ARG;
+  const int64_t tiles = int64_t((width + kTile - 1) / kTile) * int64_t((height + kTile - 1) / kTile);
+  Layout L;
+  st = make_layout(splats->n, tiles, k_capacity, &L);
+  if (st != GS_OK) return st;
+  if (workspace_bytes < L.bytes) return GS_ERR_INVALID_ARG;
+  int64_t* kinfo = reinterpret_cast<int64_t*>(static_cast<char*>(workspace) + L.kinfo);
+  // with no instance buffers only K is computed (capacity 0)
+  const int64_t cap = (sorted_ids && ranges) ? k_capacity : 0;
+  st = bin_enqueue(splats, width, height, workspace, workspace_bytes, cap, sorted_ids, ranges, kinfo, s);
+  if (st != GS_OK) return st;
+  int64_t host[3] = {0, 0, 0};
+  cudaError_t e = cudaMemcpyAsync(host, kinfo, sizeof(host), cudaMemcpyDeviceToHost, s);
   if (e != cudaSuccess) return record_cuda_error(e);
   e = cudaStreamSynchronize(s);
   if (e != cudaSuccess) return record_cuda_error(e);
-  if (host_total[1] & 1u) return GS_ERR_ZERO_QUATERNION;
-  const uint64_t K = host_total[0];
-  *k_out = int64_t(K);
-  if (K > uint64_t(kMaxInstances)) return GS_ERR_RESOURCE_LIMIT;  // rasterizer.py:99-101
-  if (K > uint64_t(INT32_MAX)) return GS_ERR_RESOURCE_LIMIT;
-  if (int64_t(K) > k_capacity) return GS_ERR_CAPACITY;
-  if (K == 0) return GS_OK;
-  if (!sorted_ids || !ranges) return GS_ERR_INVALID_ARG;
-  const int4* rect = reinterpret_cast<const int4*>(splats->rect);
-  if (small_keys(tiles))
-    return emit_sort_ranges<uint16_t>(id_out, offsets, counts, rect, tiles_x, tiles, n, int64_t(K), ws, L,
-                                      temp_bytes, sorted_ids, reinterpret_cast<int2*>(ranges), s);
-  return emit_sort_ranges<uint32_t>(id_out, offsets, counts, rect, tiles_x, tiles, n, int64_t(K), ws, L, temp_bytes,
-                                    sorted_ids, reinterpret_cast<int2*>(ranges), s);
+  *k_out = host[0];
+  if (host[1] & kFlagZeroQuat) return GS_ERR_ZERO_QUATERNION;
+  if (host[1] & kFlagLimit) return GS_ERR_RESOURCE_LIMIT;  // rasterizer.py:99-101
+  if (host[1] & kFlagCapacity) return GS_ERR_CAPACITY;
+  if (host[0] > 0 && (!sorted_ids || !ranges)) return GS_ERR_INVALID_ARG;
+  return GS_OK;
 }

@@ -79,7 +79,7 @@ ssim_forward_kernel(const float* __restrict__ img, const float* __restrict__ gt,
   const int gx = ox + lx, gy = oy + ly;
   const bool inside = gx < W && gy < H;
   const size_t p = inside ? size_t(gy) * W + gx : 0;
-  double ssim_sum = 0.0, l1_sum = 0.0;
+  double ssim_sum = 0.0, l1_sum = 0.0, sq_sum = 0.0;
   for (int ch = 0; ch < 3; ++ch) {
     __syncthreads();
     for (int i = t; i < kIn * kT; i += 256) {
@@ -120,14 +120,18 @@ ssim_forward_kernel(const float* __restrict__ img, const float* __restrict__ gt,
       src[9 * p + 3 * 0 + ch] = float(d_mu);
       src[9 * p + 3 * 1 + ch] = float(d_b2);
       src[9 * p + 3 * 2 + ch] = float(2.0 * d_a2);
-      l1_sum += fabs(double(s_x[ly + kR][lx + kR][ch]) - double(s_y[ly + kR][lx + kR][ch]));
+      const double diff = double(s_x[ly + kR][lx + kR][ch]) - double(s_y[ly + kR][lx + kR][ch]);
+      l1_sum += fabs(diff);
+      sq_sum += diff * diff;   // for the step's PSNR (optimizer.py:257-259)
     }
   }
   const double s1 = block_sum(ssim_sum, s_red);
   const double s2 = block_sum(l1_sum, s_red);
+  const double s3 = block_sum(sq_sum, s_red);
   if (t == 0) {
     atomicAdd(&sums[0], s1);
     atomicAdd(&sums[1], s2);
+    atomicAdd(&sums[2], s3);
   }
 }
 
@@ -184,6 +188,7 @@ __global__ void loss_finalize_kernel(const double* __restrict__ sums, double cou
   loss[0] = float((1.0 - lambda) * l1 + lambda * dssim);
   loss[1] = float(l1);
   loss[2] = float(sums[0] / count);
+  loss[3] = float(sums[2] / count);   // mean squared error
 }
 
 }  // namespace
@@ -207,7 +212,7 @@ extern "C" int gs_l1_dssim_loss(const float* image, const float* target, int32_t
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   double* sums = static_cast<double*>(workspace);
   float* src = reinterpret_cast<float*>(static_cast<char*>(workspace) + 256);
-  cudaError_t e = cudaMemsetAsync(sums, 0, 2 * sizeof(double), s);
+  cudaError_t e = cudaMemsetAsync(sums, 0, 3 * sizeof(double), s);
   if (e != cudaSuccess) return record_cuda_error(e);
   const double count = double(width) * height * 3.0;
   const Window win = make_window();

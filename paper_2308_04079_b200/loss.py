@@ -22,8 +22,8 @@ def _workspace(width: int, height: int, device) -> torch.Tensor:
 
 
 def l1_dssim_loss(render: torch.Tensor, ground_truth: torch.Tensor, lambda_dssim: float = 0.2):
-    """(loss, d_loss/d_render) like the reference: loss is a (3,) device tensor
-    [total, mean L1, mean SSIM]; read it with float(loss[0]).  Raises
+    """(loss, d_loss/d_render) like the reference: loss is a (4,) device tensor
+    [total, mean L1, mean SSIM, mean squared error]; read it with float(loss[0]).  Raises
     ValueError on a resolution mismatch (optimizer.py:148-149)."""
     if tuple(render.shape) != tuple(ground_truth.shape):
         raise ValueError(f"resolution mismatch: {tuple(render.shape)} vs {tuple(ground_truth.shape)}")
@@ -35,7 +35,7 @@ def l1_dssim_loss(render: torch.Tensor, ground_truth: torch.Tensor, lambda_dssim
     render = render.detach().to(torch.float32).contiguous()
     ground_truth = ground_truth.detach().to(device=render.device, dtype=torch.float32).contiguous()
     ws = _workspace(w, h, render.device)
-    loss = torch.empty(3, dtype=torch.float32, device=render.device)
+    loss = torch.empty(4, dtype=torch.float32, device=render.device)
     d_image = torch.empty_like(render)
     _lib.check(_lib.load().gs_l1_dssim_loss(render.data_ptr(), ground_truth.data_ptr(), w, h, float(lambda_dssim),
                                             ws.data_ptr(), ws.numel(), loss.data_ptr(), d_image.data_ptr(),

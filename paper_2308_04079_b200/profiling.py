@@ -20,7 +20,7 @@ import torch
 
 # our own __global__ kernels launched per training step (CUB's radix-sort and scan
 # kernels, compiled into the same library, are counted separately in DESIGN.md)
-KERNELS_PER_STEP = {"preprocess_fwd": 1, "bin_and_sort": 5, "blend_fwd": 1, "loss": 3, "blend_bwd": 1,
+KERNELS_PER_STEP = {"preprocess_fwd": 1, "bin_and_sort": 7, "blend_fwd": 1, "loss": 3, "blend_bwd": 1,
                     "preprocess_bwd": 1, "adam": 1, "preprocess_bwd_adam": 1}
 
 
@@ -28,7 +28,6 @@ class StageTimer:
     def __init__(self, enabled: bool = True):
         self.enabled = enabled
         self.events = defaultdict(list)
-        self.last_k = None
         self.last_e = None
         self.samples = []
 
@@ -47,9 +46,18 @@ class StageTimer:
             e.record()
             timer.events[name].append((s, e))
 
-    def note_instances(self, k: int, out) -> None:
-        self.last_k = int(k)
+    def note_instances(self, k, out) -> None:
+        """k: an instance count, or a TileBinning whose (device-resident) K is
+        read only when the roofline is computed, after the timed region."""
+        self._k_src = k
         self._pending_out = out
+
+    @property
+    def last_k(self):
+        src = getattr(self, "_k_src", None)
+        if src is None:
+            return None
+        return int(src) if isinstance(src, int) else int(src.num_instances)
 
     def evaluated_pairs(self, out, ranges_start_of_pixel) -> int:
         last = out.last_contributor

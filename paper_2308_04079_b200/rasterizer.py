@@ -144,14 +144,41 @@ class TileBinning:
     """Sorted instances (rasterizer.py:44-52): Gaussian id per sorted instance
     and per-tile [start, end) ranges.  Keys are implicit: (tile, depth[id])."""
 
-    splat_ids: torch.Tensor   # (K,) int32 Gaussian index (N-space)
+    splat_ids: torch.Tensor   # (K,) int32 Gaussian index (N-space); (capacity,) when k_info is set
     ranges: torch.Tensor      # (T,2) int32
     tiles_x: int
     tiles_y: int
+    k_info: torch.Tensor | None = None   # async binning: device int64 [K, flags, min(K, capacity)]
+    n_gaussians: int = 0
 
     @property
     def num_instances(self) -> int:
+        if self.k_info is not None:
+            return int(self.k_info[0].item())   # synchronises
         return self.splat_ids.shape[0]
+
+    def check(self) -> None:
+        """Raise like the synchronous bin_and_sort would (async binning only;
+        synchronises).  A capacity overflow raises CapacityError: the ranges
+        were left empty and the frame must be re-binned."""
+        if self.k_info is None:
+            return
+        self.check_host([int(v) for v in self.k_info.tolist()])
+
+    def check_host(self, k_info) -> None:
+        """check() on an already-read copy of k_info (no synchronisation)."""
+        k, flags = int(k_info[0]), int(k_info[1])
+        _capacity.update(self.splat_ids.device, k, self.n_gaussians or None)
+        if flags & 1:
+            raise InvalidPrimitiveError("zero-norm quaternion cannot be normalized")
+        if flags & 4:
+            _lib.check(_lib.GS_ERR_RESOURCE_LIMIT, "bin_and_sort")
+        if flags & 2:
+            raise CapacityError(f"bin_and_sort: {k} instances exceed the capacity {self.splat_ids.shape[0]}")
+
+
+class CapacityError(RuntimeError):
+    """Async binning overflowed its instance capacity (the hint is raised)."""
 
 
 @dataclass
@@ -258,17 +285,27 @@ def project(cloud: GaussianCloud, camera, active_sh_degree: int = 3) -> DeviceSp
 
 
 class _CapacityHint:
-    """Instance-buffer sizing: remembers the largest K seen per device so a
-    steady-state frame issues exactly one gs_bin_and_sort call."""
+    """Instance-buffer sizing: remembers, per device, the largest K and the
+    largest instances-per-Gaussian ratio seen, so a steady-state frame issues
+    exactly one binning call and a cloud that grew (densification) gets a
+    proportionally larger buffer."""
 
     def __init__(self):
         self.k = {}
+        self.ratio = {}
 
-    def get(self, device) -> int:
-        return self.k.get(str(device), 1 << 16)
+    def get(self, device, n: int | None = None) -> int:
+        key = str(device)
+        k = self.k.get(key, 1 << 16)
+        if n is not None and key in self.ratio:
+            k = max(k, int(self.ratio[key] * n * 1.15) + 1024)
+        return k
 
-    def update(self, device, k: int) -> None:
-        self.k[str(device)] = max(self.get(device), int(k * 1.15) + 1024)
+    def update(self, device, k: int, n: int | None = None) -> None:
+        key = str(device)
+        self.k[key] = max(self.k.get(key, 1 << 16), int(k * 1.15) + 1024)
+        if n:
+            self.ratio[key] = max(self.ratio.get(key, 0.0), k / n)
 
 
 _capacity = _CapacityHint()
@@ -282,7 +319,7 @@ def bin_and_sort(splats: DeviceSplats, width: int, height: int) -> TileBinning:
     n = len(splats)
     cs = splats.c_struct()
     stream = _stream()
-    cap = _capacity.get(device)
+    cap = _capacity.get(device, n)
     for _ in range(2):
         ws_bytes = ctypes.c_size_t(0)
         _lib.check(lib.gs_bin_workspace_size(n, width, height, cap, ctypes.byref(ws_bytes)), "bin_and_sort")
@@ -293,12 +330,35 @@ def bin_and_sort(splats: DeviceSplats, width: int, height: int) -> TileBinning:
         st = lib.gs_bin_and_sort(ctypes.byref(cs), width, height, ws.data_ptr(), ws_bytes.value, cap,
                                  ids.data_ptr(), ranges.data_ptr(), ctypes.byref(k), stream)
         if st == _lib.GS_ERR_CAPACITY:
-            _capacity.update(device, k.value)
-            cap = _capacity.get(device)
+            _capacity.update(device, k.value, n)
+            cap = _capacity.get(device, n)
             continue
         _lib.check(st, "bin_and_sort")
+        _capacity.update(device, k.value, n)
         return TileBinning(ids[:k.value], ranges, tiles_x, tiles_y)
     raise RuntimeError("bin_and_sort: instance capacity did not converge")
+
+
+def bin_and_sort_async(splats: DeviceSplats, width: int, height: int, capacity: int | None = None) -> TileBinning:
+    """bin_and_sort without a host synchronisation: K stays on the device
+    (binning.k_info) and the instance buffers are sized by `capacity`
+    (default: the largest K seen on this device x 1.15).  Call
+    binning.check() later (e.g. after the step) to surface errors."""
+    lib = _lib.load()
+    tiles_x, tiles_y = tile_extent(width, height)
+    device = splats.rec.device
+    cap = int(capacity) if capacity is not None else _capacity.get(device, len(splats))
+    ws_bytes = ctypes.c_size_t(0)
+    _lib.check(lib.gs_bin_workspace_size(len(splats), width, height, cap, ctypes.byref(ws_bytes)), "bin_and_sort")
+    ws = torch.empty(max(int(ws_bytes.value), 1), dtype=torch.uint8, device=device)
+    ids = torch.empty(max(cap, 1), dtype=torch.int32, device=device)
+    ranges = torch.empty((tiles_x * tiles_y, 2), dtype=torch.int32, device=device)
+    k_info = torch.empty(3, dtype=torch.int64, device=device)
+    cs = splats.c_struct()
+    _lib.check(lib.gs_bin_and_sort_async(ctypes.byref(cs), width, height, ws.data_ptr(), ws_bytes.value, cap,
+                                         ids.data_ptr(), ranges.data_ptr(), k_info.data_ptr(), _stream()),
+               "bin_and_sort")
+    return TileBinning(ids, ranges, tiles_x, tiles_y, k_info, len(splats))
 
 
 def _bg(background) -> ctypes.Array:
@@ -376,6 +436,18 @@ def render_view(cloud: GaussianCloud, camera, background, active_sh_degree: int 
     camera = _camera(camera)
     splats = _project_tensors(cloud.c_params(), len(cloud), cloud.device, camera, active_sh_degree)
     binning = bin_and_sort(splats, camera.width, camera.height)
+    out = render_forward(splats, binning, camera.width, camera.height, background, training=training)
+    return out, splats, binning
+
+
+def render_view_async(cloud: GaussianCloud, camera, background, active_sh_degree: int = 3, training: bool = False,
+                      capacity: int | None = None):
+    """render_view with the sync-free binning: no host synchronisation, so
+    the whole forward can be captured in a CUDA graph.  Errors (zero
+    quaternion, capacity overflow) surface through binning.check()."""
+    camera = _camera(camera)
+    splats = _project_tensors(cloud.c_params(), len(cloud), cloud.device, camera, active_sh_degree)
+    binning = bin_and_sort_async(splats, camera.width, camera.height, capacity)
     out = render_forward(splats, binning, camera.width, camera.height, background, training=training)
     return out, splats, binning
 

@@ -28,8 +28,79 @@ from .optimizer import TrainConfig
 @dataclass
 class TrainView:
     camera: Camera
-    image: torch.Tensor   # (H,W,3) float32 device, linear RGB in [0,1]
+    image: torch.Tensor   # (H,W,3) float32, linear RGB in [0,1]; device, or (pinned) host copied per step
     name: str = ""
+
+
+class _HostScalars:
+    """Pinned host landing buffers for the one device->host read per step."""
+
+    def __init__(self):
+        self.loss = torch.empty(4, dtype=torch.float32).pin_memory()
+        self.k_info = torch.empty(3, dtype=torch.int64).pin_memory()
+
+    def read(self, loss: torch.Tensor, k_info: torch.Tensor):
+        self.loss.copy_(loss, non_blocking=True)
+        self.k_info.copy_(k_info, non_blocking=True)
+        torch.cuda.current_stream(loss.device).synchronize()
+        return self.loss.tolist(), self.k_info.tolist()
+
+
+_host_scalars: dict = {}
+
+
+class _ImagePrefetcher:
+    """Host-resident view images: the next step's image (known in advance
+    from the epoch order) is copied H2D on a side stream while the current
+    step computes; two device buffers alternate, each released by an event
+    recorded after the loss kernels (its last reader)."""
+
+    def __init__(self, device):
+        self.device = device
+        self.stream = torch.cuda.Stream(device)
+        self.slots = [None, None]      # (view id, device tensor, ready event, consumed event)
+        self.turn = 0
+
+    def _issue(self, view: TrainView):
+        slot = self.turn
+        self.turn ^= 1
+        old = self.slots[slot]
+        buf = old[1] if old is not None and old[1].shape == view.image.shape else torch.empty(
+            view.image.shape, dtype=view.image.dtype, device=self.device)
+        ready = torch.cuda.Event()
+        with torch.cuda.stream(self.stream):
+            if old is not None:
+                self.stream.wait_event(old[3])
+            buf.copy_(view.image, non_blocking=True)
+            ready.record(self.stream)
+        self.slots[slot] = (id(view), buf, ready, torch.cuda.Event())
+        return self.slots[slot]
+
+    def get(self, view: TrainView):
+        """(device image, consumed event) for this step's view."""
+        hit = next((s for s in self.slots if s is not None and s[0] == id(view)), None)
+        if hit is None:
+            hit = self._issue(view)
+        torch.cuda.current_stream(self.device).wait_event(hit[2])
+        self.slots = [s if s is not hit else (None, s[1], s[2], s[3]) for s in self.slots]
+        return hit[1], hit[3]
+
+    def prefetch(self, view: TrainView) -> None:
+        if all(s is None or s[0] != id(view) for s in self.slots):
+            self._issue(view)
+
+
+_prefetchers: dict = {}
+
+
+def _peek_next_view(state: TrainState, num_views: int):
+    if num_views == 1:
+        return 0
+    order = getattr(state, "_epoch_order", None)
+    pos = getattr(state, "_epoch_pos", 0)
+    if order is None or pos >= len(order) or len(order) != num_views:
+        return None   # the next epoch's order is not drawn yet (RNG order must match the reference)
+    return int(order[pos])
 
 
 @dataclass
@@ -79,25 +150,82 @@ def next_view(state: TrainState, num_views: int) -> int:
     return view
 
 
-def train_step(state: TrainState, views: Sequence[TrainView], config: TrainConfig) -> StepReport:
+def _world(group) -> tuple[int, int]:
+    import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized():
+        return dist.get_world_size(group), dist.get_rank(group)
+    return 1, 0
+
+
+def train_step(state: TrainState, views: Sequence[TrainView], config: TrainConfig, group=None) -> StepReport:
+    """One iteration (optimizer.py:222-260), with ONE host synchronisation:
+    the loss, the step's MSE (for the PSNR) and the binning's instance count
+    and flags are read together after the loss kernels; the divergence check
+    (optimizer.py:245-246) and a binning capacity overflow (re-render with a
+    larger buffer) are handled there, before any gradient is applied.
+
+    Under torch.distributed (world > 1) every rank samples a view from its
+    contiguous shard of `views`, its gradients go to one flat
+    bucket, one NCCL all-reduce sums them and every rank runs the identical
+    Adam, so the replicas stay bit-identical."""
     state.iteration += 1
     it = state.iteration
     if it % config.sh_band_interval == 0 and state.active_sh_degree < 3:
         state.active_sh_degree += 1
-    view_idx = next_view(state, len(views))
+    world, rank = _world(group)
+    if world > 1:
+        from .distributed import shard_views
+        shard = shard_views(len(views), world, rank)
+        view_idx = shard[next_view(state, len(shard))]
+    else:
+        view_idx = next_view(state, len(views))
     view = views[view_idx]
     scale = warmup_scale(it, config.warmup_upsample_iters)
     camera = view.camera if scale == 1.0 else view.camera.scaled(scale)
-    gt = downscale_image(view.image, camera.height, camera.width)
+    device = state.cloud.device
+    image, consumed = view.image, None
+    if image.device != device:   # host-resident view: H2D from pinned memory, prefetched one step ahead
+        pf = _prefetchers.setdefault(str(device), _ImagePrefetcher(device))
+        image, consumed = pf.get(view)
+        if world > 1:
+            nxt = _peek_next_view(state, len(shard))
+            nxt = None if nxt is None else shard[nxt]
+        else:
+            nxt = _peek_next_view(state, len(views))
+        if nxt is not None and views[nxt].image.device != device:
+            pf.prefetch(views[nxt])
+    gt = downscale_image(image, camera.height, camera.width)
     bg = config.background
-    out, splats, binning = R.render_view(state.cloud, camera, bg, state.active_sh_degree, training=True)
-    loss, d_image = l1_dssim_loss(out.image, gt, config.lambda_dssim)
-    value = float(loss[0].item())
+    host = _host_scalars.setdefault(str(device), _HostScalars())
+    for attempt in range(3):
+        out, splats, binning = R.render_view_async(state.cloud, camera, bg, state.active_sh_degree, training=True)
+        loss, d_image = l1_dssim_loss(out.image, gt, config.lambda_dssim)
+        if consumed is not None:
+            consumed.record()
+        lvals, kvals = host.read(loss, binning.k_info)
+        try:
+            binning.check_host(kvals)
+            break
+        except R.CapacityError:
+            if attempt == 2:
+                raise
+    value, mse = float(lvals[0]), float(lvals[3])
     if not math.isfinite(value):
         raise TrainingDiverged(f"non-finite loss {value} at iteration {it}")
     g2 = R.render_backward(d_image, out, splats, binning, camera.width, camera.height, bg)
-    state.adam.backward_step(state.cloud, camera, splats, g2, state.active_sh_degree, it, config, stats=state.stats)
-    mse = float(torch.mean((out.image - gt) ** 2).item())
+    if world > 1:
+        from .distributed import GradientBucket
+        bucket = getattr(state, "_bucket", None)
+        if bucket is None or bucket.n != len(state.cloud):
+            bucket = state._bucket = GradientBucket(len(state.cloud), device)
+        bucket.zero_()
+        R.backward_project(state.cloud, camera, splats, g2, state.active_sh_degree, stats=state.stats,
+                           out=bucket.grads, accumulate=True)
+        bucket.allreduce_(group)
+        state.adam.step(state.cloud, bucket.grads, it, config)
+    else:
+        state.adam.backward_step(state.cloud, camera, splats, g2, state.active_sh_degree, it, config,
+                                 stats=state.stats)
     psnr = float("inf") if mse == 0.0 else 10.0 * math.log10(1.0 / mse)
     return StepReport(it, value, psnr, view_idx, len(state.cloud))
 

@@ -124,3 +124,68 @@ def test_multiview_accumulate_equals_sum(cuda_device):
     for key in ("d_means", "d_rotations", "d_log_scales", "d_opacity_logits", "d_sh"):
         torch.testing.assert_close(getattr(acc, key), getattr(total, key), rtol=1e-5, atol=1e-12)
     assert int(stats.accum_count.max()) <= 4 and int(stats.accum_count.sum()) > 0
+
+
+# ---------------------------------------------------------------------------
+# sync-free binning (gs_bin_and_sort_async): K stays on the device
+
+def test_async_binning_matches_sync(cuda_device):
+    cloud_np, cam = synthetic.frustum_scene(300_000, 1920, 1080, seed=4)
+    cloud = GaussianCloud.from_numpy(**cloud_np)
+    splats = R.project(cloud, cam, 3)
+    sync = R.bin_and_sort(splats, 1920, 1080)
+    K = sync.num_instances
+    asy = R.bin_and_sort_async(splats, 1920, 1080, capacity=K + 12345)
+    asy.check()
+    assert asy.num_instances == K
+    assert torch.equal(asy.splat_ids[:K], sync.splat_ids)
+    assert torch.equal(asy.ranges, sync.ranges)
+
+
+def test_async_binning_capacity_overflow_flagged(cuda_device):
+    cloud_np, cam = synthetic.frustum_scene(50_000, 640, 360, seed=5)
+    cloud = GaussianCloud.from_numpy(**cloud_np)
+    splats = R.project(cloud, cam, 3)
+    K = R.bin_and_sort(splats, 640, 360).num_instances
+    asy = R.bin_and_sort_async(splats, 640, 360, capacity=K // 2)
+    with pytest.raises(R.CapacityError):
+        asy.check()
+    assert int(asy.ranges.abs().sum()) == 0   # nothing half-binned is exposed
+    exact = R.bin_and_sort_async(splats, 640, 360, capacity=K)
+    exact.check()
+    assert exact.num_instances == K
+
+
+@pytest.mark.parametrize("w,h,n", [(7680, 4320, 150_000), (256, 256, 20_000)])
+def test_binning_other_pass_counts_vs_oracle(cuda_device, w, h, n):
+    # 8K: 129,600 tiles -> 32-bit tile keys, three 6-bit passes; 256^2: one pass
+    cloud_np, cam = synthetic.frustum_scene(n, w, h, seed=6)
+    cloud_np = synthetic.round_to_f32(cloud_np)
+    cloud = GaussianCloud.from_numpy(**cloud_np)
+    splats = R.project(cloud, cam, 3)
+    binning = R.bin_and_sort(splats, w, h)
+    check_binning_invariants(splats, binning, w, h)
+    proj = O.project(cloud_np, cam, 3)
+    bins = O.bin_and_sort(proj, w, h)
+    np.testing.assert_array_equal(binning.splat_ids.cpu().numpy(), bins["ids"])
+    np.testing.assert_array_equal(binning.ranges.cpu().numpy(), bins["ranges"])
+
+
+def test_forward_captured_in_cuda_graph(cuda_device):
+    # project -> async binning -> blend enqueue no host sync: one CUDA graph
+    cloud_np, cam = synthetic.frustum_scene(100_000, 960, 540, seed=7)
+    cloud = GaussianCloud.from_numpy(**cloud_np)
+    eager, _, _ = R.render_view(cloud, cam, (0.1, 0.2, 0.3), 3)
+    cap = R.bin_and_sort(R.project(cloud, cam, 3), 960, 540).num_instances + 1024
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):   # warm the allocator on the capture stream
+        R.render_view_async(cloud, cam, (0.1, 0.2, 0.3), 3, capacity=cap)
+    torch.cuda.current_stream().wait_stream(s)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        out, _, binning = R.render_view_async(cloud, cam, (0.1, 0.2, 0.3), 3, capacity=cap)
+    g.replay()
+    torch.cuda.synchronize()
+    binning.check()
+    assert torch.equal(out.image, eager.image)
