@@ -6,12 +6,13 @@ import of this module raises, and every stage function fails loudly.
 from __future__ import annotations
 
 import ctypes
+import os
 from ctypes import POINTER, c_double, c_float, c_int32, c_int64, c_size_t, c_uint32, c_void_p
 from pathlib import Path
 
 from .errors import InvalidPrimitiveError, ResourceLimitError
 
-LIB_PATH = Path(__file__).resolve().parent / "lib" / "libgs_b200.so"
+LIB_PATH = Path(os.environ.get("GS_B200_LIB") or Path(__file__).resolve().parent / "lib" / "libgs_b200.so")
 
 GS_OK = 0
 GS_ERR_INVALID_ARG = 1

@@ -207,21 +207,27 @@ __device__ __forceinline__ int tile_py(int t) { return (t >> 6) * 4 + ((t & 31) 
 // inflated so the test is conservative against float32 rounding: a pair is
 // skipped only if the reference would skip it (a < 1/255), so culling never
 // changes a result bit.
+// kBlockH = 4: eight 8x4 warp blocks (forward); kBlockH = 8: four 8x8
+// blocks (backward, two pixels per lane).  Warp w's block starts at
+// ((w & 1) * 8, (w >> 1) * kBlockH).
+template <int kBlockH = 4>
 __device__ __forceinline__ uint32_t warp_cover_mask(float4 r0, float4 r1, float tile_x0, float tile_y0) {
+  constexpr int kWarps = 2 * (kTile / kBlockH);
+  constexpr uint32_t kAll = (1u << kWarps) - 1u;
   const float alpha = r0.z;
   if (alpha < kAlphaEps * (1.0f - 1e-5f)) return 0u;
   const float tau = fmaxf(__logf(255.0f * alpha), 0.0f) * 1.0001f + 1e-4f;
   const float det = r1.x * r1.z - r1.y * r1.y;
-  if (!(det > 0.0f)) return 0xffu;  // degenerate conic: never cull
+  if (!(det > 0.0f)) return kAll;  // degenerate conic: never cull
   const float inv = 2.0f * tau / det;
   const float hx = sqrtf(inv * r1.z) * 1.001f + 0.05f;
   const float hy = sqrtf(inv * r1.x) * 1.001f + 0.05f;
   const float mx = r0.x + r0.w, my = r0.y + r1.w;
   uint32_t m = 0u;
 #pragma unroll
-  for (int w = 0; w < 8; ++w) {
-    const float x0 = tile_x0 + float((w & 1) * 8) + 0.5f, y0 = tile_y0 + float((w >> 1) * 4) + 0.5f;
-    if (mx + hx >= x0 && mx - hx <= x0 + 7.0f && my + hy >= y0 && my - hy <= y0 + 3.0f) m |= 1u << w;
+  for (int w = 0; w < kWarps; ++w) {
+    const float x0 = tile_x0 + float((w & 1) * 8) + 0.5f, y0 = tile_y0 + float((w >> 1) * kBlockH) + 0.5f;
+    if (mx + hx >= x0 && mx - hx <= x0 + 7.0f && my + hy >= y0 && my - hy <= y0 + float(kBlockH - 1)) m |= 1u << w;
   }
   return m;
 }
@@ -270,6 +276,11 @@ __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src)
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem_dst)), "l"(gmem_src) : "memory");
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int kPending>
+__device__ __forceinline__ void cp_async_wait_group() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(kPending) : "memory");
+}
 __device__ __forceinline__ int ld_volatile(const int* p) { return *reinterpret_cast<const volatile int*>(p); }
 
 // ---------------------------------------------------------------------------

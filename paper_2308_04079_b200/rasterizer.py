@@ -294,16 +294,18 @@ class _CapacityHint:
         self.k = {}
         self.ratio = {}
 
+    HEADROOM = 1.05   # the async tile sort runs over the whole capacity: keep the padding small
+
     def get(self, device, n: int | None = None) -> int:
         key = str(device)
         k = self.k.get(key, 1 << 16)
         if n is not None and key in self.ratio:
-            k = max(k, int(self.ratio[key] * n * 1.15) + 1024)
+            k = max(k, int(self.ratio[key] * n * self.HEADROOM) + 4096)
         return k
 
     def update(self, device, k: int, n: int | None = None) -> None:
         key = str(device)
-        self.k[key] = max(self.k.get(key, 1 << 16), int(k * 1.15) + 1024)
+        self.k[key] = max(self.k.get(key, 1 << 16), int(k * self.HEADROOM) + 4096)
         if n:
             self.ratio[key] = max(self.ratio.get(key, 0.0), k / n)
 
