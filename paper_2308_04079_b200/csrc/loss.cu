@@ -6,7 +6,7 @@
 // Two tiled passes over 16x16 output tiles with a 5-pixel halo staged in
 // shared memory:
 //   pass 1: the five filtered moments (mu_x, mu_y, E[x^2], E[y^2], E[xy]) in
-//           float64, the SSIM value, the three adjoint source maps
+//           shifted float32, the SSIM value (float64), the three adjoint source maps
 //           (d_mu_x, d_E[x^2], d_E[xy]) and block partial sums of SSIM and |x-y|;
 //   pass 2: the adjoint filter of the source maps (the symmetric, zero-padded
 //           filter is self-adjoint, ssim.py:24-31) plus the L1 sign term.
@@ -25,6 +25,8 @@ constexpr double kC2 = 0.03 * 0.03;
 struct Window {
   float w[11];
   double wd[11];
+  float rowsum;   // sum of the 11 float32 taps
+  double total;   // (sum of the float32 taps)^2: the 2-D filter's mass
 };
 
 __host__ Window make_window() {
@@ -35,10 +37,16 @@ __host__ Window make_window() {
     v[i] = exp(-(x * x) / (2.0 * 1.5 * 1.5));
     s += v[i];
   }
+  double fs = 0.0;
+  float rs = 0.0f;
   for (int i = 0; i < 11; ++i) {
     W.wd[i] = v[i] / s;
     W.w[i] = float(W.wd[i]);
+    fs += double(W.w[i]);
+    rs += W.w[i];
   }
+  W.rowsum = rs;
+  W.total = fs * fs;
   return W;
 }
 
@@ -55,12 +63,25 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
 }
 
 // pass 1 -------------------------------------------------------------------
+// The five filtered moments are accumulated in float32 on values shifted by
+// kShift (sigma^2 and the covariance are shift-invariant; mu is shifted back
+// exactly): |x - 0.5| <= 0.5 for images in [0, 1] keeps the E[x^2] - mu^2
+// cancellation error near 1e-7 absolute, four orders below the SSIM
+// constant C2 = 9e-4 that every variance is added to.  Zero padding is
+// staged as the shifted value of 0.  The per-pixel SSIM value and its
+// adjoint are formed in float64.  Register blocking: every thread filters
+// kRun consecutive outputs from one register window (horizontal pass over
+// all three channels at once, then vertical runs of kRun rows).
+constexpr float kShift = 0.5f;
+constexpr int kRun = 4;
+constexpr int kWin = kRun + 10;
+
 __global__ void __launch_bounds__(256)
 ssim_forward_kernel(const float* __restrict__ img, const float* __restrict__ gt, int W, int H, Window win,
                     double d_map, float* __restrict__ src, double* __restrict__ sums) {
-  __shared__ float s_x[kIn][kIn][3];
-  __shared__ float s_y[kIn][kIn][3];
-  __shared__ double s_h[kIn][kT][5];   // horizontal pass of one channel: 5 moments
+  __shared__ float s_x[3][kIn][kIn + 1];
+  __shared__ float s_y[3][kIn][kIn + 1];
+  __shared__ float s_h[3][5][kIn][kT + 1];   // horizontal pass: channel, moment, row, col
   __shared__ double s_red[8];
   const int t = threadIdx.x;
   const int ox = blockIdx.x * kT, oy = blockIdx.y * kT;
@@ -71,58 +92,89 @@ ssim_forward_kernel(const float* __restrict__ img, const float* __restrict__ gt,
     const size_t p = in ? (size_t(gy) * W + gx) * 3 : 0;
 #pragma unroll
     for (int ch = 0; ch < 3; ++ch) {
-      s_x[r][c][ch] = in ? img[p + ch] : 0.0f;
-      s_y[r][c][ch] = in ? gt[p + ch] : 0.0f;
+      s_x[ch][r][c] = (in ? img[p + ch] : 0.0f) - kShift;
+      s_y[ch][r][c] = (in ? gt[p + ch] : 0.0f) - kShift;
     }
   }
-  const int lx = t % kT, ly = t / kT;
-  const int gx = ox + lx, gy = oy + ly;
-  const bool inside = gx < W && gy < H;
-  const size_t p = inside ? size_t(gy) * W + gx : 0;
-  double ssim_sum = 0.0, l1_sum = 0.0, sq_sum = 0.0;
-  for (int ch = 0; ch < 3; ++ch) {
-    __syncthreads();
-    for (int i = t; i < kIn * kT; i += 256) {
-      const int r = i / kT, c = i % kT;
-      double a = 0, b = 0, xx = 0, yy = 0, xy = 0;
+  __syncthreads();
+  // horizontal: item = (channel, row, run of kRun output columns)
+  constexpr int kRunsX = kT / kRun;
+  for (int i = t; i < 3 * kIn * kRunsX; i += 256) {
+    const int ch = i / (kIn * kRunsX), rem = i - ch * (kIn * kRunsX);
+    const int r = rem / kRunsX, c0 = (rem - r * kRunsX) * kRun;
+    float x[kWin], y[kWin];
+#pragma unroll
+    for (int k = 0; k < kWin; ++k) {
+      x[k] = s_x[ch][r][c0 + k];
+      y[k] = s_y[ch][r][c0 + k];
+    }
+#pragma unroll
+    for (int o = 0; o < kRun; ++o) {
+      float a = 0.f, b = 0.f, xx = 0.f, yy = 0.f, xy = 0.f;
 #pragma unroll
       for (int k = 0; k < 11; ++k) {
-        const double x = s_x[r][c + k][ch], y = s_y[r][c + k][ch], w = win.wd[k];
-        a += w * x;
-        b += w * y;
-        xx += w * x * x;
-        yy += w * y * y;
-        xy += w * x * y;
+        const float w = win.w[k], xv = x[o + k], yv = y[o + k];
+        const float wx = w * xv, wy = w * yv;
+        a += wx;
+        b += wy;
+        xx = fmaf(wx, xv, xx);
+        yy = fmaf(wy, yv, yy);
+        xy = fmaf(wx, yv, xy);
       }
-      s_h[r][c][0] = a;
-      s_h[r][c][1] = b;
-      s_h[r][c][2] = xx;
-      s_h[r][c][3] = yy;
-      s_h[r][c][4] = xy;
+      s_h[ch][0][r][c0 + o] = a;
+      s_h[ch][1][r][c0 + o] = b;
+      s_h[ch][2][r][c0 + o] = xx;
+      s_h[ch][3][r][c0 + o] = yy;
+      s_h[ch][4][r][c0 + o] = xy;
     }
-    __syncthreads();
-    if (inside) {
-      double m[5] = {0, 0, 0, 0, 0};
+  }
+  __syncthreads();
+  // vertical: item = (channel, column, run of kRun output rows)
+  double ssim_sum = 0.0, l1_sum = 0.0, sq_sum = 0.0;
+  constexpr int kRunsY = kT / kRun;
+  if (t < 3 * kT * kRunsY) {
+    const int ch = t / (kT * kRunsY), rem = t - ch * (kT * kRunsY);
+    const int c = rem % kT, r0 = (rem / kT) * kRun;
+    float m[kRun][5];
 #pragma unroll
-      for (int k = 0; k < 11; ++k)
+    for (int j = 0; j < 5; ++j) {
+      float v[kWin];
 #pragma unroll
-        for (int j = 0; j < 5; ++j) m[j] += win.wd[k] * s_h[ly + k][lx][j];
-      const double mu_x = m[0], mu_y = m[1];
-      const double sx = m[2] - mu_x * mu_x, sy = m[3] - mu_y * mu_y, sxy = m[4] - mu_x * mu_y;
-      const double a1 = 2.0 * mu_x * mu_y + kC1, a2 = 2.0 * sxy + kC2;
-      const double b1 = mu_x * mu_x + mu_y * mu_y + kC1, b2 = sx + sy + kC2;
-      ssim_sum += (a1 * a2) / (b1 * b2);
-      // ssim_backward (ssim.py:67-84) with a constant d_map
-      const double denom = b1 * b2;
-      const double d_a1 = d_map * a2 / denom, d_a2 = d_map * a1 / denom;
-      const double d_b1 = -d_a1 * (a1 / b1), d_b2 = -d_a2 * (a2 / b2);
-      const double d_mu = 2.0 * mu_y * d_a1 + 2.0 * mu_x * d_b1 - 2.0 * mu_y * d_a2 - 2.0 * mu_x * d_b2;
-      src[9 * p + 3 * 0 + ch] = float(d_mu);
-      src[9 * p + 3 * 1 + ch] = float(d_b2);
-      src[9 * p + 3 * 2 + ch] = float(2.0 * d_a2);
-      const double diff = double(s_x[ly + kR][lx + kR][ch]) - double(s_y[ly + kR][lx + kR][ch]);
-      l1_sum += fabs(diff);
-      sq_sum += diff * diff;   // for the step's PSNR (optimizer.py:257-259)
+      for (int k = 0; k < kWin; ++k) v[k] = s_h[ch][j][r0 + k][c];
+#pragma unroll
+      for (int o = 0; o < kRun; ++o) {
+        float acc = 0.f;
+#pragma unroll
+        for (int k = 0; k < 11; ++k) acc = fmaf(win.w[k], v[o + k], acc);
+        m[o][j] = acc;
+      }
+    }
+    const int gx = ox + c;
+#pragma unroll
+    for (int o = 0; o < kRun; ++o) {
+      const int gy = oy + r0 + o;
+      if (gx < W && gy < H) {
+        const size_t p = size_t(gy) * W + gx;
+        // moments of the shifted values: sigma^2 / covariance directly, means shifted back
+        const double msx = m[o][0], msy = m[o][1];
+        const double sx = double(m[o][2]) - msx * msx, sy = double(m[o][3]) - msy * msy;
+        const double sxy = double(m[o][4]) - msx * msy;
+        const double mu_x = msx + double(kShift) * win.total, mu_y = msy + double(kShift) * win.total;
+        const double a1 = 2.0 * mu_x * mu_y + kC1, a2 = 2.0 * sxy + kC2;
+        const double b1 = mu_x * mu_x + mu_y * mu_y + kC1, b2 = sx + sy + kC2;
+        ssim_sum += (a1 * a2) / (b1 * b2);
+        // ssim_backward (ssim.py:67-84) with a constant d_map
+        const double denom = b1 * b2;
+        const double d_a1 = d_map * a2 / denom, d_a2 = d_map * a1 / denom;
+        const double d_b1 = -d_a1 * (a1 / b1), d_b2 = -d_a2 * (a2 / b2);
+        const double d_mu = 2.0 * mu_y * d_a1 + 2.0 * mu_x * d_b1 - 2.0 * mu_y * d_a2 - 2.0 * mu_x * d_b2;
+        src[9 * p + 3 * 0 + ch] = float(d_mu);
+        src[9 * p + 3 * 1 + ch] = float(d_b2);
+        src[9 * p + 3 * 2 + ch] = float(2.0 * d_a2);
+        const double diff = double(img[3 * p + ch]) - double(gt[3 * p + ch]);
+        l1_sum += fabs(diff);
+        sq_sum += diff * diff;   // for the step's PSNR (optimizer.py:257-259)
+      }
     }
   }
   const double s1 = block_sum(ssim_sum, s_red);
@@ -136,11 +188,14 @@ ssim_forward_kernel(const float* __restrict__ img, const float* __restrict__ gt,
 }
 
 // pass 2 -------------------------------------------------------------------
+// Same register blocking: horizontal runs over the nine source maps, then
+// vertical runs of kRun rows per (channel, column) that combine the three
+// filtered maps of the channel with the L1 sign term.
 __global__ void __launch_bounds__(256)
 ssim_backward_kernel(const float* __restrict__ img, const float* __restrict__ gt, const float* __restrict__ src,
                      int W, int H, Window win, float l1_scale, float* __restrict__ d_image) {
-  __shared__ float s_s[kIn][kIn][9];
-  __shared__ float s_h[kIn][kT][9];
+  __shared__ float s_s[9][kIn][kIn + 1];
+  __shared__ float s_h[9][kIn][kT + 1];
   const int t = threadIdx.x;
   const int ox = blockIdx.x * kT, oy = blockIdx.y * kT;
   for (int i = t; i < kIn * kIn; i += 256) {
@@ -149,35 +204,54 @@ ssim_backward_kernel(const float* __restrict__ img, const float* __restrict__ gt
     const bool in = gx >= 0 && gx < W && gy >= 0 && gy < H;
     const size_t p = in ? (size_t(gy) * W + gx) * 9 : 0;
 #pragma unroll
-    for (int j = 0; j < 9; ++j) s_s[r][c][j] = in ? src[p + j] : 0.0f;
+    for (int j = 0; j < 9; ++j) s_s[j][r][c] = in ? src[p + j] : 0.0f;
   }
   __syncthreads();
-  for (int i = t; i < kIn * kT; i += 256) {
-    const int r = i / kT, c = i % kT;
+  constexpr int kRunsX = kT / kRun;
+  for (int i = t; i < 9 * kIn * kRunsX; i += 256) {
+    const int j = i / (kIn * kRunsX), rem = i - j * (kIn * kRunsX);
+    const int r = rem / kRunsX, c0 = (rem - r * kRunsX) * kRun;
+    float v[kWin];
 #pragma unroll
-    for (int j = 0; j < 9; ++j) {
-      float a = 0.0f;
+    for (int k = 0; k < kWin; ++k) v[k] = s_s[j][r][c0 + k];
 #pragma unroll
-      for (int k = 0; k < 11; ++k) a = fmaf(win.w[k], s_s[r][c + k][j], a);
-      s_h[r][c][j] = a;
+    for (int o = 0; o < kRun; ++o) {
+      float acc = 0.f;
+#pragma unroll
+      for (int k = 0; k < 11; ++k) acc = fmaf(win.w[k], v[o + k], acc);
+      s_h[j][r][c0 + o] = acc;
     }
   }
   __syncthreads();
-  const int lx = t % kT, ly = t / kT;
-  const int gx = ox + lx, gy = oy + ly;
-  if (gx >= W || gy >= H) return;
-  const size_t p = size_t(gy) * W + gx;
+  constexpr int kRunsY = kT / kRun;
+  if (t >= 3 * kT * kRunsY) return;
+  const int ch = t / (kT * kRunsY), rem = t - ch * (kT * kRunsY);
+  const int c = rem % kT, r0 = (rem / kT) * kRun;
+  float f[3][kRun];
 #pragma unroll
-  for (int ch = 0; ch < 3; ++ch) {
-    float f[3] = {0.f, 0.f, 0.f};
+  for (int m = 0; m < 3; ++m) {
+    float v[kWin];
 #pragma unroll
-    for (int k = 0; k < 11; ++k)
+    for (int k = 0; k < kWin; ++k) v[k] = s_h[3 * m + ch][r0 + k][c];
 #pragma unroll
-      for (int m = 0; m < 3; ++m) f[m] = fmaf(win.w[k], s_h[ly + k][lx][3 * m + ch], f[m]);
-    const float x = img[3 * p + ch], y = gt[3 * p + ch];
-    const float diff = x - y;
-    const float sgn = diff > 0.f ? 1.f : (diff < 0.f ? -1.f : 0.f);  // np.sign
-    d_image[3 * p + ch] = sgn * l1_scale + f[0] + 2.0f * x * f[1] + y * f[2];
+    for (int o = 0; o < kRun; ++o) {
+      float acc = 0.f;
+#pragma unroll
+      for (int k = 0; k < 11; ++k) acc = fmaf(win.w[k], v[o + k], acc);
+      f[m][o] = acc;
+    }
+  }
+  const int gx = ox + c;
+#pragma unroll
+  for (int o = 0; o < kRun; ++o) {
+    const int gy = oy + r0 + o;
+    if (gx < W && gy < H) {
+      const size_t p = size_t(gy) * W + gx;
+      const float x = img[3 * p + ch], y = gt[3 * p + ch];
+      const float diff = x - y;
+      const float sgn = diff > 0.f ? 1.f : (diff < 0.f ? -1.f : 0.f);  // np.sign
+      d_image[3 * p + ch] = sgn * l1_scale + f[0][o] + 2.0f * x * f[1][o] + y * f[2][o];
+    }
   }
 }
 
