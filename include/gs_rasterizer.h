@@ -41,6 +41,10 @@ extern "C" {
 #define GS_SH_COEFFS 16        /* sh.py:25 NUM_COEFFS */
 #define GS_REC_FLOATS 16       /* floats per projected-splat record, see gs_splats_t */
 #define GS_GRAD2D_FLOATS 12    /* floats per screen-space gradient row, see gs_blend_backward */
+#define GS_MODEL_FLOATS 59     /* scene_io.py:374-376 model record (236 B) */
+#define GS_PLY_FLOATS 62       /* scene_io.py:417-439 PLY vertex */
+#define GS_LAYOUT_MODEL 0
+#define GS_LAYOUT_PLY 1
 
 enum gs_status {
   GS_OK = 0,
@@ -272,6 +276,16 @@ int gs_densify_apply(const gs_cloud_state_t* cloud, const gs_stats_t* stats, con
 int gs_loss_workspace_size(int32_t width, int32_t height, size_t* bytes);
 int gs_l1_dssim_loss(const float* image, const float* target, int32_t width, int32_t height, double lambda_dssim,
                      void* workspace, size_t workspace_bytes, float* loss_out, float* d_image, void* stream);
+
+/* ---- model / PLY records: replaces scene_io
+ * _records_from_cloud / _cloud_from_records (scene_io.py:377-391) and the
+ * export_ply vertex packing (scene_io.py:417-439).  `out` / `records` are
+ * DEVICE arrays of n x GS_MODEL_FLOATS (layout GS_LAYOUT_MODEL: mean,
+ * log_scale, rotation, opacity, SH channel-major) or n x GS_PLY_FLOATS
+ * (GS_LAYOUT_PLY: x y z, zero normals, f_dc, f_rest channel-major, opacity,
+ * scale, rot) little-endian float32, i.e. the file body byte for byte. */
+int gs_pack_records(const gs_params_t* params, int32_t layout, float* out, void* stream);
+int gs_unpack_records(const float* records, gs_params_t* params_out, void* stream);
 
 #ifdef __cplusplus
 }

@@ -22,6 +22,10 @@ GS_ERR_CAPACITY = 4
 GS_ERR_CUDA = 5
 
 REC_FLOATS = 16
+MODEL_FLOATS = 59
+PLY_FLOATS = 62
+LAYOUT_MODEL = 0
+LAYOUT_PLY = 1
 GRAD2D_FLOATS = 12
 
 
@@ -105,6 +109,8 @@ SIGNATURES = [
     ("gs_loss_workspace_size", c_int32, [c_int32, c_int32, POINTER(c_size_t)]),
     ("gs_l1_dssim_loss", c_int32, [c_void_p, c_void_p, c_int32, c_int32, c_double, c_void_p, c_size_t, c_void_p,
                                    c_void_p, c_void_p]),
+    ("gs_pack_records", c_int32, [POINTER(GsParams), c_int32, c_void_p, c_void_p]),
+    ("gs_unpack_records", c_int32, [c_void_p, POINTER(GsParams), c_void_p]),
     ("gs_adam_step", c_int32, [POINTER(GsAdamGroup), c_int32, c_double, c_double, c_double, c_double, c_double,
                                c_void_p]),
 ]
