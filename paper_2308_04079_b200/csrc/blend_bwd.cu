@@ -21,6 +21,9 @@
 namespace gs {
 namespace {
 
+#ifndef GS_WAIT_NS
+#define GS_WAIT_NS 2000
+#endif
 #ifndef GS_BWD_MIN_BLOCKS
 #define GS_BWD_MIN_BLOCKS 3  // 72 registers (small spill) beats 2 blocks at 96 (measured 1.69 vs 1.99 ms)
 #endif
@@ -168,7 +171,7 @@ blend_bwd_kernel(const float* __restrict__ d_image, const float4* __restrict__ r
     for (int b = 0; b < nb + kStages; ++b) {
       const int s = b % kStages;
       if (b >= kStages) {
-        while (!mbar_try_wait(&empty_bar[s], uint32_t((b / kStages) - 1) & 1u)) {
+        while (!mbar_try_wait_sleep(&empty_bar[s], uint32_t((b / kStages) - 1) & 1u, GS_WAIT_NS)) {
         }
         int plo, pcnt;
         batch_bounds(b - kStages, tile_top, range.x, plo, pcnt);
@@ -216,7 +219,7 @@ blend_bwd_kernel(const float* __restrict__ d_image, const float4* __restrict__ r
   float S = T * (dlx * bg.x + dly * bg.y + dlz * bg.z);
   for (int b = 0; b < nb; ++b) {
     const int s = b % kStages;
-    while (!mbar_try_wait(&full_bar[s], uint32_t(b / kStages) & 1u)) {
+    while (!mbar_try_wait_sleep(&full_bar[s], uint32_t(b / kStages) & 1u, GS_WAIT_NS)) {
     }
     int lo, cnt;
     batch_bounds(b, tile_top, range.x, lo, cnt);

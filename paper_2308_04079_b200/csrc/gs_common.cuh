@@ -272,10 +272,38 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
+// try_wait with a suspend-time hint: the waiting warp sleeps (up to
+// `hint_ns`, or until the phase completes) instead of spinning, so a waiting
+// producer or consumer does not steal issue slots from the warps that work.
+__device__ __forceinline__ bool mbar_try_wait_sleep(uint64_t* bar, uint32_t parity, uint32_t hint_ns) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity), "r"(hint_ns)
+      : "memory");
+  return ok != 0;
+}
 __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem_dst)), "l"(gmem_src) : "memory");
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+// Bulk L2 prefetch of a global span (TMA unit, no registers or shared
+// memory involved).  The span is trimmed to whole 16-byte units inside
+// [ptr, ptr + bytes) so it never touches memory outside the buffer.
+__device__ __forceinline__ void prefetch_l2_span(const void* ptr, size_t bytes) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(ptr);
+  const uintptr_t lo = (a + 15) & ~uintptr_t(15), hi = (a + bytes) & ~uintptr_t(15);
+  if (hi <= lo) return;
+  size_t n = hi - lo;
+  const char* q = reinterpret_cast<const char*>(lo);
+  while (n) {   // one bulk op moves < 2^32 bytes; keep each <= 1 MiB
+    const uint32_t chunk = uint32_t(n < (size_t(1) << 20) ? n : (size_t(1) << 20));
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(q), "r"(chunk) : "memory");
+    q += chunk;
+    n -= chunk;
+  }
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int kPending>
 __device__ __forceinline__ void cp_async_wait_group() {

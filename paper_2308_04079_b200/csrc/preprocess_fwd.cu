@@ -16,11 +16,18 @@ __device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a,
 
 __global__ void __launch_bounds__(128)
 preprocess_fwd_kernel(gs_params_t p, DevCamera cam, int degree, gs_splats_t out) {
-  __shared__ float4 s_sh[128 * kShStride];
   const int64_t g0 = int64_t(blockIdx.x) * blockDim.x;
   const int64_t g = g0 + threadIdx.x;
-  // this thread's parameter loads are issued first so their latency overlaps
-  // the block's SH staging
+  // The block's SH rows (one contiguous 192 B x 128 span) are bulk-prefetched
+  // into L2 by the TMA unit while the float64 geometry runs; the colour step
+  // then reads each thread's row from L2.  No shared-memory staging, no block
+  // barrier, and culled Gaussians never touch their SH bytes.
+  if (threadIdx.x == 0) {
+    const int64_t nbk = min(int64_t(blockDim.x), p.n - g0);
+    const int rows = (degree + 1) * (degree + 1);
+    // SH (N,16,3): the active rows of every Gaussian lie inside its 192-B record
+    prefetch_l2_span(p.sh + 48 * g0, size_t(48 * (nbk - 1) + 3 * rows) * sizeof(float));
+  }
   float pm0 = 0.f, pm1 = 0.f, pm2 = 0.f, pl0 = 0.f, pl1 = 0.f, pl2 = 0.f, pop = 0.f;
   float4 qf = make_float4(1.f, 0.f, 0.f, 0.f);
   if (g < p.n) {
@@ -30,8 +37,6 @@ preprocess_fwd_kernel(gs_params_t p, DevCamera cam, int degree, gs_splats_t out)
     pl2 = __ldg(p.log_scales + 3 * g + 2);
     pop = __ldg(p.opacity_logits + g);
   }
-  stage_sh_rows(p.sh, p.n, g0, s_sh);
-  __syncthreads();
   if (g >= p.n) return;
 
   // view = means @ W^T + t (core.py:279)
@@ -154,9 +159,10 @@ preprocess_fwd_kernel(gs_params_t p, DevCamera cam, int degree, gs_splats_t out)
   sh_basis(vx, vy, vz, degree, b);
   const int nrows = (degree + 1) * (degree + 1);
   float shv[48];
+  const float4* shrow = reinterpret_cast<const float4*>(p.sh) + 12 * g;
 #pragma unroll
   for (int k = 0; k < 12; ++k) {
-    const float4 q4 = s_sh[threadIdx.x * kShStride + k];
+    const float4 q4 = (4 * k < 3 * nrows) ? __ldg(shrow + k) : make_float4(0.f, 0.f, 0.f, 0.f);
     shv[4 * k + 0] = q4.x; shv[4 * k + 1] = q4.y; shv[4 * k + 2] = q4.z; shv[4 * k + 3] = q4.w;
   }
   float col[3] = {0.0f, 0.0f, 0.0f};

@@ -1,0 +1,184 @@
+"""Measurements for BASELINE.json's other configurations (bench.py measures
+configs[2], "c3"):
+
+  c2  synthetic 1M Gaussians, SH3, one 1080p camera, forward-only render
+  c4  3M Gaussians (SURVEY §8(d) ball cloud), a batch of 32 1080p look-at
+      cameras per training step (fwd + L1/D-SSIM + bwd accumulated over the
+      batch, one Adam step per batch) -- single-GPU form of the multi-view
+      config; under torchrun the batch is sharded over the ranks and the
+      gradients all-reduced (distributed.train_step_views)
+  c5  stress: 6M Gaussians at 3840x2160, fwd + bwd + Adam per step with
+      densify/prune every 100 iterations (training.train_step +
+      densify.densify_and_prune)
+
+Same timing rules as bench.py: warm-up, CUDA events around the timed steps,
+synchronize on both sides, NVML clocks sampled during the timed region.
+
+    python tools/bench_configs.py [--configs c2,c4,c5] [--out profiles/r1_configs.jsonl]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+
+
+def timed(fn, steps: int, warmup: int):
+    import torch
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(steps):
+        fn()
+    e.record()
+    torch.cuda.synchronize()
+    return s.elapsed_time(e) / steps
+
+
+def clocks_during(fn):
+    from bench import ClockSampler
+    c = ClockSampler(0)
+    c.start()
+    out = fn()
+    return out, c.stop()
+
+
+def run_c2(args) -> dict:
+    import torch
+    from paper_2308_04079_b200 import rasterizer as R
+    from paper_2308_04079_b200 import synthetic
+    from paper_2308_04079_b200.cloud import GaussianCloud
+    cloud_np, cam = synthetic.frustum_scene(1_000_000, 1920, 1080, seed=0)
+    cloud = GaussianCloud.from_numpy(**cloud_np)
+    bg = (0.0, 0.0, 0.0)
+    R.bin_and_sort(R.project(cloud, cam, 3), 1920, 1080)   # size the instance buffers
+    ms_async, clk = clocks_during(lambda: timed(lambda: R.render_view_async(cloud, cam, bg, 3), args.steps, 5))
+    ms_sync = timed(lambda: R.render_view(cloud, cam, bg, 3), args.steps, 5)
+    out, _, b = R.render_view(cloud, cam, bg, 3)
+    torch.cuda.synchronize()
+    return {"config": "c2: 1M Gaussians SH3, 1920x1080, forward-only render", "metric": "render FPS",
+            "value": round(1e3 / ms_async, 1), "unit": "frames/s", "ms_per_frame": round(ms_async, 4),
+            "render_view_sync_fps": round(1e3 / ms_sync, 1), "instances": b.num_instances,
+            "note": "value: render_view_async (no host sync, graph-capturable); render_view_sync_fps: the "
+                    "reference-shaped render_view (one host sync to read K)", "clocks": clk}
+
+
+def run_c4(args) -> dict:
+    import torch
+    from paper_2308_04079_b200 import rasterizer as R
+    from paper_2308_04079_b200 import synthetic
+    from paper_2308_04079_b200.cloud import GaussianCloud
+    from paper_2308_04079_b200.distributed import GradientBucket
+    from paper_2308_04079_b200.loss import l1_dssim_loss
+    from paper_2308_04079_b200.optimizer import DeviceAdam, TrainConfig
+    n, views = 3_000_000, 32
+    cloud = GaussianCloud.from_numpy(**synthetic.ball_scene(n, seed=0))
+    target_cloud = GaussianCloud.from_numpy(**synthetic.ball_scene(n, seed=1))
+    cams = synthetic.ball_cameras(views, 1920, 1080)
+    bg = (0.0, 0.0, 0.0)
+    with torch.no_grad():
+        targets = [R.render_view(target_cloud, c, bg, 3)[0].image for c in cams]
+    del target_cloud
+    adam = DeviceAdam(cloud)
+    bucket = GradientBucket(n, cloud.device)
+    stats = R.DensifyStats.zeros(n, cloud.device)
+    config = TrainConfig()
+    it = [0]
+    k_infos = []
+
+    def step():
+        it[0] += 1
+        bucket.zero_()
+        for cam, gt in zip(cams, targets):
+            out, splats, binning = R.render_view_async(cloud, cam, bg, 3, training=True)
+            k_infos.append(binning.k_info)
+            loss, d_image = l1_dssim_loss(out.image, gt, config.lambda_dssim)
+            g2 = R.render_backward(d_image, out, splats, binning, 1920, 1080, bg)
+            R.backward_project(cloud, cam, splats, g2, 3, stats=stats, out=bucket.grads, accumulate=True)
+        bucket.allreduce_()
+        adam.step(cloud, bucket.grads, it[0], config)
+
+    for cam in cams:   # size the instance buffers for every view
+        R.bin_and_sort(R.project(cloud, cam, 3), 1920, 1080)
+    ms, clk = clocks_during(lambda: timed(step, max(2, args.steps // 10), 1))
+    flags = torch.stack(k_infos)[:, 1]
+    assert not bool((flags != 0).any()), "binning overflow"
+    return {"config": "c4: 3M Gaussians (ball cloud) SH3, batch of 32 1920x1080 views per step, 1 GPU",
+            "metric": "train batch iters/s", "value": round(1e3 / ms, 3), "unit": "batches/s",
+            "views_per_s": round(views * 1e3 / ms, 1), "ms_per_batch": round(ms, 2), "clocks": clk}
+
+
+def run_c5(args) -> dict:
+    import torch
+    from paper_2308_04079_b200 import rasterizer as R
+    from paper_2308_04079_b200 import synthetic
+    from paper_2308_04079_b200.cloud import GaussianCloud
+    from paper_2308_04079_b200.densify import TrainState, densify_and_prune
+    from paper_2308_04079_b200.optimizer import TrainConfig
+    from paper_2308_04079_b200.training import TrainView, train_step
+    n, w, h = 6_000_000, 3840, 2160
+    cloud_np, cam = synthetic.frustum_scene(n, w, h, seed=0)
+    cloud = GaussianCloud.from_numpy(**cloud_np)
+    del cloud_np
+    tgt_np, _ = synthetic.frustum_scene(n, w, h, seed=1)
+    with torch.no_grad():
+        target = R.render_view(GaussianCloud.from_numpy(**tgt_np), cam, (0, 0, 0), 3)[0].image
+    del tgt_np
+    state = TrainState(cloud, scene_extent=20.0, seed=0)
+    state.active_sh_degree = 3
+    config = TrainConfig(warmup_upsample_iters=(0, 0), sh_band_interval=10**9, densify_start=0,
+                         densify_interval=100, densify_until=10**9, total_iters=30000)
+    views = [TrainView(cam, target)]
+    reports = []
+
+    def step():
+        train_step(state, views, config)
+        if state.iteration % config.densify_interval == 0:
+            reports.append(densify_and_prune(state, config))
+
+    for _ in range(5):
+        train_step(state, views, config)
+    state.iteration = 0
+    steps = 200
+    n0 = len(state.cloud)
+    ms, clk = clocks_during(lambda: timed(step, steps, 0))
+    return {"config": "c5: 6M Gaussians SH3, 3840x2160, fwd+bwd+Adam, densify/prune every 100 iterations",
+            "metric": "train iters/s", "value": round(1e3 / ms, 2), "unit": "train_iters/s",
+            "ms_per_step": round(ms, 3), "steps": steps, "gaussians_start": n0, "gaussians_end": len(state.cloud),
+            "densify_events": [r.__dict__ for r in reports], "clocks": clk,
+            "note": "timed region = 200 training steps including both densify/prune events"}
+
+
+def main() -> None:
+    import torch
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--configs", default="c2,c4,c5")
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--out", default=str(ROOT / "gpurun_out" / "configs.jsonl"))
+    args = ap.parse_args()
+    torch.cuda.set_device(0)
+    runners = {"c2": run_c2, "c4": run_c4, "c5": run_c5}
+    os.makedirs(os.path.dirname(args.out), exist_ok=True)
+    for name in args.configs.split(","):
+        t0 = time.time()
+        res = runners[name](args)
+        res["wall_s"] = round(time.time() - t0, 1)
+        line = json.dumps(res)
+        print(line, flush=True)
+        with open(args.out, "a") as f:
+            f.write(line + "\n")
+        torch.cuda.empty_cache()
+
+
+if __name__ == "__main__":
+    main()
