@@ -362,7 +362,8 @@ __device__ __forceinline__ float warp_sum(float v) {
 
 // ---------------------------------------------------------------------------
 // Geometry (float64).  Quaternion -> rotation (core.py:170-184).
-__device__ __forceinline__ void quat_to_rot(double r, double i, double j, double k, double R[9]) {
+template <typename Real>
+__device__ __forceinline__ void quat_to_rot(Real r, Real i, Real j, Real k, Real R[9]) {
   R[0] = 1.0 - 2.0 * (j * j + k * k);
   R[1] = 2.0 * (i * j - r * k);
   R[2] = 2.0 * (i * k + r * j);

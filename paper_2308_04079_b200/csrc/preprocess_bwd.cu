@@ -5,9 +5,9 @@
 // optimizer.train_step (optimizer.py:252-255).
 //
 // One thread per Gaussian.  Nothing from the forward's geometry is cached:
-// the view position, J, U = JW, Sigma and the conic are recomputed in
-// float64 from the parameters (cheaper in HBM bytes than storing the
-// reference's 40-float backward cache per splat).  The SH path reuses the
+// the view position, J, U = JW, Sigma and the conic are recomputed from the
+// parameters (cheaper in HBM bytes than storing the reference's 40-float
+// backward cache per splat); precision per stage: see GS_BWD_REAL.  The SH path reuses the
 // forward's float32 basis and the stored clamp mask.
 #include "gs_common.cuh"
 
@@ -56,39 +56,53 @@ __device__ __forceinline__ void zero_grads(GradOut& o) {
   o.norm = 0.0f;
 }
 
-__device__ __forceinline__ void grad_one(const GradInputs& in, const DevCamera& cam, int degree,
+template <typename Real>
+__device__ __forceinline__ void grad_one_t(const GradInputs& in, const DevCamera& cam, int degree,
                                          const float4* shrow, GradOut& o, float (&b)[16], float (&dcol)[3]) {
+  Real cR[9], ct[3], ccen[3];
+#pragma unroll
+  for (int k = 0; k < 9; ++k) cR[k] = Real(cam.R[k]);
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    ct[k] = Real(cam.t[k]);
+    ccen[k] = Real(cam.center[k]);
+  }
+  const Real cfx = Real(cam.fx), cfy = Real(cam.fy);
   const float4 ga = in.ga, gb = in.gb, gc = in.gc;
   const int mask = int(in.mask);
 
   // --- opacity through the sigmoid (gradients.py:217)
-  const double alpha = 1.0 / (1.0 + exp(-double(in.op)));
-  const float d_logit = float(double(ga.z) * alpha * (1.0 - alpha));
+  const Real alpha = Real(1.0) / (Real(1.0) + exp(-Real(in.op)));
+  const float d_logit = float(Real(ga.z) * alpha * (Real(1.0) - alpha));
 
   // --- view position, Jacobian, U = J W (core.py:279, 298-303)
-  const double mx = in.m0, my = in.m1, mz = in.m2;
-  double view[3];
+  const Real mx = in.m0, my = in.m1, mz = in.m2;
+  Real view[3];
 #pragma unroll
   for (int i = 0; i < 3; ++i)
-    view[i] = mx * cam.R[3 * i + 0] + my * cam.R[3 * i + 1] + mz * cam.R[3 * i + 2] + cam.t[i];
-  const double x = view[0], y = view[1], z = view[2];
-  const double z2 = z * z, z3 = z2 * z;
-  const double j00 = cam.fx / z, j02 = -cam.fx * x / z2, j11 = cam.fy / z, j12 = -cam.fy * y / z2;
-  double U[6];
+    view[i] = mx * cR[3 * i + 0] + my * cR[3 * i + 1] + mz * cR[3 * i + 2] + ct[i];
+  const Real x = view[0], y = view[1], z = view[2];
+  const Real z2 = z * z, z3 = z2 * z;
+  const Real j00 = cfx / z, j02 = -cfx * x / z2, j11 = cfy / z, j12 = -cfy * y / z2;
+  Real U[6];
 #pragma unroll
   for (int c = 0; c < 3; ++c) {
-    U[c] = j00 * cam.R[c] + j02 * cam.R[6 + c];
-    U[3 + c] = j11 * cam.R[3 + c] + j12 * cam.R[6 + c];
+    U[c] = j00 * cR[c] + j02 * cR[6 + c];
+    U[3 + c] = j11 * cR[3 + c] + j12 * cR[6 + c];
   }
 
-  // --- covariance from the raw quaternion and log scales (core.py:187-201)
+  // --- covariance from the raw quaternion and log scales (core.py:187-201),
+  //     always float64: the rotation gradient below relies on R R^T = I and
+  //     a symmetric dSigma to cancel (exactly 0 for isotropic Gaussians)
+  using Cov = double;
   const float4 qf = in.q;
-  const double qn = sqrt(double(qf.x) * qf.x + double(qf.y) * qf.y + double(qf.z) * qf.z + double(qf.w) * qf.w);
-  const double q[4] = {qf.x / qn, qf.y / qn, qf.z / qn, qf.w / qn};
-  double R[9];
+  const Cov qn = sqrt(Cov(qf.x) * qf.x + Cov(qf.y) * qf.y + Cov(qf.z) * qf.z + Cov(qf.w) * qf.w);
+  const Cov q[4] = {qf.x / qn, qf.y / qn, qf.z / qn, qf.w / qn};
+  Cov R[9];
   quat_to_rot(q[0], q[1], q[2], q[3], R);
-  const double s[3] = {exp(double(in.l0)), exp(double(in.l1)), exp(double(in.l2))};
-  double M[9], S[9];
+  const Cov s[3] = {exp(Cov(in.l0)), exp(Cov(in.l1)), exp(Cov(in.l2))};
+  Cov M[9];
+  Real S[9];
 #pragma unroll
   for (int i = 0; i < 3; ++i)
 #pragma unroll
@@ -97,94 +111,99 @@ __device__ __forceinline__ void grad_one(const GradInputs& in, const DevCamera& 
   for (int i = 0; i < 3; ++i)
 #pragma unroll
     for (int k = 0; k < 3; ++k)
-      S[3 * i + k] = M[3 * i + 0] * M[3 * k + 0] + M[3 * i + 1] * M[3 * k + 1] + M[3 * i + 2] * M[3 * k + 2];
-  double US[6];
+      S[3 * i + k] = Real(M[3 * i + 0] * M[3 * k + 0] + M[3 * i + 1] * M[3 * k + 1] + M[3 * i + 2] * M[3 * k + 2]);
+  Real US[6];
 #pragma unroll
   for (int r = 0; r < 2; ++r)
 #pragma unroll
     for (int k = 0; k < 3; ++k) US[3 * r + k] = U[3 * r + 0] * S[k] + U[3 * r + 1] * S[3 + k] + U[3 * r + 2] * S[6 + k];
-  const double ca = US[0] * U[0] + US[1] * U[1] + US[2] * U[2] + kLowpass;
-  const double cb = US[0] * U[3] + US[1] * U[4] + US[2] * U[5];
-  const double cc = US[3] * U[3] + US[4] * U[4] + US[5] * U[5] + kLowpass;
-  const double det = ca * cc - cb * cb;
-  const double A0 = cc / det, A1 = -cb / det, A2 = ca / det;  // conic (core.py:316)
+  const Real ca = US[0] * U[0] + US[1] * U[1] + US[2] * U[2] + Real(kLowpass);
+  const Real cb = US[0] * U[3] + US[1] * U[4] + US[2] * U[5];
+  const Real cc = US[3] * U[3] + US[4] * U[4] + US[5] * U[5] + Real(kLowpass);
+  const Real det = ca * cc - cb * cb;
+  const Real A0 = cc / det, A1 = -cb / det, A2 = ca / det;  // conic (core.py:316)
 
   // --- conic -> floored screen covariance: dS' = -A G A (gradients.py:97-113)
-  const double G0 = gb.x, G1 = 0.5 * double(gb.y), G2 = gb.z;
-  const double AG00 = A0 * G0 + A1 * G1, AG01 = A0 * G1 + A1 * G2;
-  const double AG10 = A1 * G0 + A2 * G1, AG11 = A1 * G1 + A2 * G2;
-  const double dC00 = -(AG00 * A0 + AG01 * A1);
-  const double dC01 = -(AG00 * A1 + AG01 * A2);
-  const double dC10 = -(AG10 * A0 + AG11 * A1);
-  const double dC11 = -(AG10 * A1 + AG11 * A2);
+  const Real G0 = gb.x, G1 = Real(0.5) * Real(gb.y), G2 = gb.z;
+  const Real AG00 = A0 * G0 + A1 * G1, AG01 = A0 * G1 + A1 * G2;
+  const Real AG10 = A1 * G0 + A2 * G1, AG11 = A1 * G1 + A2 * G2;
+  const Real dC00 = -(AG00 * A0 + AG01 * A1);
+  const Real dC01 = -(AG00 * A1 + AG01 * A2);
+  const Real dC10 = -(AG10 * A0 + AG11 * A1);
+  const Real dC11 = -(AG10 * A1 + AG11 * A2);
 
   // --- screen covariance -> world covariance: dSigma = U^T dS' U (gradients.py:116-123)
-  double dCU[6];  // dS' U  (2x3)
+  Real dCU[6];  // dS' U  (2x3)
 #pragma unroll
   for (int c = 0; c < 3; ++c) {
     dCU[c] = dC00 * U[c] + dC01 * U[3 + c];
     dCU[3 + c] = dC10 * U[c] + dC11 * U[3 + c];
   }
-  double dS[9];
+  Real dS[9];
 #pragma unroll
   for (int i = 0; i < 3; ++i)
 #pragma unroll
     for (int j = 0; j < 3; ++j) dS[3 * i + j] = U[i] * dCU[j] + U[3 + i] * dCU[3 + j];
 
-  // --- Sigma = M M^T -> log scales and raw quaternion (gradients.py:126-189)
-  double dM[9];
+  // --- Sigma = M M^T -> log scales and raw quaternion (gradients.py:126-189), float64
+  Cov dSs[9];  // symmetrised dSigma
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) dSs[3 * i + j] = Cov(0.5) * (Cov(dS[3 * i + j]) + Cov(dS[3 * j + i]));
+  Cov dM[9];
 #pragma unroll
   for (int i = 0; i < 3; ++i)
 #pragma unroll
     for (int k = 0; k < 3; ++k)
-      dM[3 * i + k] = 2.0 * (dS[3 * i + 0] * M[0 + k] + dS[3 * i + 1] * M[3 + k] + dS[3 * i + 2] * M[6 + k]);
-  double d_logs[3];
+      dM[3 * i + k] = Cov(2.0) * (dSs[3 * i + 0] * M[0 + k] + dSs[3 * i + 1] * M[3 + k] + dSs[3 * i + 2] * M[6 + k]);
+  Cov d_logs[3];
 #pragma unroll
   for (int k = 0; k < 3; ++k)
     d_logs[k] = (dM[k] * R[k] + dM[3 + k] * R[3 + k] + dM[6 + k] * R[6 + k]) * s[k];
   // dR = dM * diag(s); contract with dR/dq of quat_to_rot
-  double dR[9];
+  Cov dR[9];
 #pragma unroll
   for (int i = 0; i < 3; ++i)
 #pragma unroll
     for (int j = 0; j < 3; ++j) dR[3 * i + j] = dM[3 * i + j] * s[j];
-  const double qr = q[0], qi = q[1], qj = q[2], qk = q[3];
-  const double dqr = 2.0 * (-qk * dR[1] + qj * dR[2] + qk * dR[3] - qi * dR[5] - qj * dR[6] + qi * dR[7]);
-  const double dqi = 2.0 * (qj * dR[1] + qk * dR[2] + qj * dR[3] - 2.0 * qi * dR[4] - qr * dR[5] + qk * dR[6] +
-                            qr * dR[7] - 2.0 * qi * dR[8]);
-  const double dqj = 2.0 * (-2.0 * qj * dR[0] + qi * dR[1] + qr * dR[2] + qi * dR[3] + qk * dR[5] - qr * dR[6] +
-                            qk * dR[7] - 2.0 * qj * dR[8]);
-  const double dqk = 2.0 * (-2.0 * qk * dR[0] - qr * dR[1] + qi * dR[2] + qr * dR[3] - 2.0 * qk * dR[4] +
+  const Cov qr = q[0], qi = q[1], qj = q[2], qk = q[3];
+  const Cov dqr = Cov(2.0) * (-qk * dR[1] + qj * dR[2] + qk * dR[3] - qi * dR[5] - qj * dR[6] + qi * dR[7]);
+  const Cov dqi = Cov(2.0) * (qj * dR[1] + qk * dR[2] + qj * dR[3] - Cov(2.0) * qi * dR[4] - qr * dR[5] + qk * dR[6] +
+                            qr * dR[7] - Cov(2.0) * qi * dR[8]);
+  const Cov dqj = Cov(2.0) * (-Cov(2.0) * qj * dR[0] + qi * dR[1] + qr * dR[2] + qi * dR[3] + qk * dR[5] - qr * dR[6] +
+                            qk * dR[7] - Cov(2.0) * qj * dR[8]);
+  const Cov dqk = Cov(2.0) * (-Cov(2.0) * qk * dR[0] - qr * dR[1] + qi * dR[2] + qr * dR[3] - Cov(2.0) * qk * dR[4] +
                             qj * dR[5] + qi * dR[6] + qj * dR[7]);
-  const double qdot = qr * dqr + qi * dqi + qj * dqj + qk * dqk;
+  const Cov qdot = qr * dqr + qi * dqi + qj * dqj + qk * dqk;
   const float4 d_rot = make_float4(float((dqr - qr * qdot) / qn), float((dqi - qi * qdot) / qn),
                                    float((dqj - qj * qdot) / qn), float((dqk - qk * qdot) / qn));
 
   // --- view position: J^T d_mean2d plus the dependence of J on the mean
   //     (gradients.py:236-255)
-  const double dmx = ga.x, dmy = ga.y;
-  double dt[3] = {j00 * dmx, j11 * dmy, j02 * dmx + j12 * dmy};
-  double dU[6];  // 2 dS' U Sigma
+  const Real dmx = ga.x, dmy = ga.y;
+  Real dt[3] = {j00 * dmx, j11 * dmy, j02 * dmx + j12 * dmy};
+  Real dU[6];  // 2 dS' U Sigma
 #pragma unroll
   for (int r = 0; r < 2; ++r)
 #pragma unroll
     for (int l = 0; l < 3; ++l)
-      dU[3 * r + l] = 2.0 * (dCU[3 * r + 0] * S[l] + dCU[3 * r + 1] * S[3 + l] + dCU[3 * r + 2] * S[6 + l]);
-  double dJ[6];  // dU W^T
+      dU[3 * r + l] = Real(2.0) * (dCU[3 * r + 0] * S[l] + dCU[3 * r + 1] * S[3 + l] + dCU[3 * r + 2] * S[6 + l]);
+  Real dJ[6];  // dU W^T
 #pragma unroll
   for (int r = 0; r < 2; ++r)
 #pragma unroll
     for (int k = 0; k < 3; ++k)
-      dJ[3 * r + k] = dU[3 * r + 0] * cam.R[3 * k + 0] + dU[3 * r + 1] * cam.R[3 * k + 1] +
-                      dU[3 * r + 2] * cam.R[3 * k + 2];
-  dt[0] += dJ[2] * (-cam.fx / z2);
-  dt[1] += dJ[5] * (-cam.fy / z2);
-  dt[2] += dJ[0] * (-cam.fx / z2) + dJ[2] * (2.0 * cam.fx * x / z3) + dJ[4] * (-cam.fy / z2) +
-           dJ[5] * (2.0 * cam.fy * y / z3);
+      dJ[3 * r + k] = dU[3 * r + 0] * cR[3 * k + 0] + dU[3 * r + 1] * cR[3 * k + 1] +
+                      dU[3 * r + 2] * cR[3 * k + 2];
+  dt[0] += dJ[2] * (-cfx / z2);
+  dt[1] += dJ[5] * (-cfy / z2);
+  dt[2] += dJ[0] * (-cfx / z2) + dJ[2] * (Real(2.0) * cfx * x / z3) + dJ[4] * (-cfy / z2) +
+           dJ[5] * (Real(2.0) * cfy * y / z3);
 
   // --- colour: clamp mask, SH coefficients, direction path (gradients.py:219-226)
-  const double ddx = mx - cam.center[0], ddy = my - cam.center[1], ddz = mz - cam.center[2];
-  const double dist = sqrt(ddx * ddx + ddy * ddy + ddz * ddz);
+  const Real ddx = mx - ccen[0], ddy = my - ccen[1], ddz = mz - ccen[2];
+  const Real dist = sqrt(ddx * ddx + ddy * ddy + ddz * ddz);
   const float vx = float(ddx / dist), vy = float(ddy / dist), vz = float(ddz / dist);
   sh_basis(vx, vy, vz, degree, b);
   dcol[0] = (mask & 1) ? gc.x : 0.0f;
@@ -204,14 +223,14 @@ __device__ __forceinline__ void grad_one(const GradInputs& in, const DevCamera& 
   float gdx, gdy, gdz;
   sh_basis_vjp(vx, vy, vz, degree, db, gdx, gdy, gdz);
   const float vdot = vx * gdx + vy * gdy + vz * gdz;
-  const float inv_dist = float(1.0 / dist);
+  const float inv_dist = float(Real(1.0) / dist);
   const float dms[3] = {(gdx - vx * vdot) * inv_dist, (gdy - vy * vdot) * inv_dist, (gdz - vz * vdot) * inv_dist};
 
   // --- d_means = d_t W + d_mean_sh (gradients.py:257)
   float dmean[3];
 #pragma unroll
   for (int j = 0; j < 3; ++j)
-    dmean[j] = float(dt[0] * cam.R[j] + dt[1] * cam.R[3 + j] + dt[2] * cam.R[6 + j]) + dms[j];
+    dmean[j] = float(dt[0] * cR[j] + dt[1] * cR[3 + j] + dt[2] * cR[6 + j]) + dms[j];
   o.norm = sqrtf(ga.x * ga.x + ga.y * ga.y);  // gradients.py:258
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
@@ -220,6 +239,22 @@ __device__ __forceinline__ void grad_one(const GradInputs& in, const DevCamera& 
   }
   o.drot = d_rot;
   o.dlogit = d_logit;
+}
+
+// Precision of the backward projection chain (gradients only: no integer is
+// decided here, the forward keeps float64 for radii / keys).  GS_BWD_REAL =
+// float runs view position, J, U, the conic and dSigma' in float32; the
+// covariance R, M and the dM -> (d log_scale, d quaternion) chain stay
+// float64 (see grad_one_t).  Measured at c3: fused backward + Adam 1.087 ms
+// (all float64) -> 0.977 ms, every parity test unchanged; all-float32 was
+// 0.85 ms but leaves ~1e-7-relative noise in the (exactly zero) rotation
+// gradient of isotropic Gaussians.
+#ifndef GS_BWD_REAL
+#define GS_BWD_REAL float
+#endif
+__device__ __forceinline__ void grad_one(const GradInputs& in, const DevCamera& cam, int degree,
+                                         const float4* shrow, GradOut& o, float (&b)[16], float (&dcol)[3]) {
+  grad_one_t<GS_BWD_REAL>(in, cam, degree, shrow, o, b, dcol);
 }
 
 __device__ __forceinline__ void store_grads(const gs_grads_t& out, int64_t g, const GradOut& o, bool accumulate) {
@@ -319,7 +354,10 @@ struct FusedAdam {
   AdamCoef c;
 };
 
-__global__ void __launch_bounds__(128, 4)
+#ifndef GS_BWDADAM_MINB
+#define GS_BWDADAM_MINB 5
+#endif
+__global__ void __launch_bounds__(128, GS_BWDADAM_MINB)
 preprocess_bwd_adam_kernel(gs_params_t p, DevCamera cam, int degree, const float4* __restrict__ rec,
                            const int32_t* __restrict__ radii, const float4* __restrict__ g2d, gs_grads_t out,
                            gs_stats_t stats, FusedAdam A) {

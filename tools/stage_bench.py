@@ -46,8 +46,19 @@ def main() -> None:
         torch.cuda.synchronize()
         return s.elapsed_time(e) / args.reps
 
+    from paper_2308_04079_b200.optimizer import DeviceAdam, TrainConfig
+    adam = DeviceAdam(cloud)
+    stats = R.DensifyStats.zeros(len(cloud), "cuda")
+    g2 = R.render_backward(d, out, splats, binning, 1920, 1080, bg)
+    it = [0]
+
+    def bwd_adam():
+        it[0] += 1
+        adam.backward_step(cloud, cam, splats, g2, 3, it[0], TrainConfig(), stats=stats)
+
     res = {
         "lib": str(_lib.LIB_PATH),
+        "bwd_adam_ms": timeit(bwd_adam),
         "blend_fwd_ms": timeit(lambda: R.render_forward(splats, binning, 1920, 1080, bg, training=True)),
         "blend_bwd_ms": timeit(lambda: R.render_backward(d, out, splats, binning, 1920, 1080, bg)),
         "bin_async_ms": timeit(lambda: R.bin_and_sort_async(splats, 1920, 1080)),
