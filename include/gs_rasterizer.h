@@ -287,6 +287,18 @@ int gs_l1_dssim_loss(const float* image, const float* target, int32_t width, int
 int gs_pack_records(const gs_params_t* params, int32_t layout, float* out, void* stream);
 int gs_unpack_records(const float* records, gs_params_t* params_out, void* stream);
 
+/* ---- initialisation: replaces scene_io.mean_knn_distance
+ * (scene_io.py:304-311; scipy cKDTree, k + 1 neighbours with the self
+ * match dropped), the per-point scale of init_from_sfm / init_random
+ * (scene_io.py:314-366).  points: DEVICE (n,3) float64; out: DEVICE (n,)
+ * float32 mean distance to the k nearest other points (exact, float64
+ * distances, uniform-grid shell search).  Requires n > k; 1 <= k <= 16;
+ * max_cells bounds the grid (e.g. 2 n).  Synchronises `stream` once to read
+ * the bounding box. */
+int gs_knn_workspace_size(int64_t n, int64_t max_cells, size_t* bytes);
+int gs_knn_mean_distance(const double* points, int64_t n, int32_t k, int64_t max_cells, void* workspace,
+                         size_t workspace_bytes, float* out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -111,6 +111,9 @@ SIGNATURES = [
                                    c_void_p, c_void_p]),
     ("gs_pack_records", c_int32, [POINTER(GsParams), c_int32, c_void_p, c_void_p]),
     ("gs_unpack_records", c_int32, [c_void_p, POINTER(GsParams), c_void_p]),
+    ("gs_knn_workspace_size", c_int32, [c_int64, c_int64, POINTER(c_size_t)]),
+    ("gs_knn_mean_distance", c_int32, [c_void_p, c_int64, c_int32, c_int64, c_void_p, c_size_t, c_void_p,
+                                       c_void_p]),
     ("gs_adam_step", c_int32, [POINTER(GsAdamGroup), c_int32, c_double, c_double, c_double, c_double, c_double,
                                c_void_p]),
 ]

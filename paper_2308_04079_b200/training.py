@@ -251,6 +251,17 @@ def train(state: TrainState, views: Sequence[TrainView], config: TrainConfig, *,
     return reports
 
 
+def views_from_scene(images, pin: bool = True) -> list[TrainView]:
+    """TrainViews from colmap.SceneImage entries: the decoded float32 linear
+    images stay in (pinned) host memory and are prefetched to the device one
+    step ahead by train_step."""
+    views = []
+    for im in images:
+        t = torch.from_numpy(np.ascontiguousarray(im.load_pixels(), dtype=np.float32))
+        views.append(TrainView(im.camera, t.pin_memory() if pin and torch.cuda.is_available() else t, im.name))
+    return views
+
+
 def compute_metrics(render: torch.Tensor, ground_truth: torch.Tensor) -> tuple[float, float]:
     """(PSNR dB, mean SSIM) (optimizer.py:166-174)."""
     mse = float(torch.mean((render - ground_truth) ** 2).item())
