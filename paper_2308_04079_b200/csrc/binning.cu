@@ -7,7 +7,7 @@
 // produced depth-first, which moves most of the sorting from K to N:
 //   1. depth sort: stable radix sort of (depth bits, gaussian id) over N
 //      (ties keep index order, exactly like the reference's stable sort);
-//   2. per-Gaussian instance counts gathered in depth order, exclusive scan
+//   2. per-Gaussian instance counts read in depth order by the exclusive scan
 //      -> instance offsets and K, kept on the device (no host round trip);
 //   3. emission: warps write (tile id, gaussian id) for 32 depth-ranked
 //      Gaussians at a time into their contiguous output range, coalesced;
@@ -25,6 +25,8 @@
 // synchronous entry point, as GS_ERR_CAPACITY after one stream sync.
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
+#include <cub/iterator/counting_input_iterator.cuh>
+#include <cub/iterator/transform_input_iterator.cuh>
 
 #include "gs_common.cuh"
 
@@ -46,16 +48,17 @@ __global__ void depth_keys_kernel(const float* __restrict__ depth, const int32_t
   ids[g] = uint32_t(g);
 }
 
-__global__ void gather_counts_kernel(const uint32_t* __restrict__ order, const int32_t* __restrict__ tiles,
-                                     uint64_t* __restrict__ counts, int64_t n) {
-  const int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (r >= n) return;
-  counts[r] = uint64_t(tiles[order[r]]);
-}
+// per-Gaussian instance count in depth order, read on the fly by the scan
+struct DepthCount {
+  const uint32_t* order;
+  const int32_t* tiles;
+  __host__ __device__ __forceinline__ uint64_t operator()(int64_t r) const { return uint64_t(tiles[order[r]]); }
+};
 
-__global__ void total_kernel(const uint64_t* __restrict__ offsets, const uint64_t* __restrict__ counts, int64_t n,
-                             int64_t capacity, const int32_t* __restrict__ status, int64_t* __restrict__ kinfo) {
-  const uint64_t K = offsets[n - 1] + counts[n - 1];
+__global__ void total_kernel(const uint64_t* __restrict__ offsets, const uint32_t* __restrict__ order,
+                             const int32_t* __restrict__ tiles, int64_t n, int64_t capacity,
+                             const int32_t* __restrict__ status, int64_t* __restrict__ kinfo) {
+  const uint64_t K = offsets[n - 1] + uint64_t(tiles[order[n - 1]]);
   int64_t flags = (status[0] & 1) ? kFlagZeroQuat : 0;
   if (K > uint64_t(kMaxInstances) || K > uint64_t(INT32_MAX)) flags |= kFlagLimit;  // rasterizer.py:99-101
   if (K > uint64_t(capacity)) flags |= kFlagCapacity;
@@ -73,20 +76,18 @@ __global__ void total_kernel(const uint64_t* __restrict__ offsets, const uint64_
 template <typename KeyT>
 __global__ void __launch_bounds__(256)
 emit_instances_kernel(const uint32_t* __restrict__ order, const uint64_t* __restrict__ offsets,
-                      const uint64_t* __restrict__ counts, const int4* __restrict__ rect, int tiles_x,
+                      const int32_t* __restrict__ tiles_touched, const int4* __restrict__ rect, int tiles_x,
                       KeyT* __restrict__ tile_keys, uint32_t* __restrict__ ids, int64_t n, int64_t capacity) {
   const int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31;
   uint32_t off = 0xFFFFFFFFu, end = 0u, g = 0u;
   int4 rc = make_int4(0, 0, 0, 0);
   if (r < n) {
-    const uint32_t cnt = uint32_t(counts[r]);
+    g = order[r];
+    const uint32_t cnt = uint32_t(tiles_touched[g]);
     off = uint32_t(offsets[r]);
     end = off + cnt;
-    if (cnt) {
-      g = order[r];
-      rc = rect[g];
-    }
+    if (cnt) rc = rect[g];
   }
   const uint32_t base = __shfl_sync(0xffffffffu, off, 0);
   const uint32_t warp_end = __reduce_max_sync(0xffffffffu, end);
@@ -169,7 +170,7 @@ int bits_for(int64_t tiles) {
 bool small_keys(int64_t tiles) { return tiles <= 65536; }
 
 struct Layout {
-  size_t depth_keys_in, depth_keys_out, ids_in, ids_out, counts, offsets, kinfo, tile_keys_in, tile_keys_out,
+  size_t depth_keys_in, depth_keys_out, ids_in, ids_out, offsets, kinfo, tile_keys_in, tile_keys_out,
       inst_ids_in, cub_temp, bytes;
 };
 
@@ -185,7 +186,11 @@ int make_layout(int64_t n, int64_t tiles, int64_t kcap, Layout* L) {
   cudaError_t e = cub::DeviceRadixSort::SortPairs(nullptr, temp_depth, (const uint32_t*)nullptr, (uint32_t*)nullptr,
                                                   (const uint32_t*)nullptr, (uint32_t*)nullptr, nn, 0, 32);
   if (e != cudaSuccess) return record_cuda_error(e);
-  e = cub::DeviceScan::ExclusiveSum(nullptr, temp_scan, (const uint64_t*)nullptr, (uint64_t*)nullptr, nn);
+  {
+    cub::TransformInputIterator<uint64_t, DepthCount, cub::CountingInputIterator<int64_t>> in(
+        cub::CountingInputIterator<int64_t>(0), DepthCount{nullptr, nullptr});
+    e = cub::DeviceScan::ExclusiveSum(nullptr, temp_scan, in, (uint64_t*)nullptr, nn);
+  }
   if (e != cudaSuccess) return record_cuda_error(e);
   if (kcap > int64_t(INT32_MAX)) return GS_ERR_RESOURCE_LIMIT;
   const int64_t kk = kcap > 0 ? kcap : 1;
@@ -206,7 +211,6 @@ int make_layout(int64_t n, int64_t tiles, int64_t kcap, Layout* L) {
   L->depth_keys_out = take(4 * un);
   L->ids_in = take(4 * un);
   L->ids_out = take(4 * un);
-  L->counts = take(8 * un);
   L->offsets = take(8 * un);
   L->kinfo = take(4 * sizeof(int64_t));
   L->tile_keys_in = take(key_bytes * uk + 16);
@@ -225,7 +229,7 @@ int make_layout(int64_t n, int64_t tiles, int64_t kcap, Layout* L) {
 // passes at 1080p and 4K) and the tile ranges — all sized by the host-known
 // capacity, with K itself read on the device.
 template <typename KeyT>
-int tile_sort(const uint32_t* order, const uint64_t* offsets, const uint64_t* counts, const int4* rect, int tiles_x,
+int tile_sort(const uint32_t* order, const uint64_t* offsets, const int32_t* counts, const int4* rect, int tiles_x,
               int64_t tiles, int64_t n, int64_t cap, const int64_t* kinfo, char* ws, const Layout& L,
               size_t temp_bytes, uint32_t* sorted_ids, int2* ranges, cudaStream_t s) {
   auto* tk_in = reinterpret_cast<KeyT*>(ws + L.tile_keys_in);
@@ -273,7 +277,6 @@ int bin_enqueue(const gs_splats_t* splats, int32_t width, int32_t height, void* 
   auto* dk_out = reinterpret_cast<uint32_t*>(ws + L.depth_keys_out);
   auto* id_in = reinterpret_cast<uint32_t*>(ws + L.ids_in);
   auto* id_out = reinterpret_cast<uint32_t*>(ws + L.ids_out);
-  auto* counts = reinterpret_cast<uint64_t*>(ws + L.counts);
   auto* offsets = reinterpret_cast<uint64_t*>(ws + L.offsets);
   void* temp = ws + L.cub_temp;
   size_t temp_bytes = workspace_bytes - L.cub_temp;
@@ -284,19 +287,21 @@ int bin_enqueue(const gs_splats_t* splats, int32_t width, int32_t height, void* 
   if ((st = check_launch()) != GS_OK) return st;
   e = cub::DeviceRadixSort::SortPairs(temp, temp_bytes, dk_in, dk_out, id_in, id_out, int(n), 0, 32, s);
   if (e != cudaSuccess) return record_cuda_error(e);
-  gather_counts_kernel<<<gn, block, 0, s>>>(id_out, splats->tiles_touched, counts, n);
-  if ((st = check_launch()) != GS_OK) return st;
-  e = cub::DeviceScan::ExclusiveSum(temp, temp_bytes, counts, offsets, int(n), s);
+  {
+    cub::TransformInputIterator<uint64_t, DepthCount, cub::CountingInputIterator<int64_t>> in(
+        cub::CountingInputIterator<int64_t>(0), DepthCount{id_out, splats->tiles_touched});
+    e = cub::DeviceScan::ExclusiveSum(temp, temp_bytes, in, offsets, int(n), s);
+  }
   if (e != cudaSuccess) return record_cuda_error(e);
-  total_kernel<<<1, 1, 0, s>>>(offsets, counts, n, k_capacity, splats->status, kinfo);
+  total_kernel<<<1, 1, 0, s>>>(offsets, id_out, splats->tiles_touched, n, k_capacity, splats->status, kinfo);
   if ((st = check_launch()) != GS_OK) return st;
   if (k_capacity == 0) return GS_OK;
   const int4* rect = reinterpret_cast<const int4*>(splats->rect);
   if (small_keys(tiles))
-    return tile_sort<uint16_t>(id_out, offsets, counts, rect, tiles_x, tiles, n, k_capacity, kinfo, ws, L,
-                               temp_bytes, sorted_ids, reinterpret_cast<int2*>(ranges), s);
-  return tile_sort<uint32_t>(id_out, offsets, counts, rect, tiles_x, tiles, n, k_capacity, kinfo, ws, L, temp_bytes,
-                             sorted_ids, reinterpret_cast<int2*>(ranges), s);
+    return tile_sort<uint16_t>(id_out, offsets, splats->tiles_touched, rect, tiles_x, tiles, n, k_capacity, kinfo,
+                               ws, L, temp_bytes, sorted_ids, reinterpret_cast<int2*>(ranges), s);
+  return tile_sort<uint32_t>(id_out, offsets, splats->tiles_touched, rect, tiles_x, tiles, n, k_capacity, kinfo, ws,
+                             L, temp_bytes, sorted_ids, reinterpret_cast<int2*>(ranges), s);
 }
 
 int check_dims(int32_t width, int32_t height) {
