@@ -54,3 +54,37 @@ def test_toy_recovery_acceptance(cuda_device):
     print("held-out PSNR", psnrs, "gaussians", len(state.cloud), "densify events", len(reports), lines[-1])
     assert len(lines) == 4 and lines[-1].startswith("iter=2000 loss=")
     assert min(psnrs) >= 35.0
+
+
+@pytest.mark.gpu
+def test_train_step_recovers_from_capacity_overflow(cuda_device):
+    """A train_step whose async binning overflows the instance capacity
+    re-renders with a larger buffer before applying any gradient."""
+    from paper_2308_04079_b200 import rasterizer as R
+    from paper_2308_04079_b200.cloud import GaussianCloud
+    from paper_2308_04079_b200.densify import TrainState
+    from paper_2308_04079_b200.optimizer import TrainConfig
+    from paper_2308_04079_b200.training import TrainView, train_step
+    cloud_np, cam = synthetic.frustum_scene(20_000, 320, 240, seed=11)
+    tgt_np, _ = synthetic.frustum_scene(20_000, 320, 240, seed=12)
+    target = R.render_view(GaussianCloud.from_numpy(**tgt_np), cam, (0, 0, 0), 3)[0].image
+    cfg = TrainConfig(warmup_upsample_iters=(0, 0))
+    ref_state = TrainState(GaussianCloud.from_numpy(**cloud_np), 10.0, seed=0)
+    state = TrainState(GaussianCloud.from_numpy(**cloud_np), 10.0, seed=0)
+    for st in (ref_state, state):
+        st.active_sh_degree = 3
+    dev = str(state.cloud.device)
+    saved = (dict(R._capacity.k), dict(R._capacity.ratio))
+    try:
+        R._capacity.k[dev] = max(R._capacity.k.get(dev, 0), 10**8)   # plenty: no overflow
+        ref = train_step(ref_state, [TrainView(cam, target)], cfg)
+        R._capacity.k[dev] = 1024                                    # far too small
+        R._capacity.ratio.pop(dev, None)
+        rep = train_step(state, [TrainView(cam, target)], cfg)
+    finally:
+        R._capacity.k.clear(); R._capacity.k.update(saved[0])
+        R._capacity.ratio.clear(); R._capacity.ratio.update(saved[1])
+    assert rep.loss == ref.loss and rep.psnr == ref.psnr
+    # the backward's float atomics are order-dependent (SPEC.md:184 allows 1e-5 relative run to run)
+    for g in ("means", "rotations", "log_scales", "opacity_logits", "sh"):
+        torch.testing.assert_close(getattr(state.cloud, g), getattr(ref_state.cloud, g), rtol=1e-5, atol=1e-7)
