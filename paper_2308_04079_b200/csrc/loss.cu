@@ -3,7 +3,7 @@
 // (ssim.py:50-84): 11x11 Gaussian window (sigma 1.5), separable, zero
 // padding, per channel.
 //
-// Two tiled passes over 16x16 output tiles with a 5-pixel halo staged in
+// Two tiled passes over 32x16 output tiles with a 5-pixel halo staged in
 // shared memory:
 //   pass 1: the five filtered moments (mu_x, mu_y, E[x^2], E[y^2], E[xy]) in
 //           shifted float32, the SSIM value (float64), the three adjoint source maps
@@ -16,9 +16,7 @@
 namespace gs {
 namespace {
 
-constexpr int kT = 16;        // output tile edge
 constexpr int kR = 5;         // window radius (11 taps)
-constexpr int kIn = kT + 2 * kR;  // 26
 constexpr double kC1 = 0.01 * 0.01;
 constexpr double kC2 = 0.03 * 0.03;
 
@@ -50,18 +48,6 @@ __host__ Window make_window() {
   return W;
 }
 
-__device__ __forceinline__ double block_sum(double v, double* red) {
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  __syncthreads();
-  if (lane == 0) red[warp] = v;
-  __syncthreads();
-  double s = 0.0;
-  if (threadIdx.x == 0)
-    for (int i = 0; i < int(blockDim.x >> 5); ++i) s += red[i];
-  return s;
-}
-
 // pass 1 -------------------------------------------------------------------
 // The five filtered moments are accumulated in float32 on values shifted by
 // kShift (sigma^2 and the covariance are shift-invariant; mu is shifted back
@@ -69,47 +55,75 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
 // cancellation error near 1e-7 absolute, four orders below the SSIM
 // constant C2 = 9e-4 that every variance is added to.  Zero padding is
 // staged as the shifted value of 0.  The per-pixel SSIM value and its
-// adjoint are formed in float64.  Register blocking: every thread filters
-// kRun consecutive outputs from one register window (horizontal pass over
-// all three channels at once, then vertical runs of kRun rows).
+// adjoint are formed in float64.
+//
+// Tiles of kTW x kTH outputs (42 x 26 inputs with the halo), 384 threads,
+// register blocking: a horizontal item filters kRunX consecutive outputs of
+// one row and channel from one register window; a vertical item filters
+// kRunY consecutive rows of one column and channel.  One horizontal round
+// (3 x 26 x 4 = 312 items) and one vertical round (3 x 32 x 4 = 384 items).
 constexpr float kShift = 0.5f;
-constexpr int kRun = 4;
-constexpr int kWin = kRun + 10;
+constexpr int kTW = 32, kTH = 16;
+constexpr int kInW = kTW + 2 * kR, kInH = kTH + 2 * kR;   // 42 x 26
+constexpr int kLossThreads = 384;
+constexpr int kRunX = 8, kRunY = 4;
+constexpr int kWinX = kRunX + 10, kWinY = kRunY + 10;
+constexpr int kPitchIn = kInW + 1, kPitchH = kTW + 1;
 
-__global__ void __launch_bounds__(256)
+struct FwdSmem {
+  float x[3][kInH][kPitchIn];
+  float y[3][kInH][kPitchIn];
+  float h[3][5][kInH][kPitchH];   // horizontal pass: channel, moment, row, col
+  double red[kLossThreads / 32];
+};
+struct BwdSmem {
+  float src[9][kInH][kPitchIn];
+  float h[9][kInH][kPitchH];
+};
+
+__device__ __forceinline__ double block_sum384(double v, double* red) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  double s = 0.0;
+  if (threadIdx.x == 0)
+    for (int i = 0; i < kLossThreads / 32; ++i) s += red[i];
+  return s;
+}
+
+__global__ void __launch_bounds__(kLossThreads)
 ssim_forward_kernel(const float* __restrict__ img, const float* __restrict__ gt, int W, int H, Window win,
                     double d_map, float* __restrict__ src, double* __restrict__ sums) {
-  __shared__ float s_x[3][kIn][kIn + 1];
-  __shared__ float s_y[3][kIn][kIn + 1];
-  __shared__ float s_h[3][5][kIn][kT + 1];   // horizontal pass: channel, moment, row, col
-  __shared__ double s_red[8];
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  FwdSmem& sm = *reinterpret_cast<FwdSmem*>(smem_raw);
   const int t = threadIdx.x;
-  const int ox = blockIdx.x * kT, oy = blockIdx.y * kT;
-  for (int i = t; i < kIn * kIn; i += 256) {
-    const int r = i / kIn, c = i % kIn;
+  const int ox = blockIdx.x * kTW, oy = blockIdx.y * kTH;
+  for (int i = t; i < kInH * kInW; i += kLossThreads) {
+    const int r = i / kInW, c = i - r * kInW;
     const int gx = ox + c - kR, gy = oy + r - kR;
     const bool in = gx >= 0 && gx < W && gy >= 0 && gy < H;
     const size_t p = in ? (size_t(gy) * W + gx) * 3 : 0;
 #pragma unroll
     for (int ch = 0; ch < 3; ++ch) {
-      s_x[ch][r][c] = (in ? img[p + ch] : 0.0f) - kShift;
-      s_y[ch][r][c] = (in ? gt[p + ch] : 0.0f) - kShift;
+      sm.x[ch][r][c] = (in ? img[p + ch] : 0.0f) - kShift;
+      sm.y[ch][r][c] = (in ? gt[p + ch] : 0.0f) - kShift;
     }
   }
   __syncthreads();
-  // horizontal: item = (channel, row, run of kRun output columns)
-  constexpr int kRunsX = kT / kRun;
-  for (int i = t; i < 3 * kIn * kRunsX; i += 256) {
-    const int ch = i / (kIn * kRunsX), rem = i - ch * (kIn * kRunsX);
-    const int r = rem / kRunsX, c0 = (rem - r * kRunsX) * kRun;
-    float x[kWin], y[kWin];
+  constexpr int kRunsX = kTW / kRunX;
+  for (int i = t; i < 3 * kInH * kRunsX; i += kLossThreads) {
+    const int ch = i / (kInH * kRunsX), rem = i - ch * (kInH * kRunsX);
+    const int r = rem / kRunsX, c0 = (rem - r * kRunsX) * kRunX;
+    float x[kWinX], y[kWinX];
 #pragma unroll
-    for (int k = 0; k < kWin; ++k) {
-      x[k] = s_x[ch][r][c0 + k];
-      y[k] = s_y[ch][r][c0 + k];
+    for (int k = 0; k < kWinX; ++k) {
+      x[k] = sm.x[ch][r][c0 + k];
+      y[k] = sm.y[ch][r][c0 + k];
     }
 #pragma unroll
-    for (int o = 0; o < kRun; ++o) {
+    for (int o = 0; o < kRunX; ++o) {
       float a = 0.f, b = 0.f, xx = 0.f, yy = 0.f, xy = 0.f;
 #pragma unroll
       for (int k = 0; k < 11; ++k) {
@@ -121,28 +135,28 @@ ssim_forward_kernel(const float* __restrict__ img, const float* __restrict__ gt,
         yy = fmaf(wy, yv, yy);
         xy = fmaf(wx, yv, xy);
       }
-      s_h[ch][0][r][c0 + o] = a;
-      s_h[ch][1][r][c0 + o] = b;
-      s_h[ch][2][r][c0 + o] = xx;
-      s_h[ch][3][r][c0 + o] = yy;
-      s_h[ch][4][r][c0 + o] = xy;
+      sm.h[ch][0][r][c0 + o] = a;
+      sm.h[ch][1][r][c0 + o] = b;
+      sm.h[ch][2][r][c0 + o] = xx;
+      sm.h[ch][3][r][c0 + o] = yy;
+      sm.h[ch][4][r][c0 + o] = xy;
     }
   }
   __syncthreads();
-  // vertical: item = (channel, column, run of kRun output rows)
+  // vertical: item = (channel, column, run of kRunY output rows); 384 items
   double ssim_sum = 0.0, l1_sum = 0.0, sq_sum = 0.0;
-  constexpr int kRunsY = kT / kRun;
-  if (t < 3 * kT * kRunsY) {
-    const int ch = t / (kT * kRunsY), rem = t - ch * (kT * kRunsY);
-    const int c = rem % kT, r0 = (rem / kT) * kRun;
-    float m[kRun][5];
+  {
+    constexpr int kRunsY = kTH / kRunY;
+    const int ch = t / (kTW * kRunsY), rem = t - ch * (kTW * kRunsY);
+    const int c = rem % kTW, r0 = (rem / kTW) * kRunY;
+    float m[kRunY][5];
 #pragma unroll
     for (int j = 0; j < 5; ++j) {
-      float v[kWin];
+      float v[kWinY];
 #pragma unroll
-      for (int k = 0; k < kWin; ++k) v[k] = s_h[ch][j][r0 + k][c];
+      for (int k = 0; k < kWinY; ++k) v[k] = sm.h[ch][j][r0 + k][c];
 #pragma unroll
-      for (int o = 0; o < kRun; ++o) {
+      for (int o = 0; o < kRunY; ++o) {
         float acc = 0.f;
 #pragma unroll
         for (int k = 0; k < 11; ++k) acc = fmaf(win.w[k], v[o + k], acc);
@@ -151,7 +165,7 @@ ssim_forward_kernel(const float* __restrict__ img, const float* __restrict__ gt,
     }
     const int gx = ox + c;
 #pragma unroll
-    for (int o = 0; o < kRun; ++o) {
+    for (int o = 0; o < kRunY; ++o) {
       const int gy = oy + r0 + o;
       if (gx < W && gy < H) {
         const size_t p = size_t(gy) * W + gx;
@@ -177,9 +191,9 @@ ssim_forward_kernel(const float* __restrict__ img, const float* __restrict__ gt,
       }
     }
   }
-  const double s1 = block_sum(ssim_sum, s_red);
-  const double s2 = block_sum(l1_sum, s_red);
-  const double s3 = block_sum(sq_sum, s_red);
+  const double s1 = block_sum384(ssim_sum, sm.red);
+  const double s2 = block_sum384(l1_sum, sm.red);
+  const double s3 = block_sum384(sq_sum, sm.red);
   if (t == 0) {
     atomicAdd(&sums[0], s1);
     atomicAdd(&sums[1], s2);
@@ -188,53 +202,52 @@ ssim_forward_kernel(const float* __restrict__ img, const float* __restrict__ gt,
 }
 
 // pass 2 -------------------------------------------------------------------
-// Same register blocking: horizontal runs over the nine source maps, then
-// vertical runs of kRun rows per (channel, column) that combine the three
-// filtered maps of the channel with the L1 sign term.
-__global__ void __launch_bounds__(256)
+// Same tiling: horizontal runs over the nine source maps, then vertical runs
+// of kRunY rows per (channel, column) that combine the three filtered maps
+// of the channel with the L1 sign term.
+__global__ void __launch_bounds__(kLossThreads)
 ssim_backward_kernel(const float* __restrict__ img, const float* __restrict__ gt, const float* __restrict__ src,
                      int W, int H, Window win, float l1_scale, float* __restrict__ d_image) {
-  __shared__ float s_s[9][kIn][kIn + 1];
-  __shared__ float s_h[9][kIn][kT + 1];
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  BwdSmem& sm = *reinterpret_cast<BwdSmem*>(smem_raw);
   const int t = threadIdx.x;
-  const int ox = blockIdx.x * kT, oy = blockIdx.y * kT;
-  for (int i = t; i < kIn * kIn; i += 256) {
-    const int r = i / kIn, c = i % kIn;
+  const int ox = blockIdx.x * kTW, oy = blockIdx.y * kTH;
+  for (int i = t; i < kInH * kInW; i += kLossThreads) {
+    const int r = i / kInW, c = i - r * kInW;
     const int gx = ox + c - kR, gy = oy + r - kR;
     const bool in = gx >= 0 && gx < W && gy >= 0 && gy < H;
     const size_t p = in ? (size_t(gy) * W + gx) * 9 : 0;
 #pragma unroll
-    for (int j = 0; j < 9; ++j) s_s[j][r][c] = in ? src[p + j] : 0.0f;
+    for (int j = 0; j < 9; ++j) sm.src[j][r][c] = in ? src[p + j] : 0.0f;
   }
   __syncthreads();
-  constexpr int kRunsX = kT / kRun;
-  for (int i = t; i < 9 * kIn * kRunsX; i += 256) {
-    const int j = i / (kIn * kRunsX), rem = i - j * (kIn * kRunsX);
-    const int r = rem / kRunsX, c0 = (rem - r * kRunsX) * kRun;
-    float v[kWin];
+  constexpr int kRunsX = kTW / kRunX;
+  for (int i = t; i < 9 * kInH * kRunsX; i += kLossThreads) {
+    const int j = i / (kInH * kRunsX), rem = i - j * (kInH * kRunsX);
+    const int r = rem / kRunsX, c0 = (rem - r * kRunsX) * kRunX;
+    float v[kWinX];
 #pragma unroll
-    for (int k = 0; k < kWin; ++k) v[k] = s_s[j][r][c0 + k];
+    for (int k = 0; k < kWinX; ++k) v[k] = sm.src[j][r][c0 + k];
 #pragma unroll
-    for (int o = 0; o < kRun; ++o) {
+    for (int o = 0; o < kRunX; ++o) {
       float acc = 0.f;
 #pragma unroll
       for (int k = 0; k < 11; ++k) acc = fmaf(win.w[k], v[o + k], acc);
-      s_h[j][r][c0 + o] = acc;
+      sm.h[j][r][c0 + o] = acc;
     }
   }
   __syncthreads();
-  constexpr int kRunsY = kT / kRun;
-  if (t >= 3 * kT * kRunsY) return;
-  const int ch = t / (kT * kRunsY), rem = t - ch * (kT * kRunsY);
-  const int c = rem % kT, r0 = (rem / kT) * kRun;
-  float f[3][kRun];
+  constexpr int kRunsY = kTH / kRunY;
+  const int ch = t / (kTW * kRunsY), rem = t - ch * (kTW * kRunsY);
+  const int c = rem % kTW, r0 = (rem / kTW) * kRunY;
+  float f[3][kRunY];
 #pragma unroll
   for (int m = 0; m < 3; ++m) {
-    float v[kWin];
+    float v[kWinY];
 #pragma unroll
-    for (int k = 0; k < kWin; ++k) v[k] = s_h[3 * m + ch][r0 + k][c];
+    for (int k = 0; k < kWinY; ++k) v[k] = sm.h[3 * m + ch][r0 + k][c];
 #pragma unroll
-    for (int o = 0; o < kRun; ++o) {
+    for (int o = 0; o < kRunY; ++o) {
       float acc = 0.f;
 #pragma unroll
       for (int k = 0; k < 11; ++k) acc = fmaf(win.w[k], v[o + k], acc);
@@ -243,7 +256,7 @@ ssim_backward_kernel(const float* __restrict__ img, const float* __restrict__ gt
   }
   const int gx = ox + c;
 #pragma unroll
-  for (int o = 0; o < kRun; ++o) {
+  for (int o = 0; o < kRunY; ++o) {
     const int gy = oy + r0 + o;
     if (gx < W && gy < H) {
       const size_t p = size_t(gy) * W + gx;
@@ -290,14 +303,22 @@ extern "C" int gs_l1_dssim_loss(const float* image, const float* target, int32_t
   if (e != cudaSuccess) return record_cuda_error(e);
   const double count = double(width) * height * 3.0;
   const Window win = make_window();
-  const dim3 grid((width + kT - 1) / kT, (height + kT - 1) / kT);
+  static bool configured = false;
+  if (!configured) {
+    e = cudaFuncSetAttribute(ssim_forward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(FwdSmem)));
+    if (e != cudaSuccess) return record_cuda_error(e);
+    e = cudaFuncSetAttribute(ssim_backward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(BwdSmem)));
+    if (e != cudaSuccess) return record_cuda_error(e);
+    configured = true;
+  }
+  const dim3 grid((width + kTW - 1) / kTW, (height + kTH - 1) / kTH);
   // d_map = -lambda / (2 count) everywhere (optimizer.py:159)
-  ssim_forward_kernel<<<grid, 256, 0, s>>>(image, target, width, height, win, -lambda / (2.0 * count), src,
-                                           sums);
+  ssim_forward_kernel<<<grid, kLossThreads, sizeof(FwdSmem), s>>>(image, target, width, height, win,
+                                                                   -lambda / (2.0 * count), src, sums);
   int st = check_launch();
   if (st != GS_OK) return st;
-  ssim_backward_kernel<<<grid, 256, 0, s>>>(image, target, src, width, height, win, float((1.0 - lambda) / count),
-                                            d_image);
+  ssim_backward_kernel<<<grid, kLossThreads, sizeof(BwdSmem), s>>>(image, target, src, width, height, win,
+                                                                    float((1.0 - lambda) / count), d_image);
   if ((st = check_launch()) != GS_OK) return st;
   loss_finalize_kernel<<<1, 1, 0, s>>>(sums, count, lambda, loss_out);
   return check_launch();
