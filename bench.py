@@ -439,6 +439,10 @@ def main() -> None:
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    # test hooks: several ranks on one GPU (GS_DEVICE_OVERRIDE) with gloo
+    # (GS_DIST_BACKEND) exercise the multi-rank code path where one GPU is all there is
+    if "GS_DEVICE_OVERRIDE" in os.environ:
+        local_rank = int(os.environ["GS_DEVICE_OVERRIDE"])
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
@@ -446,7 +450,11 @@ def main() -> None:
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        backend = os.environ.get("GS_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        else:
+            dist.init_process_group(backend)
     try:
         run_ours(args, rank, world, local_rank)
     finally:
