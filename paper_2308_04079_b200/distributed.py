@@ -8,15 +8,22 @@ Adam on the reduced gradients.  Densification statistics are per view and
 accumulate on each rank before the cross-rank reduction
 (optimizer.py:252-254); the reduction sums accum_pos_grad/accum_count and
 takes the max of max_radius_frac.
+
+ShardedAdam is the reduce-scatter alternative: the same wire bytes, but each
+rank stores and updates the Adam moments of 1/G of the Gaussians only.
 """
 from __future__ import annotations
+
+import math
 
 import torch
 import torch.distributed as dist
 
+from .cloud import PARAM_GROUPS
 from .rasterizer import DensifyStats, GaussianGrads
 
 GROUP_WIDTHS = (("d_means", 3), ("d_rotations", 4), ("d_log_scales", 3), ("d_opacity_logits", 1), ("d_sh", 48))
+_ROW_SHAPE = {"means": (3,), "rotations": (4,), "log_scales": (3,), "opacity_logits": (), "sh": (16, 3)}
 FLOATS_PER_GAUSSIAN = sum(w for _, w in GROUP_WIDTHS)  # 59
 
 
@@ -82,3 +89,86 @@ def train_step_views(cloud, cameras, targets, adam, config, iteration: int, buck
     bucket.allreduce_(group)
     adam.step(cloud, bucket.grads, iteration, config)
     return total
+
+
+def _world(group=None) -> tuple[int, int]:
+    if dist.is_available() and dist.is_initialized():
+        return dist.get_world_size(group), dist.get_rank(group)
+    return 1, 0
+
+
+class ShardedAdam:
+    """View-parallel training with the optimizer sharded over the ranks
+    (the reduce-scatter alternative): the summed gradients are
+    reduce-scattered by Gaussian range, every rank runs Adam on its shard
+    only (its moments are the only ones it stores: 1/G of the Adam state and
+    of the Adam HBM traffic), and the updated parameter shards are
+    all-gathered.  Same wire bytes as an all-reduce of the gradients.
+
+    The cloud's parameter tensors are re-homed into buffers padded to a
+    multiple of the world size (the cloud keeps contiguous views of their
+    first N rows).  The Gaussian count is fixed for the lifetime of the
+    object (densify/prune re-shards by building a new one)."""
+
+    def __init__(self, cloud, group=None):
+        self.group = group
+        self.world, self.rank = _world(group)
+        self.n = n = len(cloud)
+        self.per = per = max(1, -(-n // self.world))
+        npad = per * self.world
+        dev = cloud.device
+        self.lo, self.hi = min(n, self.rank * per), min(n, (self.rank + 1) * per)
+        z = dict(dtype=torch.float32, device=dev)
+        self.pbuf = {}
+        for g in PARAM_GROUPS:
+            buf = torch.zeros((npad,) + _ROW_SHAPE[g], **z)
+            buf[:n].copy_(getattr(cloud, g))
+            setattr(cloud, g, buf[:n])
+            self.pbuf[g] = buf
+        # gradient bucket: one padded segment per group, contiguous in one flat buffer
+        widths = [math.prod(_ROW_SHAPE[g]) for g in PARAM_GROUPS]
+        self.flat = torch.zeros(npad * sum(widths), **z)
+        parts = torch.split(self.flat, [npad * w for w in widths])
+        self.gbuf = {g: part.view((npad,) + _ROW_SHAPE[g]) for g, part in zip(PARAM_GROUPS, parts)}
+        self.grads = GaussianGrads(*(self.gbuf[g][:n] for g in ("means", "rotations", "log_scales",
+                                                                   "opacity_logits", "sh")),
+                                   torch.zeros(n, **z))
+        self.shard_grad = {g: torch.zeros((per,) + _ROW_SHAPE[g], **z) for g in PARAM_GROUPS}
+        self.exp_avg = {g: torch.zeros((per,) + _ROW_SHAPE[g], **z) for g in PARAM_GROUPS}
+        self.exp_avg_sq = {g: torch.zeros((per,) + _ROW_SHAPE[g], **z) for g in PARAM_GROUPS}
+
+    def zero_(self) -> None:
+        self.flat.zero_()
+
+    def _reduce_scatter(self, out: torch.Tensor, full: torch.Tensor) -> None:
+        if self.world == 1:
+            out.copy_(full)
+        elif dist.get_backend(self.group) == "nccl":
+            dist.reduce_scatter_tensor(out, full, op=dist.ReduceOp.SUM, group=self.group)
+        else:   # gloo has no reduce-scatter: all-reduce, keep this rank's rows
+            dist.all_reduce(full, op=dist.ReduceOp.SUM, group=self.group)
+            out.copy_(full[self.rank * self.per:(self.rank + 1) * self.per])
+
+    def _all_gather(self, full: torch.Tensor) -> None:
+        shard = full[self.rank * self.per:(self.rank + 1) * self.per]
+        if self.world == 1:
+            return
+        if dist.get_backend(self.group) == "nccl":
+            dist.all_gather_into_tensor(full, shard, group=self.group)   # in place: the shard is full's slice
+        else:
+            parts = list(torch.split(full, self.per))
+            dist.all_gather(parts, shard.clone(), group=self.group)
+
+    def step(self, cloud, iteration: int, config) -> None:
+        """Reduce-scatter the bucket, Adam on this rank's shard, all-gather."""
+        from .optimizer import adam_step_tensors
+        for g in PARAM_GROUPS:
+            self._reduce_scatter(self.shard_grad[g], self.gbuf[g])
+        k = self.hi - self.lo
+        if k > 0:
+            adam_step_tensors({g: self.pbuf[g][self.lo:self.hi] for g in PARAM_GROUPS},
+                              {g: self.shard_grad[g][:k] for g in PARAM_GROUPS},
+                              {g: self.exp_avg[g][:k] for g in PARAM_GROUPS},
+                              {g: self.exp_avg_sq[g][:k] for g in PARAM_GROUPS}, iteration, config)
+        for g in PARAM_GROUPS:
+            self._all_gather(self.pbuf[g])

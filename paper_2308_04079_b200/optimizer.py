@@ -72,6 +72,38 @@ class TrainConfig:
         return self.lr_means * (self.lr_means_final / self.lr_means) ** frac
 
 
+def _lr_table(t: int, config: "TrainConfig") -> dict:
+    return {"means": config.lr_means_at(t), "log_scales": config.lr_log_scales, "rotations": config.lr_rotations,
+            "opacity_logits": config.lr_opacity, "sh": config.lr_sh_rest}
+
+
+def adam_step_tensors(params: dict, grads: dict, exp_avg: dict, exp_avg_sq: dict, iteration: int,
+                      config: "TrainConfig") -> None:
+    """One gs_adam_step launch over explicit per-group tensors (contiguous
+    row ranges of the groups, e.g. one rank's shard; the SH head LR applies to
+    the first 3 of every 48 elements, so a range must start on a Gaussian)."""
+    t = int(iteration)
+    bias1, bias2 = DeviceAdam._bias(t, config)
+    lrs = _lr_table(t, config)
+    groups = (_lib.GsAdamGroup * len(PARAM_GROUPS))()
+    for i, name in enumerate(PARAM_GROUPS):
+        p, g, m, v = params[name], grads[name], exp_avg[name], exp_avg_sq[name]
+        for x in (p, g, m, v):
+            if not x.is_contiguous():
+                raise ValueError(f"{name}: Adam tensors must be contiguous")
+        G = groups[i]
+        G.param, G.grad, G.exp_avg, G.exp_avg_sq = p.data_ptr(), g.data_ptr(), m.data_ptr(), v.data_ptr()
+        G.numel = p.numel()
+        G.lr = lrs[name]
+        if name == "sh":  # row 0 (DC) uses lr_sh_dc (optimizer.py:268-269)
+            G.lr_head, G.period, G.head = config.lr_sh_dc, 48, 3
+        else:
+            G.lr_head, G.period, G.head = lrs[name], 0, 0
+    beta1, beta2 = config.adam_betas
+    _lib.check(_lib.load().gs_adam_step(groups, len(PARAM_GROUPS), beta1, beta2, config.adam_eps, bias1, bias2,
+                                        torch.cuda.current_stream().cuda_stream), "adam_step")
+
+
 class DeviceAdam:
     """Adam moments for the five parameter groups, updated in one launch."""
 

@@ -104,3 +104,58 @@ def test_bench_two_ranks_one_gpu(cuda_device):
     assert len(lines) == 1   # rank 0 alone prints
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["value"] > 0 and d["e2e"]["value"] > 0
+
+
+def _sharded_worker(rank, world, port, out_dir):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch.distributed as dist
+    from paper_2308_04079_b200 import rasterizer as R
+    from paper_2308_04079_b200.cloud import GaussianCloud
+    from paper_2308_04079_b200.distributed import GradientBucket, ShardedAdam
+    from paper_2308_04079_b200.loss import l1_dssim_loss
+    from paper_2308_04079_b200.optimizer import DeviceAdam, TrainConfig
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        cloud_np, tgt_np, cam = _scene()
+        views = _views(cam, GaussianCloud.from_numpy(**tgt_np))
+        cfg = TrainConfig(warmup_upsample_iters=(0, 0))
+        cloud_s = GaussianCloud.from_numpy(**cloud_np)
+        cloud_r = GaussianCloud.from_numpy(**cloud_np)
+        sharded = ShardedAdam(cloud_s)
+        replicated, bucket = DeviceAdam(cloud_r), GradientBucket(len(cloud_r), "cuda")
+        v = views[rank]
+        for it in range(1, 4):
+            # one backward (float atomics are order-dependent); both optimisers get the same gradients
+            bucket.zero_()
+            out, splats, binning = R.render_view(cloud_r, v.camera, (0, 0, 0), 3, training=True)
+            _, d_image = l1_dssim_loss(out.image, v.image, cfg.lambda_dssim)
+            g2 = R.render_backward(d_image, out, splats, binning, v.camera.width, v.camera.height, (0, 0, 0))
+            R.backward_project(cloud_r, v.camera, splats, g2, 3, out=bucket.grads, accumulate=True)
+            sharded.zero_()
+            for a, b in ((sharded.grads.d_means, bucket.grads.d_means), (sharded.grads.d_sh, bucket.grads.d_sh),
+                         (sharded.grads.d_rotations, bucket.grads.d_rotations),
+                         (sharded.grads.d_log_scales, bucket.grads.d_log_scales),
+                         (sharded.grads.d_opacity_logits, bucket.grads.d_opacity_logits)):
+                a.copy_(b)
+            sharded.step(cloud_s, it, cfg)
+            bucket.allreduce_()
+            replicated.step(cloud_r, bucket.grads, it, cfg)
+        torch.save({"s": {g: getattr(cloud_s, g).cpu() for g in ("means", "sh", "rotations")},
+                    "r": {g: getattr(cloud_r, g).cpu() for g in ("means", "sh", "rotations")},
+                    "shard_rows": sharded.exp_avg["means"].shape[0]}, os.path.join(out_dir, f"sh{rank}.pt"))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharded_adam_matches_replicated(cuda_device, tmp_path):
+    """Reduce-scatter + Adam on 1/G of the Gaussians + all-gather == all-reduce + full Adam."""
+    import torch.multiprocessing as mp
+    mp.start_processes(_sharded_worker, args=(2, _free_port(), str(tmp_path)), nprocs=2, start_method="spawn")
+    res = [torch.load(tmp_path / f"sh{r}.pt") for r in range(2)]
+    for r in res:
+        assert r["shard_rows"] == 15_000   # each rank holds moments for half of the 30,000 Gaussians
+        for k in r["s"]:
+            assert torch.equal(r["s"][k], r["r"][k]), k
+    for k in res[0]["s"]:
+        assert torch.equal(res[0]["s"][k], res[1]["s"][k]), k
