@@ -69,26 +69,64 @@ def reduce_stats_(stats: DensifyStats, group=None) -> None:
 
 def train_step_views(cloud, cameras, targets, adam, config, iteration: int, bucket: GradientBucket,
                      stats: DensifyStats | None = None, background=(0.0, 0.0, 0.0), active_sh_degree: int = 3,
-                     group=None) -> torch.Tensor:
+                     group=None, streams: int = 1) -> torch.Tensor:
     """One multi-view training iteration on this rank's views: per view
     project -> bin -> blend -> loss -> blend bwd -> backward_project
-    (accumulated into the bucket), then the all-reduce and the fused Adam.
-    Returns the summed loss of this rank's views (device scalar)."""
+    (accumulated into the bucket), then the all-reduce and the Adam step.
+    Returns the summed loss of this rank's views (device scalar).
+
+    streams > 1 runs consecutive views on that many CUDA streams, each with
+    its own gradient bucket and statistics (summed / max-reduced before the
+    all-reduce), so the latency-bound binning of one view overlaps the
+    compute-bound blending of another.  The binning is the sync-free variant
+    (instance count and flags checked once, after the batch)."""
     from . import rasterizer as R
     from .loss import l1_dssim_loss
 
+    main = torch.cuda.current_stream(cloud.device)
+    lanes = [(main, bucket, stats)]
+    if streams > 1:
+        aux = getattr(bucket, "_aux_lanes", None)
+        if aux is None or len(aux) != streams - 1:
+            aux = [(torch.cuda.Stream(cloud.device), GradientBucket(bucket.n, cloud.device),
+                    DensifyStats.zeros(bucket.n, cloud.device) if stats is not None else None)
+                   for _ in range(streams - 1)]
+            bucket._aux_lanes = aux
+        lanes += aux
     bucket.zero_()
-    total = torch.zeros((), dtype=torch.float32, device=cloud.device)
-    for cam, gt in zip(cameras, targets):
-        out, splats, binning = R.render_view(cloud, cam, background, active_sh_degree, training=True)
-        loss, d_image = l1_dssim_loss(out.image, gt, config.lambda_dssim)
-        g2 = R.render_backward(d_image, out, splats, binning, cam.width, cam.height, background)
-        R.backward_project(cloud, cam, splats, g2, active_sh_degree, stats=stats, out=bucket.grads,
-                           accumulate=True)
-        total += loss[0]
+    for s, b, st in lanes[1:]:
+        s.wait_stream(main)
+        with torch.cuda.stream(s):
+            b.zero_()
+            if st is not None:
+                st.accum_pos_grad.zero_()
+                st.accum_count.zero_()
+                st.max_radius_frac.zero_()
+    totals, k_infos = [], []
+    for i, (cam, gt) in enumerate(zip(cameras, targets)):
+        s, b, st = lanes[i % len(lanes)]
+        with torch.cuda.stream(s):
+            if streams > 1:
+                out, splats, binning = R.render_view_async(cloud, cam, background, active_sh_degree, training=True)
+                k_infos.append(binning.k_info)
+            else:
+                out, splats, binning = R.render_view(cloud, cam, background, active_sh_degree, training=True)
+            loss, d_image = l1_dssim_loss(out.image, gt, config.lambda_dssim)
+            g2 = R.render_backward(d_image, out, splats, binning, cam.width, cam.height, background)
+            R.backward_project(cloud, cam, splats, g2, active_sh_degree, stats=st, out=b.grads, accumulate=True)
+            totals.append(loss[0:1])
+    for s, b, st in lanes[1:]:
+        main.wait_stream(s)
+        bucket.flat.add_(b.flat)
+        if st is not None:
+            stats.accum_pos_grad.add_(st.accum_pos_grad)
+            stats.accum_count.add_(st.accum_count)
+            torch.maximum(stats.max_radius_frac, st.max_radius_frac, out=stats.max_radius_frac)
+    if k_infos and bool((torch.stack(k_infos)[:, 1] != 0).any()):
+        raise R.CapacityError("multi-view batch: a view overflowed its instance capacity; re-run the batch")
     bucket.allreduce_(group)
     adam.step(cloud, bucket.grads, iteration, config)
-    return total
+    return torch.cat(totals).sum()
 
 
 def _world(group=None) -> tuple[int, int]:

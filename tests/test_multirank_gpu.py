@@ -159,3 +159,32 @@ def test_sharded_adam_matches_replicated(cuda_device, tmp_path):
             assert torch.equal(r["s"][k], r["r"][k]), k
     for k in res[0]["s"]:
         assert torch.equal(res[0]["s"][k], res[1]["s"][k]), k
+
+
+def test_multiview_two_streams_matches_one(cuda_device):
+    """train_step_views with views alternating over 2 CUDA streams (per-stream
+    buckets and statistics merged) == the single-stream accumulation."""
+    from paper_2308_04079_b200 import rasterizer as R
+    from paper_2308_04079_b200 import synthetic
+    from paper_2308_04079_b200.cloud import GaussianCloud
+    from paper_2308_04079_b200.distributed import GradientBucket, train_step_views
+    from paper_2308_04079_b200.optimizer import DeviceAdam, TrainConfig
+    cloud_np = synthetic.ball_scene(40_000, seed=3)
+    cams = synthetic.ball_cameras(6, width=320, height=180)
+    tgt = GaussianCloud.from_numpy(**synthetic.ball_scene(40_000, seed=4))
+    targets = [R.render_view(tgt, c, (0, 0, 0), 3)[0].image for c in cams]
+    results = []
+    for streams in (1, 2):
+        cloud = GaussianCloud.from_numpy(**cloud_np)
+        adam, bucket = DeviceAdam(cloud), GradientBucket(len(cloud), "cuda")
+        stats = R.DensifyStats.zeros(len(cloud), "cuda")
+        loss = train_step_views(cloud, cams, targets, adam, TrainConfig(), 1, bucket, stats, streams=streams)
+        torch.cuda.synchronize()
+        results.append((cloud, stats, float(loss)))
+    (c1, s1, l1), (c2, s2, l2) = results
+    assert abs(l1 - l2) <= 1e-6 * abs(l1)
+    for g in ("means", "sh", "rotations", "log_scales", "opacity_logits"):
+        torch.testing.assert_close(getattr(c2, g), getattr(c1, g), rtol=1e-5, atol=1e-7)
+    assert torch.equal(s1.accum_count, s2.accum_count)
+    assert torch.equal(s1.max_radius_frac, s2.max_radius_frac)
+    torch.testing.assert_close(s2.accum_pos_grad, s1.accum_pos_grad, rtol=1e-5, atol=1e-9)
