@@ -207,9 +207,7 @@ __device__ __forceinline__ int tile_py(int t) { return (t >> 6) * 4 + ((t & 31) 
 // inflated so the test is conservative against float32 rounding: a pair is
 // skipped only if the reference would skip it (a < 1/255), so culling never
 // changes a result bit.
-// kBlockH = 4: eight 8x4 warp blocks (forward); kBlockH = 8: four 8x8
-// blocks (backward, two pixels per lane).  Warp w's block starts at
-// ((w & 1) * 8, (w >> 1) * kBlockH).
+// Warp w's 8x4 block starts at ((w & 1) * 8, (w >> 1) * 4) of the tile.
 template <int kBlockH = 4>
 __device__ __forceinline__ uint32_t warp_cover_mask(float4 r0, float4 r1, float tile_x0, float tile_y0) {
   constexpr int kWarps = 2 * (kTile / kBlockH);
@@ -304,11 +302,7 @@ __device__ __forceinline__ void prefetch_l2_span(const void* ptr, size_t bytes) 
     n -= chunk;
   }
 }
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int kPending>
-__device__ __forceinline__ void cp_async_wait_group() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(kPending) : "memory");
-}
+
 __device__ __forceinline__ int ld_volatile(const int* p) { return *reinterpret_cast<const volatile int*>(p); }
 
 // ---------------------------------------------------------------------------
