@@ -183,7 +183,7 @@ blend_bwd_kernel(const float* __restrict__ d_image, const float4* __restrict__ r
           if (e < cnt) {
             const float4 r0 = raw->r0[e], r1 = raw->r1[e];
             make_tile_splat(r0, r1, tile_x0, tile_y0, st.geo[e], st.geo2[e]);
-            st.mask[e] = uint8_t(warp_cover_mask(r0, r1, tile_x0, tile_y0));
+            st.mask[e] = uint8_t(warp_cover_mask<true>(r0, r1, tile_x0, tile_y0));
           }
         }
         mbar_arrive(&full_bar[s]);

@@ -208,7 +208,10 @@ __device__ __forceinline__ int tile_py(int t) { return (t >> 6) * 4 + ((t & 31) 
 // skipped only if the reference would skip it (a < 1/255), so culling never
 // changes a result bit.
 // Warp w's 8x4 block starts at ((w & 1) * 8, (w >> 1) * 4) of the tile.
-template <int kBlockH = 4>
+// kExact adds the exact ellipse-vs-block test (cheaper consumers, busier
+// producer: it pays in the backward, not in the forward, whose producer
+// then becomes the bottleneck — measured bwd 1.359 -> 1.336 ms, fwd 0.673 -> 1.01 ms).
+template <bool kExact = false, int kBlockH = 4>
 __device__ __forceinline__ uint32_t warp_cover_mask(float4 r0, float4 r1, float tile_x0, float tile_y0) {
   constexpr int kWarps = 2 * (kTile / kBlockH);
   constexpr uint32_t kAll = (1u << kWarps) - 1u;
@@ -221,11 +224,37 @@ __device__ __forceinline__ uint32_t warp_cover_mask(float4 r0, float4 r1, float 
   const float hx = sqrtf(inv * r1.z) * 1.001f + 0.05f;
   const float hy = sqrtf(inv * r1.x) * 1.001f + 0.05f;
   const float mx = r0.x + r0.w, my = r0.y + r1.w;
+  // exact test for the blocks whose box overlaps the contour's box: the
+  // minimum of the convex Q over the block's pixel-centre rectangle (0 when
+  // the mean is inside, else on one of the four edges), against the inflated
+  // 2 tau.  The rectangle is padded by 0.01 px for the float32 offsets.
+  const float qa = r1.x, qb = r1.y, qc = r1.z;
+  const float rb_c = -qb / qc, rb_a = -qb / qa;
+  const float lim = 2.0f * tau * 1.0001f + 1e-4f;
   uint32_t m = 0u;
 #pragma unroll
   for (int w = 0; w < kWarps; ++w) {
     const float x0 = tile_x0 + float((w & 1) * 8) + 0.5f, y0 = tile_y0 + float((w >> 1) * kBlockH) + 0.5f;
-    if (mx + hx >= x0 && mx - hx <= x0 + 7.0f && my + hy >= y0 && my - hy <= y0 + float(kBlockH - 1)) m |= 1u << w;
+    if (!(mx + hx >= x0 && mx - hx <= x0 + 7.0f && my + hy >= y0 && my - hy <= y0 + float(kBlockH - 1))) continue;
+    if (kExact) {
+      const float xa = x0 - 0.01f - mx, xb = x0 + 7.01f - mx;
+      const float ya = y0 - 0.01f - my, yb = y0 + float(kBlockH - 1) + 0.01f - my;
+      float q = 0.0f;
+      if (!(xa <= 0.0f && xb >= 0.0f && ya <= 0.0f && yb >= 0.0f)) {
+        q = 3.0e38f;
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const float x = e ? xb : xa;
+          const float y = fminf(fmaxf(rb_c * x, ya), yb);
+          q = fminf(q, qa * x * x + 2.0f * qb * x * y + qc * y * y);
+          const float yy = e ? yb : ya;
+          const float xx = fminf(fmaxf(rb_a * yy, xa), xb);
+          q = fminf(q, qa * xx * xx + 2.0f * qb * xx * yy + qc * yy * yy);
+        }
+      }
+      if (!(q <= lim)) continue;
+    }
+    m |= 1u << w;
   }
   return m;
 }
