@@ -27,9 +27,12 @@ namespace {
 #ifndef GS_BWD_MIN_BLOCKS
 #define GS_BWD_MIN_BLOCKS 3  // 72 registers (small spill) beats 2 blocks at 96 (measured 1.69 vs 1.99 ms)
 #endif
-constexpr int kBatch = 256;
+#ifndef GS_BWD_BATCH
+#define GS_BWD_BATCH 64
+#endif
+constexpr int kBatch = GS_BWD_BATCH;
 #ifndef GS_BWD_STAGES
-#define GS_BWD_STAGES 3
+#define GS_BWD_STAGES 6
 #endif
 constexpr int kStages = GS_BWD_STAGES;
 constexpr int kConsumerWarps = 8;

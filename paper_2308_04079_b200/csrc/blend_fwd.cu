@@ -22,8 +22,14 @@
 namespace gs {
 namespace {
 
-constexpr int kBatch = 256;
-constexpr int kStages = 4;
+#ifndef GS_FWD_BATCH
+#define GS_FWD_BATCH 64
+#endif
+#ifndef GS_FWD_STAGES
+#define GS_FWD_STAGES 6
+#endif
+constexpr int kBatch = GS_FWD_BATCH;
+constexpr int kStages = GS_FWD_STAGES;
 constexpr int kConsumerWarps = 8;
 constexpr int kThreads = (kConsumerWarps + 1) * 32;
 

@@ -323,13 +323,12 @@ def bin_and_sort(splats: DeviceSplats, width: int, height: int) -> TileBinning:
     stream = _stream()
     cap = _capacity.get(device, n)
     for _ in range(2):
-        ws_bytes = ctypes.c_size_t(0)
-        _lib.check(lib.gs_bin_workspace_size(n, width, height, cap, ctypes.byref(ws_bytes)), "bin_and_sort")
-        ws = torch.empty(max(int(ws_bytes.value), 1), dtype=torch.uint8, device=device)
+        ws_bytes = _bin_workspace_bytes(n, width, height, cap)
+        ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=device)
         ids = torch.empty(max(cap, 1), dtype=torch.int32, device=device)
         ranges = torch.empty((tiles_x * tiles_y, 2), dtype=torch.int32, device=device)
         k = ctypes.c_int64(0)
-        st = lib.gs_bin_and_sort(ctypes.byref(cs), width, height, ws.data_ptr(), ws_bytes.value, cap,
+        st = lib.gs_bin_and_sort(ctypes.byref(cs), width, height, ws.data_ptr(), ws_bytes, cap,
                                  ids.data_ptr(), ranges.data_ptr(), ctypes.byref(k), stream)
         if st == _lib.GS_ERR_CAPACITY:
             _capacity.update(device, k.value, n)
@@ -341,6 +340,24 @@ def bin_and_sort(splats: DeviceSplats, width: int, height: int) -> TileBinning:
     raise RuntimeError("bin_and_sort: instance capacity did not converge")
 
 
+_ws_sizes: dict = {}
+
+
+def _bin_workspace_bytes(n: int, width: int, height: int, cap: int) -> int:
+    """gs_bin_workspace_size, memoised (a pure function of its arguments; the
+    query runs CUB's host-side size computations, a noticeable share of the
+    per-frame host time)."""
+    key = (n, width, height, cap)
+    b = _ws_sizes.get(key)
+    if b is None:
+        nbytes = ctypes.c_size_t(0)
+        _lib.check(_lib.load().gs_bin_workspace_size(n, width, height, cap, ctypes.byref(nbytes)), "bin_and_sort")
+        b = _ws_sizes[key] = int(nbytes.value)
+        if len(_ws_sizes) > 256:
+            _ws_sizes.pop(next(iter(_ws_sizes)))
+    return b
+
+
 def bin_and_sort_async(splats: DeviceSplats, width: int, height: int, capacity: int | None = None) -> TileBinning:
     """bin_and_sort without a host synchronisation: K stays on the device
     (binning.k_info) and the instance buffers are sized by `capacity`
@@ -350,9 +367,8 @@ def bin_and_sort_async(splats: DeviceSplats, width: int, height: int, capacity: 
     tiles_x, tiles_y = tile_extent(width, height)
     device = splats.rec.device
     cap = int(capacity) if capacity is not None else _capacity.get(device, len(splats))
-    ws_bytes = ctypes.c_size_t(0)
-    _lib.check(lib.gs_bin_workspace_size(len(splats), width, height, cap, ctypes.byref(ws_bytes)), "bin_and_sort")
-    ws = torch.empty(max(int(ws_bytes.value), 1), dtype=torch.uint8, device=device)
+    ws_bytes = _bin_workspace_bytes(len(splats), width, height, cap)
+    ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=device)
     ids = torch.empty(max(cap, 1), dtype=torch.int32, device=device)
     ranges = torch.empty((tiles_x * tiles_y, 2), dtype=torch.int32, device=device)
     k_info = torch.empty(3, dtype=torch.int64, device=device)
