@@ -22,6 +22,9 @@
 namespace gs {
 namespace {
 
+#ifndef GS_FWD_EXACT
+#define GS_FWD_EXACT 0   // exact ellipse-vs-block masks (see warp_cover_mask)
+#endif
 #ifndef GS_FWD_BATCH
 #define GS_FWD_BATCH 64
 #endif
@@ -73,7 +76,7 @@ __device__ __forceinline__ void produce_batch(FwdStage& st, RawRec& raw, const f
     if (e < cnt) {
       const float4 r0 = raw.r0[e], r1 = raw.r1[e];
       make_tile_splat(r0, r1, tile_x0, tile_y0, st.geo[e], st.geo2[e]);
-      st.mask[e] = uint8_t(warp_cover_mask(r0, r1, tile_x0, tile_y0));
+      st.mask[e] = uint8_t(warp_cover_mask<GS_FWD_EXACT != 0>(r0, r1, tile_x0, tile_y0));
     }
   }
 }

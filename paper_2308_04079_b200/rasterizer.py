@@ -373,7 +373,7 @@ def bin_and_sort_async(splats: DeviceSplats, width: int, height: int, capacity: 
     ranges = torch.empty((tiles_x * tiles_y, 2), dtype=torch.int32, device=device)
     k_info = torch.empty(3, dtype=torch.int64, device=device)
     cs = splats.c_struct()
-    _lib.check(lib.gs_bin_and_sort_async(ctypes.byref(cs), width, height, ws.data_ptr(), ws_bytes.value, cap,
+    _lib.check(lib.gs_bin_and_sort_async(ctypes.byref(cs), width, height, ws.data_ptr(), ws_bytes, cap,
                                          ids.data_ptr(), ranges.data_ptr(), k_info.data_ptr(), _stream()),
                "bin_and_sort")
     return TileBinning(ids, ranges, tiles_x, tiles_y, k_info, len(splats))
