@@ -4,7 +4,7 @@
 // One CTA per 16x16 tile: 8 consumer warps (one pixel per thread, each warp
 // an 8x4 pixel block) + 1 producer warp, warp-specialised over a ring of
 // kStages shared-memory batch buffers guarded by mbarriers:
-//   producer: for each 256-entry batch of the tile's sorted instance list,
+//   producer: for each kBatch-entry batch of the tile's sorted instance list,
 //     loads the Gaussian ids, gathers the 48-byte splat records with
 //     cp.async, computes each splat's 8-bit warp coverage mask
 //     (warp_cover_mask) and arrives on full[stage];
