@@ -202,6 +202,22 @@ int gs_bin_and_sort_async(const gs_splats_t* splats, int32_t width, int32_t heig
                           void* workspace, size_t workspace_bytes, int64_t k_capacity,
                           uint32_t* sorted_ids, int32_t* ranges, int64_t* k_info, void* stream);
 
+/* Banded binning (the same per-tile lists, built per band of tile rows so
+ * bands can overlap on separate streams):
+ *   gs_depth_order — order[r] = Gaussian of depth rank r (float32 depth, then
+ *     index; culled last), the shared first step;
+ *   gs_bin_rows_async — steps 2-5 for tile rows [tile_row_begin,
+ *     tile_row_end): its own instance list (sorted_ids, k_info as in
+ *     gs_bin_and_sort_async) and the ranges of its tiles, written into the
+ *     frame's (T,2) ranges array (which the caller zeroes once per frame). */
+int gs_depth_order_workspace_size(int64_t n, size_t* bytes);
+int gs_depth_order(const gs_splats_t* splats, void* workspace, size_t workspace_bytes, uint32_t* order,
+                   void* stream);
+int gs_bin_rows_workspace_size(int64_t n, int32_t width, int32_t height, int64_t k_capacity, size_t* bytes);
+int gs_bin_rows_async(const gs_splats_t* splats, const uint32_t* order, int32_t width, int32_t height,
+                      int32_t tile_row_begin, int32_t tile_row_end, void* workspace, size_t workspace_bytes,
+                      int64_t k_capacity, uint32_t* sorted_ids, int32_t* ranges, int64_t* k_info, void* stream);
+
 /* ---- K6 forward blend: replaces rasterizer.render_forward (rasterizer.py:201-240)
  * image (H,W,3) float32.  When training != 0, t_final (H,W) float32 and
  * last (H,W) int32 (global sorted index of the last blended instance, -1 =
@@ -209,6 +225,12 @@ int gs_bin_and_sort_async(const gs_splats_t* splats, int32_t width, int32_t heig
 int gs_blend_forward(const gs_splats_t* splats, const uint32_t* sorted_ids, const int32_t* ranges,
                      int32_t width, int32_t height, const float background[3], int32_t training,
                      float* image, float* t_final, int32_t* last, void* stream);
+/* The tiles of rows [tile_row_begin, tile_row_end) only (sorted_ids: that
+ * band's instance list from gs_bin_rows_async). */
+int gs_blend_forward_rows(const gs_splats_t* splats, const uint32_t* sorted_ids, const int32_t* ranges,
+                          int32_t width, int32_t height, int32_t tile_row_begin, int32_t tile_row_end,
+                          const float background[3], int32_t training, float* image, float* t_final,
+                          int32_t* last, void* stream);
 
 /* ---- K7 backward blend: replaces rasterizer.render_backward (rasterizer.py:253-316)
  * with gradients.backward_blend (gradients.py:30-94).
@@ -220,6 +242,12 @@ int gs_blend_backward(const float* d_image, const gs_splats_t* splats, const uin
                       const int32_t* ranges, const float* t_final, const int32_t* last,
                       int32_t width, int32_t height, const float background[3],
                       float* grads2d, void* stream);
+/* The tiles of rows [tile_row_begin, tile_row_end) only, ACCUMULATING into
+ * grads2d (not cleared: clear it once per frame, then one call per band). */
+int gs_blend_backward_rows(const float* d_image, const gs_splats_t* splats, const uint32_t* sorted_ids,
+                           const int32_t* ranges, const float* t_final, const int32_t* last, int32_t width,
+                           int32_t height, int32_t tile_row_begin, int32_t tile_row_end,
+                           const float background[3], float* grads2d, void* stream);
 
 /* ---- K8 backward preprocess: replaces gradients.backward_project
  * (gradients.py:192-259) and the densification statistics update of

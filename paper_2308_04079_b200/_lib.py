@@ -91,6 +91,16 @@ SIGNATURES = [
                                   c_void_p, POINTER(c_int64), c_void_p]),
     ("gs_bin_and_sort_async", c_int32, [POINTER(GsSplats), c_int32, c_int32, c_void_p, c_size_t, c_int64,
                                         c_void_p, c_void_p, c_void_p, c_void_p]),
+    ("gs_depth_order_workspace_size", c_int32, [c_int64, POINTER(c_size_t)]),
+    ("gs_depth_order", c_int32, [POINTER(GsSplats), c_void_p, c_size_t, c_void_p, c_void_p]),
+    ("gs_bin_rows_workspace_size", c_int32, [c_int64, c_int32, c_int32, c_int64, POINTER(c_size_t)]),
+    ("gs_bin_rows_async", c_int32, [POINTER(GsSplats), c_void_p, c_int32, c_int32, c_int32, c_int32, c_void_p,
+                                    c_size_t, c_int64, c_void_p, c_void_p, c_void_p, c_void_p]),
+    ("gs_blend_forward_rows", c_int32, [POINTER(GsSplats), c_void_p, c_void_p, c_int32, c_int32, c_int32, c_int32,
+                                        POINTER(c_float), c_int32, c_void_p, c_void_p, c_void_p, c_void_p]),
+    ("gs_blend_backward_rows", c_int32, [c_void_p, POINTER(GsSplats), c_void_p, c_void_p, c_void_p, c_void_p,
+                                         c_int32, c_int32, c_int32, c_int32, POINTER(c_float), c_void_p,
+                                         c_void_p]),
     ("gs_blend_forward", c_int32, [POINTER(GsSplats), c_void_p, c_void_p, c_int32, c_int32, POINTER(c_float),
                                    c_int32, c_void_p, c_void_p, c_void_p, c_void_p]),
     ("gs_blend_backward", c_int32, [c_void_p, POINTER(GsSplats), c_void_p, c_void_p, c_void_p, c_void_p, c_int32,

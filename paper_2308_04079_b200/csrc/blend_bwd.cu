@@ -101,14 +101,14 @@ __device__ __forceinline__ void batch_bounds(int b, int tile_top, int range_lo, 
 __global__ void __launch_bounds__(kThreads, GS_BWD_MIN_BLOCKS)
 blend_bwd_kernel(const float* __restrict__ d_image, const float4* __restrict__ rec, const uint32_t* __restrict__ ids,
                  const int2* __restrict__ ranges, const float* __restrict__ t_final, const int32_t* __restrict__ last,
-                 int width, int height, int tiles_x, float3 bg, float4* __restrict__ grads2d) {
+                 int width, int height, int tiles_x, int tile0, float3 bg, float4* __restrict__ grads2d) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   BwdStage* stages = reinterpret_cast<BwdStage*>(smem_raw);
   RawRec* raw = reinterpret_cast<RawRec*>(smem_raw + sizeof(BwdStage) * kStages);
   __shared__ uint64_t full_bar[kStages], empty_bar[kStages];
   __shared__ int s_warp_max[kConsumerWarps + 1];
 
-  const int tile = blockIdx.x;
+  const int tile = tile0 + int(blockIdx.x);
   const int t = threadIdx.x;
   const int lane = t & 31, warp = t >> 5;
   const bool consumer = warp < kConsumerWarps;
@@ -272,6 +272,33 @@ blend_bwd_kernel(const float* __restrict__ d_image, const float4* __restrict__ r
   }
 }
 
+int blend_backward_rows(const float* d_image, const gs_splats_t* splats, const uint32_t* sorted_ids,
+                        const int32_t* ranges, const float* t_final, const int32_t* last, int32_t width,
+                        int32_t height, int32_t row_begin, int32_t row_end, const float background[3],
+                        float* grads2d, void* stream) {
+  if (!d_image || !splats || !ranges || !t_final || !last || !grads2d || !background || width <= 0 ||
+      height <= 0)
+    return GS_ERR_INVALID_ARG;
+  const int tiles_x = (width + kTile - 1) / kTile, tiles_y = (height + kTile - 1) / kTile;
+  const int64_t tiles = int64_t(tiles_x) * tiles_y;
+  if (tiles > int64_t(INT32_MAX)) return GS_ERR_RESOURCE_LIMIT;
+  if (row_begin < 0 || row_end > tiles_y || row_begin > row_end) return GS_ERR_INVALID_ARG;
+  if (splats->n == 0 || row_begin == row_end) return GS_OK;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(blend_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(kSmemBytes));
+    if (e != cudaSuccess) return record_cuda_error(e);
+    configured = true;
+  }
+  const float3 bg = make_float3(background[0], background[1], background[2]);
+  const int64_t ntiles = int64_t(row_end - row_begin) * tiles_x;
+  blend_bwd_kernel<<<unsigned(ntiles), kThreads, kSmemBytes, static_cast<cudaStream_t>(stream)>>>(
+      d_image, reinterpret_cast<const float4*>(splats->rec), sorted_ids, reinterpret_cast<const int2*>(ranges),
+      t_final, last, width, height, tiles_x, row_begin * tiles_x, bg, reinterpret_cast<float4*>(grads2d));
+  return check_launch();
+}
+
 }  // namespace
 }  // namespace gs
 
@@ -279,25 +306,20 @@ extern "C" int gs_blend_backward(const float* d_image, const gs_splats_t* splats
                                  const int32_t* ranges, const float* t_final, const int32_t* last, int32_t width,
                                  int32_t height, const float background[3], float* grads2d, void* stream) {
   using namespace gs;
-  if (!d_image || !splats || !ranges || !t_final || !last || !grads2d || !background || width <= 0 ||
-      height <= 0)
-    return GS_ERR_INVALID_ARG;
-  const int tiles_x = (width + kTile - 1) / kTile, tiles_y = (height + kTile - 1) / kTile;
-  const int64_t tiles = int64_t(tiles_x) * tiles_y;
-  if (tiles > int64_t(INT32_MAX)) return GS_ERR_RESOURCE_LIMIT;
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  cudaError_t e = cudaMemsetAsync(grads2d, 0, size_t(splats->n) * GS_GRAD2D_FLOATS * sizeof(float), s);
+  if (!splats || !grads2d || width <= 0 || height <= 0) return GS_ERR_INVALID_ARG;
+  cudaError_t e = cudaMemsetAsync(grads2d, 0, size_t(splats->n) * GS_GRAD2D_FLOATS * sizeof(float),
+                                  static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return record_cuda_error(e);
-  if (splats->n == 0) return GS_OK;
-  static bool configured = false;
-  if (!configured) {
-    e = cudaFuncSetAttribute(blend_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmemBytes));
-    if (e != cudaSuccess) return record_cuda_error(e);
-    configured = true;
-  }
-  const float3 bg = make_float3(background[0], background[1], background[2]);
-  blend_bwd_kernel<<<unsigned(tiles), kThreads, kSmemBytes, s>>>(
-      d_image, reinterpret_cast<const float4*>(splats->rec), sorted_ids, reinterpret_cast<const int2*>(ranges),
-      t_final, last, width, height, tiles_x, bg, reinterpret_cast<float4*>(grads2d));
-  return check_launch();
+  return blend_backward_rows(d_image, splats, sorted_ids, ranges, t_final, last, width, height, 0,
+                             (height + kTile - 1) / kTile, background, grads2d, stream);
+}
+
+// The tiles of rows [tile_row_begin, tile_row_end) only, accumulating into
+// grads2d (not cleared here: one clear per frame, then one call per band).
+extern "C" int gs_blend_backward_rows(const float* d_image, const gs_splats_t* splats, const uint32_t* sorted_ids,
+                                      const int32_t* ranges, const float* t_final, const int32_t* last,
+                                      int32_t width, int32_t height, int32_t tile_row_begin, int32_t tile_row_end,
+                                      const float background[3], float* grads2d, void* stream) {
+  return gs::blend_backward_rows(d_image, splats, sorted_ids, ranges, t_final, last, width, height, tile_row_begin,
+                                 tile_row_end, background, grads2d, stream);
 }

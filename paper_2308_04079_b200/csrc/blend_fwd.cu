@@ -84,7 +84,7 @@ __device__ __forceinline__ void produce_batch(FwdStage& st, RawRec& raw, const f
 template <bool kTraining>
 __global__ void __launch_bounds__(kThreads)
 blend_fwd_kernel(const float4* __restrict__ rec, const uint32_t* __restrict__ ids, const int2* __restrict__ ranges,
-                 int width, int height, int tiles_x, float3 bg, float* __restrict__ image,
+                 int width, int height, int tiles_x, int tile0, float3 bg, float* __restrict__ image,
                  float* __restrict__ t_final, int32_t* __restrict__ last) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   FwdStage* stages = reinterpret_cast<FwdStage*>(smem_raw);
@@ -92,7 +92,7 @@ blend_fwd_kernel(const float4* __restrict__ rec, const uint32_t* __restrict__ id
   __shared__ uint64_t full_bar[kStages], empty_bar[kStages];
   __shared__ int s_done, s_stop;
 
-  const int tile = blockIdx.x;
+  const int tile = tile0 + int(blockIdx.x);
   const int t = threadIdx.x;
   const int lane = t & 31, warp = t >> 5;
   const int tx = tile % tiles_x, ty = tile / tiles_x;
@@ -198,8 +198,8 @@ blend_fwd_kernel(const float4* __restrict__ rec, const uint32_t* __restrict__ id
 }
 
 template <bool kTraining>
-int launch(const float4* rec, const uint32_t* ids, const int2* rg, int width, int height, int tiles_x, int64_t tiles,
-           float3 bg, float* image, float* t_final, int32_t* last, cudaStream_t s) {
+int launch(const float4* rec, const uint32_t* ids, const int2* rg, int width, int height, int tiles_x, int tile0,
+           int64_t ntiles, float3 bg, float* image, float* t_final, int32_t* last, cudaStream_t s) {
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(blend_fwd_kernel<kTraining>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -207,9 +207,30 @@ int launch(const float4* rec, const uint32_t* ids, const int2* rg, int width, in
     if (e != cudaSuccess) return record_cuda_error(e);
     configured = true;
   }
-  blend_fwd_kernel<kTraining><<<unsigned(tiles), kThreads, kSmemBytes, s>>>(rec, ids, rg, width, height, tiles_x, bg,
-                                                                            image, t_final, last);
+  if (ntiles <= 0) return GS_OK;
+  blend_fwd_kernel<kTraining><<<unsigned(ntiles), kThreads, kSmemBytes, s>>>(rec, ids, rg, width, height, tiles_x,
+                                                                             tile0, bg, image, t_final, last);
   return check_launch();
+}
+
+int blend_forward_rows(const gs_splats_t* splats, const uint32_t* sorted_ids, const int32_t* ranges, int32_t width,
+                       int32_t height, int32_t row_begin, int32_t row_end, const float background[3],
+                       int32_t training, float* image, float* t_final, int32_t* last, void* stream) {
+  if (!splats || !ranges || !image || !background || width <= 0 || height <= 0) return GS_ERR_INVALID_ARG;
+  if (training && (!t_final || !last)) return GS_ERR_INVALID_ARG;
+  const int tiles_x = (width + kTile - 1) / kTile, tiles_y = (height + kTile - 1) / kTile;
+  const int64_t tiles = int64_t(tiles_x) * tiles_y;
+  if (tiles > int64_t(INT32_MAX)) return GS_ERR_RESOURCE_LIMIT;
+  if (row_begin < 0 || row_end > tiles_y || row_begin > row_end) return GS_ERR_INVALID_ARG;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const float3 bg = make_float3(background[0], background[1], background[2]);
+  const float4* rec = reinterpret_cast<const float4*>(splats->rec);
+  const int2* rg = reinterpret_cast<const int2*>(ranges);
+  const int tile0 = row_begin * tiles_x;
+  const int64_t ntiles = int64_t(row_end - row_begin) * tiles_x;
+  if (training)
+    return launch<true>(rec, sorted_ids, rg, width, height, tiles_x, tile0, ntiles, bg, image, t_final, last, s);
+  return launch<false>(rec, sorted_ids, rg, width, height, tiles_x, tile0, ntiles, bg, image, nullptr, nullptr, s);
 }
 
 }  // namespace
@@ -218,16 +239,15 @@ int launch(const float4* rec, const uint32_t* ids, const int2* rg, int width, in
 extern "C" int gs_blend_forward(const gs_splats_t* splats, const uint32_t* sorted_ids, const int32_t* ranges,
                                 int32_t width, int32_t height, const float background[3], int32_t training,
                                 float* image, float* t_final, int32_t* last, void* stream) {
-  using namespace gs;
-  if (!splats || !ranges || !image || !background || width <= 0 || height <= 0) return GS_ERR_INVALID_ARG;
-  if (training && (!t_final || !last)) return GS_ERR_INVALID_ARG;
-  const int tiles_x = (width + kTile - 1) / kTile, tiles_y = (height + kTile - 1) / kTile;
-  const int64_t tiles = int64_t(tiles_x) * tiles_y;
-  if (tiles > int64_t(INT32_MAX)) return GS_ERR_RESOURCE_LIMIT;
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  const float3 bg = make_float3(background[0], background[1], background[2]);
-  const float4* rec = reinterpret_cast<const float4*>(splats->rec);
-  const int2* rg = reinterpret_cast<const int2*>(ranges);
-  if (training) return launch<true>(rec, sorted_ids, rg, width, height, tiles_x, tiles, bg, image, t_final, last, s);
-  return launch<false>(rec, sorted_ids, rg, width, height, tiles_x, tiles, bg, image, nullptr, nullptr, s);
+  if (width <= 0 || height <= 0) return GS_ERR_INVALID_ARG;
+  return gs::blend_forward_rows(splats, sorted_ids, ranges, width, height, 0, (height + gs::kTile - 1) / gs::kTile,
+                                background, training, image, t_final, last, stream);
+}
+
+extern "C" int gs_blend_forward_rows(const gs_splats_t* splats, const uint32_t* sorted_ids, const int32_t* ranges,
+                                     int32_t width, int32_t height, int32_t tile_row_begin, int32_t tile_row_end,
+                                     const float background[3], int32_t training, float* image, float* t_final,
+                                     int32_t* last, void* stream) {
+  return gs::blend_forward_rows(splats, sorted_ids, ranges, width, height, tile_row_begin, tile_row_end, background,
+                                training, image, t_final, last, stream);
 }

@@ -297,14 +297,14 @@ class _CapacityHint:
     HEADROOM = 1.05   # the async tile sort runs over the whole capacity: keep the padding small
 
     def get(self, device, n: int | None = None) -> int:
-        key = str(device)
+        key = device if isinstance(device, str) else str(device)
         k = self.k.get(key, 1 << 16)
         if n is not None and key in self.ratio:
             k = max(k, int(self.ratio[key] * n * self.HEADROOM) + 4096)
         return k
 
     def update(self, device, k: int, n: int | None = None) -> None:
-        key = str(device)
+        key = device if isinstance(device, str) else str(device)
         self.k[key] = max(self.k.get(key, 1 << 16), int(k * self.HEADROOM) + 4096)
         if n:
             self.ratio[key] = max(self.ratio.get(key, 0.0), k / n)
@@ -468,6 +468,150 @@ def render_view_async(cloud: GaussianCloud, camera, background, active_sh_degree
     binning = bin_and_sort_async(splats, camera.width, camera.height, capacity)
     out = render_forward(splats, binning, camera.width, camera.height, background, training=training)
     return out, splats, binning
+
+
+# ---------------------------------------------------------------------------
+# banded frames: the binning and the blends per band of tile rows, the bands
+# on their own CUDA streams so one band's latency-bound sort overlaps another
+# band's compute-bound blend (the per-tile lists, hence the images and
+# gradients, are those of the full-frame path)
+
+_side_streams: dict = {}
+
+
+def _streams(device, count: int) -> list:
+    key = str(device)
+    ss = _side_streams.setdefault(key, [])
+    while len(ss) < count:
+        ss.append(torch.cuda.Stream(device))
+    return ss[:count]
+
+
+def band_rows(tiles_y: int, bands: int) -> list[tuple[int, int]]:
+    bands = max(1, min(bands, tiles_y))
+    return [(tiles_y * b // bands, tiles_y * (b + 1) // bands) for b in range(bands)]
+
+
+@dataclass
+class BandedBinning:
+    """Per-band instance lists over one frame-wide ranges array."""
+
+    rows: list            # [(tile_row_begin, tile_row_end)]
+    splat_ids: list       # per band: (capacity,) int32
+    k_info: list          # per band: device int64 [K, flags, min(K, capacity)]
+    ranges: torch.Tensor  # (T,2) int32
+    tiles_x: int
+    tiles_y: int
+    keys: list            # capacity-hint keys
+
+    @property
+    def num_instances(self) -> int:
+        return sum(int(k[0].item()) for k in self.k_info)
+
+    def check(self) -> None:
+        self.check_host([k.tolist() for k in self.k_info])
+
+    def check_host(self, k_infos) -> None:
+        """Raise like TileBinning.check_host for the first band that failed
+        (every band's capacity hint is updated first)."""
+        errors = []
+        for key, ids, (k, flags, _) in zip(self.keys, self.splat_ids, k_infos):
+            _capacity.update(key, int(k))
+            errors.append((int(k), int(flags), ids.shape[0]))
+        for k, flags, cap in errors:
+            if flags & 1:
+                raise InvalidPrimitiveError("zero-norm quaternion cannot be normalized")
+            if flags & 4:
+                _lib.check(_lib.GS_ERR_RESOURCE_LIMIT, "bin_and_sort")
+            if flags & 2:
+                raise CapacityError(f"bin_and_sort: {k} instances exceed the band capacity {cap}")
+
+
+def render_view_banded(cloud: GaussianCloud, camera, background, active_sh_degree: int = 3, training: bool = False,
+                       bands: int = 2):
+    """render_view_async with the frame split into `bands` bands of tile rows,
+    binned and blended on separate CUDA streams after one shared projection
+    and depth order.  No host synchronisation; errors surface through
+    binning.check() (or check_host on a copy of the k_info tensors)."""
+    camera = _camera(camera)
+    lib = _lib.load()
+    device = cloud.device
+    n = len(cloud)
+    W, H = camera.width, camera.height
+    tiles_x, tiles_y = tile_extent(W, H)
+    splats = _project_tensors(cloud.c_params(), n, device, camera, active_sh_degree)
+    cs = splats.c_struct()
+    main = torch.cuda.current_stream(device)
+    # shared step: the depth order
+    dbytes = ctypes.c_size_t(0)
+    _lib.check(lib.gs_depth_order_workspace_size(n, ctypes.byref(dbytes)), "depth_order")
+    dws = torch.empty(max(int(dbytes.value), 1), dtype=torch.uint8, device=device)
+    order = torch.empty(max(n, 1), dtype=torch.int32, device=device)
+    _lib.check(lib.gs_depth_order(ctypes.byref(cs), dws.data_ptr(), dbytes.value, order.data_ptr(),
+                                  main.cuda_stream), "depth_order")
+    ranges = torch.zeros((tiles_x * tiles_y, 2), dtype=torch.int32, device=device)
+    image = torch.empty((H, W, 3), dtype=torch.float32, device=device)
+    t_final = torch.empty((H, W), dtype=torch.float32, device=device) if training else None
+    last = torch.empty((H, W), dtype=torch.int32, device=device) if training else None
+    rows = band_rows(tiles_y, bands)
+    keys = [f"{device}/band{b}of{len(rows)}@{W}x{H}" for b in range(len(rows))]
+    # every buffer is allocated on the main stream, before the side streams use it
+    per_band = []
+    for (y0, y1), key in zip(rows, keys):
+        if key in _capacity.k:
+            cap = _capacity.get(key)
+        else:   # first frame of this band layout: the frame-wide hint, pro rata, with a margin
+            cap = int(_capacity.get(device, n) * 1.3 * (y1 - y0) / tiles_y) + 4096
+        nbytes = ctypes.c_size_t(0)
+        _lib.check(lib.gs_bin_rows_workspace_size(n, W, H, cap, ctypes.byref(nbytes)), "bin_rows")
+        per_band.append((cap, int(nbytes.value), torch.empty(max(int(nbytes.value), 1), dtype=torch.uint8,
+                                                               device=device),
+                         torch.empty(max(cap, 1), dtype=torch.int32, device=device),
+                         torch.empty(3, dtype=torch.int64, device=device)))
+    ready = torch.cuda.Event()
+    ready.record(main)
+    bg = _bg(background)
+    for (y0, y1), stream, (cap, nbytes, ws, ids, kinfo) in zip(rows, _streams(device, len(rows)), per_band):
+        stream.wait_event(ready)
+        _lib.check(lib.gs_bin_rows_async(ctypes.byref(cs), order.data_ptr(), W, H, y0, y1, ws.data_ptr(), nbytes, cap,
+                                         ids.data_ptr(), ranges.data_ptr(), kinfo.data_ptr(), stream.cuda_stream),
+                   "bin_rows")
+        _lib.check(lib.gs_blend_forward_rows(ctypes.byref(cs), ids.data_ptr(), ranges.data_ptr(), W, H, y0, y1, bg,
+                                             int(bool(training)), image.data_ptr(), _lib.ptr(t_final), _lib.ptr(last),
+                                             stream.cuda_stream), "render_forward")
+    for stream in _streams(device, len(rows)):
+        main.wait_stream(stream)
+    binning = BandedBinning(rows, [b[3] for b in per_band], [b[4] for b in per_band], ranges, tiles_x, tiles_y, keys)
+    return RenderOutput(image, t_final, last), splats, binning
+
+
+def render_backward_banded(d_image: torch.Tensor, output: RenderOutput, splats: DeviceSplats,
+                           binning: BandedBinning, width: int, height: int, background) -> SplatGrads2D:
+    """render_backward over the bands of a render_view_banded frame, one
+    stream per band, accumulating into one cleared gradient buffer."""
+    if output.final_transmittance is None or output.last_contributor is None:
+        raise ValueError("backward pass needs a training-mode RenderOutput")  # rasterizer.py:265-266
+    lib = _lib.load()
+    device = splats.rec.device
+    d_image = d_image.to(dtype=torch.float32).contiguous()
+    if tuple(d_image.shape) != (height, width, 3):
+        raise ValueError(f"d_image shape {tuple(d_image.shape)} != {(height, width, 3)}")
+    packed = torch.zeros((len(splats), _lib.GRAD2D_FLOATS), dtype=torch.float32, device=device)
+    cs = splats.c_struct()
+    main = torch.cuda.current_stream(device)
+    ready = torch.cuda.Event()
+    ready.record(main)
+    bg = _bg(background)
+    streams = _streams(device, len(binning.rows))
+    for (y0, y1), stream, ids in zip(binning.rows, streams, binning.splat_ids):
+        stream.wait_event(ready)
+        _lib.check(lib.gs_blend_backward_rows(d_image.data_ptr(), ctypes.byref(cs), ids.data_ptr(),
+                                              binning.ranges.data_ptr(), output.final_transmittance.data_ptr(),
+                                              output.last_contributor.data_ptr(), width, height, y0, y1, bg,
+                                              packed.data_ptr(), stream.cuda_stream), "render_backward")
+    for stream in streams:
+        main.wait_stream(stream)
+    return SplatGrads2D(packed)
 
 
 # ---------------------------------------------------------------------------
