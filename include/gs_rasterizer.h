@@ -39,7 +39,7 @@ extern "C" {
 #define GS_ABI_VERSION 1
 #define GS_TILE_SIZE 16        /* rasterizer.py:13 TILE_SIZE */
 #define GS_SH_COEFFS 16        /* sh.py:25 NUM_COEFFS */
-#define GS_REC_FLOATS 16       /* floats per projected-splat record, see gs_splats_t */
+#define GS_REC_FLOATS 20       /* floats per projected-splat record, see gs_splats_t */
 #define GS_GRAD2D_FLOATS 12    /* floats per screen-space gradient row, see gs_blend_backward */
 #define GS_MODEL_FLOATS 59     /* scene_io.py:374-376 model record (236 B) */
 #define GS_PLY_FLOATS 62       /* scene_io.py:417-439 PLY vertex */
@@ -82,13 +82,16 @@ typedef struct gs_params {
  * counterpart of ProjectedSplats, core.py:236-263, kept in N-space instead of
  * compacted; a row is a survivor of project() iff radii[row] > 0).
  *
- *   rec (N,16) float32, four 16-byte words per row:
- *     [0..3]   mean2d.x (hi), mean2d.y (hi), alpha (hi), mean2d.x (lo)
- *     [4..7]   conic a, b, c (hi), mean2d.y (lo)
- *     [8..11]  color r, g, b, clamp mask (bits 0..2 as float: channel active)
- *     [12..15] conic a, b, c (lo), alpha (lo)
- *   hi + lo reproduces the float64 value to ~2^-48; the blend kernels read
- *   the lo word only for the rare pairs whose alpha sits at a threshold.
+ *   rec (N,20) float32, five 16-byte words per row:
+ *     [0..3]   mean2d.x (hi), mean2d.y (hi), mean2d.x (lo), mean2d.y (lo)
+ *     [4..7]   conic eigenbasis k = (k1.x, k1.y, k2.x, k2.y), k_i = sqrt(log2(e) lambda_i / 2) e_i,
+ *              so log2(e) * power = -(k1.d)^2 - (k2.d)^2 for d = pixel - mean2d
+ *     [8..11]  color r, g, b, alpha (hi)
+ *     [12..15] conic a, b, c (hi), clamp mask (bits 0..2 as float: channel active)
+ *     [16..19] conic a, b, c (lo), alpha (lo)
+ *   hi + lo reproduces the float64 value to ~2^-48; the blend kernels gather
+ *   words 0..2 per (splat, tile) and read words 3..4 only for the rare pairs
+ *   whose alpha sits at a threshold.
  *   depth (N,)  float32 view-space z (the sort key's source, rasterizer.py:61)
  *   radii (N,)  int32 ceil(3 sqrt(lambda_max)), 0 = culled
  *   rect  (N,4) int32 clipped inclusive tile rectangle x0,y0,x1,y1

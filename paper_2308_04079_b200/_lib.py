@@ -21,7 +21,7 @@ GS_ERR_RESOURCE_LIMIT = 3
 GS_ERR_CAPACITY = 4
 GS_ERR_CUDA = 5
 
-REC_FLOATS = 16
+REC_FLOATS = 20
 MODEL_FLOATS = 59
 PLY_FLOATS = 62
 LAYOUT_MODEL = 0

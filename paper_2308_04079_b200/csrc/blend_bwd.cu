@@ -41,15 +41,15 @@ constexpr int kG = 2;    // splats per reduction group (group_reduce2)
 constexpr int kC = 9;    // gradient components per splat
 
 struct BwdStage {
-  float4 geo[kBatch];    // (mx - tile_x0, my - tile_y0, A, B), see make_tile_splat
+  float4 k[kBatch];      // eigenbasis rows (record word 1), see make_tile_splat
+  float4 m[kBatch];      // (-k1 . mean_rel, -k2 . mean_rel, alpha, 0)
   float4 col[kBatch];
-  float2 geo2[kBatch];   // (C, alpha)
+  float2 ctr[kBatch];    // mean - tile origin
   uint32_t id[kBatch];
   uint8_t mask[kBatch];
 };
 struct RawRec {          // the producer's landing buffer for the cp.async gathers
   float4 r0[kBatch];
-  float4 r1[kBatch];
 };
 constexpr size_t kSmemBytes = sizeof(BwdStage) * kStages + sizeof(RawRec);
 
@@ -172,10 +172,10 @@ blend_bwd_kernel(const float* __restrict__ d_image, const float4* __restrict__ r
         for (int u = 0; u < kBatch / 32; ++u) {
           const int e = lane + 32 * u;
           if (e < cnt) {
-            const float4* src = rec + 4 * size_t(gid[u]);
+            const float4* src = rec + kRecWords * size_t(gid[u]);
             st.id[e] = gid[u];
             cp_async16(&raw->r0[e], src + 0);
-            cp_async16(&raw->r1[e], src + 1);
+            cp_async16(&st.k[e], src + 1);
             cp_async16(&st.col[e], src + 2);
           }
         }
@@ -184,9 +184,10 @@ blend_bwd_kernel(const float* __restrict__ d_image, const float4* __restrict__ r
         for (int u = 0; u < kBatch / 32; ++u) {
           const int e = lane + 32 * u;
           if (e < cnt) {
-            const float4 r0 = raw->r0[e], r1 = raw->r1[e];
-            make_tile_splat(r0, r1, tile_x0, tile_y0, st.geo[e], st.geo2[e]);
-            st.mask[e] = uint8_t(warp_cover_mask<true>(r0, r1, tile_x0, tile_y0));
+            const float4 r0 = raw->r0[e], k = st.k[e];
+            const float alpha = st.col[e].w;
+            make_tile_splat(r0, k, alpha, tile_x0, tile_y0, st.m[e], st.ctr[e]);
+            st.mask[e] = uint8_t(warp_cover_mask<true>(r0, k, alpha, tile_x0, tile_y0));
           }
         }
         mbar_arrive(&full_bar[s]);
@@ -222,9 +223,8 @@ blend_bwd_kernel(const float* __restrict__ d_image, const float4* __restrict__ r
 #pragma unroll
           for (int u = 0; u < kG; ++u) {
             const int j = max(js[u], 0);
-            const float4 geo = st.geo[j];
-            const float2 geo2 = st.geo2[j];
-            const AlphaEval e = eval_alpha_tile(lx, ly, fx, fy, geo, geo2, rec, st.id, j);
+            const float4 kk = st.k[j];
+            const AlphaEval e = eval_alpha_tile(lx, ly, fx, fy, kk, st.m[j], rec, st.id, j);
             // branch-free body: lanes past their last contributor (or the
             // padding slots of a short group) evaluate with a = 0, which
             // leaves T and S unchanged and zeroes every gradient term
@@ -244,14 +244,17 @@ blend_bwd_kernel(const float* __restrict__ d_image, const float4* __restrict__ r
             v[u * kC + 7] = w * dly;
             v[u * kC + 8] = w * dlz;
             const float dp = d_a * e.a_raw;
-            // d power / d mean = (a dx + b dy, b dx + c dy) = -(2A dx + B dy, B dx + 2C dy) / log2(e)
-            const float q = dp * (-1.0f / kLog2e);
-            v[u * kC + 0] = q * (2.0f * geo.z * e.dx + geo.w * e.dy);   // d_mean2d.x
-            v[u * kC + 1] = q * (geo.w * e.dx + 2.0f * geo2.x * e.dy);  // d_mean2d.y
-            v[u * kC + 2] = d_a * e.g;                                  // d_alpha
-            v[u * kC + 3] = -0.5f * dp * e.dx * e.dx;                   // d_conic a
-            v[u * kC + 4] = -dp * e.dx * e.dy;                          // d_conic b
-            v[u * kC + 5] = -0.5f * dp * e.dy * e.dy;                   // d_conic c
+            // d power / d mean = (a dx + b dy, b dx + c dy) = 2 (v1 k1 + v2 k2) / log2(e)
+            // (eigenbasis form: no cancellation for elongated conics)
+            const float q = dp * (2.0f / kLog2e);
+            v[u * kC + 0] = q * fmaf(e.v1, kk.x, e.v2 * kk.z);   // d_mean2d.x
+            v[u * kC + 1] = q * fmaf(e.v1, kk.y, e.v2 * kk.w);   // d_mean2d.y
+            v[u * kC + 2] = d_a * e.g;                           // d_alpha
+            const float2 c2 = st.ctr[j];
+            const float dx = lx - c2.x, dy = ly - c2.y;
+            v[u * kC + 3] = -0.5f * dp * dx * dx;                // d_conic a
+            v[u * kC + 4] = -dp * dx * dy;                       // d_conic b
+            v[u * kC + 5] = -0.5f * dp * dy * dy;                // d_conic c
           }
           if (!__any_sync(0xffffffffu, any)) continue;
           float out, out8;

@@ -37,15 +37,14 @@ constexpr int kConsumerWarps = 8;
 constexpr int kThreads = (kConsumerWarps + 1) * 32;
 
 struct FwdStage {
-  float4 geo[kBatch];    // (mx - tile_x0, my - tile_y0, A, B), see make_tile_splat
+  float4 k[kBatch];      // eigenbasis rows (record word 1), see make_tile_splat
+  float4 m[kBatch];      // (-k1 . mean_rel, -k2 . mean_rel, alpha, 0)
   float4 col[kBatch];
-  float2 geo2[kBatch];   // (C, alpha)
   uint32_t id[kBatch];
   uint8_t mask[kBatch];
 };
 struct RawRec {          // the producer's landing buffer for the cp.async gathers
   float4 r0[kBatch];
-  float4 r1[kBatch];
 };
 constexpr size_t kSmemBytes = sizeof(FwdStage) * kStages + sizeof(RawRec);
 
@@ -62,10 +61,10 @@ __device__ __forceinline__ void produce_batch(FwdStage& st, RawRec& raw, const f
   for (int u = 0; u < kBatch / 32; ++u) {
     const int e = lane + 32 * u;
     if (e < cnt) {
-      const float4* src = rec + 4 * size_t(gid[u]);
+      const float4* src = rec + kRecWords * size_t(gid[u]);
       st.id[e] = gid[u];
       cp_async16(&raw.r0[e], src + 0);
-      cp_async16(&raw.r1[e], src + 1);
+      cp_async16(&st.k[e], src + 1);
       cp_async16(&st.col[e], src + 2);
     }
   }
@@ -74,9 +73,11 @@ __device__ __forceinline__ void produce_batch(FwdStage& st, RawRec& raw, const f
   for (int u = 0; u < kBatch / 32; ++u) {
     const int e = lane + 32 * u;
     if (e < cnt) {
-      const float4 r0 = raw.r0[e], r1 = raw.r1[e];
-      make_tile_splat(r0, r1, tile_x0, tile_y0, st.geo[e], st.geo2[e]);
-      st.mask[e] = uint8_t(warp_cover_mask<GS_FWD_EXACT != 0>(r0, r1, tile_x0, tile_y0));
+      const float4 r0 = raw.r0[e], k = st.k[e];
+      const float alpha = st.col[e].w;
+      float2 ctr;
+      make_tile_splat(r0, k, alpha, tile_x0, tile_y0, st.m[e], ctr);
+      st.mask[e] = uint8_t(warp_cover_mask<GS_FWD_EXACT != 0>(r0, k, alpha, tile_x0, tile_y0));
     }
   }
 }
@@ -160,7 +161,7 @@ blend_fwd_kernel(const float4* __restrict__ rec, const uint32_t* __restrict__ id
           live &= live - 1;
           // branch-light body: finished lanes evaluate too (free under SIMT)
           // and are masked by `take`
-          const AlphaEval e = eval_alpha_tile(lx, ly, fx, fy, st.geo[j], st.geo2[j], rec, st.id, j);
+          const AlphaEval e = eval_alpha_tile(lx, ly, fx, fy, st.k[j], st.m[j], rec, st.id, j);
           const float t_new = T * (1.0f - e.a);
           const bool blend = !done && e.a > 0.0f;
           const bool sat = t_new < kTransSat;  // 1 - T_new > 0.9999

@@ -82,13 +82,18 @@ __host__ inline DevCamera make_dev_camera(const gs_camera_t& c) {
 // 0.99 the pair is re-evaluated in float64 from the split records
 // (mean, conic and opacity hi + lo), so the skip / clamp decisions agree with
 // the float64 reference.  The float32 fast path is accurate to < 5e-6
-// relative, kGuard = 1e-5 covers it; about 4e-5 of pairs take the slow path.
+// relative for every conic conditioning (eigenbasis form, see
+// make_tile_splat), kGuard = 1e-5 covers it; about 4e-5 of pairs take the
+// slow path.
 struct AlphaEval {
-  float dx, dy, g, a_raw, a;   // a: clamped and eps-skipped alpha (0 = skip)
+  float v1, v2, g, a_raw, a;   // v: eigenbasis offsets; a: clamped and eps-skipped alpha (0 = skip)
   bool live;                   // a_raw < 0.99: the pair passes gradient to alpha/power
 };
 
-constexpr float kGuard = 1e-5f;
+#ifndef GS_ALPHA_GUARD
+#define GS_ALPHA_GUARD 1e-5f
+#endif
+constexpr float kGuard = GS_ALPHA_GUARD;
 
 __device__ __forceinline__ float ex2_approx(float x) {
   float y;
@@ -104,15 +109,21 @@ __device__ __forceinline__ float rcp_approx(float x) {
   return y;
 }
 
-// Record layout (gs_splats_t.rec, 4 x float4 per Gaussian):
-//   r0 = (mx_hi, my_hi, alpha_hi, mx_lo)   r1 = (ca_hi, cb_hi, cc_hi, my_lo)
-//   r2 = (r, g, b, mask)                   r3 = (ca_lo, cb_lo, cc_lo, alpha_lo)
+// Record layout (gs_splats_t.rec, kRecWords x float4 per Gaussian):
+//   r0 = (mx_hi, my_hi, mx_lo, my_lo)      r1 = k = (k1.x, k1.y, k2.x, k2.y)  (conic_basis)
+//   r2 = (r, g, b, alpha_hi)               r3 = (ca_hi, cb_hi, cc_hi, mask)
+//   r4 = (ca_lo, cb_lo, cc_lo, alpha_lo)
+// The blend producers gather r0..r2 (48 B); r3, r4 are read by the float64
+// slow path and the projection backward only.
+constexpr int kRecWords = 5;
+
 // Returns (G, a_raw, a, live) by value (registers, no local memory).
-static __device__ __noinline__ float4 alpha_f64(float px, float py, float4 r0, float4 r1, float4 r3) {
-  const double dx = double(px) - (double(r0.x) + double(r0.w));
-  const double dy = double(py) - (double(r0.y) + double(r1.w));
-  const double ca = double(r1.x) + double(r3.x), cb = double(r1.y) + double(r3.y), cc = double(r1.z) + double(r3.z);
-  const double al = double(r0.z) + double(r3.w);
+static __device__ __noinline__ float4 alpha_f64(float px, float py, const float4* __restrict__ r) {
+  const float4 r0 = r[0], r2 = r[2], r3 = r[3], r4 = r[4];
+  const double dx = double(px) - (double(r0.x) + double(r0.z));
+  const double dy = double(py) - (double(r0.y) + double(r0.w));
+  const double ca = double(r3.x) + double(r4.x), cb = double(r3.y) + double(r4.y), cc = double(r3.z) + double(r4.z);
+  const double al = double(r2.w) + double(r4.w);
   const double power = -0.5 * (ca * dx * dx + cc * dy * dy) - cb * dx * dy;
   const double g = power > 0.0 ? 0.0 : exp(power);
   const double ar = al * g;
@@ -120,33 +131,12 @@ static __device__ __noinline__ float4 alpha_f64(float px, float py, float4 r0, f
   return make_float4(float(g), float(ar), (a < 1.0 / 255.0) ? 0.0f : float(a), ar < 0.99 ? 1.0f : 0.0f);
 }
 
-__device__ __forceinline__ void eval_alpha_f64(float px, float py, float4 r0, float4 r1, float4 r3, AlphaEval& e) {
-  const float4 v = alpha_f64(px, py, r0, r1, r3);
+__device__ __forceinline__ void eval_alpha_f64(float px, float py, const float4* __restrict__ r, AlphaEval& e) {
+  const float4 v = alpha_f64(px, py, r);
   e.g = v.x;
   e.a_raw = v.y;
   e.a = v.z;
   e.live = v.w != 0.0f;
-}
-
-__device__ __forceinline__ AlphaEval eval_alpha(float px, float py, float4 r0, float4 r1,
-                                                const float4* __restrict__ rec, uint32_t gid) {
-  AlphaEval e;
-  e.dx = __fsub_rn(__fsub_rn(px, r0.x), r0.w);
-  e.dy = __fsub_rn(__fsub_rn(py, r0.y), r1.w);
-  const float qa = __fmul_rn(__fmul_rn(r1.x, e.dx), e.dx);
-  const float qc = __fmul_rn(__fmul_rn(r1.z, e.dy), e.dy);
-  const float qb = __fmul_rn(__fmul_rn(r1.y, e.dx), e.dy);
-  const float power = __fsub_rn(__fmul_rn(-0.5f, __fadd_rn(qa, qc)), qb);
-  e.g = (power > 0.0f) ? 0.0f : ex2_approx(__fmul_rn(power, 1.4426950408889634f));
-  e.a_raw = __fmul_rn(r0.z, e.g);
-  if (fabsf(e.a_raw - kAlphaEps) <= kGuard * kAlphaEps || fabsf(e.a_raw - kAlphaClamp) <= kGuard) {
-    eval_alpha_f64(px, py, r0, r1, rec[4 * size_t(gid) + 3], e);
-    return e;
-  }
-  e.live = e.a_raw < kAlphaClamp;
-  const float a = fminf(kAlphaClamp, e.a_raw);
-  e.a = (a < kAlphaEps) ? 0.0f : a;
-  return e;
 }
 
 // ---------------------------------------------------------------------------
@@ -212,25 +202,28 @@ __device__ __forceinline__ int tile_py(int t) { return (t >> 6) * 4 + ((t & 31) 
 // producer: it pays in the backward, not in the forward, whose producer
 // then becomes the bottleneck — measured bwd 1.359 -> 1.336 ms, fwd 0.673 -> 1.01 ms).
 template <bool kExact = false, int kBlockH = 4>
-__device__ __forceinline__ uint32_t warp_cover_mask(float4 r0, float4 r1, float tile_x0, float tile_y0) {
+__device__ __forceinline__ uint32_t warp_cover_mask(float4 r0, float4 k, float alpha, float tile_x0, float tile_y0) {
   constexpr int kWarps = 2 * (kTile / kBlockH);
   constexpr uint32_t kAll = (1u << kWarps) - 1u;
-  const float alpha = r0.z;
   if (alpha < kAlphaEps * (1.0f - 1e-5f)) return 0u;
-  const float tau = fmaxf(__logf(255.0f * alpha), 0.0f) * 1.0001f + 1e-4f;
-  const float det = r1.x * r1.z - r1.y * r1.y;
-  if (!(det > 0.0f)) return kAll;  // degenerate conic: never cull
-  const float inv = 2.0f * tau / det;
-  const float hx = sqrtf(inv * r1.z) * 1.001f + 0.05f;
-  const float hy = sqrtf(inv * r1.x) * 1.001f + 0.05f;
-  const float mx = r0.x + r0.w, my = r0.y + r1.w;
+  // alpha 2^-(|k d|^2) >= 1/255  <=>  |k d|^2 <= tau = log2(255 alpha)
+  const float tau = fmaxf(__log2f(255.0f * alpha), 0.0f) * 1.0001f + 1e-4f;
+  // det k = f1 f2 (ex^2 + ey^2): a sum of same-signed terms, no cancellation
+  const float detk = k.x * k.w - k.y * k.z;
+  if (!(detk > 0.0f)) return kAll;  // degenerate basis: never cull
+  // the contour's half extents: sqrt(tau) |row of k^-1|
+  const float st = sqrtf(tau) / detk;
+  const float hx = st * sqrtf(k.y * k.y + k.w * k.w) * 1.001f + 0.05f;
+  const float hy = st * sqrtf(k.x * k.x + k.z * k.z) * 1.001f + 0.05f;
+  const float mx = r0.x + r0.z, my = r0.y + r0.w;
   // exact test for the blocks whose box overlaps the contour's box: the
-  // minimum of the convex Q over the block's pixel-centre rectangle (0 when
-  // the mean is inside, else on one of the four edges), against the inflated
-  // 2 tau.  The rectangle is padded by 0.01 px for the float32 offsets.
-  const float qa = r1.x, qb = r1.y, qc = r1.z;
+  // minimum of the convex |k d|^2 over the block's pixel-centre rectangle (0
+  // when the mean is inside, else on one of the four edges; the edge
+  // minimiser comes from the expanded form, the value is evaluated as a sum
+  // of squares), against the inflated tau.  The rectangle is padded by 0.01 px.
+  const float qa = k.x * k.x + k.z * k.z, qb = k.x * k.y + k.z * k.w, qc = k.y * k.y + k.w * k.w;
   const float rb_c = -qb / qc, rb_a = -qb / qa;
-  const float lim = 2.0f * tau * 1.0001f + 1e-4f;
+  const float lim = tau * 1.0001f + 1e-4f;
   uint32_t m = 0u;
 #pragma unroll
   for (int w = 0; w < kWarps; ++w) {
@@ -242,14 +235,16 @@ __device__ __forceinline__ uint32_t warp_cover_mask(float4 r0, float4 r1, float 
       float q = 0.0f;
       if (!(xa <= 0.0f && xb >= 0.0f && ya <= 0.0f && yb >= 0.0f)) {
         q = 3.0e38f;
+        auto sq = [&](float x, float y) {
+          const float u = fmaf(k.x, x, k.y * y), v = fmaf(k.z, x, k.w * y);
+          return fmaf(u, u, v * v);
+        };
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           const float x = e ? xb : xa;
-          const float y = fminf(fmaxf(rb_c * x, ya), yb);
-          q = fminf(q, qa * x * x + 2.0f * qb * x * y + qc * y * y);
+          q = fminf(q, sq(x, fminf(fmaxf(rb_c * x, ya), yb)));
           const float yy = e ? yb : ya;
-          const float xx = fminf(fmaxf(rb_a * yy, xa), xb);
-          q = fminf(q, qa * xx * xx + 2.0f * qb * xx * yy + qc * yy * yy);
+          q = fminf(q, sq(fminf(fmaxf(rb_a * yy, xa), xb), yy));
         }
       }
       if (!(q <= lim)) continue;
@@ -335,40 +330,63 @@ __device__ __forceinline__ void prefetch_l2_span(const void* ptr, size_t bytes) 
 __device__ __forceinline__ int ld_volatile(const int* p) { return *reinterpret_cast<const volatile int*>(p); }
 
 // ---------------------------------------------------------------------------
-// Per-(splat, tile) blend record, built once by the producer warp:
-//   geo  = (mx - tile_x0, my - tile_y0, A, B)     (tile-relative mean, from hi+lo in f64)
-//   geo2 = (C, alpha)
-// with (A, B, C) = -log2(e) * (a/2, b, c/2): the exponent in log2 units is
-//   p2 = A dx^2 + B dx dy + C dy^2 = log2(e) * power,  G = 2^p2
-// so the per-pixel evaluation needs no constant multiplies.  Both blend
-// kernels evaluate from the same records with the same intrinsics, so their
-// alphas (and contributor sets) are bit-identical; near the 1/255 and 0.99
-// thresholds the float64 slow path (eval_alpha_f64) decides from the global
-// hi/lo record.
+// The exponent is evaluated as a sum of two squares in the conic's eigenbasis,
+//   p2 = log2(e) * power = -(v1^2 + v2^2),   v_i = k_i . (p - mean),
+//   k_i = sqrt(log2(e) * lambda_i / 2) * e_i   (lambda_i, e_i: conic eigenpairs)
+// so no cancellation occurs for elongated (near-singular) conics: the
+// expanded form a dx^2 + 2b dx dy + c dy^2 loses ~cond(conic) * 6e-8 of
+// relative accuracy in float32, which for needle-like splats (cond ~1e4)
+// exceeds the parity tolerance.  conic_basis runs once per Gaussian in the
+// projection (float64, from the float64 conic and its determinant).
 constexpr float kLog2e = 1.4426950408889634f;
 
-__device__ __forceinline__ void make_tile_splat(float4 r0, float4 r1, float tile_x0, float tile_y0, float4& geo,
-                                                float2& geo2) {
-  const double mx = (double(r0.x) + double(r0.w)) - double(tile_x0);
-  const double my = (double(r0.y) + double(r1.w)) - double(tile_y0);
-  geo = make_float4(float(mx), float(my), -0.5f * kLog2e * r1.x, -kLog2e * r1.y);
-  geo2 = make_float2(-0.5f * kLog2e * r1.z, r0.z);
+__device__ __forceinline__ float4 conic_basis(double a, double b, double c, double det) {
+  const double h = 0.5 * (a - c);
+  const double r = sqrt(h * h + b * b);
+  const double l1 = 0.5 * (a + c) + r;             // larger eigenvalue, no cancellation
+  const double l2 = l1 > 0.0 ? fmax(det, 0.0) / l1 : 0.0;  // smaller one from the determinant
+  double ex = h >= 0.0 ? h + r : b, ey = h >= 0.0 ? b : r - h;  // whichever form does not cancel
+  const double nn = sqrt(ex * ex + ey * ey);
+  if (nn > 0.0) {
+    ex /= nn;
+    ey /= nn;
+  } else {
+    ex = 1.0;
+    ey = 0.0;
+  }
+  const double f1 = sqrt(0.5 * double(kLog2e) * l1), f2 = sqrt(0.5 * double(kLog2e) * l2);
+  return make_float4(float(f1 * ex), float(f1 * ey), float(-f2 * ey), float(f2 * ex));
+}
+
+// Per-(splat, tile) blend record, built once by the producer warp from r0, r1:
+//   k   = r1
+//   m   = (-k1 . mean_rel, -k2 . mean_rel, alpha, 0)
+//   ctr = mean_rel = mean - tile origin (the backward's d_conic offsets)
+// so a pixel costs four FFMA + FMUL + FFMA, and p2 <= 0 by construction.
+// Both blend kernels evaluate from the same records with the same
+// intrinsics, so their alphas (and contributor sets) are bit-identical; near
+// the 1/255 and 0.99 thresholds the float64 slow path (eval_alpha_f64)
+// decides from the global hi/lo record.
+__device__ __forceinline__ void make_tile_splat(float4 r0, float4 k, float alpha, float tile_x0, float tile_y0,
+                                                float4& m, float2& ctr) {
+  // tile-relative mean in float32 (two roundings, < 1 ulp of |mean_rel|)
+  const float mx = __fadd_rn(__fsub_rn(r0.x, tile_x0), r0.z);
+  const float my = __fadd_rn(__fsub_rn(r0.y, tile_y0), r0.w);
+  m = make_float4(-__fmaf_rn(k.x, mx, __fmul_rn(k.y, my)), -__fmaf_rn(k.z, mx, __fmul_rn(k.w, my)), alpha, 0.0f);
+  ctr = make_float2(mx, my);
 }
 
 // lx, ly: tile-local pixel centre (col + 0.5); px, py: absolute pixel centre
-__device__ __forceinline__ AlphaEval eval_alpha_tile(float lx, float ly, float px, float py, float4 geo,
-                                                     float2 geo2, const float4* __restrict__ rec,
-                                                     const uint32_t* s_id, int j) {
+__device__ __forceinline__ AlphaEval eval_alpha_tile(float lx, float ly, float px, float py, float4 k, float4 m,
+                                                     const float4* __restrict__ rec, const uint32_t* s_id, int j) {
   AlphaEval e;
-  e.dx = __fsub_rn(lx, geo.x);
-  e.dy = __fsub_rn(ly, geo.y);
-  const float p2 = __fmaf_rn(e.dx, __fmaf_rn(geo.z, e.dx, __fmul_rn(geo.w, e.dy)),
-                             __fmul_rn(__fmul_rn(geo2.x, e.dy), e.dy));
-  e.g = (p2 > 0.0f) ? 0.0f : ex2_approx(p2);
-  e.a_raw = __fmul_rn(geo2.y, e.g);
+  e.v1 = __fmaf_rn(k.x, lx, __fmaf_rn(k.y, ly, m.x));
+  e.v2 = __fmaf_rn(k.z, lx, __fmaf_rn(k.w, ly, m.y));
+  const float p2 = __fmaf_rn(-e.v1, e.v1, -__fmul_rn(e.v2, e.v2));
+  e.g = ex2_approx(p2);
+  e.a_raw = __fmul_rn(m.z, e.g);
   if (fabsf(e.a_raw - kAlphaEps) <= kGuard * kAlphaEps || fabsf(e.a_raw - kAlphaClamp) <= kGuard) {
-    const uint32_t gid = s_id[j];
-    eval_alpha_f64(px, py, rec[4 * size_t(gid) + 0], rec[4 * size_t(gid) + 1], rec[4 * size_t(gid) + 3], e);
+    eval_alpha_f64(px, py, rec + kRecWords * size_t(s_id[j]), e);
     return e;
   }
   e.live = e.a_raw < kAlphaClamp;

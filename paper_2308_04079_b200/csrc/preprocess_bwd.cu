@@ -31,7 +31,7 @@ __device__ __forceinline__ void load_inputs(const gs_params_t& p, const float4* 
   in.ga = __ldg(g2d + 3 * g + 0);
   in.gb = __ldg(g2d + 3 * g + 1);
   in.gc = __ldg(g2d + 3 * g + 2);
-  in.mask = __ldg(rec + 4 * g + 2).w;
+  in.mask = __ldg(rec + kRecWords * g + 3).w;
   in.q = __ldg(reinterpret_cast<const float4*>(p.rotations) + g);
   in.m0 = __ldg(p.means + 3 * g + 0); in.m1 = __ldg(p.means + 3 * g + 1); in.m2 = __ldg(p.means + 3 * g + 2);
   in.l0 = __ldg(p.log_scales + 3 * g + 0); in.l1 = __ldg(p.log_scales + 3 * g + 1);
@@ -250,7 +250,7 @@ __device__ __forceinline__ void grad_one_t(const GradInputs& in, const DevCamera
 // 0.85 ms but leaves ~1e-7-relative noise in the (exactly zero) rotation
 // gradient of isotropic Gaussians.
 #ifndef GS_BWD_REAL
-#define GS_BWD_REAL float
+#define GS_BWD_REAL double
 #endif
 __device__ __forceinline__ void grad_one(const GradInputs& in, const DevCamera& cam, int degree,
                                          const float4* shrow, GradOut& o, float (&b)[16], float (&dcol)[3]) {

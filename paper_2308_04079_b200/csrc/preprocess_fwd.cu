@@ -189,11 +189,12 @@ preprocess_fwd_kernel(gs_params_t p, DevCamera cam, int degree, gs_splats_t out)
   // split float64 -> (hi, lo) float32 pairs for the blend's threshold guard
   const double c0 = __ddiv_rn(cc, det), c1 = __ddiv_rn(-cb, det), c2 = __ddiv_rn(ca, det);
   const float c0h = float(c0), c1h = float(c1), c2h = float(c2), ah = float(alpha);
-  float4* rec = reinterpret_cast<float4*>(out.rec) + 4 * g;
-  rec[0] = make_float4(ux_hi, uy_hi, ah, ux_lo);
-  rec[1] = make_float4(c0h, c1h, c2h, uy_lo);
-  rec[2] = make_float4(col[0], col[1], col[2], float(mask));
-  rec[3] = make_float4(float(dsub(c0, double(c0h))), float(dsub(c1, double(c1h))), float(dsub(c2, double(c2h))),
+  float4* rec = reinterpret_cast<float4*>(out.rec) + kRecWords * g;
+  rec[0] = make_float4(ux_hi, uy_hi, ux_lo, uy_lo);
+  rec[1] = conic_basis(c0, c1, c2, __drcp_rn(det));   // det(conic) = 1 / det(cov2d)
+  rec[2] = make_float4(col[0], col[1], col[2], ah);
+  rec[3] = make_float4(c0h, c1h, c2h, float(mask));
+  rec[4] = make_float4(float(dsub(c0, double(c0h))), float(dsub(c1, double(c1h))), float(dsub(c2, double(c2h))),
                        float(dsub(alpha, double(ah))));
   out.depth[g] = float(z);
   reinterpret_cast<int4*>(out.rect)[g] = make_int4(x0, y0, x1, y1);

@@ -32,6 +32,27 @@ SATURATION = 0.9999       # rasterizer.py:19
 MAX_TILES = 2**32 - 1     # rasterizer.py:24
 MAX_INSTANCES = 2**31     # rasterizer.py:25
 
+LOG2E = 1.4426950408889634
+
+
+def conic_basis(conic: np.ndarray) -> np.ndarray:
+    """Host restatement of the device conic_basis (gs_common.cuh): rows
+    k = (k1.x, k1.y, k2.x, k2.y) with k_i = sqrt(log2(e) lambda_i / 2) e_i over
+    the conic's eigenpairs, so log2(e) * power = -(k1.d)^2 - (k2.d)^2 (record
+    word 1; the blend kernels' cancellation-free exponent)."""
+    a, b, c = (np.asarray(conic, np.float64).reshape(-1, 3)[:, i] for i in range(3))
+    h = 0.5 * (a - c)
+    r = np.sqrt(h * h + b * b)
+    l1 = 0.5 * (a + c) + r
+    det = np.maximum(a * c - b * b, 0.0)
+    l2 = np.where(l1 > 0, det / np.where(l1 > 0, l1, 1.0), 0.0)
+    ex, ey = np.where(h >= 0, h + r, b), np.where(h >= 0, b, r - h)
+    nn = np.sqrt(ex * ex + ey * ey)
+    ok = nn > 0
+    ex, ey = np.where(ok, ex / np.where(ok, nn, 1.0), 1.0), np.where(ok, ey / np.where(ok, nn, 1.0), 0.0)
+    f1, f2 = np.sqrt(0.5 * LOG2E * l1), np.sqrt(0.5 * LOG2E * l2)
+    return np.stack([f1 * ex, f1 * ey, -f2 * ey, f2 * ex], axis=1).astype(np.float32)
+
 
 def tile_extent(width: int, height: int) -> tuple[int, int]:
     return (width + TILE_SIZE - 1) // TILE_SIZE, (height + TILE_SIZE - 1) // TILE_SIZE
@@ -79,17 +100,17 @@ class DeviceSplats:
         radius = np.asarray(radius, np.int64).reshape(n)
         rec = np.zeros((n, _lib.REC_FLOATS), np.float32)
         hi = mean2d.astype(np.float32)
-        rec[:, 0], rec[:, 1] = hi[:, 0], hi[:, 1]
-        rec[:, 3] = (mean2d[:, 0] - hi[:, 0]).astype(np.float32)
-        rec[:, 7] = (mean2d[:, 1] - hi[:, 1]).astype(np.float32)
+        rec[:, 0:2] = hi
+        rec[:, 2:4] = (mean2d - hi).astype(np.float32)
+        rec[:, 4:8] = conic_basis(conic)
         alpha = np.asarray(alpha, np.float64).reshape(n)
-        rec[:, 2] = alpha
-        rec[:, 4:7] = conic
-        rec[:, 12:15] = conic - rec[:, 4:7].astype(np.float64)
-        rec[:, 15] = alpha - rec[:, 2].astype(np.float64)
         rec[:, 8:11] = color
+        rec[:, 11] = alpha
+        rec[:, 12:15] = conic
+        rec[:, 16:19] = conic - rec[:, 12:15].astype(np.float64)
+        rec[:, 19] = alpha - rec[:, 11].astype(np.float64)
         active = np.ones((n, 3), bool) if color_active is None else np.asarray(color_active, bool).reshape(n, 3)
-        rec[:, 11] = (active * np.array([1, 2, 4])).sum(axis=1)
+        rec[:, 15] = (active * np.array([1, 2, 4])).sum(axis=1)
         tx, ty = tile_extent(width, height)
         r = radius.astype(np.float64)
         x0, x1 = np.floor((mean2d[:, 0] - r) / TILE_SIZE), np.floor((mean2d[:, 0] + r) / TILE_SIZE)
@@ -119,15 +140,15 @@ class DeviceSplats:
     @property
     def mean2d(self) -> torch.Tensor:
         r = self.rec.double()
-        return torch.stack([r[:, 0] + r[:, 3], r[:, 1] + r[:, 7]], dim=1)
+        return r[:, 0:2] + r[:, 2:4]
 
     @property
     def conic(self) -> torch.Tensor:
-        return self.rec[:, 4:7]
+        return self.rec[:, 12:15]
 
     @property
     def alpha(self) -> torch.Tensor:
-        return self.rec[:, 2]
+        return self.rec[:, 11]
 
     @property
     def color(self) -> torch.Tensor:
@@ -135,7 +156,7 @@ class DeviceSplats:
 
     @property
     def color_active(self) -> torch.Tensor:
-        bits = self.rec[:, 11].to(torch.int32)
+        bits = self.rec[:, 15].to(torch.int32)
         return torch.stack([(bits >> c) & 1 for c in range(3)], dim=1).bool()
 
 

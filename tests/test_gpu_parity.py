@@ -327,3 +327,36 @@ def test_fused_backward_adam_matches_unfused(cuda_device):
             opt_b.exp_avg_sq[k].copy_(opt_a.exp_avg_sq[k])
     assert torch.equal(st_a.accum_count, st_b.accum_count)
     torch.testing.assert_close(st_b.accum_pos_grad, st_a.accum_pos_grad, rtol=1e-6, atol=0)
+
+
+def _fuzz_scene(seed: int):
+    """Adversarial mixes: random look-at camera, Gaussians behind / at / beyond
+    the near plane and the guard band, extreme anisotropy and scales,
+    opacities straddling 1/255 and 0.99, zero-alpha and huge splats."""
+    from paper_2308_04079_b200.camera import look_at
+    rng = np.random.default_rng(seed)
+    w, h = int(rng.integers(8, 200)), int(rng.integers(8, 120))
+    n = int(rng.integers(1, 3000))
+    eye = rng.normal(size=3) * 4.0
+    cam = look_at(eye, rng.normal(size=3) * 0.3, width=w, height=h, fx=float(rng.uniform(0.3, 2.0) * w),
+                  fy=float(rng.uniform(0.3, 2.0) * w), near=float(rng.uniform(0.05, 1.0)))
+    means = rng.normal(size=(n, 3)) * rng.uniform(0.2, 3.0)
+    log_scales = rng.uniform(-7.0, 0.5, (n, 3))
+    log_scales[rng.random(n) < 0.3] += rng.uniform(-3.0, 3.0, (1, 3))       # strong anisotropy
+    q = rng.normal(size=(n, 4))
+    logit_eps = np.log((1 / 255) / (1 - 1 / 255))
+    op = rng.uniform(-6.0, 6.0, n)
+    op[rng.random(n) < 0.1] = logit_eps                  # peak alpha exactly 1/255
+    op[rng.random(n) < 0.1] = np.log(0.99 / 0.01)        # peak alpha exactly 0.99
+    sh = rng.normal(scale=0.5, size=(n, 16, 3))
+    from paper_2308_04079_b200 import synthetic
+    cloud = synthetic.round_to_f32(dict(means=means, rotations=q, log_scales=log_scales, opacity_logits=op, sh=sh))
+    return cloud, cam, int(rng.integers(0, 4)), rng.uniform(0, 1, 3)
+
+
+@pytest.mark.parametrize("seed", range(200, 216))
+def test_fuzz_scenes_vs_oracle(cuda_device, seed):
+    cloud_np, cam, deg, bg = _fuzz_scene(seed)
+    d_image = golden_scenes.d_image_for(seed, cam.width, cam.height)
+    check_against_oracle(device_pipeline(cloud_np, cam, deg, bg, d_image),
+                         oracle_pipeline(cloud_np, cam, deg, bg, d_image))
