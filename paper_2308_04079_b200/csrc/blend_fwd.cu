@@ -26,10 +26,10 @@ namespace {
 #define GS_FWD_EXACT 0   // exact ellipse-vs-block masks (see warp_cover_mask)
 #endif
 #ifndef GS_FWD_BATCH
-#define GS_FWD_BATCH 64
+#define GS_FWD_BATCH 32
 #endif
 #ifndef GS_FWD_STAGES
-#define GS_FWD_STAGES 6
+#define GS_FWD_STAGES 12
 #endif
 constexpr int kBatch = GS_FWD_BATCH;
 constexpr int kStages = GS_FWD_STAGES;

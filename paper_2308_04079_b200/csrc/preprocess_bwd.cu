@@ -357,6 +357,9 @@ struct FusedAdam {
 #ifndef GS_BWDADAM_MINB
 #define GS_BWDADAM_MINB 5
 #endif
+#ifndef GS_BWDADAM_SWEEP_U
+#define GS_BWDADAM_SWEEP_U 4
+#endif
 __global__ void __launch_bounds__(128, GS_BWDADAM_MINB)
 preprocess_bwd_adam_kernel(gs_params_t p, DevCamera cam, int degree, const float4* __restrict__ rec,
                            const int32_t* __restrict__ radii, const float4* __restrict__ g2d, gs_grads_t out,
@@ -455,7 +458,7 @@ preprocess_bwd_adam_kernel(gs_params_t p, DevCamera cam, int degree, const float
   float4* __restrict__ m4 = reinterpret_cast<float4*>(A.m[4]) + g0 * 12;
   float4* __restrict__ v4 = reinterpret_cast<float4*>(A.v[4]) + g0 * 12;
   const int total = nb * 12, step = blockDim.x;
-  constexpr int kU = 3;  // 3 x 3 float4 loads in flight per thread
+  constexpr int kU = GS_BWDADAM_SWEEP_U;  // kU x 3 float4 loads in flight per thread
   for (int f0 = threadIdx.x; f0 < total; f0 += kU * step) {
     float4 pq[kU], mq[kU], vq[kU];
 #pragma unroll
