@@ -360,3 +360,28 @@ def test_fuzz_scenes_vs_oracle(cuda_device, seed):
     d_image = golden_scenes.d_image_for(seed, cam.width, cam.height)
     check_against_oracle(device_pipeline(cloud_np, cam, deg, bg, d_image),
                          oracle_pipeline(cloud_np, cam, deg, bg, d_image))
+
+
+@pytest.mark.parametrize("seed,thin", [(300, -4.0), (301, -6.0), (302, -8.0)])
+def test_needle_splats_vs_oracle(cuda_device, seed, thin):
+    """Needle-like Gaussians (one axis e^thin of the other two): screen conics
+    with condition numbers up to ~1e5, where the expanded float32 quadratic
+    form a dx^2 + 2b dx dy + c dy^2 cancels.  The blends evaluate it as a sum
+    of squares in the conic's eigenbasis (gs_common.cuh: make_tile_splat), so
+    the full pipeline stays within the oracle tolerances."""
+    from paper_2308_04079_b200 import synthetic
+    from paper_2308_04079_b200.camera import look_at
+    rng = np.random.default_rng(seed)
+    n, w, h = 400, 320, 192
+    cam = look_at(np.array([0.0, -4.0, 0.5]), np.zeros(3), width=w, height=h, fx=float(w), fy=float(w))
+    means = rng.normal(size=(n, 3)) * 0.8
+    log_scales = np.empty((n, 3))
+    log_scales[:, 0] = rng.uniform(-1.0, 1.0, n)           # long axis
+    log_scales[:, 1:] = log_scales[:, :1] + thin            # two thin axes
+    log_scales = np.take_along_axis(log_scales, rng.permuted(np.tile(np.arange(3), (n, 1)), axis=1), axis=1)
+    cloud = synthetic.round_to_f32(dict(means=means, rotations=rng.normal(size=(n, 4)), log_scales=log_scales,
+                                        opacity_logits=rng.uniform(-1.0, 5.0, n),
+                                        sh=rng.normal(scale=0.5, size=(n, 16, 3))))
+    bg = rng.uniform(0, 1, 3)
+    d_image = golden_scenes.d_image_for(seed, w, h)
+    check_against_oracle(device_pipeline(cloud, cam, 3, bg, d_image), oracle_pipeline(cloud, cam, 3, bg, d_image))
