@@ -25,17 +25,21 @@ namespace {
 #define GS_WAIT_NS 2000
 #endif
 #ifndef GS_BWD_MIN_BLOCKS
-#define GS_BWD_MIN_BLOCKS 3  // 72 registers (small spill) beats 2 blocks at 96 (measured 1.69 vs 1.99 ms)
+#define GS_BWD_MIN_BLOCKS 6  // half-tile CTAs: 64 registers, 6 CTAs (24 warps) per SM
 #endif
 #ifndef GS_BWD_BATCH
 #define GS_BWD_BATCH 64
 #endif
 constexpr int kBatch = GS_BWD_BATCH;
 #ifndef GS_BWD_STAGES
-#define GS_BWD_STAGES 6
+#define GS_BWD_STAGES 4
 #endif
 constexpr int kStages = GS_BWD_STAGES;
-constexpr int kConsumerWarps = 8;
+#ifndef GS_BWD_PARTS
+#define GS_BWD_PARTS 2   // CTAs per tile: 2 = one CTA per 16x8 half tile (4 consumer warps)
+#endif
+constexpr int kParts = GS_BWD_PARTS;
+constexpr int kConsumerWarps = 8 / kParts;
 constexpr int kThreads = (kConsumerWarps + 1) * 32;
 constexpr int kG = 2;    // splats per reduction group (group_reduce2)
 constexpr int kC = 9;    // gradient components per splat
@@ -108,16 +112,17 @@ blend_bwd_kernel(const float* __restrict__ d_image, const float4* __restrict__ r
   __shared__ uint64_t full_bar[kStages], empty_bar[kStages];
   __shared__ int s_warp_max[kConsumerWarps + 1];
 
-  const int tile = tile0 + int(blockIdx.x);
+  const int tile = tile0 + int(blockIdx.x) / kParts;
+  const int part = int(blockIdx.x) % kParts;   // this CTA's rows: [part * 16 / kParts, (part + 1) * 16 / kParts)
   const int t = threadIdx.x;
   const int lane = t & 31, warp = t >> 5;
   const bool consumer = warp < kConsumerWarps;
   const int tx = tile % tiles_x, ty = tile / tiles_x;
   const int px = tx * kTile + tile_px(t);
-  const int py = ty * kTile + tile_py(t);
+  const int py = ty * kTile + tile_py(t) + part * (kTile / kParts);
   const bool inside = consumer && (px < width) && (py < height);
   const float fx = float(px) + 0.5f, fy = float(py) + 0.5f;
-  const float lx = float(tile_px(t)) + 0.5f, ly = float(tile_py(t)) + 0.5f;
+  const float lx = float(tile_px(t)) + 0.5f, ly = float(tile_py(t) + part * (kTile / kParts)) + 0.5f;
   const float tile_x0 = float(tx * kTile), tile_y0 = float(ty * kTile);
   const int2 range = ranges[tile];
 
@@ -187,7 +192,7 @@ blend_bwd_kernel(const float* __restrict__ d_image, const float4* __restrict__ r
             const float4 r0 = raw->r0[e], k = st.k[e];
             const float alpha = st.col[e].w;
             make_tile_splat(r0, k, alpha, tile_x0, tile_y0, st.m[e], st.ctr[e]);
-            st.mask[e] = uint8_t(warp_cover_mask<true>(r0, k, alpha, tile_x0, tile_y0));
+            st.mask[e] = uint8_t(warp_cover_mask<true>(r0, k, alpha, tile_x0, tile_y0) >> (part * kConsumerWarps));
           }
         }
         mbar_arrive(&full_bar[s]);
@@ -296,7 +301,7 @@ int blend_backward_rows(const float* d_image, const gs_splats_t* splats, const u
   }
   const float3 bg = make_float3(background[0], background[1], background[2]);
   const int64_t ntiles = int64_t(row_end - row_begin) * tiles_x;
-  blend_bwd_kernel<<<unsigned(ntiles), kThreads, kSmemBytes, static_cast<cudaStream_t>(stream)>>>(
+  blend_bwd_kernel<<<unsigned(ntiles * kParts), kThreads, kSmemBytes, static_cast<cudaStream_t>(stream)>>>(
       d_image, reinterpret_cast<const float4*>(splats->rec), sorted_ids, reinterpret_cast<const int2*>(ranges),
       t_final, last, width, height, tiles_x, row_begin * tiles_x, bg, reinterpret_cast<float4*>(grads2d));
   return check_launch();

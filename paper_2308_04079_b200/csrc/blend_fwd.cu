@@ -33,7 +33,11 @@ namespace {
 #endif
 constexpr int kBatch = GS_FWD_BATCH;
 constexpr int kStages = GS_FWD_STAGES;
-constexpr int kConsumerWarps = 8;
+#ifndef GS_FWD_PARTS
+#define GS_FWD_PARTS 1   // CTAs per tile: 2 = one CTA per 16x8 half tile (4 consumer warps)
+#endif
+constexpr int kParts = GS_FWD_PARTS;
+constexpr int kConsumerWarps = 8 / kParts;
 constexpr int kThreads = (kConsumerWarps + 1) * 32;
 
 struct FwdStage {
@@ -50,7 +54,7 @@ constexpr size_t kSmemBytes = sizeof(FwdStage) * kStages + sizeof(RawRec);
 
 __device__ __forceinline__ void produce_batch(FwdStage& st, RawRec& raw, const float4* __restrict__ rec,
                                               const uint32_t* __restrict__ ids, int base, int cnt, int lane,
-                                              float tile_x0, float tile_y0) {
+                                              float tile_x0, float tile_y0, int mask_shift) {
   uint32_t gid[kBatch / 32];
 #pragma unroll
   for (int u = 0; u < kBatch / 32; ++u) {
@@ -77,7 +81,7 @@ __device__ __forceinline__ void produce_batch(FwdStage& st, RawRec& raw, const f
       const float alpha = st.col[e].w;
       float2 ctr;
       make_tile_splat(r0, k, alpha, tile_x0, tile_y0, st.m[e], ctr);
-      st.mask[e] = uint8_t(warp_cover_mask<GS_FWD_EXACT != 0>(r0, k, alpha, tile_x0, tile_y0));
+      st.mask[e] = uint8_t(warp_cover_mask<GS_FWD_EXACT != 0>(r0, k, alpha, tile_x0, tile_y0) >> mask_shift);
     }
   }
 }
@@ -93,7 +97,8 @@ blend_fwd_kernel(const float4* __restrict__ rec, const uint32_t* __restrict__ id
   __shared__ uint64_t full_bar[kStages], empty_bar[kStages];
   __shared__ int s_done, s_stop;
 
-  const int tile = tile0 + int(blockIdx.x);
+  const int tile = tile0 + int(blockIdx.x) / kParts;
+  const int part = int(blockIdx.x) % kParts;   // this CTA's rows: [part * 16 / kParts, (part + 1) * 16 / kParts)
   const int t = threadIdx.x;
   const int lane = t & 31, warp = t >> 5;
   const int tx = tile % tiles_x, ty = tile / tiles_x;
@@ -120,7 +125,8 @@ blend_fwd_kernel(const float4* __restrict__ rec, const uint32_t* __restrict__ id
       }
       if (ld_volatile(&s_stop)) return;
       const int base = range.x + b * kBatch;
-      produce_batch(stages[s], *raw, rec, ids, base, min(kBatch, range.y - base), lane, tile_x0, tile_y0);
+      produce_batch(stages[s], *raw, rec, ids, base, min(kBatch, range.y - base), lane, tile_x0, tile_y0,
+                    part * kConsumerWarps);
       mbar_arrive(&full_bar[s]);
     }
     return;
@@ -128,10 +134,10 @@ blend_fwd_kernel(const float4* __restrict__ rec, const uint32_t* __restrict__ id
 
   // ---------------- consumer warps
   const int px = tx * kTile + tile_px(t);
-  const int py = ty * kTile + tile_py(t);
+  const int py = ty * kTile + tile_py(t) + part * (kTile / kParts);
   const bool inside = (px < width) && (py < height);
   const float fx = float(px) + 0.5f, fy = float(py) + 0.5f;  // rasterizer.py:142
-  const float lx = float(tile_px(t)) + 0.5f, ly = float(tile_py(t)) + 0.5f;
+  const float lx = float(tile_px(t)) + 0.5f, ly = float(tile_py(t) + part * (kTile / kParts)) + 0.5f;
   float T = 1.0f;
   float cr = 0.0f, cg = 0.0f, cb = 0.0f;
   int32_t last_idx = -1;
@@ -209,7 +215,7 @@ int launch(const float4* rec, const uint32_t* ids, const int2* rg, int width, in
     configured = true;
   }
   if (ntiles <= 0) return GS_OK;
-  blend_fwd_kernel<kTraining><<<unsigned(ntiles), kThreads, kSmemBytes, s>>>(rec, ids, rg, width, height, tiles_x,
+  blend_fwd_kernel<kTraining><<<unsigned(ntiles * kParts), kThreads, kSmemBytes, s>>>(rec, ids, rg, width, height, tiles_x,
                                                                              tile0, bg, image, t_final, last);
   return check_launch();
 }
