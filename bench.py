@@ -242,15 +242,18 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
     # one view per rank (each rank trains on its own shard of the view list)
     views = [TrainView(view_for(r), gt_host) for r in range(world)]
 
+    # lookahead (train_step enqueues the next iteration's forward before it
+    # waits for this one) is off for the last warm-up and the last timed step,
+    # so the timed region holds exactly `steps` forwards, backwards and Adams
     for i in range(args.warmup):
-        train_step(state, views, e2e_config)
+        train_step(state, views, e2e_config, lookahead=i < args.warmup - 1)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for i in range(args.steps):
-        report = train_step(state, views, e2e_config)
+        report = train_step(state, views, e2e_config, lookahead=i < args.steps - 1)
     e1.record()
     torch.cuda.synchronize()
     e_ms = torch.tensor([e0.elapsed_time(e1)], device=dev)
@@ -309,7 +312,8 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
         "e2e": {"value": round(e2e_value, 3), "unit": UNIT, "h2d_bytes_per_step": WIDTH * HEIGHT * 3 * 4,
                 "d2h_bytes_per_step": 4 * 4 + 3 * 8,
                 "path": "training.train_step (mirror of splatlab optimizer.train_step): target image H2D from "
-                        "pinned host memory every step, [loss, L1, SSIM, MSE] + [K, flags, K] read D2H",
+                        "pinned host memory every step, [loss, L1, SSIM, MSE] + [K, flags, K] read D2H every "
+                        "step; lookahead: the next iteration's forward is enqueued before the host waits",
                 "last_loss": round(e2e_loss, 6)},
         "gpu_launches": timer.launches_per_step() * args.steps,
         "roofline": roof["primary"], "roofline_hbm": roof["hbm"], "roofline_stages": roof["stages"],

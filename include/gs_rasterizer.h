@@ -276,6 +276,21 @@ int gs_preprocess_backward_adam(const gs_params_t* params, const gs_camera_t* ca
                                 double bias1, double bias2, const gs_stats_t* stats,
                                 const gs_grads_t* grads_out, void* stream);
 
+/* The same with a device-side step guard: when *skip != 0 (device int32,
+ * written by gs_step_guard on the same stream) the launch applies nothing.
+ * Lets a training step enqueue its backward and Adam before the host has
+ * read the loss: the reference's divergence check (optimizer.py:245-246,
+ * raise before any update) and the binning-capacity retry stay exact. */
+int gs_preprocess_backward_adam_guarded(const gs_params_t* params, const gs_camera_t* camera,
+                                        int32_t active_sh_degree, const gs_splats_t* splats,
+                                        const float* grads2d, const gs_adam_group_t* groups, double beta1,
+                                        double beta2, double eps, double bias1, double bias2,
+                                        const gs_stats_t* stats, const gs_grads_t* grads_out,
+                                        const int32_t* skip, void* stream);
+
+/* *skip = (k_info[1] != 0 (binning overflow / limit flags) || loss[0] not finite). */
+int gs_step_guard(const float* loss, const int64_t* k_info, int32_t* skip, void* stream);
+
 /* ---- K9 fused Adam: replaces optimizer._adam_step (optimizer.py:263-293)
  * over all groups in one launch; bias1 = 1-beta1^t, bias2 = 1-beta2^t. */
 int gs_adam_step(const gs_adam_group_t* groups, int32_t num_groups, double beta1, double beta2,

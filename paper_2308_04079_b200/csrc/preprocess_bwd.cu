@@ -363,7 +363,11 @@ struct FusedAdam {
 __global__ void __launch_bounds__(128, GS_BWDADAM_MINB)
 preprocess_bwd_adam_kernel(gs_params_t p, DevCamera cam, int degree, const float4* __restrict__ rec,
                            const int32_t* __restrict__ radii, const float4* __restrict__ g2d, gs_grads_t out,
-                           gs_stats_t stats, FusedAdam A) {
+                           gs_stats_t stats, FusedAdam A, const int32_t* __restrict__ skip) {
+  // device-side step guard (gs_step_guard): a step whose loss is not finite
+  // or whose binning overflowed applies nothing — parameters, moments and
+  // statistics stay untouched, as the reference raises before updating
+  if (skip != nullptr && *skip != 0) return;
   extern __shared__ __align__(16) float4 smem4[];
   float4* s_sh = smem4;                      // staged SH coefficients (the SH parameters)
   float4* s_dsh = smem4;  // d_sh rows: each thread overwrites its own SH row after grad_one read it
@@ -491,11 +495,12 @@ preprocess_bwd_adam_kernel(gs_params_t p, DevCamera cam, int degree, const float
 }  // namespace
 }  // namespace gs
 
-extern "C" int gs_preprocess_backward_adam(const gs_params_t* params, const gs_camera_t* camera,
-                                           int32_t active_sh_degree, const gs_splats_t* splats,
-                                           const float* grads2d, const gs_adam_group_t* groups, double beta1,
-                                           double beta2, double eps, double bias1, double bias2,
-                                           const gs_stats_t* stats, const gs_grads_t* grads_out, void* stream) {
+extern "C" int gs_preprocess_backward_adam_guarded(const gs_params_t* params, const gs_camera_t* camera,
+                                                   int32_t active_sh_degree, const gs_splats_t* splats,
+                                                   const float* grads2d, const gs_adam_group_t* groups, double beta1,
+                                                   double beta2, double eps, double bias1, double bias2,
+                                                   const gs_stats_t* stats, const gs_grads_t* grads_out,
+                                                   const int32_t* skip, void* stream) {
   if (!params || !camera || !splats || !grads2d || !groups) return GS_ERR_INVALID_ARG;
   if (active_sh_degree < 0 || active_sh_degree > 3) return GS_ERR_INVALID_ARG;
   if (splats->n != params->n || !(bias1 > 0) || !(bias2 > 0)) return GS_ERR_INVALID_ARG;
@@ -529,7 +534,31 @@ extern "C" int gs_preprocess_backward_adam(const gs_params_t* params, const gs_c
   gs::preprocess_bwd_adam_kernel<<<grid, 128, smem, s>>>(*params, cam, active_sh_degree,
                                                          reinterpret_cast<const float4*>(splats->rec),
                                                          splats->radii, reinterpret_cast<const float4*>(grads2d),
-                                                         go, st, A);
+                                                         go, st, A, skip);
+  return gs::check_launch();
+}
+
+extern "C" int gs_preprocess_backward_adam(const gs_params_t* params, const gs_camera_t* camera,
+                                           int32_t active_sh_degree, const gs_splats_t* splats,
+                                           const float* grads2d, const gs_adam_group_t* groups, double beta1,
+                                           double beta2, double eps, double bias1, double bias2,
+                                           const gs_stats_t* stats, const gs_grads_t* grads_out, void* stream) {
+  return gs_preprocess_backward_adam_guarded(params, camera, active_sh_degree, splats, grads2d, groups, beta1, beta2,
+                                             eps, bias1, bias2, stats, grads_out, nullptr, stream);
+}
+
+namespace gs {
+namespace {
+__global__ void step_guard_kernel(const float* loss, const int64_t* k_info, int32_t* skip) {
+  const float v = loss[0];
+  skip[0] = (k_info[1] != 0 || !isfinite(v)) ? 1 : 0;
+}
+}  // namespace
+}  // namespace gs
+
+extern "C" int gs_step_guard(const float* loss, const int64_t* k_info, int32_t* skip, void* stream) {
+  if (!loss || !k_info || !skip) return GS_ERR_INVALID_ARG;
+  gs::step_guard_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(loss, k_info, skip);
   return gs::check_launch();
 }
 

@@ -46,6 +46,16 @@ class TrainState:
         self.adam = DeviceAdam(cloud)
         self.stats = DensifyStats.zeros(len(cloud), cloud.device)
 
+    def discard_lookahead(self) -> None:
+        """Drop a speculative next-iteration forward enqueued by train_step
+        (lookahead) and restore the view-sampling state it consumed, so the
+        next draw (and any other use of `rng`) matches the reference order."""
+        la = getattr(self, "_lookahead", None)
+        self._lookahead = None
+        if la is not None:
+            self._epoch_order, self._epoch_pos, rng_state = la.snapshot
+            self.rng.bit_generator.state = rng_state
+
     def reset_stats(self) -> None:
         self.stats = DensifyStats.zeros(len(self.cloud), self.cloud.device)
 
@@ -88,6 +98,7 @@ def densify_and_prune(state: TrainState, config: TrainConfig) -> DensifyReport:
     """Clone small / split large high-gradient Gaussians, prune transparent or
     oversized ones, periodically reset opacity; moments stay aligned and new
     Gaussians start with zero moments; statistics reset (optimizer.py:304-374)."""
+    state.discard_lookahead()   # its forward used the pre-densify cloud, and it drew from state.rng
     lib = _lib.load()
     cloud, adam, dev = state.cloud, state.adam, state.cloud.device
     n = len(cloud)

@@ -150,10 +150,13 @@ class DeviceAdam:
                                             torch.cuda.current_stream().cuda_stream), "adam_step")
 
     def backward_step(self, cloud: GaussianCloud, camera, splats, grads2d, active_sh_degree: int, iteration: int,
-                      config: TrainConfig, stats=None, grads_out: GaussianGrads | None = None) -> None:
+                      config: TrainConfig, stats=None, grads_out: GaussianGrads | None = None,
+                      skip: torch.Tensor | None = None) -> None:
         """backward_project + densify statistics + Adam fused in one kernel
         (gs_preprocess_backward_adam): parameters are updated in place, the
-        raw gradients never round-trip through HBM unless `grads_out` is given."""
+        raw gradients never round-trip through HBM unless `grads_out` is given.
+        `skip` (device int32 from `step_guard`): when set on the device, the
+        launch applies nothing."""
         from .rasterizer import _camera
         if not 0 <= active_sh_degree <= 3:
             raise ValueError(f"SH degree must be in 0..3, got {active_sh_degree}")
@@ -164,11 +167,25 @@ class DeviceAdam:
         cs = splats.c_struct()
         cst = stats.c_struct() if stats is not None else None
         cg = grads_out.c_struct() if grads_out is not None else None
-        _lib.check(_lib.load().gs_preprocess_backward_adam(
+        _lib.check(_lib.load().gs_preprocess_backward_adam_guarded(
             ctypes.byref(cloud.c_params()), ctypes.byref(_camera(camera).to_c()), int(active_sh_degree),
             ctypes.byref(cs), grads2d.packed.data_ptr(), groups, beta1, beta2, config.adam_eps, bias1, bias2,
             ctypes.byref(cst) if cst is not None else None, ctypes.byref(cg) if cg is not None else None,
-            torch.cuda.current_stream().cuda_stream), "backward_adam")
+            skip.data_ptr() if skip is not None else None, torch.cuda.current_stream().cuda_stream),
+            "backward_adam")
 
 
-__all__ = ["TrainConfig", "DeviceAdam", "DensifyStats"]
+def step_guard(loss: torch.Tensor, k_info: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+    """Device int32 flag: 1 when the step must not update anything (loss not
+    finite, or the binning overflowed its capacity), written on the current
+    stream without a host synchronisation (gs_step_guard)."""
+    if out is None:
+        out = torch.empty(1, dtype=torch.int32, device=loss.device)
+    if loss.dtype != torch.float32 or k_info.dtype != torch.int64:
+        raise TypeError("step_guard expects float32 loss and int64 k_info")
+    _lib.check(_lib.load().gs_step_guard(loss.data_ptr(), k_info.data_ptr(), out.data_ptr(),
+                                         torch.cuda.current_stream(loss.device).cuda_stream), "step_guard")
+    return out
+
+
+__all__ = ["TrainConfig", "DeviceAdam", "DensifyStats", "step_guard"]

@@ -22,7 +22,7 @@ from .camera import Camera
 from .densify import DensifyReport, TrainState, densify_and_prune
 from .errors import TrainingDiverged
 from .loss import l1_dssim_loss
-from .optimizer import TrainConfig
+from .optimizer import TrainConfig, step_guard
 
 
 @dataclass
@@ -39,10 +39,25 @@ class _HostScalars:
         self.loss = torch.empty(4, dtype=torch.float32).pin_memory()
         self.k_info = torch.empty(3, dtype=torch.int64).pin_memory()
 
+    def skip_device(self, device) -> torch.Tensor:
+        flag = getattr(self, "_skip", None)
+        if flag is None or flag.device != torch.device(device):
+            flag = self._skip = torch.zeros(1, dtype=torch.int32, device=device)
+        return flag
+
     def read(self, loss: torch.Tensor, k_info: torch.Tensor):
+        self.stage(loss, k_info).synchronize()
+        return self.values()
+
+    def stage(self, loss: torch.Tensor, k_info: torch.Tensor) -> torch.cuda.Event:
+        """Enqueue the D2H copies; the returned event marks their completion."""
         self.loss.copy_(loss, non_blocking=True)
         self.k_info.copy_(k_info, non_blocking=True)
-        torch.cuda.current_stream(loss.device).synchronize()
+        done = torch.cuda.Event()
+        done.record(torch.cuda.current_stream(loss.device))
+        return done
+
+    def values(self):
         return self.loss.tolist(), self.k_info.tolist()
 
 
@@ -157,28 +172,42 @@ def _world(group) -> tuple[int, int]:
     return 1, 0
 
 
-def train_step(state: TrainState, views: Sequence[TrainView], config: TrainConfig, group=None) -> StepReport:
-    """One iteration (optimizer.py:222-260), with ONE host synchronisation:
-    the loss, the step's MSE (for the PSNR) and the binning's instance count
-    and flags are read together after the loss kernels; the divergence check
-    (optimizer.py:245-246) and a binning capacity overflow (re-render with a
-    larger buffer) are handled there, before any gradient is applied.
+def _degree_for(prev_degree: int, it: int, config: TrainConfig) -> int:
+    """Active SH degree at iteration `it` given the degree before it (one band
+    every sh_band_interval iterations, optimizer.py:232-233)."""
+    return prev_degree + 1 if (it % config.sh_band_interval == 0 and prev_degree < 3) else prev_degree
 
-    Under torch.distributed (world > 1) every rank samples a view from its
-    contiguous shard of `views` (SURVEY §8(e)), its gradients go to one flat
-    bucket, one NCCL all-reduce sums them and every rank runs the identical
-    Adam, so the replicas stay bit-identical."""
-    state.iteration += 1
-    it = state.iteration
-    if it % config.sh_band_interval == 0 and state.active_sh_degree < 3:
-        state.active_sh_degree += 1
-    world, rank = _world(group)
-    if world > 1:
-        from .distributed import shard_views
-        shard = shard_views(len(views), world, rank)
-        view_idx = shard[next_view(state, len(shard))]
-    else:
-        view_idx = next_view(state, len(views))
+
+def _cloud_key(state: TrainState) -> tuple:
+    c = state.cloud
+    return (id(c), len(c), c.means.data_ptr(), c.rotations.data_ptr(), c.sh.data_ptr())
+
+
+@dataclass
+class _Forward:
+    """One iteration's sampled view and its enqueued forward + loss."""
+    it: int
+    view_idx: int
+    camera: Camera
+    degree: int
+    gt: torch.Tensor
+    consumed: object
+    snapshot: tuple     # view-sampling state before this view was drawn (TrainState.discard_lookahead)
+    views: Sequence[TrainView]   # the objects the forward was made for (held: identity compared)
+    config: TrainConfig
+    cloud_key: tuple
+    out: object = None
+    splats: object = None
+    binning: object = None
+    loss: torch.Tensor = None
+    d_image: torch.Tensor = None
+
+
+def _sample_view(state: TrainState, views: Sequence[TrainView], config: TrainConfig, it: int,
+                 degree: int) -> _Forward:
+    snapshot = (getattr(state, "_epoch_order", None), getattr(state, "_epoch_pos", 0),
+                state.rng.bit_generator.state)
+    view_idx = next_view(state, len(views))
     view = views[view_idx]
     scale = warmup_scale(it, config.warmup_upsample_iters)
     camera = view.camera if scale == 1.0 else view.camera.scaled(scale)
@@ -187,11 +216,115 @@ def train_step(state: TrainState, views: Sequence[TrainView], config: TrainConfi
     if image.device != device:   # host-resident view: H2D from pinned memory, prefetched one step ahead
         pf = _prefetchers.setdefault(str(device), _ImagePrefetcher(device))
         image, consumed = pf.get(view)
-        if world > 1:
-            nxt = _peek_next_view(state, len(shard))
-            nxt = None if nxt is None else shard[nxt]
-        else:
-            nxt = _peek_next_view(state, len(views))
+        nxt = _peek_next_view(state, len(views))
+        if nxt is not None and views[nxt].image.device != device:
+            pf.prefetch(views[nxt])
+    gt = downscale_image(image, camera.height, camera.width)
+    return _Forward(it, view_idx, camera, degree, gt, consumed, snapshot, views, config, _cloud_key(state))
+
+
+def _enqueue_forward(state: TrainState, fw: _Forward, config: TrainConfig) -> _Forward:
+    fw.out, fw.splats, fw.binning = R.render_view_async(state.cloud, fw.camera, config.background, fw.degree,
+                                                        training=True)
+    fw.loss, fw.d_image = l1_dssim_loss(fw.out.image, fw.gt, config.lambda_dssim)
+    if fw.consumed is not None:
+        fw.consumed.record()
+    return fw
+
+
+def train_step(state: TrainState, views: Sequence[TrainView], config: TrainConfig, group=None,
+               lookahead: bool = True) -> StepReport:
+    """One iteration (optimizer.py:222-260), with ONE host synchronisation:
+    the loss, the step's MSE (for the PSNR) and the binning's instance count
+    and flags are read together at the end of the step.  The backward and
+    the fused Adam are enqueued before that read behind a device-side guard
+    (`step_guard`: loss not finite, capacity overflow, zero quaternion), so
+    the divergence check (optimizer.py:245-246) and a capacity overflow
+    (re-render with a larger buffer) still find nothing applied.
+
+    lookahead: before waiting for this step, the NEXT iteration's view is
+    drawn and its forward + loss enqueued behind this step's Adam (stream
+    order: it sees the updated parameters), so the GPU never idles while the
+    host reads the loss.  The next train_step call consumes it when the
+    iteration, views, config and cloud still match; otherwise (and in
+    densify_and_prune) `TrainState.discard_lookahead` restores the view
+    sampling state, so the sampled sequence is exactly the reference's.
+    After modifying parameters outside train_step, call
+    `state.discard_lookahead()`.
+
+    Under torch.distributed (world > 1) every rank samples a view from its
+    contiguous shard of `views` (SURVEY §8(e)), its gradients go to one flat
+    bucket, one NCCL all-reduce sums them and every rank runs the identical
+    Adam, so the replicas stay bit-identical (no lookahead)."""
+    world, rank = _world(group)
+    if world > 1:
+        return _train_step_sharded(state, views, config, group, world, rank)
+    it = state.iteration + 1
+    degree = _degree_for(state.active_sh_degree, it, config)
+    fw = getattr(state, "_lookahead", None)
+    if fw is not None and (fw.it != it or fw.degree != degree or fw.views is not views or fw.config is not config
+                           or fw.cloud_key != _cloud_key(state)):
+        state.discard_lookahead()
+        fw = None
+    state._lookahead = None
+    if fw is None:
+        fw = _enqueue_forward(state, _sample_view(state, views, config, it, degree), config)
+    device = state.cloud.device
+    host = _host_scalars.setdefault(str(device), _HostScalars())
+    nxt = None
+    for attempt in range(3):
+        skip = step_guard(fw.loss, fw.binning.k_info, host.skip_device(device))
+        g2 = R.render_backward(fw.d_image, fw.out, fw.splats, fw.binning, fw.camera.width, fw.camera.height,
+                               config.background)
+        state.adam.backward_step(state.cloud, fw.camera, fw.splats, g2, fw.degree, it, config, stats=state.stats,
+                                 skip=skip)
+        done = host.stage(fw.loss, fw.binning.k_info)
+        if lookahead:
+            nxt = _enqueue_forward(state, _sample_view(state, views, config, it + 1,
+                                                       _degree_for(degree, it + 1, config)), config)
+        done.synchronize()
+        lvals, kvals = host.values()
+        try:
+            fw.binning.check_host(kvals)
+            break
+        except R.CapacityError:   # nothing was applied: re-render this view with the larger capacity
+            if nxt is not None:
+                state._lookahead, nxt = nxt, None
+                state.discard_lookahead()
+            if attempt == 2:
+                raise
+            fw = _enqueue_forward(state, fw, config)
+    state.iteration, state.active_sh_degree = it, degree
+    value, mse = float(lvals[0]), float(lvals[3])
+    if not math.isfinite(value):
+        if nxt is not None:
+            state._lookahead = nxt
+            state.discard_lookahead()
+        raise TrainingDiverged(f"non-finite loss {value} at iteration {it}")
+    state._lookahead = nxt
+    psnr = float("inf") if mse == 0.0 else 10.0 * math.log10(1.0 / mse)
+    return StepReport(it, value, psnr, fw.view_idx, len(state.cloud))
+
+
+def _train_step_sharded(state: TrainState, views: Sequence[TrainView], config: TrainConfig, group, world: int,
+                        rank: int) -> StepReport:
+    from .distributed import GradientBucket, shard_views
+    state.discard_lookahead()
+    state.iteration += 1
+    it = state.iteration
+    state.active_sh_degree = _degree_for(state.active_sh_degree, it, config)
+    shard = shard_views(len(views), world, rank)
+    view_idx = shard[next_view(state, len(shard))]
+    view = views[view_idx]
+    scale = warmup_scale(it, config.warmup_upsample_iters)
+    camera = view.camera if scale == 1.0 else view.camera.scaled(scale)
+    device = state.cloud.device
+    image, consumed = view.image, None
+    if image.device != device:
+        pf = _prefetchers.setdefault(str(device), _ImagePrefetcher(device))
+        image, consumed = pf.get(view)
+        nxt = _peek_next_view(state, len(shard))
+        nxt = None if nxt is None else shard[nxt]
         if nxt is not None and views[nxt].image.device != device:
             pf.prefetch(views[nxt])
     gt = downscale_image(image, camera.height, camera.width)
@@ -213,19 +346,14 @@ def train_step(state: TrainState, views: Sequence[TrainView], config: TrainConfi
     if not math.isfinite(value):
         raise TrainingDiverged(f"non-finite loss {value} at iteration {it}")
     g2 = R.render_backward(d_image, out, splats, binning, camera.width, camera.height, bg)
-    if world > 1:
-        from .distributed import GradientBucket
-        bucket = getattr(state, "_bucket", None)
-        if bucket is None or bucket.n != len(state.cloud):
-            bucket = state._bucket = GradientBucket(len(state.cloud), device)
-        bucket.zero_()
-        R.backward_project(state.cloud, camera, splats, g2, state.active_sh_degree, stats=state.stats,
-                           out=bucket.grads, accumulate=True)
-        bucket.allreduce_(group)
-        state.adam.step(state.cloud, bucket.grads, it, config)
-    else:
-        state.adam.backward_step(state.cloud, camera, splats, g2, state.active_sh_degree, it, config,
-                                 stats=state.stats)
+    bucket = getattr(state, "_bucket", None)
+    if bucket is None or bucket.n != len(state.cloud):
+        bucket = state._bucket = GradientBucket(len(state.cloud), device)
+    bucket.zero_()
+    R.backward_project(state.cloud, camera, splats, g2, state.active_sh_degree, stats=state.stats,
+                       out=bucket.grads, accumulate=True)
+    bucket.allreduce_(group)
+    state.adam.step(state.cloud, bucket.grads, it, config)
     psnr = float("inf") if mse == 0.0 else 10.0 * math.log10(1.0 / mse)
     return StepReport(it, value, psnr, view_idx, len(state.cloud))
 
@@ -238,7 +366,9 @@ def train(state: TrainState, views: Sequence[TrainView], config: TrainConfig, *,
     densify_until = config.resolve_densify_until()
     reports = []
     while state.iteration < iterations:
-        step = train_step(state, views, config)
+        nxt = state.iteration + 1
+        densify_next = (config.densify_start < nxt <= densify_until and nxt % config.densify_interval == 0)
+        step = train_step(state, views, config, lookahead=nxt < iterations and not densify_next)
         if (config.densify_start < state.iteration <= densify_until
                 and state.iteration % config.densify_interval == 0):
             report = densify_and_prune(state, config)

@@ -88,3 +88,79 @@ def test_train_step_recovers_from_capacity_overflow(cuda_device):
     # the backward's float atomics are order-dependent (SPEC.md:184 allows 1e-5 relative run to run)
     for g in ("means", "rotations", "log_scales", "opacity_logits", "sh"):
         torch.testing.assert_close(getattr(state.cloud, g), getattr(ref_state.cloud, g), rtol=1e-5, atol=1e-7)
+
+
+@pytest.mark.gpu
+def test_train_step_divergence_applies_nothing(cuda_device):
+    """A non-finite loss raises TrainingDiverged (optimizer.py:245-246) with
+    parameters, Adam moments and densify statistics untouched: the fused
+    backward + Adam was already enqueued, behind the device-side step guard."""
+    from paper_2308_04079_b200 import rasterizer as R
+    from paper_2308_04079_b200.cloud import GaussianCloud
+    from paper_2308_04079_b200.densify import TrainState
+    from paper_2308_04079_b200.errors import TrainingDiverged
+    from paper_2308_04079_b200.optimizer import TrainConfig, step_guard
+    from paper_2308_04079_b200.training import TrainView, train_step
+    cloud_np, cam = synthetic.frustum_scene(5_000, 160, 120, seed=21)
+    target = R.render_view(GaussianCloud.from_numpy(**synthetic.frustum_scene(5_000, 160, 120, seed=22)[0]),
+                           cam, (0, 0, 0), 3)[0].image
+    cfg = TrainConfig(warmup_upsample_iters=(0, 0))
+    state = TrainState(GaussianCloud.from_numpy(**cloud_np), 10.0, seed=0)
+    train_step(state, [TrainView(cam, target)], cfg)          # one good step: moments and stats non-zero
+    snap = {g: getattr(state.cloud, g).clone() for g in ("means", "rotations", "log_scales", "opacity_logits", "sh")}
+    moments = [t.clone() for d in (state.adam.exp_avg, state.adam.exp_avg_sq) for t in d.values()]
+    stats = [state.stats.accum_pos_grad.clone(), state.stats.accum_count.clone(), state.stats.max_radius_frac.clone()]
+    bad = target.clone()
+    bad[3, 5, 1] = float("nan")
+    with pytest.raises(TrainingDiverged):
+        train_step(state, [TrainView(cam, bad)], cfg)
+    torch.cuda.synchronize()
+    for g, t in snap.items():
+        assert torch.equal(getattr(state.cloud, g), t), g
+    for a, b in zip([t for d in (state.adam.exp_avg, state.adam.exp_avg_sq) for t in d.values()], moments):
+        assert torch.equal(a, b)
+    assert torch.equal(state.stats.accum_pos_grad, stats[0]) and torch.equal(state.stats.accum_count, stats[1])
+    assert torch.equal(state.stats.max_radius_frac, stats[2])
+    # the guard itself
+    k = torch.tensor([10, 0, 10], dtype=torch.int64, device="cuda")
+    assert step_guard(torch.tensor([1.0, 0, 0, 0], device="cuda"), k).item() == 0
+    assert step_guard(torch.tensor([float("inf"), 0, 0, 0], device="cuda"), k).item() == 1
+    assert step_guard(torch.tensor([1.0, 0, 0, 0], device="cuda"), torch.tensor([10, 2, 5], dtype=torch.int64,
+                                                                                 device="cuda")).item() == 1
+
+
+@pytest.mark.gpu
+def test_lookahead_matches_plain_steps(cuda_device):
+    """train_step(lookahead=True) enqueues the next iteration's forward before
+    waiting; the sampled views, losses and parameters must equal the plain
+    sequence, including across densify_and_prune (which discards the
+    lookahead and restores the view-sampling RNG it consumed)."""
+    from paper_2308_04079_b200 import rasterizer as R
+    from paper_2308_04079_b200.cloud import GaussianCloud
+    from paper_2308_04079_b200.densify import TrainState, densify_and_prune
+    from paper_2308_04079_b200.optimizer import TrainConfig
+    from paper_2308_04079_b200.training import TrainView, train_step
+    cloud_np, cam = synthetic.frustum_scene(8_000, 160, 120, seed=31)
+    tcloud = GaussianCloud.from_numpy(**synthetic.frustum_scene(8_000, 160, 120, seed=32)[0])
+    cams = [cam, cam.scaled(1.0)]
+    targets = [R.render_view(tcloud, c, (0, 0, 0), 3)[0].image.cpu().pin_memory() for c in cams]
+    views = [TrainView(c, t) for c, t in zip(cams, targets)] * 2
+    cfg = TrainConfig(warmup_upsample_iters=(0, 0), sh_band_interval=4, densify_start=0)
+    runs = []
+    for look in (False, True):
+        state = TrainState(GaussianCloud.from_numpy(**cloud_np), 10.0, seed=5)
+        seq = []
+        for i in range(14):
+            rep = train_step(state, views, cfg, lookahead=look)
+            seq.append((rep.view_index, rep.loss, state.active_sh_degree))
+            if i == 6:
+                densify_and_prune(state, cfg)
+        state.discard_lookahead()
+        runs.append((seq, state))
+    (a, sa), (b, sb) = runs
+    assert [x[0] for x in a] == [x[0] for x in b] and [x[2] for x in a] == [x[2] for x in b]
+    np.testing.assert_allclose([x[1] for x in a], [x[1] for x in b], rtol=1e-4)
+    assert sa.rng.bit_generator.state == sb.rng.bit_generator.state
+    assert len(sa.cloud) == len(sb.cloud)
+    for g in ("means", "rotations", "log_scales", "opacity_logits", "sh"):
+        torch.testing.assert_close(getattr(sa.cloud, g), getattr(sb.cloud, g), rtol=1e-3, atol=1e-5)
