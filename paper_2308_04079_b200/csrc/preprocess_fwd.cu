@@ -14,7 +14,10 @@ __device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a,
 __device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
 __device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
 
-__global__ void __launch_bounds__(128)
+#ifndef GS_PREFWD_MINB
+#define GS_PREFWD_MINB 6   // 80 registers, no spills: 0.196 vs 0.208 ms at the default 94
+#endif
+__global__ void __launch_bounds__(128, GS_PREFWD_MINB)
 preprocess_fwd_kernel(gs_params_t p, DevCamera cam, int degree, gs_splats_t out) {
   const int64_t g0 = int64_t(blockIdx.x) * blockDim.x;
   const int64_t g = g0 + threadIdx.x;

@@ -64,6 +64,7 @@ def main() -> None:
         "blend_fwd_ms": timeit(lambda: R.render_forward(splats, binning, 1920, 1080, bg, training=True)),
         "blend_bwd_ms": timeit(lambda: R.render_backward(d, out, splats, binning, 1920, 1080, bg)),
         "bin_async_ms": timeit(lambda: R.bin_and_sort_async(splats, 1920, 1080)),
+        "preprocess_fwd_ms": timeit(lambda: R._project_tensors(cloud.c_params(), len(cloud), "cuda", cam, 3)),
     }
     if "--bands" in sys.argv:
         def full_frame():
