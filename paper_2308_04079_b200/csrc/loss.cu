@@ -176,11 +176,12 @@ ssim_forward_kernel(const float* __restrict__ img, const float* __restrict__ gt,
         const double mu_x = msx + double(kShift) * win.total, mu_y = msy + double(kShift) * win.total;
         const double a1 = 2.0 * mu_x * mu_y + kC1, a2 = 2.0 * sxy + kC2;
         const double b1 = mu_x * mu_x + mu_y * mu_y + kC1, b2 = sx + sy + kC2;
-        ssim_sum += (a1 * a2) / (b1 * b2);
+        // one float64 division per pixel and channel: 1/b1 = b2/(b1 b2), 1/b2 = b1/(b1 b2)
+        const double inv = 1.0 / (b1 * b2);
+        ssim_sum += (a1 * a2) * inv;
         // ssim_backward (ssim.py:67-84) with a constant d_map
-        const double denom = b1 * b2;
-        const double d_a1 = d_map * a2 / denom, d_a2 = d_map * a1 / denom;
-        const double d_b1 = -d_a1 * (a1 / b1), d_b2 = -d_a2 * (a2 / b2);
+        const double d_a1 = d_map * a2 * inv, d_a2 = d_map * a1 * inv;
+        const double d_b1 = -d_a1 * (a1 * b2 * inv), d_b2 = -d_a2 * (a2 * b1 * inv);
         const double d_mu = 2.0 * mu_y * d_a1 + 2.0 * mu_x * d_b1 - 2.0 * mu_y * d_a2 - 2.0 * mu_x * d_b2;
         src[9 * p + 3 * 0 + ch] = float(d_mu);
         src[9 * p + 3 * 1 + ch] = float(d_b2);
