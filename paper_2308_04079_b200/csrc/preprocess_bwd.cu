@@ -82,8 +82,10 @@ __device__ __forceinline__ void grad_one_t(const GradInputs& in, const DevCamera
   for (int i = 0; i < 3; ++i)
     view[i] = mx * cR[3 * i + 0] + my * cR[3 * i + 1] + mz * cR[3 * i + 2] + ct[i];
   const Real x = view[0], y = view[1], z = view[2];
-  const Real z2 = z * z, z3 = z2 * z;
-  const Real j00 = cfx / z, j02 = -cfx * x / z2, j11 = cfy / z, j12 = -cfy * y / z2;
+  // gradients only from here on (no integer is decided): reciprocals are
+  // formed once and multiplied, ~1e-16 relative from the divided form
+  const Real inv_z = Real(1.0) / z, inv_z2 = inv_z * inv_z, inv_z3 = inv_z2 * inv_z;
+  const Real j00 = cfx * inv_z, j02 = -cfx * x * inv_z2, j11 = cfy * inv_z, j12 = -cfy * y * inv_z2;
   Real U[6];
 #pragma unroll
   for (int c = 0; c < 3; ++c) {
@@ -121,7 +123,8 @@ __device__ __forceinline__ void grad_one_t(const GradInputs& in, const DevCamera
   const Real cb = US[0] * U[3] + US[1] * U[4] + US[2] * U[5];
   const Real cc = US[3] * U[3] + US[4] * U[4] + US[5] * U[5] + Real(kLowpass);
   const Real det = ca * cc - cb * cb;
-  const Real A0 = cc / det, A1 = -cb / det, A2 = ca / det;  // conic (core.py:316)
+  const Real inv_det = Real(1.0) / det;
+  const Real A0 = cc * inv_det, A1 = -cb * inv_det, A2 = ca * inv_det;  // conic (core.py:316)
 
   // --- conic -> floored screen covariance: dS' = -A G A (gradients.py:97-113)
   const Real G0 = gb.x, G1 = Real(0.5) * Real(gb.y), G2 = gb.z;
@@ -176,8 +179,9 @@ __device__ __forceinline__ void grad_one_t(const GradInputs& in, const DevCamera
   const Cov dqk = Cov(2.0) * (-Cov(2.0) * qk * dR[0] - qr * dR[1] + qi * dR[2] + qr * dR[3] - Cov(2.0) * qk * dR[4] +
                             qj * dR[5] + qi * dR[6] + qj * dR[7]);
   const Cov qdot = qr * dqr + qi * dqi + qj * dqj + qk * dqk;
-  const float4 d_rot = make_float4(float((dqr - qr * qdot) / qn), float((dqi - qi * qdot) / qn),
-                                   float((dqj - qj * qdot) / qn), float((dqk - qk * qdot) / qn));
+  const Cov inv_qn = Cov(1.0) / qn;
+  const float4 d_rot = make_float4(float((dqr - qr * qdot) * inv_qn), float((dqi - qi * qdot) * inv_qn),
+                                   float((dqj - qj * qdot) * inv_qn), float((dqk - qk * qdot) * inv_qn));
 
   // --- view position: J^T d_mean2d plus the dependence of J on the mean
   //     (gradients.py:236-255)
@@ -196,15 +200,16 @@ __device__ __forceinline__ void grad_one_t(const GradInputs& in, const DevCamera
     for (int k = 0; k < 3; ++k)
       dJ[3 * r + k] = dU[3 * r + 0] * cR[3 * k + 0] + dU[3 * r + 1] * cR[3 * k + 1] +
                       dU[3 * r + 2] * cR[3 * k + 2];
-  dt[0] += dJ[2] * (-cfx / z2);
-  dt[1] += dJ[5] * (-cfy / z2);
-  dt[2] += dJ[0] * (-cfx / z2) + dJ[2] * (Real(2.0) * cfx * x / z3) + dJ[4] * (-cfy / z2) +
-           dJ[5] * (Real(2.0) * cfy * y / z3);
+  dt[0] += dJ[2] * (-cfx * inv_z2);
+  dt[1] += dJ[5] * (-cfy * inv_z2);
+  dt[2] += dJ[0] * (-cfx * inv_z2) + dJ[2] * (Real(2.0) * cfx * x * inv_z3) + dJ[4] * (-cfy * inv_z2) +
+           dJ[5] * (Real(2.0) * cfy * y * inv_z3);
 
   // --- colour: clamp mask, SH coefficients, direction path (gradients.py:219-226)
   const Real ddx = mx - ccen[0], ddy = my - ccen[1], ddz = mz - ccen[2];
   const Real dist = sqrt(ddx * ddx + ddy * ddy + ddz * ddz);
-  const float vx = float(ddx / dist), vy = float(ddy / dist), vz = float(ddz / dist);
+  const Real inv_dist_r = Real(1.0) / dist;
+  const float vx = float(ddx * inv_dist_r), vy = float(ddy * inv_dist_r), vz = float(ddz * inv_dist_r);
   sh_basis(vx, vy, vz, degree, b);
   dcol[0] = (mask & 1) ? gc.x : 0.0f;
   dcol[1] = (mask & 2) ? gc.y : 0.0f;
@@ -223,7 +228,7 @@ __device__ __forceinline__ void grad_one_t(const GradInputs& in, const DevCamera
   float gdx, gdy, gdz;
   sh_basis_vjp(vx, vy, vz, degree, db, gdx, gdy, gdz);
   const float vdot = vx * gdx + vy * gdy + vz * gdz;
-  const float inv_dist = float(Real(1.0) / dist);
+  const float inv_dist = float(inv_dist_r);
   const float dms[3] = {(gdx - vx * vdot) * inv_dist, (gdy - vy * vdot) * inv_dist, (gdz - vz * vdot) * inv_dist};
 
   // --- d_means = d_t W + d_mean_sh (gradients.py:257)
