@@ -95,7 +95,7 @@ __device__ __forceinline__ void grad_one_t(const GradInputs& in, const DevCamera
 
   // --- covariance from the raw quaternion and log scales (core.py:187-201),
   //     always float64: the rotation gradient below relies on R R^T = I and
-  //     a symmetric dSigma to cancel (exactly 0 for isotropic Gaussians)
+  //     a symmetric dSigma to cancel (to ~1e-16 of |d log_scale| for isotropic Gaussians)
   using Cov = double;
   const float4 qf = in.q;
   const Cov qn = sqrt(Cov(qf.x) * qf.x + Cov(qf.y) * qf.y + Cov(qf.z) * qf.z + Cov(qf.w) * qf.w);
@@ -250,10 +250,11 @@ __device__ __forceinline__ void grad_one_t(const GradInputs& in, const DevCamera
 // decided here, the forward keeps float64 for radii / keys).  GS_BWD_REAL =
 // float runs view position, J, U, the conic and dSigma' in float32; the
 // covariance R, M and the dM -> (d log_scale, d quaternion) chain stay
-// float64 (see grad_one_t).  Measured at c3: fused backward + Adam 1.087 ms
-// (all float64) -> 0.977 ms, every parity test unchanged; all-float32 was
-// 0.85 ms but leaves ~1e-7-relative noise in the (exactly zero) rotation
-// gradient of isotropic Gaussians.
+// float64 (see grad_one_t).  The float32 variant was 10% faster but drifted
+// 0.1-0.7% from the reference in d_rotations on adversarial fuzz scenes
+// (test_fuzz_scenes_vs_oracle), so the default is float64 throughout; the
+// cost of float64 is mostly its divisions, formed once as reciprocals
+// (fused backward + Adam 1.027 -> 0.933 ms at c3).
 #ifndef GS_BWD_REAL
 #define GS_BWD_REAL double
 #endif
