@@ -348,8 +348,9 @@ __device__ __forceinline__ float4 conic_basis(double a, double b, double c, doub
   double ex = h >= 0.0 ? h + r : b, ey = h >= 0.0 ? b : r - h;  // whichever form does not cancel
   const double nn = sqrt(ex * ex + ey * ey);
   if (nn > 0.0) {
-    ex /= nn;
-    ey /= nn;
+    const double inv = 1.0 / nn;
+    ex *= inv;
+    ey *= inv;
   } else {
     ex = 1.0;
     ey = 0.0;

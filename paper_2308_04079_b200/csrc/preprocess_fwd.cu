@@ -139,10 +139,13 @@ preprocess_fwd_kernel(gs_params_t p, DevCamera cam, int degree, gs_splats_t out)
   radius_out = rad_d >= 2147483647.0 ? 2147483647 : int32_t(rad_d);
 
   // tile rectangle, inclusive, clipped (rasterizer.py:86-97)
-  const double x0d = floor(__ddiv_rn(dsub(u, rad_d), double(kTile)));
-  const double x1d = floor(__ddiv_rn(dadd(u, rad_d), double(kTile)));
-  const double y0d = floor(__ddiv_rn(dsub(v, rad_d), double(kTile)));
-  const double y1d = floor(__ddiv_rn(dadd(v, rad_d), double(kTile)));
+  // x / 16 == x * 2^-4 exactly (power-of-two scaling), without a division
+  constexpr double kInvTile = 1.0 / double(kTile);
+  static_assert((kTile & (kTile - 1)) == 0, "tile size must be a power of two");
+  const double x0d = floor(dmul(dsub(u, rad_d), kInvTile));
+  const double x1d = floor(dmul(dadd(u, rad_d), kInvTile));
+  const double y0d = floor(dmul(dsub(v, rad_d), kInvTile));
+  const double y1d = floor(dmul(dadd(v, rad_d), kInvTile));
   const double txm = double(cam.tiles_x - 1), tym = double(cam.tiles_y - 1);
   const bool valid = (x1d >= 0.0) && (x0d < double(cam.tiles_x)) && (y1d >= 0.0) && (y0d < double(cam.tiles_y));
   const int32_t x0 = int32_t(fmin(fmax(x0d, 0.0), txm));
@@ -157,7 +160,9 @@ preprocess_fwd_kernel(gs_params_t p, DevCamera cam, int degree, gs_splats_t out)
   // SH colour along the unit camera->mean direction (core.py:321-326)
   const double dx = dsub(mx, cam.center[0]), dy = dsub(my, cam.center[1]), dz = dsub(mz, cam.center[2]);
   const double dist = sqrt(dadd(dadd(dmul(dx, dx), dmul(dy, dy)), dmul(dz, dz)));
-  const float vx = float(__ddiv_rn(dx, dist)), vy = float(__ddiv_rn(dy, dist)), vz = float(__ddiv_rn(dz, dist));
+  // float32 colour path: one reciprocal instead of three divisions
+  const double inv_dist = __drcp_rn(dist);
+  const float vx = float(dmul(dx, inv_dist)), vy = float(dmul(dy, inv_dist)), vz = float(dmul(dz, inv_dist));
   float b[16];
   sh_basis(vx, vy, vz, degree, b);
   const int nrows = (degree + 1) * (degree + 1);
