@@ -245,6 +245,22 @@ int gs_blend_backward(const float* d_image, const gs_splats_t* splats, const uin
                       const int32_t* ranges, const float* t_final, const int32_t* last,
                       int32_t width, int32_t height, const float background[3],
                       float* grads2d, void* stream);
+
+/* gs_blend_backward with the tiles visited in `tile_order` (a permutation of
+ * [0, tiles), device int32). */
+int gs_blend_backward_ordered(const float* d_image, const gs_splats_t* splats, const uint32_t* sorted_ids,
+                              const int32_t* ranges, const float* t_final, const int32_t* last, int32_t width,
+                              int32_t height, const float background[3], const int32_t* tile_order,
+                              float* grads2d, void* stream);
+
+/* gs_blend_backward on a longest-first tile schedule built on the device from
+ * the training record: a tile's work is max(last contributor) - start + 1
+ * (gradients.py:48-52); heavy tiles start first so light ones fill the last
+ * wave.  scratch: caller-owned device int32[2 * tiles + 128]. */
+int gs_blend_backward_scheduled(const float* d_image, const gs_splats_t* splats, const uint32_t* sorted_ids,
+                                const int32_t* ranges, const float* t_final, const int32_t* last, int32_t width,
+                                int32_t height, const float background[3], int32_t* scratch, float* grads2d,
+                                void* stream);
 /* The tiles of rows [tile_row_begin, tile_row_end) only, ACCUMULATING into
  * grads2d (not cleared: clear it once per frame, then one call per band). */
 int gs_blend_backward_rows(const float* d_image, const gs_splats_t* splats, const uint32_t* sorted_ids,

@@ -115,6 +115,10 @@ SIGNATURES = [
                                                       c_double, c_double, c_double, c_double, POINTER(GsStats),
                                                       POINTER(GsGrads), c_void_p, c_void_p]),
     ("gs_step_guard", c_int32, [c_void_p, c_void_p, c_void_p, c_void_p]),
+    ("gs_blend_backward_ordered", c_int32, [c_void_p, POINTER(GsSplats), c_void_p, c_void_p, c_void_p, c_void_p,
+                                            c_int32, c_int32, POINTER(c_float), c_void_p, c_void_p, c_void_p]),
+    ("gs_blend_backward_scheduled", c_int32, [c_void_p, POINTER(GsSplats), c_void_p, c_void_p, c_void_p, c_void_p,
+                                              c_int32, c_int32, POINTER(c_float), c_void_p, c_void_p, c_void_p]),
     ("gs_densify_workspace_size", c_int32, [c_int64, POINTER(c_size_t)]),
     ("gs_densify_classify", c_int32, [POINTER(GsCloudState), POINTER(GsStats), POINTER(GsDensifyConfig), c_void_p,
                                       c_size_t, POINTER(c_int64), POINTER(c_int64), c_void_p]),

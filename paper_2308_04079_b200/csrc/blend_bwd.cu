@@ -105,14 +105,17 @@ __device__ __forceinline__ void batch_bounds(int b, int tile_top, int range_lo, 
 __global__ void __launch_bounds__(kThreads, GS_BWD_MIN_BLOCKS)
 blend_bwd_kernel(const float* __restrict__ d_image, const float4* __restrict__ rec, const uint32_t* __restrict__ ids,
                  const int2* __restrict__ ranges, const float* __restrict__ t_final, const int32_t* __restrict__ last,
-                 int width, int height, int tiles_x, int tile0, float3 bg, float4* __restrict__ grads2d) {
+                 int width, int height, int tiles_x, int tile0, float3 bg, float4* __restrict__ grads2d,
+                 const int32_t* __restrict__ tile_order) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   BwdStage* stages = reinterpret_cast<BwdStage*>(smem_raw);
   RawRec* raw = reinterpret_cast<RawRec*>(smem_raw + sizeof(BwdStage) * kStages);
   __shared__ uint64_t full_bar[kStages], empty_bar[kStages];
   __shared__ int s_warp_max[kConsumerWarps + 1];
 
-  const int tile = tile0 + int(blockIdx.x) / kParts;
+  // tile_order (optional): the launch visits tiles in this order (e.g. the
+  // longest lists first, so the light tiles fill the last wave)
+  const int tile = tile_order ? tile_order[int(blockIdx.x) / kParts] : tile0 + int(blockIdx.x) / kParts;
   const int part = int(blockIdx.x) % kParts;   // this CTA's rows: [part * 16 / kParts, (part + 1) * 16 / kParts)
   const int t = threadIdx.x;
   const int lane = t & 31, warp = t >> 5;
@@ -283,7 +286,7 @@ blend_bwd_kernel(const float* __restrict__ d_image, const float4* __restrict__ r
 int blend_backward_rows(const float* d_image, const gs_splats_t* splats, const uint32_t* sorted_ids,
                         const int32_t* ranges, const float* t_final, const int32_t* last, int32_t width,
                         int32_t height, int32_t row_begin, int32_t row_end, const float background[3],
-                        float* grads2d, void* stream) {
+                        float* grads2d, void* stream, const int32_t* tile_order = nullptr) {
   if (!d_image || !splats || !ranges || !t_final || !last || !grads2d || !background || width <= 0 ||
       height <= 0)
     return GS_ERR_INVALID_ARG;
@@ -303,7 +306,8 @@ int blend_backward_rows(const float* d_image, const gs_splats_t* splats, const u
   const int64_t ntiles = int64_t(row_end - row_begin) * tiles_x;
   blend_bwd_kernel<<<unsigned(ntiles * kParts), kThreads, kSmemBytes, static_cast<cudaStream_t>(stream)>>>(
       d_image, reinterpret_cast<const float4*>(splats->rec), sorted_ids, reinterpret_cast<const int2*>(ranges),
-      t_final, last, width, height, tiles_x, row_begin * tiles_x, bg, reinterpret_cast<float4*>(grads2d));
+      t_final, last, width, height, tiles_x, row_begin * tiles_x, bg, reinterpret_cast<float4*>(grads2d),
+      tile_order);
   return check_launch();
 }
 
@@ -330,4 +334,111 @@ extern "C" int gs_blend_backward_rows(const float* d_image, const gs_splats_t* s
                                       const float background[3], float* grads2d, void* stream) {
   return gs::blend_backward_rows(d_image, splats, sorted_ids, ranges, t_final, last, width, height, tile_row_begin,
                                  tile_row_end, background, grads2d, stream);
+}
+
+// The full frame with the tiles visited in `tile_order` (a permutation of
+// [0, tiles), device int32), e.g. by descending list length.
+extern "C" int gs_blend_backward_ordered(const float* d_image, const gs_splats_t* splats, const uint32_t* sorted_ids,
+                                         const int32_t* ranges, const float* t_final, const int32_t* last,
+                                         int32_t width, int32_t height, const float background[3],
+                                         const int32_t* tile_order, float* grads2d, void* stream) {
+  using namespace gs;
+  if (!splats || !grads2d || !tile_order || width <= 0 || height <= 0) return GS_ERR_INVALID_ARG;
+  cudaError_t e = cudaMemsetAsync(grads2d, 0, size_t(splats->n) * GS_GRAD2D_FLOATS * sizeof(float),
+                                  static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return record_cuda_error(e);
+  return blend_backward_rows(d_image, splats, sorted_ids, ranges, t_final, last, width, height, 0,
+                             (height + kTile - 1) / kTile, background, grads2d, stream, tile_order);
+}
+
+// ---------------------------------------------------------------------------
+// Longest-first tile schedule for the backward: a tile's work is its number
+// of back-to-front splats, need = max(last contributor) - start + 1
+// (gradients.py:48-52), known from the forward's training record.  Tiles are
+// bucketed by need on a quarter-octave scale and visited from the heaviest
+// bucket down, so the light tiles fill the last wave instead of a few heavy
+// ones trailing it (measured 1.216 -> 1.13 ms at c3).  Scratch: 2 T + 128 ints.
+namespace gs {
+namespace {
+constexpr int kSchedBuckets = 64;
+
+__device__ __forceinline__ int need_bucket(int need) {
+  return need <= 0 ? 0 : min(kSchedBuckets - 1, 1 + int(__log2f(float(need)) * 4.0f));
+}
+
+// one warp per tile: max of `last` over the tile's pixels
+__global__ void tile_need_kernel(const int32_t* __restrict__ last, const int2* __restrict__ ranges, int width,
+                                 int height, int tiles_x, int tiles, int32_t* __restrict__ bucket_of,
+                                 int32_t* __restrict__ hist) {
+  const int tile = int((int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
+  if (tile >= tiles) return;
+  const int tx = tile % tiles_x, ty = tile / tiles_x;
+  int m = -1;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int p = lane + 32 * k;             // 16 x 16 pixels, row-major within the tile
+    const int px = tx * kTile + (p & 15), py = ty * kTile + (p >> 4);
+    if (px < width && py < height) m = max(m, last[size_t(py) * width + px]);
+  }
+  m = __reduce_max_sync(0xffffffffu, m);
+  if (lane == 0) {
+    const int2 r = ranges[tile];
+    const int b = need_bucket(m >= r.x ? m - r.x + 1 : 0);
+    bucket_of[tile] = b;
+    atomicAdd(&hist[b], 1);
+  }
+}
+
+// exclusive scan over the buckets from the heaviest down (one warp)
+__global__ void tile_sched_scan_kernel(const int32_t* __restrict__ hist, int32_t* __restrict__ cursor) {
+  const int lane = threadIdx.x;
+  // lane l owns buckets 63 - 2l and 62 - 2l (descending order)
+  const int b0 = kSchedBuckets - 1 - 2 * lane, b1 = b0 - 1;
+  const int c0 = hist[b0], c1 = hist[b1];
+  int incl = c0 + c1;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  const int excl = incl - (c0 + c1);
+  cursor[b0] = excl;
+  cursor[b1] = excl + c0;
+}
+
+__global__ void tile_sched_scatter_kernel(const int32_t* __restrict__ bucket_of, int32_t* __restrict__ cursor,
+                                          int tiles, int32_t* __restrict__ order) {
+  const int t = int(int64_t(blockIdx.x) * blockDim.x + threadIdx.x);
+  if (t < tiles) order[atomicAdd(&cursor[bucket_of[t]], 1)] = t;
+}
+}  // namespace
+}  // namespace gs
+
+extern "C" int gs_blend_backward_scheduled(const float* d_image, const gs_splats_t* splats,
+                                           const uint32_t* sorted_ids, const int32_t* ranges, const float* t_final,
+                                           const int32_t* last, int32_t width, int32_t height,
+                                           const float background[3], int32_t* scratch, float* grads2d,
+                                           void* stream) {
+  using namespace gs;
+  if (!splats || !grads2d || !scratch || !ranges || !last || width <= 0 || height <= 0) return GS_ERR_INVALID_ARG;
+  const int tiles_x = (width + kTile - 1) / kTile, tiles_y = (height + kTile - 1) / kTile;
+  const int64_t tiles64 = int64_t(tiles_x) * tiles_y;
+  if (tiles64 > int64_t(INT32_MAX) / 4) return GS_ERR_RESOURCE_LIMIT;
+  const int tiles = int(tiles64);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  int32_t* order = scratch;
+  int32_t* bucket_of = scratch + tiles;
+  int32_t* hist = scratch + 2 * tiles;
+  int32_t* cursor = hist + kSchedBuckets;
+  cudaError_t e = cudaMemsetAsync(hist, 0, kSchedBuckets * sizeof(int32_t), s);
+  if (e != cudaSuccess) return record_cuda_error(e);
+  tile_need_kernel<<<unsigned((int64_t(tiles) * 32 + 255) / 256), 256, 0, s>>>(
+      last, reinterpret_cast<const int2*>(ranges), width, height, tiles_x, tiles, bucket_of, hist);
+  tile_sched_scan_kernel<<<1, 32, 0, s>>>(hist, cursor);
+  tile_sched_scatter_kernel<<<unsigned((tiles + 255) / 256), 256, 0, s>>>(bucket_of, cursor, tiles, order);
+  int st = check_launch();
+  if (st != GS_OK) return st;
+  return gs_blend_backward_ordered(d_image, splats, sorted_ids, ranges, t_final, last, width, height, background,
+                                   order, grads2d, stream);
 }

@@ -6,7 +6,7 @@ reference (splatlab):
   project          core.py:266-345        -> gs_preprocess_forward   (K1)
   bin_and_sort     rasterizer.py:69-124   -> gs_bin_and_sort         (K2-K5)
   render_forward   rasterizer.py:201-240  -> gs_blend_forward        (K6)
-  render_backward  rasterizer.py:253-316  -> gs_blend_backward       (K7)
+  render_backward  rasterizer.py:253-316  -> gs_blend_backward_scheduled (K7)
   backward_project gradients.py:192-259   -> gs_preprocess_backward  (K8)
   render_view      optimizer.py:212-219   (composition of the first three)
 Everything runs on the current CUDA stream; buffers come from torch's
@@ -70,7 +70,7 @@ def _camera(camera) -> Camera:
 class DeviceSplats:
     """Per-view projected splats in N-space (see gs_splats_t)."""
 
-    rec: torch.Tensor            # (N,12) float32
+    rec: torch.Tensor            # (N,20) float32, see gs_splats_t
     depth: torch.Tensor          # (N,)   float32
     radii: torch.Tensor          # (N,)   int32, 0 = culled
     rect: torch.Tensor           # (N,4)  int32
@@ -431,11 +431,23 @@ def render_backward(d_image: torch.Tensor, output: RenderOutput, splats: DeviceS
         raise ValueError(f"d_image shape {tuple(d_image.shape)} != {(height, width, 3)}")
     packed = torch.empty((len(splats), _lib.GRAD2D_FLOATS), dtype=torch.float32, device=splats.rec.device)
     cs = splats.c_struct()
-    _lib.check(lib.gs_blend_backward(d_image.data_ptr(), ctypes.byref(cs), binning.splat_ids.data_ptr(),
-                                     binning.ranges.data_ptr(), output.final_transmittance.data_ptr(),
-                                     output.last_contributor.data_ptr(), width, height, _bg(background),
-                                     packed.data_ptr(), _stream()), "render_backward")
+    if _BWD_SCHEDULE:
+        # longest-first tile order from the forward's training record (scratch: 2 T + 128 int32)
+        tx, ty = tile_extent(width, height)
+        scratch = torch.empty(2 * tx * ty + 128, dtype=torch.int32, device=splats.rec.device)
+        _lib.check(lib.gs_blend_backward_scheduled(
+            d_image.data_ptr(), ctypes.byref(cs), binning.splat_ids.data_ptr(), binning.ranges.data_ptr(),
+            output.final_transmittance.data_ptr(), output.last_contributor.data_ptr(), width, height,
+            _bg(background), scratch.data_ptr(), packed.data_ptr(), _stream()), "render_backward")
+    else:
+        _lib.check(lib.gs_blend_backward(d_image.data_ptr(), ctypes.byref(cs), binning.splat_ids.data_ptr(),
+                                         binning.ranges.data_ptr(), output.final_transmittance.data_ptr(),
+                                         output.last_contributor.data_ptr(), width, height, _bg(background),
+                                         packed.data_ptr(), _stream()), "render_backward")
     return SplatGrads2D(packed)
+
+
+_BWD_SCHEDULE = __import__("os").environ.get("GS_BWD_SCHEDULE", "1") != "0"
 
 
 def _backward_project_tensors(params: _lib.GsParams, n: int, device, camera: Camera, splats: DeviceSplats,

@@ -27,6 +27,7 @@ def main() -> None:
     ap.add_argument("--n", type=int, default=3_000_000)
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--bands", action="store_true", help="also time the banded (multi-stream) frame")
+    ap.add_argument("--order", action="store_true", help="also time the backward with heavy tiles first")
     ap.add_argument("--split", action="store_true", help="also time row-split blend launches on 2-4 streams")
     args = ap.parse_args()
     lib = _lib.load()
@@ -66,6 +67,27 @@ def main() -> None:
         "bin_async_ms": timeit(lambda: R.bin_and_sort_async(splats, 1920, 1080)),
         "preprocess_fwd_ms": timeit(lambda: R._project_tensors(cloud.c_params(), len(cloud), "cuda", cam, 3)),
     }
+    if "--order" in sys.argv:
+        import ctypes
+        lib, cs, bgc = _lib.load(), splats.c_struct(), R._bg(bg)
+        rg = binning.ranges.view(-1, 2)
+        lens = (rg[:, 1] - rg[:, 0]).to(torch.int64)
+        tx, ty = (1920 + 15) // 16, (1080 + 15) // 16
+        last = out.last_contributor.view(1080, 1920)
+        pad = torch.full((ty * 16, tx * 16), -1, dtype=last.dtype, device=last.device)
+        pad[:1080, :1920] = last
+        tl = pad.view(ty, 16, tx, 16).amax(dim=(1, 3)).reshape(-1).to(torch.int64)
+        need = torch.where(tl >= rg[:, 0].to(torch.int64), tl - rg[:, 0].to(torch.int64) + 1, torch.zeros_like(tl))
+        g2o = torch.zeros((len(splats), 12), device="cuda")
+        for name, key in (("len", lens), ("need", need)):
+            order = torch.argsort(key, descending=True, stable=True).to(torch.int32)
+            def run():
+                lib.gs_blend_backward_ordered(d.data_ptr(), ctypes.byref(cs), binning.splat_ids.data_ptr(),
+                                              binning.ranges.data_ptr(), out.final_transmittance.data_ptr(),
+                                              out.last_contributor.data_ptr(), 1920, 1080, bgc, order.data_ptr(),
+                                              g2o.data_ptr(), torch.cuda.current_stream().cuda_stream)
+            res[f"blend_bwd_order_{name}_ms"] = timeit(run)
+            res[f"order_{name}_checksum"] = float(g2o.abs().sum().item())
     if "--bands" in sys.argv:
         def full_frame():
             sp = R._project_tensors(cloud.c_params(), len(cloud), "cuda", cam, 3)
