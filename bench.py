@@ -155,6 +155,7 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
         grads = R.GaussianGrads.zeros(n, dev)
     timer = StageTimer(enabled=True)
     iteration = [0]
+    prev_order = [None]
 
     def train_step(gt: torch.Tensor, timed: bool) -> torch.Tensor:
         iteration[0] += 1
@@ -167,11 +168,13 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
             binning = R.bin_and_sort_async(splats, WIDTH, HEIGHT)
         binnings.append(binning.k_info)
         with StageTimer.stage(tm, "blend_fwd"):
-            out = R.render_forward(splats, binning, WIDTH, HEIGHT, bg, training=True)
+            # tiles in the previous backward's longest-first order (same view)
+            out = R.render_forward(splats, binning, WIDTH, HEIGHT, bg, training=True, tile_order=prev_order[0])
         with StageTimer.stage(tm, "loss"):
             loss, d_image = l1_dssim_loss(out.image, gt, LAMBDA_DSSIM)
         with StageTimer.stage(tm, "blend_bwd"):
             g2 = R.render_backward(d_image, out, splats, binning, WIDTH, HEIGHT, bg)
+        prev_order[0] = g2.tile_order
         if sharded is None and os.environ.get("GS_BENCH_UNFUSED") != "1":
             # single GPU: backward_project + stats + Adam fused (no gradient round trip)
             with StageTimer.stage(tm, "preprocess_bwd_adam"):

@@ -228,6 +228,13 @@ int gs_bin_rows_async(const gs_splats_t* splats, const uint32_t* order, int32_t 
 int gs_blend_forward(const gs_splats_t* splats, const uint32_t* sorted_ids, const int32_t* ranges,
                      int32_t width, int32_t height, const float background[3], int32_t training,
                      float* image, float* t_final, int32_t* last, void* stream);
+
+/* gs_blend_forward with the tiles launched in `tile_order` (a permutation of
+ * [0, tiles), device int32; e.g. the previous backward's longest-first
+ * schedule of the same view).  The outputs do not depend on the order. */
+int gs_blend_forward_ordered(const gs_splats_t* splats, const uint32_t* sorted_ids, const int32_t* ranges,
+                             int32_t width, int32_t height, const float background[3], int32_t training,
+                             const int32_t* tile_order, float* image, float* t_final, int32_t* last, void* stream);
 /* The tiles of rows [tile_row_begin, tile_row_end) only (sorted_ids: that
  * band's instance list from gs_bin_rows_async). */
 int gs_blend_forward_rows(const gs_splats_t* splats, const uint32_t* sorted_ids, const int32_t* ranges,

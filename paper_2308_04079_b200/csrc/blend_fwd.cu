@@ -90,14 +90,14 @@ template <bool kTraining>
 __global__ void __launch_bounds__(kThreads)
 blend_fwd_kernel(const float4* __restrict__ rec, const uint32_t* __restrict__ ids, const int2* __restrict__ ranges,
                  int width, int height, int tiles_x, int tile0, float3 bg, float* __restrict__ image,
-                 float* __restrict__ t_final, int32_t* __restrict__ last) {
+                 float* __restrict__ t_final, int32_t* __restrict__ last, const int32_t* __restrict__ tile_order) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   FwdStage* stages = reinterpret_cast<FwdStage*>(smem_raw);
   RawRec* raw = reinterpret_cast<RawRec*>(smem_raw + sizeof(FwdStage) * kStages);
   __shared__ uint64_t full_bar[kStages], empty_bar[kStages];
   __shared__ int s_done, s_stop;
 
-  const int tile = tile0 + int(blockIdx.x) / kParts;
+  const int tile = tile_order ? tile_order[int(blockIdx.x) / kParts] : tile0 + int(blockIdx.x) / kParts;
   const int part = int(blockIdx.x) % kParts;   // this CTA's rows: [part * 16 / kParts, (part + 1) * 16 / kParts)
   const int t = threadIdx.x;
   const int lane = t & 31, warp = t >> 5;
@@ -205,7 +205,8 @@ blend_fwd_kernel(const float4* __restrict__ rec, const uint32_t* __restrict__ id
 }
 
 template <bool kTraining>
-int launch(const float4* rec, const uint32_t* ids, const int2* rg, int width, int height, int tiles_x, int tile0,
+int launch(const int32_t* order, const float4* rec, const uint32_t* ids, const int2* rg, int width, int height,
+           int tiles_x, int tile0,
            int64_t ntiles, float3 bg, float* image, float* t_final, int32_t* last, cudaStream_t s) {
   static bool configured = false;
   if (!configured) {
@@ -216,13 +217,15 @@ int launch(const float4* rec, const uint32_t* ids, const int2* rg, int width, in
   }
   if (ntiles <= 0) return GS_OK;
   blend_fwd_kernel<kTraining><<<unsigned(ntiles * kParts), kThreads, kSmemBytes, s>>>(rec, ids, rg, width, height, tiles_x,
-                                                                             tile0, bg, image, t_final, last);
+                                                                             tile0, bg, image, t_final, last,
+                                                                             order);
   return check_launch();
 }
 
 int blend_forward_rows(const gs_splats_t* splats, const uint32_t* sorted_ids, const int32_t* ranges, int32_t width,
                        int32_t height, int32_t row_begin, int32_t row_end, const float background[3],
-                       int32_t training, float* image, float* t_final, int32_t* last, void* stream) {
+                       int32_t training, float* image, float* t_final, int32_t* last, void* stream,
+                       const int32_t* tile_order = nullptr) {
   if (!splats || !ranges || !image || !background || width <= 0 || height <= 0) return GS_ERR_INVALID_ARG;
   if (training && (!t_final || !last)) return GS_ERR_INVALID_ARG;
   const int tiles_x = (width + kTile - 1) / kTile, tiles_y = (height + kTile - 1) / kTile;
@@ -236,8 +239,8 @@ int blend_forward_rows(const gs_splats_t* splats, const uint32_t* sorted_ids, co
   const int tile0 = row_begin * tiles_x;
   const int64_t ntiles = int64_t(row_end - row_begin) * tiles_x;
   if (training)
-    return launch<true>(rec, sorted_ids, rg, width, height, tiles_x, tile0, ntiles, bg, image, t_final, last, s);
-  return launch<false>(rec, sorted_ids, rg, width, height, tiles_x, tile0, ntiles, bg, image, nullptr, nullptr, s);
+    return launch<true>(tile_order, rec, sorted_ids, rg, width, height, tiles_x, tile0, ntiles, bg, image, t_final, last, s);
+  return launch<false>(tile_order, rec, sorted_ids, rg, width, height, tiles_x, tile0, ntiles, bg, image, nullptr, nullptr, s);
 }
 
 }  // namespace
@@ -257,4 +260,15 @@ extern "C" int gs_blend_forward_rows(const gs_splats_t* splats, const uint32_t* 
                                      int32_t* last, void* stream) {
   return gs::blend_forward_rows(splats, sorted_ids, ranges, width, height, tile_row_begin, tile_row_end, background,
                                 training, image, t_final, last, stream);
+}
+
+// The full frame with the tiles visited in `tile_order` (a permutation of
+// [0, tiles), device int32).
+extern "C" int gs_blend_forward_ordered(const gs_splats_t* splats, const uint32_t* sorted_ids, const int32_t* ranges,
+                                        int32_t width, int32_t height, const float background[3], int32_t training,
+                                        const int32_t* tile_order, float* image, float* t_final, int32_t* last,
+                                        void* stream) {
+  if (!tile_order || height <= 0) return GS_ERR_INVALID_ARG;
+  return gs::blend_forward_rows(splats, sorted_ids, ranges, width, height, 0, (height + gs::kTile - 1) / gs::kTile,
+                                background, training, image, t_final, last, stream, tile_order);
 }

@@ -214,6 +214,9 @@ class SplatGrads2D:
     """Screen-space gradients (rasterizer.py:243-250) in the packed (N,12) row."""
 
     packed: torch.Tensor  # (N,12) float32
+    # the longest-first tile schedule the backward ran on (int32 (T,)), a good
+    # launch order for the next forward of the same view (render_forward)
+    tile_order: torch.Tensor | None = None
 
     @property
     def d_mean2d(self) -> torch.Tensor:
@@ -406,17 +409,28 @@ def _bg(background) -> ctypes.Array:
 
 
 def render_forward(splats: DeviceSplats, binning: TileBinning, width: int, height: int, background,
-                   training: bool = False) -> RenderOutput:
-    """K6: per-tile front-to-back blend (rasterizer.py:201)."""
+                   training: bool = False, tile_order: torch.Tensor | None = None) -> RenderOutput:
+    """K6: per-tile front-to-back blend (rasterizer.py:201).
+
+    tile_order: optional launch order of the tiles (a permutation of
+    [0, tiles), e.g. SplatGrads2D.tile_order from the previous backward of the
+    same view: heavy tiles first).  The result does not depend on it."""
     lib = _lib.load()
     device = splats.rec.device
     image = torch.empty((height, width, 3), dtype=torch.float32, device=device)
     t_final = torch.empty((height, width), dtype=torch.float32, device=device) if training else None
     last = torch.empty((height, width), dtype=torch.int32, device=device) if training else None
     cs = splats.c_struct()
-    _lib.check(lib.gs_blend_forward(ctypes.byref(cs), binning.splat_ids.data_ptr(), binning.ranges.data_ptr(),
-                                    width, height, _bg(background), int(bool(training)), image.data_ptr(),
-                                    _lib.ptr(t_final), _lib.ptr(last), _stream()), "render_forward")
+    tx, ty = tile_extent(width, height)
+    if tile_order is not None and tile_order.numel() == tx * ty and tile_order.device == device:
+        _lib.check(lib.gs_blend_forward_ordered(ctypes.byref(cs), binning.splat_ids.data_ptr(),
+                                                binning.ranges.data_ptr(), width, height, _bg(background),
+                                                int(bool(training)), tile_order.data_ptr(), image.data_ptr(),
+                                                _lib.ptr(t_final), _lib.ptr(last), _stream()), "render_forward")
+    else:
+        _lib.check(lib.gs_blend_forward(ctypes.byref(cs), binning.splat_ids.data_ptr(), binning.ranges.data_ptr(),
+                                        width, height, _bg(background), int(bool(training)), image.data_ptr(),
+                                        _lib.ptr(t_final), _lib.ptr(last), _stream()), "render_forward")
     return RenderOutput(image, t_final, last)
 
 
@@ -439,6 +453,7 @@ def render_backward(d_image: torch.Tensor, output: RenderOutput, splats: DeviceS
             d_image.data_ptr(), ctypes.byref(cs), binning.splat_ids.data_ptr(), binning.ranges.data_ptr(),
             output.final_transmittance.data_ptr(), output.last_contributor.data_ptr(), width, height,
             _bg(background), scratch.data_ptr(), packed.data_ptr(), _stream()), "render_backward")
+        return SplatGrads2D(packed, scratch[:tx * ty])
     else:
         _lib.check(lib.gs_blend_backward(d_image.data_ptr(), ctypes.byref(cs), binning.splat_ids.data_ptr(),
                                          binning.ranges.data_ptr(), output.final_transmittance.data_ptr(),
@@ -492,14 +507,16 @@ def render_view(cloud: GaussianCloud, camera, background, active_sh_degree: int 
 
 
 def render_view_async(cloud: GaussianCloud, camera, background, active_sh_degree: int = 3, training: bool = False,
-                      capacity: int | None = None):
+                      capacity: int | None = None, tile_order: torch.Tensor | None = None):
     """render_view with the sync-free binning: no host synchronisation, so
     the whole forward can be captured in a CUDA graph.  Errors (zero
-    quaternion, capacity overflow) surface through binning.check()."""
+    quaternion, capacity overflow) surface through binning.check().
+    tile_order: see render_forward."""
     camera = _camera(camera)
     splats = _project_tensors(cloud.c_params(), len(cloud), cloud.device, camera, active_sh_degree)
     binning = bin_and_sort_async(splats, camera.width, camera.height, capacity)
-    out = render_forward(splats, binning, camera.width, camera.height, background, training=training)
+    out = render_forward(splats, binning, camera.width, camera.height, background, training=training,
+                         tile_order=tile_order)
     return out, splats, binning
 
 

@@ -224,8 +224,11 @@ def _sample_view(state: TrainState, views: Sequence[TrainView], config: TrainCon
 
 
 def _enqueue_forward(state: TrainState, fw: _Forward, config: TrainConfig) -> _Forward:
+    # the view's last backward schedule (heavy tiles first) orders this forward's tiles
+    orders = getattr(state, "_tile_orders", None)
+    order = orders.get((fw.view_idx, fw.camera.width, fw.camera.height)) if orders else None
     fw.out, fw.splats, fw.binning = R.render_view_async(state.cloud, fw.camera, config.background, fw.degree,
-                                                        training=True)
+                                                        training=True, tile_order=order)
     fw.loss, fw.d_image = l1_dssim_loss(fw.out.image, fw.gt, config.lambda_dssim)
     if fw.consumed is not None:
         fw.consumed.record()
@@ -276,6 +279,10 @@ def train_step(state: TrainState, views: Sequence[TrainView], config: TrainConfi
         skip = step_guard(fw.loss, fw.binning.k_info, host.skip_device(device))
         g2 = R.render_backward(fw.d_image, fw.out, fw.splats, fw.binning, fw.camera.width, fw.camera.height,
                                config.background)
+        if g2.tile_order is not None:
+            if not hasattr(state, "_tile_orders"):
+                state._tile_orders = {}
+            state._tile_orders[(fw.view_idx, fw.camera.width, fw.camera.height)] = g2.tile_order
         state.adam.backward_step(state.cloud, fw.camera, fw.splats, g2, fw.degree, it, config, stats=state.stats,
                                  skip=skip)
         done = host.stage(fw.loss, fw.binning.k_info)
