@@ -103,16 +103,22 @@ def train_step_views(cloud, cameras, targets, adam, config, iteration: int, buck
                 st.accum_count.zero_()
                 st.max_radius_frac.zero_()
     totals, k_infos = [], []
+    # per view: the previous batch's longest-first backward schedule orders this forward's tiles
+    orders = bucket.__dict__.setdefault("_tile_orders", {})
     for i, (cam, gt) in enumerate(zip(cameras, targets)):
         s, b, st = lanes[i % len(lanes)]
+        key = (i, cam.width, cam.height)
         with torch.cuda.stream(s):
             if streams > 1:
-                out, splats, binning = R.render_view_async(cloud, cam, background, active_sh_degree, training=True)
+                out, splats, binning = R.render_view_async(cloud, cam, background, active_sh_degree, training=True,
+                                                           tile_order=orders.get(key))
                 k_infos.append(binning.k_info)
             else:
                 out, splats, binning = R.render_view(cloud, cam, background, active_sh_degree, training=True)
             loss, d_image = l1_dssim_loss(out.image, gt, config.lambda_dssim)
             g2 = R.render_backward(d_image, out, splats, binning, cam.width, cam.height, background)
+            if g2.tile_order is not None:
+                orders[key] = g2.tile_order
             R.backward_project(cloud, cam, splats, g2, active_sh_degree, stats=st, out=b.grads, accumulate=True)
             totals.append(loss[0:1])
     for s, b, st in lanes[1:]:
