@@ -270,15 +270,18 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
     # sync-free render_view_async (K stays on the device; every frame's
     # capacity flags are checked after the loop), and the reference-shaped
     # render_view (one host read of K per frame) for comparison
+    # (a TileSchedule carries each frame's per-tile work to the next frame's
+    # launch order, heaviest tiles first)
     fps_steps = max(args.steps, 10)
+    sched = R.TileSchedule()
     for _ in range(3):
-        R.render_view_async(cloud, cam, bg, DEGREE)[2].check()
+        R.render_view_async(cloud, cam, bg, DEGREE, schedule=sched)[2].check()
     torch.cuda.synchronize()
     f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     kinfos = []
     f0.record()
     for _ in range(fps_steps):
-        kinfos.append(R.render_view_async(cloud, cam, bg, DEGREE)[2].k_info)
+        kinfos.append(R.render_view_async(cloud, cam, bg, DEGREE, schedule=sched)[2].k_info)
     f1.record()
     torch.cuda.synchronize()
     check_binned(kinfos)

@@ -229,12 +229,20 @@ int gs_blend_forward(const gs_splats_t* splats, const uint32_t* sorted_ids, cons
                      int32_t width, int32_t height, const float background[3], int32_t training,
                      float* image, float* t_final, int32_t* last, void* stream);
 
-/* gs_blend_forward with the tiles launched in `tile_order` (a permutation of
- * [0, tiles), device int32; e.g. the previous backward's longest-first
- * schedule of the same view).  The outputs do not depend on the order. */
+/* gs_blend_forward with the tiles launched in `tile_order` (nullable; a
+ * permutation of [0, tiles), device int32, e.g. the previous backward's
+ * longest-first schedule of the same view, or gs_tile_schedule of the
+ * previous frame's tile_work).  tile_work (nullable, device int32[tiles])
+ * receives each tile's work (splats handed to the blend before it stopped).
+ * The outputs do not depend on the order. */
 int gs_blend_forward_ordered(const gs_splats_t* splats, const uint32_t* sorted_ids, const int32_t* ranges,
                              int32_t width, int32_t height, const float background[3], int32_t training,
-                             const int32_t* tile_order, float* image, float* t_final, int32_t* last, void* stream);
+                             const int32_t* tile_order, int32_t* tile_work, float* image, float* t_final,
+                             int32_t* last, void* stream);
+
+/* Longest-first tile order from a per-tile work estimate (quarter-octave
+ * buckets, heaviest first).  scratch: device int32[tiles + 128]. */
+int gs_tile_schedule(const int32_t* work, int32_t tiles, int32_t* scratch, int32_t* order, void* stream);
 /* The tiles of rows [tile_row_begin, tile_row_end) only (sorted_ids: that
  * band's instance list from gs_bin_rows_async). */
 int gs_blend_forward_rows(const gs_splats_t* splats, const uint32_t* sorted_ids, const int32_t* ranges,

@@ -118,7 +118,8 @@ SIGNATURES = [
     ("gs_blend_backward_ordered", c_int32, [c_void_p, POINTER(GsSplats), c_void_p, c_void_p, c_void_p, c_void_p,
                                             c_int32, c_int32, POINTER(c_float), c_void_p, c_void_p, c_void_p]),
     ("gs_blend_forward_ordered", c_int32, [POINTER(GsSplats), c_void_p, c_void_p, c_int32, c_int32, POINTER(c_float),
-                                           c_int32, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
+                                           c_int32, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
+    ("gs_tile_schedule", c_int32, [c_void_p, c_int32, c_void_p, c_void_p, c_void_p]),
     ("gs_blend_backward_scheduled", c_int32, [c_void_p, POINTER(GsSplats), c_void_p, c_void_p, c_void_p, c_void_p,
                                               c_int32, c_int32, POINTER(c_float), c_void_p, c_void_p, c_void_p]),
     ("gs_densify_workspace_size", c_int32, [c_int64, POINTER(c_size_t)]),

@@ -366,7 +366,7 @@ __device__ __forceinline__ int need_bucket(int need) {
   return need <= 0 ? 0 : min(kSchedBuckets - 1, 1 + int(__log2f(float(need)) * 4.0f));
 }
 
-// one warp per tile: max of `last` over the tile's pixels
+// one warp per tile: max of `last` over the tile's pixels -> the tile's work
 __global__ void tile_need_kernel(const int32_t* __restrict__ last, const int2* __restrict__ ranges, int width,
                                  int height, int tiles_x, int tiles, int32_t* __restrict__ bucket_of,
                                  int32_t* __restrict__ hist) {
@@ -388,6 +388,16 @@ __global__ void tile_need_kernel(const int32_t* __restrict__ last, const int2* _
     bucket_of[tile] = b;
     atomicAdd(&hist[b], 1);
   }
+}
+
+// bucket of a given per-tile work (gs_tile_schedule)
+__global__ void tile_bucket_kernel(const int32_t* __restrict__ work, int tiles, int32_t* __restrict__ bucket_of,
+                                   int32_t* __restrict__ hist) {
+  const int t = int(int64_t(blockIdx.x) * blockDim.x + threadIdx.x);
+  if (t >= tiles) return;
+  const int b = need_bucket(work[t]);
+  bucket_of[t] = b;
+  atomicAdd(&hist[b], 1);
 }
 
 // exclusive scan over the buckets from the heaviest down (one warp)
@@ -441,4 +451,23 @@ extern "C" int gs_blend_backward_scheduled(const float* d_image, const gs_splats
   if (st != GS_OK) return st;
   return gs_blend_backward_ordered(d_image, splats, sorted_ids, ranges, t_final, last, width, height, background,
                                    order, grads2d, stream);
+}
+
+// Longest-first order of `tiles` tiles from any per-tile work estimate
+// (e.g. the forward's gs_blend_forward_ordered tile_work of the previous frame).
+// scratch: device int32[tiles + 128]; order: device int32[tiles].
+extern "C" int gs_tile_schedule(const int32_t* work, int32_t tiles, int32_t* scratch, int32_t* order, void* stream) {
+  using namespace gs;
+  if (!work || !scratch || !order || tiles < 0) return GS_ERR_INVALID_ARG;
+  if (tiles == 0) return GS_OK;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  int32_t* bucket_of = scratch;
+  int32_t* hist = scratch + tiles;
+  int32_t* cursor = hist + kSchedBuckets;
+  cudaError_t e = cudaMemsetAsync(hist, 0, kSchedBuckets * sizeof(int32_t), s);
+  if (e != cudaSuccess) return record_cuda_error(e);
+  tile_bucket_kernel<<<unsigned((tiles + 255) / 256), 256, 0, s>>>(work, tiles, bucket_of, hist);
+  tile_sched_scan_kernel<<<1, 32, 0, s>>>(hist, cursor);
+  tile_sched_scatter_kernel<<<unsigned((tiles + 255) / 256), 256, 0, s>>>(bucket_of, cursor, tiles, order);
+  return check_launch();
 }

@@ -90,7 +90,8 @@ template <bool kTraining>
 __global__ void __launch_bounds__(kThreads)
 blend_fwd_kernel(const float4* __restrict__ rec, const uint32_t* __restrict__ ids, const int2* __restrict__ ranges,
                  int width, int height, int tiles_x, int tile0, float3 bg, float* __restrict__ image,
-                 float* __restrict__ t_final, int32_t* __restrict__ last, const int32_t* __restrict__ tile_order) {
+                 float* __restrict__ t_final, int32_t* __restrict__ last, const int32_t* __restrict__ tile_order,
+                 int32_t* __restrict__ tile_work) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   FwdStage* stages = reinterpret_cast<FwdStage*>(smem_raw);
   RawRec* raw = reinterpret_cast<RawRec*>(smem_raw + sizeof(FwdStage) * kStages);
@@ -117,18 +118,25 @@ blend_fwd_kernel(const float4* __restrict__ rec, const uint32_t* __restrict__ id
   __syncthreads();
 
   if (warp == kConsumerWarps) {  // ---------------- producer warp
-    for (int b = 0; b < nb; ++b) {
+    int b = 0;
+    for (; b < nb; ++b) {
       const int s = b % kStages;
+      bool stop = false;
       if (b >= kStages) {
         while (!mbar_try_wait(&empty_bar[s], uint32_t((b / kStages) - 1) & 1u))
-          if (ld_volatile(&s_stop)) return;
+          if (ld_volatile(&s_stop)) {
+            stop = true;
+            break;
+          }
       }
-      if (ld_volatile(&s_stop)) return;
+      if (stop || ld_volatile(&s_stop)) break;
       const int base = range.x + b * kBatch;
       produce_batch(stages[s], *raw, rec, ids, base, min(kBatch, range.y - base), lane, tile_x0, tile_y0,
                     part * kConsumerWarps);
       mbar_arrive(&full_bar[s]);
     }
+    // the tile's work (splats handed to the consumers) for the next frame's schedule
+    if (tile_work && lane == 0) tile_work[tile] = b * kBatch;
     return;
   }
 
@@ -205,7 +213,7 @@ blend_fwd_kernel(const float4* __restrict__ rec, const uint32_t* __restrict__ id
 }
 
 template <bool kTraining>
-int launch(const int32_t* order, const float4* rec, const uint32_t* ids, const int2* rg, int width, int height,
+int launch(const int32_t* order, int32_t* work, const float4* rec, const uint32_t* ids, const int2* rg, int width, int height,
            int tiles_x, int tile0,
            int64_t ntiles, float3 bg, float* image, float* t_final, int32_t* last, cudaStream_t s) {
   static bool configured = false;
@@ -218,14 +226,14 @@ int launch(const int32_t* order, const float4* rec, const uint32_t* ids, const i
   if (ntiles <= 0) return GS_OK;
   blend_fwd_kernel<kTraining><<<unsigned(ntiles * kParts), kThreads, kSmemBytes, s>>>(rec, ids, rg, width, height, tiles_x,
                                                                              tile0, bg, image, t_final, last,
-                                                                             order);
+                                                                             order, work);
   return check_launch();
 }
 
 int blend_forward_rows(const gs_splats_t* splats, const uint32_t* sorted_ids, const int32_t* ranges, int32_t width,
                        int32_t height, int32_t row_begin, int32_t row_end, const float background[3],
                        int32_t training, float* image, float* t_final, int32_t* last, void* stream,
-                       const int32_t* tile_order = nullptr) {
+                       const int32_t* tile_order = nullptr, int32_t* tile_work = nullptr) {
   if (!splats || !ranges || !image || !background || width <= 0 || height <= 0) return GS_ERR_INVALID_ARG;
   if (training && (!t_final || !last)) return GS_ERR_INVALID_ARG;
   const int tiles_x = (width + kTile - 1) / kTile, tiles_y = (height + kTile - 1) / kTile;
@@ -239,8 +247,8 @@ int blend_forward_rows(const gs_splats_t* splats, const uint32_t* sorted_ids, co
   const int tile0 = row_begin * tiles_x;
   const int64_t ntiles = int64_t(row_end - row_begin) * tiles_x;
   if (training)
-    return launch<true>(tile_order, rec, sorted_ids, rg, width, height, tiles_x, tile0, ntiles, bg, image, t_final, last, s);
-  return launch<false>(tile_order, rec, sorted_ids, rg, width, height, tiles_x, tile0, ntiles, bg, image, nullptr, nullptr, s);
+    return launch<true>(tile_order, tile_work, rec, sorted_ids, rg, width, height, tiles_x, tile0, ntiles, bg, image, t_final, last, s);
+  return launch<false>(tile_order, tile_work, rec, sorted_ids, rg, width, height, tiles_x, tile0, ntiles, bg, image, nullptr, nullptr, s);
 }
 
 }  // namespace
@@ -266,9 +274,9 @@ extern "C" int gs_blend_forward_rows(const gs_splats_t* splats, const uint32_t* 
 // [0, tiles), device int32).
 extern "C" int gs_blend_forward_ordered(const gs_splats_t* splats, const uint32_t* sorted_ids, const int32_t* ranges,
                                         int32_t width, int32_t height, const float background[3], int32_t training,
-                                        const int32_t* tile_order, float* image, float* t_final, int32_t* last,
-                                        void* stream) {
-  if (!tile_order || height <= 0) return GS_ERR_INVALID_ARG;
+                                        const int32_t* tile_order, int32_t* tile_work, float* image, float* t_final,
+                                        int32_t* last, void* stream) {
+  if (height <= 0) return GS_ERR_INVALID_ARG;
   return gs::blend_forward_rows(splats, sorted_ids, ranges, width, height, 0, (height + gs::kTile - 1) / gs::kTile,
-                                background, training, image, t_final, last, stream, tile_order);
+                                background, training, image, t_final, last, stream, tile_order, tile_work);
 }

@@ -409,12 +409,15 @@ def _bg(background) -> ctypes.Array:
 
 
 def render_forward(splats: DeviceSplats, binning: TileBinning, width: int, height: int, background,
-                   training: bool = False, tile_order: torch.Tensor | None = None) -> RenderOutput:
+                   training: bool = False, tile_order: torch.Tensor | None = None,
+                   tile_work: torch.Tensor | None = None) -> RenderOutput:
     """K6: per-tile front-to-back blend (rasterizer.py:201).
 
     tile_order: optional launch order of the tiles (a permutation of
     [0, tiles), e.g. SplatGrads2D.tile_order from the previous backward of the
-    same view: heavy tiles first).  The result does not depend on it."""
+    same view: heavy tiles first).  tile_work: optional int32 (tiles,) that
+    receives each tile's work (see TileSchedule).  The result does not depend
+    on either."""
     lib = _lib.load()
     device = splats.rec.device
     image = torch.empty((height, width, 3), dtype=torch.float32, device=device)
@@ -422,11 +425,16 @@ def render_forward(splats: DeviceSplats, binning: TileBinning, width: int, heigh
     last = torch.empty((height, width), dtype=torch.int32, device=device) if training else None
     cs = splats.c_struct()
     tx, ty = tile_extent(width, height)
-    if tile_order is not None and tile_order.numel() == tx * ty and tile_order.device == device:
+    if tile_order is not None and (tile_order.numel() != tx * ty or tile_order.device != device):
+        tile_order = None
+    if tile_work is not None and (tile_work.numel() != tx * ty or tile_work.device != device):
+        raise ValueError("tile_work must be a (tiles,) int32 tensor on the splats' device")
+    if tile_order is not None or tile_work is not None:
         _lib.check(lib.gs_blend_forward_ordered(ctypes.byref(cs), binning.splat_ids.data_ptr(),
                                                 binning.ranges.data_ptr(), width, height, _bg(background),
-                                                int(bool(training)), tile_order.data_ptr(), image.data_ptr(),
-                                                _lib.ptr(t_final), _lib.ptr(last), _stream()), "render_forward")
+                                                int(bool(training)), _lib.ptr(tile_order), _lib.ptr(tile_work),
+                                                image.data_ptr(), _lib.ptr(t_final), _lib.ptr(last), _stream()),
+                   "render_forward")
     else:
         _lib.check(lib.gs_blend_forward(ctypes.byref(cs), binning.splat_ids.data_ptr(), binning.ranges.data_ptr(),
                                         width, height, _bg(background), int(bool(training)), image.data_ptr(),
@@ -507,17 +515,55 @@ def render_view(cloud: GaussianCloud, camera, background, active_sh_degree: int 
 
 
 def render_view_async(cloud: GaussianCloud, camera, background, active_sh_degree: int = 3, training: bool = False,
-                      capacity: int | None = None, tile_order: torch.Tensor | None = None):
+                      capacity: int | None = None, tile_order: torch.Tensor | None = None,
+                      schedule: "TileSchedule | None" = None):
     """render_view with the sync-free binning: no host synchronisation, so
     the whole forward can be captured in a CUDA graph.  Errors (zero
     quaternion, capacity overflow) surface through binning.check().
-    tile_order: see render_forward."""
+    tile_order: see render_forward.  schedule: a TileSchedule for repeated
+    renders of one view (its order, when present, overrides tile_order)."""
     camera = _camera(camera)
     splats = _project_tensors(cloud.c_params(), len(cloud), cloud.device, camera, active_sh_degree)
     binning = bin_and_sort_async(splats, camera.width, camera.height, capacity)
+    work = None
+    if schedule is not None:
+        order, work = schedule.prepare(camera.width, camera.height, cloud.device)
+        tile_order = order if order is not None else tile_order
     out = render_forward(splats, binning, camera.width, camera.height, background, training=training,
-                         tile_order=tile_order)
+                         tile_order=tile_order, tile_work=work)
+    if schedule is not None:
+        schedule.update()
     return out, splats, binning
+
+
+class TileSchedule:
+    """Launch schedule for repeated renders of one view (a viewer, a render
+    benchmark): every forward records each tile's work (splats handed to the
+    blend before the tile saturated) and the next frame launches the heaviest
+    tiles first (gs_tile_schedule), so light tiles fill the last wave.  The
+    images do not depend on it."""
+
+    def __init__(self):
+        self.key = None
+        self.order = self.work = self.scratch = None
+        self.ready = False
+
+    def prepare(self, width: int, height: int, device):
+        tx, ty = tile_extent(width, height)
+        key = (tx * ty, str(device))
+        if key != self.key:
+            z = dict(dtype=torch.int32, device=device)
+            self.order, self.work = torch.empty(tx * ty, **z), torch.empty(tx * ty, **z)
+            self.scratch = torch.empty(tx * ty + 128, **z)
+            self.key, self.ready = key, False
+        return (self.order if self.ready else None), self.work
+
+    def update(self) -> None:
+        """Rebuild the order from the work just recorded (stream-ordered after
+        the forward that read the previous order)."""
+        _lib.check(_lib.load().gs_tile_schedule(self.work.data_ptr(), self.work.numel(), self.scratch.data_ptr(),
+                                                self.order.data_ptr(), _stream()), "tile_schedule")
+        self.ready = True
 
 
 # ---------------------------------------------------------------------------

@@ -424,3 +424,20 @@ def test_tile_orders_do_not_change_results(cuda_device):
     diff = torch.linalg.norm((g2.packed - plain).double(), dim=0)
     ref = torch.linalg.norm(plain.double(), dim=0)
     assert bool((diff <= 1e-5 * ref + 1e-30).all()), (diff / ref.clamp_min(1e-30)).tolist()
+
+
+def test_tile_schedule_repeated_renders(cuda_device):
+    """TileSchedule: the forward records per-tile work and the next frame
+    launches heaviest-first; every frame's image equals the plain render."""
+    from paper_2308_04079_b200 import synthetic
+    cloud_np, cam = synthetic.frustum_scene(30_000, 320, 200, seed=52)
+    cloud = GaussianCloud.from_numpy(**cloud_np)
+    ref = R.render_view(cloud, cam, (0, 0, 0), 3)[0].image
+    sched = R.TileSchedule()
+    for _ in range(3):
+        out, _, binning = R.render_view_async(cloud, cam, (0, 0, 0), 3, schedule=sched)
+        binning.check()
+        assert torch.equal(out.image, ref)
+    tx, ty = R.tile_extent(cam.width, cam.height)
+    assert torch.equal(torch.sort(sched.order.long()).values, torch.arange(tx * ty, device="cuda"))
+    assert int(sched.work.min()) >= 0 and int(sched.work.max()) > 0

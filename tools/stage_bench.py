@@ -93,8 +93,8 @@ def main() -> None:
             ls = torch.empty_like(out.last_contributor)
             def runf():
                 lib.gs_blend_forward_ordered(ctypes.byref(cs), binning.splat_ids.data_ptr(), binning.ranges.data_ptr(),
-                                             1920, 1080, bgc, 1, order.data_ptr(), img.data_ptr(), tf.data_ptr(),
-                                             ls.data_ptr(), torch.cuda.current_stream().cuda_stream)
+                                             1920, 1080, bgc, 1, order.data_ptr(), None, img.data_ptr(),
+                                             tf.data_ptr(), ls.data_ptr(), torch.cuda.current_stream().cuda_stream)
             res[f"blend_fwd_order_{name}_ms"] = timeit(runf)
             res[f"fwd_order_{name}_same"] = bool(torch.equal(img, out.image) and torch.equal(ls, out.last_contributor))
     if "--bands" in sys.argv:
