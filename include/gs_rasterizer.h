@@ -240,8 +240,8 @@ int gs_blend_forward_ordered(const gs_splats_t* splats, const uint32_t* sorted_i
                              const int32_t* tile_order, int32_t* tile_work, float* image, float* t_final,
                              int32_t* last, void* stream);
 
-/* Longest-first tile order from a per-tile work estimate (quarter-octave
- * buckets, heaviest first).  scratch: device int32[tiles + 128]. */
+/* Longest-first tile order from a per-tile work estimate (1/64-octave
+ * buckets, heaviest first).  scratch: device int32[tiles + 2048]. */
 int gs_tile_schedule(const int32_t* work, int32_t tiles, int32_t* scratch, int32_t* order, void* stream);
 /* The tiles of rows [tile_row_begin, tile_row_end) only (sorted_ids: that
  * band's instance list from gs_bin_rows_async). */
@@ -271,7 +271,7 @@ int gs_blend_backward_ordered(const float* d_image, const gs_splats_t* splats, c
 /* gs_blend_backward on a longest-first tile schedule built on the device from
  * the training record: a tile's work is max(last contributor) - start + 1
  * (gradients.py:48-52); heavy tiles start first so light ones fill the last
- * wave.  scratch: caller-owned device int32[2 * tiles + 128]. */
+ * wave.  scratch: caller-owned device int32[2 * tiles + 2048]. */
 int gs_blend_backward_scheduled(const float* d_image, const gs_splats_t* splats, const uint32_t* sorted_ids,
                                 const int32_t* ranges, const float* t_final, const int32_t* last, int32_t width,
                                 int32_t height, const float background[3], int32_t* scratch, float* grads2d,

@@ -355,15 +355,15 @@ extern "C" int gs_blend_backward_ordered(const float* d_image, const gs_splats_t
 // Longest-first tile schedule for the backward: a tile's work is its number
 // of back-to-front splats, need = max(last contributor) - start + 1
 // (gradients.py:48-52), known from the forward's training record.  Tiles are
-// bucketed by need on a quarter-octave scale and visited from the heaviest
+// bucketed by need on a 1/64-octave scale and visited from the heaviest
 // bucket down, so the light tiles fill the last wave instead of a few heavy
-// ones trailing it (measured 1.216 -> 1.13 ms at c3).  Scratch: 2 T + 128 ints.
+// ones trailing it.  Scratch: 2 T + 2048 ints.
 namespace gs {
 namespace {
-constexpr int kSchedBuckets = 64;
+constexpr int kSchedBuckets = 1024;   // 1/64-octave buckets: close to an exact descending sort
 
 __device__ __forceinline__ int need_bucket(int need) {
-  return need <= 0 ? 0 : min(kSchedBuckets - 1, 1 + int(__log2f(float(need)) * 4.0f));
+  return need <= 0 ? 0 : min(kSchedBuckets - 1, 1 + int(__log2f(float(need)) * 64.0f));
 }
 
 // one warp per tile: max of `last` over the tile's pixels -> the tile's work
@@ -400,21 +400,33 @@ __global__ void tile_bucket_kernel(const int32_t* __restrict__ work, int tiles, 
   atomicAdd(&hist[b], 1);
 }
 
-// exclusive scan over the buckets from the heaviest down (one warp)
-__global__ void tile_sched_scan_kernel(const int32_t* __restrict__ hist, int32_t* __restrict__ cursor) {
-  const int lane = threadIdx.x;
-  // lane l owns buckets 63 - 2l and 62 - 2l (descending order)
-  const int b0 = kSchedBuckets - 1 - 2 * lane, b1 = b0 - 1;
-  const int c0 = hist[b0], c1 = hist[b1];
-  int incl = c0 + c1;
+// exclusive scan over the buckets from the heaviest down (one block of
+// kSchedBuckets threads; thread i owns bucket kSchedBuckets - 1 - i)
+__global__ void __launch_bounds__(kSchedBuckets) tile_sched_scan_kernel(const int32_t* __restrict__ hist,
+                                                                        int32_t* __restrict__ cursor) {
+  __shared__ int warp_tot[kSchedBuckets / 32];
+  const int i = threadIdx.x, lane = i & 31, w = i >> 5;
+  const int b = kSchedBuckets - 1 - i;
+  const int c = hist[b];
+  int incl = c;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
     const int v = __shfl_up_sync(0xffffffffu, incl, o);
     if (lane >= o) incl += v;
   }
-  const int excl = incl - (c0 + c1);
-  cursor[b0] = excl;
-  cursor[b1] = excl + c0;
+  if (lane == 31) warp_tot[w] = incl;
+  __syncthreads();
+  if (w == 0) {
+    int t = lane < kSchedBuckets / 32 ? warp_tot[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, t, o);
+      if (lane >= o) t += v;
+    }
+    if (lane < kSchedBuckets / 32) warp_tot[lane] = t;   // inclusive over warps
+  }
+  __syncthreads();
+  cursor[b] = incl - c + (w > 0 ? warp_tot[w - 1] : 0);
 }
 
 __global__ void tile_sched_scatter_kernel(const int32_t* __restrict__ bucket_of, int32_t* __restrict__ cursor,
@@ -445,7 +457,7 @@ extern "C" int gs_blend_backward_scheduled(const float* d_image, const gs_splats
   if (e != cudaSuccess) return record_cuda_error(e);
   tile_need_kernel<<<unsigned((int64_t(tiles) * 32 + 255) / 256), 256, 0, s>>>(
       last, reinterpret_cast<const int2*>(ranges), width, height, tiles_x, tiles, bucket_of, hist);
-  tile_sched_scan_kernel<<<1, 32, 0, s>>>(hist, cursor);
+  tile_sched_scan_kernel<<<1, kSchedBuckets, 0, s>>>(hist, cursor);
   tile_sched_scatter_kernel<<<unsigned((tiles + 255) / 256), 256, 0, s>>>(bucket_of, cursor, tiles, order);
   int st = check_launch();
   if (st != GS_OK) return st;
@@ -455,7 +467,7 @@ extern "C" int gs_blend_backward_scheduled(const float* d_image, const gs_splats
 
 // Longest-first order of `tiles` tiles from any per-tile work estimate
 // (e.g. the forward's gs_blend_forward_ordered tile_work of the previous frame).
-// scratch: device int32[tiles + 128]; order: device int32[tiles].
+// scratch: device int32[tiles + 2048]; order: device int32[tiles].
 extern "C" int gs_tile_schedule(const int32_t* work, int32_t tiles, int32_t* scratch, int32_t* order, void* stream) {
   using namespace gs;
   if (!work || !scratch || !order || tiles < 0) return GS_ERR_INVALID_ARG;
@@ -467,7 +479,7 @@ extern "C" int gs_tile_schedule(const int32_t* work, int32_t tiles, int32_t* scr
   cudaError_t e = cudaMemsetAsync(hist, 0, kSchedBuckets * sizeof(int32_t), s);
   if (e != cudaSuccess) return record_cuda_error(e);
   tile_bucket_kernel<<<unsigned((tiles + 255) / 256), 256, 0, s>>>(work, tiles, bucket_of, hist);
-  tile_sched_scan_kernel<<<1, 32, 0, s>>>(hist, cursor);
+  tile_sched_scan_kernel<<<1, kSchedBuckets, 0, s>>>(hist, cursor);
   tile_sched_scatter_kernel<<<unsigned((tiles + 255) / 256), 256, 0, s>>>(bucket_of, cursor, tiles, order);
   return check_launch();
 }

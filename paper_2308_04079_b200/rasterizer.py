@@ -454,9 +454,9 @@ def render_backward(d_image: torch.Tensor, output: RenderOutput, splats: DeviceS
     packed = torch.empty((len(splats), _lib.GRAD2D_FLOATS), dtype=torch.float32, device=splats.rec.device)
     cs = splats.c_struct()
     if _BWD_SCHEDULE:
-        # longest-first tile order from the forward's training record (scratch: 2 T + 128 int32)
+        # longest-first tile order from the forward's training record (scratch: 2 T + 2048 int32)
         tx, ty = tile_extent(width, height)
-        scratch = torch.empty(2 * tx * ty + 128, dtype=torch.int32, device=splats.rec.device)
+        scratch = torch.empty(2 * tx * ty + 2048, dtype=torch.int32, device=splats.rec.device)
         _lib.check(lib.gs_blend_backward_scheduled(
             d_image.data_ptr(), ctypes.byref(cs), binning.splat_ids.data_ptr(), binning.ranges.data_ptr(),
             output.final_transmittance.data_ptr(), output.last_contributor.data_ptr(), width, height,
@@ -554,7 +554,7 @@ class TileSchedule:
         if key != self.key:
             z = dict(dtype=torch.int32, device=device)
             self.order, self.work = torch.empty(tx * ty, **z), torch.empty(tx * ty, **z)
-            self.scratch = torch.empty(tx * ty + 128, **z)
+            self.scratch = torch.empty(tx * ty + 2048, **z)
             self.key, self.ready = key, False
         return (self.order if self.ready else None), self.work
 

@@ -79,8 +79,27 @@ def main() -> None:
         tl = pad.view(ty, 16, tx, 16).amax(dim=(1, 3)).reshape(-1).to(torch.int64)
         need = torch.where(tl >= rg[:, 0].to(torch.int64), tl - rg[:, 0].to(torch.int64) + 1, torch.zeros_like(tl))
         g2o = torch.zeros((len(splats), 12), device="cuda")
-        for name, key in (("len", lens), ("need", need)):
-            order = torch.argsort(key, descending=True, stable=True).to(torch.int32)
+        # super-tile variants: groups of g x g tiles ordered by their summed need,
+        # the group's tiles launched consecutively (L2 reuse of shared splats)
+        def grouped(g):
+            tyy, txx = -(-ty // g), -(-tx // g)
+            nd = torch.zeros(tyy * g, txx * g, dtype=torch.int64, device="cuda")
+            nd[:ty, :tx] = need.view(ty, tx)
+            gs_ = nd.view(tyy, g, txx, g).sum(dim=(1, 3)).reshape(-1)
+            gorder = torch.argsort(gs_, descending=True, stable=True)
+            gy, gx = gorder // txx, gorder % txx
+            oy = torch.arange(g, device="cuda").view(1, g, 1)
+            ox = torch.arange(g, device="cuda").view(1, 1, g)
+            yy = (gy.view(-1, 1, 1) * g + oy).expand(-1, g, g).reshape(-1)
+            xx = (gx.view(-1, 1, 1) * g + ox).expand(-1, g, g).reshape(-1)
+            ok = (yy < ty) & (xx < tx)
+            return (yy[ok] * tx + xx[ok]).to(torch.int32)
+        variants = [("len", lens), ("need", need)]
+        for name, key in variants + [("need2x2", None), ("need4x4", None)]:
+            if key is None:
+                order = grouped(2 if name == "need2x2" else 4)
+            else:
+                order = torch.argsort(key, descending=True, stable=True).to(torch.int32)
             def run():
                 lib.gs_blend_backward_ordered(d.data_ptr(), ctypes.byref(cs), binning.splat_ids.data_ptr(),
                                               binning.ranges.data_ptr(), out.final_transmittance.data_ptr(),
