@@ -319,8 +319,11 @@ int gs_preprocess_backward_adam_guarded(const gs_params_t* params, const gs_came
                                         const gs_stats_t* stats, const gs_grads_t* grads_out,
                                         const int32_t* skip, void* stream);
 
-/* *skip = (k_info[1] != 0 (binning overflow / limit flags) || loss[0] not finite). */
-int gs_step_guard(const float* loss, const int64_t* k_info, int32_t* skip, void* stream);
+/* *skip = (k_info[1] != 0 (binning overflow / limit flags) || loss[0] not finite).
+ * report (nullable; 8 doubles, device memory or mapped pinned host memory):
+ * [loss[0..3], k_info[0..2], skip] -- the step's one host read, without a
+ * separate copy. */
+int gs_step_guard(const float* loss, const int64_t* k_info, int32_t* skip, double* report, void* stream);
 
 /* ---- K9 fused Adam: replaces optimizer._adam_step (optimizer.py:263-293)
  * over all groups in one launch; bias1 = 1-beta1^t, bias2 = 1-beta2^t. */

@@ -114,7 +114,7 @@ SIGNATURES = [
                                                       POINTER(GsSplats), c_void_p, POINTER(GsAdamGroup), c_double,
                                                       c_double, c_double, c_double, c_double, POINTER(GsStats),
                                                       POINTER(GsGrads), c_void_p, c_void_p]),
-    ("gs_step_guard", c_int32, [c_void_p, c_void_p, c_void_p, c_void_p]),
+    ("gs_step_guard", c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     ("gs_blend_backward_ordered", c_int32, [c_void_p, POINTER(GsSplats), c_void_p, c_void_p, c_void_p, c_void_p,
                                             c_int32, c_int32, POINTER(c_float), c_void_p, c_void_p, c_void_p]),
     ("gs_blend_forward_ordered", c_int32, [POINTER(GsSplats), c_void_p, c_void_p, c_int32, c_int32, POINTER(c_float),

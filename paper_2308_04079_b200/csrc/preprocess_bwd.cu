@@ -555,16 +555,24 @@ extern "C" int gs_preprocess_backward_adam(const gs_params_t* params, const gs_c
 
 namespace gs {
 namespace {
-__global__ void step_guard_kernel(const float* loss, const int64_t* k_info, int32_t* skip) {
+__global__ void step_guard_kernel(const float* loss, const int64_t* k_info, int32_t* skip, double* report) {
   const float v = loss[0];
-  skip[0] = (k_info[1] != 0 || !isfinite(v)) ? 1 : 0;
+  const int32_t sk = (k_info[1] != 0 || !isfinite(v)) ? 1 : 0;
+  skip[0] = sk;
+  if (report) {   // the step's host-visible summary, written straight into (mapped) pinned memory
+    for (int i = 0; i < 4; ++i) report[i] = double(loss[i]);
+    for (int i = 0; i < 3; ++i) report[4 + i] = double(k_info[i]);
+    report[7] = double(sk);
+    __threadfence_system();
+  }
 }
 }  // namespace
 }  // namespace gs
 
-extern "C" int gs_step_guard(const float* loss, const int64_t* k_info, int32_t* skip, void* stream) {
+extern "C" int gs_step_guard(const float* loss, const int64_t* k_info, int32_t* skip, double* report,
+                             void* stream) {
   if (!loss || !k_info || !skip) return GS_ERR_INVALID_ARG;
-  gs::step_guard_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(loss, k_info, skip);
+  gs::step_guard_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(loss, k_info, skip, report);
   return gs::check_launch();
 }
 

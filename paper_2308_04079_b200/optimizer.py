@@ -175,15 +175,20 @@ class DeviceAdam:
             "backward_adam")
 
 
-def step_guard(loss: torch.Tensor, k_info: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+def step_guard(loss: torch.Tensor, k_info: torch.Tensor, out: torch.Tensor | None = None,
+               report: torch.Tensor | None = None) -> torch.Tensor:
     """Device int32 flag: 1 when the step must not update anything (loss not
     finite, or the binning overflowed its capacity), written on the current
-    stream without a host synchronisation (gs_step_guard)."""
+    stream without a host synchronisation (gs_step_guard).  report: optional
+    float64 (8,) pinned host (or device) tensor that receives [loss[0..3],
+    k_info[0..2], skip] from the same kernel."""
     if out is None:
         out = torch.empty(1, dtype=torch.int32, device=loss.device)
     if loss.dtype != torch.float32 or k_info.dtype != torch.int64:
         raise TypeError("step_guard expects float32 loss and int64 k_info")
-    _lib.check(_lib.load().gs_step_guard(loss.data_ptr(), k_info.data_ptr(), out.data_ptr(),
+    if report is not None and (report.dtype != torch.float64 or report.numel() < 8):
+        raise TypeError("report must be a float64 tensor of 8 elements")
+    _lib.check(_lib.load().gs_step_guard(loss.data_ptr(), k_info.data_ptr(), out.data_ptr(), _lib.ptr(report),
                                          torch.cuda.current_stream(loss.device).cuda_stream), "step_guard")
     return out
 

@@ -38,6 +38,8 @@ class _HostScalars:
     def __init__(self):
         self.loss = torch.empty(4, dtype=torch.float32).pin_memory()
         self.k_info = torch.empty(3, dtype=torch.int64).pin_memory()
+        # written by the step-guard kernel itself (mapped pinned memory, no copy)
+        self.report = torch.zeros(8, dtype=torch.float64).pin_memory()
 
     def skip_device(self, device) -> torch.Tensor:
         flag = getattr(self, "_skip", None)
@@ -59,6 +61,10 @@ class _HostScalars:
 
     def values(self):
         return self.loss.tolist(), self.k_info.tolist()
+
+    def report_values(self):
+        r = self.report.tolist()
+        return r[0:4], [int(v) for v in r[4:7]]
 
 
 _host_scalars: dict = {}
@@ -276,7 +282,11 @@ def train_step(state: TrainState, views: Sequence[TrainView], config: TrainConfi
     host = _host_scalars.setdefault(str(device), _HostScalars())
     nxt = None
     for attempt in range(3):
-        skip = step_guard(fw.loss, fw.binning.k_info, host.skip_device(device))
+        skip = step_guard(fw.loss, fw.binning.k_info, host.skip_device(device), report=host.report)
+        # the host waits for this step's forward, loss and guard only: the
+        # backward, the guarded Adam and the next forward stay queued behind it
+        done = torch.cuda.Event()
+        done.record(torch.cuda.current_stream(device))
         g2 = R.render_backward(fw.d_image, fw.out, fw.splats, fw.binning, fw.camera.width, fw.camera.height,
                                config.background)
         if g2.tile_order is not None:
@@ -285,12 +295,11 @@ def train_step(state: TrainState, views: Sequence[TrainView], config: TrainConfi
             state._tile_orders[(fw.view_idx, fw.camera.width, fw.camera.height)] = g2.tile_order
         state.adam.backward_step(state.cloud, fw.camera, fw.splats, g2, fw.degree, it, config, stats=state.stats,
                                  skip=skip)
-        done = host.stage(fw.loss, fw.binning.k_info)
         if lookahead:
             nxt = _enqueue_forward(state, _sample_view(state, views, config, it + 1,
                                                        _degree_for(degree, it + 1, config)), config)
         done.synchronize()
-        lvals, kvals = host.values()
+        lvals, kvals = host.report_values()
         try:
             fw.binning.check_host(kvals)
             break

@@ -127,6 +127,12 @@ def test_train_step_divergence_applies_nothing(cuda_device):
     assert step_guard(torch.tensor([float("inf"), 0, 0, 0], device="cuda"), k).item() == 1
     assert step_guard(torch.tensor([1.0, 0, 0, 0], device="cuda"), torch.tensor([10, 2, 5], dtype=torch.int64,
                                                                                  device="cuda")).item() == 1
+    # the guard's host report lands directly in (mapped) pinned memory
+    rep = torch.zeros(8, dtype=torch.float64).pin_memory()
+    step_guard(torch.tensor([0.5, 0.25, 0.125, 2.0], device="cuda"), torch.tensor([7, 0, 7], dtype=torch.int64,
+                                                                                   device="cuda"), report=rep)
+    torch.cuda.synchronize()
+    assert rep.tolist() == [0.5, 0.25, 0.125, 2.0, 7.0, 0.0, 7.0, 0.0]
 
 
 @pytest.mark.gpu
