@@ -17,6 +17,10 @@ namespace gs {
 namespace {
 
 constexpr int kR = 5;         // window radius (11 taps)
+#ifndef GS_SSIM_REAL
+#define GS_SSIM_REAL double   // per-pixel SSIM and adjoint precision
+#endif
+using SsimReal = GS_SSIM_REAL;
 constexpr double kC1 = 0.01 * 0.01;
 constexpr double kC2 = 0.03 * 0.03;
 
@@ -170,23 +174,23 @@ ssim_forward_kernel(const float* __restrict__ img, const float* __restrict__ gt,
       if (gx < W && gy < H) {
         const size_t p = size_t(gy) * W + gx;
         // moments of the shifted values: sigma^2 / covariance directly, means shifted back
-        const double msx = m[o][0], msy = m[o][1];
-        const double sx = double(m[o][2]) - msx * msx, sy = double(m[o][3]) - msy * msy;
-        const double sxy = double(m[o][4]) - msx * msy;
-        const double mu_x = msx + double(kShift) * win.total, mu_y = msy + double(kShift) * win.total;
-        const double a1 = 2.0 * mu_x * mu_y + kC1, a2 = 2.0 * sxy + kC2;
-        const double b1 = mu_x * mu_x + mu_y * mu_y + kC1, b2 = sx + sy + kC2;
+        const SsimReal msx = m[o][0], msy = m[o][1];
+        const SsimReal sx = SsimReal(m[o][2]) - msx * msx, sy = SsimReal(m[o][3]) - msy * msy;
+        const SsimReal sxy = SsimReal(m[o][4]) - msx * msy;
+        const SsimReal mu_x = msx + SsimReal(kShift) * SsimReal(win.total), mu_y = msy + SsimReal(kShift) * SsimReal(win.total);
+        const SsimReal a1 = SsimReal(2.0) * mu_x * mu_y + SsimReal(kC1), a2 = SsimReal(2.0) * sxy + SsimReal(kC2);
+        const SsimReal b1 = mu_x * mu_x + mu_y * mu_y + SsimReal(kC1), b2 = sx + sy + SsimReal(kC2);
         // one float64 division per pixel and channel: 1/b1 = b2/(b1 b2), 1/b2 = b1/(b1 b2)
-        const double inv = 1.0 / (b1 * b2);
+        const SsimReal inv = SsimReal(1.0) / (b1 * b2);
         ssim_sum += (a1 * a2) * inv;
         // ssim_backward (ssim.py:67-84) with a constant d_map
-        const double d_a1 = d_map * a2 * inv, d_a2 = d_map * a1 * inv;
-        const double d_b1 = -d_a1 * (a1 * b2 * inv), d_b2 = -d_a2 * (a2 * b1 * inv);
-        const double d_mu = 2.0 * mu_y * d_a1 + 2.0 * mu_x * d_b1 - 2.0 * mu_y * d_a2 - 2.0 * mu_x * d_b2;
+        const SsimReal d_a1 = SsimReal(d_map) * a2 * inv, d_a2 = SsimReal(d_map) * a1 * inv;
+        const SsimReal d_b1 = -d_a1 * (a1 * b2 * inv), d_b2 = -d_a2 * (a2 * b1 * inv);
+        const SsimReal d_mu = SsimReal(2.0) * mu_y * d_a1 + SsimReal(2.0) * mu_x * d_b1 - SsimReal(2.0) * mu_y * d_a2 - SsimReal(2.0) * mu_x * d_b2;
         src[9 * p + 3 * 0 + ch] = float(d_mu);
         src[9 * p + 3 * 1 + ch] = float(d_b2);
-        src[9 * p + 3 * 2 + ch] = float(2.0 * d_a2);
-        const double diff = double(img[3 * p + ch]) - double(gt[3 * p + ch]);
+        src[9 * p + 3 * 2 + ch] = float(SsimReal(2.0) * d_a2);
+        const SsimReal diff = SsimReal(img[3 * p + ch]) - SsimReal(gt[3 * p + ch]);
         l1_sum += fabs(diff);
         sq_sum += diff * diff;   // for the step's PSNR (optimizer.py:257-259)
       }

@@ -37,6 +37,9 @@ def main() -> None:
     out, splats, binning = R.render_view(cloud, cam, bg, 3, training=True)
     d = torch.from_numpy(np.random.default_rng(1).uniform(-1, 1, (1080, 1920, 3)).astype(np.float32) / 6e6).cuda()
 
+    from paper_2308_04079_b200.loss import l1_dssim_loss
+    tgt = torch.rand_like(out.image)
+
     def timeit(fn):
         for _ in range(3):
             fn()
@@ -66,6 +69,7 @@ def main() -> None:
         "blend_bwd_ms": timeit(lambda: R.render_backward(d, out, splats, binning, 1920, 1080, bg)),
         "bin_async_ms": timeit(lambda: R.bin_and_sort_async(splats, 1920, 1080)),
         "preprocess_fwd_ms": timeit(lambda: R._project_tensors(cloud.c_params(), len(cloud), "cuda", cam, 3)),
+        "loss_ms": timeit(lambda: l1_dssim_loss(out.image, tgt, 0.2)),
     }
     if "--order" in sys.argv:
         import ctypes
