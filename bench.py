@@ -125,6 +125,9 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
     cloud_np, cam0 = synthetic.frustum_scene(n, WIDTH, HEIGHT, seed=0)
     cloud = GaussianCloud.from_numpy(**cloud_np, device=dev)
     del cloud_np
+    # the e2e arm starts from the same initial scene as the device loop (the
+    # loop trains `cloud` in place)
+    initial = {g: getattr(cloud, g).clone() for g in ("means", "rotations", "log_scales", "opacity_logits", "sh")}
     # each rank renders its own view: the frustum camera panned by a small per-rank offset
     def view_for(r: int) -> Camera:
         return Camera(np.eye(3), np.array([0.02 * r, -0.01 * r, 0.0]), cam0.fx, cam0.fy, cam0.cx, cam0.cy,
@@ -237,8 +240,7 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
     from paper_2308_04079_b200.densify import TrainState
     from paper_2308_04079_b200.training import TrainView, train_step
     gt_host = target.cpu().pin_memory()
-    e2e_cloud = GaussianCloud(**{g: getattr(cloud, g).clone() for g in
-                                 ("means", "rotations", "log_scales", "opacity_logits", "sh")})
+    e2e_cloud = GaussianCloud(**initial)
     state = TrainState(e2e_cloud, scene_extent=10.0, seed=rank)
     state.active_sh_degree = DEGREE
     e2e_config = TrainConfig(lambda_dssim=LAMBDA_DSSIM, warmup_upsample_iters=(0, 0), sh_band_interval=10**9)
@@ -264,7 +266,7 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
         dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
     e2e_ms = float(e_ms.item())
     e2e_loss = report.loss
-    del state, e2e_cloud
+    del state, e2e_cloud, initial
 
     # inference render FPS (forward only, same scene, same camera): the
     # sync-free render_view_async (K stays on the device; every frame's
