@@ -333,10 +333,10 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
         "stage_ms": {k: round(v, 4) for k, v in stage_ms.items()},
         "instances_per_view": timer.last_k, "evaluated_pairs_per_view": e_pairs, "visible_gaussians": visible,
         "e2e": {"value": round(e2e_value, 3), "unit": UNIT, "h2d_bytes_per_step": WIDTH * HEIGHT * 3 * 4,
-                "d2h_bytes_per_step": 4 * 4 + 3 * 8,
+                "d2h_bytes_per_step": 8 * 8,   # the guard's report: [loss x4, K, flags, min(K, cap), skip] f64
                 "path": "training.train_step (mirror of splatlab optimizer.train_step): target image H2D from "
-                        "pinned host memory every step, [loss, L1, SSIM, MSE] + [K, flags, K] read D2H every "
-                        "step; lookahead: the next iteration's forward is enqueued before the host waits",
+                        "pinned host memory every step, [loss, L1, SSIM, MSE, K, flags, K, skip] written D2H into "
+                        "mapped pinned memory by the step-guard kernel every step; lookahead: the next iteration's forward is enqueued before the host waits",
                 "last_loss": round(e2e_loss, 6)},
         "gpu_launches": timer.launches_per_step() * args.steps,
         "roofline": roof["primary"], "roofline_hbm": roof["hbm"], "roofline_stages": roof["stages"],
