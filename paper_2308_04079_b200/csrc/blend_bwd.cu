@@ -43,6 +43,10 @@ constexpr int kConsumerWarps = 8 / kParts;
 constexpr int kThreads = (kConsumerWarps + 1) * 32;
 constexpr int kG = 2;    // splats per reduction group (group_reduce2)
 constexpr int kC = 9;    // gradient components per splat
+// factors applied after the reduction: d_mean2d x/y (2/log2 e), d_alpha,
+// d_conic a, b, c (-1/2, -1, -1/2), colour r, g (colour b = component 8: 1)
+__constant__ float kCompScale[8] = {2.0f / 1.4426950408889634f, 2.0f / 1.4426950408889634f, 1.0f, -0.5f, -1.0f,
+                                    -0.5f, 1.0f, 1.0f};
 
 struct BwdStage {
   float4 k[kBatch];      // eigenbasis rows (record word 1), see make_tile_splat
@@ -205,6 +209,8 @@ blend_bwd_kernel(const float* __restrict__ d_image, const float4* __restrict__ r
   }
 
   // ---------------- consumer warps
+  // this lane's reduced component ((lane >> 1) & 7) and its constant factor
+  const float comp_scale = kCompScale[(lane >> 1) & 7];
   // composited tail behind the current splat, starts at the background term
   float S = T * (dlx * bg.x + dly * bg.y + dlz * bg.z);
   for (int b = 0; b < nb; ++b) {
@@ -253,16 +259,18 @@ blend_bwd_kernel(const float* __restrict__ d_image, const float4* __restrict__ r
             v[u * kC + 8] = w * dlz;
             const float dp = d_a * e.a_raw;
             // d power / d mean = (a dx + b dy, b dx + c dy) = 2 (v1 k1 + v2 k2) / log2(e)
-            // (eigenbasis form: no cancellation for elongated conics)
-            const float q = dp * (2.0f / kLog2e);
-            v[u * kC + 0] = q * fmaf(e.v1, kk.x, e.v2 * kk.z);   // d_mean2d.x
-            v[u * kC + 1] = q * fmaf(e.v1, kk.y, e.v2 * kk.w);   // d_mean2d.y
+            // (eigenbasis form: no cancellation for elongated conics); the
+            // constant factors (2/log2(e), -1/2, -1) are applied once per
+            // splat after the warp reduction (kCompScale)
+            v[u * kC + 0] = dp * fmaf(e.v1, kk.x, e.v2 * kk.z);  // d_mean2d.x / (2/log2e)
+            v[u * kC + 1] = dp * fmaf(e.v1, kk.y, e.v2 * kk.w);  // d_mean2d.y / (2/log2e)
             v[u * kC + 2] = d_a * e.g;                           // d_alpha
             const float2 c2 = st.ctr[j];
             const float dx = lx - c2.x, dy = ly - c2.y;
-            v[u * kC + 3] = -0.5f * dp * dx * dx;                // d_conic a
-            v[u * kC + 4] = -dp * dx * dy;                       // d_conic b
-            v[u * kC + 5] = -0.5f * dp * dy * dy;                // d_conic c
+            const float dpdx = dp * dx;
+            v[u * kC + 3] = dpdx * dx;                           // d_conic a / (-1/2)
+            v[u * kC + 4] = dpdx * dy;                           // d_conic b / (-1)
+            v[u * kC + 5] = dp * dy * dy;                        // d_conic c / (-1/2)
           }
           if (!__any_sync(0xffffffffu, any)) continue;
           float out, out8;
@@ -272,7 +280,7 @@ blend_bwd_kernel(const float* __restrict__ d_image, const float4* __restrict__ r
           if (j >= 0 && (lane & 1) == 0) {
             // fire-and-forget reductions into the (N,12) screen-gradient rows
             float* row = reinterpret_cast<float*>(grads2d) + 12 * size_t(st.id[j]);
-            atomicAdd(row + comp + comp / 3, out);
+            atomicAdd(row + comp + comp / 3, out * comp_scale);
             if (comp == 0) atomicAdd(row + 10, out8);
           }
         }
