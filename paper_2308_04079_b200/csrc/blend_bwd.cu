@@ -222,6 +222,9 @@ blend_bwd_kernel(const float* __restrict__ d_image, const float4* __restrict__ r
     BwdStage& st = stages[s];
     if (lo <= warp_last) {
       const int jmax = min(cnt - 1, warp_last - lo);
+      // this lane takes batch slots j < lim (its last contributor and before);
+      // padding slots of a short group carry j = -1, i.e. 0xffffffff unsigned
+      const uint32_t lim = uint32_t(max(last_idx - lo + 1, 0));
       for (int c = jmax; c >= 0; c -= 32) {
         const int jl = c - lane;  // lane l looks at splat c - l: ascending lanes = back to front
         unsigned live = __ballot_sync(0xffffffffu, jl >= 0 && ((st.mask[jl] >> warp) & 1u));
@@ -242,7 +245,7 @@ blend_bwd_kernel(const float* __restrict__ d_image, const float4* __restrict__ r
             // branch-free body: lanes past their last contributor (or the
             // padding slots of a short group) evaluate with a = 0, which
             // leaves T and S unchanged and zeroes every gradient term
-            const bool use = (js[u] >= 0) && (lo + j <= last_idx) && (e.a > 0.0f);
+            const bool use = (uint32_t(js[u]) < lim) && (e.a > 0.0f);
             any |= use;
             const float a = use ? e.a : 0.0f;
             // 1 - a >= 0.01: MUFU reciprocal (~1 ulp), no IEEE/denormal sequence
