@@ -86,8 +86,13 @@ __device__ __forceinline__ void produce_batch(FwdStage& st, RawRec& raw, const f
   }
 }
 
+#ifdef GS_FWD_MIN_BLOCKS
+#define GS_FWD_LB __launch_bounds__(kThreads, GS_FWD_MIN_BLOCKS)
+#else
+#define GS_FWD_LB __launch_bounds__(kThreads)
+#endif
 template <bool kTraining>
-__global__ void __launch_bounds__(kThreads)
+__global__ void GS_FWD_LB
 blend_fwd_kernel(const float4* __restrict__ rec, const uint32_t* __restrict__ ids, const int2* __restrict__ ranges,
                  int width, int height, int tiles_x, int tile0, float3 bg, float* __restrict__ image,
                  float* __restrict__ t_final, int32_t* __restrict__ last, const int32_t* __restrict__ tile_order,
