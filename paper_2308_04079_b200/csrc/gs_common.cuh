@@ -396,12 +396,6 @@ __device__ __forceinline__ AlphaEval eval_alpha_tile(float lx, float ly, float p
   return e;
 }
 
-__device__ __forceinline__ float warp_sum(float v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
-}
-
 // ---------------------------------------------------------------------------
 // Geometry (float64).  Quaternion -> rotation (core.py:170-184).
 template <typename Real>
