@@ -395,13 +395,14 @@ def test_needle_splats_vs_oracle(cuda_device, seed, thin):
                          grad_tol={"d_log_scales": 5e-3, "d_rotations": 5e-3})
 
 
-def test_tile_orders_do_not_change_results(cuda_device):
+@pytest.mark.parametrize("n,w,h", [(30_000, 320, 200), (200_000, 3840, 2160)])
+def test_tile_orders_do_not_change_results(cuda_device, n, w, h):
     """The forward launched in the previous backward's longest-first order,
     and the scheduled backward, give the plain launches' results (forward
     bit-identical; backward within the float atomics' run-to-run contract)."""
     import ctypes
     from paper_2308_04079_b200 import _lib, synthetic
-    cloud_np, cam = synthetic.frustum_scene(30_000, 320, 200, seed=51)
+    cloud_np, cam = synthetic.frustum_scene(n, w, h, seed=51)
     cloud = GaussianCloud.from_numpy(**cloud_np)
     bg = (0.2, 0.1, 0.3)
     out, splats, binning = R.render_view(cloud, cam, bg, 3, training=True)
