@@ -1,9 +1,12 @@
 // K7 blend_bwd — replaces splatlab rasterizer.render_backward
 // (rasterizer.py:253-316) and gradients.backward_blend (gradients.py:30-94).
 //
-// Same tiling as the forward (8 consumer warps = 8x4 pixel blocks + 1
-// producer warp, kStages-deep ring of shared-memory batches with mbarriers).
-// Each tile walks its list back to front from the largest last contributor
+// One CTA per 16x8 half tile (GS_BWD_PARTS = 2): 4 consumer warps (8x4
+// pixel blocks) + 1 producer warp over a kStages-deep ring of shared-memory
+// batches with mbarriers, like the forward; the two halves of a tile run as
+// independent CTAs (less warp drift per ring, overlapping start-ups), and
+// gs_blend_backward_scheduled launches the tiles heaviest first.
+// Each CTA walks its list back to front from the largest last contributor
 // of its pixels (gradients.py:48-52), re-evaluating alpha with the forward's
 // exact code so the contributor sets coincide.  Each pixel rebuilds T_before
 // by dividing out (1 - a) (gradients.py:67-70) and carries the composited
@@ -16,6 +19,7 @@
 // straight to global memory as a fire-and-forget float reduction (RED) into
 // the splat's screen-gradient row: L2 absorbs them (measured 1.39 ms vs
 // 1.45 ms for shared-memory CAS accumulators flushed per (splat, tile)).
+// The terms' constant factors are applied once per reduced value.
 #include "gs_common.cuh"
 
 namespace gs {

@@ -5,8 +5,9 @@
 // an 8x4 pixel block) + 1 producer warp, warp-specialised over a ring of
 // kStages shared-memory batch buffers guarded by mbarriers:
 //   producer: for each kBatch-entry batch of the tile's sorted instance list,
-//     loads the Gaussian ids, gathers the 48-byte splat records with
-//     cp.async, computes each splat's 8-bit warp coverage mask
+//     loads the Gaussian ids, gathers the 48-byte splat records (words 0-2)
+//     with cp.async, folds the tile origin into them and computes each
+//     splat's 8-bit warp coverage mask
 //     (warp_cover_mask) and arrives on full[stage];
 //   consumers: wait on full[stage], visit (front to back, by ballot over the
 //     mask bits) only the splats that can reach alpha >= 1/255 in their
@@ -16,7 +17,8 @@
 // A pixel stops before its accumulated opacity would exceed 0.9999
 // (rasterizer.py:179-180); once every consumer warp is done the CTA stops
 // (rasterizer.py:194-195): the last warp to finish raises s_stop, which the
-// producer and any waiting consumer poll.
+// producer and any waiting consumer poll.  gs_blend_forward_ordered launches
+// the tiles in a given order (heaviest first) and can record each tile's work.
 #include "gs_common.cuh"
 
 namespace gs {
