@@ -5,6 +5,9 @@
 // (culling, radius, tile rectangle, float32 depth key) runs in float64 with
 // non-contracted IEEE operations, mirroring the float64 reference, so radii
 // and binning agree bit-for-bit.  Appearance (SH colour) runs in float32.
+// Besides the hi/lo split of mean, conic and alpha, each record carries the
+// conic's scaled eigenbasis (conic_basis, float64) from which the blends
+// evaluate the exponent as a sum of two squares.
 #include "gs_common.cuh"
 
 namespace gs {
