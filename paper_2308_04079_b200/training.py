@@ -242,7 +242,7 @@ def _enqueue_forward(state: TrainState, fw: _Forward, config: TrainConfig) -> _F
 
 
 def train_step(state: TrainState, views: Sequence[TrainView], config: TrainConfig, group=None,
-               lookahead: bool = True) -> StepReport:
+               lookahead: bool = False) -> StepReport:
     """One iteration (optimizer.py:222-260), with ONE host synchronisation:
     the loss, the step's MSE (for the PSNR) and the binning's instance count
     and flags are read together at the end of the step.  The backward and
@@ -251,7 +251,8 @@ def train_step(state: TrainState, views: Sequence[TrainView], config: TrainConfi
     the divergence check (optimizer.py:245-246) and a capacity overflow
     (re-render with a larger buffer) still find nothing applied.
 
-    lookahead: before waiting for this step, the NEXT iteration's view is
+    lookahead (opt-in; `train` turns it on): before waiting for this step,
+    the NEXT iteration's view is
     drawn and its forward + loss enqueued behind this step's Adam (stream
     order: it sees the updated parameters), so the GPU never idles while the
     host reads the loss.  The next train_step call consumes it when the

@@ -139,7 +139,8 @@ def run_c5(args) -> dict:
     reports = []
 
     def step():
-        train_step(state, views, config)
+        # lookahead except on the steps a densify follows (it would discard it)
+        train_step(state, views, config, lookahead=(state.iteration + 1) % config.densify_interval != 0)
         if state.iteration % config.densify_interval == 0:
             reports.append(densify_and_prune(state, config))
 
