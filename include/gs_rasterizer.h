@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define GS_ABI_VERSION 1
+#define GS_ABI_VERSION 2
 #define GS_TILE_SIZE 16        /* rasterizer.py:13 TILE_SIZE */
 #define GS_SH_COEFFS 16        /* sh.py:25 NUM_COEFFS */
 #define GS_REC_FLOATS 20       /* floats per projected-splat record, see gs_splats_t */
@@ -184,17 +184,23 @@ int gs_preprocess_forward(const gs_params_t* params, const gs_camera_t* camera,
                           int32_t active_sh_degree, gs_splats_t* splats, void* stream);
 
 /* ---- K2-K5 binning: replaces rasterizer.bin_and_sort (rasterizer.py:69-124)
+ * and make_keys (rasterizer.py:55-62).
  * Orders every (tile, splat) instance by (tile, float32 depth, Gaussian
  * index) — the reference's stable sort on (tile<<32 | depth bits) — and
  * writes the Gaussian id of every sorted instance plus per-tile [start,end)
- * ranges (T,2) int32 (empty tiles [0,0]).  Synchronises `stream` once to
- * read K, written to *k_out (host).  Returns GS_ERR_CAPACITY (and K) when
- * k_capacity < K; the instance buffers then hold unspecified values. */
+ * ranges (T,2) int32 (empty tiles [0,0]).  keys (nullable, device uint64
+ * (capacity,)) additionally receives the reference's sort key of every
+ * sorted instance, (tile << 32) | float32 bits of depth (TileBinning.keys,
+ * rasterizer.py:48).  Hand-written kernels only (see binning.cu): a depth
+ * radix sort over the Gaussians, super-tile buckets, per-tile lists.
+ * gs_bin_and_sort synchronises `stream` once to read K, written to *k_out
+ * (host).  Returns GS_ERR_CAPACITY (and K) when k_capacity < K; the
+ * instance buffers then hold unspecified values. */
 int gs_bin_workspace_size(int64_t n, int32_t width, int32_t height, int64_t k_capacity,
                           size_t* bytes);
 int gs_bin_and_sort(const gs_splats_t* splats, int32_t width, int32_t height,
                     void* workspace, size_t workspace_bytes, int64_t k_capacity,
-                    uint32_t* sorted_ids, int32_t* ranges, int64_t* k_out, void* stream);
+                    uint32_t* sorted_ids, int32_t* ranges, uint64_t* keys, int64_t* k_out, void* stream);
 /* Same binning, enqueued without any host synchronisation (CUDA-graph
  * capturable): K never leaves the device.  k_info is a caller-owned DEVICE
  * int64[3]: [0] = K, [1] = flags (1: zero quaternion among the survivors,
@@ -203,23 +209,8 @@ int gs_bin_and_sort(const gs_splats_t* splats, int32_t width, int32_t height,
  * (e.g. one step later) and re-run with a larger capacity / raise. */
 int gs_bin_and_sort_async(const gs_splats_t* splats, int32_t width, int32_t height,
                           void* workspace, size_t workspace_bytes, int64_t k_capacity,
-                          uint32_t* sorted_ids, int32_t* ranges, int64_t* k_info, void* stream);
-
-/* Banded binning (the same per-tile lists, built per band of tile rows so
- * bands can overlap on separate streams):
- *   gs_depth_order — order[r] = Gaussian of depth rank r (float32 depth, then
- *     index; culled last), the shared first step;
- *   gs_bin_rows_async — steps 2-5 for tile rows [tile_row_begin,
- *     tile_row_end): its own instance list (sorted_ids, k_info as in
- *     gs_bin_and_sort_async) and the ranges of its tiles, written into the
- *     frame's (T,2) ranges array (which the caller zeroes once per frame). */
-int gs_depth_order_workspace_size(int64_t n, size_t* bytes);
-int gs_depth_order(const gs_splats_t* splats, void* workspace, size_t workspace_bytes, uint32_t* order,
-                   void* stream);
-int gs_bin_rows_workspace_size(int64_t n, int32_t width, int32_t height, int64_t k_capacity, size_t* bytes);
-int gs_bin_rows_async(const gs_splats_t* splats, const uint32_t* order, int32_t width, int32_t height,
-                      int32_t tile_row_begin, int32_t tile_row_end, void* workspace, size_t workspace_bytes,
-                      int64_t k_capacity, uint32_t* sorted_ids, int32_t* ranges, int64_t* k_info, void* stream);
+                          uint32_t* sorted_ids, int32_t* ranges, uint64_t* keys, int64_t* k_info,
+                          void* stream);
 
 /* ---- K6 forward blend: replaces rasterizer.render_forward (rasterizer.py:201-240)
  * image (H,W,3) float32.  When training != 0, t_final (H,W) float32 and
@@ -243,12 +234,6 @@ int gs_blend_forward_ordered(const gs_splats_t* splats, const uint32_t* sorted_i
 /* Longest-first tile order from a per-tile work estimate (1/64-octave
  * buckets, heaviest first).  scratch: device int32[tiles + 2048]. */
 int gs_tile_schedule(const int32_t* work, int32_t tiles, int32_t* scratch, int32_t* order, void* stream);
-/* The tiles of rows [tile_row_begin, tile_row_end) only (sorted_ids: that
- * band's instance list from gs_bin_rows_async). */
-int gs_blend_forward_rows(const gs_splats_t* splats, const uint32_t* sorted_ids, const int32_t* ranges,
-                          int32_t width, int32_t height, int32_t tile_row_begin, int32_t tile_row_end,
-                          const float background[3], int32_t training, float* image, float* t_final,
-                          int32_t* last, void* stream);
 
 /* ---- K7 backward blend: replaces rasterizer.render_backward (rasterizer.py:253-316)
  * with gradients.backward_blend (gradients.py:30-94).
@@ -276,12 +261,6 @@ int gs_blend_backward_scheduled(const float* d_image, const gs_splats_t* splats,
                                 const int32_t* ranges, const float* t_final, const int32_t* last, int32_t width,
                                 int32_t height, const float background[3], int32_t* scratch, float* grads2d,
                                 void* stream);
-/* The tiles of rows [tile_row_begin, tile_row_end) only, ACCUMULATING into
- * grads2d (not cleared: clear it once per frame, then one call per band). */
-int gs_blend_backward_rows(const float* d_image, const gs_splats_t* splats, const uint32_t* sorted_ids,
-                           const int32_t* ranges, const float* t_final, const int32_t* last, int32_t width,
-                           int32_t height, int32_t tile_row_begin, int32_t tile_row_end,
-                           const float background[3], float* grads2d, void* stream);
 
 /* ---- K8 backward preprocess: replaces gradients.backward_project
  * (gradients.py:192-259) and the densification statistics update of

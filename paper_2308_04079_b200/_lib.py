@@ -21,6 +21,8 @@ GS_ERR_RESOURCE_LIMIT = 3
 GS_ERR_CAPACITY = 4
 GS_ERR_CUDA = 5
 
+ABI_VERSION = 2
+
 REC_FLOATS = 20
 MODEL_FLOATS = 59
 PLY_FLOATS = 62
@@ -88,19 +90,9 @@ SIGNATURES = [
     ("gs_preprocess_forward", c_int32, [POINTER(GsParams), POINTER(GsCamera), c_int32, POINTER(GsSplats), c_void_p]),
     ("gs_bin_workspace_size", c_int32, [c_int64, c_int32, c_int32, c_int64, POINTER(c_size_t)]),
     ("gs_bin_and_sort", c_int32, [POINTER(GsSplats), c_int32, c_int32, c_void_p, c_size_t, c_int64, c_void_p,
-                                  c_void_p, POINTER(c_int64), c_void_p]),
+                                  c_void_p, c_void_p, POINTER(c_int64), c_void_p]),
     ("gs_bin_and_sort_async", c_int32, [POINTER(GsSplats), c_int32, c_int32, c_void_p, c_size_t, c_int64,
-                                        c_void_p, c_void_p, c_void_p, c_void_p]),
-    ("gs_depth_order_workspace_size", c_int32, [c_int64, POINTER(c_size_t)]),
-    ("gs_depth_order", c_int32, [POINTER(GsSplats), c_void_p, c_size_t, c_void_p, c_void_p]),
-    ("gs_bin_rows_workspace_size", c_int32, [c_int64, c_int32, c_int32, c_int64, POINTER(c_size_t)]),
-    ("gs_bin_rows_async", c_int32, [POINTER(GsSplats), c_void_p, c_int32, c_int32, c_int32, c_int32, c_void_p,
-                                    c_size_t, c_int64, c_void_p, c_void_p, c_void_p, c_void_p]),
-    ("gs_blend_forward_rows", c_int32, [POINTER(GsSplats), c_void_p, c_void_p, c_int32, c_int32, c_int32, c_int32,
-                                        POINTER(c_float), c_int32, c_void_p, c_void_p, c_void_p, c_void_p]),
-    ("gs_blend_backward_rows", c_int32, [c_void_p, POINTER(GsSplats), c_void_p, c_void_p, c_void_p, c_void_p,
-                                         c_int32, c_int32, c_int32, c_int32, POINTER(c_float), c_void_p,
-                                         c_void_p]),
+                                        c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     ("gs_blend_forward", c_int32, [POINTER(GsSplats), c_void_p, c_void_p, c_int32, c_int32, POINTER(c_float),
                                    c_int32, c_void_p, c_void_p, c_void_p, c_void_p]),
     ("gs_blend_backward", c_int32, [c_void_p, POINTER(GsSplats), c_void_p, c_void_p, c_void_p, c_void_p, c_int32,
@@ -158,7 +150,7 @@ def load(path: Path | str | None = None) -> ctypes.CDLL:
         fn = getattr(lib, name)
         fn.restype = restype
         fn.argtypes = argtypes
-    if lib.gs_abi_version() != 1:
+    if lib.gs_abi_version() != ABI_VERSION:
         raise RuntimeError("libgs_b200.so ABI version mismatch")
     if path is None:
         _lib = lib

@@ -341,16 +341,6 @@ extern "C" int gs_blend_backward(const float* d_image, const gs_splats_t* splats
                              (height + kTile - 1) / kTile, background, grads2d, stream);
 }
 
-// The tiles of rows [tile_row_begin, tile_row_end) only, accumulating into
-// grads2d (not cleared here: one clear per frame, then one call per band).
-extern "C" int gs_blend_backward_rows(const float* d_image, const gs_splats_t* splats, const uint32_t* sorted_ids,
-                                      const int32_t* ranges, const float* t_final, const int32_t* last,
-                                      int32_t width, int32_t height, int32_t tile_row_begin, int32_t tile_row_end,
-                                      const float background[3], float* grads2d, void* stream) {
-  return gs::blend_backward_rows(d_image, splats, sorted_ids, ranges, t_final, last, width, height, tile_row_begin,
-                                 tile_row_end, background, grads2d, stream);
-}
-
 // The full frame with the tiles visited in `tile_order` (a permutation of
 // [0, tiles), device int32), e.g. by descending list length.
 extern "C" int gs_blend_backward_ordered(const float* d_image, const gs_splats_t* splats, const uint32_t* sorted_ids,

@@ -269,14 +269,6 @@ extern "C" int gs_blend_forward(const gs_splats_t* splats, const uint32_t* sorte
                                 background, training, image, t_final, last, stream);
 }
 
-extern "C" int gs_blend_forward_rows(const gs_splats_t* splats, const uint32_t* sorted_ids, const int32_t* ranges,
-                                     int32_t width, int32_t height, int32_t tile_row_begin, int32_t tile_row_end,
-                                     const float background[3], int32_t training, float* image, float* t_final,
-                                     int32_t* last, void* stream) {
-  return gs::blend_forward_rows(splats, sorted_ids, ranges, width, height, tile_row_begin, tile_row_end, background,
-                                training, image, t_final, last, stream);
-}
-
 // The full frame with the tiles visited in `tile_order` (a permutation of
 // [0, tiles), device int32).
 extern "C" int gs_blend_forward_ordered(const gs_splats_t* splats, const uint32_t* sorted_ids, const int32_t* ranges,

@@ -67,6 +67,27 @@ def reduce_stats_(stats: DensifyStats, group=None) -> None:
     dist.all_reduce(stats.max_radius_frac, op=dist.ReduceOp.MAX, group=group)
 
 
+def any_rank_(flag: bool, device, group=None) -> bool:
+    """True on every rank when `flag` is true on any rank (MAX all-reduce)."""
+    if not (dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1):
+        return bool(flag)
+    dev = device if dist.get_backend(group) == "nccl" else "cpu"
+    t = torch.tensor([1 if flag else 0], dtype=torch.int32, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+    return bool(t.item())
+
+
+def sync_rng_(state, group=None) -> None:
+    """Give every rank rank 0's training-RNG state (TrainState.rng), so the
+    split samples drawn by densify_and_prune (optimizer.py:335) are identical
+    on all replicas."""
+    if not (dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1):
+        return
+    obj = [state.rng.bit_generator.state]
+    dist.broadcast_object_list(obj, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
+    state.rng.bit_generator.state = obj[0]
+
+
 def train_step_views(cloud, cameras, targets, adam, config, iteration: int, bucket: GradientBucket,
                      stats: DensifyStats | None = None, background=(0.0, 0.0, 0.0), active_sh_degree: int = 3,
                      group=None, streams: int = 1) -> torch.Tensor:

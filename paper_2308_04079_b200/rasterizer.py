@@ -162,8 +162,10 @@ class DeviceSplats:
 
 @dataclass
 class TileBinning:
-    """Sorted instances (rasterizer.py:44-52): Gaussian id per sorted instance
-    and per-tile [start, end) ranges.  Keys are implicit: (tile, depth[id])."""
+    """Sorted instances (rasterizer.py:44-52): Gaussian id per sorted instance,
+    per-tile [start, end) ranges and, when requested (with_keys=True), the
+    reference's 64-bit sort keys (tile << 32) | float32 bits of depth
+    (make_keys, rasterizer.py:55-62) as int64."""
 
     splat_ids: torch.Tensor   # (K,) int32 Gaussian index (N-space); (capacity,) when k_info is set
     ranges: torch.Tensor      # (T,2) int32
@@ -171,6 +173,8 @@ class TileBinning:
     tiles_y: int
     k_info: torch.Tensor | None = None   # async binning: device int64 [K, flags, min(K, capacity)]
     n_gaussians: int = 0
+    keys: torch.Tensor | None = None     # (K,) int64 (capacity-sized when k_info is set)
+    hint: str | None = None              # capacity-hint key (device @ frame size)
 
     @property
     def num_instances(self) -> int:
@@ -189,7 +193,8 @@ class TileBinning:
     def check_host(self, k_info) -> None:
         """check() on an already-read copy of k_info (no synchronisation)."""
         k, flags = int(k_info[0]), int(k_info[1])
-        _capacity.update(self.splat_ids.device, k, self.n_gaussians or None)
+        _capacity.update(self.hint or _capacity.key(self.splat_ids.device, 16 * self.tiles_x, 16 * self.tiles_y),
+                         k, self.n_gaussians or None)
         if flags & 1:
             raise InvalidPrimitiveError("zero-norm quaternion cannot be normalized")
         if flags & 4:
@@ -309,27 +314,34 @@ def project(cloud: GaussianCloud, camera, active_sh_degree: int = 3) -> DeviceSp
 
 
 class _CapacityHint:
-    """Instance-buffer sizing: remembers, per device, the largest K and the
-    largest instances-per-Gaussian ratio seen, so a steady-state frame issues
-    exactly one binning call and a cloud that grew (densification) gets a
-    proportionally larger buffer."""
+    """Instance-buffer sizing: remembers, per device and frame size, the
+    largest K and the largest instances-per-Gaussian ratio seen, so a
+    steady-state frame issues exactly one binning call and a cloud that grew
+    (densification) gets a proportionally larger buffer.  Never above the
+    reference's instance limit (rasterizer.py:25)."""
 
     def __init__(self):
         self.k = {}
         self.ratio = {}
 
-    HEADROOM = 1.05   # the async tile sort runs over the whole capacity: keep the padding small
+    HEADROOM = 1.05
+    LIMIT = MAX_INSTANCES - 1
 
-    def get(self, device, n: int | None = None) -> int:
-        key = device if isinstance(device, str) else str(device)
+    @staticmethod
+    def key(device, width: int | None = None, height: int | None = None) -> str:
+        d = device if isinstance(device, str) else str(device)
+        return d if width is None else f"{d}@{width}x{height}"
+
+    def get(self, key, n: int | None = None) -> int:
+        key = self.key(key)
         k = self.k.get(key, 1 << 16)
         if n is not None and key in self.ratio:
             k = max(k, int(self.ratio[key] * n * self.HEADROOM) + 4096)
-        return k
+        return min(k, self.LIMIT)
 
-    def update(self, device, k: int, n: int | None = None) -> None:
-        key = device if isinstance(device, str) else str(device)
-        self.k[key] = max(self.k.get(key, 1 << 16), int(k * self.HEADROOM) + 4096)
+    def update(self, key, k: int, n: int | None = None) -> None:
+        key = self.key(key)
+        self.k[key] = min(max(self.k.get(key, 1 << 16), int(k * self.HEADROOM) + 4096), self.LIMIT)
         if n:
             self.ratio[key] = max(self.ratio.get(key, 0.0), k / n)
 
@@ -337,30 +349,34 @@ class _CapacityHint:
 _capacity = _CapacityHint()
 
 
-def bin_and_sort(splats: DeviceSplats, width: int, height: int) -> TileBinning:
-    """K2-K5: duplicate, sort by (tile, depth, index), find tile ranges (rasterizer.py:69)."""
+def bin_and_sort(splats: DeviceSplats, width: int, height: int, with_keys: bool = False) -> TileBinning:
+    """K2-K5: duplicate, sort by (tile, depth, index), find tile ranges (rasterizer.py:69).
+    with_keys: also return the 64-bit sort keys (TileBinning.keys, rasterizer.py:48)."""
     lib = _lib.load()
     tiles_x, tiles_y = tile_extent(width, height)
     device = splats.rec.device
+    hint = _capacity.key(device, width, height)
     n = len(splats)
     cs = splats.c_struct()
     stream = _stream()
-    cap = _capacity.get(device, n)
+    cap = _capacity.get(hint, n)
     for _ in range(2):
         ws_bytes = _bin_workspace_bytes(n, width, height, cap)
         ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=device)
         ids = torch.empty(max(cap, 1), dtype=torch.int32, device=device)
+        keys = torch.empty(max(cap, 1), dtype=torch.int64, device=device) if with_keys else None
         ranges = torch.empty((tiles_x * tiles_y, 2), dtype=torch.int32, device=device)
         k = ctypes.c_int64(0)
         st = lib.gs_bin_and_sort(ctypes.byref(cs), width, height, ws.data_ptr(), ws_bytes, cap,
-                                 ids.data_ptr(), ranges.data_ptr(), ctypes.byref(k), stream)
+                                 ids.data_ptr(), ranges.data_ptr(), _lib.ptr(keys), ctypes.byref(k), stream)
         if st == _lib.GS_ERR_CAPACITY:
-            _capacity.update(device, k.value, n)
-            cap = _capacity.get(device, n)
+            _capacity.update(hint, k.value, n)
+            cap = _capacity.get(hint, n)
             continue
         _lib.check(st, "bin_and_sort")
-        _capacity.update(device, k.value, n)
-        return TileBinning(ids[:k.value], ranges, tiles_x, tiles_y)
+        _capacity.update(hint, k.value, n)
+        return TileBinning(ids[:k.value], ranges, tiles_x, tiles_y,
+                           keys=keys[:k.value] if keys is not None else None)
     raise RuntimeError("bin_and_sort: instance capacity did not converge")
 
 
@@ -368,9 +384,7 @@ _ws_sizes: dict = {}
 
 
 def _bin_workspace_bytes(n: int, width: int, height: int, cap: int) -> int:
-    """gs_bin_workspace_size, memoised (a pure function of its arguments; the
-    query runs CUB's host-side size computations, a noticeable share of the
-    per-frame host time)."""
+    """gs_bin_workspace_size, memoised (a pure function of its arguments)."""
     key = (n, width, height, cap)
     b = _ws_sizes.get(key)
     if b is None:
@@ -382,7 +396,8 @@ def _bin_workspace_bytes(n: int, width: int, height: int, cap: int) -> int:
     return b
 
 
-def bin_and_sort_async(splats: DeviceSplats, width: int, height: int, capacity: int | None = None) -> TileBinning:
+def bin_and_sort_async(splats: DeviceSplats, width: int, height: int, capacity: int | None = None,
+                       with_keys: bool = False) -> TileBinning:
     """bin_and_sort without a host synchronisation: K stays on the device
     (binning.k_info) and the instance buffers are sized by `capacity`
     (default: the largest K seen on this device x 1.15).  Call
@@ -390,17 +405,20 @@ def bin_and_sort_async(splats: DeviceSplats, width: int, height: int, capacity: 
     lib = _lib.load()
     tiles_x, tiles_y = tile_extent(width, height)
     device = splats.rec.device
-    cap = int(capacity) if capacity is not None else _capacity.get(device, len(splats))
+    hint = _capacity.key(device, width, height)
+    cap = int(capacity) if capacity is not None else _capacity.get(hint, len(splats))
     ws_bytes = _bin_workspace_bytes(len(splats), width, height, cap)
     ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=device)
     ids = torch.empty(max(cap, 1), dtype=torch.int32, device=device)
     ranges = torch.empty((tiles_x * tiles_y, 2), dtype=torch.int32, device=device)
+    keys = torch.empty(max(cap, 1), dtype=torch.int64, device=device) if with_keys else None
     k_info = torch.empty(3, dtype=torch.int64, device=device)
     cs = splats.c_struct()
     _lib.check(lib.gs_bin_and_sort_async(ctypes.byref(cs), width, height, ws.data_ptr(), ws_bytes, cap,
-                                         ids.data_ptr(), ranges.data_ptr(), k_info.data_ptr(), _stream()),
+                                         ids.data_ptr(), ranges.data_ptr(), _lib.ptr(keys), k_info.data_ptr(),
+                                         _stream()),
                "bin_and_sort")
-    return TileBinning(ids, ranges, tiles_x, tiles_y, k_info, len(splats))
+    return TileBinning(ids, ranges, tiles_x, tiles_y, k_info, len(splats), keys, hint)
 
 
 def _bg(background) -> ctypes.Array:
@@ -564,150 +582,6 @@ class TileSchedule:
         _lib.check(_lib.load().gs_tile_schedule(self.work.data_ptr(), self.work.numel(), self.scratch.data_ptr(),
                                                 self.order.data_ptr(), _stream()), "tile_schedule")
         self.ready = True
-
-
-# ---------------------------------------------------------------------------
-# banded frames: the binning and the blends per band of tile rows, the bands
-# on their own CUDA streams so one band's latency-bound sort overlaps another
-# band's compute-bound blend (the per-tile lists, hence the images and
-# gradients, are those of the full-frame path)
-
-_side_streams: dict = {}
-
-
-def _streams(device, count: int) -> list:
-    key = str(device)
-    ss = _side_streams.setdefault(key, [])
-    while len(ss) < count:
-        ss.append(torch.cuda.Stream(device))
-    return ss[:count]
-
-
-def band_rows(tiles_y: int, bands: int) -> list[tuple[int, int]]:
-    bands = max(1, min(bands, tiles_y))
-    return [(tiles_y * b // bands, tiles_y * (b + 1) // bands) for b in range(bands)]
-
-
-@dataclass
-class BandedBinning:
-    """Per-band instance lists over one frame-wide ranges array."""
-
-    rows: list            # [(tile_row_begin, tile_row_end)]
-    splat_ids: list       # per band: (capacity,) int32
-    k_info: list          # per band: device int64 [K, flags, min(K, capacity)]
-    ranges: torch.Tensor  # (T,2) int32
-    tiles_x: int
-    tiles_y: int
-    keys: list            # capacity-hint keys
-
-    @property
-    def num_instances(self) -> int:
-        return sum(int(k[0].item()) for k in self.k_info)
-
-    def check(self) -> None:
-        self.check_host([k.tolist() for k in self.k_info])
-
-    def check_host(self, k_infos) -> None:
-        """Raise like TileBinning.check_host for the first band that failed
-        (every band's capacity hint is updated first)."""
-        errors = []
-        for key, ids, (k, flags, _) in zip(self.keys, self.splat_ids, k_infos):
-            _capacity.update(key, int(k))
-            errors.append((int(k), int(flags), ids.shape[0]))
-        for k, flags, cap in errors:
-            if flags & 1:
-                raise InvalidPrimitiveError("zero-norm quaternion cannot be normalized")
-            if flags & 4:
-                _lib.check(_lib.GS_ERR_RESOURCE_LIMIT, "bin_and_sort")
-            if flags & 2:
-                raise CapacityError(f"bin_and_sort: {k} instances exceed the band capacity {cap}")
-
-
-def render_view_banded(cloud: GaussianCloud, camera, background, active_sh_degree: int = 3, training: bool = False,
-                       bands: int = 2):
-    """render_view_async with the frame split into `bands` bands of tile rows,
-    binned and blended on separate CUDA streams after one shared projection
-    and depth order.  No host synchronisation; errors surface through
-    binning.check() (or check_host on a copy of the k_info tensors)."""
-    camera = _camera(camera)
-    lib = _lib.load()
-    device = cloud.device
-    n = len(cloud)
-    W, H = camera.width, camera.height
-    tiles_x, tiles_y = tile_extent(W, H)
-    splats = _project_tensors(cloud.c_params(), n, device, camera, active_sh_degree)
-    cs = splats.c_struct()
-    main = torch.cuda.current_stream(device)
-    # shared step: the depth order
-    dbytes = ctypes.c_size_t(0)
-    _lib.check(lib.gs_depth_order_workspace_size(n, ctypes.byref(dbytes)), "depth_order")
-    dws = torch.empty(max(int(dbytes.value), 1), dtype=torch.uint8, device=device)
-    order = torch.empty(max(n, 1), dtype=torch.int32, device=device)
-    _lib.check(lib.gs_depth_order(ctypes.byref(cs), dws.data_ptr(), dbytes.value, order.data_ptr(),
-                                  main.cuda_stream), "depth_order")
-    ranges = torch.zeros((tiles_x * tiles_y, 2), dtype=torch.int32, device=device)
-    image = torch.empty((H, W, 3), dtype=torch.float32, device=device)
-    t_final = torch.empty((H, W), dtype=torch.float32, device=device) if training else None
-    last = torch.empty((H, W), dtype=torch.int32, device=device) if training else None
-    rows = band_rows(tiles_y, bands)
-    keys = [f"{device}/band{b}of{len(rows)}@{W}x{H}" for b in range(len(rows))]
-    # every buffer is allocated on the main stream, before the side streams use it
-    per_band = []
-    for (y0, y1), key in zip(rows, keys):
-        if key in _capacity.k:
-            cap = _capacity.get(key)
-        else:   # first frame of this band layout: the frame-wide hint, pro rata, with a margin
-            cap = int(_capacity.get(device, n) * 1.3 * (y1 - y0) / tiles_y) + 4096
-        nbytes = ctypes.c_size_t(0)
-        _lib.check(lib.gs_bin_rows_workspace_size(n, W, H, cap, ctypes.byref(nbytes)), "bin_rows")
-        per_band.append((cap, int(nbytes.value), torch.empty(max(int(nbytes.value), 1), dtype=torch.uint8,
-                                                               device=device),
-                         torch.empty(max(cap, 1), dtype=torch.int32, device=device),
-                         torch.empty(3, dtype=torch.int64, device=device)))
-    ready = torch.cuda.Event()
-    ready.record(main)
-    bg = _bg(background)
-    for (y0, y1), stream, (cap, nbytes, ws, ids, kinfo) in zip(rows, _streams(device, len(rows)), per_band):
-        stream.wait_event(ready)
-        _lib.check(lib.gs_bin_rows_async(ctypes.byref(cs), order.data_ptr(), W, H, y0, y1, ws.data_ptr(), nbytes, cap,
-                                         ids.data_ptr(), ranges.data_ptr(), kinfo.data_ptr(), stream.cuda_stream),
-                   "bin_rows")
-        _lib.check(lib.gs_blend_forward_rows(ctypes.byref(cs), ids.data_ptr(), ranges.data_ptr(), W, H, y0, y1, bg,
-                                             int(bool(training)), image.data_ptr(), _lib.ptr(t_final), _lib.ptr(last),
-                                             stream.cuda_stream), "render_forward")
-    for stream in _streams(device, len(rows)):
-        main.wait_stream(stream)
-    binning = BandedBinning(rows, [b[3] for b in per_band], [b[4] for b in per_band], ranges, tiles_x, tiles_y, keys)
-    return RenderOutput(image, t_final, last), splats, binning
-
-
-def render_backward_banded(d_image: torch.Tensor, output: RenderOutput, splats: DeviceSplats,
-                           binning: BandedBinning, width: int, height: int, background) -> SplatGrads2D:
-    """render_backward over the bands of a render_view_banded frame, one
-    stream per band, accumulating into one cleared gradient buffer."""
-    if output.final_transmittance is None or output.last_contributor is None:
-        raise ValueError("backward pass needs a training-mode RenderOutput")  # rasterizer.py:265-266
-    lib = _lib.load()
-    device = splats.rec.device
-    d_image = d_image.to(dtype=torch.float32).contiguous()
-    if tuple(d_image.shape) != (height, width, 3):
-        raise ValueError(f"d_image shape {tuple(d_image.shape)} != {(height, width, 3)}")
-    packed = torch.zeros((len(splats), _lib.GRAD2D_FLOATS), dtype=torch.float32, device=device)
-    cs = splats.c_struct()
-    main = torch.cuda.current_stream(device)
-    ready = torch.cuda.Event()
-    ready.record(main)
-    bg = _bg(background)
-    streams = _streams(device, len(binning.rows))
-    for (y0, y1), stream, ids in zip(binning.rows, streams, binning.splat_ids):
-        stream.wait_event(ready)
-        _lib.check(lib.gs_blend_backward_rows(d_image.data_ptr(), ctypes.byref(cs), ids.data_ptr(),
-                                              binning.ranges.data_ptr(), output.final_transmittance.data_ptr(),
-                                              output.last_contributor.data_ptr(), width, height, y0, y1, bg,
-                                              packed.data_ptr(), stream.cuda_stream), "render_backward")
-    for stream in streams:
-        main.wait_stream(stream)
-    return SplatGrads2D(packed)
 
 
 # ---------------------------------------------------------------------------

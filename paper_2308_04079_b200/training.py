@@ -74,41 +74,55 @@ class _ImagePrefetcher:
     """Host-resident view images: the next step's image (known in advance
     from the epoch order) is copied H2D on a side stream while the current
     step computes; two device buffers alternate, each released by an event
-    recorded after the loss kernels (its last reader)."""
+    recorded after the loss kernels (its last reader).  A slot holds the view
+    object itself (identity-compared, so a recycled id() can never alias a
+    stale slot) and the image's pointer and shape."""
 
     def __init__(self, device):
         self.device = device
         self.stream = torch.cuda.Stream(device)
-        self.slots = [None, None]      # (view id, device tensor, ready event, consumed event)
+        self.slots = [None, None]      # (view, (data_ptr, shape), device tensor, ready event, consumed event)
         self.turn = 0
+
+    @staticmethod
+    def _tag(view: TrainView):
+        return view.image.data_ptr(), tuple(view.image.shape)
 
     def _issue(self, view: TrainView):
         slot = self.turn
         self.turn ^= 1
         old = self.slots[slot]
-        buf = old[1] if old is not None and old[1].shape == view.image.shape else torch.empty(
+        buf = old[2] if old is not None and old[2].shape == view.image.shape else torch.empty(
             view.image.shape, dtype=view.image.dtype, device=self.device)
         ready = torch.cuda.Event()
         with torch.cuda.stream(self.stream):
             if old is not None:
-                self.stream.wait_event(old[3])
+                self.stream.wait_event(old[4])
             buf.copy_(view.image, non_blocking=True)
             ready.record(self.stream)
-        self.slots[slot] = (id(view), buf, ready, torch.cuda.Event())
+        self.slots[slot] = (view, self._tag(view), buf, ready, torch.cuda.Event())
         return self.slots[slot]
 
-    def get(self, view: TrainView):
-        """(device image, consumed event) for this step's view."""
-        hit = next((s for s in self.slots if s is not None and s[0] == id(view)), None)
+    def _match(self, s, view: TrainView) -> bool:
+        return s is not None and s[0] is view and s[1] == self._tag(view)
+
+    def get(self, view: TrainView, fresh: bool = False):
+        """(device image, consumed event) for this step's view.  fresh: copy
+        it again even if a slot holds it (its buffer may have been reused)."""
+        hit = None if fresh else next((s for s in self.slots if self._match(s, view)), None)
         if hit is None:
             hit = self._issue(view)
-        torch.cuda.current_stream(self.device).wait_event(hit[2])
-        self.slots = [s if s is not hit else (None, s[1], s[2], s[3]) for s in self.slots]
-        return hit[1], hit[3]
+        torch.cuda.current_stream(self.device).wait_event(hit[3])
+        self.slots = [s if s is not hit else (None, None, s[2], s[3], s[4]) for s in self.slots]
+        return hit[2], hit[4]
 
     def prefetch(self, view: TrainView) -> None:
-        if all(s is None or s[0] != id(view) for s in self.slots):
+        if not any(self._match(s, view) for s in self.slots):
             self._issue(view)
+
+    def clear(self) -> None:
+        """Drop the view references (end of a training run)."""
+        self.slots = [None if s is None else (None, None, s[2], s[3], s[4]) for s in self.slots]
 
 
 _prefetchers: dict = {}
@@ -217,16 +231,25 @@ def _sample_view(state: TrainState, views: Sequence[TrainView], config: TrainCon
     view = views[view_idx]
     scale = warmup_scale(it, config.warmup_upsample_iters)
     camera = view.camera if scale == 1.0 else view.camera.scaled(scale)
+    gt, consumed = _ground_truth(state, view, camera)
     device = state.cloud.device
-    image, consumed = view.image, None
-    if image.device != device:   # host-resident view: H2D from pinned memory, prefetched one step ahead
-        pf = _prefetchers.setdefault(str(device), _ImagePrefetcher(device))
-        image, consumed = pf.get(view)
+    if view.image.device != device:   # prefetch the next view's image one step ahead
         nxt = _peek_next_view(state, len(views))
         if nxt is not None and views[nxt].image.device != device:
-            pf.prefetch(views[nxt])
-    gt = downscale_image(image, camera.height, camera.width)
+            _prefetchers[str(device)].prefetch(views[nxt])
     return _Forward(it, view_idx, camera, degree, gt, consumed, snapshot, views, config, _cloud_key(state))
+
+
+def _ground_truth(state: TrainState, view: TrainView, camera: Camera, fresh: bool = False):
+    """(target image at the camera's resolution, consumed event or None).
+    A host-resident view is copied H2D from pinned memory by the prefetcher;
+    fresh: copy it again (the slot's buffer may have been handed on)."""
+    device = state.cloud.device
+    image, consumed = view.image, None
+    if image.device != device:
+        pf = _prefetchers.setdefault(str(device), _ImagePrefetcher(device))
+        image, consumed = pf.get(view, fresh=fresh)
+    return downscale_image(image, camera.height, camera.width), consumed
 
 
 def _enqueue_forward(state: TrainState, fw: _Forward, config: TrainConfig) -> _Forward:
@@ -310,6 +333,8 @@ def train_step(state: TrainState, views: Sequence[TrainView], config: TrainConfi
                 state.discard_lookahead()
             if attempt == 2:
                 raise
+            # the lookahead's prefetch may have refilled this view's image buffer: copy it again
+            fw.gt, fw.consumed = _ground_truth(state, fw.views[fw.view_idx], fw.camera, fresh=True)
             fw = _enqueue_forward(state, fw, config)
     state.iteration, state.active_sh_degree = it, degree
     value, mse = float(lvals[0]), float(lvals[3])
@@ -360,8 +385,11 @@ def _train_step_sharded(state: TrainState, views: Sequence[TrainView], config: T
             if attempt == 2:
                 raise
     value, mse = float(lvals[0]), float(lvals[3])
-    if not math.isfinite(value):
-        raise TrainingDiverged(f"non-finite loss {value} at iteration {it}")
+    # every rank must take the same branch: one rank's non-finite loss stops all of them
+    from .distributed import any_rank_
+    if any_rank_(not math.isfinite(value), device, group):
+        raise TrainingDiverged(f"non-finite loss {value} at iteration {it}"
+                               + ("" if not math.isfinite(value) else " (on another rank)"))
     g2 = R.render_backward(d_image, out, splats, binning, camera.width, camera.height, bg)
     bucket = getattr(state, "_bucket", None)
     if bucket is None or bucket.n != len(state.cloud):
@@ -377,24 +405,47 @@ def _train_step_sharded(state: TrainState, views: Sequence[TrainView], config: T
 
 def train(state: TrainState, views: Sequence[TrainView], config: TrainConfig, *, iterations: int | None = None,
           eval_interval: int = 500, progress: Callable[[str], None] | None = None,
-          densify_hook: Callable[[DensifyReport], None] | None = None) -> list[DensifyReport]:
-    """Drive training with densification interleaved (optimizer.py:377-400)."""
+          densify_hook: Callable[[DensifyReport], None] | None = None,
+          checkpoint_hook: Callable[[TrainState], None] | None = None,
+          checkpoint_iters: Sequence[int] = (7000, 30000), group=None) -> list[DensifyReport]:
+    """Drive training with densification interleaved (optimizer.py:377-400),
+    including the reference's checkpoint hook (optimizer.py:398-399).
+
+    The lookahead (see train_step) is skipped on iterations followed by a
+    densification or a checkpoint, so the hooks see a state with nothing
+    pending.  Under torch.distributed the densification statistics are
+    reduced over the ranks (sum / max) and every rank densifies with rank 0's
+    RNG state, so the replicas clone, split and prune identically."""
     iterations = config.total_iters if iterations is None else iterations
     densify_until = config.resolve_densify_until()
+    world, _ = _world(group)
     reports = []
-    while state.iteration < iterations:
-        nxt = state.iteration + 1
-        densify_next = (config.densify_start < nxt <= densify_until and nxt % config.densify_interval == 0)
-        step = train_step(state, views, config, lookahead=nxt < iterations and not densify_next)
-        if (config.densify_start < state.iteration <= densify_until
-                and state.iteration % config.densify_interval == 0):
-            report = densify_and_prune(state, config)
-            reports.append(report)
-            if densify_hook:
-                densify_hook(report)
-        if progress and (state.iteration % eval_interval == 0 or state.iteration == iterations):
-            progress(f"iter={step.iteration} loss={step.loss:.6f} "
-                     f"gaussians={len(state.cloud)} psnr={step.psnr:.2f}")
+    try:
+        while state.iteration < iterations:
+            nxt = state.iteration + 1
+            densify_next = (config.densify_start < nxt <= densify_until and nxt % config.densify_interval == 0)
+            ckpt_next = checkpoint_hook is not None and nxt in checkpoint_iters
+            step = train_step(state, views, config, group=group,
+                              lookahead=nxt < iterations and not densify_next and not ckpt_next)
+            if (config.densify_start < state.iteration <= densify_until
+                    and state.iteration % config.densify_interval == 0):
+                if world > 1:
+                    from .distributed import reduce_stats_, sync_rng_
+                    reduce_stats_(state.stats, group)
+                    sync_rng_(state, group)
+                report = densify_and_prune(state, config)
+                reports.append(report)
+                if densify_hook:
+                    densify_hook(report)
+            if progress and (state.iteration % eval_interval == 0 or state.iteration == iterations):
+                progress(f"iter={step.iteration} loss={step.loss:.6f} "
+                         f"gaussians={len(state.cloud)} psnr={step.psnr:.2f}")
+            if checkpoint_hook and state.iteration in checkpoint_iters:
+                state.discard_lookahead()
+                checkpoint_hook(state)
+    finally:
+        for pf in _prefetchers.values():
+            pf.clear()
     return reports
 
 

@@ -36,7 +36,7 @@ def test_ctypes_signatures_cover_header():
 
 def test_library_info_calls_without_gpu():
     lib = _lib.load()
-    assert lib.gs_abi_version() == 1
+    assert lib.gs_abi_version() == _lib.ABI_VERSION
     assert lib.gs_status_string(_lib.GS_ERR_ZERO_QUATERNION).decode().startswith("zero-norm")
     buf = ctypes.create_string_buffer(64)
     assert lib.gs_last_cuda_error(buf, 64) == _lib.GS_OK

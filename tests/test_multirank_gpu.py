@@ -188,3 +188,51 @@ def test_multiview_two_streams_matches_one(cuda_device):
     assert torch.equal(s1.accum_count, s2.accum_count)
     assert torch.equal(s1.max_radius_frac, s2.max_radius_frac)
     torch.testing.assert_close(s2.accum_pos_grad, s1.accum_pos_grad, rtol=1e-5, atol=1e-9)
+
+
+def _densify_worker(rank, world, port, out_dir):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch.distributed as dist
+    from paper_2308_04079_b200 import rasterizer as R
+    from paper_2308_04079_b200.camera import Camera
+    from paper_2308_04079_b200.cloud import GaussianCloud
+    from paper_2308_04079_b200.densify import TrainState
+    from paper_2308_04079_b200.optimizer import TrainConfig
+    from paper_2308_04079_b200.training import TrainView, train
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        cloud_np, tgt_np, cam = _scene()
+        tgt = GaussianCloud.from_numpy(**tgt_np)
+        # three views over two ranks: uneven shards (1 and 2 views), so the ranks'
+        # view-sampling RNG streams diverge before the densify step
+        cams = [Camera(np.eye(3), np.array([0.03 * i, -0.02 * i, 0.0]), cam.fx, cam.fy, cam.cx, cam.cy, cam.width,
+                       cam.height, cam.near) for i in range(3)]
+        views = [TrainView(c, R.render_view(tgt, c, (0, 0, 0), 3)[0].image) for c in cams]
+        state = TrainState(GaussianCloud.from_numpy(**cloud_np), 2.0, seed=rank)   # different RNG seeds too
+        cfg = TrainConfig(warmup_upsample_iters=(0, 0), densify_start=0, densify_interval=3,
+                          densify_grad_threshold=2e-6)
+        ckpts = []
+        reports = train(state, views, cfg, iterations=7, checkpoint_hook=lambda s: ckpts.append(
+            (s.iteration, len(s.cloud), getattr(s, "_lookahead", None) is None)), checkpoint_iters=(4, 7))
+        torch.save({"params": {g: getattr(state.cloud, g).cpu() for g in ("means", "sh", "opacity_logits")},
+                    "n": len(state.cloud), "reports": [(r.cloned, r.split, r.pruned) for r in reports],
+                    "ckpts": ckpts}, os.path.join(out_dir, f"dn{rank}.pt"))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_ranks_train_across_densify_stay_identical(cuda_device, tmp_path):
+    """train() under torch.distributed crossing two densify intervals: the
+    statistics are reduced over the ranks and rank 0's RNG is shared, so both
+    replicas clone / split / prune identically and stay bit-identical; the
+    checkpoint hook fires at its iterations with no lookahead pending."""
+    import torch.multiprocessing as mp
+    mp.start_processes(_densify_worker, args=(2, _free_port(), str(tmp_path)), nprocs=2, start_method="spawn")
+    r0, r1 = (torch.load(tmp_path / f"dn{r}.pt") for r in range(2))
+    assert r0["reports"] == r1["reports"] and len(r0["reports"]) == 2
+    assert sum(c + s for c, s, _ in r0["reports"]) > 0   # the densification really cloned / split
+    assert r0["n"] == r1["n"]
+    for k in r0["params"]:
+        assert torch.equal(r0["params"][k], r1["params"][k]), k
+    assert [c[0] for c in r0["ckpts"]] == [4, 7] and all(c[2] for c in r0["ckpts"])

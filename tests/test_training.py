@@ -76,10 +76,11 @@ def test_train_step_recovers_from_capacity_overflow(cuda_device):
     dev = str(state.cloud.device)
     saved = (dict(R._capacity.k), dict(R._capacity.ratio))
     try:
-        R._capacity.k[dev] = max(R._capacity.k.get(dev, 0), 10**8)   # plenty: no overflow
+        key = R._capacity.key(dev, 320, 240)
+        R._capacity.k[key] = 10**8                                   # plenty: no overflow
         ref = train_step(ref_state, [TrainView(cam, target)], cfg)
-        R._capacity.k[dev] = 1024                                    # far too small
-        R._capacity.ratio.pop(dev, None)
+        R._capacity.k[key] = 1024                                    # far too small
+        R._capacity.ratio.pop(key, None)
         rep = train_step(state, [TrainView(cam, target)], cfg)
     finally:
         R._capacity.k.clear(); R._capacity.k.update(saved[0])
@@ -170,3 +171,60 @@ def test_lookahead_matches_plain_steps(cuda_device):
     assert len(sa.cloud) == len(sb.cloud)
     for g in ("means", "rotations", "log_scales", "opacity_logits", "sh"):
         torch.testing.assert_close(getattr(sa.cloud, g), getattr(sb.cloud, g), rtol=1e-3, atol=1e-5)
+
+
+@pytest.mark.gpu
+def test_capacity_retry_with_host_views_and_lookahead(cuda_device):
+    """with host-resident (pinned) views and lookahead, a capacity
+    overflow retry must re-render against THIS view's image, not the buffer the
+    lookahead's prefetch has already refilled with another view."""
+    from paper_2308_04079_b200 import rasterizer as R
+    from paper_2308_04079_b200.camera import Camera
+    from paper_2308_04079_b200.cloud import GaussianCloud
+    from paper_2308_04079_b200.densify import TrainState
+    from paper_2308_04079_b200.optimizer import TrainConfig
+    from paper_2308_04079_b200.training import TrainView, train_step
+    cloud_np, cam = synthetic.frustum_scene(20_000, 256, 160, seed=41)
+    cams = [Camera(np.eye(3), np.array([0.05 * i, 0.0, 0.0]), cam.fx, cam.fy, cam.cx, cam.cy, cam.width, cam.height,
+                   cam.near) for i in range(4)]
+    targets = [R.render_view(GaussianCloud.from_numpy(**synthetic.frustum_scene(20_000, 256, 160, seed=50 + i)[0]),
+                             c, (0, 0, 0), 3)[0].image.cpu().pin_memory() for i, c in enumerate(cams)]
+    views = [TrainView(c, t) for c, t in zip(cams, targets)]
+    cfg = TrainConfig(warmup_upsample_iters=(0, 0))
+    dev = "cuda:0"
+    saved = (dict(R._capacity.k), dict(R._capacity.ratio))
+    runs = []
+    try:
+        for small in (False, True):
+            R._capacity.k.clear(); R._capacity.ratio.clear()
+            R._capacity.k[R._capacity.key(dev, 256, 160)] = 1024 if small else 10**8
+            state = TrainState(GaussianCloud.from_numpy(**cloud_np), 10.0, seed=3)
+            seq = [train_step(state, views, cfg, lookahead=True) for _ in range(4)]
+            state.discard_lookahead()
+            runs.append([(r.view_index, r.loss) for r in seq])
+    finally:
+        R._capacity.k.clear(); R._capacity.k.update(saved[0])
+        R._capacity.ratio.clear(); R._capacity.ratio.update(saved[1])
+    (a, b) = runs
+    assert [v for v, _ in a] == [v for v, _ in b]
+    assert a[0][1] == b[0][1]   # the retried first step saw its own target
+    np.testing.assert_allclose([l for _, l in a], [l for _, l in b], rtol=1e-4)
+
+
+@pytest.mark.gpu
+def test_train_checkpoint_hook(cuda_device):
+    """train(checkpoint_hook, checkpoint_iters) (optimizer.py:398-399)."""
+    from paper_2308_04079_b200 import rasterizer as R
+    from paper_2308_04079_b200.cloud import GaussianCloud
+    from paper_2308_04079_b200.densify import TrainState
+    from paper_2308_04079_b200.optimizer import TrainConfig
+    from paper_2308_04079_b200.training import TrainView, train
+    cloud_np, cam = synthetic.frustum_scene(4_000, 128, 96, seed=61)
+    target = R.render_view(GaussianCloud.from_numpy(**synthetic.frustum_scene(4_000, 128, 96, seed=62)[0]),
+                           cam, (0, 0, 0), 3)[0].image
+    state = TrainState(GaussianCloud.from_numpy(**cloud_np), 10.0, seed=0)
+    seen = []
+    train(state, [TrainView(cam, target)], TrainConfig(warmup_upsample_iters=(0, 0)), iterations=9,
+          checkpoint_hook=lambda s: seen.append((s.iteration, getattr(s, "_lookahead", None) is None)),
+          checkpoint_iters=(3, 9, 12))
+    assert seen == [(3, True), (9, True)]

@@ -26,9 +26,7 @@ def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--n", type=int, default=3_000_000)
     ap.add_argument("--reps", type=int, default=20)
-    ap.add_argument("--bands", action="store_true", help="also time the banded (multi-stream) frame")
     ap.add_argument("--order", action="store_true", help="also time the backward with heavy tiles first")
-    ap.add_argument("--split", action="store_true", help="also time row-split blend launches on 2-4 streams")
     args = ap.parse_args()
     lib = _lib.load()
     cloud_np, cam = synthetic.frustum_scene(args.n, 1920, 1080, seed=0)
@@ -120,78 +118,6 @@ def main() -> None:
                                              tf.data_ptr(), ls.data_ptr(), torch.cuda.current_stream().cuda_stream)
             res[f"blend_fwd_order_{name}_ms"] = timeit(runf)
             res[f"fwd_order_{name}_same"] = bool(torch.equal(img, out.image) and torch.equal(ls, out.last_contributor))
-    if "--bands" in sys.argv:
-        def full_frame():
-            sp = R._project_tensors(cloud.c_params(), len(cloud), "cuda", cam, 3)
-            b = R.bin_and_sort_async(sp, 1920, 1080)
-            R.render_forward(sp, b, 1920, 1080, bg, training=True)
-        res["frame_fwd_full_ms"] = timeit(full_frame)
-        for nb in (2, 3, 4):
-            o, sp, bb = R.render_view_banded(cloud, cam, bg, 3, training=True, bands=nb)
-            try:
-                bb.check()
-            except R.CapacityError:
-                pass
-            res[f"frame_fwd_bands{nb}_ms"] = timeit(lambda: R.render_view_banded(cloud, cam, bg, 3, training=True,
-                                                                                 bands=nb))
-            o, sp, bb = R.render_view_banded(cloud, cam, bg, 3, training=True, bands=nb)
-            res[f"bwd_bands{nb}_ms"] = timeit(lambda: R.render_backward_banded(d, o, sp, bb, 1920, 1080, bg))
-            if nb == 2:
-                # the same banded backward launched on ONE stream (data effect vs concurrency)
-                import ctypes
-                from paper_2308_04079_b200 import _lib
-                lib, cs, bgc = _lib.load(), sp.c_struct(), R._bg(bg)
-                g2 = torch.zeros((len(sp), 12), device="cuda")
-                def one_stream():
-                    g2.zero_()
-                    for (y0, y1), ids in zip(bb.rows, bb.splat_ids):
-                        lib.gs_blend_backward_rows(d.data_ptr(), ctypes.byref(cs), ids.data_ptr(), bb.ranges.data_ptr(),
-                                                   o.final_transmittance.data_ptr(), o.last_contributor.data_ptr(),
-                                                   1920, 1080, y0, y1, bgc, g2.data_ptr(),
-                                                   torch.cuda.current_stream().cuda_stream)
-                res["bwd_bands2_one_stream_ms"] = timeit(one_stream)
-                def full_one_stream():
-                    g2.zero_()
-                    lib.gs_blend_backward_rows(d.data_ptr(), ctypes.byref(splats.c_struct()), binning.splat_ids.data_ptr(),
-                                               binning.ranges.data_ptr(), out.final_transmittance.data_ptr(),
-                                               out.last_contributor.data_ptr(), 1920, 1080, 0, 68, bgc, g2.data_ptr(),
-                                               torch.cuda.current_stream().cuda_stream)
-                res["bwd_full_rows_call_ms"] = timeit(full_one_stream)
-    if "--split" in sys.argv:
-        import ctypes
-        from paper_2308_04079_b200 import _lib
-        lib = _lib.load()
-        cs = splats.c_struct()
-        bgc = R._bg(bg)
-        main = torch.cuda.current_stream()
-
-        def split_launch(fn, parts):
-            ev = torch.cuda.Event()
-            ev.record(main)
-            rows = R.band_rows(68, parts)
-            ss = R._streams("cuda", parts)
-            for (y0, y1), st in zip(rows, ss):
-                st.wait_event(ev)
-                fn(y0, y1, st.cuda_stream)
-            for st in ss:
-                main.wait_stream(st)
-
-        img = torch.empty((1080, 1920, 3), device="cuda")
-        tf = torch.empty((1080, 1920), device="cuda")
-        ls = torch.empty((1080, 1920), dtype=torch.int32, device="cuda")
-        g2 = torch.zeros((len(splats), 12), device="cuda")
-        for parts in (2, 3, 4):
-            res[f"fwd_split{parts}_ms"] = timeit(lambda: split_launch(
-                lambda y0, y1, st: lib.gs_blend_forward_rows(ctypes.byref(cs), binning.splat_ids.data_ptr(),
-                                                             binning.ranges.data_ptr(), 1920, 1080, y0, y1, bgc, 1,
-                                                             img.data_ptr(), tf.data_ptr(), ls.data_ptr(), st),
-                parts))
-            res[f"bwd_split{parts}_ms"] = timeit(lambda: split_launch(
-                lambda y0, y1, st: lib.gs_blend_backward_rows(d.data_ptr(), ctypes.byref(cs),
-                                                              binning.splat_ids.data_ptr(), binning.ranges.data_ptr(),
-                                                              out.final_transmittance.data_ptr(),
-                                                              out.last_contributor.data_ptr(), 1920, 1080, y0, y1,
-                                                              bgc, g2.data_ptr(), st), parts))
     g_ref = R.render_backward(d, out, splats, binning, 1920, 1080, bg).packed
     res["bwd_checksum"] = float(g_ref.double().abs().sum())
     print(json.dumps(res))
