@@ -215,10 +215,13 @@ int gs_bin_and_sort_async(const gs_splats_t* splats, int32_t width, int32_t heig
 /* ---- K6 forward blend: replaces rasterizer.render_forward (rasterizer.py:201-240)
  * image (H,W,3) float32.  When training != 0, t_final (H,W) float32 and
  * last (H,W) int32 (global sorted index of the last blended instance, -1 =
- * none; rasterizer.py:131, 225-231) are written too. */
+ * none; rasterizer.py:131, 225-231) are written too, and every saturation
+ * stop is the reference's float64 decision: pixels whose float32
+ * transmittance is within 1e-4 (relative) of the stop are re-blended in
+ * float64; scratch (training only, else NULL): device int32[2 + W*H]. */
 int gs_blend_forward(const gs_splats_t* splats, const uint32_t* sorted_ids, const int32_t* ranges,
                      int32_t width, int32_t height, const float background[3], int32_t training,
-                     float* image, float* t_final, int32_t* last, void* stream);
+                     float* image, float* t_final, int32_t* last, int32_t* scratch, void* stream);
 
 /* gs_blend_forward with the tiles launched in `tile_order` (nullable; a
  * permutation of [0, tiles), device int32, e.g. the previous backward's
@@ -229,7 +232,7 @@ int gs_blend_forward(const gs_splats_t* splats, const uint32_t* sorted_ids, cons
 int gs_blend_forward_ordered(const gs_splats_t* splats, const uint32_t* sorted_ids, const int32_t* ranges,
                              int32_t width, int32_t height, const float background[3], int32_t training,
                              const int32_t* tile_order, int32_t* tile_work, float* image, float* t_final,
-                             int32_t* last, void* stream);
+                             int32_t* last, int32_t* scratch, void* stream);
 
 /* Longest-first tile order from a per-tile work estimate (1/64-octave
  * buckets, heaviest first).  scratch: device int32[tiles + 2048]. */

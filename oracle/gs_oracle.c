@@ -220,15 +220,23 @@ int or_project(int64_t n, const double* means, const double* rots, const double*
 }
 
 /* ---- binning (rasterizer.py:69-124) ---------------------------------- */
+/* The reference expands every splat into its tiles splat-major (row-major
+ * tiles inside a splat, rasterizer.py:105-111), packs (tile << 32) | float32
+ * depth bits (make_keys, rasterizer.py:55-62) and argsorts stably
+ * (rasterizer.py:113-116).  A stable sort on (tile, depth bits) of that
+ * expansion orders equal keys by splat index, so the result is the
+ * lexicographic (tile, depth bits, index) order.  Restated here in O(N log N
+ * + K): the survivors sorted by (depth bits, index), then a stable counting
+ * sort by tile (keeps large frames — 10^8 instances — tractable on the host). */
 typedef struct {
-  uint64_t key;
+  uint32_t bits;
   int32_t id;
-} inst_t;
+} dk_t;
 
-static int inst_cmp(const void* a, const void* b) {
-  const inst_t* x = (const inst_t*)a;
-  const inst_t* y = (const inst_t*)b;
-  if (x->key != y->key) return x->key < y->key ? -1 : 1;
+static int dk_cmp(const void* a, const void* b) {
+  const dk_t* x = (const dk_t*)a;
+  const dk_t* y = (const dk_t*)b;
+  if (x->bits != y->bits) return x->bits < y->bits ? -1 : 1;
   return x->id < y->id ? -1 : (x->id > y->id);
 }
 
@@ -238,36 +246,52 @@ int64_t or_bin_count(int64_t n, const int64_t* tiles) {
   return k;
 }
 
-/* keys: (tile << 32) | float32(depth) bits (make_keys, rasterizer.py:55-62);
- * ordered by key then Gaussian index, which is the reference's stable order. */
+static uint32_t depth_bits(double depth) {
+  float f = (float)depth; /* rasterizer.py:61: float32 depth */
+  uint32_t bits;
+  memcpy(&bits, &f, 4);
+  return bits;
+}
+
+/* keys (nullable): (tile << 32) | float32(depth) bits per sorted instance;
+ * ids: Gaussian index per sorted instance; ranges: [start, end) per tile,
+ * empty tiles [0, 0] (rasterizer.py:118-123). */
 void or_bin_fill(int64_t n, const int32_t* rect, const int64_t* tiles, const double* depth, int tiles_x,
                  int64_t num_tiles, uint64_t* keys, int32_t* ids, int64_t* ranges) {
-  int64_t k = or_bin_count(n, tiles);
-  inst_t* buf = (inst_t*)malloc((size_t)(k > 0 ? k : 1) * sizeof(inst_t));
+  int64_t m = 0;
+  for (int64_t g = 0; g < n; ++g) m += tiles[g] != 0;
+  dk_t* order = (dk_t*)malloc((size_t)(m > 0 ? m : 1) * sizeof(dk_t));
+  int64_t* cursor = (int64_t*)calloc((size_t)(num_tiles > 0 ? num_tiles : 1), sizeof(int64_t));
   int64_t o = 0;
   for (int64_t g = 0; g < n; ++g) {
     if (tiles[g] == 0) continue;
-    float f = (float)depth[g];
-    uint32_t bits;
-    memcpy(&bits, &f, 4);
+    order[o].bits = depth_bits(depth[g]);
+    order[o].id = (int32_t)g;
+    ++o;
+    for (int ty = rect[4 * g + 1]; ty <= rect[4 * g + 3]; ++ty)
+      for (int tx = rect[4 * g]; tx <= rect[4 * g + 2]; ++tx) cursor[(int64_t)ty * tiles_x + tx] += 1;
+  }
+  qsort(order, (size_t)m, sizeof(dk_t), dk_cmp);
+  int64_t run = 0;
+  for (int64_t t = 0; t < num_tiles; ++t) {
+    const int64_t c = cursor[t];
+    ranges[2 * t] = c ? run : 0;
+    ranges[2 * t + 1] = c ? run + c : 0;
+    cursor[t] = run;
+    run += c;
+  }
+  for (int64_t r = 0; r < m; ++r) {
+    const int64_t g = order[r].id;
     for (int ty = rect[4 * g + 1]; ty <= rect[4 * g + 3]; ++ty)
       for (int tx = rect[4 * g]; tx <= rect[4 * g + 2]; ++tx) {
-        uint64_t tile = (uint64_t)ty * (uint64_t)tiles_x + (uint64_t)tx;
-        buf[o].key = (tile << 32) | bits;
-        buf[o].id = (int32_t)g;
-        ++o;
+        const int64_t t = (int64_t)ty * tiles_x + tx;
+        const int64_t pos = cursor[t]++;
+        ids[pos] = (int32_t)g;
+        if (keys) keys[pos] = ((uint64_t)t << 32) | order[r].bits;
       }
   }
-  qsort(buf, (size_t)k, sizeof(inst_t), inst_cmp);
-  memset(ranges, 0, (size_t)num_tiles * 2 * sizeof(int64_t));
-  for (int64_t i = 0; i < k; ++i) {
-    keys[i] = buf[i].key;
-    ids[i] = buf[i].id;
-    uint64_t t = buf[i].key >> 32;
-    if (i == 0 || (buf[i - 1].key >> 32) != t) ranges[2 * t] = i;
-    if (i == k - 1 || (buf[i + 1].key >> 32) != t) ranges[2 * t + 1] = i + 1;
-  }
-  free(buf);
+  free(cursor);
+  free(order);
 }
 
 /* ---- forward blend (rasterizer.py:152-240), one pixel at a time ---------- */

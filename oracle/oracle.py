@@ -92,17 +92,20 @@ def project(params: dict, camera, degree: int = 3) -> dict:
     return out
 
 
-def bin_and_sort(proj: dict, width: int, height: int) -> dict:
-    """rasterizer.bin_and_sort (rasterizer.py:69-124); ids are Gaussian indices."""
+def bin_and_sort(proj: dict, width: int, height: int, with_keys: bool = True) -> dict:
+    """rasterizer.bin_and_sort (rasterizer.py:69-124); ids are Gaussian indices.
+    with_keys=False skips the (K,) uint64 keys (large frames)."""
     n = proj["radius"].shape[0]
     tx, ty = (width + TILE - 1) // TILE, (height + TILE - 1) // TILE
     k = int(lib().or_bin_count(c_int64(n), _p(proj["tiles"], c_int64)))
-    keys = np.zeros(max(k, 1), np.uint64)
+    keys = np.zeros(max(k, 1), np.uint64) if with_keys else None
     ids = np.zeros(max(k, 1), np.int32)
     ranges = np.zeros((tx * ty, 2), np.int64)
     lib().or_bin_fill(c_int64(n), _p(proj["rect"], c_int32), _p(proj["tiles"], c_int64), _p(proj["depth"]),
-                      c_int(tx), c_int64(tx * ty), _p(keys, ctypes.c_uint64), _p(ids, c_int32), _p(ranges, c_int64))
-    return {"keys": keys[:k], "ids": ids[:k], "ranges": ranges, "tiles_x": tx, "tiles_y": ty}
+                      c_int(tx), c_int64(tx * ty), None if keys is None else _p(keys, ctypes.c_uint64),
+                      _p(ids, c_int32), _p(ranges, c_int64))
+    return {"keys": None if keys is None else keys[:k], "ids": ids[:k], "ranges": ranges, "tiles_x": tx,
+            "tiles_y": ty}
 
 
 def render_forward(proj: dict, bins: dict, width: int, height: int, background) -> dict:

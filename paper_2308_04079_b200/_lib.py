@@ -94,7 +94,7 @@ SIGNATURES = [
     ("gs_bin_and_sort_async", c_int32, [POINTER(GsSplats), c_int32, c_int32, c_void_p, c_size_t, c_int64,
                                         c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     ("gs_blend_forward", c_int32, [POINTER(GsSplats), c_void_p, c_void_p, c_int32, c_int32, POINTER(c_float),
-                                   c_int32, c_void_p, c_void_p, c_void_p, c_void_p]),
+                                   c_int32, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     ("gs_blend_backward", c_int32, [c_void_p, POINTER(GsSplats), c_void_p, c_void_p, c_void_p, c_void_p, c_int32,
                                     c_int32, POINTER(c_float), c_void_p, c_void_p]),
     ("gs_preprocess_backward", c_int32, [POINTER(GsParams), POINTER(GsCamera), c_int32, POINTER(GsSplats),
@@ -110,7 +110,8 @@ SIGNATURES = [
     ("gs_blend_backward_ordered", c_int32, [c_void_p, POINTER(GsSplats), c_void_p, c_void_p, c_void_p, c_void_p,
                                             c_int32, c_int32, POINTER(c_float), c_void_p, c_void_p, c_void_p]),
     ("gs_blend_forward_ordered", c_int32, [POINTER(GsSplats), c_void_p, c_void_p, c_int32, c_int32, POINTER(c_float),
-                                           c_int32, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
+                                           c_int32, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                                           c_void_p]),
     ("gs_tile_schedule", c_int32, [c_void_p, c_int32, c_void_p, c_void_p, c_void_p]),
     ("gs_blend_backward_scheduled", c_int32, [c_void_p, POINTER(GsSplats), c_void_p, c_void_p, c_void_p, c_void_p,
                                               c_int32, c_int32, POINTER(c_float), c_void_p, c_void_p, c_void_p]),

@@ -20,6 +20,17 @@
 // the splat's screen-gradient row: L2 absorbs them (measured 1.39 ms vs
 // 1.45 ms for shared-memory CAS accumulators flushed per (splat, tile)).
 // The terms' constant factors are applied once per reduced value.
+//
+// Conic gradient in the conic's eigenbasis: instead of d_conic (a, b, c) =
+// -1/2 sum dL/dpower (dx^2, 2 dx dy, dy^2) (gradients.py:90-93) the kernel
+// accumulates the moments M = sum dL/dpower (v1^2, v1 v2, v2^2) of the
+// eigenbasis offsets v = K d the exponent is built from (log2(e) power =
+// -|v|^2).  For an elongated conic the x/y sums are dominated by the long
+// axis and carry the short axis' component only to float32 rounding of the
+// large one, which d Sigma' = -A G A then multiplies by cond(A); the moments
+// keep each axis at its own relative precision.  The projection backward
+// forms d Sigma' = 2 / log2(e)^2 K^T M K in float64 (preprocess_bwd.cu);
+// SplatGrads2D.d_conic converts M back to the reference's d_conic.
 #include "gs_common.cuh"
 
 namespace gs {
@@ -48,15 +59,14 @@ constexpr int kThreads = (kConsumerWarps + 1) * 32;
 constexpr int kG = 2;    // splats per reduction group (group_reduce2)
 constexpr int kC = 9;    // gradient components per splat
 // factors applied after the reduction: d_mean2d x/y (2/log2 e), d_alpha,
-// d_conic a, b, c (-1/2, -1, -1/2), colour r, g (colour b = component 8: 1)
-__constant__ float kCompScale[8] = {2.0f / 1.4426950408889634f, 2.0f / 1.4426950408889634f, 1.0f, -0.5f, -1.0f,
-                                    -0.5f, 1.0f, 1.0f};
+// conic moments M11, M12, M22 (1), colour r, g (colour b = component 8: 1)
+__constant__ float kCompScale[8] = {2.0f / 1.4426950408889634f, 2.0f / 1.4426950408889634f, 1.0f, 1.0f, 1.0f,
+                                    1.0f, 1.0f, 1.0f};
 
 struct BwdStage {
   float4 k[kBatch];      // eigenbasis rows (record word 1), see make_tile_splat
   float4 m[kBatch];      // (-k1 . mean_rel, -k2 . mean_rel, alpha, 0)
   float4 col[kBatch];
-  float2 ctr[kBatch];    // mean - tile origin
   uint32_t id[kBatch];
   uint8_t mask[kBatch];
 };
@@ -202,7 +212,8 @@ blend_bwd_kernel(const float* __restrict__ d_image, const float4* __restrict__ r
           if (e < cnt) {
             const float4 r0 = raw->r0[e], k = st.k[e];
             const float alpha = st.col[e].w;
-            make_tile_splat(r0, k, alpha, tile_x0, tile_y0, st.m[e], st.ctr[e]);
+            float2 ctr;
+            make_tile_splat(r0, k, alpha, tile_x0, tile_y0, st.m[e], ctr);
             st.mask[e] = uint8_t(warp_cover_mask<true>(r0, k, alpha, tile_x0, tile_y0) >> (part * kConsumerWarps));
           }
         }
@@ -272,12 +283,10 @@ blend_bwd_kernel(const float* __restrict__ d_image, const float4* __restrict__ r
             v[u * kC + 0] = dp * fmaf(e.v1, kk.x, e.v2 * kk.z);  // d_mean2d.x / (2/log2e)
             v[u * kC + 1] = dp * fmaf(e.v1, kk.y, e.v2 * kk.w);  // d_mean2d.y / (2/log2e)
             v[u * kC + 2] = d_a * e.g;                           // d_alpha
-            const float2 c2 = st.ctr[j];
-            const float dx = lx - c2.x, dy = ly - c2.y;
-            const float dpdx = dp * dx;
-            v[u * kC + 3] = dpdx * dx;                           // d_conic a / (-1/2)
-            v[u * kC + 4] = dpdx * dy;                           // d_conic b / (-1)
-            v[u * kC + 5] = dp * dy * dy;                        // d_conic c / (-1/2)
+            const float dpv1 = dp * e.v1;
+            v[u * kC + 3] = dpv1 * e.v1;                         // conic moment M11
+            v[u * kC + 4] = dpv1 * e.v2;                         // M12
+            v[u * kC + 5] = dp * e.v2 * e.v2;                    // M22
           }
           if (!__any_sync(0xffffffffu, any)) continue;
           float out, out8;

@@ -15,7 +15,11 @@
 // Warps therefore drift apart by up to kStages-1 batches instead of meeting
 // at a CTA barrier after every batch (the v1 kernel's dominant stall).
 // A pixel stops before its accumulated opacity would exceed 0.9999
-// (rasterizer.py:179-180); once every consumer warp is done the CTA stops
+// (rasterizer.py:179-180); in training mode a pixel whose float32 T_new is
+// too close to the threshold to decide (kSatGuard) is re-blended in float64
+// by the tile's consumer warps after the blend (exact_pixel: the
+// reference's stop, T_final and last contributor).  Once every consumer
+// warp is done the CTA stops
 // (rasterizer.py:194-195): the last warp to finish raises s_stop, which the
 // producer and any waiting consumer poll.  gs_blend_forward_ordered launches
 // the tiles in a given order (heaviest first) and can record each tile's work.
@@ -88,6 +92,191 @@ __device__ __forceinline__ void produce_batch(FwdStage& st, RawRec& raw, const f
   }
 }
 
+// ---------------------------------------------------------------------------
+// Exact float64 re-blend of a flagged pixel (training).  The forward appends
+// every pixel whose stop float32 cannot decide (kSatGuard) to a list and
+// stores its float32 last contributor L as last = -3 - L; blend_exact_kernel
+// then re-blends each listed pixel with a whole CTA.  Every candidate up to
+// L was accepted with float32 T_new >= thr (1 + kSatGuard), hence with exact
+// T_new >= thr: those are included exactly when their float64 alpha is > 0
+// (rasterizer.py:171-180; the 1/255 and 0.99 decisions are already the
+// reference's).  Their product and colour are block prefix products over the
+// list prefix; then the candidates after L are visited in order until the
+// exact stop (1 - T_new > 0.9999), as the reference's sequential rule.
+constexpr int kFixThreads = 256, kFixItems = 2, kFixPass = kFixThreads * kFixItems;
+
+struct FixShared {
+  double wscan[kFixThreads / 32];
+  double total;
+  double col[3][kFixThreads / 32];
+  double tail_a[kFixThreads];
+  int stop;
+  int item;
+};
+
+__device__ __forceinline__ void consumer_sync() { __syncthreads(); }
+
+// float64 alpha of one list entry at pixel centre (fx, fy), reference
+// arithmetic (rasterizer.py:171-177); a cheap float32 exclusion skips the
+// exp for entries whose exponent is far below log2(1/255)
+__device__ __forceinline__ double exact_alpha(const float4* __restrict__ rec, uint32_t id, double fx, double fy,
+                                              float4& col) {
+  const float4* r = rec + kRecWords * size_t(id);
+  const float4 r0 = r[0], k = r[1];
+  const float mx = float(fx - double(r0.x)) - r0.z, my = float(fy - double(r0.y)) - r0.w;
+  const float v1 = fmaf(k.x, mx, k.y * my), v2 = fmaf(k.z, mx, k.w * my);
+  if (-(v1 * v1 + v2 * v2) < -8.004f) return 0.0;   // log2(e) power < log2(1/255) - 0.01
+  const float4 r3 = r[3], r4 = r[4];
+  col = r[2];
+  const double dx = fx - (double(r0.x) + double(r0.z));
+  const double dy = fy - (double(r0.y) + double(r0.w));
+  const double ca = double(r3.x) + double(r4.x), cb = double(r3.y) + double(r4.y);
+  const double cc = double(r3.z) + double(r4.z), al = double(col.w) + double(r4.w);
+  const double power = -0.5 * (ca * dx * dx + cc * dy * dy) - cb * dx * dy;
+  const double g = power > 0.0 ? 0.0 : exp(power);
+  const double a = fmin(0.99, al * g);   // ALPHA_CLAMP
+  return a < 1.0 / 255.0 ? 0.0 : a;      // ALPHA_EPS
+}
+
+// exclusive product of v over the consumer threads; *total = the product
+__device__ __forceinline__ double consumer_exclusive_product(double v, FixShared& sh, double* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double incl = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const double t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl *= t;
+  }
+  if (lane == 31) sh.wscan[warp] = incl;
+  consumer_sync();
+  if (threadIdx.x == 0) {
+    double run = 1.0;
+    for (int w = 0; w < kFixThreads / 32; ++w) {
+      const double x = sh.wscan[w];
+      sh.wscan[w] = run;
+      run *= x;
+    }
+    sh.total = run;
+  }
+  consumer_sync();
+  double excl = __shfl_up_sync(0xffffffffu, incl, 1);
+  excl = (lane == 0 ? 1.0 : excl) * sh.wscan[warp];
+  *total = sh.total;
+  consumer_sync();
+  return excl;
+}
+
+__device__ void exact_pixel(const float4* __restrict__ rec, const uint32_t* __restrict__ ids, int2 range, int px,
+                            int py, int last_f32, int width, float3 bg, float* __restrict__ image,
+                            float* __restrict__ t_final, int32_t* __restrict__ last, FixShared& sh) {
+  const double fx = double(px) + 0.5, fy = double(py) + 0.5;   // rasterizer.py:142
+  double T = 1.0, cr = 0.0, cg = 0.0, cb = 0.0;
+  // 1. the accepted prefix [range.x, last_f32]
+  for (int base = range.x; base <= last_f32; base += kFixPass) {
+    double a[kFixItems];
+    float4 col[kFixItems];
+    const int i0 = base + int(threadIdx.x) * kFixItems;
+    double local = 1.0;
+#pragma unroll
+    for (int u = 0; u < kFixItems; ++u) {
+      col[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+      a[u] = i0 + u <= last_f32 ? exact_alpha(rec, ids[i0 + u], fx, fy, col[u]) : 0.0;
+      local *= 1.0 - a[u];
+    }
+    double pass;
+    double tb = T * consumer_exclusive_product(local, sh, &pass);
+#pragma unroll
+    for (int u = 0; u < kFixItems; ++u) {
+      const double w = tb * a[u];
+      cr += w * col[u].x;
+      cg += w * col[u].y;
+      cb += w * col[u].z;
+      tb *= 1.0 - a[u];
+    }
+    T *= pass;
+  }
+  // colour sums
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    cr += __shfl_xor_sync(0xffffffffu, cr, o);
+    cg += __shfl_xor_sync(0xffffffffu, cg, o);
+    cb += __shfl_xor_sync(0xffffffffu, cb, o);
+  }
+  if (lane == 0) {
+    sh.col[0][warp] = cr;
+    sh.col[1][warp] = cg;
+    sh.col[2][warp] = cb;
+  }
+  if (threadIdx.x == 0) sh.stop = 0;
+  consumer_sync();
+  // 2. the candidates after it, in order, until the exact stop (thread 0
+  //    walks each batch's alphas; the float32 stop candidate is the first)
+  double c[3] = {0.0, 0.0, 0.0};
+  if (threadIdx.x == 0)
+    for (int w = 0; w < kFixThreads / 32; ++w)
+      for (int k = 0; k < 3; ++k) c[k] += sh.col[k][w];
+  int lst = last_f32;
+  for (int base = last_f32 + 1; base < range.y; base += kFixThreads) {
+    const int i = base + int(threadIdx.x);
+    float4 col = make_float4(0.f, 0.f, 0.f, 0.f);
+    sh.tail_a[threadIdx.x] = i < range.y ? exact_alpha(rec, ids[i], fx, fy, col) : 0.0;
+    consumer_sync();
+    if (threadIdx.x == 0) {
+      for (int u = 0; u < kFixThreads && base + u < range.y; ++u) {
+        const double a = sh.tail_a[u];
+        if (a <= 0.0) continue;
+        const double t_new = T * (1.0 - a);
+        if ((1.0 - t_new) > 0.9999) {   // SATURATION
+          sh.stop = 1;
+          break;
+        }
+        float4 cc;
+        exact_alpha(rec, ids[base + u], fx, fy, cc);
+        c[0] += T * a * cc.x;
+        c[1] += T * a * cc.y;
+        c[2] += T * a * cc.z;
+        T = t_new;
+        lst = base + u;
+      }
+    }
+    consumer_sync();
+    if (sh.stop) break;
+  }
+  if (threadIdx.x == 0) {
+    const size_t p = size_t(py) * width + px;
+    image[3 * p + 0] = float(c[0] + T * double(bg.x));   // rasterizer.py:197
+    image[3 * p + 1] = float(c[1] + T * double(bg.y));
+    image[3 * p + 2] = float(c[2] + T * double(bg.z));
+    t_final[p] = float(T);
+    last[p] = lst;
+  }
+  consumer_sync();
+}
+
+// Persistent CTAs take the listed pixels one at a time (fix[0] = count,
+// fix[1] = work counter, fix[2 + i] = pixel index).
+__global__ void __launch_bounds__(kFixThreads, 6) blend_exact_kernel(const float4* __restrict__ rec,
+                                                                 const uint32_t* __restrict__ ids,
+                                                                 const int2* __restrict__ ranges, int width,
+                                                                 int tiles_x, float3 bg, float* __restrict__ image,
+                                                                 float* __restrict__ t_final,
+                                                                 int32_t* __restrict__ last, int32_t* fix) {
+  __shared__ FixShared sh;
+  const int count = *reinterpret_cast<volatile int32_t*>(fix);
+  for (;;) {
+    if (threadIdx.x == 0) sh.item = atomicAdd(fix + 1, 1);
+    __syncthreads();
+    const int item = sh.item;
+    __syncthreads();
+    if (item >= count) return;
+    const int64_t q = fix[2 + item];
+    const int px = int(q % width), py = int(q / width);
+    exact_pixel(rec, ids, ranges[(py / kTile) * tiles_x + px / kTile], px, py, -3 - last[q], width, bg, image,
+                t_final, last, sh);
+  }
+}
+
 #ifdef GS_FWD_MIN_BLOCKS
 #define GS_FWD_LB __launch_bounds__(kThreads, GS_FWD_MIN_BLOCKS)
 #else
@@ -98,7 +287,7 @@ __global__ void GS_FWD_LB
 blend_fwd_kernel(const float4* __restrict__ rec, const uint32_t* __restrict__ ids, const int2* __restrict__ ranges,
                  int width, int height, int tiles_x, int tile0, float3 bg, float* __restrict__ image,
                  float* __restrict__ t_final, int32_t* __restrict__ last, const int32_t* __restrict__ tile_order,
-                 int32_t* __restrict__ tile_work) {
+                 int32_t* __restrict__ tile_work, int32_t* __restrict__ fix) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   FwdStage* stages = reinterpret_cast<FwdStage*>(smem_raw);
   RawRec* raw = reinterpret_cast<RawRec*>(smem_raw + sizeof(FwdStage) * kStages);
@@ -156,6 +345,7 @@ blend_fwd_kernel(const float4* __restrict__ rec, const uint32_t* __restrict__ id
   float T = 1.0f;
   float cr = 0.0f, cg = 0.0f, cb = 0.0f;
   int32_t last_idx = -1;
+  float t_stop = 0.0f;    // T_new of the splat the pixel stopped before (training: kSatGuard check)
   bool done = !inside;
   bool warp_done = __all_sync(0xffffffffu, done);
   if (warp_done && lane == 0 && atomicAdd(&s_done, 1) == kConsumerWarps - 1) s_stop = 1;
@@ -185,8 +375,10 @@ blend_fwd_kernel(const float4* __restrict__ rec, const uint32_t* __restrict__ id
           const AlphaEval e = eval_alpha_tile(lx, ly, fx, fy, st.k[j], st.m[j], rec, st.id, j);
           const float t_new = T * (1.0f - e.a);
           const bool blend = !done && e.a > 0.0f;
-          const bool sat = t_new < kTransSat;  // 1 - T_new > 0.9999
-          done = done || (blend && sat);
+          const bool sat = t_new < (kTraining ? kTransSatHi : kTransSat);  // 1 - T_new > 0.9999
+          const bool stopping = blend && sat;
+          done = done || stopping;
+          if (kTraining) t_stop = stopping ? t_new : t_stop;
           if (blend && !sat) {
             const float4 c = st.col[j];
             const float w = T * e.a;
@@ -215,14 +407,19 @@ blend_fwd_kernel(const float4* __restrict__ rec, const uint32_t* __restrict__ id
   image[3 * p + 2] = fmaf(T, bg.z, cb);
   if (kTraining) {
     t_final[p] = T;
-    last[p] = last_idx;
+    if (t_stop >= kTransSatLo) {   // the stop is undecidable in float32: list it for blend_exact_kernel
+      last[p] = -3 - last_idx;
+      fix[2 + atomicAdd(fix, 1)] = int32_t(p);
+    } else {
+      last[p] = last_idx;
+    }
   }
 }
 
 template <bool kTraining>
 int launch(const int32_t* order, int32_t* work, const float4* rec, const uint32_t* ids, const int2* rg, int width, int height,
            int tiles_x, int tile0,
-           int64_t ntiles, float3 bg, float* image, float* t_final, int32_t* last, cudaStream_t s) {
+           int64_t ntiles, float3 bg, float* image, float* t_final, int32_t* last, int32_t* fix, cudaStream_t s) {
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(blend_fwd_kernel<kTraining>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -231,18 +428,25 @@ int launch(const int32_t* order, int32_t* work, const float4* rec, const uint32_
     configured = true;
   }
   if (ntiles <= 0) return GS_OK;
+  if (kTraining) {
+    cudaError_t e = cudaMemsetAsync(fix, 0, 2 * sizeof(int32_t), s);
+    if (e != cudaSuccess) return record_cuda_error(e);
+  }
   blend_fwd_kernel<kTraining><<<unsigned(ntiles * kParts), kThreads, kSmemBytes, s>>>(rec, ids, rg, width, height, tiles_x,
                                                                              tile0, bg, image, t_final, last,
-                                                                             order, work);
+                                                                             order, work, fix);
+  int st = check_launch();
+  if (st != GS_OK || !kTraining) return st;
+  blend_exact_kernel<<<148 * 6, kFixThreads, 0, s>>>(rec, ids, rg, width, tiles_x, bg, image, t_final, last, fix);
   return check_launch();
 }
 
 int blend_forward_rows(const gs_splats_t* splats, const uint32_t* sorted_ids, const int32_t* ranges, int32_t width,
                        int32_t height, int32_t row_begin, int32_t row_end, const float background[3],
-                       int32_t training, float* image, float* t_final, int32_t* last, void* stream,
+                       int32_t training, float* image, float* t_final, int32_t* last, int32_t* scratch, void* stream,
                        const int32_t* tile_order = nullptr, int32_t* tile_work = nullptr) {
   if (!splats || !ranges || !image || !background || width <= 0 || height <= 0) return GS_ERR_INVALID_ARG;
-  if (training && (!t_final || !last)) return GS_ERR_INVALID_ARG;
+  if (training && (!t_final || !last || !scratch)) return GS_ERR_INVALID_ARG;
   const int tiles_x = (width + kTile - 1) / kTile, tiles_y = (height + kTile - 1) / kTile;
   const int64_t tiles = int64_t(tiles_x) * tiles_y;
   if (tiles > int64_t(INT32_MAX)) return GS_ERR_RESOURCE_LIMIT;
@@ -254,8 +458,10 @@ int blend_forward_rows(const gs_splats_t* splats, const uint32_t* sorted_ids, co
   const int tile0 = row_begin * tiles_x;
   const int64_t ntiles = int64_t(row_end - row_begin) * tiles_x;
   if (training)
-    return launch<true>(tile_order, tile_work, rec, sorted_ids, rg, width, height, tiles_x, tile0, ntiles, bg, image, t_final, last, s);
-  return launch<false>(tile_order, tile_work, rec, sorted_ids, rg, width, height, tiles_x, tile0, ntiles, bg, image, nullptr, nullptr, s);
+    return launch<true>(tile_order, tile_work, rec, sorted_ids, rg, width, height, tiles_x, tile0, ntiles, bg, image,
+                        t_final, last, scratch, s);
+  return launch<false>(tile_order, tile_work, rec, sorted_ids, rg, width, height, tiles_x, tile0, ntiles, bg, image,
+                       nullptr, nullptr, nullptr, s);
 }
 
 }  // namespace
@@ -263,10 +469,10 @@ int blend_forward_rows(const gs_splats_t* splats, const uint32_t* sorted_ids, co
 
 extern "C" int gs_blend_forward(const gs_splats_t* splats, const uint32_t* sorted_ids, const int32_t* ranges,
                                 int32_t width, int32_t height, const float background[3], int32_t training,
-                                float* image, float* t_final, int32_t* last, void* stream) {
+                                float* image, float* t_final, int32_t* last, int32_t* scratch, void* stream) {
   if (width <= 0 || height <= 0) return GS_ERR_INVALID_ARG;
   return gs::blend_forward_rows(splats, sorted_ids, ranges, width, height, 0, (height + gs::kTile - 1) / gs::kTile,
-                                background, training, image, t_final, last, stream);
+                                background, training, image, t_final, last, scratch, stream);
 }
 
 // The full frame with the tiles visited in `tile_order` (a permutation of
@@ -274,8 +480,8 @@ extern "C" int gs_blend_forward(const gs_splats_t* splats, const uint32_t* sorte
 extern "C" int gs_blend_forward_ordered(const gs_splats_t* splats, const uint32_t* sorted_ids, const int32_t* ranges,
                                         int32_t width, int32_t height, const float background[3], int32_t training,
                                         const int32_t* tile_order, int32_t* tile_work, float* image, float* t_final,
-                                        int32_t* last, void* stream) {
+                                        int32_t* last, int32_t* scratch, void* stream) {
   if (height <= 0) return GS_ERR_INVALID_ARG;
   return gs::blend_forward_rows(splats, sorted_ids, ranges, width, height, 0, (height + gs::kTile - 1) / gs::kTile,
-                                background, training, image, t_final, last, stream, tile_order, tile_work);
+                                background, training, image, t_final, last, scratch, stream, tile_order, tile_work);
 }

@@ -25,6 +25,17 @@ constexpr float kAlphaClamp = 0.99f;            // rasterizer.py:18 ALPHA_CLAMP
 // T_new < 1 - 0.9999 so float32 keeps full relative precision near T = 1e-4
 // (1.0f - T would quantise T to ulp(1) = 6e-8, i.e. 6e-4 relative).
 constexpr float kTransSat = float(1.0 - 0.9999);
+// Saturation guard (training forward): the float32 transmittance differs
+// from the float64 reference's by ~sum_i eps_a a_i / (1 - a_i) relative
+// (float32 alphas are ~1e-7..2e-6 relative off, the 1/255 and 0.99
+// decisions are exact), ~1e-5 at the stop for realistic alpha mixes.  A
+// pixel whose T_new lands within kSatGuard (relative) of the threshold is
+// flagged (last = kLastPending) and re-blended exactly in float64 by the
+// fix-up kernel, so every stop decision is the reference's.
+constexpr float kSatGuard = 1e-4f;
+constexpr float kTransSatLo = kTransSat * (1.0f - kSatGuard);
+constexpr float kTransSatHi = kTransSat * (1.0f + kSatGuard);
+constexpr int32_t kLastPending = -2;
 constexpr int64_t kMaxInstances = int64_t(1) << 31;    // rasterizer.py:25
 constexpr int64_t kMaxTiles = (int64_t(1) << 32) - 1;  // rasterizer.py:24
 

@@ -21,7 +21,8 @@ namespace {
 // Per-Gaussian inputs, loaded before the block's SH staging so their
 // latency overlaps it.
 struct GradInputs {
-  float4 ga, gb, gc;   // grads2d row: (d_mx, d_my, d_alpha), (d_ca, d_cb, d_cc), (d_r, d_g, d_b)
+  float4 ga, gb, gc;   // grads2d row: (d_mx, d_my, d_alpha), conic moments (M11, M12, M22), (d_r, d_g, d_b)
+  float4 k;            // the conic's eigenbasis rows (record word 1) the blends built the exponent from
   float4 q;            // raw quaternion
   float m0, m1, m2, l0, l1, l2, op, mask;
 };
@@ -32,6 +33,7 @@ __device__ __forceinline__ void load_inputs(const gs_params_t& p, const float4* 
   in.gb = __ldg(g2d + 3 * g + 1);
   in.gc = __ldg(g2d + 3 * g + 2);
   in.mask = __ldg(rec + kRecWords * g + 3).w;
+  in.k = __ldg(rec + kRecWords * g + 1);
   in.q = __ldg(reinterpret_cast<const float4*>(p.rotations) + g);
   in.m0 = __ldg(p.means + 3 * g + 0); in.m1 = __ldg(p.means + 3 * g + 1); in.m2 = __ldg(p.means + 3 * g + 2);
   in.l0 = __ldg(p.log_scales + 3 * g + 0); in.l1 = __ldg(p.log_scales + 3 * g + 1);
@@ -119,21 +121,20 @@ __device__ __forceinline__ void grad_one_t(const GradInputs& in, const DevCamera
   for (int r = 0; r < 2; ++r)
 #pragma unroll
     for (int k = 0; k < 3; ++k) US[3 * r + k] = U[3 * r + 0] * S[k] + U[3 * r + 1] * S[3 + k] + U[3 * r + 2] * S[6 + k];
-  const Real ca = US[0] * U[0] + US[1] * U[1] + US[2] * U[2] + Real(kLowpass);
-  const Real cb = US[0] * U[3] + US[1] * U[4] + US[2] * U[5];
-  const Real cc = US[3] * U[3] + US[4] * U[4] + US[5] * U[5] + Real(kLowpass);
-  const Real det = ca * cc - cb * cb;
-  const Real inv_det = Real(1.0) / det;
-  const Real A0 = cc * inv_det, A1 = -cb * inv_det, A2 = ca * inv_det;  // conic (core.py:316)
-
-  // --- conic -> floored screen covariance: dS' = -A G A (gradients.py:97-113)
-  const Real G0 = gb.x, G1 = Real(0.5) * Real(gb.y), G2 = gb.z;
-  const Real AG00 = A0 * G0 + A1 * G1, AG01 = A0 * G1 + A1 * G2;
-  const Real AG10 = A1 * G0 + A2 * G1, AG11 = A1 * G1 + A2 * G2;
-  const Real dC00 = -(AG00 * A0 + AG01 * A1);
-  const Real dC01 = -(AG00 * A1 + AG01 * A2);
-  const Real dC10 = -(AG10 * A0 + AG11 * A1);
-  const Real dC11 = -(AG10 * A1 + AG11 * A2);
+  // --- conic moments -> floored screen covariance.  The reference forms
+  //     d_conic = -1/2 sum dp d d^T and dS' = -A G A (gradients.py:97-113);
+  //     with d = K^-1 v and A = 2 / log2(e) K^T K (the blends' exponent,
+  //     gs_common.cuh: conic_basis) that is dS' = 2 / log2(e)^2 K^T M K,
+  //     which never mixes the axes' magnitudes (see blend_bwd.cu).
+  const Real k1x = in.k.x, k1y = in.k.y, k2x = in.k.z, k2y = in.k.w;
+  const Real M11 = gb.x, M12 = gb.y, M22 = gb.z;
+  const Real P1x = M11 * k1x + M12 * k2x, P1y = M11 * k1y + M12 * k2y;
+  const Real P2x = M12 * k1x + M22 * k2x, P2y = M12 * k1y + M22 * k2y;
+  const Real cm = Real(2.0 / (1.4426950408889634 * 1.4426950408889634));
+  const Real dC00 = cm * (k1x * P1x + k2x * P2x);
+  const Real dC01 = cm * (k1x * P1y + k2x * P2y);
+  const Real dC10 = dC01;
+  const Real dC11 = cm * (k1y * P1y + k2y * P2y);
 
   // --- screen covariance -> world covariance: dSigma = U^T dS' U (gradients.py:116-123)
   Real dCU[6];  // dS' U  (2x3)

@@ -36,16 +36,25 @@ def shard_views(num_views: int, world: int, rank: int) -> list[int]:
     return list(range(lo, hi))
 
 
+def _seg(numel: int) -> int:
+    """Segment length padded to 64 floats (256 B), so every group of a flat
+    bucket starts 16-byte aligned for the kernels' vector accesses whatever
+    the Gaussian count."""
+    return -(-numel // 64) * 64
+
+
 class GradientBucket:
-    """One flat float32 buffer with GaussianGrads views into it."""
+    """One flat float32 buffer with GaussianGrads views into it (one padded,
+    aligned segment per parameter group)."""
 
     def __init__(self, n: int, device, dtype=torch.float32):
         self.n = n
-        self.flat = torch.zeros(n * FLOATS_PER_GAUSSIAN, dtype=dtype, device=device)
-        parts = torch.split(self.flat, [n * w for _, w in GROUP_WIDTHS])
+        segs = [_seg(n * w) for _, w in GROUP_WIDTHS]
+        self.flat = torch.zeros(sum(segs), dtype=dtype, device=device)
+        parts = torch.split(self.flat, segs)
         shapes = {"d_means": (n, 3), "d_rotations": (n, 4), "d_log_scales": (n, 3), "d_opacity_logits": (n,),
                   "d_sh": (n, 16, 3)}
-        views = {name: part.view(shapes[name]) for (name, _), part in zip(GROUP_WIDTHS, parts)}
+        views = {name: part[:n * w].view(shapes[name]) for (name, w), part in zip(GROUP_WIDTHS, parts)}
         self.grads = GaussianGrads(views["d_means"], views["d_rotations"], views["d_log_scales"],
                                    views["d_opacity_logits"], views["d_sh"],
                                    torch.zeros(n, dtype=dtype, device=device))
@@ -192,9 +201,11 @@ class ShardedAdam:
             self.pbuf[g] = buf
         # gradient bucket: one padded segment per group, contiguous in one flat buffer
         widths = [math.prod(_ROW_SHAPE[g]) for g in PARAM_GROUPS]
-        self.flat = torch.zeros(npad * sum(widths), **z)
-        parts = torch.split(self.flat, [npad * w for w in widths])
-        self.gbuf = {g: part.view((npad,) + _ROW_SHAPE[g]) for g, part in zip(PARAM_GROUPS, parts)}
+        segs = [_seg(npad * w) for w in widths]
+        self.flat = torch.zeros(sum(segs), **z)
+        parts = torch.split(self.flat, segs)
+        self.gbuf = {g: part[:npad * w].view((npad,) + _ROW_SHAPE[g]) for g, w, part in zip(PARAM_GROUPS, widths,
+                                                                                             parts)}
         self.grads = GaussianGrads(*(self.gbuf[g][:n] for g in ("means", "rotations", "log_scales",
                                                                    "opacity_logits", "sh")),
                                    torch.zeros(n, **z))

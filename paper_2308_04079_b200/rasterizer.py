@@ -216,12 +216,18 @@ class RenderOutput:
 
 @dataclass
 class SplatGrads2D:
-    """Screen-space gradients (rasterizer.py:243-250) in the packed (N,12) row."""
+    """Screen-space gradients (rasterizer.py:243-250) in the packed (N,12) row:
+    [0:2] d_mean2d, [2] d_alpha, [4:7] the conic moments M = sum dL/dpower
+    (v1^2, v1 v2, v2^2) over the eigenbasis offsets v = K (pixel - mean) the
+    blends evaluate the exponent from (log2(e) power = -|v|^2; K = record
+    words 4:8), [8:11] d_color.  d_conic converts M to the reference's
+    d_conic = -1/2 sum dL/dpower (dx^2, 2 dx dy, dy^2) (gradients.py:90-93)."""
 
     packed: torch.Tensor  # (N,12) float32
     # the longest-first tile schedule the backward ran on (int32 (T,)), a good
     # launch order for the next forward of the same view (render_forward)
     tile_order: torch.Tensor | None = None
+    rec: torch.Tensor | None = None   # the splats' records (for d_conic)
 
     @property
     def d_mean2d(self) -> torch.Tensor:
@@ -232,8 +238,29 @@ class SplatGrads2D:
         return self.packed[:, 2]
 
     @property
-    def d_conic(self) -> torch.Tensor:
+    def conic_moments(self) -> torch.Tensor:
         return self.packed[:, 4:7]
+
+    @property
+    def d_conic(self) -> torch.Tensor:
+        """(N,3) float64 d_conic (a, b, c): Q = K^-1 M K^-T, d_conic =
+        (-Q_xx / 2, -Q_xy, -Q_yy / 2)."""
+        if self.rec is None:
+            raise ValueError("d_conic needs the splats' records (SplatGrads2D.rec)")
+        m = self.packed[:, 4:7].double()
+        k = self.rec[:, 4:8].double()
+        det = k[:, 0] * k[:, 3] - k[:, 1] * k[:, 2]
+        ok = (det != 0) & (m != 0).any(dim=1)
+        inv = torch.where(ok, 1.0 / torch.where(ok, det, torch.ones_like(det)), torch.zeros_like(det))
+        # K^-1 = [[k2y, -k1y], [-k2x, k1x]] / det
+        a, b = k[:, 3] * inv, -k[:, 1] * inv
+        c, d = -k[:, 2] * inv, k[:, 0] * inv
+        m11, m12, m22 = m[:, 0], m[:, 1], m[:, 2]
+        qxx = a * (a * m11 + b * m12) + b * (a * m12 + b * m22)
+        qxy = a * (c * m11 + d * m12) + b * (c * m12 + d * m22)
+        qyy = c * (c * m11 + d * m12) + d * (c * m12 + d * m22)
+        out = torch.stack([-0.5 * qxx, -qxy, -0.5 * qyy], dim=1)
+        return torch.where(ok[:, None], out, torch.zeros_like(out))   # culled rows: records undefined
 
     @property
     def d_color(self) -> torch.Tensor:
@@ -441,6 +468,8 @@ def render_forward(splats: DeviceSplats, binning: TileBinning, width: int, heigh
     image = torch.empty((height, width, 3), dtype=torch.float32, device=device)
     t_final = torch.empty((height, width), dtype=torch.float32, device=device) if training else None
     last = torch.empty((height, width), dtype=torch.int32, device=device) if training else None
+    # exact-stop re-blend list (training): count, work counter, pixel indices
+    scratch = torch.empty(2 + width * height, dtype=torch.int32, device=device) if training else None
     cs = splats.c_struct()
     tx, ty = tile_extent(width, height)
     if tile_order is not None and (tile_order.numel() != tx * ty or tile_order.device != device):
@@ -451,12 +480,14 @@ def render_forward(splats: DeviceSplats, binning: TileBinning, width: int, heigh
         _lib.check(lib.gs_blend_forward_ordered(ctypes.byref(cs), binning.splat_ids.data_ptr(),
                                                 binning.ranges.data_ptr(), width, height, _bg(background),
                                                 int(bool(training)), _lib.ptr(tile_order), _lib.ptr(tile_work),
-                                                image.data_ptr(), _lib.ptr(t_final), _lib.ptr(last), _stream()),
+                                                image.data_ptr(), _lib.ptr(t_final), _lib.ptr(last), _lib.ptr(scratch),
+                                                _stream()),
                    "render_forward")
     else:
         _lib.check(lib.gs_blend_forward(ctypes.byref(cs), binning.splat_ids.data_ptr(), binning.ranges.data_ptr(),
                                         width, height, _bg(background), int(bool(training)), image.data_ptr(),
-                                        _lib.ptr(t_final), _lib.ptr(last), _stream()), "render_forward")
+                                        _lib.ptr(t_final), _lib.ptr(last), _lib.ptr(scratch), _stream()),
+                   "render_forward")
     return RenderOutput(image, t_final, last)
 
 
@@ -479,13 +510,13 @@ def render_backward(d_image: torch.Tensor, output: RenderOutput, splats: DeviceS
             d_image.data_ptr(), ctypes.byref(cs), binning.splat_ids.data_ptr(), binning.ranges.data_ptr(),
             output.final_transmittance.data_ptr(), output.last_contributor.data_ptr(), width, height,
             _bg(background), scratch.data_ptr(), packed.data_ptr(), _stream()), "render_backward")
-        return SplatGrads2D(packed, scratch[:tx * ty])
+        return SplatGrads2D(packed, scratch[:tx * ty], splats.rec)
     else:
         _lib.check(lib.gs_blend_backward(d_image.data_ptr(), ctypes.byref(cs), binning.splat_ids.data_ptr(),
                                          binning.ranges.data_ptr(), output.final_transmittance.data_ptr(),
                                          output.last_contributor.data_ptr(), width, height, _bg(background),
                                          packed.data_ptr(), _stream()), "render_backward")
-    return SplatGrads2D(packed)
+    return SplatGrads2D(packed, None, splats.rec)
 
 
 _BWD_SCHEDULE = __import__("os").environ.get("GS_BWD_SCHEDULE", "1") != "0"

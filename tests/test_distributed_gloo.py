@@ -68,8 +68,11 @@ def test_gradient_bucket_and_stats_allreduce_world2():
 
 def test_bucket_layout():
     b = GradientBucket(7, "cpu")
-    assert b.flat.numel() == 7 * FLOATS_PER_GAUSSIAN == 7 * 59
+    assert FLOATS_PER_GAUSSIAN == 59 and b.flat.numel() >= 7 * FLOATS_PER_GAUSSIAN
     assert b.grads.d_sh.shape == (7, 16, 3) and b.grads.d_rotations.shape == (7, 4)
+    # every group view starts 16-byte aligned whatever N (the kernels use vector accesses)
+    for t in (b.grads.d_means, b.grads.d_rotations, b.grads.d_log_scales, b.grads.d_opacity_logits, b.grads.d_sh):
+        assert t.data_ptr() % 16 == 0 and t.is_contiguous()
     b.grads.d_sh.fill_(1.0)
     assert float(b.flat.sum()) == 7 * 48
 

@@ -1,7 +1,7 @@
 """GPU parity at benchmark scale (SURVEY §8(c) "parity at scale").
 
 * 300K-Gaussian frustum scene at 1920x1080 against the float64 oracle: bit-exact
-  radii / ids / ranges, image within tolerance with saturation flips attributed.
+  radii / ids / ranges, last contributor exact, image within tolerance.
 * c2 (1M, 1080p) and c5 (6M, 3840x2160): size-independent invariants of the
   binning (ranges partition the instances; per-tile (depth, id) order; every
   Gaussian appears exactly tiles_touched times, each time in a tile of its

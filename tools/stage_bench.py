@@ -112,10 +112,12 @@ def main() -> None:
             img = torch.empty_like(out.image)
             tf = torch.empty_like(out.final_transmittance)
             ls = torch.empty_like(out.last_contributor)
+            fx = torch.empty(2 + 1920 * 1080, dtype=torch.int32, device="cuda")
             def runf():
                 lib.gs_blend_forward_ordered(ctypes.byref(cs), binning.splat_ids.data_ptr(), binning.ranges.data_ptr(),
                                              1920, 1080, bgc, 1, order.data_ptr(), None, img.data_ptr(),
-                                             tf.data_ptr(), ls.data_ptr(), torch.cuda.current_stream().cuda_stream)
+                                             tf.data_ptr(), ls.data_ptr(), fx.data_ptr(),
+                                             torch.cuda.current_stream().cuda_stream)
             res[f"blend_fwd_order_{name}_ms"] = timeit(runf)
             res[f"fwd_order_{name}_same"] = bool(torch.equal(img, out.image) and torch.equal(ls, out.last_contributor))
     g_ref = R.render_backward(d, out, splats, binning, 1920, 1080, bg).packed
