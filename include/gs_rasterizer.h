@@ -265,6 +265,21 @@ int gs_blend_backward_scheduled(const float* d_image, const gs_splats_t* splats,
                                 int32_t height, const float background[3], int32_t* scratch, float* grads2d,
                                 void* stream);
 
+/* Deterministic backward blend (the reference's deterministic=True /
+ * workers=1 contract, rasterizer.py:32-41: bit-identical runs): no float
+ * atomics — one partial row per (sorted instance, half tile), summed per
+ * splat in a fixed order (its tiles row-major, rasterizer.py:105-111).
+ * grads2d is fully written (no clearing needed).  tile_order nullable.
+ * workspace: gs_blend_backward_det_workspace_size(n, W, H, k_capacity)
+ * bytes, k_capacity >= K (the instance buffers' length). */
+int gs_blend_backward_det_workspace_size(int64_t n, int32_t width, int32_t height, int64_t k_capacity,
+                                         size_t* bytes);
+int gs_blend_backward_deterministic(const float* d_image, const gs_splats_t* splats, const uint32_t* sorted_ids,
+                                    const int32_t* ranges, const float* t_final, const int32_t* last,
+                                    int32_t width, int32_t height, const float background[3],
+                                    const int32_t* tile_order, void* workspace, size_t workspace_bytes,
+                                    int64_t k_capacity, float* grads2d, void* stream);
+
 /* ---- K8 backward preprocess: replaces gradients.backward_project
  * (gradients.py:192-259) and the densification statistics update of
  * train_step (optimizer.py:252-255).  accumulate = 0 overwrites `grads`

@@ -74,6 +74,32 @@ struct RawRec {          // the producer's landing buffer for the cp.async gathe
   float4 r0[kBatch];
 };
 constexpr size_t kSmemBytes = sizeof(BwdStage) * kStages + sizeof(RawRec);
+// deterministic mode: per stage, each consumer warp's reduced partials
+// [warp][slot][component], combined by the producer in warp order
+struct DetPart {
+  float v[kConsumerWarps][kBatch][kC];
+};
+constexpr size_t kSmemBytesDet = kSmemBytes + sizeof(DetPart) * kStages;
+
+// deterministic mode: the producer sums the released stage's warp partials
+// in warp order into the per-instance rows part_out[pos][tile part][kC]
+// (one row per (sorted instance, half tile)), and clears them.
+__device__ __forceinline__ void det_flush(DetPart& dp, int lo, int cnt, int part, float* __restrict__ part_out,
+                                          int lane) {
+  for (int e = lane; e < cnt; e += 32) {
+    float* row = part_out + (size_t(lo + e) * kParts + part) * kC;
+#pragma unroll
+    for (int c = 0; c < kC; ++c) {
+      float acc = 0.0f;
+#pragma unroll
+      for (int w = 0; w < kConsumerWarps; ++w) {
+        acc += dp.v[w][e][c];
+        dp.v[w][e][c] = 0.0f;
+      }
+      row[c] = acc;
+    }
+  }
+}
 
 // Two-splat variant: sum v[0..17] over the warp.  On return lane l holds, in
 // `out`, component ((l >> 1) & 7) of splat (l >> 4) (lanes l and l^1 hold the
@@ -120,14 +146,21 @@ __device__ __forceinline__ void batch_bounds(int b, int tile_top, int range_lo, 
   cnt = top - lo;
 }
 
-__global__ void __launch_bounds__(kThreads, GS_BWD_MIN_BLOCKS)
+// kDet: no float atomics; every (instance, half tile) gets its own partial
+// row, summed in a fixed order per splat afterwards (det_reduce_kernel), so
+// runs are bit-identical (the reference's deterministic=True,
+// rasterizer.py:32-41).  top_out[tile * kParts + part] = the CTA's last
+// processed sorted position + 1 (rows at or above it are never written).
+template <bool kDet>
+__global__ void __launch_bounds__(kThreads, kDet ? 3 : GS_BWD_MIN_BLOCKS)
 blend_bwd_kernel(const float* __restrict__ d_image, const float4* __restrict__ rec, const uint32_t* __restrict__ ids,
                  const int2* __restrict__ ranges, const float* __restrict__ t_final, const int32_t* __restrict__ last,
                  int width, int height, int tiles_x, int tile0, float3 bg, float4* __restrict__ grads2d,
-                 const int32_t* __restrict__ tile_order) {
+                 const int32_t* __restrict__ tile_order, float* __restrict__ part_out, int32_t* __restrict__ top_out) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   BwdStage* stages = reinterpret_cast<BwdStage*>(smem_raw);
   RawRec* raw = reinterpret_cast<RawRec*>(smem_raw + sizeof(BwdStage) * kStages);
+  DetPart* dparts = reinterpret_cast<DetPart*>(smem_raw + kSmemBytes);
   __shared__ uint64_t full_bar[kStages], empty_bar[kStages];
   __shared__ int s_warp_max[kConsumerWarps + 1];
 
@@ -159,6 +192,7 @@ blend_bwd_kernel(const float* __restrict__ d_image, const float4* __restrict__ r
   }
   // a tile with an all-zero gradient contributes nothing (rasterizer.py:286-287)
   const bool nonzero = (dlx != 0.0f) || (dly != 0.0f) || (dlz != 0.0f);
+  if (kDet && t == 0) top_out[tile * kParts + part] = range.x;   // nothing written (yet)
   if (!__syncthreads_or(nonzero)) return;
   // needed = max(last_local) + 1 (gradients.py:48-52)
   const int warp_last = __reduce_max_sync(0xffffffffu, last_idx);
@@ -176,12 +210,22 @@ blend_bwd_kernel(const float* __restrict__ d_image, const float4* __restrict__ r
   if (tile_last < range.x) return;
   const int tile_top = tile_last + 1;
   const int nb = (tile_top - range.x + kBatch - 1) / kBatch;
+  if (kDet && t == 0) top_out[tile * kParts + part] = tile_top;
 
   if (!consumer) {  // ---------------- producer warp
+    if (kDet)
+      for (int i = lane; i < int(sizeof(DetPart) * kStages / sizeof(float)); i += 32)
+        reinterpret_cast<float*>(dparts)[i] = 0.0f;
     for (int b = 0; b < nb; ++b) {
       const int s = b % kStages;
       if (b >= kStages) {
         while (!mbar_try_wait_sleep(&empty_bar[s], uint32_t((b / kStages) - 1) & 1u, GS_WAIT_NS)) {
+        }
+        if (kDet) {   // batch b - kStages is complete: its rows, in warp order
+          int plo, pcnt;
+          batch_bounds(b - kStages, tile_top, range.x, plo, pcnt);
+          det_flush(dparts[s], plo, pcnt, part, part_out, lane);
+          __syncwarp();
         }
       }
       {
@@ -220,6 +264,15 @@ blend_bwd_kernel(const float* __restrict__ d_image, const float4* __restrict__ r
         mbar_arrive(&full_bar[s]);
       }
     }
+    if (kDet)   // the last kStages batches
+      for (int b = max(nb - kStages, 0); b < nb; ++b) {
+        const int s = b % kStages;
+        while (!mbar_try_wait_sleep(&empty_bar[s], uint32_t(b / kStages) & 1u, GS_WAIT_NS)) {
+        }
+        int plo, pcnt;
+        batch_bounds(b, tile_top, range.x, plo, pcnt);
+        det_flush(dparts[s], plo, pcnt, part, part_out, lane);
+      }
     return;
   }
 
@@ -294,10 +347,15 @@ blend_bwd_kernel(const float* __restrict__ d_image, const float4* __restrict__ r
           const int j = (lane & 16) ? js[1] : js[0];
           const int comp = (lane >> 1) & 7;
           if (j >= 0 && (lane & 1) == 0) {
-            // fire-and-forget reductions into the (N,12) screen-gradient rows
-            float* row = reinterpret_cast<float*>(grads2d) + 12 * size_t(st.id[j]);
-            atomicAdd(row + comp + comp / 3, out * comp_scale);
-            if (comp == 0) atomicAdd(row + 10, out8);
+            if (kDet) {   // this warp's partial, combined in warp order by the producer
+              dparts[s].v[warp][j][comp] = out * comp_scale;
+              if (comp == 0) dparts[s].v[warp][j][8] = out8;
+            } else {
+              // fire-and-forget reductions into the (N,12) screen-gradient rows
+              float* row = reinterpret_cast<float*>(grads2d) + 12 * size_t(st.id[j]);
+              atomicAdd(row + comp + comp / 3, out * comp_scale);
+              if (comp == 0) atomicAdd(row + 10, out8);
+            }
           }
         }
       }
@@ -310,7 +368,8 @@ blend_bwd_kernel(const float* __restrict__ d_image, const float4* __restrict__ r
 int blend_backward_rows(const float* d_image, const gs_splats_t* splats, const uint32_t* sorted_ids,
                         const int32_t* ranges, const float* t_final, const int32_t* last, int32_t width,
                         int32_t height, int32_t row_begin, int32_t row_end, const float background[3],
-                        float* grads2d, void* stream, const int32_t* tile_order = nullptr) {
+                        float* grads2d, void* stream, const int32_t* tile_order = nullptr,
+                        float* part_out = nullptr, int32_t* top_out = nullptr) {
   if (!d_image || !splats || !ranges || !t_final || !last || !grads2d || !background || width <= 0 ||
       height <= 0)
     return GS_ERR_INVALID_ARG;
@@ -321,17 +380,26 @@ int blend_backward_rows(const float* d_image, const gs_splats_t* splats, const u
   if (splats->n == 0 || row_begin == row_end) return GS_OK;
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(blend_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(blend_bwd_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          int(kSmemBytes));
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(blend_bwd_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               int(kSmemBytesDet));
     if (e != cudaSuccess) return record_cuda_error(e);
     configured = true;
   }
   const float3 bg = make_float3(background[0], background[1], background[2]);
   const int64_t ntiles = int64_t(row_end - row_begin) * tiles_x;
-  blend_bwd_kernel<<<unsigned(ntiles * kParts), kThreads, kSmemBytes, static_cast<cudaStream_t>(stream)>>>(
-      d_image, reinterpret_cast<const float4*>(splats->rec), sorted_ids, reinterpret_cast<const int2*>(ranges),
-      t_final, last, width, height, tiles_x, row_begin * tiles_x, bg, reinterpret_cast<float4*>(grads2d),
-      tile_order);
+  if (part_out)
+    blend_bwd_kernel<true><<<unsigned(ntiles * kParts), kThreads, kSmemBytesDet, static_cast<cudaStream_t>(stream)>>>(
+        d_image, reinterpret_cast<const float4*>(splats->rec), sorted_ids, reinterpret_cast<const int2*>(ranges),
+        t_final, last, width, height, tiles_x, row_begin * tiles_x, bg, reinterpret_cast<float4*>(grads2d),
+        tile_order, part_out, top_out);
+  else
+    blend_bwd_kernel<false><<<unsigned(ntiles * kParts), kThreads, kSmemBytes, static_cast<cudaStream_t>(stream)>>>(
+        d_image, reinterpret_cast<const float4*>(splats->rec), sorted_ids, reinterpret_cast<const int2*>(ranges),
+        t_final, last, width, height, tiles_x, row_begin * tiles_x, bg, reinterpret_cast<float4*>(grads2d),
+        tile_order, nullptr, nullptr);
   return check_launch();
 }
 
@@ -495,5 +563,210 @@ extern "C" int gs_tile_schedule(const int32_t* work, int32_t tiles, int32_t* scr
   tile_bucket_kernel<<<unsigned((tiles + 255) / 256), 256, 0, s>>>(work, tiles, bucket_of, hist);
   tile_sched_scan_kernel<<<1, kSchedBuckets, 0, s>>>(hist, cursor);
   tile_sched_scatter_kernel<<<unsigned((tiles + 255) / 256), 256, 0, s>>>(bucket_of, cursor, tiles, order);
+  return check_launch();
+}
+
+// ---------------------------------------------------------------------------
+// Deterministic backward (the reference's deterministic=True / workers=1
+// contract, rasterizer.py:32-41, test_cli.py:24-35: bit-identical runs).
+// The blend writes one partial row per (sorted instance, half tile) — no
+// float atomics — and each splat's rows are then summed in a fixed order:
+// its tiles in row-major order over its rectangle (the reference's own
+// expansion order, rasterizer.py:105-111), the two halves of a tile in order.
+// The instance position of (splat, k-th tile of its rectangle) comes from an
+// inverse index built from the sorted list.
+namespace gs {
+namespace {
+
+constexpr int kScanBlock = 1024;
+
+// off[g] = exclusive prefix of max(tiles_touched, 0): block sums, then a
+// single-block scan of the sums, then the per-block add
+__global__ void __launch_bounds__(kScanBlock) det_count_kernel(const int32_t* __restrict__ tiles, int64_t n,
+                                                               uint32_t* __restrict__ off, uint32_t* __restrict__ sums) {
+  __shared__ uint32_t s_w[32];
+  const int64_t g = int64_t(blockIdx.x) * kScanBlock + threadIdx.x;
+  const uint32_t v = g < n ? uint32_t(max(tiles[g], 0)) : 0u;
+  uint32_t incl = v;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  if (lane == 31) s_w[w] = incl;
+  __syncthreads();
+  if (w == 0) {
+    uint32_t x = s_w[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += t;
+    }
+    s_w[lane] = x;   // inclusive over warps
+  }
+  __syncthreads();
+  const uint32_t excl = incl - v + (w > 0 ? s_w[w - 1] : 0u);
+  if (g < n) off[g] = excl;
+  if (threadIdx.x == kScanBlock - 1) sums[blockIdx.x] = excl + v;
+}
+
+__global__ void __launch_bounds__(kScanBlock) det_sums_kernel(uint32_t* __restrict__ sums, int64_t blocks) {
+  __shared__ uint32_t s_run;
+  if (threadIdx.x == 0) s_run = 0u;
+  __syncthreads();
+  for (int64_t b0 = 0; b0 < blocks; b0 += kScanBlock) {
+    const int64_t b = b0 + threadIdx.x;
+    const uint32_t v = b < blocks ? sums[b] : 0u;
+    // serial-per-chunk scan by a warp-free simple approach: one thread per element
+    uint32_t incl = v;
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    __shared__ uint32_t s_w[32];
+    if (lane == 31) s_w[threadIdx.x >> 5] = incl;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      uint32_t x = s_w[threadIdx.x];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xffffffffu, x, o);
+        if (int(threadIdx.x) >= o) x += t;
+      }
+      s_w[threadIdx.x] = x;
+    }
+    __syncthreads();
+    const int w = threadIdx.x >> 5;
+    const uint32_t excl = s_run + incl - v + (w > 0 ? s_w[w - 1] : 0u);
+    if (b < blocks) sums[b] = excl;
+    __syncthreads();
+    if (threadIdx.x == kScanBlock - 1) s_run = excl + v;
+    __syncthreads();
+  }
+}
+
+__global__ void det_add_kernel(uint32_t* __restrict__ off, const uint32_t* __restrict__ sums, int64_t n) {
+  const int64_t g = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (g < n) off[g] += sums[g / kScanBlock];
+}
+
+// inv[off[g] + k] = sorted position of (g, k-th tile of its rectangle); one warp per tile
+__global__ void det_inverse_kernel(const uint32_t* __restrict__ ids, const int2* __restrict__ ranges,
+                                   const int4* __restrict__ rect, const uint32_t* __restrict__ off, int tiles_x,
+                                   int64_t tiles, uint32_t* __restrict__ inv) {
+  const int64_t tile = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  if (tile >= tiles) return;
+  const int tx = int(tile % tiles_x), ty = int(tile / tiles_x);
+  const int2 r = ranges[tile];
+  for (int pos = r.x + (threadIdx.x & 31); pos < r.y; pos += 32) {
+    const uint32_t g = ids[pos];
+    const int4 rc = rect[g];
+    inv[off[g] + uint32_t((ty - rc.y) * (rc.z - rc.x + 1) + (tx - rc.x))] = uint32_t(pos);
+  }
+}
+
+// one thread per splat: its partial rows in the fixed order -> the (N,12) row
+__global__ void det_reduce_kernel(const int32_t* __restrict__ tiles, const int4* __restrict__ rect,
+                                  const uint32_t* __restrict__ off, const uint32_t* __restrict__ inv,
+                                  const float* __restrict__ part_rows, const int32_t* __restrict__ top,
+                                  int tiles_x, int64_t n, float* __restrict__ grads2d) {
+  const int64_t g = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (g >= n) return;
+  float acc[kC];
+#pragma unroll
+  for (int c = 0; c < kC; ++c) acc[c] = 0.0f;
+  if (tiles[g] > 0) {
+    const int4 rc = rect[g];
+    uint32_t k = off[g];
+    for (int ty = rc.y; ty <= rc.w; ++ty)
+      for (int tx = rc.x; tx <= rc.z; ++tx, ++k) {
+        const int64_t t = int64_t(ty) * tiles_x + tx;
+        const uint32_t pos = inv[k];
+#pragma unroll
+        for (int part = 0; part < kParts; ++part)
+          if (int64_t(pos) < int64_t(top[t * kParts + part])) {
+            const float* row = part_rows + (size_t(pos) * kParts + part) * kC;
+#pragma unroll
+            for (int c = 0; c < kC; ++c) acc[c] += row[c];
+          }
+      }
+  }
+  float4* out = reinterpret_cast<float4*>(grads2d) + 3 * g;
+  out[0] = make_float4(acc[0], acc[1], acc[2], 0.0f);
+  out[1] = make_float4(acc[3], acc[4], acc[5], 0.0f);
+  out[2] = make_float4(acc[6], acc[7], acc[8], 0.0f);
+}
+
+struct DetLayout {
+  size_t part_rows, inv, off, sums, top, bytes;
+};
+
+inline size_t det_align(size_t x) { return (x + 255) & ~size_t(255); }
+
+int det_layout(int64_t n, int32_t width, int32_t height, int64_t cap, DetLayout* L) {
+  if (n < 0 || cap < 0 || width <= 0 || height <= 0) return GS_ERR_INVALID_ARG;
+  if (cap > int64_t(INT32_MAX)) return GS_ERR_RESOURCE_LIMIT;
+  const int64_t tiles = int64_t((width + kTile - 1) / kTile) * ((height + kTile - 1) / kTile);
+  const size_t un = size_t(n > 0 ? n : 1), uc = size_t(cap > 0 ? cap : 1);
+  size_t o = 0;
+  L->part_rows = o; o += det_align(sizeof(float) * uc * kParts * kC);
+  L->inv = o; o += det_align(sizeof(uint32_t) * uc);
+  L->off = o; o += det_align(sizeof(uint32_t) * un);
+  L->sums = o; o += det_align(sizeof(uint32_t) * (un / kScanBlock + 1));
+  L->top = o; o += det_align(sizeof(int32_t) * size_t(tiles) * kParts);
+  L->bytes = o;
+  return GS_OK;
+}
+
+}  // namespace
+}  // namespace gs
+
+extern "C" int gs_blend_backward_det_workspace_size(int64_t n, int32_t width, int32_t height, int64_t k_capacity,
+                                                    size_t* bytes) {
+  if (!bytes) return GS_ERR_INVALID_ARG;
+  gs::DetLayout L;
+  const int st = gs::det_layout(n, width, height, k_capacity, &L);
+  if (st == GS_OK) *bytes = L.bytes;
+  return st;
+}
+
+extern "C" int gs_blend_backward_deterministic(const float* d_image, const gs_splats_t* splats,
+                                               const uint32_t* sorted_ids, const int32_t* ranges,
+                                               const float* t_final, const int32_t* last, int32_t width,
+                                               int32_t height, const float background[3],
+                                               const int32_t* tile_order, void* workspace, size_t workspace_bytes,
+                                               int64_t k_capacity, float* grads2d, void* stream) {
+  using namespace gs;
+  if (!splats || !grads2d || !ranges || !sorted_ids || !workspace) return GS_ERR_INVALID_ARG;
+  DetLayout L;
+  int st = det_layout(splats->n, width, height, k_capacity, &L);
+  if (st != GS_OK) return st;
+  if (workspace_bytes < L.bytes) return GS_ERR_INVALID_ARG;
+  const int64_t n = splats->n;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (n == 0) return GS_OK;
+  char* ws = static_cast<char*>(workspace);
+  float* part_rows = reinterpret_cast<float*>(ws + L.part_rows);
+  uint32_t* inv = reinterpret_cast<uint32_t*>(ws + L.inv);
+  uint32_t* off = reinterpret_cast<uint32_t*>(ws + L.off);
+  uint32_t* sums = reinterpret_cast<uint32_t*>(ws + L.sums);
+  int32_t* top = reinterpret_cast<int32_t*>(ws + L.top);
+  const int tiles_x = (width + kTile - 1) / kTile, tiles_y = (height + kTile - 1) / kTile;
+  const int64_t tiles = int64_t(tiles_x) * tiles_y;
+  st = blend_backward_rows(d_image, splats, sorted_ids, ranges, t_final, last, width, height, 0, tiles_y, background,
+                           grads2d, stream, tile_order, part_rows, top);
+  if (st != GS_OK) return st;
+  const int64_t blocks = (n + kScanBlock - 1) / kScanBlock;
+  det_count_kernel<<<unsigned(blocks), kScanBlock, 0, s>>>(splats->tiles_touched, n, off, sums);
+  det_sums_kernel<<<1, kScanBlock, 0, s>>>(sums, blocks);
+  det_add_kernel<<<unsigned((n + 255) / 256), 256, 0, s>>>(off, sums, n);
+  const int4* rect = reinterpret_cast<const int4*>(splats->rect);
+  det_inverse_kernel<<<unsigned((tiles * 32 + 255) / 256), 256, 0, s>>>(
+      sorted_ids, reinterpret_cast<const int2*>(ranges), rect, off, tiles_x, tiles, inv);
+  det_reduce_kernel<<<unsigned((n + 255) / 256), 256, 0, s>>>(splats->tiles_touched, rect, off, inv, part_rows, top,
+                                                              tiles_x, n, grads2d);
   return check_launch();
 }

@@ -199,10 +199,11 @@ ssim_forward_kernel(const float* __restrict__ img, const float* __restrict__ gt,
   const double s1 = block_sum384(ssim_sum, sm.red);
   const double s2 = block_sum384(l1_sum, sm.red);
   const double s3 = block_sum384(sq_sum, sm.red);
-  if (t == 0) {
-    atomicAdd(&sums[0], s1);
-    atomicAdd(&sums[1], s2);
-    atomicAdd(&sums[2], s3);
+  if (t == 0) {   // per-block partials, summed in a fixed order by the finalize kernel (deterministic)
+    const size_t b = size_t(blockIdx.y) * gridDim.x + blockIdx.x;
+    sums[3 * b + 0] = s1;
+    sums[3 * b + 1] = s2;
+    sums[3 * b + 2] = s3;
   }
 }
 
@@ -273,22 +274,48 @@ ssim_backward_kernel(const float* __restrict__ img, const float* __restrict__ gt
   }
 }
 
-__global__ void loss_finalize_kernel(const double* __restrict__ sums, double count, double lambda,
-                                     float* __restrict__ loss) {
-  const double l1 = sums[1] / count;
-  const double dssim = (1.0 - sums[0] / count) / 2.0;
-  loss[0] = float((1.0 - lambda) * l1 + lambda * dssim);
-  loss[1] = float(l1);
-  loss[2] = float(sums[0] / count);
-  loss[3] = float(sums[2] / count);   // mean squared error
+// one block of 256 threads: the block partials in a fixed order (strided
+// per thread, then a fixed shared-memory tree), so the loss is bit-identical
+// run to run
+__global__ void __launch_bounds__(256) loss_finalize_kernel(const double* __restrict__ part, int64_t blocks,
+                                                            double count, double lambda, float* __restrict__ loss) {
+  __shared__ double red[3][256];
+  double a[3] = {0.0, 0.0, 0.0};
+  for (int64_t b = threadIdx.x; b < blocks; b += 256)
+    for (int k = 0; k < 3; ++k) a[k] += part[3 * b + k];
+  for (int k = 0; k < 3; ++k) red[k][threadIdx.x] = a[k];
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (int(threadIdx.x) < w)
+      for (int k = 0; k < 3; ++k) red[k][threadIdx.x] += red[k][threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const double sums[3] = {red[0][0], red[1][0], red[2][0]};
+    const double l1 = sums[1] / count;
+    const double dssim = (1.0 - sums[0] / count) / 2.0;
+    loss[0] = float((1.0 - lambda) * l1 + lambda * dssim);
+    loss[1] = float(l1);
+    loss[2] = float(sums[0] / count);
+    loss[3] = float(sums[2] / count);   // mean squared error
+  }
 }
 
 }  // namespace
 }  // namespace gs
 
+namespace {
+size_t loss_blocks(int32_t width, int32_t height) {
+  return size_t((width + gs::kTW - 1) / gs::kTW) * size_t((height + gs::kTH - 1) / gs::kTH);
+}
+size_t loss_src_offset(int32_t width, int32_t height) {
+  return (3 * sizeof(double) * loss_blocks(width, height) + 255) & ~size_t(255);
+}
+}  // namespace
+
 extern "C" int gs_loss_workspace_size(int32_t width, int32_t height, size_t* bytes) {
   if (!bytes || width <= 0 || height <= 0) return GS_ERR_INVALID_ARG;
-  *bytes = 256 + size_t(width) * height * 9 * sizeof(float);
+  *bytes = loss_src_offset(width, height) + size_t(width) * height * 9 * sizeof(float);
   return GS_OK;
 }
 
@@ -303,9 +330,8 @@ extern "C" int gs_l1_dssim_loss(const float* image, const float* target, int32_t
   if (workspace_bytes < need) return GS_ERR_INVALID_ARG;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   double* sums = static_cast<double*>(workspace);
-  float* src = reinterpret_cast<float*>(static_cast<char*>(workspace) + 256);
-  cudaError_t e = cudaMemsetAsync(sums, 0, 3 * sizeof(double), s);
-  if (e != cudaSuccess) return record_cuda_error(e);
+  float* src = reinterpret_cast<float*>(static_cast<char*>(workspace) + loss_src_offset(width, height));
+  cudaError_t e = cudaSuccess;
   const double count = double(width) * height * 3.0;
   const Window win = make_window();
   static bool configured = false;
@@ -325,6 +351,6 @@ extern "C" int gs_l1_dssim_loss(const float* image, const float* target, int32_t
   ssim_backward_kernel<<<grid, kLossThreads, sizeof(BwdSmem), s>>>(image, target, src, width, height, win,
                                                                     float((1.0 - lambda) / count), d_image);
   if ((st = check_launch()) != GS_OK) return st;
-  loss_finalize_kernel<<<1, 1, 0, s>>>(sums, count, lambda, loss_out);
+  loss_finalize_kernel<<<1, 256, 0, s>>>(sums, int64_t(loss_blocks(width, height)), count, lambda, loss_out);
   return check_launch();
 }

@@ -47,6 +47,8 @@ class TrainConfig:
     adam_eps: float = 1e-15
     background: tuple[float, float, float] = (0.0, 0.0, 0.0)
     sh_band_interval: int = 1000
+    workers: int = 1                 # the reference's tile threads (kept for API parity; tiles are CTAs)
+    deterministic: bool = False      # bit-identical runs: atomic-free backward (the CLI's --deterministic)
 
     def __post_init__(self):
         if not 0.0 <= self.lambda_dssim <= 1.0:

@@ -54,6 +54,21 @@ def conic_basis(conic: np.ndarray) -> np.ndarray:
     return np.stack([f1 * ex, f1 * ey, -f2 * ey, f2 * ex], axis=1).astype(np.float32)
 
 
+def resolve_workers(workers: int | None = None, deterministic: bool = False) -> int:
+    """The reference's worker resolution (rasterizer.py:32-41), kept for API
+    compatibility: CPU tile threads have no GPU counterpart (tiles are CTAs).
+    The GPU side of `deterministic` is render_backward(deterministic=True)
+    (TrainConfig.deterministic in training): bit-identical runs."""
+    if deterministic:
+        return 1
+    if workers is None:
+        workers = __import__("os").cpu_count() or 1
+    cap = __import__("os").environ.get("SPLATLAB_THREADS")
+    if cap:
+        workers = min(workers, max(1, int(cap)))
+    return max(1, workers)
+
+
 def tile_extent(width: int, height: int) -> tuple[int, int]:
     return (width + TILE_SIZE - 1) // TILE_SIZE, (height + TILE_SIZE - 1) // TILE_SIZE
 
@@ -492,8 +507,12 @@ def render_forward(splats: DeviceSplats, binning: TileBinning, width: int, heigh
 
 
 def render_backward(d_image: torch.Tensor, output: RenderOutput, splats: DeviceSplats, binning: TileBinning,
-                    width: int, height: int, background) -> SplatGrads2D:
-    """K7: back-to-front blend gradient (rasterizer.py:253)."""
+                    width: int, height: int, background, deterministic: bool = False) -> SplatGrads2D:
+    """K7: back-to-front blend gradient (rasterizer.py:253).
+
+    deterministic: no float atomics (per-instance partial rows summed per
+    splat in a fixed order): bit-identical results run to run, the
+    reference's deterministic=True (rasterizer.py:34-35)."""
     if output.final_transmittance is None or output.last_contributor is None:
         raise ValueError("backward pass needs a training-mode RenderOutput")  # rasterizer.py:265-266
     lib = _lib.load()
@@ -502,6 +521,18 @@ def render_backward(d_image: torch.Tensor, output: RenderOutput, splats: DeviceS
         raise ValueError(f"d_image shape {tuple(d_image.shape)} != {(height, width, 3)}")
     packed = torch.empty((len(splats), _lib.GRAD2D_FLOATS), dtype=torch.float32, device=splats.rec.device)
     cs = splats.c_struct()
+    if deterministic:
+        cap = int(binning.splat_ids.shape[0])
+        nbytes = ctypes.c_size_t(0)
+        _lib.check(lib.gs_blend_backward_det_workspace_size(len(splats), width, height, cap, ctypes.byref(nbytes)),
+                   "render_backward")
+        ws = torch.empty(max(int(nbytes.value), 1), dtype=torch.uint8, device=splats.rec.device)
+        _lib.check(lib.gs_blend_backward_deterministic(
+            d_image.data_ptr(), ctypes.byref(cs), binning.splat_ids.data_ptr(), binning.ranges.data_ptr(),
+            output.final_transmittance.data_ptr(), output.last_contributor.data_ptr(), width, height,
+            _bg(background), None, ws.data_ptr(), int(nbytes.value), cap, packed.data_ptr(), _stream()),
+            "render_backward")
+        return SplatGrads2D(packed, None, splats.rec)
     if _BWD_SCHEDULE:
         # longest-first tile order from the forward's training record (scratch: 2 T + 2048 int32)
         tx, ty = tile_extent(width, height)

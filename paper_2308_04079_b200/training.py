@@ -312,7 +312,7 @@ def train_step(state: TrainState, views: Sequence[TrainView], config: TrainConfi
         done = torch.cuda.Event()
         done.record(torch.cuda.current_stream(device))
         g2 = R.render_backward(fw.d_image, fw.out, fw.splats, fw.binning, fw.camera.width, fw.camera.height,
-                               config.background)
+                               config.background, deterministic=config.deterministic)
         if g2.tile_order is not None:
             if not hasattr(state, "_tile_orders"):
                 state._tile_orders = {}
@@ -390,7 +390,8 @@ def _train_step_sharded(state: TrainState, views: Sequence[TrainView], config: T
     if any_rank_(not math.isfinite(value), device, group):
         raise TrainingDiverged(f"non-finite loss {value} at iteration {it}"
                                + ("" if not math.isfinite(value) else " (on another rank)"))
-    g2 = R.render_backward(d_image, out, splats, binning, camera.width, camera.height, bg)
+    g2 = R.render_backward(d_image, out, splats, binning, camera.width, camera.height, bg,
+                           deterministic=config.deterministic)
     bucket = getattr(state, "_bucket", None)
     if bucket is None or bucket.n != len(state.cloud):
         bucket = state._bucket = GradientBucket(len(state.cloud), device)
