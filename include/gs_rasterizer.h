@@ -327,6 +327,26 @@ int gs_step_guard(const float* loss, const int64_t* k_info, int32_t* skip, doubl
 int gs_adam_step(const gs_adam_group_t* groups, int32_t num_groups, double beta1, double beta2,
                  double eps, double bias1, double bias2, void* stream);
 
+/* ---- fused single-call stages --------------------------
+ * gs_forward = gs_preprocess_forward + gs_bin_and_sort_async +
+ * gs_blend_forward_ordered (render_view, optimizer.py:212-219): no host
+ * synchronisation; K and the flags land in k_info (see
+ * gs_bin_and_sort_async), tile_order nullable, scratch as gs_blend_forward.
+ * gs_backward = the backward blend (longest-first when sched_scratch, device
+ * int32[2 T + 2048], is given) + gs_preprocess_backward (render_backward +
+ * backward_project, rasterizer.py:253-316, gradients.py:192-259); grads
+ * overwritten, stats nullable. */
+int gs_forward(const gs_params_t* params, const gs_camera_t* camera, int32_t active_sh_degree,
+               gs_splats_t* splats, void* bin_workspace, size_t bin_workspace_bytes, int64_t k_capacity,
+               uint32_t* sorted_ids, int32_t* ranges, int64_t* k_info, const float background[3],
+               int32_t training, const int32_t* tile_order, float* image, float* t_final, int32_t* last,
+               int32_t* scratch, void* stream);
+int gs_backward(const float* d_image, const gs_params_t* params, const gs_camera_t* camera,
+                int32_t active_sh_degree, const gs_splats_t* splats, const uint32_t* sorted_ids,
+                const int32_t* ranges, const float* t_final, const int32_t* last, const float background[3],
+                int32_t* sched_scratch, float* grads2d, const gs_grads_t* grads, const gs_stats_t* stats,
+                void* stream);
+
 /* ---- adaptive density control: replaces
  * optimizer.densify_and_prune (optimizer.py:304-374).
  * gs_densify_classify counts clones and splits (synchronises `stream`);

@@ -119,6 +119,12 @@ SIGNATURES = [
     ("gs_blend_backward_deterministic", c_int32, [c_void_p, POINTER(GsSplats), c_void_p, c_void_p, c_void_p, c_void_p,
                                                   c_int32, c_int32, POINTER(c_float), c_void_p, c_void_p, c_size_t,
                                                   c_int64, c_void_p, c_void_p]),
+    ("gs_forward", c_int32, [POINTER(GsParams), POINTER(GsCamera), c_int32, POINTER(GsSplats), c_void_p, c_size_t,
+                             c_int64, c_void_p, c_void_p, c_void_p, POINTER(c_float), c_int32, c_void_p, c_void_p,
+                             c_void_p, c_void_p, c_void_p, c_void_p]),
+    ("gs_backward", c_int32, [c_void_p, POINTER(GsParams), POINTER(GsCamera), c_int32, POINTER(GsSplats), c_void_p,
+                              c_void_p, c_void_p, c_void_p, POINTER(c_float), c_void_p, c_void_p, POINTER(GsGrads),
+                              POINTER(GsStats), c_void_p]),
     ("gs_densify_workspace_size", c_int32, [c_int64, POINTER(c_size_t)]),
     ("gs_densify_classify", c_int32, [POINTER(GsCloudState), POINTER(GsStats), POINTER(GsDensifyConfig), c_void_p,
                                       c_size_t, POINTER(c_int64), POINTER(c_int64), c_void_p]),

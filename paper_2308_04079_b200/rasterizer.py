@@ -649,32 +649,102 @@ class TileSchedule:
 # ---------------------------------------------------------------------------
 # drop-in autograd Function
 
+class _TileOrderCache:
+    """Per-camera longest-first tile order from the camera's last backward
+    (a few hundred cameras): the next forward of the same view launches its
+    heaviest tiles first.  The images do not depend on it."""
+
+    def __init__(self, size: int = 256):
+        self.size = size
+        self.orders: dict = {}
+
+    @staticmethod
+    def key(camera: Camera, device) -> tuple:
+        return (str(device), int(camera.width), int(camera.height), float(camera.fx), float(camera.fy),
+                float(camera.cx), float(camera.cy), tuple(np.asarray(camera.rotation, np.float64).reshape(-1)),
+                tuple(np.asarray(camera.translation, np.float64).reshape(-1)))
+
+    def get(self, key):
+        return self.orders.get(key)
+
+    def put(self, key, order) -> None:
+        self.orders.pop(key, None)
+        self.orders[key] = order
+        while len(self.orders) > self.size:
+            self.orders.pop(next(iter(self.orders)))
+
+
+_tile_orders = _TileOrderCache()
+
+
 class GaussianRasterizer(torch.autograd.Function):
     """Differentiable rasterizer: raw parameters + camera in; image (H,W,3)
     and radii (N,) int32 (0 = culled) out; gradients w.r.t. the raw means,
     log-scales, quaternions, opacity logits and SH coefficients back.
 
-    The forward is render_view(training=True); the backward is
-    render_backward + backward_project, optionally updating `stats`."""
+    Forward: one gs_forward call (projection, sync-free binning, blend) on
+    the current stream, with the camera's previous longest-first tile order.
+    The instance count and flags are copied to pinned host memory behind the
+    binning; the backward checks them (by then the loss has consumed the
+    image, so the wait is for work already done) and raises like the
+    reference — InvalidPrimitiveError for a zero quaternion (core.py:164-165),
+    ResourceLimitError past 2^31 instances (rasterizer.py:99-101) — or
+    CapacityError when the frame outgrew the instance-buffer hint (the hint is
+    raised; re-run the step).  The first frame of a frame size bins
+    synchronously to learn its instance count.  Backward: one gs_backward
+    call (scheduled backward blend + backward_project, densify statistics when
+    `stats` is given), or the deterministic blend when deterministic=True."""
 
     @staticmethod
-    def forward(ctx, means, log_scales, rotations, opacity_logits, sh, camera, background,
-                active_sh_degree=3, stats=None):
+    def forward(ctx, means, log_scales, rotations, opacity_logits, sh, camera, background, active_sh_degree=3,
+                stats=None, deterministic=False):
         camera = _camera(camera)
+        degree = int(active_sh_degree)
+        if not 0 <= degree <= 3:
+            raise ValueError(f"SH degree must be in 0..3, got {degree}")  # sh.py:37-38
         tensors = [t.detach().contiguous() for t in (means, log_scales, rotations, opacity_logits, sh)]
         params = c_params_from(*tensors)
-        n = means.shape[0]
-        splats = _project_tensors(params, n, means.device, camera, int(active_sh_degree))
-        binning = bin_and_sort(splats, camera.width, camera.height)
-        out = render_forward(splats, binning, camera.width, camera.height, background, training=True)
+        n, device = means.shape[0], means.device
+        W, H = camera.width, camera.height
+        hint = _capacity.key(device, W, H)
+        okey = _TileOrderCache.key(camera, device)
+        if hint not in _capacity.k:   # first frame of this size: learn K synchronously
+            splats = _project_tensors(params, n, device, camera, degree)
+            binning = bin_and_sort(splats, W, H)
+            out = render_forward(splats, binning, W, H, background, training=True)
+            k_report, k_event = None, None
+        else:
+            lib = _lib.load()
+            cap = _capacity.get(hint, n)
+            ws_bytes = _bin_workspace_bytes(n, W, H, cap)
+            ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=device)
+            tiles_x, tiles_y = tile_extent(W, H)
+            splats = DeviceSplats.empty(n, device)
+            binning = TileBinning(torch.empty(max(cap, 1), dtype=torch.int32, device=device),
+                                  torch.empty((tiles_x * tiles_y, 2), dtype=torch.int32, device=device), tiles_x,
+                                  tiles_y, torch.empty(3, dtype=torch.int64, device=device), n, None, hint)
+            f32 = dict(dtype=torch.float32, device=device)
+            out = RenderOutput(torch.empty((H, W, 3), **f32), torch.empty((H, W), **f32),
+                               torch.empty((H, W), dtype=torch.int32, device=device))
+            scratch = torch.empty(2 + W * H, dtype=torch.int32, device=device)
+            order = _tile_orders.get(okey)
+            cs = splats.c_struct()
+            _lib.check(lib.gs_forward(ctypes.byref(params), ctypes.byref(camera.to_c()), degree, ctypes.byref(cs),
+                                      ws.data_ptr(), ws_bytes, cap, binning.splat_ids.data_ptr(),
+                                      binning.ranges.data_ptr(), binning.k_info.data_ptr(), _bg(background), 1,
+                                      _lib.ptr(order), out.image.data_ptr(), out.final_transmittance.data_ptr(),
+                                      out.last_contributor.data_ptr(), scratch.data_ptr(), _stream()),
+                       "render_view")
+            k_report = torch.empty(3, dtype=torch.int64).pin_memory()
+            k_report.copy_(binning.k_info, non_blocking=True)
+            k_event = torch.cuda.Event()
+            k_event.record(torch.cuda.current_stream(device))
         ctx.save_for_backward(*tensors, splats.rec, splats.depth, splats.radii, splats.rect, splats.tiles_touched,
                               splats.status, binning.splat_ids, binning.ranges, out.final_transmittance,
                               out.last_contributor)
-        ctx.camera = camera
-        ctx.background = background
-        ctx.degree = int(active_sh_degree)
-        ctx.stats = stats
-        ctx.tiles = (binning.tiles_x, binning.tiles_y)
+        ctx.camera, ctx.background, ctx.degree, ctx.stats = camera, background, degree, stats
+        ctx.deterministic, ctx.okey = bool(deterministic), okey
+        ctx.tiles, ctx.hint, ctx.k_report, ctx.k_event = (binning.tiles_x, binning.tiles_y), hint, k_report, k_event
         ctx.mark_non_differentiable(splats.radii)
         return out.image, splats.radii
 
@@ -683,20 +753,40 @@ class GaussianRasterizer(torch.autograd.Function):
         (means, log_scales, rotations, opacity_logits, sh, rec, depth, radii, rect, tiles_touched, status,
          ids, ranges, t_final, last) = ctx.saved_tensors
         camera = ctx.camera
+        if ctx.k_event is not None:   # the forward's deferred binning check
+            ctx.k_event.synchronize()
+            TileBinning(ids, ranges, *ctx.tiles, ctx.k_report, means.shape[0], None, ctx.hint).check_host(
+                [int(v) for v in ctx.k_report.tolist()])
         splats = DeviceSplats(rec, depth, radii, rect, tiles_touched, status)
-        binning = TileBinning(ids, ranges, *ctx.tiles)
-        output = RenderOutput(None, t_final, last)
-        g2d = render_backward(d_image, output, splats, binning, camera.width, camera.height, ctx.background)
+        n, device = means.shape[0], means.device
+        d_image = d_image.to(dtype=torch.float32).contiguous()
         params = c_params_from(means, log_scales, rotations, opacity_logits, sh)
-        grads = _backward_project_tensors(params, means.shape[0], means.device, camera, splats, g2d, ctx.degree,
-                                          ctx.stats, None, False)
+        z = dict(dtype=torch.float32, device=device)
+        grads = GaussianGrads(torch.empty((n, 3), **z), torch.empty((n, 4), **z), torch.empty((n, 3), **z),
+                              torch.empty(n, **z), torch.empty((n, 16, 3), **z), torch.empty(n, **z))
+        if ctx.deterministic:
+            g2 = render_backward(d_image, RenderOutput(None, t_final, last), splats, TileBinning(ids, ranges, *ctx.tiles),
+                                 camera.width, camera.height, ctx.background, deterministic=True)
+            _backward_project_tensors(params, n, device, camera, splats, g2, ctx.degree, ctx.stats, grads, False)
+        else:
+            tx, ty = ctx.tiles
+            sched = torch.empty(2 * tx * ty + 2048, dtype=torch.int32, device=device)
+            packed = torch.empty((n, _lib.GRAD2D_FLOATS), **z)
+            cs, cg = splats.c_struct(), grads.c_struct()
+            cst = ctx.stats.c_struct() if ctx.stats is not None else None
+            _lib.check(_lib.load().gs_backward(
+                d_image.data_ptr(), ctypes.byref(params), ctypes.byref(camera.to_c()), ctx.degree, ctypes.byref(cs),
+                ids.data_ptr(), ranges.data_ptr(), t_final.data_ptr(), last.data_ptr(), _bg(ctx.background),
+                sched.data_ptr(), packed.data_ptr(), ctypes.byref(cg), ctypes.byref(cst) if cst is not None else None,
+                _stream()), "render_backward")
+            _tile_orders.put(ctx.okey, sched[:tx * ty])
         ctx.view_pos_grad_norm = grads.view_pos_grad_norm
         return (grads.d_means, grads.d_log_scales, grads.d_rotations, grads.d_opacity_logits, grads.d_sh,
-                None, None, None, None)
+                None, None, None, None, None)
 
 
 def rasterize_gaussians(means, log_scales, rotations, opacity_logits, sh, camera, background=(0.0, 0.0, 0.0),
-                        active_sh_degree: int = 3, stats: DensifyStats | None = None):
+                        active_sh_degree: int = 3, stats: DensifyStats | None = None, deterministic: bool = False):
     """Functional form of GaussianRasterizer.apply -> (image, radii)."""
     return GaussianRasterizer.apply(means, log_scales, rotations, opacity_logits, sh, camera, background,
-                                    active_sh_degree, stats)
+                                    active_sh_degree, stats, deterministic)
