@@ -1,9 +1,13 @@
 """Per-stage CUDA-event timing and roofline arithmetic for bench.py.
 
-Algorithmic bytes / flops per stage follow SURVEY.md §8(d):
+Algorithmic bytes / flops per stage follow SURVEY.md §8(d), except for the
+binning, which is charged the bytes the implemented algorithm must move
+(binning.cu; SURVEY's formula assumes the reference's 64-bit sort over K):
   K1 preprocess_fwd  44 N + 192 V read + 48 V write
-  K2-K5 bin_and_sort 8 V + (20 V + 12 K) + (8 K + 24 D K) + (8 K + 8 T), D = radix passes of the
-                     reference's 64-bit key sort (the algorithmic formula, not this implementation's)
+  K2-K5 bin_and_sort 156 N + 24 E + 4 K + 12 T: depth histogram 8 N, four onesweep passes over the
+                     depth keys 16 + 16 + 16 + 44 N (the last gathers the tile rectangles), bucket count
+                     16 N, bucket scatter 40 N + 8 E, window count 8 E, instance write 8 E + 4 K,
+                     tile ranges 12 T; E = (Gaussian, super-tile) bucket entries
   K6 blend_fwd       40 K + 20 P bytes (training); 25 FP32 ops + 1 ex2 per evaluated (pixel, splat) pair
   K7 blend_bwd       40 K + 20 P + 36 V bytes; 60 FP32 ops + 1 ex2 + 1 rcp per evaluated pair
   K8 preprocess_bwd  276 V + 240 N + 20 N bytes
@@ -18,10 +22,12 @@ from collections import defaultdict
 
 import torch
 
-# our own __global__ kernels launched per training step (CUB's radix-sort and scan
-# kernels, compiled into the same library, are counted separately in DESIGN.md)
-# (blend_bwd: the three tile-schedule kernels + the blend)
-KERNELS_PER_STEP = {"preprocess_fwd": 1, "bin_and_sort": 5, "blend_fwd": 1, "loss": 3, "blend_bwd": 4,
+# our own __global__ kernels launched per training step (every one hand-written;
+# blend_fwd: the blend + the exact re-blend of undecidable stops; blend_bwd:
+# the three tile-schedule kernels + the blend; bin_and_sort: depth histogram,
+# sort setup, 4 onesweep passes, bucket count, scan, window setup, bucket
+# scatter, window count, window prefix, tile ranges, instance write)
+KERNELS_PER_STEP = {"preprocess_fwd": 1, "bin_and_sort": 14, "blend_fwd": 2, "loss": 3, "blend_bwd": 4,
                     "preprocess_bwd": 1, "adam": 1, "preprocess_bwd_adam": 1, "sharded_adam": 1}
 
 
@@ -73,17 +79,16 @@ class StageTimer:
         return sum(KERNELS_PER_STEP.get(k, 0) for k in self.events)
 
     def roofline(self, n: int, width: int, height: int, peaks: dict, visible: int | None = None,
-                 e_pairs: int | None = None) -> dict:
+                 e_pairs: int | None = None, bucket_entries: int | None = None) -> dict:
         ms = self.mean_ms()
         V = n if visible is None else visible
         K = self.last_k or 0
         P = width * height
         T = ((width + 15) // 16) * ((height + 15) // 16)
-        b = max(1, (T - 1).bit_length())
-        D = -(-(32 + b) // 8)
+        E = bucket_entries or 0
         bytes_ = {
             "preprocess_fwd": 44 * n + 192 * V + 48 * V,
-            "bin_and_sort": 8 * V + 20 * V + 12 * K + 8 * K + 24 * D * K + 8 * K + 8 * T,
+            "bin_and_sort": 156 * n + 24 * E + 4 * K + 12 * T,
             "blend_fwd": 40 * K + 20 * P,
             "blend_bwd": 40 * K + 20 * P + 36 * V,
             "preprocess_bwd": 276 * V + 240 * n + 20 * n,
@@ -154,6 +159,20 @@ def measure_fp32_peak(device=None, iters: int = 4096) -> float:
     torch.cuda.synchronize(device)
     secs = s.elapsed_time(e) / 1e3 / reps
     return blocks * 256 * iters * 8 * 2 / secs
+
+
+def bucket_entries(splats, width: int, height: int) -> int:
+    """(Gaussian, super-tile) pairs of the binning's bucket stage (binning.cu:
+    super-tiles of 8 x 4 tiles, 2 x / 4 x larger for frames past 4096 of them)."""
+    tx, ty = (width + 15) // 16, (height + 15) // 16
+    lq = 0
+    while lq < 2 and -(-tx // (8 << lq)) * -(-ty // (4 << lq)) > 4096:
+        lq += 1
+    rc = splats.rect.long()
+    ok = splats.tiles_touched > 0
+    nx = (rc[:, 2] >> (3 + lq)) - (rc[:, 0] >> (3 + lq)) + 1
+    ny = (rc[:, 3] >> (2 + lq)) - (rc[:, 1] >> (2 + lq)) + 1
+    return int(torch.where(ok, nx * ny, torch.zeros_like(nx)).sum().item())
 
 
 def evaluated_pairs(out, binning, width: int) -> int:
