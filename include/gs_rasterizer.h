@@ -290,6 +290,15 @@ int gs_preprocess_backward(const gs_params_t* params, const gs_camera_t* camera,
                            const float* grads2d, const gs_grads_t* grads, int32_t accumulate,
                            const gs_stats_t* stats, void* stream);
 
+/* gs_preprocess_backward leaving the densify statistics untouched when
+ * *skip != 0 (device int32 from gs_step_guard, e.g. max-reduced over the
+ * ranks): a multi-view step enqueues its backward before the host has read
+ * the loss (optimizer.py:245-246 raises before any update). */
+int gs_preprocess_backward_guarded(const gs_params_t* params, const gs_camera_t* camera,
+                                   int32_t active_sh_degree, const gs_splats_t* splats,
+                                   const float* grads2d, const gs_grads_t* grads, int32_t accumulate,
+                                   const gs_stats_t* stats, const int32_t* skip, void* stream);
+
 /* ---- K8+K9 fused: backward_project + densify statistics + dense Adam in one
  * pass (gradients.py:192-259, optimizer.py:252-257 and 263-293 back to back,
  * as train_step runs them).  The parameters in *params are UPDATED IN PLACE.
@@ -326,6 +335,9 @@ int gs_step_guard(const float* loss, const int64_t* k_info, int32_t* skip, doubl
  * over all groups in one launch; bias1 = 1-beta1^t, bias2 = 1-beta2^t. */
 int gs_adam_step(const gs_adam_group_t* groups, int32_t num_groups, double beta1, double beta2,
                  double eps, double bias1, double bias2, void* stream);
+/* gs_adam_step applying nothing when *skip != 0 (device int32). */
+int gs_adam_step_guarded(const gs_adam_group_t* groups, int32_t num_groups, double beta1, double beta2,
+                         double eps, double bias1, double bias2, const int32_t* skip, void* stream);
 
 /* ---- fused single-call stages --------------------------
  * gs_forward = gs_preprocess_forward + gs_bin_and_sort_async +

@@ -141,6 +141,11 @@ SIGNATURES = [
                                        c_void_p]),
     ("gs_adam_step", c_int32, [POINTER(GsAdamGroup), c_int32, c_double, c_double, c_double, c_double, c_double,
                                c_void_p]),
+    ("gs_adam_step_guarded", c_int32, [POINTER(GsAdamGroup), c_int32, c_double, c_double, c_double, c_double,
+                                       c_double, c_void_p, c_void_p]),
+    ("gs_preprocess_backward_guarded", c_int32, [POINTER(GsParams), POINTER(GsCamera), c_int32, POINTER(GsSplats),
+                                                 c_void_p, POINTER(GsGrads), c_int32, POINTER(GsStats), c_void_p,
+                                                 c_void_p]),
 ]
 
 _lib = None

@@ -24,9 +24,10 @@ __device__ __forceinline__ void adam_elem(float& p, float gr, float& m, float& v
                                         a.inv_bias2});
 }
 
-__global__ void __launch_bounds__(256) adam_kernel(AdamArgs a) {
+__global__ void __launch_bounds__(256) adam_kernel(AdamArgs a, const int32_t* __restrict__ skip) {
   const int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (q >= a.quad_start[a.num_groups]) return;
+  if (skip != nullptr && *skip != 0) return;   // the step guard (gs_step_guard) vetoed this step
   int gi = 0;
   while (gi + 1 < a.num_groups && q >= a.quad_start[gi + 1]) ++gi;
   const gs_adam_group_t& G = a.g[gi];
@@ -68,9 +69,10 @@ __global__ void __launch_bounds__(256) adam_kernel(AdamArgs a) {
 }  // namespace
 }  // namespace gs
 
-extern "C" int gs_adam_step(const gs_adam_group_t* groups, int32_t num_groups, double beta1, double beta2, double eps,
-                            double bias1, double bias2, void* stream) {
-  using namespace gs;
+namespace gs {
+namespace {
+int adam_step(const gs_adam_group_t* groups, int32_t num_groups, double beta1, double beta2, double eps, double bias1,
+              double bias2, const int32_t* skip, void* stream) {
   if (!groups || num_groups <= 0 || num_groups > kMaxGroups) return GS_ERR_INVALID_ARG;
   if (!(bias1 > 0) || !(bias2 > 0)) return GS_ERR_INVALID_ARG;
   AdamArgs a;
@@ -95,6 +97,19 @@ extern "C" int gs_adam_step(const gs_adam_group_t* groups, int32_t num_groups, d
   const int64_t quads = a.quad_start[num_groups];
   if (quads == 0) return GS_OK;
   const int block = 256;
-  adam_kernel<<<unsigned((quads + block - 1) / block), block, 0, static_cast<cudaStream_t>(stream)>>>(a);
+  adam_kernel<<<unsigned((quads + block - 1) / block), block, 0, static_cast<cudaStream_t>(stream)>>>(a, skip);
   return check_launch();
+}
+}  // namespace
+}  // namespace gs
+
+extern "C" int gs_adam_step(const gs_adam_group_t* groups, int32_t num_groups, double beta1, double beta2, double eps,
+                            double bias1, double bias2, void* stream) {
+  return gs::adam_step(groups, num_groups, beta1, beta2, eps, bias1, bias2, nullptr, stream);
+}
+
+// gs_adam_step applying nothing when *skip != 0 (device int32, gs_step_guard)
+extern "C" int gs_adam_step_guarded(const gs_adam_group_t* groups, int32_t num_groups, double beta1, double beta2,
+                                    double eps, double bias1, double bias2, const int32_t* skip, void* stream) {
+  return gs::adam_step(groups, num_groups, beta1, beta2, eps, bias1, bias2, skip, stream);
 }

@@ -302,8 +302,9 @@ __device__ __forceinline__ float4 dsh_quad(const float (&b)[16], const float (&d
 __global__ void __launch_bounds__(128, 4)
 preprocess_bwd_kernel(gs_params_t p, DevCamera cam, int degree, const float4* __restrict__ rec,
                       const int32_t* __restrict__ radii, const float4* __restrict__ g2d, gs_grads_t out,
-                      int accumulate, gs_stats_t stats) {
+                      int accumulate, gs_stats_t stats, const int32_t* __restrict__ stats_skip) {
   __shared__ float4 s_sh[128 * kShStride];
+  if (stats_skip != nullptr && *stats_skip != 0) stats = gs_stats_t{nullptr, nullptr, nullptr};
   const int64_t g0 = int64_t(blockIdx.x) * blockDim.x;
   const int64_t g = g0 + threadIdx.x;
   const bool valid = g < p.n;
@@ -577,9 +578,11 @@ extern "C" int gs_step_guard(const float* loss, const int64_t* k_info, int32_t* 
   return gs::check_launch();
 }
 
-extern "C" int gs_preprocess_backward(const gs_params_t* params, const gs_camera_t* camera, int32_t active_sh_degree,
-                                      const gs_splats_t* splats, const float* grads2d, const gs_grads_t* grads,
-                                      int32_t accumulate, const gs_stats_t* stats, void* stream) {
+namespace gs {
+namespace {
+int preprocess_backward(const gs_params_t* params, const gs_camera_t* camera, int32_t active_sh_degree,
+                        const gs_splats_t* splats, const float* grads2d, const gs_grads_t* grads, int32_t accumulate,
+                        const gs_stats_t* stats, const int32_t* skip, void* stream) {
   if (!params || !camera || !splats || !grads2d || !grads) return GS_ERR_INVALID_ARG;
   if (active_sh_degree < 0 || active_sh_degree > 3) return GS_ERR_INVALID_ARG;
   if (splats->n != params->n) return GS_ERR_INVALID_ARG;
@@ -587,11 +590,32 @@ extern "C" int gs_preprocess_backward(const gs_params_t* params, const gs_camera
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   gs_stats_t st = {nullptr, nullptr, nullptr};
   if (stats) st = *stats;
-  const gs::DevCamera cam = gs::make_dev_camera(*camera);
+  const DevCamera cam = make_dev_camera(*camera);
   const int block = 128;
   const unsigned grid = unsigned((params->n + block - 1) / block);
-  gs::preprocess_bwd_kernel<<<grid, block, 0, s>>>(*params, cam, active_sh_degree,
-                                                   reinterpret_cast<const float4*>(splats->rec), splats->radii,
-                                                   reinterpret_cast<const float4*>(grads2d), *grads, accumulate, st);
-  return gs::check_launch();
+  preprocess_bwd_kernel<<<grid, block, 0, s>>>(*params, cam, active_sh_degree,
+                                               reinterpret_cast<const float4*>(splats->rec), splats->radii,
+                                               reinterpret_cast<const float4*>(grads2d), *grads, accumulate, st,
+                                               skip);
+  return check_launch();
+}
+}  // namespace
+}  // namespace gs
+
+extern "C" int gs_preprocess_backward(const gs_params_t* params, const gs_camera_t* camera, int32_t active_sh_degree,
+                                      const gs_splats_t* splats, const float* grads2d, const gs_grads_t* grads,
+                                      int32_t accumulate, const gs_stats_t* stats, void* stream) {
+  return gs::preprocess_backward(params, camera, active_sh_degree, splats, grads2d, grads, accumulate, stats, nullptr,
+                                 stream);
+}
+
+// The same, with the densify statistics left untouched when *skip != 0
+// (device int32 from gs_step_guard, e.g. reduced over the ranks): the
+// multi-view step enqueues its backward before the host has read the loss.
+extern "C" int gs_preprocess_backward_guarded(const gs_params_t* params, const gs_camera_t* camera,
+                                              int32_t active_sh_degree, const gs_splats_t* splats,
+                                              const float* grads2d, const gs_grads_t* grads, int32_t accumulate,
+                                              const gs_stats_t* stats, const int32_t* skip, void* stream) {
+  return gs::preprocess_backward(params, camera, active_sh_degree, splats, grads2d, grads, accumulate, stats, skip,
+                                 stream);
 }

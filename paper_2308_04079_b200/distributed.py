@@ -76,6 +76,19 @@ def reduce_stats_(stats: DensifyStats, group=None) -> None:
     dist.all_reduce(stats.max_radius_frac, op=dist.ReduceOp.MAX, group=group)
 
 
+def max_reduce_(t: torch.Tensor, group=None) -> torch.Tensor:
+    """In-place MAX all-reduce of a small device tensor (no host round trip
+    on NCCL; gloo stages it through the host)."""
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+        if dist.get_backend(group) == "nccl":
+            dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+        else:
+            h = t.cpu()
+            dist.all_reduce(h, op=dist.ReduceOp.MAX, group=group)
+            t.copy_(h)
+    return t
+
+
 def any_rank_(flag: bool, device, group=None) -> bool:
     """True on every rank when `flag` is true on any rank (MAX all-reduce)."""
     if not (dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1):
@@ -182,7 +195,9 @@ class ShardedAdam:
     The cloud's parameter tensors are re-homed into buffers padded to a
     multiple of the world size (the cloud keeps contiguous views of their
     first N rows).  The Gaussian count is fixed for the lifetime of the
-    object (densify/prune re-shards by building a new one)."""
+    object: densify / prune gathers the moments (full_moments), realigns them
+    with the cloud (densify_and_prune on replicated moments) and re-shards
+    (from_moments)."""
 
     def __init__(self, cloud, group=None):
         self.group = group
@@ -235,8 +250,9 @@ class ShardedAdam:
             parts = list(torch.split(full, self.per))
             dist.all_gather(parts, shard.clone(), group=self.group)
 
-    def step(self, cloud, iteration: int, config) -> None:
-        """Reduce-scatter the bucket, Adam on this rank's shard, all-gather."""
+    def step(self, cloud, iteration: int, config, skip: torch.Tensor | None = None) -> None:
+        """Reduce-scatter the bucket, Adam on this rank's shard, all-gather.
+        skip (device int32, the same on every rank): applies nothing."""
         from .optimizer import adam_step_tensors
         for g in PARAM_GROUPS:
             self._reduce_scatter(self.shard_grad[g], self.gbuf[g])
@@ -245,6 +261,31 @@ class ShardedAdam:
             adam_step_tensors({g: self.pbuf[g][self.lo:self.hi] for g in PARAM_GROUPS},
                               {g: self.shard_grad[g][:k] for g in PARAM_GROUPS},
                               {g: self.exp_avg[g][:k] for g in PARAM_GROUPS},
-                              {g: self.exp_avg_sq[g][:k] for g in PARAM_GROUPS}, iteration, config)
+                              {g: self.exp_avg_sq[g][:k] for g in PARAM_GROUPS}, iteration, config, skip=skip)
         for g in PARAM_GROUPS:
             self._all_gather(self.pbuf[g])
+
+    def full_moments(self) -> tuple[dict, dict]:
+        """Every rank's moment shards gathered into full (N, ...) tensors."""
+        out = []
+        for src in (self.exp_avg, self.exp_avg_sq):
+            full = {}
+            for g in PARAM_GROUPS:
+                buf = torch.zeros((self.per * self.world,) + _ROW_SHAPE[g], dtype=torch.float32,
+                                  device=src[g].device)
+                buf[self.rank * self.per:(self.rank + 1) * self.per].copy_(src[g])
+                self._all_gather(buf)
+                full[g] = buf[:self.n].contiguous()
+            out.append(full)
+        return out[0], out[1]
+
+    @classmethod
+    def from_moments(cls, cloud, exp_avg: dict, exp_avg_sq: dict, group=None) -> "ShardedAdam":
+        """A ShardedAdam for `cloud` whose shards start from full moments."""
+        sa = cls(cloud, group)
+        k = sa.hi - sa.lo
+        for g in PARAM_GROUPS:
+            if k > 0:
+                sa.exp_avg[g][:k].copy_(exp_avg[g][sa.lo:sa.hi])
+                sa.exp_avg_sq[g][:k].copy_(exp_avg_sq[g][sa.lo:sa.hi])
+        return sa

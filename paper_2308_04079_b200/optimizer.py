@@ -80,7 +80,7 @@ def _lr_table(t: int, config: "TrainConfig") -> dict:
 
 
 def adam_step_tensors(params: dict, grads: dict, exp_avg: dict, exp_avg_sq: dict, iteration: int,
-                      config: "TrainConfig") -> None:
+                      config: "TrainConfig", skip: torch.Tensor | None = None) -> None:
     """One gs_adam_step launch over explicit per-group tensors (contiguous
     row ranges of the groups, e.g. one rank's shard; the SH head LR applies to
     the first 3 of every 48 elements, so a range must start on a Gaussian)."""
@@ -102,8 +102,9 @@ def adam_step_tensors(params: dict, grads: dict, exp_avg: dict, exp_avg_sq: dict
         else:
             G.lr_head, G.period, G.head = lrs[name], 0, 0
     beta1, beta2 = config.adam_betas
-    _lib.check(_lib.load().gs_adam_step(groups, len(PARAM_GROUPS), beta1, beta2, config.adam_eps, bias1, bias2,
-                                        torch.cuda.current_stream().cuda_stream), "adam_step")
+    _lib.check(_lib.load().gs_adam_step_guarded(groups, len(PARAM_GROUPS), beta1, beta2, config.adam_eps, bias1,
+                                                bias2, _lib.ptr(skip), torch.cuda.current_stream().cuda_stream),
+               "adam_step")
 
 
 class DeviceAdam:
@@ -142,14 +143,17 @@ class DeviceAdam:
         beta1, beta2 = config.adam_betas
         return 1.0 - beta1**t, 1.0 - beta2**t
 
-    def step(self, cloud: GaussianCloud, grads: GaussianGrads, iteration: int, config: TrainConfig) -> None:
-        """One dense Adam step at `iteration` (= the bias-correction t)."""
+    def step(self, cloud: GaussianCloud, grads: GaussianGrads, iteration: int, config: TrainConfig,
+             skip: torch.Tensor | None = None) -> None:
+        """One dense Adam step at `iteration` (= the bias-correction t).
+        skip (device int32, e.g. from step_guard): applies nothing when set."""
         t = int(iteration)
         bias1, bias2 = self._bias(t, config)
         groups = self._groups(cloud, grads, t, config)
         beta1, beta2 = config.adam_betas
-        _lib.check(_lib.load().gs_adam_step(groups, len(PARAM_GROUPS), beta1, beta2, config.adam_eps, bias1, bias2,
-                                            torch.cuda.current_stream().cuda_stream), "adam_step")
+        _lib.check(_lib.load().gs_adam_step_guarded(groups, len(PARAM_GROUPS), beta1, beta2, config.adam_eps, bias1,
+                                                    bias2, _lib.ptr(skip), torch.cuda.current_stream().cuda_stream),
+                   "adam_step")
 
     def backward_step(self, cloud: GaussianCloud, camera, splats, grads2d, active_sh_degree: int, iteration: int,
                       config: TrainConfig, stats=None, grads_out: GaussianGrads | None = None,

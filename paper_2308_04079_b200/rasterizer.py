@@ -555,7 +555,8 @@ _BWD_SCHEDULE = __import__("os").environ.get("GS_BWD_SCHEDULE", "1") != "0"
 
 def _backward_project_tensors(params: _lib.GsParams, n: int, device, camera: Camera, splats: DeviceSplats,
                               grads2d: SplatGrads2D, active_sh_degree: int, stats: DensifyStats | None,
-                              out: GaussianGrads | None, accumulate: bool) -> GaussianGrads:
+                              out: GaussianGrads | None, accumulate: bool,
+                              skip: torch.Tensor | None = None) -> GaussianGrads:
     if not 0 <= active_sh_degree <= 3:
         raise ValueError(f"SH degree must be in 0..3, got {active_sh_degree}")
     lib = _lib.load()
@@ -567,22 +568,25 @@ def _backward_project_tensors(params: _lib.GsParams, n: int, device, camera: Cam
     cs = splats.c_struct()
     cg = out.c_struct()
     cst = stats.c_struct() if stats is not None else None
-    _lib.check(lib.gs_preprocess_backward(ctypes.byref(params), ctypes.byref(camera.to_c()), int(active_sh_degree),
-                                          ctypes.byref(cs), grads2d.packed.data_ptr(), ctypes.byref(cg),
-                                          int(bool(accumulate)), ctypes.byref(cst) if cst is not None else None,
-                                          _stream()), "backward_project")
+    _lib.check(lib.gs_preprocess_backward_guarded(ctypes.byref(params), ctypes.byref(camera.to_c()),
+                                                  int(active_sh_degree), ctypes.byref(cs), grads2d.packed.data_ptr(),
+                                                  ctypes.byref(cg), int(bool(accumulate)),
+                                                  ctypes.byref(cst) if cst is not None else None, _lib.ptr(skip),
+                                                  _stream()), "backward_project")
     return out
 
 
 def backward_project(cloud: GaussianCloud, camera, splats: DeviceSplats, grads2d: SplatGrads2D,
                      active_sh_degree: int = 3, *, stats: DensifyStats | None = None,
-                     out: GaussianGrads | None = None, accumulate: bool = False) -> GaussianGrads:
+                     out: GaussianGrads | None = None, accumulate: bool = False,
+                     skip: torch.Tensor | None = None) -> GaussianGrads:
     """K8: chain screen-space gradients to the raw parameters (gradients.py:192).
 
     `stats` (optional) receives the densification statistics update of
-    optimizer.py:252-255; `out` + `accumulate` sum several views in place."""
+    optimizer.py:252-255; `out` + `accumulate` sum several views in place;
+    `skip` (device int32 from step_guard) leaves the statistics untouched."""
     return _backward_project_tensors(cloud.c_params(), len(cloud), cloud.device, _camera(camera), splats, grads2d,
-                                     active_sh_degree, stats, out, accumulate)
+                                     active_sh_degree, stats, out, accumulate, skip)
 
 
 def render_view(cloud: GaussianCloud, camera, background, active_sh_degree: int = 3, training: bool = False):

@@ -20,7 +20,7 @@ import torch
 from . import rasterizer as R
 from .camera import Camera
 from .densify import DensifyReport, TrainState, densify_and_prune
-from .errors import TrainingDiverged
+from .errors import InvalidPrimitiveError, TrainingDiverged
 from .loss import l1_dssim_loss
 from .optimizer import TrainConfig, step_guard
 
@@ -350,56 +350,91 @@ def train_step(state: TrainState, views: Sequence[TrainView], config: TrainConfi
 
 def _train_step_sharded(state: TrainState, views: Sequence[TrainView], config: TrainConfig, group, world: int,
                         rank: int) -> StepReport:
-    from .distributed import GradientBucket, shard_views
+    """The view-parallel step: this rank's view of its shard,
+    the backward into one flat gradient bucket, one NCCL all-reduce (or, with
+    state.shard_optimizer, a reduce-scatter into ZeRO-1 sharded Adam and an
+    all-gather), the identical update on every rank.  No host wait before the
+    update: every rank's step guard (loss not finite, instance capacity, zero
+    quaternion) is MAX-reduced over the ranks on the device, and the
+    statistics and Adam apply nothing when any rank vetoed; the host reads the
+    reduced verdict once at the end, so every rank raises (or retries a
+    capacity overflow) together."""
+    from .distributed import GradientBucket, ShardedAdam, max_reduce_, shard_views
     state.discard_lookahead()
-    state.iteration += 1
-    it = state.iteration
-    state.active_sh_degree = _degree_for(state.active_sh_degree, it, config)
+    it = state.iteration + 1
+    degree = _degree_for(state.active_sh_degree, it, config)
     shard = shard_views(len(views), world, rank)
     view_idx = shard[next_view(state, len(shard))]
     view = views[view_idx]
     scale = warmup_scale(it, config.warmup_upsample_iters)
     camera = view.camera if scale == 1.0 else view.camera.scaled(scale)
     device = state.cloud.device
-    image, consumed = view.image, None
-    if image.device != device:
-        pf = _prefetchers.setdefault(str(device), _ImagePrefetcher(device))
-        image, consumed = pf.get(view)
+    gt, consumed = _ground_truth(state, view, camera)
+    if view.image.device != device:
         nxt = _peek_next_view(state, len(shard))
         nxt = None if nxt is None else shard[nxt]
         if nxt is not None and views[nxt].image.device != device:
-            pf.prefetch(views[nxt])
-    gt = downscale_image(image, camera.height, camera.width)
+            _prefetchers[str(device)].prefetch(views[nxt])
     bg = config.background
     host = _host_scalars.setdefault(str(device), _HostScalars())
+    n = len(state.cloud)
+    sharded = None
+    if getattr(state, "shard_optimizer", False):
+        sharded = getattr(state, "_sharded", None)
+        if sharded is None or sharded.n != n:
+            sharded = state._sharded = ShardedAdam.from_moments(state.cloud, state.adam.exp_avg,
+                                                                 state.adam.exp_avg_sq, group)
+        grads = sharded.grads
+    else:
+        bucket = getattr(state, "_bucket", None)
+        if bucket is None or bucket.n != n:
+            bucket = state._bucket = GradientBucket(n, device)
+        grads = bucket.grads
     for attempt in range(3):
-        out, splats, binning = R.render_view_async(state.cloud, camera, bg, state.active_sh_degree, training=True)
+        out, splats, binning = R.render_view_async(state.cloud, camera, bg, degree, training=True)
         loss, d_image = l1_dssim_loss(out.image, gt, config.lambda_dssim)
         if consumed is not None:
             consumed.record()
-        lvals, kvals = host.read(loss, binning.k_info)
-        try:
-            binning.check_host(kvals)
+        step_guard(loss, binning.k_info, host.skip_device(device), report=host.report)
+        # every rank's verdict, bit by bit: [zero quaternion, capacity, instance limit, loss not finite]
+        fl = binning.k_info[1]
+        verdict = torch.stack([(fl & 1) != 0, (fl & 2) != 0, (fl & 4) != 0, ~torch.isfinite(loss[0])]).to(torch.int32)
+        max_reduce_(verdict, group)
+        skip = verdict.amax().reshape(1).contiguous()
+        g2 = R.render_backward(d_image, out, splats, binning, camera.width, camera.height, bg,
+                               deterministic=config.deterministic)
+        if sharded is not None:
+            sharded.zero_()
+        else:
+            bucket.zero_()
+        R.backward_project(state.cloud, camera, splats, g2, degree, stats=state.stats, out=grads, accumulate=True,
+                           skip=skip)
+        if sharded is not None:
+            sharded.step(state.cloud, it, config, skip=skip)
+        else:
+            bucket.allreduce_(group)
+            state.adam.step(state.cloud, grads, it, config, skip=skip)
+        zero_q, capacity, limit, nonfinite = (int(v) for v in verdict.tolist())   # the step's one host read
+        lvals, kvals = host.report_values()
+        # every rank takes the same branch
+        if nonfinite:
+            raise TrainingDiverged(f"non-finite loss {lvals[0]} at iteration {it}"
+                                   + ("" if not math.isfinite(lvals[0]) else " (on another rank)"))
+        if zero_q:
+            raise InvalidPrimitiveError("zero-norm quaternion cannot be normalized")
+        if limit:
+            from . import _lib
+            _lib.check(_lib.GS_ERR_RESOURCE_LIMIT, "bin_and_sort")
+        if not capacity:
             break
+        try:   # a rank that overflowed raises its capacity hint; every rank re-renders its view
+            binning.check_host(kvals)
         except R.CapacityError:
-            if attempt == 2:
-                raise
+            pass
+        if attempt == 2:
+            raise R.CapacityError("bin_and_sort: instance capacity did not converge")
+    state.iteration, state.active_sh_degree = it, degree
     value, mse = float(lvals[0]), float(lvals[3])
-    # every rank must take the same branch: one rank's non-finite loss stops all of them
-    from .distributed import any_rank_
-    if any_rank_(not math.isfinite(value), device, group):
-        raise TrainingDiverged(f"non-finite loss {value} at iteration {it}"
-                               + ("" if not math.isfinite(value) else " (on another rank)"))
-    g2 = R.render_backward(d_image, out, splats, binning, camera.width, camera.height, bg,
-                           deterministic=config.deterministic)
-    bucket = getattr(state, "_bucket", None)
-    if bucket is None or bucket.n != len(state.cloud):
-        bucket = state._bucket = GradientBucket(len(state.cloud), device)
-    bucket.zero_()
-    R.backward_project(state.cloud, camera, splats, g2, state.active_sh_degree, stats=state.stats,
-                       out=bucket.grads, accumulate=True)
-    bucket.allreduce_(group)
-    state.adam.step(state.cloud, bucket.grads, it, config)
     psnr = float("inf") if mse == 0.0 else 10.0 * math.log10(1.0 / mse)
     return StepReport(it, value, psnr, view_idx, len(state.cloud))
 
@@ -434,6 +469,10 @@ def train(state: TrainState, views: Sequence[TrainView], config: TrainConfig, *,
                     from .distributed import reduce_stats_, sync_rng_
                     reduce_stats_(state.stats, group)
                     sync_rng_(state, group)
+                    sharded = getattr(state, "_sharded", None)
+                    if sharded is not None:   # ZeRO-1: realign the full moments, re-shard next step
+                        state.adam.exp_avg, state.adam.exp_avg_sq = sharded.full_moments()
+                        state._sharded = None
                 report = densify_and_prune(state, config)
                 reports.append(report)
                 if densify_hook:

@@ -1,6 +1,7 @@
-"""Multi-process (gloo, world size 2, CPU) tests of the view-parallel plumbing:
-view sharding, the flat gradient bucket and its all-reduce, and the
-cross-rank densification statistics."""
+"""Multi-process (gloo, world sizes 2 and 4, CPU) tests of the view-parallel
+plumbing: view sharding, the flat gradient bucket and its all-reduce, the
+cross-rank densification statistics, the rank-reduced step verdict and the
+shared training RNG."""
 import os
 import socket
 
@@ -9,8 +10,8 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2308_04079_b200.distributed import (FLOATS_PER_GAUSSIAN, GradientBucket, reduce_stats_,
-                                                shard_views)
+from paper_2308_04079_b200.distributed import (FLOATS_PER_GAUSSIAN, GradientBucket, any_rank_, max_reduce_,
+                                                reduce_stats_, shard_views, sync_rng_)
 from paper_2308_04079_b200.rasterizer import DensifyStats
 
 
@@ -83,3 +84,57 @@ def test_shard_views_partition(views, world):
     flat = [v for s in shards for v in s]
     assert flat == list(range(views))
     assert max(map(len, shards)) - min(map(len, shards)) <= 1
+
+
+def _worker4(rank, world, port, results):
+    """World size 4: every rank holds a different shard of a 32-view batch,
+    accumulates one gradient per view into its bucket, and the reduced bucket
+    equals the sum over all 32 views; the step verdict is the union of the
+    ranks' flags; the shared RNG leaves every rank with rank 0's state."""
+    import numpy as np
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        n = 7
+        mine = shard_views(32, world, rank)
+        bucket = GradientBucket(n, "cpu")
+        for v in mine:   # per-view gradients accumulate before the reduction
+            bucket.grads.d_means += float(v + 1)
+            bucket.grads.d_sh[:, 3, 1] += 0.5
+        bucket.allreduce_()
+        stats = DensifyStats(torch.full((n,), 1.0), torch.full((n,), len(mine), dtype=torch.int32),
+                             torch.full((n,), 0.01 * (rank + 1)))
+        reduce_stats_(stats)
+        verdict = torch.tensor([1 if rank == 2 else 0, 0, 1 if rank == 3 else 0, 0], dtype=torch.int32)
+        max_reduce_(verdict)
+
+        class _S:
+            rng = np.random.default_rng(100 + rank)
+        st = _S()
+        sync_rng_(st)
+        results[rank] = {"views": mine, "means": bucket.grads.d_means.clone(), "sh": bucket.grads.d_sh[:, 3, 1].clone(),
+                         "accum": stats.accum_pos_grad.clone(), "count": stats.accum_count.clone(),
+                         "maxr": stats.max_radius_frac.clone(), "verdict": verdict.tolist(),
+                         "any": any_rank_(rank == 1, "cpu"), "draw": float(st.rng.standard_normal())}
+    finally:
+        dist.destroy_process_group()
+
+
+def test_view_parallel_plumbing_world4():
+    import numpy as np
+    world = 4
+    port = _free_port()
+    with mp.Manager() as mgr:
+        results = mgr.dict()
+        mp.spawn(_worker4, args=(world, port, results), nprocs=world, join=True)
+        res = dict(results)
+    assert sorted(v for r in range(world) for v in res[r]["views"]) == list(range(32))
+    expect = float(sum(range(1, 33)))
+    for r in range(world):
+        assert torch.all(res[r]["means"] == expect)
+        assert torch.all(res[r]["sh"] == 16.0)
+        assert torch.all(res[r]["accum"] == 4.0) and torch.all(res[r]["count"] == 32)
+        assert torch.allclose(res[r]["maxr"], torch.full((7,), 0.04))
+        assert res[r]["verdict"] == [1, 0, 1, 0] and res[r]["any"] is True
+        assert res[r]["draw"] == float(np.random.default_rng(100).standard_normal())

@@ -236,3 +236,71 @@ def test_two_ranks_train_across_densify_stay_identical(cuda_device, tmp_path):
     for k in r0["params"]:
         assert torch.equal(r0["params"][k], r1["params"][k]), k
     assert [c[0] for c in r0["ckpts"]] == [4, 7] and all(c[2] for c in r0["ckpts"])
+
+
+def _zero1_worker(rank, world, port, out_dir, sharded, nan_rank):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch.distributed as dist
+    from paper_2308_04079_b200 import rasterizer as R
+    from paper_2308_04079_b200.camera import Camera
+    from paper_2308_04079_b200.cloud import GaussianCloud
+    from paper_2308_04079_b200.densify import TrainState
+    from paper_2308_04079_b200.errors import TrainingDiverged
+    from paper_2308_04079_b200.optimizer import TrainConfig
+    from paper_2308_04079_b200.training import TrainView, train, train_step
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        cloud_np, tgt_np, cam = _scene()
+        tgt = GaussianCloud.from_numpy(**tgt_np)
+        cams = [Camera(np.eye(3), np.array([0.03 * i, -0.02 * i, 0.0]), cam.fx, cam.fy, cam.cx, cam.cy, cam.width,
+                       cam.height, cam.near) for i in range(4)]
+        views = [TrainView(c, R.render_view(tgt, c, (0, 0, 0), 3)[0].image) for c in cams]
+        state = TrainState(GaussianCloud.from_numpy(**cloud_np), 2.0, seed=0)
+        state.shard_optimizer = sharded
+        # deterministic backward: the two runs (separate processes) must not
+        # differ by float-atomic order
+        cfg = TrainConfig(warmup_upsample_iters=(0, 0), densify_start=0, densify_interval=3,
+                          densify_grad_threshold=2e-6, deterministic=True)
+        if nan_rank is not None:   # one rank's view diverges: every rank must raise, none may hang
+            train_step(state, views, cfg)
+            bad = [TrainView(v.camera, v.image.clone()) for v in views]
+            if rank == nan_rank:
+                for v in bad:
+                    v.image[0, 0, 0] = float("nan")
+            try:
+                train_step(state, bad, cfg)
+                raised = False
+            except TrainingDiverged:
+                raised = True
+            torch.save({"raised": raised}, os.path.join(out_dir, f"nan{rank}.pt"))
+            return
+        reports = train(state, views, cfg, iterations=7)
+        torch.save({"params": {g: getattr(state.cloud, g).cpu() for g in ("means", "sh", "opacity_logits")},
+                    "n": len(state.cloud), "reports": [(r.cloned, r.split, r.pruned) for r in reports]},
+                   os.path.join(out_dir, f"z{int(sharded)}_{rank}.pt"))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_zero1_training_across_densify_matches_replicated(cuda_device, tmp_path):
+    """state.shard_optimizer: reduce-scatter + Adam on 1/G of the Gaussians +
+    all-gather, re-sharded after every densification (moments gathered,
+    realigned, re-sharded): bit-identical to the replicated all-reduce path."""
+    import torch.multiprocessing as mp
+    for sharded in (False, True):
+        mp.start_processes(_zero1_worker, args=(2, _free_port(), str(tmp_path), sharded, None), nprocs=2,
+                           start_method="spawn")
+    res = {(s, r): torch.load(tmp_path / f"z{s}_{r}.pt") for s in (0, 1) for r in (0, 1)}
+    assert res[(1, 0)]["reports"] == res[(0, 0)]["reports"] and sum(c + s for c, s, _ in res[(1, 0)]["reports"]) > 0
+    for r in (0, 1):
+        assert res[(1, r)]["n"] == res[(0, r)]["n"]
+        for k in res[(0, 0)]["params"]:
+            assert torch.equal(res[(1, r)]["params"][k], res[(0, 0)]["params"][k]), (r, k)
+
+
+def test_one_rank_diverging_raises_on_every_rank(cuda_device, tmp_path):
+    import torch.multiprocessing as mp
+    mp.start_processes(_zero1_worker, args=(2, _free_port(), str(tmp_path), False, 1), nprocs=2,
+                       start_method="spawn")
+    assert all(torch.load(tmp_path / f"nan{r}.pt")["raised"] for r in (0, 1))
