@@ -200,7 +200,9 @@ blend_bwd_kernel(const float* __restrict__ d_image, const float4* __restrict__ r
   if (t == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full_bar[s], 32);
-      mbar_init(&empty_bar[s], kConsumerWarps);
+      // deterministic mode: every consumer lane arrives (each releases its own
+      // partial-row writes to the producer that combines them)
+      mbar_init(&empty_bar[s], kDet ? kConsumerWarps * 32 : kConsumerWarps);
     }
   }
   __syncthreads();
@@ -361,7 +363,7 @@ blend_bwd_kernel(const float* __restrict__ d_image, const float4* __restrict__ r
       }
     }
     __syncwarp();
-    if (lane == 0) mbar_arrive(&empty_bar[s]);
+    if (kDet || lane == 0) mbar_arrive(&empty_bar[s]);
   }
 }
 
