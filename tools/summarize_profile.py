@@ -23,6 +23,11 @@ PROFILES = ROOT / "profiles"
 STAGE_OF = {"blend_bwd_kernel": "blend_bwd", "blend_fwd_kernel": "blend_fwd",
             "preprocess_bwd_adam_kernel": "preprocess_bwd_adam", "preprocess_bwd_kernel": "preprocess_bwd",
             "preprocess_fwd_kernel": "preprocess_fwd", "adam_kernel": "adam"}
+# the binning is several kernels per frame: its traffic is summed per frame
+# (frames = launches of the last binning kernel, tile_ranges_kernel)
+BIN_KERNELS = ("depth_hist_kernel", "onesweep_kernel", "sort_setup_kernel", "bucket_count_kernel", "scan_kernel",
+               "bucket_scatter_kernel", "window_setup_kernel", "window_count_kernel", "window_prefix_kernel",
+               "instance_write", "tile_ranges_kernel")
 METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
            "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
            "smsp__issue_active.avg.pct_of_peak_sustained_active",
@@ -71,6 +76,7 @@ def full(rep: Path, tag: str, desc: str) -> dict:
            "| kernel | time ms | DRAM rd+wr MB | DRAM % | issue % | warps % | regs | FMA % | warp instr | top stalls |",
            "|---|---|---|---|---|---|---|---|---|---|"]
     traffic = defaultdict(list)
+    bin_bytes, bin_frames = 0.0, 0
     for r in rows[2:]:
         name = short(r[ki])
         val = {m: r[h.index(m)] for m in METRICS if m in h}
@@ -89,8 +95,14 @@ def full(rep: Path, tag: str, desc: str) -> dict:
         stage = next((s for k, s in STAGE_OF.items() if name.startswith(k)), None)
         if stage:
             traffic[stage].append(rd + wr)
+        if name.startswith(BIN_KERNELS):
+            bin_bytes += rd + wr
+            bin_frames += name.startswith("tile_ranges_kernel")
     (PROFILES / f"{tag}_ncu_full.md").write_text("\n".join(out) + "\n")
-    return {k: sum(v) / len(v) for k, v in traffic.items()}
+    res = {k: sum(v) / len(v) for k, v in traffic.items()}
+    if bin_frames:
+        res["bin_and_sort"] = bin_bytes / bin_frames
+    return res
 
 
 def main() -> None:
