@@ -61,7 +61,10 @@ constexpr uint64_t kStAgg = uint64_t(1) << 32, kStPre = uint64_t(2) << 32;
 // super-tile buckets and walk windows
 constexpr int kMaxSuper = 4096;                 // bucket scatter keeps kWarps x S cursors in smem
 constexpr int kChunk = 4096;                    // Gaussians per bucketing block (512 per warp)
-constexpr int kWindow = 512;                    // bucket entries per walk window
+#ifndef GS_BIN_WINDOW
+#define GS_BIN_WINDOW 1024
+#endif
+constexpr int kWindow = GS_BIN_WINDOW;          // bucket entries per walk window
 constexpr uint32_t kEmptyRect = 0x0000FFFFu;    // packed local rect that covers nothing (x0 = y0 = 255 > x1 = y1 = 0)
 
 struct Grid {
@@ -119,8 +122,16 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
 // with valid set; invalid lanes get 0): one ballot per bit.  MATCH.ANY does
 // the same in one instruction but issues at a small fraction of the ballot
 // rate on sm_100.
+#ifndef GS_BIN_MATCH
+#define GS_BIN_MATCH 0
+#endif
 template <int BITS>
 __device__ __forceinline__ uint32_t peer_mask(uint32_t v, bool valid) {
+  if (GS_BIN_MATCH) {
+    // invalid lanes get a value no valid lane can hold
+    const uint32_t m = __match_any_sync(0xffffffffu, valid ? v : 0xFFFFFFFFu);
+    return valid ? m : 0u;
+  }
   uint32_t peers = __ballot_sync(0xffffffffu, valid);
 #pragma unroll
   for (int i = 0; i < BITS; ++i) {
@@ -171,28 +182,54 @@ __device__ __forceinline__ uint32_t depth_key(const float* depth, const int32_t*
 }
 
 // Digit histograms of all four passes + K = sum of tiles_touched (u64).
+// kHistItems consecutive Gaussians per thread, loaded as vectors up front
+// (one memory round trip per thread instead of a dependent grid-stride loop).
+constexpr int kHistItems = 8;
 __global__ void __launch_bounds__(kThreads) depth_hist_kernel(const float* __restrict__ depth,
                                                              const int32_t* __restrict__ tiles, int64_t n,
                                                              uint32_t* __restrict__ hist, int64_t* __restrict__ kinfo) {
   __shared__ uint32_t s_h[kPasses * kRadix];
   for (int i = threadIdx.x; i < kPasses * kRadix; i += kThreads) s_h[i] = 0;
   __syncthreads();
-  uint64_t ksum = 0;
-  for (int64_t g = int64_t(blockIdx.x) * kThreads + threadIdx.x; g < n; g += int64_t(gridDim.x) * kThreads) {
-    const int32_t t = tiles[g];
-    const uint32_t key = t > 0 ? __float_as_uint(depth[g]) : kCulledKey;
-    ksum += t > 0 ? uint64_t(t) : 0u;
-    // the high digits of a warp's depths often coincide: then one atomic for the warp
-    const uint32_t active = __activemask();
-    const int leader = __ffs(active) - 1;
+  const int64_t i0 = (int64_t(blockIdx.x) * kThreads + threadIdx.x) * kHistItems;
+  uint32_t dk[kHistItems];
+  int32_t tt[kHistItems];
+  const bool vec = i0 + kHistItems <= n && ((reinterpret_cast<uintptr_t>(depth) | reinterpret_cast<uintptr_t>(tiles)) & 15u) == 0;
+  if (vec) {
 #pragma unroll
-    for (int p = 0; p < kPasses; ++p) {
-      const uint32_t d = (key >> (8 * p)) & 0xFFu;
-      if (__all_sync(active, d == __shfl_sync(active, d, leader))) {
-        if ((threadIdx.x & 31) == leader) atomicAdd(&s_h[p * kRadix + d], uint32_t(__popc(active)));
-      } else {
-        atomicAdd(&s_h[p * kRadix + d], 1u);
-      }
+    for (int q = 0; q < kHistItems / 4; ++q) {
+      const uint4 d4 = reinterpret_cast<const uint4*>(depth + i0)[q];
+      const int4 t4 = reinterpret_cast<const int4*>(tiles + i0)[q];
+      dk[4 * q] = d4.x; dk[4 * q + 1] = d4.y; dk[4 * q + 2] = d4.z; dk[4 * q + 3] = d4.w;
+      tt[4 * q] = t4.x; tt[4 * q + 1] = t4.y; tt[4 * q + 2] = t4.z; tt[4 * q + 3] = t4.w;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < kHistItems; ++j) {
+      const bool ok = i0 + j < n;
+      dk[j] = ok ? __float_as_uint(depth[i0 + j]) : 0u;
+      tt[j] = ok ? tiles[i0 + j] : -1;   // -1: past the end, not counted
+    }
+  }
+  uint64_t ksum = 0;
+#pragma unroll
+  for (int j = 0; j < kHistItems; ++j) {
+    const bool ok = tt[j] >= 0;
+    const uint32_t key = tt[j] > 0 ? dk[j] : kCulledKey;
+    ksum += tt[j] > 0 ? uint64_t(tt[j]) : 0u;
+    // the top digit takes a handful of values per frame: one atomic per
+    // distinct value of the warp; the lower digits are spread over the bins
+    uint32_t todo = __ballot_sync(0xffffffffu, ok);
+    const uint32_t top = key >> 24;
+    while (todo) {
+      const uint32_t v = __shfl_sync(0xffffffffu, top, __ffs(todo) - 1);
+      const uint32_t m = __ballot_sync(0xffffffffu, ok && top == v) & todo;
+      if ((threadIdx.x & 31) == __ffs(todo) - 1) atomicAdd(&s_h[3 * kRadix + v], uint32_t(__popc(m)));
+      todo &= ~m;
+    }
+    if (ok) {
+#pragma unroll
+      for (int p = 0; p < kPasses - 1; ++p) atomicAdd(&s_h[p * kRadix + ((key >> (8 * p)) & 0xFFu)], 1u);
     }
   }
 #pragma unroll
@@ -242,7 +279,13 @@ __global__ void __launch_bounds__(1024) sort_setup_kernel(const uint32_t* __rest
 // order and gathers the tile rectangles (empty rect for Gaussians without
 // instances).
 template <bool kFirst, bool kLast>
-__global__ void __launch_bounds__(kThreads, 2) onesweep_kernel(
+#ifndef GS_SORT_RANK_OR
+#define GS_SORT_RANK_OR 1
+#endif
+#ifndef GS_SORT_MIN_BLOCKS
+#define GS_SORT_MIN_BLOCKS 3
+#endif
+__global__ void __launch_bounds__(kThreads, GS_SORT_MIN_BLOCKS) onesweep_kernel(
     const float* __restrict__ depth, const int32_t* __restrict__ tiles, const int4* __restrict__ rect,
     const uint32_t* __restrict__ keys_in, const uint32_t* __restrict__ ids_in, uint32_t* __restrict__ keys_out,
     uint32_t* __restrict__ ids_out, int4* __restrict__ drect_out, const uint32_t* __restrict__ digit_base,
@@ -257,7 +300,13 @@ __global__ void __launch_bounds__(kThreads, 2) onesweep_kernel(
   if (kinfo[1] != 0) return;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) s_block = atomicAdd(ticket, 1u);
-  for (int i = tid; i < kWarps * kRadix; i += kThreads) (&s_cnt[0][0])[i] = 0u;
+  // peer masks by shared-memory OR: the ranking phase borrows s_keys as
+  // [kWarps][kRadix] bitmask bins (lane bits), cleared again by each digit's leader
+  uint32_t* bins = s_keys + warp * kRadix;
+  for (int i = tid; i < kWarps * kRadix; i += kThreads) {
+    (&s_cnt[0][0])[i] = 0u;
+    if (GS_SORT_RANK_OR) s_keys[i] = 0u;
+  }
   __syncthreads();
   const uint32_t b = s_block;
   const int64_t base = int64_t(b) * kSortTile + warp * (32 * kItems);
@@ -278,11 +327,22 @@ __global__ void __launch_bounds__(kThreads, 2) onesweep_kernel(
   for (int j = 0; j < kItems; ++j) {
     const bool ok = base + j * 32 + lane < n;
     const uint32_t d = (key[j] >> shift) & 0xFFu;
-    const uint32_t peers = peer_mask<8>(d, ok);
+    uint32_t peers;
+    if (GS_SORT_RANK_OR) {
+      // the lanes holding digit d set their bits in bins[d]; OR is order-free
+      if (ok) atomicOr(&bins[d], 1u << lane);
+      __syncwarp();
+      peers = ok ? bins[d] : 0u;
+    } else {
+      peers = peer_mask<8>(d, ok);
+    }
     const uint32_t c = ok ? s_cnt[warp][d] : 0u;
     rank[j] = c + __popc(peers & lt);
     __syncwarp();
-    if (ok && lane == 31 - __clz(peers)) s_cnt[warp][d] = c + __popc(peers);
+    if (ok && lane == 31 - __clz(peers)) {
+      s_cnt[warp][d] = c + __popc(peers);
+      if (GS_SORT_RANK_OR) bins[d] = 0u;
+    }
     __syncwarp();
   }
   __syncthreads();
@@ -321,14 +381,37 @@ __global__ void __launch_bounds__(kThreads, 2) onesweep_kernel(
   __syncthreads();
   const int64_t left = n - int64_t(b) * kSortTile;
   const int cnt = left < kSortTile ? int(left) : kSortTile;
-  for (int i = tid; i < cnt; i += kThreads) {
-    const uint32_t k = s_keys[i], v = s_vals[i];
-    const uint32_t pos = uint32_t(i) + s_delta[(k >> shift) & 0xFFu];
-    ids_out[pos] = v;
-    if (kLast)
-      drect_out[pos] = k != kCulledKey ? rect[v] : make_int4(0, 0, -1, -1);
-    else
+  if (kLast) {
+    // the rectangle gathers are random 16-byte reads: issue a group of them
+    // before any store so their latencies overlap
+    constexpr int kGroup = 8;
+#pragma unroll 1
+    for (int i0 = 0; i0 < kItems; i0 += kGroup) {
+      int4 rc[kGroup];
+      uint32_t pos[kGroup], v[kGroup];
+#pragma unroll
+      for (int u = 0; u < kGroup; ++u) {
+        const int i = tid + (i0 + u) * kThreads;
+        const bool ok = i < cnt;
+        const uint32_t k = ok ? s_keys[i] : kCulledKey;
+        v[u] = ok ? s_vals[i] : 0u;
+        pos[u] = ok ? uint32_t(i) + s_delta[(k >> shift) & 0xFFu] : 0xFFFFFFFFu;
+        rc[u] = (ok && k != kCulledKey) ? rect[v[u]] : make_int4(0, 0, -1, -1);
+      }
+#pragma unroll
+      for (int u = 0; u < kGroup; ++u)
+        if (pos[u] != 0xFFFFFFFFu) {
+          ids_out[pos[u]] = v[u];
+          drect_out[pos[u]] = rc[u];
+        }
+    }
+  } else {
+    for (int i = tid; i < cnt; i += kThreads) {
+      const uint32_t k = s_keys[i], v = s_vals[i];
+      const uint32_t pos = uint32_t(i) + s_delta[(k >> shift) & 0xFFu];
+      ids_out[pos] = v;
       keys_out[pos] = k;
+    }
   }
 }
 
@@ -485,12 +568,13 @@ __global__ void __launch_bounds__(1024) window_setup_kernel(const uint32_t* __re
 // rectangle clipped to the super-tile, local tile coordinates packed
 // x0 | y0 << 8 | x1 << 16 | y1 << 24).  (Staging the block's entries in
 // shared memory for coalesced writes measured slower: 116-133 vs 96 us at c3.)
+template <bool kOrBins>
 __global__ void __launch_bounds__(kThreads) bucket_scatter_kernel(const int4* __restrict__ drect,
                                                                  const uint32_t* __restrict__ order, int64_t n, Grid g,
                                                                  const uint32_t* __restrict__ M, int64_t chunks,
                                                                  uint2* __restrict__ entries, int64_t capacity,
                                                                  const int64_t* __restrict__ kinfo) {
-  extern __shared__ uint32_t s_cur[];   // [kWarps][S]
+  extern __shared__ uint32_t s_cur[];   // [kWarps][S] cursors, then [kWarps][S] bytes of bucket stamps
   if (kinfo[1] != 0) return;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int S = g.S;
@@ -498,6 +582,10 @@ __global__ void __launch_bounds__(kThreads) bucket_scatter_kernel(const int4* __
   __syncthreads();
   const int64_t rw = int64_t(blockIdx.x) * kChunk + warp * (kChunk / kWarps);
   uint32_t* cur = s_cur + warp * S;
+  uint8_t* stamp = reinterpret_cast<uint8_t*>(s_cur + kWarps * S) + warp * S;
+  uint32_t* bins = s_cur + kWarps * S + warp * S;   // kOrBins: [kWarps][S] lane bitmasks
+  if (kOrBins)
+    for (int i = tid; i < kWarps * S; i += kThreads) s_cur[kWarps * S + i] = 0u;
   for (int i = 0; i < kChunk / kWarps; i += 32) {
     const int64_t r = rw + i + lane;
     if (r < n) {
@@ -530,6 +618,8 @@ __global__ void __launch_bounds__(kThreads) bucket_scatter_kernel(const int4* __
     const SuperRect q = super_rect(rc, g);
     const int nsx = q.x1 - q.x0 + 1;
     const uint32_t cnt = q.x1 >= q.x0 ? uint32_t(nsx * (q.y1 - q.y0 + 1)) : 0u;
+    // jj / nsx = umulhi(jj, ceil(2^32 / nsx)), exact for jj * nsx < 2^32
+    const uint32_t magic = nsx > 1 ? 0xFFFFFFFFu / uint32_t(nsx) + 1u : 0u;
     const uint32_t end = warp_inclusive_sum(cnt);   // non-decreasing over the lanes
     const uint32_t off = end - cnt;
     const uint32_t tot = __shfl_sync(0xffffffffu, end, 31);
@@ -544,6 +634,7 @@ __global__ void __launch_bounds__(kThreads) bucket_scatter_kernel(const int4* __
       owner = min(owner, 31);
       const uint32_t jj = o - __shfl_sync(0xffffffffu, off, owner);
       const int onsx = __shfl_sync(0xffffffffu, nsx, owner);
+      const uint32_t omagic = __shfl_sync(0xffffffffu, magic, owner);
       const int ox0 = __shfl_sync(0xffffffffu, q.x0, owner);
       const int oy0 = __shfl_sync(0xffffffffu, q.y0, owner);
       const int rx0 = __shfl_sync(0xffffffffu, rc.x, owner);
@@ -554,18 +645,53 @@ __global__ void __launch_bounds__(kThreads) bucket_scatter_kernel(const int4* __
       const bool valid = o < tot;
       int s = 0, bx = 0, by = 0;
       if (valid) {
-        const int jy = onsx == 1 ? int(jj) : int(jj) / onsx;
+        const int jy = onsx == 1 ? int(jj) : int(__umulhi(jj, omagic));
         bx = ox0 + int(jj) - jy * onsx;
         by = oy0 + jy;
         s = by * g.sx + bx;
       }
-      const uint32_t peers = peer_mask<12>(uint32_t(s), valid);
-      const uint32_t c = valid ? cur[s] : 0u;
+      uint32_t pos = 0;
+      if (kOrBins) {
+        // peer masks by shared-memory OR into per-warp bucket bins (order-free)
+        if (valid) atomicOr(&bins[s], 1u << lane);
+        __syncwarp();
+        const uint32_t peers = valid ? bins[s] : 0u;
+        const uint32_t c = valid ? cur[s] : 0u;
+        pos = c + __popc(peers & lt);
+        __syncwarp();
+        if (valid && lane == 31 - __clz(peers)) {
+          cur[s] = c + __popc(peers);
+          bins[s] = 0u;
+        }
+        __syncwarp();
+        if (valid) {
+          const int tx0 = bx * sw, ty0 = by * sh;
+          const uint32_t lx0 = uint32_t(max(rx0, tx0) - tx0), ly0 = uint32_t(max(ry0, ty0) - ty0);
+          const uint32_t lx1 = uint32_t(min(rx1, tx0 + sw - 1) - tx0), ly1 = uint32_t(min(ry1, ty0 + sh - 1) - ty0);
+          if (int64_t(pos) < capacity) entries[pos] = make_uint2(og, lx0 | (ly0 << 8) | (lx1 << 16) | (ly1 << 24));
+        }
+        continue;
+      }
+      // the warp's 32 pairs usually lie in 32 distinct buckets: detect a
+      // shared bucket with a byte stamp per bucket (a lane whose stamp was
+      // overwritten shares its bucket), and rank by lane only then
+      if (valid) stamp[s] = uint8_t(lane);
       __syncwarp();
-      if (valid && lane == 31 - __clz(peers)) cur[s] = c + __popc(peers);
+      const bool shared = valid && stamp[s] != uint8_t(lane);
+      if (!__any_sync(0xffffffffu, shared)) {
+        if (valid) {
+          pos = cur[s];
+          cur[s] = pos + 1u;
+        }
+      } else {
+        const uint32_t peers = peer_mask<12>(uint32_t(s), valid);
+        const uint32_t c = valid ? cur[s] : 0u;
+        __syncwarp();
+        if (valid && lane == 31 - __clz(peers)) cur[s] = c + __popc(peers);
+        pos = c + __popc(peers & lt);
+      }
       __syncwarp();
       if (valid) {
-        const uint32_t pos = c + __popc(peers & lt);
         const int tx0 = bx * sw, ty0 = by * sh;
         const uint32_t lx0 = uint32_t(max(rx0, tx0) - tx0), ly0 = uint32_t(max(ry0, ty0) - ty0);
         const uint32_t lx1 = uint32_t(min(rx1, tx0 + sw - 1) - tx0), ly1 = uint32_t(min(ry1, ty0 + sh - 1) - ty0);
@@ -828,6 +954,7 @@ __global__ void __launch_bounds__(kThreads) instance_write_staged_kernel(
   uint32_t* ring = s_ring + (threadIdx.x >> 5) * 32 * kRingStride;
   uint32_t* mine = ring + lane * kRingStride;
   uint32_t* eid = s_eid[threadIdx.x >> 5];
+  const uint32_t mine_s = smem_u32(mine), eid_s = smem_u32(eid);
   const uint32_t nwin = wstart[g.S];
   const uint32_t stride = gridDim.x * kWarps;
   for (uint32_t w = blockIdx.x * kWarps + (threadIdx.x >> 5); w < nwin; w += stride) {
@@ -843,12 +970,17 @@ __global__ void __launch_bounds__(kThreads) instance_write_staged_kernel(
       uint32_t col = transpose32(cover_mask(ent.y), lane);
       __syncwarp();
       const int rounds = __reduce_max_sync(0xffffffffu, uint32_t(__popc(col)));
+      // branch-free rounds on raw shared addresses: a lane whose column is
+      // exhausted rewrites its current ring slot with the entry-0 id (the slot
+      // is past its staged ids and is overwritten before it is flushed)
       for (int r = 0; r < rounds; ++r) {
-        if (col) {
-          mine[wp & (kRing - 1)] = eid[__ffs(col) - 1];
-          ++wp;
-          col &= col - 1;
-        }
+        const uint32_t live = col != 0u ? 1u : 0u;
+        const uint32_t bit = uint32_t(__ffs(col) - 1) & 31u;
+        uint32_t id;
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(id) : "r"(eid_s + 4u * bit) : "memory");
+        asm volatile("st.shared.u32 [%0], %1;" ::"r"(mine_s + 4u * (wp & (kRing - 1))), "r"(id) : "memory");
+        wp += live;
+        col &= col - 1u;
       }
       __syncwarp();
       // at most 32 ids were staged since the last flush, so a lane holds < 64
@@ -1018,8 +1150,8 @@ int bin_enqueue(const gs_splats_t* splats, int32_t width, int32_t height, void* 
   uint32_t* digit_base = at<uint32_t>(ws, L.digit_base);
   uint64_t* sort_status = at<uint64_t>(ws, L.sort_status);
   const unsigned blocks = unsigned(L.blocks);
-  depth_hist_kernel<<<unsigned(L.blocks < 148 * 4 ? L.blocks : 148 * 4), kThreads, 0, s>>>(splats->depth,
-                                                                                splats->tiles_touched, n, hist, kinfo);
+  depth_hist_kernel<<<unsigned((n + int64_t(kThreads) * kHistItems - 1) / (int64_t(kThreads) * kHistItems)), kThreads, 0,
+                      s>>>(splats->depth, splats->tiles_touched, n, hist, kinfo);
   if ((st = check_launch()) != GS_OK) return st;
   sort_setup_kernel<<<1, 1024, 0, s>>>(hist, digit_base, splats->status, cap, kinfo);
   if ((st = check_launch()) != GS_OK) return st;
@@ -1064,11 +1196,18 @@ int bin_enqueue(const gs_splats_t* splats, int32_t width, int32_t height, void* 
   window_setup_kernel<<<1, 1024, 0, s>>>(M, L.chunks, mtotal, g, at<uint32_t>(ws, L.bstart),
                                          at<uint32_t>(ws, L.wstart), at<uint32_t>(ws, L.wmap), kinfo);
   if ((st = check_launch()) != GS_OK) return st;
-  const size_t smem_scatter = sizeof(uint32_t) * kWarps * size_t(g.S);
-  if ((e = smem_opt_in(reinterpret_cast<const void*>(bucket_scatter_kernel), smem_scatter)) != cudaSuccess)
-    return record_cuda_error(e);
-  bucket_scatter_kernel<<<unsigned(L.chunks), kThreads, smem_scatter, s>>>(drect, order, n, g, M, L.chunks,
-                                                               at<uint2>(ws, L.entries), cap, kinfo);
+  // cursors + OR bins (<= 2048 super-tiles) or cursors + byte stamps
+  const bool or_bins = g.S <= 2048;
+  const size_t smem_scatter = (sizeof(uint32_t) + (or_bins ? sizeof(uint32_t) : 1)) * kWarps * size_t(g.S);
+  const void* scatter_fn = or_bins ? reinterpret_cast<const void*>(bucket_scatter_kernel<true>)
+                                   : reinterpret_cast<const void*>(bucket_scatter_kernel<false>);
+  if ((e = smem_opt_in(scatter_fn, smem_scatter)) != cudaSuccess) return record_cuda_error(e);
+  if (or_bins)
+    bucket_scatter_kernel<true><<<unsigned(L.chunks), kThreads, smem_scatter, s>>>(drect, order, n, g, M, L.chunks,
+                                                                      at<uint2>(ws, L.entries), cap, kinfo);
+  else
+    bucket_scatter_kernel<false><<<unsigned(L.chunks), kThreads, smem_scatter, s>>>(drect, order, n, g, M, L.chunks,
+                                                                       at<uint2>(ws, L.entries), cap, kinfo);
   if ((st = check_launch()) != GS_OK) return st;
   // 3-5. windows, ranges, instance lists
   unsigned long long* k64 = reinterpret_cast<unsigned long long*>(keys);

@@ -1,5 +1,6 @@
 """Device densify/prune against the reference's own
 densify_and_prune outputs (tests/golden/densify_*.npz, make_golden.py)."""
+import sys
 from pathlib import Path
 
 import numpy as np
@@ -55,4 +56,69 @@ def test_device_densify_matches_reference(cuda_device, name):
         np.testing.assert_array_equal(state.adam.exp_avg_sq[grp].cpu().numpy().astype(np.float64),
                                       g[f"out_v_{grp}"])
     assert int(state.stats.accum_count.sum()) == 0
+    state.check_alignment()
+
+
+def _large():
+    sys.path.insert(0, str(GOLDEN))
+    import make_densify_large as L
+    return L
+
+
+def test_densify_large_inputs_regenerate():
+    """The 200K-Gaussian fixture's inputs are regenerated from seeds at test
+    time; their digest must match the one the reference run recorded."""
+    L = _large()
+    g = np.load(GOLDEN / "densify_large.npz")
+    cloud, stats, moments = L.inputs()
+    assert L.input_digest(cloud, stats, moments) == str(g["input_sha256"])
+    assert int(g["n_out"]) == L.N - int(g["split"]) + int(g["cloned"]) + 2 * int(g["split"]) - int(g["pruned"])
+    assert int(g["cloned"]) > 10_000 and int(g["split"]) > 10_000 and int(g["pruned"]) > 10_000
+
+
+@pytest.mark.gpu
+def test_device_densify_matches_reference_200k(cuda_device):
+    """densify_and_prune at 200K Gaussians (56K clones, 34K splits, 28K
+    prunes incl. the world- and screen-size prunes) against the reference:
+    counts exact, moments bit-exact (SHA-256), parameters on 8K sampled rows
+    and the split tail within 2e-6, column sums within 1e-9 relative."""
+    import hashlib
+
+    from paper_2308_04079_b200.cloud import GaussianCloud
+    from paper_2308_04079_b200.densify import TrainState, densify_and_prune
+    from paper_2308_04079_b200.optimizer import TrainConfig
+
+    L = _large()
+    g = np.load(GOLDEN / "densify_large.npz")
+    cloud_np, stats, moments = L.inputs()
+    cloud = GaussianCloud.from_numpy(**cloud_np)
+    state = TrainState(cloud, float(g["extent"]), seed=int(g["seed"]))
+    state.iteration = int(g["iteration"])
+    for grp in GROUPS:
+        state.adam.exp_avg[grp].copy_(torch.from_numpy(moments[f"m_{grp}"].astype(np.float32)))
+        state.adam.exp_avg_sq[grp].copy_(torch.from_numpy(moments[f"v_{grp}"].astype(np.float32)))
+    state.stats.accum_pos_grad.copy_(torch.from_numpy(stats["accum"].astype(np.float32)))
+    state.stats.accum_count.copy_(torch.from_numpy(stats["count"].astype(np.int32)))
+    state.stats.max_radius_frac.copy_(torch.from_numpy(stats["maxr"].astype(np.float32)))
+
+    rep = densify_and_prune(state, TrainConfig(total_iters=30000))
+    torch.cuda.synchronize()
+    assert (rep.cloned, rep.split, rep.pruned, rep.opacity_reset) == (
+        int(g["cloned"]), int(g["split"]), int(g["pruned"]), bool(g["opacity_reset"]))
+    assert len(state.cloud) == int(g["n_out"])
+
+    def sha(t):
+        return hashlib.sha256(t.detach().cpu().numpy().astype(np.float32).tobytes()).hexdigest()
+
+    rows, tail = g["rows"], g["children"]
+    for grp in GROUPS:
+        assert sha(state.adam.exp_avg[grp]) == str(g[f"sha_m_{grp}"]), grp
+        assert sha(state.adam.exp_avg_sq[grp]) == str(g[f"sha_v_{grp}"]), grp
+        got = getattr(state.cloud, grp).cpu().numpy().astype(np.float64)
+        np.testing.assert_allclose(got[rows], g[f"rows_{grp}"], rtol=2e-6, atol=2e-6, err_msg=grp)
+        np.testing.assert_allclose(got[tail], g[f"children_{grp}"], rtol=2e-6, atol=2e-6, err_msg=grp)
+        ref_sum = g[f"colsum_{grp}"]
+        got_sum = got.reshape(len(got), -1).sum(axis=0)
+        scale = np.abs(got).reshape(len(got), -1).sum(axis=0) + 1e-30
+        assert np.all(np.abs(got_sum - ref_sum) <= 1e-6 * scale), grp
     state.check_alignment()
