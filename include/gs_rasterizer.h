@@ -240,10 +240,16 @@ int gs_tile_schedule(const int32_t* work, int32_t tiles, int32_t* scratch, int32
 
 /* ---- K7 backward blend: replaces rasterizer.render_backward (rasterizer.py:253-316)
  * with gradients.backward_blend (gradients.py:30-94).
- * grads2d (N,12) float32 is zeroed and then accumulated:
- *   [0..3] d_mean2d.x, d_mean2d.y, d_alpha, 0
- *   [4..7] d_conic a, b, c, 0
- *   [8..11] d_color r, g, b, 0          (SplatGrads2D, rasterizer.py:243-250) */
+ * grads2d (N,12) float32 is zeroed and then accumulated with the eigenbasis
+ * moments of dp = dL/da * a_raw over the offsets v = K (pixel - mean2d)
+ * (K = record words 4..7; log2(e) power = -|v|^2):
+ *   [0..3]  S1 = sum dp v1, S2 = sum dp v2, S0 = sum dp, 0
+ *   [4..7]  M11 = sum dp v1^2, M12 = sum dp v1 v2, M22 = sum dp v2^2, 0
+ *   [8..11] d_color r, g, b, 0
+ * The reference's SplatGrads2D (rasterizer.py:243-250) follows as
+ * d_mean2d = 2 / log2(e) K^T (S1, S2), d_alpha = S0 / alpha and
+ * d_conic = (-Q_xx / 2, -Q_xy, -Q_yy / 2) with Q = K^-1 M K^-T
+ * (the host mirror's SplatGrads2D properties). */
 int gs_blend_backward(const float* d_image, const gs_splats_t* splats, const uint32_t* sorted_ids,
                       const int32_t* ranges, const float* t_final, const int32_t* last,
                       int32_t width, int32_t height, const float background[3],

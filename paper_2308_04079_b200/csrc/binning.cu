@@ -275,16 +275,15 @@ __global__ void __launch_bounds__(1024) sort_setup_kernel(const uint32_t* __rest
 // writing staged slot i: consecutive threads of one digit write consecutive
 // global positions, so the scatter is coalesced in runs (~16 keys per digit
 // per block) instead of one 4-byte sector write per key.  kFirst: keys from
-// depth / tiles_touched and values = Gaussian index.  kLast: writes the depth
-// order and gathers the tile rectangles (empty rect for Gaussians without
-// instances).
-template <bool kFirst, bool kLast>
+// depth / tiles_touched and values = Gaussian index.  kLast: writes only
+// the depth order (the values); bucket_count gathers the rectangles.
 #ifndef GS_SORT_RANK_OR
 #define GS_SORT_RANK_OR 1
 #endif
 #ifndef GS_SORT_MIN_BLOCKS
 #define GS_SORT_MIN_BLOCKS 3
 #endif
+template <bool kFirst, bool kLast>
 __global__ void __launch_bounds__(kThreads, GS_SORT_MIN_BLOCKS) onesweep_kernel(
     const float* __restrict__ depth, const int32_t* __restrict__ tiles, const int4* __restrict__ rect,
     const uint32_t* __restrict__ keys_in, const uint32_t* __restrict__ ids_in, uint32_t* __restrict__ keys_out,
@@ -382,28 +381,9 @@ __global__ void __launch_bounds__(kThreads, GS_SORT_MIN_BLOCKS) onesweep_kernel(
   const int64_t left = n - int64_t(b) * kSortTile;
   const int cnt = left < kSortTile ? int(left) : kSortTile;
   if (kLast) {
-    // the rectangle gathers are random 16-byte reads: issue a group of them
-    // before any store so their latencies overlap
-    constexpr int kGroup = 8;
-#pragma unroll 1
-    for (int i0 = 0; i0 < kItems; i0 += kGroup) {
-      int4 rc[kGroup];
-      uint32_t pos[kGroup], v[kGroup];
-#pragma unroll
-      for (int u = 0; u < kGroup; ++u) {
-        const int i = tid + (i0 + u) * kThreads;
-        const bool ok = i < cnt;
-        const uint32_t k = ok ? s_keys[i] : kCulledKey;
-        v[u] = ok ? s_vals[i] : 0u;
-        pos[u] = ok ? uint32_t(i) + s_delta[(k >> shift) & 0xFFu] : 0xFFFFFFFFu;
-        rc[u] = (ok && k != kCulledKey) ? rect[v[u]] : make_int4(0, 0, -1, -1);
-      }
-#pragma unroll
-      for (int u = 0; u < kGroup; ++u)
-        if (pos[u] != 0xFFFFFFFFu) {
-          ids_out[pos[u]] = v[u];
-          drect_out[pos[u]] = rc[u];
-        }
+    for (int i = tid; i < cnt; i += kThreads) {
+      const uint32_t k = s_keys[i];
+      ids_out[uint32_t(i) + s_delta[(k >> shift) & 0xFFu]] = s_vals[i];
     }
   } else {
     for (int i = tid; i < cnt; i += kThreads) {
@@ -430,18 +410,34 @@ __device__ __forceinline__ SuperRect super_rect(int4 rc, const Grid& g) {
 
 // per chunk of kChunk depth-ranked Gaussians: the number of Gaussians meeting
 // each super-tile -> M[s * chunks + chunk]
-__global__ void __launch_bounds__(kThreads) bucket_count_kernel(const int4* __restrict__ drect, int64_t n, Grid g,
-                                                               uint32_t* __restrict__ M, int64_t chunks,
-                                                               const int64_t* __restrict__ kinfo) {
+// The rectangles are gathered into depth order here (drect[r] =
+// rect[order[r]]; the Gaussians without instances, which the sort put last,
+// get the empty rectangle), with the gathers of a thread issued together.
+__global__ void __launch_bounds__(kThreads) bucket_count_kernel(const int4* __restrict__ rect,
+                                                               const uint32_t* __restrict__ order,
+                                                               const uint32_t* __restrict__ hist, int4* __restrict__ drect,
+                                                               int64_t n, Grid g, uint32_t* __restrict__ M,
+                                                               int64_t chunks, const int64_t* __restrict__ kinfo) {
   extern __shared__ uint32_t s_h[];
   if (kinfo[1] != 0) return;
   for (int s = threadIdx.x; s < g.S; s += kThreads) s_h[s] = 0u;
+  // Gaussians with instances: every key except the culled 0xFFFFFFFF (depth > 0, so no other key has top byte 0xFF)
+  const int64_t visible = n - int64_t(hist[3 * kRadix + 255]);
   __syncthreads();
   const int64_t r0 = int64_t(blockIdx.x) * kChunk;
-  for (int k = threadIdx.x; k < kChunk; k += kThreads) {
-    const int64_t r = r0 + k;
+  constexpr int kPer = kChunk / kThreads;
+  int4 rc[kPer];
+#pragma unroll
+  for (int u = 0; u < kPer; ++u) {
+    const int64_t r = r0 + threadIdx.x + u * kThreads;
+    rc[u] = r < visible ? rect[order[r]] : make_int4(0, 0, -1, -1);
+  }
+#pragma unroll
+  for (int u = 0; u < kPer; ++u) {
+    const int64_t r = r0 + threadIdx.x + u * kThreads;
     if (r >= n) break;
-    const SuperRect q = super_rect(drect[r], g);
+    drect[r] = rc[u];
+    const SuperRect q = super_rect(rc[u], g);
     for (int y = q.y0; y <= q.y1; ++y)
       for (int x = q.x0; x <= q.x1; ++x) atomicAdd(&s_h[y * g.sx + x], 1u);
   }
@@ -1187,7 +1183,8 @@ int bin_enqueue(const gs_splats_t* splats, int32_t width, int32_t height, void* 
   const size_t smem_count = sizeof(uint32_t) * size_t(g.S);
   if ((e = smem_opt_in(reinterpret_cast<const void*>(bucket_count_kernel), smem_count)) != cudaSuccess)
     return record_cuda_error(e);
-  bucket_count_kernel<<<unsigned(L.chunks), kThreads, smem_count, s>>>(drect, n, g, M, L.chunks, kinfo);
+  bucket_count_kernel<<<unsigned(L.chunks), kThreads, smem_count, s>>>(rect, order, hist, drect, n, g, M, L.chunks,
+                                                                       kinfo);
   if ((st = check_launch()) != GS_OK) return st;
   uint32_t* mtotal = at<uint32_t>(ws, L.mtotal);
   scan_kernel<<<unsigned((L.mlen + kSortTile - 1) / kSortTile), kThreads, 0, s>>>(

@@ -58,10 +58,13 @@ constexpr int kConsumerWarps = 8 / kParts;
 constexpr int kThreads = (kConsumerWarps + 1) * 32;
 constexpr int kG = 2;    // splats per reduction group (group_reduce2)
 constexpr int kC = 9;    // gradient components per splat
-// factors applied after the reduction: d_mean2d x/y (2/log2 e), d_alpha,
-// conic moments M11, M12, M22 (1), colour r, g (colour b = component 8: 1)
-__constant__ float kCompScale[8] = {2.0f / 1.4426950408889634f, 2.0f / 1.4426950408889634f, 1.0f, 1.0f, 1.0f,
-                                    1.0f, 1.0f, 1.0f};
+
+#ifndef GS_BWD_STATS
+#define GS_BWD_STATS 0
+#endif
+#if GS_BWD_STATS
+__device__ unsigned long long g_bwd_hist[33];   // visited (warp, splat) pairs by active-lane count
+#endif
 
 struct BwdStage {
   float4 k[kBatch];      // eigenbasis rows (record word 1), see make_tile_splat
@@ -279,8 +282,6 @@ blend_bwd_kernel(const float* __restrict__ d_image, const float4* __restrict__ r
   }
 
   // ---------------- consumer warps
-  // this lane's reduced component ((lane >> 1) & 7) and its constant factor
-  const float comp_scale = kCompScale[(lane >> 1) & 7];
   // composited tail behind the current splat, starts at the background term
   float S = T * (dlx * bg.x + dly * bg.y + dlz * bg.z);
   for (int b = 0; b < nb; ++b) {
@@ -317,6 +318,12 @@ blend_bwd_kernel(const float* __restrict__ d_image, const float4* __restrict__ r
             // leaves T and S unchanged and zeroes every gradient term
             const bool use = (uint32_t(js[u]) < lim) && (e.a > 0.0f);
             any |= use;
+#if GS_BWD_STATS
+            {
+              const uint32_t bu = __ballot_sync(0xffffffffu, use);
+              if (lane == 0 && js[u] >= 0) atomicAdd(&g_bwd_hist[__popc(bu)], 1ull);
+            }
+#endif
             const float a = use ? e.a : 0.0f;
             // 1 - a >= 0.01: MUFU reciprocal (~1 ulp), no IEEE/denormal sequence
             const float inv = rcp_approx(1.0f - a);
@@ -330,18 +337,18 @@ blend_bwd_kernel(const float* __restrict__ d_image, const float4* __restrict__ r
             v[u * kC + 6] = w * dlx;
             v[u * kC + 7] = w * dly;
             v[u * kC + 8] = w * dlz;
+            // dp = dL/d(log2(e) power) up to sign; the row holds its
+            // eigenbasis moments sum dp (v1, v2, 1, v1^2, v1 v2, v2^2), from
+            // which the projection backward forms d_mean2d = 2/log2(e) K^T
+            // (sum dp v), d_alpha = sum dp / alpha and d_conic (see above)
             const float dp = d_a * e.a_raw;
-            // d power / d mean = (a dx + b dy, b dx + c dy) = 2 (v1 k1 + v2 k2) / log2(e)
-            // (eigenbasis form: no cancellation for elongated conics); the
-            // constant factors (2/log2(e), -1/2, -1) are applied once per
-            // splat after the warp reduction (kCompScale)
-            v[u * kC + 0] = dp * fmaf(e.v1, kk.x, e.v2 * kk.z);  // d_mean2d.x / (2/log2e)
-            v[u * kC + 1] = dp * fmaf(e.v1, kk.y, e.v2 * kk.w);  // d_mean2d.y / (2/log2e)
-            v[u * kC + 2] = d_a * e.g;                           // d_alpha
-            const float dpv1 = dp * e.v1;
+            const float dpv1 = dp * e.v1, dpv2 = dp * e.v2;
+            v[u * kC + 0] = dpv1;                                // S1
+            v[u * kC + 1] = dpv2;                                // S2
+            v[u * kC + 2] = dp;                                  // S0
             v[u * kC + 3] = dpv1 * e.v1;                         // conic moment M11
             v[u * kC + 4] = dpv1 * e.v2;                         // M12
-            v[u * kC + 5] = dp * e.v2 * e.v2;                    // M22
+            v[u * kC + 5] = dpv2 * e.v2;                         // M22
           }
           if (!__any_sync(0xffffffffu, any)) continue;
           float out, out8;
@@ -350,12 +357,12 @@ blend_bwd_kernel(const float* __restrict__ d_image, const float4* __restrict__ r
           const int comp = (lane >> 1) & 7;
           if (j >= 0 && (lane & 1) == 0) {
             if (kDet) {   // this warp's partial, combined in warp order by the producer
-              dparts[s].v[warp][j][comp] = out * comp_scale;
+              dparts[s].v[warp][j][comp] = out;
               if (comp == 0) dparts[s].v[warp][j][8] = out8;
             } else {
               // fire-and-forget reductions into the (N,12) screen-gradient rows
               float* row = reinterpret_cast<float*>(grads2d) + 12 * size_t(st.id[j]);
-              atomicAdd(row + comp + comp / 3, out * comp_scale);
+              atomicAdd(row + comp + comp / 3, out);
               if (comp == 0) atomicAdd(row + 10, out8);
             }
           }
@@ -772,3 +779,14 @@ extern "C" int gs_blend_backward_deterministic(const float* d_image, const gs_sp
                                                               tiles_x, n, grads2d);
   return check_launch();
 }
+
+#if GS_BWD_STATS
+extern "C" int gs_debug_bwd_hist(unsigned long long* out, int reset) {
+  cudaError_t e = cudaMemcpyFromSymbol(out, gs::g_bwd_hist, sizeof(unsigned long long) * 33);
+  if (e == cudaSuccess && reset) {
+    unsigned long long z[33] = {};
+    e = cudaMemcpyToSymbol(gs::g_bwd_hist, z, sizeof(z));
+  }
+  return e == cudaSuccess ? 0 : 1;
+}
+#endif

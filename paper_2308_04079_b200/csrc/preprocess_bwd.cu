@@ -21,7 +21,7 @@ namespace {
 // Per-Gaussian inputs, loaded before the block's SH staging so their
 // latency overlaps it.
 struct GradInputs {
-  float4 ga, gb, gc;   // grads2d row: (d_mx, d_my, d_alpha), conic moments (M11, M12, M22), (d_r, d_g, d_b)
+  float4 ga, gb, gc;   // grads2d row: moments (S1, S2, S0), conic moments (M11, M12, M22), (d_r, d_g, d_b)
   float4 k;            // the conic's eigenbasis rows (record word 1) the blends built the exponent from
   float4 q;            // raw quaternion
   float m0, m1, m2, l0, l1, l2, op, mask;
@@ -73,9 +73,10 @@ __device__ __forceinline__ void grad_one_t(const GradInputs& in, const DevCamera
   const float4 ga = in.ga, gb = in.gb, gc = in.gc;
   const int mask = int(in.mask);
 
-  // --- opacity through the sigmoid (gradients.py:217)
+  // --- opacity through the sigmoid (gradients.py:217): d_alpha = S0 / alpha
+  //     (S0 = sum dL/da a_raw with a_raw = alpha g), so d_logit = S0 (1 - alpha)
   const Real alpha = Real(1.0) / (Real(1.0) + exp(-Real(in.op)));
-  const float d_logit = float(Real(ga.z) * alpha * (Real(1.0) - alpha));
+  const float d_logit = float(Real(ga.z) * (Real(1.0) - alpha));
 
   // --- view position, Jacobian, U = J W (core.py:279, 298-303)
   const Real mx = in.m0, my = in.m1, mz = in.m2;
@@ -135,6 +136,10 @@ __device__ __forceinline__ void grad_one_t(const GradInputs& in, const DevCamera
   const Real dC01 = cm * (k1x * P1y + k2x * P2y);
   const Real dC10 = dC01;
   const Real dC11 = cm * (k1y * P1y + k2y * P2y);
+  // d_mean2d = 2 / log2(e) K^T (S1, S2) from the row's moments (float32, like
+  // the per-pixel products the blends summed before)
+  const float fmx = (2.0f / 1.4426950408889634f) * fmaf(in.k.x, ga.x, in.k.z * ga.y);
+  const float fmy = (2.0f / 1.4426950408889634f) * fmaf(in.k.y, ga.x, in.k.w * ga.y);
 
   // --- screen covariance -> world covariance: dSigma = U^T dS' U (gradients.py:116-123)
   Real dCU[6];  // dS' U  (2x3)
@@ -186,7 +191,7 @@ __device__ __forceinline__ void grad_one_t(const GradInputs& in, const DevCamera
 
   // --- view position: J^T d_mean2d plus the dependence of J on the mean
   //     (gradients.py:236-255)
-  const Real dmx = ga.x, dmy = ga.y;
+  const Real dmx = fmx, dmy = fmy;
   Real dt[3] = {j00 * dmx, j11 * dmy, j02 * dmx + j12 * dmy};
   Real dU[6];  // 2 dS' U Sigma
 #pragma unroll
@@ -237,7 +242,7 @@ __device__ __forceinline__ void grad_one_t(const GradInputs& in, const DevCamera
 #pragma unroll
   for (int j = 0; j < 3; ++j)
     dmean[j] = float(dt[0] * cR[j] + dt[1] * cR[3 + j] + dt[2] * cR[6 + j]) + dms[j];
-  o.norm = sqrtf(ga.x * ga.x + ga.y * ga.y);  // gradients.py:258
+  o.norm = sqrtf(fmx * fmx + fmy * fmy);  // gradients.py:258
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
     o.dmean[k] = dmean[k];

@@ -231,12 +231,14 @@ class RenderOutput:
 
 @dataclass
 class SplatGrads2D:
-    """Screen-space gradients (rasterizer.py:243-250) in the packed (N,12) row:
-    [0:2] d_mean2d, [2] d_alpha, [4:7] the conic moments M = sum dL/dpower
-    (v1^2, v1 v2, v2^2) over the eigenbasis offsets v = K (pixel - mean) the
-    blends evaluate the exponent from (log2(e) power = -|v|^2; K = record
-    words 4:8), [8:11] d_color.  d_conic converts M to the reference's
-    d_conic = -1/2 sum dL/dpower (dx^2, 2 dx dy, dy^2) (gradients.py:90-93)."""
+    """Screen-space gradients (rasterizer.py:243-250) in the packed (N,12) row
+    of eigenbasis moments of dp = dL/da a_raw over the offsets v = K (pixel -
+    mean) the blends evaluate the exponent from (log2(e) power = -|v|^2;
+    K = record words 4:8): [0:2] (S1, S2) = sum dp v, [2] S0 = sum dp,
+    [4:7] M = sum dp (v1^2, v1 v2, v2^2), [8:11] d_color.  The properties
+    convert them to the reference's quantities: d_mean2d = 2/log2(e) K^T S,
+    d_alpha = S0 / alpha, d_conic = -1/2 sum dL/dpower (dx^2, 2 dx dy, dy^2)
+    (gradients.py:54-93)."""
 
     packed: torch.Tensor  # (N,12) float32
     # the longest-first tile schedule the backward ran on (int32 (T,)), a good
@@ -244,13 +246,26 @@ class SplatGrads2D:
     tile_order: torch.Tensor | None = None
     rec: torch.Tensor | None = None   # the splats' records (for d_conic)
 
+    def _need_rec(self, what: str) -> torch.Tensor:
+        if self.rec is None:
+            raise ValueError(f"{what} needs the splats' records (SplatGrads2D.rec)")
+        return self.rec
+
     @property
     def d_mean2d(self) -> torch.Tensor:
-        return self.packed[:, 0:2]
+        """(N,2) float64 d_mean2d = 2/log2(e) K^T (S1, S2)."""
+        k = self._need_rec("d_mean2d")[:, 4:8].double()
+        s1, s2 = self.packed[:, 0].double(), self.packed[:, 1].double()
+        c = 2.0 / 1.4426950408889634
+        return torch.stack([c * (k[:, 0] * s1 + k[:, 2] * s2), c * (k[:, 1] * s1 + k[:, 3] * s2)], dim=1)
 
     @property
     def d_alpha(self) -> torch.Tensor:
-        return self.packed[:, 2]
+        """(N,) float64 d_alpha = S0 / alpha (0 where S0 = 0, e.g. culled rows)."""
+        alpha = self._need_rec("d_alpha")[:, 11].double()
+        s0 = self.packed[:, 2].double()
+        ok = s0 != 0
+        return torch.where(ok, s0 / torch.where(ok, alpha, torch.ones_like(alpha)), torch.zeros_like(s0))
 
     @property
     def conic_moments(self) -> torch.Tensor:

@@ -80,8 +80,8 @@ def test_c3_training_step_vs_oracle(cuda_device):
     og2 = O.render_backward(od_image, proj, bins, fwd, w, h, bg)
     del bins
     p = g2.packed.cpu().numpy()
-    assert rel(p[:, 0:2], og2[:, 0:2]) < 1e-3
-    assert rel(p[:, 2], og2[:, 5]) < 1e-3
+    assert rel(g2.d_mean2d.cpu().numpy(), og2[:, 0:2]) < 1e-3
+    assert rel(g2.d_alpha.cpu().numpy(), og2[:, 5]) < 1e-3        # S0 / alpha
     assert rel(g2.d_conic.cpu().numpy(), og2[:, 2:5]) < 1e-3
     assert rel(p[:, 8:11], og2[:, 6:9]) < 1e-3
     ograds = O.backward_project(cloud_np, cam, 3, proj, og2)

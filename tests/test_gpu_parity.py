@@ -74,8 +74,8 @@ def check_against_oracle(dev, orc, floor_scale=1e-9, grad_tol=None):
                    color_max=float(proj["color"].max(initial=1.0)))
     # backward blend: packed rows vs oracle's (N,9)
     p = g2.packed.cpu().numpy()
-    assert rel(p[:, 0:2], og2[:, 0:2]) < GRAD_TOL
-    assert rel(p[:, 2], og2[:, 5]) < GRAD_TOL
+    assert rel(g2.d_mean2d.cpu().numpy(), og2[:, 0:2]) < GRAD_TOL
+    assert rel(g2.d_alpha.cpu().numpy(), og2[:, 5]) < GRAD_TOL        # S0 / alpha
     assert rel(g2.d_conic.cpu().numpy(), og2[:, 2:5]) < GRAD_TOL   # from the eigenbasis moments
     assert rel(p[:, 8:11], og2[:, 6:9]) < GRAD_TOL
     # parameter gradients

@@ -134,7 +134,9 @@ def run_c5(args, split_quantile: float | None = None) -> dict:
     with torch.no_grad():
         target = R.render_view(GaussianCloud.from_numpy(**tgt_np), cam, (0, 0, 0), 3)[0].image
     del tgt_np
-    state = TrainState(cloud, scene_extent=20.0, seed=0)
+    # c5s: a smaller extent (split threshold 1% of it = 0.02) so that the large
+    # hot Gaussians split while the small ones clone
+    state = TrainState(cloud, scene_extent=20.0 if split_quantile is None else 2.0, seed=0)
     state.active_sh_degree = 3
     config = TrainConfig(warmup_upsample_iters=(0, 0), sh_band_interval=10**9, densify_start=0,
                          densify_interval=100, densify_until=10**9, total_iters=30000)
