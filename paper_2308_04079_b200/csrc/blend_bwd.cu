@@ -297,14 +297,17 @@ blend_bwd_kernel(const float* __restrict__ d_image, const float4* __restrict__ r
       // padding slots of a short group carry j = -1, i.e. 0xffffffff unsigned
       const uint32_t lim = uint32_t(max(last_idx - lo + 1, 0));
       for (int c = jmax; c >= 0; c -= 32) {
-        const int jl = c - lane;  // lane l looks at splat c - l: ascending lanes = back to front
+        // lane l looks at splat c - 31 + l: the highest set bit is the
+        // backmost remaining splat (one FLO per pick)
+        const int jl = c - 31 + lane;
         unsigned live = __ballot_sync(0xffffffffu, jl >= 0 && ((st.mask[jl] >> warp) & 1u));
         while (live) {
           int js[kG];
 #pragma unroll
           for (int u = 0; u < kG; ++u) {
-            js[u] = live ? c - (__ffs(live) - 1) : -1;
-            live &= live - 1;
+            const int hb = 31 - __clz(live);   // -1 when empty
+            js[u] = live ? c - 31 + hb : -1;
+            live &= ~(1u << (hb & 31));
           }
           float v[kG * kC];
           bool any = false;
@@ -312,11 +315,11 @@ blend_bwd_kernel(const float* __restrict__ d_image, const float4* __restrict__ r
           for (int u = 0; u < kG; ++u) {
             const int j = max(js[u], 0);
             const float4 kk = st.k[j];
-            const AlphaEval e = eval_alpha_tile(lx, ly, fx, fy, kk, st.m[j], rec, st.id, j);
+            const AlphaEval e = eval_alpha_tile_bwd(lx, ly, fx, fy, kk, st.m[j], rec, st.id, j);
             // branch-free body: lanes past their last contributor (or the
             // padding slots of a short group) evaluate with a = 0, which
             // leaves T and S unchanged and zeroes every gradient term
-            const bool use = (uint32_t(js[u]) < lim) && (e.a > 0.0f);
+            const bool use = (uint32_t(js[u]) < lim) && e.ok;
             any |= use;
 #if GS_BWD_STATS
             {
