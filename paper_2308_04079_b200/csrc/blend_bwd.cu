@@ -315,7 +315,7 @@ blend_bwd_kernel(const float* __restrict__ d_image, const float4* __restrict__ r
           for (int u = 0; u < kG; ++u) {
             const int j = max(js[u], 0);
             const float4 kk = st.k[j];
-            const AlphaEval e = eval_alpha_tile_bwd(lx, ly, fx, fy, kk, st.m[j], rec, st.id, j);
+            const AlphaEval e = eval_alpha_tile(lx, ly, fx, fy, kk, st.m[j], rec, st.id, j);
             // branch-free body: lanes past their last contributor (or the
             // padding slots of a short group) evaluate with a = 0, which
             // leaves T and S unchanged and zeroes every gradient term

@@ -373,8 +373,8 @@ blend_fwd_kernel(const float4* __restrict__ rec, const uint32_t* __restrict__ id
           // branch-light body: finished lanes evaluate too (free under SIMT)
           // and are masked by `take`
           const AlphaEval e = eval_alpha_tile(lx, ly, fx, fy, st.k[j], st.m[j], rec, st.id, j);
-          const float t_new = T * (1.0f - e.a);
-          const bool blend = !done && e.a > 0.0f;
+          const float t_new = T * (1.0f - e.a);   // used only when blended
+          const bool blend = !done && e.ok;
           const bool sat = t_new < (kTraining ? kTransSatHi : kTransSat);  // 1 - T_new > 0.9999
           const bool stopping = blend && sat;
           done = done || stopping;

@@ -99,8 +99,8 @@ __host__ inline DevCamera make_dev_camera(const gs_camera_t& c) {
 struct AlphaEval {
   float v1, v2, g, a_raw, a;   // v: eigenbasis offsets; a: clamped and eps-skipped alpha (0 = skip)
   bool live;                   // a_raw < 0.99: the pair passes gradient to alpha/power
-  bool ok;                     // eval_alpha_tile_bwd only: the pair is blended (a >= 1/255); a is then
-                               // the clamped alpha and is not zeroed for skipped pairs
+  bool ok;                     // the pair is blended (a >= 1/255); for ok = false a is not
+                               // zeroed on the float32 path (callers select on ok)
 };
 
 #ifndef GS_ALPHA_GUARD
@@ -390,29 +390,14 @@ __device__ __forceinline__ void make_tile_splat(float4 r0, float4 k, float alpha
   ctr = make_float2(mx, my);
 }
 
-// lx, ly: tile-local pixel centre (col + 0.5); px, py: absolute pixel centre
+// Alpha of one (pixel, splat) pair (rasterizer.py:171-177).  lx, ly:
+// tile-local pixel centre (col + 0.5); px, py: absolute pixel centre.
+// e.ok says whether the pair is blended (min(0.99, a_raw) >= 1/255 iff
+// a_raw >= 1/255) and e.a is min(0.99, a_raw) without the skip zeroing,
+// which the callers fold into their own selects.  Within kGuard of either
+// threshold the pair is re-evaluated in float64 from the hi/lo record, so
+// the skip and clamp decisions are the reference's.
 __device__ __forceinline__ AlphaEval eval_alpha_tile(float lx, float ly, float px, float py, float4 k, float4 m,
-                                                     const float4* __restrict__ rec, const uint32_t* s_id, int j) {
-  AlphaEval e;
-  e.v1 = __fmaf_rn(k.x, lx, __fmaf_rn(k.y, ly, m.x));
-  e.v2 = __fmaf_rn(k.z, lx, __fmaf_rn(k.w, ly, m.y));
-  const float p2 = __fmaf_rn(-e.v1, e.v1, -__fmul_rn(e.v2, e.v2));
-  e.g = ex2_approx(p2);
-  e.a_raw = __fmul_rn(m.z, e.g);
-  if (fabsf(e.a_raw - kAlphaEps) <= kGuard * kAlphaEps || fabsf(e.a_raw - kAlphaClamp) <= kGuard) {
-    eval_alpha_f64(px, py, rec + kRecWords * size_t(s_id[j]), e);
-    return e;
-  }
-  e.live = e.a_raw < kAlphaClamp;
-  const float a = fminf(kAlphaClamp, e.a_raw);
-  e.a = (a < kAlphaEps) ? 0.0f : a;
-  return e;
-}
-
-// The backward's variant: e.ok says whether the pair is blended (min(0.99,
-// a_raw) >= 1/255 iff a_raw >= 1/255) and e.a is min(0.99, a_raw) without
-// the skip zeroing, which the caller folds into its own select.
-__device__ __forceinline__ AlphaEval eval_alpha_tile_bwd(float lx, float ly, float px, float py, float4 k, float4 m,
                                                          const float4* __restrict__ rec, const uint32_t* s_id, int j) {
   AlphaEval e;
   e.v1 = __fmaf_rn(k.x, lx, __fmaf_rn(k.y, ly, m.x));
