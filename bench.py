@@ -149,7 +149,8 @@ def run_single(args, local_rank: int) -> None:
     from paper_2308_04079_b200.cloud import GaussianCloud
     from paper_2308_04079_b200.loss import l1_dssim_loss
     from paper_2308_04079_b200.optimizer import DeviceAdam, TrainConfig
-    from paper_2308_04079_b200.profiling import StageTimer, bucket_entries, evaluated_pairs, measure_fp32_peak
+    from paper_2308_04079_b200.profiling import (StageTimer, bucket_entries, evaluated_pairs, fp32_nominal_tflops,
+                                                  measure_fp32_peak)
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
@@ -321,6 +322,7 @@ def run_single(args, local_rank: int) -> None:
     stage_ms = timer.mean_ms()
     pk = dict(peaks())
     pk["fp32_tflops"] = fp32_peak
+    pk["fp32_nominal_tflops"] = fp32_nominal_tflops(dev, pk.get("sm_max_mhz"))
     traffic_file = ROOT / "profiles" / "traffic_bytes.json"
     if traffic_file.exists():
         pk["traffic_bytes"] = json.loads(traffic_file.read_text()).get("per_launch", {})
@@ -356,6 +358,7 @@ def run_single(args, local_rank: int) -> None:
         "gpu_launches": timer.launches_per_step() * args.steps,
         "roofline": roof["primary"], "roofline_hbm": roof["hbm"], "roofline_stages": roof["stages"],
         "fp32_peak_tflops_measured": round(fp32_peak, 2),
+        "fp32_peak_tflops_nominal": round(pk["fp32_nominal_tflops"], 2),
         "clocks": clock_info,
     }
     if args.cpu_baseline:

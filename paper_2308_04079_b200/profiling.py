@@ -4,10 +4,11 @@ Algorithmic bytes / flops per stage follow SURVEY.md §8(d), except for the
 binning, which is charged the bytes the implemented algorithm must move
 (binning.cu; SURVEY's formula assumes the reference's 64-bit sort over K):
   K1 preprocess_fwd  44 N + 192 V read + 48 V write
-  K2-K5 bin_and_sort 156 N + 24 E + 4 K + 12 T: depth histogram 8 N, four onesweep passes over the
-                     depth keys 16 + 16 + 16 + 44 N (the last gathers the tile rectangles), bucket count
-                     16 N, bucket scatter 40 N + 8 E, window count 8 E, instance write 8 E + 4 K,
-                     tile ranges 12 T; E = (Gaussian, super-tile) bucket entries
+  K2-K5 bin_and_sort 140 N + 24 E + 4 K + 12 T: depth histogram 8 N, four onesweep passes over the
+                     depth keys 16 + 16 + 16 + 12 N (the last writes only the order), bucket count
+                     36 N (order, rectangle gather, depth-ordered rectangles), bucket scatter 36 N + 8 E,
+                     window count 8 E, instance write 8 E + 4 K, tile ranges 12 T;
+                     E = (Gaussian, super-tile) bucket entries
   K6 blend_fwd       40 K + 20 P bytes (training); 25 FP32 ops + 1 ex2 per evaluated (pixel, splat) pair
   K7 blend_bwd       40 K + 20 P + 36 V bytes; 60 FP32 ops + 1 ex2 + 1 rcp per evaluated pair
   K8 preprocess_bwd  276 V + 240 N + 20 N bytes
@@ -88,7 +89,7 @@ class StageTimer:
         E = bucket_entries or 0
         bytes_ = {
             "preprocess_fwd": 44 * n + 192 * V + 48 * V,
-            "bin_and_sort": 156 * n + 24 * E + 4 * K + 12 * T,
+            "bin_and_sort": 140 * n + 24 * E + 4 * K + 12 * T,
             "blend_fwd": 40 * K + 20 * P,
             "blend_bwd": 40 * K + 20 * P + 36 * V,
             "preprocess_bwd": 276 * V + 240 * n + 20 * n,
@@ -98,7 +99,10 @@ class StageTimer:
             "loss": 132 * P,
         }
         hbm = float(peaks.get("hbm_gbs", 6650.0))
-        fp32 = peaks.get("fp32_tflops")  # measured in-run by measure_fp32_peak
+        # the FP32 roofline's denominator: the larger of the in-run FMA probe
+        # and the nominal SMs x 128 x 2 x max clock (a probe run at a dipped
+        # clock must not inflate the fraction)
+        fp32 = max(peaks.get("fp32_tflops") or 0.0, peaks.get("fp32_nominal_tflops") or 0.0) or None
         flops = {}
         if e_pairs:
             flops = {"blend_fwd": 25.0 * e_pairs, "blend_bwd": 60.0 * e_pairs}
@@ -121,8 +125,9 @@ class StageTimer:
             if "frac_fp32" in st:
                 primary = {"kernel": dom, "bound": "fp32", "achieved": st["achieved_tflops"], "peak": round(fp32, 2),
                            "unit": "TFLOP/s", "frac": st["frac_fp32"], "traffic": traffic.get(dom),
-                           "peak_source": "in-run FP32 FMA probe (gs_fp32_fma_probe); MEASURED_PEAKS.json has "
-                                          "no FP32 figure and this kernel is FP32-issue-bound, not HBM/tensor",
+                           "peak_source": "max(in-run FP32 FMA probe gs_fp32_fma_probe, nominal SMs x 128 x 2 x "
+                                          "sm_max_mhz); MEASURED_PEAKS.json has no FP32 figure and this kernel is "
+                                          "FP32-issue-bound, not HBM/tensor",
                            "algorithmic": f"{st['algorithmic_flops']:.4g} FLOP per launch "
                                           f"(25|60 FP32 ops x E={e_pairs} evaluated pairs)"}
             else:
@@ -140,25 +145,36 @@ class StageTimer:
         return {"primary": primary, "hbm": secondary, "stages": stages}
 
 
-def measure_fp32_peak(device=None, iters: int = 4096) -> float:
-    """FP32 FMA throughput (FLOP/s, FMA = 2) of this GPU, from gs_fp32_fma_probe."""
+def measure_fp32_peak(device=None, iters: int = 4096, trials: int = 7) -> float:
+    """FP32 FMA throughput (FLOP/s, FMA = 2) of this GPU, from gs_fp32_fma_probe:
+    ~50 ms of untimed launches to bring the clocks up, then the best of
+    `trials` timed groups of 5 launches (CUDA events)."""
     from . import _lib
     lib = _lib.load()
     props = torch.cuda.get_device_properties(device)
     blocks = props.multi_processor_count * 8
     scratch = torch.empty(blocks, dtype=torch.float32, device=device)
     stream = torch.cuda.current_stream(device).cuda_stream
-    for _ in range(2):
+    for _ in range(200):
         _lib.check(lib.gs_fp32_fma_probe(scratch.data_ptr(), blocks, iters, stream), "fma_probe")
-    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    s.record()
-    reps = 5
-    for _ in range(reps):
-        _lib.check(lib.gs_fp32_fma_probe(scratch.data_ptr(), blocks, iters, stream), "fma_probe")
-    e.record()
-    torch.cuda.synchronize(device)
-    secs = s.elapsed_time(e) / 1e3 / reps
-    return blocks * 256 * iters * 8 * 2 / secs
+    reps, best = 5, float("inf")
+    for _ in range(trials):
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        for _ in range(reps):
+            _lib.check(lib.gs_fp32_fma_probe(scratch.data_ptr(), blocks, iters, stream), "fma_probe")
+        e.record()
+        torch.cuda.synchronize(device)
+        best = min(best, s.elapsed_time(e) / 1e3 / reps)
+    return blocks * 256 * iters * 8 * 2 / best
+
+
+def fp32_nominal_tflops(device=None, sm_max_mhz: float | None = None) -> float:
+    """Nominal FP32 FMA peak: SMs x 128 FP32 lanes x 2 FLOP x the maximum SM
+    clock (MEASURED_PEAKS.json sm_max_mhz, else the device's)."""
+    props = torch.cuda.get_device_properties(device)
+    mhz = sm_max_mhz or getattr(props, "clock_rate", 0) / 1e3 or 1965.0
+    return props.multi_processor_count * 128 * 2 * mhz * 1e6 / 1e12
 
 
 def bucket_entries(splats, width: int, height: int) -> int:
