@@ -46,6 +46,24 @@ constexpr int kParts = GS_FWD_PARTS;
 constexpr int kConsumerWarps = 8 / kParts;
 constexpr int kThreads = (kConsumerWarps + 1) * 32;
 
+#ifndef GS_FWD_TMA
+#define GS_FWD_TMA 0     // 1: the producer gathers the records with TMA tile::gather4 (see produce_batch_tma)
+#endif
+
+#if GS_FWD_TMA
+// TMA variant: record words 0-3 of each splat land as one 64-byte row
+// (rec4[4 e + w] = word w of splat e), four splats per gather4 (256 B)
+struct alignas(128) FwdStage {
+  float4 rec4[4 * kBatch];
+  float4 m[kBatch];      // (-k1 . mean_rel, -k2 . mean_rel, alpha, 0)
+  uint32_t id[kBatch];
+  uint8_t mask[kBatch];
+};
+__device__ __forceinline__ float4 stage_k(const FwdStage& st, int j) { return st.rec4[4 * j + 1]; }
+__device__ __forceinline__ float4 stage_col(const FwdStage& st, int j) { return st.rec4[4 * j + 2]; }
+struct RawRec {};
+constexpr size_t kSmemBytes = sizeof(FwdStage) * kStages + 128;   // + alignment slack
+#else
 struct FwdStage {
   float4 k[kBatch];      // eigenbasis rows (record word 1), see make_tile_splat
   float4 m[kBatch];      // (-k1 . mean_rel, -k2 . mean_rel, alpha, 0)
@@ -53,11 +71,47 @@ struct FwdStage {
   uint32_t id[kBatch];
   uint8_t mask[kBatch];
 };
+__device__ __forceinline__ float4 stage_k(const FwdStage& st, int j) { return st.k[j]; }
+__device__ __forceinline__ float4 stage_col(const FwdStage& st, int j) { return st.col[j]; }
 struct RawRec {          // the producer's landing buffer for the cp.async gathers
   float4 r0[kBatch];
 };
 constexpr size_t kSmemBytes = sizeof(FwdStage) * kStages + sizeof(RawRec);
+#endif
 
+#if GS_FWD_TMA
+// TMA producer: lane l < ceil(cnt / 4) issues one tile::gather4 of splats
+// 4l..4l+3 (record rows of the 2-D tensor map over rec: 20 floats x N, box
+// 16 x 1), completing on the stage's tma mbarrier; the rows past cnt repeat
+// the last id (never read).  Then the tile-relative record and coverage mask.
+__device__ __forceinline__ void produce_batch_tma(FwdStage& st, uint64_t* tma_bar, uint32_t parity,
+                                                  const CUtensorMap* tmap, const float4* __restrict__ rec,
+                                                  const uint32_t* __restrict__ ids, int base, int cnt, int lane,
+                                                  float tile_x0, float tile_y0, int mask_shift) {
+  static_assert(kBatch == 32, "one id per lane");
+  const uint32_t gid = __ldg(ids + base + min(lane, cnt - 1));
+  if (lane < cnt) st.id[lane] = gid;
+  const int ng = (cnt + 3) >> 2;
+  const int r0 = __shfl_sync(0xffffffffu, int(gid), (4 * lane + 0) & 31);
+  const int r1 = __shfl_sync(0xffffffffu, int(gid), (4 * lane + 1) & 31);
+  const int r2 = __shfl_sync(0xffffffffu, int(gid), (4 * lane + 2) & 31);
+  const int r3 = __shfl_sync(0xffffffffu, int(gid), (4 * lane + 3) & 31);
+  if (lane == 0) mbar_arrive_expect_tx(tma_bar, uint32_t(ng) * 256u);
+  __syncwarp();
+  if (lane < ng) tma_gather4(&st.rec4[16 * lane], tmap, tma_bar, 0, r0, r1, r2, r3);
+  while (!mbar_try_wait(tma_bar, parity)) {
+  }
+  if (lane < cnt) {
+    const float4 w0 = st.rec4[4 * lane], k = st.rec4[4 * lane + 1];
+    const float alpha = st.rec4[4 * lane + 2].w;
+    float2 ctr;
+    make_tile_splat(w0, k, alpha, tile_x0, tile_y0, st.m[lane], ctr);
+    st.mask[lane] = uint8_t(warp_cover_mask<GS_FWD_EXACT != 0>(w0, k, alpha, tile_x0, tile_y0) >> mask_shift);
+  }
+}
+#endif
+
+#if !GS_FWD_TMA
 __device__ __forceinline__ void produce_batch(FwdStage& st, RawRec& raw, const float4* __restrict__ rec,
                                               const uint32_t* __restrict__ ids, int base, int cnt, int lane,
                                               float tile_x0, float tile_y0, int mask_shift) {
@@ -91,6 +145,7 @@ __device__ __forceinline__ void produce_batch(FwdStage& st, RawRec& raw, const f
     }
   }
 }
+#endif
 
 // ---------------------------------------------------------------------------
 // Exact float64 re-blend of a flagged pixel (training).  The forward appends
@@ -287,10 +342,16 @@ __global__ void GS_FWD_LB
 blend_fwd_kernel(const float4* __restrict__ rec, const uint32_t* __restrict__ ids, const int2* __restrict__ ranges,
                  int width, int height, int tiles_x, int tile0, float3 bg, float* __restrict__ image,
                  float* __restrict__ t_final, int32_t* __restrict__ last, const int32_t* __restrict__ tile_order,
-                 int32_t* __restrict__ tile_work, int32_t* __restrict__ fix) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+                 int32_t* __restrict__ tile_work, int32_t* __restrict__ fix, const __grid_constant__ CUtensorMap tmap) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+#if GS_FWD_TMA
+  FwdStage* stages = reinterpret_cast<FwdStage*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+  RawRec* raw = nullptr;
+  __shared__ uint64_t tma_bar[kStages];
+#else
   FwdStage* stages = reinterpret_cast<FwdStage*>(smem_raw);
   RawRec* raw = reinterpret_cast<RawRec*>(smem_raw + sizeof(FwdStage) * kStages);
+#endif
   __shared__ uint64_t full_bar[kStages], empty_bar[kStages];
   __shared__ int s_done, s_stop;
 
@@ -307,9 +368,15 @@ blend_fwd_kernel(const float4* __restrict__ rec, const uint32_t* __restrict__ id
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full_bar[s], 32);
       mbar_init(&empty_bar[s], kConsumerWarps);
+#if GS_FWD_TMA
+      mbar_init(&tma_bar[s], 1);
+#endif
     }
     s_done = 0;
     s_stop = 0;
+#if GS_FWD_TMA
+    fence_mbarrier_init();
+#endif
   }
   __syncthreads();
 
@@ -327,8 +394,14 @@ blend_fwd_kernel(const float4* __restrict__ rec, const uint32_t* __restrict__ id
       }
       if (stop || ld_volatile(&s_stop)) break;
       const int base = range.x + b * kBatch;
+#if GS_FWD_TMA
+      (void)raw;
+      produce_batch_tma(stages[s], &tma_bar[s], uint32_t(b / kStages) & 1u, &tmap, rec, ids, base,
+                        min(kBatch, range.y - base), lane, tile_x0, tile_y0, part * kConsumerWarps);
+#else
       produce_batch(stages[s], *raw, rec, ids, base, min(kBatch, range.y - base), lane, tile_x0, tile_y0,
                     part * kConsumerWarps);
+#endif
       mbar_arrive(&full_bar[s]);
     }
     // the tile's work (splats handed to the consumers) for the next frame's schedule
@@ -372,7 +445,7 @@ blend_fwd_kernel(const float4* __restrict__ rec, const uint32_t* __restrict__ id
           live &= live - 1;
           // branch-light body: finished lanes evaluate too (free under SIMT)
           // and are masked by `take`
-          const AlphaEval e = eval_alpha_tile(lx, ly, fx, fy, st.k[j], st.m[j], rec, st.id, j);
+          const AlphaEval e = eval_alpha_tile(lx, ly, fx, fy, stage_k(st, j), st.m[j], rec, st.id, j);
           const float t_new = T * (1.0f - e.a);   // used only when blended
           const bool blend = !done && e.ok;
           const bool sat = t_new < (kTraining ? kTransSatHi : kTransSat);  // 1 - T_new > 0.9999
@@ -380,7 +453,7 @@ blend_fwd_kernel(const float4* __restrict__ rec, const uint32_t* __restrict__ id
           done = done || stopping;
           if (kTraining) t_stop = stopping ? t_new : t_stop;
           if (blend && !sat) {
-            const float4 c = st.col[j];
+            const float4 c = stage_col(st, j);
             const float w = T * e.a;
             cr = fmaf(w, c.x, cr);
             cg = fmaf(w, c.y, cg);
@@ -417,9 +490,34 @@ blend_fwd_kernel(const float4* __restrict__ rec, const uint32_t* __restrict__ id
 }
 
 template <bool kTraining>
-int launch(const int32_t* order, int32_t* work, const float4* rec, const uint32_t* ids, const int2* rg, int width, int height,
-           int tiles_x, int tile0,
+int launch(const int32_t* order, int32_t* work, const float4* rec, int64_t n, const uint32_t* ids, const int2* rg,
+           int width, int height, int tiles_x, int tile0,
            int64_t ntiles, float3 bg, float* image, float* t_final, int32_t* last, int32_t* fix, cudaStream_t s) {
+  CUtensorMap tmap{};
+#if GS_FWD_TMA
+  {   // 2-D map over the records: 20 floats x n rows (80-byte stride), box 16 x 1 (words 0-3)
+    using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+    static EncodeFn encode = nullptr;
+    if (!encode) {
+      cudaDriverEntryPointQueryResult q;
+      void* fn = nullptr;
+      if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn)
+        return GS_ERR_CUDA;
+      encode = reinterpret_cast<EncodeFn>(fn);
+    }
+    const cuuint64_t dims[2] = {cuuint64_t(kRecWords * 4), cuuint64_t(n > 0 ? n : 1)};
+    const cuuint64_t strides[1] = {cuuint64_t(kRecWords * 16)};
+    const cuuint32_t box[2] = {16, 1}, estr[2] = {1, 1};
+    if (encode(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float4*>(rec), dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return GS_ERR_CUDA;
+  }
+#else
+  (void)n;
+#endif
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(blend_fwd_kernel<kTraining>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -434,7 +532,7 @@ int launch(const int32_t* order, int32_t* work, const float4* rec, const uint32_
   }
   blend_fwd_kernel<kTraining><<<unsigned(ntiles * kParts), kThreads, kSmemBytes, s>>>(rec, ids, rg, width, height, tiles_x,
                                                                              tile0, bg, image, t_final, last,
-                                                                             order, work, fix);
+                                                                             order, work, fix, tmap);
   int st = check_launch();
   if (st != GS_OK || !kTraining) return st;
   blend_exact_kernel<<<148 * 6, kFixThreads, 0, s>>>(rec, ids, rg, width, tiles_x, bg, image, t_final, last, fix);
@@ -458,9 +556,9 @@ int blend_forward_rows(const gs_splats_t* splats, const uint32_t* sorted_ids, co
   const int tile0 = row_begin * tiles_x;
   const int64_t ntiles = int64_t(row_end - row_begin) * tiles_x;
   if (training)
-    return launch<true>(tile_order, tile_work, rec, sorted_ids, rg, width, height, tiles_x, tile0, ntiles, bg, image,
+    return launch<true>(tile_order, tile_work, rec, splats->n, sorted_ids, rg, width, height, tiles_x, tile0, ntiles, bg, image,
                         t_final, last, scratch, s);
-  return launch<false>(tile_order, tile_work, rec, sorted_ids, rg, width, height, tiles_x, tile0, ntiles, bg, image,
+  return launch<false>(tile_order, tile_work, rec, splats->n, sorted_ids, rg, width, height, tiles_x, tile0, ntiles, bg, image,
                        nullptr, nullptr, nullptr, s);
 }
 
