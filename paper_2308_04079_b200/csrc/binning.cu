@@ -52,8 +52,13 @@ constexpr int64_t kFlagZeroQuat = 1, kFlagCapacity = 2, kFlagLimit = 4;
 // depth sort
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
-constexpr int kItems = 16;
-constexpr int kSortTile = kThreads * kItems;   // 4096 keys per block
+constexpr int kItems = 16;                     // scan items per thread
+constexpr int kScanTile = kThreads * kItems;   // 4096 values per scan block
+#ifndef GS_SORT_ITEMS
+#define GS_SORT_ITEMS 8
+#endif
+constexpr int kSortItems = GS_SORT_ITEMS;      // depth keys per thread and sort pass
+constexpr int kSortTile = kThreads * kSortItems;
 constexpr int kRadix = 256;
 constexpr int kPasses = 4;
 constexpr uint64_t kStAgg = uint64_t(1) << 32, kStPre = uint64_t(2) << 32;
@@ -281,7 +286,7 @@ __global__ void __launch_bounds__(1024) sort_setup_kernel(const uint32_t* __rest
 #define GS_SORT_RANK_OR 1
 #endif
 #ifndef GS_SORT_MIN_BLOCKS
-#define GS_SORT_MIN_BLOCKS 3
+#define GS_SORT_MIN_BLOCKS 4
 #endif
 template <bool kFirst, bool kLast>
 __global__ void __launch_bounds__(kThreads, GS_SORT_MIN_BLOCKS) onesweep_kernel(
@@ -308,10 +313,10 @@ __global__ void __launch_bounds__(kThreads, GS_SORT_MIN_BLOCKS) onesweep_kernel(
   }
   __syncthreads();
   const uint32_t b = s_block;
-  const int64_t base = int64_t(b) * kSortTile + warp * (32 * kItems);
-  uint32_t key[kItems], val[kItems], rank[kItems];
+  const int64_t base = int64_t(b) * kSortTile + warp * (32 * kSortItems);
+  uint32_t key[kSortItems], val[kSortItems], rank[kSortItems];
 #pragma unroll
-  for (int j = 0; j < kItems; ++j) {
+  for (int j = 0; j < kSortItems; ++j) {
     const int64_t i = base + j * 32 + lane;
     if (kFirst) {
       key[j] = i < n ? depth_key(depth, tiles, i) : kCulledKey;
@@ -323,7 +328,7 @@ __global__ void __launch_bounds__(kThreads, GS_SORT_MIN_BLOCKS) onesweep_kernel(
   }
   const uint32_t lt = lanemask_lt();
 #pragma unroll
-  for (int j = 0; j < kItems; ++j) {
+  for (int j = 0; j < kSortItems; ++j) {
     const bool ok = base + j * 32 + lane < n;
     const uint32_t d = (key[j] >> shift) & 0xFFu;
     uint32_t peers;
@@ -370,7 +375,7 @@ __global__ void __launch_bounds__(kThreads, GS_SORT_MIN_BLOCKS) onesweep_kernel(
   }
   __syncthreads();
 #pragma unroll
-  for (int j = 0; j < kItems; ++j) {
+  for (int j = 0; j < kSortItems; ++j) {
     if (base + j * 32 + lane >= n) continue;
     const uint32_t d = (key[j] >> shift) & 0xFFu;
     const uint32_t lp = s_local[d] + s_cnt[warp][d] + rank[j];
@@ -455,7 +460,7 @@ __global__ void __launch_bounds__(kThreads) scan_kernel(uint32_t* data, int64_t 
   if (threadIdx.x == 0) s_block = atomicAdd(ticket, 1u);
   __syncthreads();
   const uint32_t b = s_block;
-  const int64_t i0 = int64_t(b) * kSortTile + int64_t(threadIdx.x) * kItems;
+  const int64_t i0 = int64_t(b) * kScanTile + int64_t(threadIdx.x) * kItems;
   uint32_t v[kItems];
   uint32_t sum = 0;
   if (i0 + kItems <= len) {
@@ -484,7 +489,7 @@ __global__ void __launch_bounds__(kThreads) scan_kernel(uint32_t* data, int64_t 
       st_status(st, kStPre | (excl + total));
     }
     s_excl = excl;
-    if (int64_t(b + 1) * kSortTile >= len) *total_out = excl + total;   // the last block
+    if (int64_t(b + 1) * kScanTile >= len) *total_out = excl + total;   // the last block
   }
   __syncthreads();
   uint32_t run = s_excl + excl_t;
@@ -1047,7 +1052,7 @@ int layout(int64_t n, int width, int height, int64_t cap, Layout* L) {
   L->mlen = int64_t(L->g.S) * L->chunks;
   L->wmax = (cap + kWindow - 1) / kWindow + L->g.S;
   const size_t un = size_t(n > 0 ? n : 1), ub = size_t(L->blocks > 0 ? L->blocks : 1);
-  const size_t scan_blocks = size_t((L->mlen + kSortTile - 1) / kSortTile) + 1;
+  const size_t scan_blocks = size_t((L->mlen + kScanTile - 1) / kScanTile) + 1;
   size_t off = 0;
   auto take = [&](size_t bytes) {
     const size_t o = off;
@@ -1187,7 +1192,7 @@ int bin_enqueue(const gs_splats_t* splats, int32_t width, int32_t height, void* 
                                                                        kinfo);
   if ((st = check_launch()) != GS_OK) return st;
   uint32_t* mtotal = at<uint32_t>(ws, L.mtotal);
-  scan_kernel<<<unsigned((L.mlen + kSortTile - 1) / kSortTile), kThreads, 0, s>>>(
+  scan_kernel<<<unsigned((L.mlen + kScanTile - 1) / kScanTile), kThreads, 0, s>>>(
       M, L.mlen, at<uint64_t>(ws, L.scan_status), tickets + 4, mtotal, kinfo);
   if ((st = check_launch()) != GS_OK) return st;
   window_setup_kernel<<<1, 1024, 0, s>>>(M, L.chunks, mtotal, g, at<uint32_t>(ws, L.bstart),
