@@ -95,17 +95,21 @@ __device__ __forceinline__ void st_status(uint64_t* p, uint64_t v) {
 
 // Decoupled look-back for one counter of block b: the exclusive prefix over
 // blocks [0, b), walking back over the predecessors' status words
-// (base + p * stride) eight at a time (one memory round trip per eight
-// blocks) until an inclusive prefix is met.
+// (base + p * stride) GS_LOOKBACK at a time (one memory round trip each)
+// until an inclusive prefix is met.
+#ifndef GS_LOOKBACK
+#define GS_LOOKBACK 8
+#endif
 __device__ __forceinline__ uint32_t look_back(const uint64_t* base, int64_t stride, int64_t b) {
+  constexpr int kW = GS_LOOKBACK;   // predecessors read per memory round trip
   uint32_t excl = 0;
-  for (int64_t p = b - 1; p >= 0; p -= 8) {
-    uint64_t v[8];
+  for (int64_t p = b - 1; p >= 0; p -= kW) {
+    uint64_t v[kW];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) v[i] = p - i >= 0 ? ld_status(base + (p - i) * stride) : kStPre;
+    for (int i = 0; i < kW; ++i) v[i] = p - i >= 0 ? ld_status(base + (p - i) * stride) : kStPre;
     bool done = false;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
+    for (int i = 0; i < kW; ++i) {
       if (!done) {
         while (v[i] == 0) v[i] = ld_status(base + (p - i) * stride);   // not yet published
         excl += uint32_t(v[i]);
