@@ -8,9 +8,11 @@ one training iteration: project -> bin/sort -> forward blend -> L1+D-SSIM
 loss (lambda 0.2) -> backward blend -> backward preprocess (+densify stats)
 -> fused Adam.  Multi-GPU (torchrun, BASELINE configs[3], "c4"): a batch of
 32 look-at 1080p cameras around the 3M-Gaussian ball scene per step, sharded
-32/N per rank; every rank accumulates its views' gradients, the gradients
-are reduce-scattered over NCCL, each rank runs Adam on its 1/N of the
-Gaussians and the parameters are all-gathered.  The metric counts view
+32/N per rank; every rank accumulates its views' gradients range by range
+(one Gaussian range per rank), the last view's per-range reductions to the
+range owners run on NCCL's stream while the later ranges are still being
+computed, each rank runs Adam on its 1/N of the Gaussians and the
+parameters are all-gathered.  The metric counts view
 iterations (one view's forward + backward and its share of the update) per
 second, so c3 at N = 1 and c4's 32-view batches share the unit; the N = 1
 line also reports c4's 32-view batch on one GPU (the c4 scaling base).
@@ -389,13 +391,14 @@ def c4_setup(n: int, rank: int, world: int, dev):
 
 def c4_batches(args, rank: int, world: int, dev, steps: int, warmup: int) -> dict:
     """Timed c4 steps: each rank renders / backpropagates its views into the
-    flat gradient bucket; then reduce-scatter + Adam on the rank's shard +
-    all-gather (distributed.ShardedAdam; plain Adam at world 1).  Returns
+    gradient bucket; the last view's per-Gaussian-range reductions to their
+    owners overlap its later ranges' backward, then Adam on the rank's range +
+    all-gather (distributed.OverlapShardedAdam; plain Adam at world 1).  Returns
     views/s over the whole batch (max over ranks)."""
     import torch
 
     from paper_2308_04079_b200 import rasterizer as R
-    from paper_2308_04079_b200.distributed import GradientBucket, ShardedAdam
+    from paper_2308_04079_b200.distributed import GradientBucket, OverlapShardedAdam
     from paper_2308_04079_b200.loss import l1_dssim_loss
     from paper_2308_04079_b200.optimizer import DeviceAdam, TrainConfig
     n = args.n_gaussians
@@ -403,8 +406,8 @@ def c4_batches(args, rank: int, world: int, dev, steps: int, warmup: int) -> dic
     config = TrainConfig(lambda_dssim=LAMBDA_DSSIM)
     stats = R.DensifyStats.zeros(n, dev)
     if world > 1:
-        opt = ShardedAdam(cloud)
-        grads = opt.grads
+        opt = OverlapShardedAdam(cloud)
+        grads = None
     else:
         opt, bucket = DeviceAdam(cloud), GradientBucket(n, dev)
         grads = bucket.grads
@@ -425,7 +428,10 @@ def c4_batches(args, rank: int, world: int, dev, steps: int, warmup: int) -> dic
             _, d_image = l1_dssim_loss(out.image, gt, LAMBDA_DSSIM)
             g2 = R.render_backward(d_image, out, splats, binning, WIDTH, HEIGHT, (0.0, 0.0, 0.0))
             orders[v] = g2.tile_order
-            R.backward_project(cloud, cam, splats, g2, DEGREE, stats=stats, out=grads, accumulate=True)
+            if world > 1:   # range by range; the last view's per-range reductions overlap the later ranges
+                opt.accumulate(cloud, cam, splats, g2, DEGREE, stats=stats, reduce=v == len(cams) - 1)
+            else:
+                R.backward_project(cloud, cam, splats, g2, DEGREE, stats=stats, out=grads, accumulate=True)
         if world > 1:
             opt.step(cloud, it[0], config)
         else:
@@ -448,7 +454,8 @@ def c4_batches(args, rank: int, world: int, dev, steps: int, warmup: int) -> dic
 
 def run_multi(args, rank: int, world: int, local_rank: int) -> None:
     """c4 on `world` GPUs: 32 views per step sharded 32/world per rank,
-    gradients reduce-scattered, Adam sharded, parameters all-gathered."""
+    gradients reduced range by range (overlapping the last view's backward),
+    Adam sharded, parameters all-gathered."""
     import torch
     import torch.distributed as dist
 
@@ -493,7 +500,8 @@ def run_multi(args, rank: int, world: int, local_rank: int) -> None:
         "config": {"workload": c4["workload"] + "; train_iters = view iterations (a view's fwd + loss + bwd "
                                                 "and its share of the update)",
                    "gaussians": args.n_gaussians, "width": WIDTH, "height": HEIGHT, "sh_degree": DEGREE,
-                   "views_per_step": C4_VIEWS, "parallelism": f"dp{world} (view-parallel, ZeRO-1 sharded Adam)",
+                   "views_per_step": C4_VIEWS, "parallelism": f"dp{world} (view-parallel, ZeRO-1 sharded Adam, range-wise reductions overlapping the "
+                                          "last view's backward)",
                    "l2": "inputs larger than L2"},
         "c4": c4,
         "e2e": {"value": round(C4_VIEWS * args.steps / (e_ms / 1e3), 3), "unit": UNIT,

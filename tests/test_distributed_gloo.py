@@ -138,3 +138,63 @@ def test_view_parallel_plumbing_world4():
         assert torch.allclose(res[r]["maxr"], torch.full((7,), 0.04))
         assert res[r]["verdict"] == [1, 0, 1, 0] and res[r]["any"] is True
         assert res[r]["draw"] == float(np.random.default_rng(100).standard_normal())
+
+
+def _overlap_worker(rank, world, port, results):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2308_04079_b200.cloud import GaussianCloud
+        from paper_2308_04079_b200.distributed import OverlapShardedAdam
+        n = 300
+        g = torch.Generator().manual_seed(0)
+        cloud = GaussianCloud(torch.randn(n, 3, generator=g), torch.randn(n, 4, generator=g),
+                              torch.randn(n, 3, generator=g), torch.randn(n, generator=g),
+                              torch.randn(n, 16, 3, generator=g))
+        means0 = cloud.means.clone()
+        opt = OverlapShardedAdam(cloud)
+        # every range's gradient block gets a rank-dependent value, then the
+        # per-range reductions run as the last view's backward would issue them
+        for r, (a, b) in enumerate(opt.bounds):
+            cg = opt.chunk_grads(r)
+            cg.d_means.fill_(rank + 1.0)
+            cg.d_sh[:, 0, 0] = 10.0 * (rank + 1) + r
+        for r in range(world):
+            opt._reduce_block(r)
+        for w in opt._works:
+            w.wait()
+        own = opt.chunk_grads(opt.rank)
+        results[rank] = {"per": opt.per, "bounds": opt.bounds, "lo": opt.lo, "hi": opt.hi,
+                         "own_means": own.d_means.clone(), "own_sh00": own.d_sh[:, 0, 0].clone(),
+                         "cloud_is_view": cloud.means.data_ptr() == opt.pbuf["means"].data_ptr(),
+                         "params_kept": bool(torch.equal(cloud.means, means0)),
+                         "block_aligned": all((opt.chunk[r][grp].data_ptr() % 16) == 0
+                                              for r in range(world) for grp in opt.chunk[r]),
+                         "blocks_in_flat": all(opt.blocks[r].data_ptr() == opt.flat.data_ptr() + 4 * r * opt.block
+                                               for r in range(world))}
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_overlap_sharded_layout_and_reduction(world):
+    """OverlapShardedAdam: rank-major gradient blocks (one per Gaussian range,
+    128-row aligned), the cloud re-homed into padded parameter buffers, and
+    the per-range reduction leaving every owner its range's summed gradient."""
+    port = _free_port()
+    with mp.Manager() as mgr:
+        results = mgr.dict()
+        mp.spawn(_overlap_worker, args=(world, port, results), nprocs=world, join=True)
+        res = dict(results)
+    total = sum(range(1, world + 1))
+    for rank in range(world):
+        r = res[rank]
+        assert r["per"] % 128 == 0 and r["per"] * world >= 300
+        assert r["bounds"][0][0] == 0 and r["bounds"][-1][1] == 300
+        assert all(r["bounds"][i][1] == r["bounds"][i + 1][0] for i in range(world - 1))
+        assert r["cloud_is_view"] and r["params_kept"] and r["block_aligned"] and r["blocks_in_flat"]
+        k = r["hi"] - r["lo"]
+        assert r["own_means"].shape == (k, 3)
+        assert torch.all(r["own_means"] == float(total))
+        assert torch.all(r["own_sh00"] == 10.0 * total + world * rank)

@@ -161,6 +161,63 @@ def test_sharded_adam_matches_replicated(cuda_device, tmp_path):
         assert torch.equal(res[0]["s"][k], res[1]["s"][k]), k
 
 
+def _overlap_worker(rank, world, port, out_dir):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch.distributed as dist
+    from paper_2308_04079_b200 import rasterizer as R
+    from paper_2308_04079_b200.cloud import GaussianCloud
+    from paper_2308_04079_b200.distributed import GradientBucket, OverlapShardedAdam
+    from paper_2308_04079_b200.loss import l1_dssim_loss
+    from paper_2308_04079_b200.optimizer import DeviceAdam, TrainConfig
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        cloud_np, tgt_np, cam = _scene()
+        views = _views(cam, GaussianCloud.from_numpy(**tgt_np))
+        cfg = TrainConfig(warmup_upsample_iters=(0, 0))
+        cloud_o = GaussianCloud.from_numpy(**cloud_np)
+        cloud_r = GaussianCloud.from_numpy(**cloud_np)
+        opt = OverlapShardedAdam(cloud_o)
+        replicated, bucket = DeviceAdam(cloud_r), GradientBucket(len(cloud_r), "cuda")
+        mine = [views[rank], views[1 - rank]]   # two views per rank, the second one reduces
+        for it in range(1, 4):
+            opt.zero_()
+            bucket.zero_()
+            for i, v in enumerate(mine):
+                # the same screen-space gradients feed both paths (the blend's float atomics are order-dependent)
+                out, splats, binning = R.render_view(cloud_r, v.camera, (0, 0, 0), 3, training=True)
+                _, d_image = l1_dssim_loss(out.image, v.image, cfg.lambda_dssim)
+                g2 = R.render_backward(d_image, out, splats, binning, v.camera.width, v.camera.height, (0, 0, 0))
+                R.backward_project(cloud_r, v.camera, splats, g2, 3, out=bucket.grads, accumulate=True)
+                splats_o = R._project_tensors(cloud_o.c_params(), len(cloud_o), "cuda", v.camera, 3)
+                assert torch.equal(splats_o.rec, splats.rec)
+                opt.accumulate(cloud_o, v.camera, splats_o, g2, 3, reduce=(i == len(mine) - 1))
+            opt.step(cloud_o, it, cfg)
+            bucket.allreduce_()
+            replicated.step(cloud_r, bucket.grads, it, cfg)
+        torch.save({"o": {g: getattr(cloud_o, g).cpu() for g in ("means", "sh", "rotations", "log_scales",
+                                                                  "opacity_logits")},
+                    "r": {g: getattr(cloud_r, g).cpu() for g in ("means", "sh", "rotations", "log_scales",
+                                                                  "opacity_logits")}},
+                   os.path.join(out_dir, f"ov{rank}.pt"))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_overlap_sharded_adam_matches_replicated(cuda_device, tmp_path):
+    """Range-by-range backward with the last view's per-range reductions
+    enqueued as the ranges finish, Adam on the rank's range, all-gather ==
+    all-reduce + full Adam (bit-identical at two ranks)."""
+    import torch.multiprocessing as mp
+    mp.start_processes(_overlap_worker, args=(2, _free_port(), str(tmp_path)), nprocs=2, start_method="spawn")
+    res = [torch.load(tmp_path / f"ov{r}.pt") for r in range(2)]
+    for r in res:
+        for k in r["o"]:
+            assert torch.equal(r["o"][k], r["r"][k]), k
+    for k in res[0]["o"]:
+        assert torch.equal(res[0]["o"][k], res[1]["o"][k]), k
+
+
 def test_multiview_two_streams_matches_one(cuda_device):
     """train_step_views with views alternating over 2 CUDA streams (per-stream
     buckets and statistics merged) == the single-stream accumulation."""
