@@ -122,19 +122,40 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
         run_single(args, local_rank)
 
 
+ALLOC_EVENTS: list = []   # caching-allocator cudaMalloc / cudaFree / retry counts per timed loop
+
+
 def _time_loop(step, steps: int, world: int, dev) -> float:
-    """Device milliseconds of `steps` calls of step(), max over ranks."""
+    """Device milliseconds of `steps` calls of step(), max over ranks.  The
+    device loop is enqueued without host synchronisation, so the GPU idles
+    whenever the host falls behind; Python's cyclic garbage collector (a
+    multi-millisecond pause at times) is therefore held off during the timed
+    region (collected just before it)."""
+    import gc
+
     import torch
     import torch.distributed as dist
+    gc.collect()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    s.record()
-    for i in range(steps):
-        step(i)
-    e.record()
-    torch.cuda.synchronize()
+    gc_was_enabled = gc.isenabled()
+    if os.environ.get("GS_BENCH_GC") != "1":
+        gc.disable()
+    m0 = torch.cuda.memory_stats(dev)
+    try:
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        for i in range(steps):
+            step(i)
+        e.record()
+        torch.cuda.synchronize()
+    finally:
+        if gc_was_enabled:
+            gc.enable()
+    m1 = torch.cuda.memory_stats(dev)
+    ALLOC_EVENTS.append({k: m1.get(k, 0) - m0.get(k, 0) for k in ("num_device_alloc", "num_device_free",
+                                                                   "num_alloc_retries", "num_sync_all_streams")})
     if world > 1:
         dist.barrier()
     ms = torch.tensor([s.elapsed_time(e)], device=dev)
@@ -218,9 +239,13 @@ def run_single(args, local_rank: int) -> None:
 
     # size the instance buffers once from a synchronous binning of the view
     R.bin_and_sort(R._project_tensors(cloud.c_params(), n, dev, cam, DEGREE), WIDTH, HEIGHT)
+    # the warm-up runs the timed path itself (it keeps the last step's
+    # buffers alive like the timed steps do), so the caching allocator has
+    # every block it needs before the timed region (no cudaMalloc inside it)
     for _ in range(args.warmup):
-        train_step(target, False)
+        train_step(target, True)
     torch.cuda.synchronize()
+    timer.events.clear()
     check_binned(binnings)
     clocks = ClockSampler(local_rank)
     clocks.start()
@@ -359,6 +384,7 @@ def run_single(args, local_rank: int) -> None:
         "c4_1gpu": c4,
         "gpu_launches": timer.launches_per_step() * args.steps,
         "roofline": roof["primary"], "roofline_hbm": roof["hbm"], "roofline_stages": roof["stages"],
+        "allocator_during_timed_loops": ALLOC_EVENTS[:4],
         "fp32_peak_tflops_measured": round(fp32_peak, 2),
         "fp32_peak_tflops_nominal": round(pk["fp32_nominal_tflops"], 2),
         "clocks": clock_info,
