@@ -35,16 +35,25 @@ sys.path.insert(0, str(ROOT))
 
 
 def timed(fn, steps: int, warmup: int):
+    """CUDA-event milliseconds per call; Python's cyclic GC is held off during
+    the timed calls (the loops are enqueued without host synchronisation)."""
+    import gc
+
     import torch
     for _ in range(warmup):
         fn()
+    gc.collect()
     torch.cuda.synchronize()
-    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    s.record()
-    for _ in range(steps):
-        fn()
-    e.record()
-    torch.cuda.synchronize()
+    gc.disable()
+    try:
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        for _ in range(steps):
+            fn()
+        e.record()
+        torch.cuda.synchronize()
+    finally:
+        gc.enable()
     return s.elapsed_time(e) / steps
 
 
