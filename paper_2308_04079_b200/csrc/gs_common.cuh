@@ -218,6 +218,9 @@ __device__ __forceinline__ int tile_py(int t) { return (t >> 6) * 4 + ((t & 31) 
 #ifndef GS_COVER_BALL
 #define GS_COVER_BALL 1
 #endif
+#ifndef GS_COVER_BALL_EXACT
+#define GS_COVER_BALL_EXACT 0
+#endif
 template <bool kExact = false, int kBlockH = 4>
 __device__ __forceinline__ uint32_t warp_cover_mask(float4 r0, float4 k, float alpha, float tile_x0, float tile_y0) {
   constexpr int kWarps = 2 * (kTile / kBlockH);
@@ -257,7 +260,7 @@ __device__ __forceinline__ uint32_t warp_cover_mask(float4 r0, float4 k, float a
     const float x0 = tile_x0 + float((w & 1) * 8) + 0.5f, y0 = tile_y0 + float((w >> 1) * kBlockH) + 0.5f;
     if (!(mx + hx >= x0 && mx - hx <= x0 + 7.0f && my + hy >= y0 && my - hy <= y0 + float(kBlockH - 1))) continue;
 #if GS_COVER_BALL
-    if (!kExact) {
+    if (!kExact || GS_COVER_BALL_EXACT) {   // with kExact: a cheap pre-filter of the exact test
       const float cx = x0 + 3.5f - mx, cy = y0 + 0.5f * float(kBlockH - 1) - my;
       const float u = fmaf(k.x, cx, k.y * cy), v = fmaf(k.z, cx, k.w * cy);
       if (fmaf(u, u, v * v) > ball_r2) continue;
