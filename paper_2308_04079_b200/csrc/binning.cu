@@ -841,24 +841,28 @@ __global__ void __launch_bounds__(kThreads) window_prefix_kernel(const uint32_t*
 }
 
 // One block of 1024 threads: exclusive scan of the tile totals in tile order
-// -> ranges [start, end), empty tiles [0, 0] (rasterizer.py:118-123).  A
-// flagged frame gets all-empty ranges.
+// -> ranges [start, end), empty tiles [0, 0] (rasterizer.py:118-123), in
+// rounds of 4096 consecutive tiles (4 per thread: coalesced loads and
+// stores) carrying the running total.  A flagged frame gets all-empty ranges.
 __global__ void __launch_bounds__(1024) tile_ranges_kernel(const uint32_t* __restrict__ tile_total, int64_t tiles,
                                                            int2* __restrict__ ranges,
                                                            const int64_t* __restrict__ kinfo) {
   __shared__ uint32_t s_w[33];
   const bool flagged = kinfo[1] != 0;
-  const int64_t per = (tiles + blockDim.x - 1) / blockDim.x;
-  const int64_t t0 = int64_t(threadIdx.x) * per, t1 = min(t0 + per, tiles);
-  uint32_t sum = 0;
-  if (!flagged)
-    for (int64_t t = t0; t < t1; ++t) sum += tile_total[t];
-  uint32_t total;
-  uint32_t run = block_exclusive_sum(sum, s_w, &total);
-  for (int64_t t = t0; t < t1; ++t) {
-    const uint32_t c = flagged ? 0u : tile_total[t];
-    ranges[t] = c ? make_int2(int(run), int(run + c)) : make_int2(0, 0);
-    run += c;
+  uint32_t carry = 0;
+  for (int64_t base = 0; base < tiles; base += 4 * 1024) {
+    const int64_t t0 = base + 4 * int64_t(threadIdx.x);
+    uint32_t c[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) c[u] = (!flagged && t0 + u < tiles) ? tile_total[t0 + u] : 0u;
+    uint32_t total;
+    uint32_t run = carry + block_exclusive_sum(c[0] + c[1] + c[2] + c[3], s_w, &total);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (t0 + u < tiles) ranges[t0 + u] = c[u] ? make_int2(int(run), int(run + c[u])) : make_int2(0, 0);
+      run += c[u];
+    }
+    carry += total;
   }
 }
 
