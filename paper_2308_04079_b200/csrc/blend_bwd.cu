@@ -42,6 +42,9 @@ namespace {
 #ifndef GS_BWD_MIN_BLOCKS
 #define GS_BWD_MIN_BLOCKS 6  // half-tile CTAs: 64 registers, 6 CTAs (24 warps) per SM
 #endif
+#ifndef GS_BWD_EXACT_MASK
+#define GS_BWD_EXACT_MASK 1   // 0: the forward's box + eigen-metric ball masks
+#endif
 #ifndef GS_BWD_BATCH
 #define GS_BWD_BATCH 64
 #endif
@@ -263,7 +266,7 @@ blend_bwd_kernel(const float* __restrict__ d_image, const float4* __restrict__ r
             const float alpha = st.col[e].w;
             float2 ctr;
             make_tile_splat(r0, k, alpha, tile_x0, tile_y0, st.m[e], ctr);
-            st.mask[e] = uint8_t(warp_cover_mask<true>(r0, k, alpha, tile_x0, tile_y0) >> (part * kConsumerWarps));
+            st.mask[e] = uint8_t(warp_cover_mask<GS_BWD_EXACT_MASK != 0>(r0, k, alpha, tile_x0, tile_y0) >> (part * kConsumerWarps));
           }
         }
         mbar_arrive(&full_bar[s]);
