@@ -43,7 +43,7 @@ namespace {
 #define GS_BWD_MIN_BLOCKS 6  // half-tile CTAs: 64 registers, 6 CTAs (24 warps) per SM
 #endif
 #ifndef GS_BWD_EXACT_MASK
-#define GS_BWD_EXACT_MASK 1   // 0: the forward's box + eigen-metric ball masks
+#define GS_BWD_EXACT_MASK 0   // 1: exact ellipse-vs-block masks (slower since the ball test: 1.031 vs 0.994 ms)
 #endif
 #ifndef GS_BWD_BATCH
 #define GS_BWD_BATCH 64
