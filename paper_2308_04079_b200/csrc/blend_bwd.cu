@@ -31,6 +31,12 @@
 // keep each axis at its own relative precision.  The projection backward
 // forms d Sigma' = 2 / log2(e)^2 K^T M K in float64 (preprocess_bwd.cu);
 // SplatGrads2D.d_conic converts M back to the reference's d_conic.
+// coverage masks: box + eigen-metric ball + the directional separating-axis
+// test (GS_COVER_BALL 2, gs_common.cuh): 0.980 vs 0.991 ms here; the
+// forward keeps 1 (its single producer warp: 0.664 vs 0.569 ms with 2)
+#ifndef GS_COVER_BALL
+#define GS_COVER_BALL 2
+#endif
 #include "gs_common.cuh"
 
 namespace gs {

@@ -245,6 +245,7 @@ __device__ __forceinline__ uint32_t warp_cover_mask(float4 r0, float4 k, float a
   const float ball_r = sqrtf(tau) + 3.5f * sqrtf(k.x * k.x + k.z * k.z) +
                        (0.5f * float(kBlockH - 1)) * sqrtf(k.y * k.y + k.w * k.w);
   const float ball_r2 = ball_r * ball_r * 1.0002f + 1e-3f;
+  const float sat_r2 = tau * 1.0002f + 1e-3f;   // (GS_COVER_BALL >= 2) the contour radius^2, inflated
 #endif
   // exact test for the blocks whose box overlaps the contour's box: the
   // minimum of the convex |k d|^2 over the block's pixel-centre rectangle (0
@@ -263,7 +264,19 @@ __device__ __forceinline__ uint32_t warp_cover_mask(float4 r0, float4 k, float a
     if (!kExact || GS_COVER_BALL_EXACT) {   // with kExact: a cheap pre-filter of the exact test
       const float cx = x0 + 3.5f - mx, cy = y0 + 0.5f * float(kBlockH - 1) - my;
       const float u = fmaf(k.x, cx, k.y * cy), v = fmaf(k.z, cx, k.w * cy);
-      if (fmaf(u, u, v * v) > ball_r2) continue;
+      const float d2 = fmaf(u, u, v * v);
+      if (d2 > ball_r2) continue;
+#if GS_COVER_BALL >= 2
+      // separating axis through the centre's image c' = (u, v): the block's
+      // image (a parallelogram, half-edges 3.5 K e_x and hh K e_y) reaches at
+      // most A / |c'| towards the origin along c', A = 3.5 |c'.K e_x| + hh
+      // |c'.K e_y|; missed when |c'| - A / |c'| > sqrt(tau), i.e. (squared,
+      // for d2 > A) (d2 - A)^2 > tau' d2
+      const float hh = 0.5f * float(kBlockH - 1);
+      const float A = (3.5f * fabsf(fmaf(u, k.x, v * k.z)) + hh * fabsf(fmaf(u, k.y, v * k.w))) * 1.001f + 1e-3f;
+      const float e = d2 - A;
+      if (e > 0.0f && e * e > sat_r2 * d2) continue;
+#endif
     }
 #endif
     if (kExact) {
