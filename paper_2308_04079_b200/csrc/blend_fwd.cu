@@ -44,7 +44,11 @@ constexpr int kStages = GS_FWD_STAGES;
 #endif
 constexpr int kParts = GS_FWD_PARTS;
 constexpr int kConsumerWarps = 8 / kParts;
-constexpr int kThreads = (kConsumerWarps + 1) * 32;
+#ifndef GS_FWD_PRODUCERS
+#define GS_FWD_PRODUCERS 1   // producer warps; producer p fills batches p, p + P, ... (kStages % P == 0)
+#endif
+constexpr int kProducers = GS_FWD_PRODUCERS;
+constexpr int kThreads = (kConsumerWarps + kProducers) * 32;
 
 #ifndef GS_FWD_TMA
 #define GS_FWD_TMA 0     // 1: the producer gathers the records with TMA tile::gather4 (see produce_batch_tma)
@@ -76,7 +80,7 @@ __device__ __forceinline__ float4 stage_col(const FwdStage& st, int j) { return 
 struct RawRec {          // the producer's landing buffer for the cp.async gathers
   float4 r0[kBatch];
 };
-constexpr size_t kSmemBytes = sizeof(FwdStage) * kStages + sizeof(RawRec);
+constexpr size_t kSmemBytes = sizeof(FwdStage) * kStages + sizeof(RawRec) * kProducers;
 #endif
 
 #if GS_FWD_TMA
@@ -353,7 +357,8 @@ blend_fwd_kernel(const float4* __restrict__ rec, const uint32_t* __restrict__ id
   RawRec* raw = reinterpret_cast<RawRec*>(smem_raw + sizeof(FwdStage) * kStages);
 #endif
   __shared__ uint64_t full_bar[kStages], empty_bar[kStages];
-  __shared__ int s_done, s_stop;
+  __shared__ int s_done, s_stop, s_work;
+  static_assert(kStages % kProducers == 0, "every stage must have a single producer");
 
   const int tile = tile_order ? tile_order[int(blockIdx.x) / kParts] : tile0 + int(blockIdx.x) / kParts;
   const int part = int(blockIdx.x) % kParts;   // this CTA's rows: [part * 16 / kParts, (part + 1) * 16 / kParts)
@@ -374,15 +379,17 @@ blend_fwd_kernel(const float4* __restrict__ rec, const uint32_t* __restrict__ id
     }
     s_done = 0;
     s_stop = 0;
+    s_work = 0;
 #if GS_FWD_TMA
     fence_mbarrier_init();
 #endif
   }
   __syncthreads();
 
-  if (warp == kConsumerWarps) {  // ---------------- producer warp
-    int b = 0;
-    for (; b < nb; ++b) {
+  if (warp >= kConsumerWarps) {  // ---------------- producer warp(s)
+    const int prod = warp - kConsumerWarps;
+    int b = prod;
+    for (; b < nb; b += kProducers) {
       const int s = b % kStages;
       bool stop = false;
       if (b >= kStages) {
@@ -399,13 +406,19 @@ blend_fwd_kernel(const float4* __restrict__ rec, const uint32_t* __restrict__ id
       produce_batch_tma(stages[s], &tma_bar[s], uint32_t(b / kStages) & 1u, &tmap, rec, ids, base,
                         min(kBatch, range.y - base), lane, tile_x0, tile_y0, part * kConsumerWarps);
 #else
-      produce_batch(stages[s], *raw, rec, ids, base, min(kBatch, range.y - base), lane, tile_x0, tile_y0,
+      produce_batch(stages[s], raw[prod], rec, ids, base, min(kBatch, range.y - base), lane, tile_x0, tile_y0,
                     part * kConsumerWarps);
 #endif
       mbar_arrive(&full_bar[s]);
     }
     // the tile's work (splats handed to the consumers) for the next frame's schedule
-    if (tile_work && lane == 0) tile_work[tile] = b * kBatch;
+    if (kProducers == 1) {
+      if (tile_work && lane == 0) tile_work[tile] = b * kBatch;
+    } else if (tile_work) {
+      if (lane == 0) atomicMax(&s_work, b - kProducers + 1);   // batches handed, up to the producers' stagger
+      asm volatile("bar.sync 1, %0;" ::"r"(kProducers * 32) : "memory");
+      if (prod == 0 && lane == 0) tile_work[tile] = min(s_work, nb) * kBatch;
+    }
     return;
   }
 
