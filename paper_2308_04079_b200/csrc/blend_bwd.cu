@@ -272,7 +272,8 @@ blend_bwd_kernel(const float* __restrict__ d_image, const float4* __restrict__ r
             const float alpha = st.col[e].w;
             float2 ctr;
             make_tile_splat(r0, k, alpha, tile_x0, tile_y0, st.m[e], ctr);
-            st.mask[e] = uint8_t(warp_cover_mask<GS_BWD_EXACT_MASK != 0>(r0, k, alpha, tile_x0, tile_y0) >> (part * kConsumerWarps));
+            st.mask[e] = uint8_t(warp_cover_mask<GS_BWD_EXACT_MASK != 0, 4, kConsumerWarps / 2>(
+                r0, k, alpha, tile_x0, tile_y0 + float(part * (kTile / kParts))));
           }
         }
         mbar_arrive(&full_bar[s]);

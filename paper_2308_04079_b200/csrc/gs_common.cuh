@@ -221,9 +221,11 @@ __device__ __forceinline__ int tile_py(int t) { return (t >> 6) * 4 + ((t & 31) 
 #ifndef GS_COVER_BALL_EXACT
 #define GS_COVER_BALL_EXACT 0
 #endif
-template <bool kExact = false, int kBlockH = 4>
+// kRows: block rows tested from tile_y0 (a half-tile CTA passes 2 and its
+// half's origin, so only its own four blocks are tested)
+template <bool kExact = false, int kBlockH = 4, int kRows = kTile / kBlockH>
 __device__ __forceinline__ uint32_t warp_cover_mask(float4 r0, float4 k, float alpha, float tile_x0, float tile_y0) {
-  constexpr int kWarps = 2 * (kTile / kBlockH);
+  constexpr int kWarps = 2 * kRows;
   constexpr uint32_t kAll = (1u << kWarps) - 1u;
   if (alpha < kAlphaEps * (1.0f - 1e-5f)) return 0u;
   // alpha 2^-(|k d|^2) >= 1/255  <=>  |k d|^2 <= tau = log2(255 alpha)
