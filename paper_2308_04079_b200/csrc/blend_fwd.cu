@@ -145,7 +145,11 @@ __device__ __forceinline__ void produce_batch(FwdStage& st, RawRec& raw, const f
       const float alpha = st.col[e].w;
       float2 ctr;
       make_tile_splat(r0, k, alpha, tile_x0, tile_y0, st.m[e], ctr);
-      st.mask[e] = uint8_t(warp_cover_mask<GS_FWD_EXACT != 0>(r0, k, alpha, tile_x0, tile_y0) >> mask_shift);
+      // kParts = 2: only the half tile's blocks (mask_shift = part * 4 rows of 4 px)
+      st.mask[e] = kParts == 1
+                       ? uint8_t(warp_cover_mask<GS_FWD_EXACT != 0>(r0, k, alpha, tile_x0, tile_y0))
+                       : uint8_t(warp_cover_mask<GS_FWD_EXACT != 0, 4, kConsumerWarps / 2>(
+                             r0, k, alpha, tile_x0, tile_y0 + float(mask_shift / kConsumerWarps * (kTile / kParts))));
     }
   }
 }
