@@ -221,6 +221,9 @@ __device__ __forceinline__ int tile_py(int t) { return (t >> 6) * 4 + ((t & 31) 
 #ifndef GS_COVER_BALL_EXACT
 #define GS_COVER_BALL_EXACT 0
 #endif
+#ifndef GS_COVER_FAST
+#define GS_COVER_FAST 1   // separable box + incremental centre images (branch-free); 0: per-block loop
+#endif
 // kRows: block rows tested from tile_y0 (a half-tile CTA passes 2 and its
 // half's origin, so only its own four blocks are tested)
 template <bool kExact = false, int kBlockH = 4, int kRows = kTile / kBlockH>
@@ -248,6 +251,43 @@ __device__ __forceinline__ uint32_t warp_cover_mask(float4 r0, float4 k, float a
                        (0.5f * float(kBlockH - 1)) * sqrtf(k.y * k.y + k.w * k.w);
   const float ball_r2 = ball_r * ball_r * 1.0002f + 1e-3f;
   const float sat_r2 = tau * 1.0002f + 1e-3f;   // (GS_COVER_BALL >= 2) the contour radius^2, inflated
+#endif
+#if GS_COVER_BALL && GS_COVER_FAST
+  if (!kExact) {
+    // branch-free form: the box test is separable (2 block columns x kRows
+    // rows), and the block centres' images c' = K (c - mean) step by the
+    // constant 8 K e_x per column and kBlockH K e_y per row
+    const float cx0 = tile_x0 + 4.0f - mx, cy0 = tile_y0 + 0.5f * float(kBlockH) - my;
+    const float u00 = fmaf(k.x, cx0, k.y * cy0), v00 = fmaf(k.z, cx0, k.w * cy0);
+    const float dux = 8.0f * k.x, dvx = 8.0f * k.z, duy = float(kBlockH) * k.y, dvy = float(kBlockH) * k.w;
+    bool okx[2];
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      const float x0 = tile_x0 + float(c * 8) + 0.5f;
+      okx[c] = (mx + hx >= x0) && (mx - hx <= x0 + 7.0f);
+    }
+    uint32_t m = 0u;
+#pragma unroll
+    for (int r = 0; r < kRows; ++r) {
+      const float y0 = tile_y0 + float(r * kBlockH) + 0.5f;
+      const bool oky = (my + hy >= y0) && (my - hy <= y0 + float(kBlockH - 1));
+      const float ur = fmaf(float(r), duy, u00), vr = fmaf(float(r), dvy, v00);
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const float u = c ? ur + dux : ur, v = c ? vr + dvx : vr;
+        const float d2 = fmaf(u, u, v * v);
+        bool pass = okx[c] && oky && d2 <= ball_r2;
+#if GS_COVER_BALL >= 2
+        const float hh = 0.5f * float(kBlockH - 1);
+        const float A = (3.5f * fabsf(fmaf(u, k.x, v * k.z)) + hh * fabsf(fmaf(u, k.y, v * k.w))) * 1.001f + 1e-3f;
+        const float e = d2 - A;
+        pass = pass && !(e > 0.0f && e * e > sat_r2 * d2);
+#endif
+        m |= pass ? (1u << (2 * r + c)) : 0u;
+      }
+    }
+    return m;
+  }
 #endif
   // exact test for the blocks whose box overlaps the contour's box: the
   // minimum of the convex |k d|^2 over the block's pixel-centre rectangle (0
