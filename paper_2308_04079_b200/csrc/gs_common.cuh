@@ -224,6 +224,12 @@ __device__ __forceinline__ int tile_py(int t) { return (t >> 6) * 4 + ((t & 31) 
 #ifndef GS_COVER_FAST
 #define GS_COVER_FAST 1   // separable box + incremental centre images (branch-free); 0: per-block loop
 #endif
+// |(a, b)| by the MUFU reciprocal square root (0 for a zero vector)
+__device__ __forceinline__ float fast_norm(float a, float b) {
+  const float q = fmaf(a, a, b * b);
+  return q > 0.0f ? q * rsqrtf(q) : 0.0f;
+}
+
 // kRows: block rows tested from tile_y0 (a half-tile CTA passes 2 and its
 // half's origin, so only its own four blocks are tested)
 template <bool kExact = false, int kBlockH = 4, int kRows = kTile / kBlockH>
@@ -236,10 +242,14 @@ __device__ __forceinline__ uint32_t warp_cover_mask(float4 r0, float4 k, float a
   // det k = f1 f2 (ex^2 + ey^2): a sum of same-signed terms, no cancellation
   const float detk = k.x * k.w - k.y * k.z;
   if (!(detk > 0.0f)) return kAll;  // degenerate basis: never cull
-  // the contour's half extents: sqrt(tau) |row of k^-1|
-  const float st = sqrtf(tau) / detk;
-  const float hx = st * sqrtf(k.y * k.y + k.w * k.w) * 1.001f + 0.05f;
-  const float hy = st * sqrtf(k.x * k.x + k.z * k.z) * 1.001f + 0.05f;
+  // the contour's half extents: sqrt(tau) |row of k^-1|.  The square roots
+  // and the division are the MUFU approximations (a few ulp): every bound
+  // below carries a 1e-3 relative inflation, so the masks stay conservative
+  const float sqrt_tau = tau * rsqrtf(tau);   // tau >= 1e-4 > 0
+  const float kex = fast_norm(k.x, k.z), key = fast_norm(k.y, k.w);   // |K e_x|, |K e_y|
+  const float st = __fdividef(sqrt_tau, detk);
+  const float hx = st * key * 1.001f + 0.05f;
+  const float hy = st * kex * 1.001f + 0.05f;
   const float mx = r0.x + r0.z, my = r0.y + r0.w;
 #if GS_COVER_BALL
   // !kExact: a cheap conservative metric test after the box test: in the
@@ -247,8 +257,7 @@ __device__ __forceinline__ uint32_t warp_cover_mask(float4 r0, float4 k, float a
   // the block's pixel centres lie within hw |K e_x| + hh |K e_y| of its
   // centre's image (triangle inequality), so the block is missed when
   // |K (c - mean)| exceeds sqrt(tau) plus that radius
-  const float ball_r = sqrtf(tau) + 3.5f * sqrtf(k.x * k.x + k.z * k.z) +
-                       (0.5f * float(kBlockH - 1)) * sqrtf(k.y * k.y + k.w * k.w);
+  const float ball_r = sqrt_tau + 3.5f * kex + (0.5f * float(kBlockH - 1)) * key;
   const float ball_r2 = ball_r * ball_r * 1.0002f + 1e-3f;
   const float sat_r2 = tau * 1.0002f + 1e-3f;   // (GS_COVER_BALL >= 2) the contour radius^2, inflated
 #endif
