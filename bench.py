@@ -220,8 +220,8 @@ def run_single(args, local_rank: int) -> None:
             out = R.render_forward(splats, binning, WIDTH, HEIGHT, bg, training=True, tile_order=prev_order[0])
         with StageTimer.stage(tm, "loss"):
             loss, d_image = l1_dssim_loss(out.image, gt, LAMBDA_DSSIM)
-        with StageTimer.stage(tm, "blend_bwd"):
-            g2 = R.render_backward(d_image, out, splats, binning, WIDTH, HEIGHT, bg)
+        # the blend kernel timed alone ("blend_bwd"); schedule + row clearing as "blend_bwd_setup"
+        g2 = R.render_backward(d_image, out, splats, binning, WIDTH, HEIGHT, bg, stage_timer=tm)
         prev_order[0] = g2.tile_order
         if os.environ.get("GS_BENCH_UNFUSED") != "1":
             # backward_project + stats + Adam fused (no gradient round trip)
@@ -383,7 +383,8 @@ def run_single(args, local_rank: int) -> None:
                                  "target H2D and loss.item() every step"},
         "c4_1gpu": c4,
         "gpu_launches": timer.launches_per_step() * args.steps,
-        "roofline": roof["primary"], "roofline_hbm": roof["hbm"], "roofline_stages": roof["stages"],
+        "roofline": roof["primary"], "roofline_hbm": roof["hbm"], "roofline_fp32": roof["fp32"],
+        "roofline_stages": roof["stages"],
         "allocator_during_timed_loops": ALLOC_EVENTS[:4],
         "fp32_peak_tflops_measured": round(fp32_peak, 2),
         "fp32_peak_tflops_nominal": round(pk["fp32_nominal_tflops"], 2),

@@ -271,6 +271,17 @@ int gs_blend_backward_scheduled(const float* d_image, const gs_splats_t* splats,
                                 int32_t height, const float background[3], int32_t* scratch, float* grads2d,
                                 void* stream);
 
+/* The two halves of gs_blend_backward_scheduled: the longest-first order into
+ * scratch[0, tiles) (scratch: device int32[2 * tiles + 2048]), and the blend
+ * kernel alone, accumulating into a caller-cleared grads2d (tile_order
+ * nullable: row-major). */
+int gs_blend_backward_schedule(const int32_t* ranges, const int32_t* last, int32_t width, int32_t height,
+                               int32_t* scratch, void* stream);
+int gs_blend_backward_accumulate(const float* d_image, const gs_splats_t* splats, const uint32_t* sorted_ids,
+                                 const int32_t* ranges, const float* t_final, const int32_t* last, int32_t width,
+                                 int32_t height, const float background[3], const int32_t* tile_order,
+                                 float* grads2d, void* stream);
+
 /* Deterministic backward blend (the reference's deterministic=True /
  * workers=1 contract, rasterizer.py:32-41: bit-identical runs): no float
  * atomics — one partial row per (sorted instance, half tile), summed per

@@ -115,6 +115,9 @@ SIGNATURES = [
     ("gs_tile_schedule", c_int32, [c_void_p, c_int32, c_void_p, c_void_p, c_void_p]),
     ("gs_blend_backward_scheduled", c_int32, [c_void_p, POINTER(GsSplats), c_void_p, c_void_p, c_void_p, c_void_p,
                                               c_int32, c_int32, POINTER(c_float), c_void_p, c_void_p, c_void_p]),
+    ("gs_blend_backward_schedule", c_int32, [c_void_p, c_void_p, c_int32, c_int32, c_void_p, c_void_p]),
+    ("gs_blend_backward_accumulate", c_int32, [c_void_p, POINTER(GsSplats), c_void_p, c_void_p, c_void_p, c_void_p,
+                                               c_int32, c_int32, POINTER(c_float), c_void_p, c_void_p, c_void_p]),
     ("gs_blend_backward_det_workspace_size", c_int32, [c_int64, c_int32, c_int32, c_int64, POINTER(c_size_t)]),
     ("gs_blend_backward_deterministic", c_int32, [c_void_p, POINTER(GsSplats), c_void_p, c_void_p, c_void_p, c_void_p,
                                                   c_int32, c_int32, POINTER(c_float), c_void_p, c_void_p, c_size_t,

@@ -541,13 +541,11 @@ __global__ void tile_sched_scatter_kernel(const int32_t* __restrict__ bucket_of,
 }  // namespace
 }  // namespace gs
 
-extern "C" int gs_blend_backward_scheduled(const float* d_image, const gs_splats_t* splats,
-                                           const uint32_t* sorted_ids, const int32_t* ranges, const float* t_final,
-                                           const int32_t* last, int32_t width, int32_t height,
-                                           const float background[3], int32_t* scratch, float* grads2d,
-                                           void* stream) {
+// The longest-first order alone (scratch[0, tiles) receives it).
+extern "C" int gs_blend_backward_schedule(const int32_t* ranges, const int32_t* last, int32_t width, int32_t height,
+                                          int32_t* scratch, void* stream) {
   using namespace gs;
-  if (!splats || !grads2d || !scratch || !ranges || !last || width <= 0 || height <= 0) return GS_ERR_INVALID_ARG;
+  if (!scratch || !ranges || !last || width <= 0 || height <= 0) return GS_ERR_INVALID_ARG;
   const int tiles_x = (width + kTile - 1) / kTile, tiles_y = (height + kTile - 1) / kTile;
   const int64_t tiles64 = int64_t(tiles_x) * tiles_y;
   if (tiles64 > int64_t(INT32_MAX) / 4) return GS_ERR_RESOURCE_LIMIT;
@@ -563,10 +561,32 @@ extern "C" int gs_blend_backward_scheduled(const float* d_image, const gs_splats
       last, reinterpret_cast<const int2*>(ranges), width, height, tiles_x, tiles, bucket_of, hist);
   tile_sched_scan_kernel<<<1, kSchedBuckets, 0, s>>>(hist, cursor);
   tile_sched_scatter_kernel<<<unsigned((tiles + 255) / 256), 256, 0, s>>>(bucket_of, cursor, tiles, order);
-  int st = check_launch();
+  return check_launch();
+}
+
+// The blend kernel alone: accumulates into the caller's grads2d (no
+// clearing), tiles in `tile_order` (nullable: row-major).
+extern "C" int gs_blend_backward_accumulate(const float* d_image, const gs_splats_t* splats,
+                                            const uint32_t* sorted_ids, const int32_t* ranges, const float* t_final,
+                                            const int32_t* last, int32_t width, int32_t height,
+                                            const float background[3], const int32_t* tile_order, float* grads2d,
+                                            void* stream) {
+  using namespace gs;
+  if (!splats || !grads2d || width <= 0 || height <= 0) return GS_ERR_INVALID_ARG;
+  return blend_backward_rows(d_image, splats, sorted_ids, ranges, t_final, last, width, height, 0,
+                             (height + kTile - 1) / kTile, background, grads2d, stream, tile_order);
+}
+
+extern "C" int gs_blend_backward_scheduled(const float* d_image, const gs_splats_t* splats,
+                                           const uint32_t* sorted_ids, const int32_t* ranges, const float* t_final,
+                                           const int32_t* last, int32_t width, int32_t height,
+                                           const float background[3], int32_t* scratch, float* grads2d,
+                                           void* stream) {
+  if (!splats || !grads2d) return GS_ERR_INVALID_ARG;
+  const int st = gs_blend_backward_schedule(ranges, last, width, height, scratch, stream);
   if (st != GS_OK) return st;
   return gs_blend_backward_ordered(d_image, splats, sorted_ids, ranges, t_final, last, width, height, background,
-                                   order, grads2d, stream);
+                                   scratch, grads2d, stream);
 }
 
 // Longest-first order of `tiles` tiles from any per-tile work estimate

@@ -25,10 +25,11 @@ import torch
 
 # our own __global__ kernels launched per training step (every one hand-written;
 # blend_fwd: the blend + the exact re-blend of undecidable stops; blend_bwd:
-# the three tile-schedule kernels + the blend; bin_and_sort: depth histogram,
+# the blend (its three tile-schedule kernels: blend_bwd_setup); bin_and_sort: depth histogram,
 # sort setup, 4 onesweep passes, bucket count, scan, window setup, bucket
 # scatter, window count, window prefix, tile ranges, instance write)
-KERNELS_PER_STEP = {"preprocess_fwd": 1, "bin_and_sort": 14, "blend_fwd": 2, "loss": 3, "blend_bwd": 4,
+KERNELS_PER_STEP = {"preprocess_fwd": 1, "bin_and_sort": 14, "blend_fwd": 2, "loss": 3, "blend_bwd": 1,
+                    "blend_bwd_setup": 3,
                     "preprocess_bwd": 1, "adam": 1, "preprocess_bwd_adam": 1, "sharded_adam": 1}
 
 
@@ -118,31 +119,32 @@ class StageTimer:
                     st.update({"algorithmic_flops": flops[k], "achieved_tflops": round(tf, 2),
                                "frac_fp32": round(tf / fp32, 4)})
                 stages[k] = st
-        dom = max(ms, key=lambda k: ms[k]) if ms else None
+        def fp32_entry(k):
+            st = stages[k]
+            return {"kernel": k, "bound": "fp32", "achieved": st["achieved_tflops"], "peak": round(fp32, 2),
+                    "unit": "TFLOP/s", "frac": st["frac_fp32"], "traffic": traffic.get(k),
+                    "peak_source": "max(in-run FP32 FMA probe gs_fp32_fma_probe, nominal SMs x 128 x 2 x "
+                                   "sm_max_mhz); MEASURED_PEAKS.json has no FP32 figure and this kernel is "
+                                   "FP32-issue-bound, not HBM/tensor",
+                    "algorithmic": f"{st['algorithmic_flops']:.4g} FLOP per launch "
+                                   f"(25|60 FP32 ops x E={e_pairs} evaluated pairs)"}
+
+        def hbm_entry(k):
+            st = stages[k]
+            return {"kernel": k, "bound": "hbm", "achieved": st["achieved_gbs"], "peak": hbm,
+                    "unit": "GB/s", "frac": st["frac_hbm"], "traffic": traffic.get(k),
+                    "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6650"}
+
+        timed = [k for k in ms if k in stages]
+        dom = max(timed, key=lambda k: ms[k]) if timed else None
         primary = None
-        if dom in stages:
-            st = stages[dom]
-            if "frac_fp32" in st:
-                primary = {"kernel": dom, "bound": "fp32", "achieved": st["achieved_tflops"], "peak": round(fp32, 2),
-                           "unit": "TFLOP/s", "frac": st["frac_fp32"], "traffic": traffic.get(dom),
-                           "peak_source": "max(in-run FP32 FMA probe gs_fp32_fma_probe, nominal SMs x 128 x 2 x "
-                                          "sm_max_mhz); MEASURED_PEAKS.json has no FP32 figure and this kernel is "
-                                          "FP32-issue-bound, not HBM/tensor",
-                           "algorithmic": f"{st['algorithmic_flops']:.4g} FLOP per launch "
-                                          f"(25|60 FP32 ops x E={e_pairs} evaluated pairs)"}
-            else:
-                primary = {"kernel": dom, "bound": "hbm", "achieved": st["achieved_gbs"], "peak": hbm,
-                           "unit": "GB/s", "frac": st["frac_hbm"], "traffic": traffic.get(dom),
-                           "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6650"}
-        hbm_stages = {k: v for k, v in stages.items() if k not in flops}
-        top_hbm = max(hbm_stages, key=lambda k: hbm_stages[k]["ms"]) if hbm_stages else None
-        secondary = None
-        if top_hbm:
-            st = hbm_stages[top_hbm]
-            secondary = {"kernel": top_hbm, "bound": "hbm", "achieved": st["achieved_gbs"], "peak": hbm,
-                         "unit": "GB/s", "frac": st["frac_hbm"], "traffic": traffic.get(top_hbm),
-                         "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6650"}
-        return {"primary": primary, "hbm": secondary, "stages": stages}
+        if dom is not None:
+            primary = fp32_entry(dom) if "frac_fp32" in stages[dom] else hbm_entry(dom)
+        hbm_stages = [k for k in timed if k not in flops]
+        fp32_stages = [k for k in timed if "frac_fp32" in stages[k]]
+        secondary = hbm_entry(max(hbm_stages, key=lambda k: ms[k])) if hbm_stages else None
+        top_fp32 = fp32_entry(max(fp32_stages, key=lambda k: ms[k])) if fp32_stages else None
+        return {"primary": primary, "hbm": secondary, "fp32": top_fp32, "stages": stages}
 
 
 def measure_fp32_peak(device=None, iters: int = 4096, trials: int = 7) -> float:

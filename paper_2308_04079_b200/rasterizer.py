@@ -522,12 +522,16 @@ def render_forward(splats: DeviceSplats, binning: TileBinning, width: int, heigh
 
 
 def render_backward(d_image: torch.Tensor, output: RenderOutput, splats: DeviceSplats, binning: TileBinning,
-                    width: int, height: int, background, deterministic: bool = False) -> SplatGrads2D:
+                    width: int, height: int, background, deterministic: bool = False,
+                    stage_timer=None) -> SplatGrads2D:
     """K7: back-to-front blend gradient (rasterizer.py:253).
 
     deterministic: no float atomics (per-instance partial rows summed per
     splat in a fixed order): bit-identical results run to run, the
-    reference's deterministic=True (rasterizer.py:34-35)."""
+    reference's deterministic=True (rasterizer.py:34-35).
+    stage_timer (profiling.StageTimer, optional): the tile schedule and the
+    clearing of the rows are timed as stage "blend_bwd_setup" and the blend
+    kernel alone as "blend_bwd" (the roofline's launch duration)."""
     if output.final_transmittance is None or output.last_contributor is None:
         raise ValueError("backward pass needs a training-mode RenderOutput")  # rasterizer.py:265-266
     lib = _lib.load()
@@ -548,6 +552,20 @@ def render_backward(d_image: torch.Tensor, output: RenderOutput, splats: DeviceS
             _bg(background), None, ws.data_ptr(), int(nbytes.value), cap, packed.data_ptr(), _stream()),
             "render_backward")
         return SplatGrads2D(packed, None, splats.rec)
+    if _BWD_SCHEDULE and stage_timer is not None:
+        from .profiling import StageTimer
+        tx, ty = tile_extent(width, height)
+        scratch = torch.empty(2 * tx * ty + 2048, dtype=torch.int32, device=splats.rec.device)
+        with StageTimer.stage(stage_timer, "blend_bwd_setup"):
+            _lib.check(lib.gs_blend_backward_schedule(binning.ranges.data_ptr(), output.last_contributor.data_ptr(),
+                                                      width, height, scratch.data_ptr(), _stream()), "render_backward")
+            packed.zero_()
+        with StageTimer.stage(stage_timer, "blend_bwd"):
+            _lib.check(lib.gs_blend_backward_accumulate(
+                d_image.data_ptr(), ctypes.byref(cs), binning.splat_ids.data_ptr(), binning.ranges.data_ptr(),
+                output.final_transmittance.data_ptr(), output.last_contributor.data_ptr(), width, height,
+                _bg(background), scratch.data_ptr(), packed.data_ptr(), _stream()), "render_backward")
+        return SplatGrads2D(packed, scratch[:tx * ty], splats.rec)
     if _BWD_SCHEDULE:
         # longest-first tile order from the forward's training record (scratch: 2 T + 2048 int32)
         tx, ty = tile_extent(width, height)
