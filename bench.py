@@ -218,10 +218,12 @@ def run_single(args, local_rank: int) -> None:
         with StageTimer.stage(tm, "blend_fwd"):
             # tiles in the previous backward's longest-first order (same view)
             out = R.render_forward(splats, binning, WIDTH, HEIGHT, bg, training=True, tile_order=prev_order[0])
+        # the backward's tile schedule + row clearing on a side stream, beside the loss
+        prep = R.prepare_backward(out, splats, binning, WIDTH, HEIGHT)
         with StageTimer.stage(tm, "loss"):
             loss, d_image = l1_dssim_loss(out.image, gt, LAMBDA_DSSIM)
-        # the blend kernel timed alone ("blend_bwd"); schedule + row clearing as "blend_bwd_setup"
-        g2 = R.render_backward(d_image, out, splats, binning, WIDTH, HEIGHT, bg, stage_timer=tm)
+        # the blend kernel timed alone ("blend_bwd")
+        g2 = R.render_backward(d_image, out, splats, binning, WIDTH, HEIGHT, bg, stage_timer=tm, prep=prep)
         prev_order[0] = g2.tile_order
         if os.environ.get("GS_BENCH_UNFUSED") != "1":
             # backward_project + stats + Adam fused (no gradient round trip)
@@ -452,8 +454,9 @@ def c4_batches(args, rank: int, world: int, dev, steps: int, warmup: int) -> dic
             out, splats, binning = R.render_view_async(cloud, cam, (0.0, 0.0, 0.0), DEGREE, training=True,
                                                        tile_order=orders.get(v))
             k_infos.append(binning.k_info)
+            prep = R.prepare_backward(out, splats, binning, WIDTH, HEIGHT)   # beside the loss
             _, d_image = l1_dssim_loss(out.image, gt, LAMBDA_DSSIM)
-            g2 = R.render_backward(d_image, out, splats, binning, WIDTH, HEIGHT, (0.0, 0.0, 0.0))
+            g2 = R.render_backward(d_image, out, splats, binning, WIDTH, HEIGHT, (0.0, 0.0, 0.0), prep=prep)
             orders[v] = g2.tile_order
             if world > 1:   # range by range; the last view's per-range reductions overlap the later ranges
                 opt.accumulate(cloud, cam, splats, g2, DEGREE, stats=stats, reduce=v == len(cams) - 1)

@@ -158,8 +158,9 @@ def train_step_views(cloud, cameras, targets, adam, config, iteration: int, buck
                 k_infos.append(binning.k_info)
             else:
                 out, splats, binning = R.render_view(cloud, cam, background, active_sh_degree, training=True)
+            prep = R.prepare_backward(out, splats, binning, cam.width, cam.height)   # beside the loss
             loss, d_image = l1_dssim_loss(out.image, gt, config.lambda_dssim)
-            g2 = R.render_backward(d_image, out, splats, binning, cam.width, cam.height, background)
+            g2 = R.render_backward(d_image, out, splats, binning, cam.width, cam.height, background, prep=prep)
             if g2.tile_order is not None:
                 orders[key] = g2.tile_order
             R.backward_project(cloud, cam, splats, g2, active_sh_degree, stats=st, out=b.grads, accumulate=True)

@@ -257,7 +257,10 @@ class SplatGrads2D:
         k = self._need_rec("d_mean2d")[:, 4:8].double()
         s1, s2 = self.packed[:, 0].double(), self.packed[:, 1].double()
         c = 2.0 / 1.4426950408889634
-        return torch.stack([c * (k[:, 0] * s1 + k[:, 2] * s2), c * (k[:, 1] * s1 + k[:, 3] * s2)], dim=1)
+        out = torch.stack([c * (k[:, 0] * s1 + k[:, 2] * s2), c * (k[:, 1] * s1 + k[:, 3] * s2)], dim=1)
+        # culled rows: S = 0 and the record is undefined (never written)
+        ok = (s1 != 0) | (s2 != 0)
+        return torch.where(ok[:, None], out, torch.zeros_like(out))
 
     @property
     def d_alpha(self) -> torch.Tensor:
@@ -521,9 +524,55 @@ def render_forward(splats: DeviceSplats, binning: TileBinning, width: int, heigh
     return RenderOutput(image, t_final, last)
 
 
+@dataclass
+class BackwardPrep:
+    """The backward's longest-first tile schedule and its cleared gradient rows,
+    enqueued on a side stream by prepare_backward (so they overlap the loss)."""
+
+    scratch: torch.Tensor   # int32 (2 T + 2048,): the order in [0, T)
+    packed: torch.Tensor    # (N,12) float32, zeroed
+    done: torch.cuda.Event
+    tiles: int
+
+
+_side_streams: dict = {}
+
+
+def prepare_backward(output: RenderOutput, splats: DeviceSplats, binning: TileBinning, width: int,
+                     height: int) -> BackwardPrep:
+    """Enqueue, on a side stream behind the current stream's work so far (the
+    forward), the tile schedule of the coming render_backward and the
+    clearing of its gradient rows: they depend only on the forward's
+    training record, so they run while the loss is computed.  Pass the
+    result to render_backward(prep=...)."""
+    if output.last_contributor is None:
+        raise ValueError("backward pass needs a training-mode RenderOutput")
+    device = splats.rec.device
+    tx, ty = tile_extent(width, height)
+    scratch = torch.empty(2 * tx * ty + 2048, dtype=torch.int32, device=device)
+    packed = torch.empty((len(splats), _lib.GRAD2D_FLOATS), dtype=torch.float32, device=device)
+    main = torch.cuda.current_stream(device)
+    side = _side_streams.get(str(device))
+    if side is None:
+        side = _side_streams[str(device)] = torch.cuda.Stream(device)
+    side.wait_stream(main)
+    with torch.cuda.stream(side):
+        _lib.check(_lib.load().gs_blend_backward_schedule(binning.ranges.data_ptr(),
+                                                          output.last_contributor.data_ptr(), width, height,
+                                                          scratch.data_ptr(), side.cuda_stream), "render_backward")
+        packed.zero_()
+    # the buffers may be dropped unused (a discarded lookahead): keep them out of
+    # the allocator's reach until the side stream is done with them
+    scratch.record_stream(side)
+    packed.record_stream(side)
+    done = torch.cuda.Event()
+    done.record(side)
+    return BackwardPrep(scratch, packed, done, tx * ty)
+
+
 def render_backward(d_image: torch.Tensor, output: RenderOutput, splats: DeviceSplats, binning: TileBinning,
                     width: int, height: int, background, deterministic: bool = False,
-                    stage_timer=None) -> SplatGrads2D:
+                    stage_timer=None, prep: BackwardPrep | None = None) -> SplatGrads2D:
     """K7: back-to-front blend gradient (rasterizer.py:253).
 
     deterministic: no float atomics (per-instance partial rows summed per
@@ -531,15 +580,26 @@ def render_backward(d_image: torch.Tensor, output: RenderOutput, splats: DeviceS
     reference's deterministic=True (rasterizer.py:34-35).
     stage_timer (profiling.StageTimer, optional): the tile schedule and the
     clearing of the rows are timed as stage "blend_bwd_setup" and the blend
-    kernel alone as "blend_bwd" (the roofline's launch duration)."""
+    kernel alone as "blend_bwd" (the roofline's launch duration).
+    prep: the schedule and cleared rows from prepare_backward (then only the
+    blend kernel is launched here, after waiting for them)."""
     if output.final_transmittance is None or output.last_contributor is None:
         raise ValueError("backward pass needs a training-mode RenderOutput")  # rasterizer.py:265-266
     lib = _lib.load()
     d_image = d_image.to(dtype=torch.float32).contiguous()
     if tuple(d_image.shape) != (height, width, 3):
         raise ValueError(f"d_image shape {tuple(d_image.shape)} != {(height, width, 3)}")
-    packed = torch.empty((len(splats), _lib.GRAD2D_FLOATS), dtype=torch.float32, device=splats.rec.device)
     cs = splats.c_struct()
+    if prep is not None and not deterministic:
+        from .profiling import StageTimer
+        torch.cuda.current_stream(splats.rec.device).wait_event(prep.done)
+        with StageTimer.stage(stage_timer, "blend_bwd"):
+            _lib.check(lib.gs_blend_backward_accumulate(
+                d_image.data_ptr(), ctypes.byref(cs), binning.splat_ids.data_ptr(), binning.ranges.data_ptr(),
+                output.final_transmittance.data_ptr(), output.last_contributor.data_ptr(), width, height,
+                _bg(background), prep.scratch.data_ptr(), prep.packed.data_ptr(), _stream()), "render_backward")
+        return SplatGrads2D(prep.packed, prep.scratch[:prep.tiles], splats.rec)
+    packed = torch.empty((len(splats), _lib.GRAD2D_FLOATS), dtype=torch.float32, device=splats.rec.device)
     if deterministic:
         cap = int(binning.splat_ids.shape[0])
         nbytes = ctypes.c_size_t(0)

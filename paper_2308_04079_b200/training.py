@@ -221,6 +221,7 @@ class _Forward:
     binning: object = None
     loss: torch.Tensor = None
     d_image: torch.Tensor = None
+    prep: object = None   # rasterizer.BackwardPrep (side-stream tile schedule + cleared rows)
 
 
 def _sample_view(state: TrainState, views: Sequence[TrainView], config: TrainConfig, it: int,
@@ -258,6 +259,9 @@ def _enqueue_forward(state: TrainState, fw: _Forward, config: TrainConfig) -> _F
     order = orders.get((fw.view_idx, fw.camera.width, fw.camera.height)) if orders else None
     fw.out, fw.splats, fw.binning = R.render_view_async(state.cloud, fw.camera, config.background, fw.degree,
                                                         training=True, tile_order=order)
+    # the backward's tile schedule and row clearing run on a side stream, beside the loss
+    fw.prep = None if config.deterministic else R.prepare_backward(fw.out, fw.splats, fw.binning, fw.camera.width,
+                                                                  fw.camera.height)
     fw.loss, fw.d_image = l1_dssim_loss(fw.out.image, fw.gt, config.lambda_dssim)
     if fw.consumed is not None:
         fw.consumed.record()
@@ -312,7 +316,7 @@ def train_step(state: TrainState, views: Sequence[TrainView], config: TrainConfi
         done = torch.cuda.Event()
         done.record(torch.cuda.current_stream(device))
         g2 = R.render_backward(fw.d_image, fw.out, fw.splats, fw.binning, fw.camera.width, fw.camera.height,
-                               config.background, deterministic=config.deterministic)
+                               config.background, deterministic=config.deterministic, prep=fw.prep)
         if g2.tile_order is not None:
             if not hasattr(state, "_tile_orders"):
                 state._tile_orders = {}
