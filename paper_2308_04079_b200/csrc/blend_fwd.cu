@@ -173,6 +173,7 @@ struct FixShared {
   double total;
   double col[3][kFixThreads / 32];
   double tail_a[kFixThreads];
+  float4 tail_c[kFixThreads];   // the candidates' colours (the serial walk reads them)
   int stop;
   int item;
 };
@@ -284,6 +285,7 @@ __device__ void exact_pixel(const float4* __restrict__ rec, const uint32_t* __re
     const int i = base + int(threadIdx.x);
     float4 col = make_float4(0.f, 0.f, 0.f, 0.f);
     sh.tail_a[threadIdx.x] = i < range.y ? exact_alpha(rec, ids[i], fx, fy, col) : 0.0;
+    sh.tail_c[threadIdx.x] = col;
     consumer_sync();
     if (threadIdx.x == 0) {
       for (int u = 0; u < kFixThreads && base + u < range.y; ++u) {
@@ -294,8 +296,7 @@ __device__ void exact_pixel(const float4* __restrict__ rec, const uint32_t* __re
           sh.stop = 1;
           break;
         }
-        float4 cc;
-        exact_alpha(rec, ids[base + u], fx, fy, cc);
+        const float4 cc = sh.tail_c[u];
         c[0] += T * a * cc.x;
         c[1] += T * a * cc.y;
         c[2] += T * a * cc.z;
