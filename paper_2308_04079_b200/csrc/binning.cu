@@ -422,14 +422,19 @@ __device__ __forceinline__ SuperRect super_rect(int4 rc, const Grid& g) {
 // The rectangles are gathered into depth order here (drect[r] =
 // rect[order[r]]; the Gaussians without instances, which the sort put last,
 // get the empty rectangle), with the gathers of a thread issued together.
+// Counts are kept per warp range of the chunk (kChunk / kWarps Gaussians, the
+// ranges bucket_scatter's warps own): M[s * chunks + chunk] = their sum and
+// Mw[(chunk * kWarps + w) * S + s] (u16) the warp range's own count, from
+// which the scatter's warps take their cursor bases without recounting.
 __global__ void __launch_bounds__(kThreads) bucket_count_kernel(const int4* __restrict__ rect,
                                                                const uint32_t* __restrict__ order,
                                                                const uint32_t* __restrict__ hist, int4* __restrict__ drect,
                                                                int64_t n, Grid g, uint32_t* __restrict__ M,
-                                                               int64_t chunks, const int64_t* __restrict__ kinfo) {
-  extern __shared__ uint32_t s_h[];
+                                                               uint16_t* __restrict__ Mw, int64_t chunks,
+                                                               const int64_t* __restrict__ kinfo) {
+  extern __shared__ uint32_t s_h[];   // [kWarps][S]
   if (kinfo[1] != 0) return;
-  for (int s = threadIdx.x; s < g.S; s += kThreads) s_h[s] = 0u;
+  for (int s = threadIdx.x; s < kWarps * g.S; s += kThreads) s_h[s] = 0u;
   // Gaussians with instances: every key except the culled 0xFFFFFFFF (depth > 0, so no other key has top byte 0xFF)
   const int64_t visible = n - int64_t(hist[3 * kRadix + 255]);
   __syncthreads();
@@ -447,11 +452,21 @@ __global__ void __launch_bounds__(kThreads) bucket_count_kernel(const int4* __re
     if (r >= n) break;
     drect[r] = rc[u];
     const SuperRect q = super_rect(rc[u], g);
+    uint32_t* h = s_h + ((threadIdx.x + u * kThreads) / (kChunk / kWarps)) * g.S;
     for (int y = q.y0; y <= q.y1; ++y)
-      for (int x = q.x0; x <= q.x1; ++x) atomicAdd(&s_h[y * g.sx + x], 1u);
+      for (int x = q.x0; x <= q.x1; ++x) atomicAdd(&h[y * g.sx + x], 1u);
   }
   __syncthreads();
-  for (int s = threadIdx.x; s < g.S; s += kThreads) M[int64_t(s) * chunks + blockIdx.x] = s_h[s];
+  for (int s = threadIdx.x; s < g.S; s += kThreads) {
+    uint32_t sum = 0;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) {
+      const uint32_t c = s_h[w * g.S + s];
+      Mw[(int64_t(blockIdx.x) * kWarps + w) * g.S + s] = uint16_t(c);
+      sum += c;
+    }
+    M[int64_t(s) * chunks + blockIdx.x] = sum;
+  }
 }
 
 // In-place exclusive scan of a u32 array (single pass, decoupled look-back
@@ -576,7 +591,8 @@ __global__ void __launch_bounds__(1024) window_setup_kernel(const uint32_t* __re
 template <bool kOrBins>
 __global__ void __launch_bounds__(kThreads) bucket_scatter_kernel(const int4* __restrict__ drect,
                                                                  const uint32_t* __restrict__ order, int64_t n, Grid g,
-                                                                 const uint32_t* __restrict__ M, int64_t chunks,
+                                                                 const uint32_t* __restrict__ M,
+                                                                 const uint16_t* __restrict__ Mw, int64_t chunks,
                                                                  uint2* __restrict__ entries, int64_t capacity,
                                                                  const int64_t* __restrict__ kinfo) {
   extern __shared__ uint32_t s_cur[];   // [kWarps][S] cursors, then [kWarps][S] bytes of bucket stamps
@@ -591,22 +607,14 @@ __global__ void __launch_bounds__(kThreads) bucket_scatter_kernel(const int4* __
   uint32_t* bins = s_cur + kWarps * S + warp * S;   // kOrBins: [kWarps][S] lane bitmasks
   if (kOrBins)
     for (int i = tid; i < kWarps * S; i += kThreads) s_cur[kWarps * S + i] = 0u;
-  for (int i = 0; i < kChunk / kWarps; i += 32) {
-    const int64_t r = rw + i + lane;
-    if (r < n) {
-      const SuperRect q = super_rect(drect[r], g);
-      for (int y = q.y0; y <= q.y1; ++y)
-        for (int x = q.x0; x <= q.x1; ++x) atomicAdd(&cur[y * g.sx + x], 1u);
-    }
-  }
-  __syncthreads();
+  // each warp range's cursors start at the chunk's scanned count plus the
+  // counts of the ranges before it (bucket_count's Mw)
   for (int s = tid; s < S; s += kThreads) {
     uint32_t run = M[int64_t(s) * chunks + blockIdx.x];
 #pragma unroll
     for (int w = 0; w < kWarps; ++w) {
-      const uint32_t c = s_cur[w * S + s];
       s_cur[w * S + s] = run;
-      run += c;
+      run += Mw[(int64_t(blockIdx.x) * kWarps + w) * S + s];
     }
   }
   __syncthreads();
@@ -1043,7 +1051,7 @@ struct Layout {
   int64_t n, cap, tiles, blocks, chunks, mlen, wmax;
   size_t zero, zero_bytes;                              // memset region
   size_t hist, tickets, mtotal, sort_status, scan_status;  // inside it
-  size_t digit_base, keys_a, keys_b, ids_a, ids_b, order, drect, m, bstart, wstart, wmap, entries, cnt, tile_total,
+  size_t digit_base, keys_a, keys_b, ids_a, ids_b, order, drect, m, mw, bstart, wstart, wmap, entries, cnt, tile_total,
       kinfo, bytes;
 };
 
@@ -1082,6 +1090,7 @@ int layout(int64_t n, int width, int height, int64_t cap, Layout* L) {
   L->order = take(4 * un);
   L->drect = take(16 * un);
   L->m = take(4 * size_t(L->mlen > 0 ? L->mlen : 1) + 16);
+  L->mw = take(2 * size_t(L->mlen > 0 ? L->mlen : 1) * kWarps + 16);   // per warp range, u16
   L->bstart = take(4 * size_t(L->g.S + 1));
   L->wstart = take(4 * size_t(L->g.S + 1));
   L->wmap = take(4 * size_t(L->wmax));
@@ -1193,10 +1202,11 @@ int bin_enqueue(const gs_splats_t* splats, int32_t width, int32_t height, void* 
   if ((st = check_launch()) != GS_OK) return st;
   // 2. super-tile buckets
   uint32_t* M = at<uint32_t>(ws, L.m);
-  const size_t smem_count = sizeof(uint32_t) * size_t(g.S);
+  const size_t smem_count = sizeof(uint32_t) * kWarps * size_t(g.S);
+  uint16_t* Mw = at<uint16_t>(ws, L.mw);
   if ((e = smem_opt_in(reinterpret_cast<const void*>(bucket_count_kernel), smem_count)) != cudaSuccess)
     return record_cuda_error(e);
-  bucket_count_kernel<<<unsigned(L.chunks), kThreads, smem_count, s>>>(rect, order, hist, drect, n, g, M, L.chunks,
+  bucket_count_kernel<<<unsigned(L.chunks), kThreads, smem_count, s>>>(rect, order, hist, drect, n, g, M, Mw, L.chunks,
                                                                        kinfo);
   if ((st = check_launch()) != GS_OK) return st;
   uint32_t* mtotal = at<uint32_t>(ws, L.mtotal);
@@ -1213,10 +1223,10 @@ int bin_enqueue(const gs_splats_t* splats, int32_t width, int32_t height, void* 
                                    : reinterpret_cast<const void*>(bucket_scatter_kernel<false>);
   if ((e = smem_opt_in(scatter_fn, smem_scatter)) != cudaSuccess) return record_cuda_error(e);
   if (or_bins)
-    bucket_scatter_kernel<true><<<unsigned(L.chunks), kThreads, smem_scatter, s>>>(drect, order, n, g, M, L.chunks,
+    bucket_scatter_kernel<true><<<unsigned(L.chunks), kThreads, smem_scatter, s>>>(drect, order, n, g, M, Mw, L.chunks,
                                                                       at<uint2>(ws, L.entries), cap, kinfo);
   else
-    bucket_scatter_kernel<false><<<unsigned(L.chunks), kThreads, smem_scatter, s>>>(drect, order, n, g, M, L.chunks,
+    bucket_scatter_kernel<false><<<unsigned(L.chunks), kThreads, smem_scatter, s>>>(drect, order, n, g, M, Mw, L.chunks,
                                                                        at<uint2>(ws, L.entries), cap, kinfo);
   if ((st = check_launch()) != GS_OK) return st;
   // 3-5. windows, ranges, instance lists
