@@ -948,17 +948,8 @@ constexpr int kRing = 64, kRingStride = kRing + 1;
 constexpr int kWriteWarps = kWarps;
 constexpr size_t kStagedSmem = sizeof(uint32_t) * kWarps * 32 * kRingStride;
 
-__device__ __forceinline__ void flush_run(const uint32_t* __restrict__ ring, int owner, uint32_t from, uint32_t count,
-                                          uint32_t dst, int64_t tile, const float* __restrict__ depth,
-                                          uint32_t* __restrict__ ids, unsigned long long* __restrict__ keys,
-                                          int lane) {
-  if (uint32_t(lane) < count) {
-    const uint32_t id = ring[owner * kRingStride + ((from + lane) & (kRing - 1))];
-    ids[dst + lane] = id;
-    if (keys) keys[dst + lane] = (static_cast<unsigned long long>(tile) << 32) | __float_as_uint(depth[id]);
-  }
-}
 
+template <bool kKeys>
 __global__ void __launch_bounds__(kThreads) instance_write_staged_kernel(
     const uint2* __restrict__ entries, const uint32_t* __restrict__ wmap, const uint32_t* __restrict__ bstart,
     const uint32_t* __restrict__ wstart, Grid g, const uint32_t* __restrict__ cnt, const int2* __restrict__ ranges,
@@ -971,7 +962,19 @@ __global__ void __launch_bounds__(kThreads) instance_write_staged_kernel(
   uint32_t* ring = s_ring + (threadIdx.x >> 5) * 32 * kRingStride;
   uint32_t* mine = ring + lane * kRingStride;
   uint32_t* eid = s_eid[threadIdx.x >> 5];
-  const uint32_t mine_s = smem_u32(mine), eid_s = smem_u32(eid);
+  const uint32_t mine_s = smem_u32(mine), eid_s = smem_u32(eid), ring_s = smem_u32(ring);
+  // flush of lane f's ring: 32 (or count) ids from slot `from` to ids[dst...]
+  auto flush = [&](int f, uint32_t from, uint32_t dst, uint32_t count, int64_t tile_f) {
+    if (uint32_t(lane) < count) {
+      uint32_t id;
+      asm volatile("ld.shared.u32 %0, [%1];"
+                   : "=r"(id)
+                   : "r"(ring_s + 4u * (uint32_t(f) * kRingStride + ((from + uint32_t(lane)) & (kRing - 1))))
+                   : "memory");
+      ids[dst + lane] = id;
+      if (kKeys) keys[dst + lane] = (static_cast<unsigned long long>(tile_f) << 32) | __float_as_uint(depth[id]);
+    }
+  };
   const uint32_t nwin = wstart[g.S];
   const uint32_t stride = gridDim.x * kWarps;
   for (uint32_t w = blockIdx.x * kWarps + (threadIdx.x >> 5); w < nwin; w += stride) {
@@ -1005,8 +1008,8 @@ __global__ void __launch_bounds__(kThreads) instance_write_staged_kernel(
       while (full) {
         const int f = __ffs(full) - 1;
         full &= full - 1;
-        flush_run(ring, f, __shfl_sync(0xffffffffu, fp, f), 32u, __shfl_sync(0xffffffffu, cur, f),
-                  __shfl_sync(0xffffffffu, tile, f), depth, ids, keys, lane);
+        flush(f, __shfl_sync(0xffffffffu, fp, f), __shfl_sync(0xffffffffu, cur, f), 32u,
+              kKeys ? __shfl_sync(0xffffffffu, tile, f) : int64_t(0));
         if (lane == f) {
           fp += 32u;
           cur += 32u;
@@ -1018,8 +1021,8 @@ __global__ void __launch_bounds__(kThreads) instance_write_staged_kernel(
     while (rest) {
       const int f = __ffs(rest) - 1;
       rest &= rest - 1;
-      flush_run(ring, f, __shfl_sync(0xffffffffu, fp, f), __shfl_sync(0xffffffffu, wp - fp, f),
-                __shfl_sync(0xffffffffu, cur, f), __shfl_sync(0xffffffffu, tile, f), depth, ids, keys, lane);
+      flush(f, __shfl_sync(0xffffffffu, fp, f), __shfl_sync(0xffffffffu, cur, f),
+            __shfl_sync(0xffffffffu, wp - fp, f), kKeys ? __shfl_sync(0xffffffffu, tile, f) : int64_t(0));
     }
     __syncwarp();
   }
@@ -1128,9 +1131,16 @@ int walk(const Layout& L, char* ws, const float* depth, uint32_t* ids, int2* ran
   tile_ranges_kernel<<<1, 1024, 0, s>>>(at<uint32_t>(ws, L.tile_total), L.tiles, ranges, kinfo);
   if ((st = check_launch()) != GS_OK) return st;
   if (Q == 1) {
-    cudaError_t e = smem_opt_in(reinterpret_cast<const void*>(instance_write_staged_kernel), kStagedSmem);
+    const void* fn = keys ? reinterpret_cast<const void*>(instance_write_staged_kernel<true>)
+                          : reinterpret_cast<const void*>(instance_write_staged_kernel<false>);
+    cudaError_t e = smem_opt_in(fn, kStagedSmem);
     if (e != cudaSuccess) return record_cuda_error(e);
-    instance_write_staged_kernel<<<148 * 3, kThreads, kStagedSmem, s>>>(
+    if (keys)
+      instance_write_staged_kernel<true><<<148 * 3, kThreads, kStagedSmem, s>>>(
+          at<uint2>(ws, L.entries), at<uint32_t>(ws, L.wmap), at<uint32_t>(ws, L.bstart), at<uint32_t>(ws, L.wstart),
+          g, at<uint32_t>(ws, L.cnt), ranges, depth, ids, keys, kinfo);
+    else
+      instance_write_staged_kernel<false><<<148 * 3, kThreads, kStagedSmem, s>>>(
         at<uint2>(ws, L.entries), at<uint32_t>(ws, L.wmap), at<uint32_t>(ws, L.bstart), at<uint32_t>(ws, L.wstart),
         g, at<uint32_t>(ws, L.cnt), ranges, depth, ids, keys, kinfo);
   } else {
