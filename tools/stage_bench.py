@@ -26,14 +26,17 @@ def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--n", type=int, default=3_000_000)
     ap.add_argument("--reps", type=int, default=20)
+    ap.add_argument("--width", type=int, default=1920)
+    ap.add_argument("--height", type=int, default=1080)
     ap.add_argument("--order", action="store_true", help="also time the backward with heavy tiles first")
     args = ap.parse_args()
     lib = _lib.load()
-    cloud_np, cam = synthetic.frustum_scene(args.n, 1920, 1080, seed=0)
+    W, H = args.width, args.height
+    cloud_np, cam = synthetic.frustum_scene(args.n, W, H, seed=0)
     cloud = GaussianCloud.from_numpy(**cloud_np)
     bg = (0.0, 0.0, 0.0)
     out, splats, binning = R.render_view(cloud, cam, bg, 3, training=True)
-    d = torch.from_numpy(np.random.default_rng(1).uniform(-1, 1, (1080, 1920, 3)).astype(np.float32) / 6e6).cuda()
+    d = torch.from_numpy(np.random.default_rng(1).uniform(-1, 1, (H, W, 3)).astype(np.float32) / 6e6).cuda()
 
     from paper_2308_04079_b200.loss import l1_dssim_loss
     tgt = torch.rand_like(out.image)
@@ -53,7 +56,7 @@ def main() -> None:
     from paper_2308_04079_b200.optimizer import DeviceAdam, TrainConfig
     adam = DeviceAdam(cloud)
     stats = R.DensifyStats.zeros(len(cloud), "cuda")
-    g2 = R.render_backward(d, out, splats, binning, 1920, 1080, bg)
+    g2 = R.render_backward(d, out, splats, binning, W, H, bg)
     it = [0]
 
     def bwd_adam():
@@ -61,11 +64,12 @@ def main() -> None:
         adam.backward_step(cloud, cam, splats, g2, 3, it[0], TrainConfig(), stats=stats)
 
     res = {
-        "lib": str(_lib.LIB_PATH),
+        "lib": str(_lib.LIB_PATH), "n": args.n, "width": W, "height": H,
+        "instances": binning.num_instances,
         "bwd_adam_ms": timeit(bwd_adam),
-        "blend_fwd_ms": timeit(lambda: R.render_forward(splats, binning, 1920, 1080, bg, training=True)),
-        "blend_bwd_ms": timeit(lambda: R.render_backward(d, out, splats, binning, 1920, 1080, bg)),
-        "bin_async_ms": timeit(lambda: R.bin_and_sort_async(splats, 1920, 1080)),
+        "blend_fwd_ms": timeit(lambda: R.render_forward(splats, binning, W, H, bg, training=True)),
+        "blend_bwd_ms": timeit(lambda: R.render_backward(d, out, splats, binning, W, H, bg)),
+        "bin_async_ms": timeit(lambda: R.bin_and_sort_async(splats, W, H)),
         "preprocess_fwd_ms": timeit(lambda: R._project_tensors(cloud.c_params(), len(cloud), "cuda", cam, 3)),
         "loss_ms": timeit(lambda: l1_dssim_loss(out.image, tgt, 0.2)),
     }
@@ -105,7 +109,7 @@ def main() -> None:
             def run():
                 lib.gs_blend_backward_ordered(d.data_ptr(), ctypes.byref(cs), binning.splat_ids.data_ptr(),
                                               binning.ranges.data_ptr(), out.final_transmittance.data_ptr(),
-                                              out.last_contributor.data_ptr(), 1920, 1080, bgc, order.data_ptr(),
+                                              out.last_contributor.data_ptr(), W, H, bgc, order.data_ptr(),
                                               g2o.data_ptr(), torch.cuda.current_stream().cuda_stream)
             res[f"blend_bwd_order_{name}_ms"] = timeit(run)
             res[f"order_{name}_checksum"] = float(g2o.abs().sum().item())
@@ -115,12 +119,12 @@ def main() -> None:
             fx = torch.empty(2 + 1920 * 1080, dtype=torch.int32, device="cuda")
             def runf():
                 lib.gs_blend_forward_ordered(ctypes.byref(cs), binning.splat_ids.data_ptr(), binning.ranges.data_ptr(),
-                                             1920, 1080, bgc, 1, order.data_ptr(), None, img.data_ptr(),
+                                             W, H, bgc, 1, order.data_ptr(), None, img.data_ptr(),
                                              tf.data_ptr(), ls.data_ptr(), fx.data_ptr(),
                                              torch.cuda.current_stream().cuda_stream)
             res[f"blend_fwd_order_{name}_ms"] = timeit(runf)
             res[f"fwd_order_{name}_same"] = bool(torch.equal(img, out.image) and torch.equal(ls, out.last_contributor))
-    g_ref = R.render_backward(d, out, splats, binning, 1920, 1080, bg).packed
+    g_ref = R.render_backward(d, out, splats, binning, W, H, bg).packed
     res["bwd_checksum"] = float(g_ref.double().abs().sum())
     print(json.dumps(res))
 

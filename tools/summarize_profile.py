@@ -73,7 +73,7 @@ def full(rep: Path, tag: str, desc: str) -> dict:
     ki = h.index("Kernel Name")
     stall = [w for w in h if w.startswith("smsp__average_warps_issue_stalled") and w.endswith("per_issue_active.ratio")]
     out = [f"# {tag} — `ncu --set full` per-launch summary\n", f"{desc}\n",
-           "| kernel | time ms | DRAM rd+wr MB | DRAM % | issue % | warps % | regs | FMA % | warp instr | top stalls |",
+           f"| kernel | time {u[h.index('gpu__time_duration.sum')]} | DRAM rd+wr MB | DRAM % | issue % | warps % | regs | FMA % | warp instr | top stalls |",
            "|---|---|---|---|---|---|---|---|---|---|"]
     traffic = defaultdict(list)
     bin_bytes, bin_frames = 0.0, 0
