@@ -205,12 +205,21 @@ def run_single(args, local_rank: int) -> None:
     binnings = []
     last_step = {}
 
+    # GS_BENCH_FUSED_PROJECT=1: the fused backward + Adam also projects the
+    # updated parameters for the next step (gs_preprocess_backward_adam_project,
+    # what train_step's lookahead does); default: K1 timed as its own stage
+    fused_project = [os.environ.get("GS_BENCH_FUSED_PROJECT") == "1"]
+    pending = [None]
+
     def train_step(gt: torch.Tensor, timed: bool) -> torch.Tensor:
         iteration[0] += 1
         tm = timer if timed else None
         params = cloud.c_params()
-        with StageTimer.stage(tm, "preprocess_fwd"):
-            splats = R._project_tensors(params, n, dev, cam, DEGREE)
+        if pending[0] is not None:
+            splats, pending[0] = pending[0], None
+        else:
+            with StageTimer.stage(tm, "preprocess_fwd"):
+                splats = R._project_tensors(params, n, dev, cam, DEGREE)
         with StageTimer.stage(tm, "bin_and_sort"):
             # sync-free binning: K stays on the device, checked after the loop
             binning = R.bin_and_sort_async(splats, WIDTH, HEIGHT)
@@ -225,7 +234,11 @@ def run_single(args, local_rank: int) -> None:
         # the blend kernel timed alone ("blend_bwd")
         g2 = R.render_backward(d_image, out, splats, binning, WIDTH, HEIGHT, bg, stage_timer=tm, prep=prep)
         prev_order[0] = g2.tile_order
-        if os.environ.get("GS_BENCH_UNFUSED") != "1":
+        if fused_project[0]:
+            with StageTimer.stage(tm, "preprocess_bwd_adam_project"):
+                pending[0] = adam.backward_step(cloud, cam, splats, g2, DEGREE, iteration[0], config, stats=stats,
+                                                project_next=(cam, DEGREE))
+        elif os.environ.get("GS_BENCH_UNFUSED") != "1":
             # backward_project + stats + Adam fused (no gradient round trip)
             with StageTimer.stage(tm, "preprocess_bwd_adam"):
                 adam.backward_step(cloud, cam, splats, g2, DEGREE, iteration[0], config, stats=stats)
@@ -262,6 +275,21 @@ def run_single(args, local_rank: int) -> None:
         entries = bucket_entries(last_step["splats"], WIDTH, HEIGHT)
     k_last = timer.last_k
     last_step.clear()
+    # the same device loop with each step's backward + Adam launch also
+    # projecting the updated parameters for the next step (train_step's
+    # lookahead path; reported beside `value`, which times K1 as its own stage)
+    fused_project[0] = not fused_project[0]
+    for _ in range(3):
+        train_step(target, False)
+    binnings.clear()
+    alt_ms = _time_loop(lambda i: train_step(target, False), args.steps, 1, dev)
+    check_binned(binnings)
+    fused_project[0] = not fused_project[0]
+    pending[0] = None
+    alt_key = "unfused_project" if fused_project[0] else "fused_project"
+    alt = {"value": round(args.steps * 1e3 / alt_ms, 3), "ms_per_step": round(alt_ms / args.steps, 4),
+           "path": "next step's K1 inside the fused backward + Adam launch (gs_preprocess_backward_adam_project)"
+                   if alt_key == "fused_project" else "K1 as its own launch (gs_preprocess_forward)"}
 
     if args.profile:
         # profiling mode (ncu): warm-up + timed steps only, one summary line
@@ -377,12 +405,14 @@ def run_single(args, local_rank: int) -> None:
                         "pinned host memory every step, [loss, L1, SSIM, MSE, K, flags, K, skip] written D2H into "
                         "mapped pinned memory by the step-guard kernel every step; lookahead: the next "
                         "iteration's forward is enqueued before the host waits",
-                "last_loss": round(e2e_loss, 6)},
+                "last_loss": round(e2e_loss, 6),
+                "next_view_projection": "fused into the backward + Adam launch (lookahead steps)"},
         "e2e_autograd": {"value": round(args.steps / (ag_ms / 1e3), 3), "unit": UNIT,
                          "h2d_bytes_per_step": WIDTH * HEIGHT * 3 * 4, "d2h_bytes_per_step": 4 + 24,
                          "path": "rasterize_gaussians (GaussianRasterizer.apply: gs_forward / gs_backward) on leaf "
                                  "tensors + device L1/D-SSIM + autograd backward + Adam on the leaf gradients; "
                                  "target H2D and loss.item() every step"},
+        alt_key: alt,
         "c4_1gpu": c4,
         "gpu_launches": timer.launches_per_step() * args.steps,
         "roofline": roof["primary"], "roofline_hbm": roof["hbm"], "roofline_fp32": roof["fp32"],

@@ -342,7 +342,24 @@ int gs_preprocess_backward_adam_guarded(const gs_params_t* params, const gs_came
                                         const gs_stats_t* stats, const gs_grads_t* grads_out,
                                         const int32_t* skip, void* stream);
 
-/* *skip = (k_info[1] != 0 (binning overflow / limit flags) || loss[0] not finite).
+/* gs_preprocess_backward_adam_guarded that ALSO projects the updated
+ * parameters for the next iteration's view (gs_preprocess_forward with
+ * next_camera / next_active_sh_degree into next_splats, bit-identical to
+ * calling it after this launch), from the values the update leaves in
+ * registers and shared memory: the next forward skips K1 and its 236-B
+ * parameter read per Gaussian (optimizer.py:222-260 steps i and i+1 run
+ * back to back).  When *skip != 0 nothing is updated and the next view is
+ * projected from the unchanged parameters.  next_splats must not alias
+ * splats (this step's records are still read). */
+int gs_preprocess_backward_adam_project(const gs_params_t* params, const gs_camera_t* camera,
+                                        int32_t active_sh_degree, const gs_splats_t* splats,
+                                        const float* grads2d, const gs_adam_group_t* groups, double beta1,
+                                        double beta2, double eps, double bias1, double bias2,
+                                        const gs_stats_t* stats, const gs_grads_t* grads_out,
+                                        const int32_t* skip, const gs_camera_t* next_camera,
+                                        int32_t next_active_sh_degree, gs_splats_t* next_splats, void* stream);
+
+/* *skip =(k_info[1] != 0 (binning overflow / limit flags) || loss[0] not finite).
  * report (nullable; 8 doubles, device memory or mapped pinned host memory):
  * [loss[0..3], k_info[0..2], skip] -- the step's one host read, without a
  * separate copy. */

@@ -106,6 +106,11 @@ SIGNATURES = [
                                                       POINTER(GsSplats), c_void_p, POINTER(GsAdamGroup), c_double,
                                                       c_double, c_double, c_double, c_double, POINTER(GsStats),
                                                       POINTER(GsGrads), c_void_p, c_void_p]),
+    ("gs_preprocess_backward_adam_project", c_int32, [POINTER(GsParams), POINTER(GsCamera), c_int32,
+                                                      POINTER(GsSplats), c_void_p, POINTER(GsAdamGroup), c_double,
+                                                      c_double, c_double, c_double, c_double, POINTER(GsStats),
+                                                      POINTER(GsGrads), c_void_p, POINTER(GsCamera), c_int32,
+                                                      POINTER(GsSplats), c_void_p]),
     ("gs_step_guard", c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     ("gs_blend_backward_ordered", c_int32, [c_void_p, POINTER(GsSplats), c_void_p, c_void_p, c_void_p, c_void_p,
                                             c_int32, c_int32, POINTER(c_float), c_void_p, c_void_p, c_void_p]),

@@ -63,6 +63,7 @@ struct DevCamera {
   double center[3];   // -R^T t (core.py:143-146)
   double fx, fy, cx, cy;
   double near_plane;
+  double inv_half_w, inv_half_h;   // 1 / (0.5 width), 1 / (0.5 height): the guard-band test's fast path
   int width, height;
   int tiles_x, tiles_y;
 };
@@ -76,6 +77,8 @@ __host__ inline DevCamera make_dev_camera(const gs_camera_t& c) {
                     c.rotation[2 * 3 + i] * c.translation[2]);
   d.fx = c.fx; d.fy = c.fy; d.cx = c.cx; d.cy = c.cy;
   d.near_plane = c.near_plane;
+  d.inv_half_w = 1.0 / (0.5 * double(c.width));
+  d.inv_half_h = 1.0 / (0.5 * double(c.height));
   d.width = c.width; d.height = c.height;
   d.tiles_x = (c.width + kTile - 1) / kTile;
   d.tiles_y = (c.height + kTile - 1) / kTile;

@@ -9,7 +9,7 @@
 // parameters (cheaper in HBM bytes than storing the reference's 40-float
 // backward cache per splat); precision per stage: see GS_BWD_REAL.  The SH path reuses the
 // forward's float32 basis and the stored clamp mask.
-#include "gs_common.cuh"
+#include "project.cuh"
 
 namespace gs {
 namespace {
@@ -373,14 +373,28 @@ struct FusedAdam {
 #ifndef GS_BWDADAM_SWEEP_U
 #define GS_BWDADAM_SWEEP_U 4
 #endif
+// The next view's projection (kProject): after the update every thread
+// stages its Gaussian's new parameters in shared memory (in place of the
+// gradients it consumed) and runs K1's per-Gaussian projection on them for
+// `ncam`, writing the next forward's splats `nout`, so that forward does not
+// re-read the 236 B of parameters per Gaussian the update just wrote.
+struct NextView {
+  DevCamera cam;
+  int degree;
+  gs_splats_t out;
+};
+
+template <bool kProject>
 __global__ void __launch_bounds__(128, GS_BWDADAM_MINB)
 preprocess_bwd_adam_kernel(gs_params_t p, DevCamera cam, int degree, const float4* __restrict__ rec,
                            const int32_t* __restrict__ radii, const float4* __restrict__ g2d, gs_grads_t out,
-                           gs_stats_t stats, FusedAdam A, const int32_t* __restrict__ skip) {
+                           gs_stats_t stats, FusedAdam A, const int32_t* __restrict__ skip, NextView next) {
   // device-side step guard (gs_step_guard): a step whose loss is not finite
   // or whose binning overflowed applies nothing — parameters, moments and
-  // statistics stay untouched, as the reference raises before updating
-  if (skip != nullptr && *skip != 0) return;
+  // statistics stay untouched, as the reference raises before updating (the
+  // next view is then projected from the unchanged parameters)
+  const bool apply = skip == nullptr || *skip == 0;
+  if (!kProject && !apply) return;
   extern __shared__ __align__(16) float4 smem4[];
   float4* s_sh = smem4;                      // staged SH coefficients (the SH parameters)
   float4* s_dsh = smem4;  // d_sh rows: each thread overwrites its own SH row after grad_one read it
@@ -401,7 +415,7 @@ preprocess_bwd_adam_kernel(gs_params_t p, DevCamera cam, int degree, const float
   for (int k = 0; k < 16; ++k) b[k] = 0.0f;
   GradOut o;
   zero_grads(o);
-  if (radius > 0) {
+  if (radius > 0 && apply) {
     grad_one(in, cam, degree, s_sh + threadIdx.x * kShStride, o, b, dcol);
     update_stats(stats, g, o.norm, radius, cam.height);
   }
@@ -409,7 +423,7 @@ preprocess_bwd_adam_kernel(gs_params_t p, DevCamera cam, int degree, const float
   // coalesced sweep over the block's contiguous span
   const int tid = threadIdx.x;
   if (valid) {
-    if (out.d_means) store_grads(out, g, o, false);
+    if (out.d_means && apply) store_grads(out, g, o, false);
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
       s_gmean[3 * tid + k] = o.dmean[k];
@@ -422,7 +436,7 @@ preprocess_bwd_adam_kernel(gs_params_t p, DevCamera cam, int degree, const float
     for (int k = 0; k < 12; ++k) row[k] = dsh_quad(b, dcol, k);
   }
   __syncthreads();
-  if (out.d_sh) store_sh_rows(s_dsh, p.n, g0, out.d_sh);
+  if (out.d_sh && apply) store_sh_rows(s_dsh, p.n, g0, out.d_sh);
   const int64_t left = p.n - g0;
   const int nb = left < int64_t(blockDim.x) ? int(left) : int(blockDim.x);
   {  // dense Adam: means, log_scales (N,3); rotations (N,4); opacity (N,)
@@ -445,28 +459,40 @@ preprocess_bwd_adam_kernel(gs_params_t p, DevCamera cam, int degree, const float
 #pragma unroll
     for (int u = 0; u < 3; ++u) {
       const int f = tid + u * int(blockDim.x);
-      if (f < 3 * nb) {
+      if (f < 3 * nb && apply) {
         adam_update(x[u], s_gmean[f], m[u], v[u], A.lr[0], A.c);
         adam_update(y[u], s_glogs[f], m2[u], v2[u], A.lr[1], A.c);
         pm[f] = x[u]; mm[f] = m[u]; vm[f] = v[u];
         pl[f] = y[u]; ml[f] = m2[u]; vl[f] = v2[u];
+      }
+      if (kProject && f < 3 * nb) {   // element f is this thread's alone: the new value replaces its gradient
+        s_gmean[f] = x[u];
+        s_glogs[f] = y[u];
       }
     }
     if (tid < nb) {
       float4* pr = reinterpret_cast<float4*>(const_cast<float*>(p.rotations)) + g0 + tid;
       float4* mr = reinterpret_cast<float4*>(A.m[2]) + g0 + tid;
       float4* vr = reinterpret_cast<float4*>(A.v[2]) + g0 + tid;
-      float4 q = *pr, m = *mr, v = *vr;
-      const float4 gq = s_grot[tid];
-      adam_update(q.x, gq.x, m.x, v.x, A.lr[2], A.c);
-      adam_update(q.y, gq.y, m.y, v.y, A.lr[2], A.c);
-      adam_update(q.z, gq.z, m.z, v.z, A.lr[2], A.c);
-      adam_update(q.w, gq.w, m.w, v.w, A.lr[2], A.c);
-      *pr = q; *mr = m; *vr = v;
+      float4 q = *pr;
       float* po = const_cast<float*>(p.opacity_logits) + g0 + tid;
-      float op = *po, mo = A.m[3][g0 + tid], vo = A.v[3][g0 + tid];
-      adam_update(op, s_gop[tid], mo, vo, A.lr[3], A.c);
-      *po = op; A.m[3][g0 + tid] = mo; A.v[3][g0 + tid] = vo;
+      float op = *po;
+      if (apply) {
+        float4 m = *mr, v = *vr;
+        const float4 gq = s_grot[tid];
+        adam_update(q.x, gq.x, m.x, v.x, A.lr[2], A.c);
+        adam_update(q.y, gq.y, m.y, v.y, A.lr[2], A.c);
+        adam_update(q.z, gq.z, m.z, v.z, A.lr[2], A.c);
+        adam_update(q.w, gq.w, m.w, v.w, A.lr[2], A.c);
+        *pr = q; *mr = m; *vr = v;
+        float mo = A.m[3][g0 + tid], vo = A.v[3][g0 + tid];
+        adam_update(op, s_gop[tid], mo, vo, A.lr[3], A.c);
+        *po = op; A.m[3][g0 + tid] = mo; A.v[3][g0 + tid] = vo;
+      }
+      if (kProject) {   // this thread's own Gaussian
+        s_grot[tid] = q;
+        s_gop[tid] = op;
+      }
     }
   }
   // dense Adam on the SH rows: coalesced float4 sweep over the block's span;
@@ -492,15 +518,28 @@ preprocess_bwd_adam_kernel(gs_params_t p, DevCamera cam, int degree, const float
       const int f = f0 + u * step;
       if (f >= total) break;
       const int j = f / 12, k = f - j * 12;
-      const float4 gq = s_dsh[j * kShStride + k];
-      const float lr0 = (k == 0) ? A.lr_sh_dc : A.lr[4];
-      adam_update(pq[u].x, gq.x, mq[u].x, vq[u].x, lr0, A.c);
-      adam_update(pq[u].y, gq.y, mq[u].y, vq[u].y, lr0, A.c);
-      adam_update(pq[u].z, gq.z, mq[u].z, vq[u].z, lr0, A.c);
-      adam_update(pq[u].w, gq.w, mq[u].w, vq[u].w, A.lr[4], A.c);
-      shp[f] = pq[u];
-      m4[f] = mq[u];
-      v4[f] = vq[u];
+      if (apply) {
+        const float4 gq = s_dsh[j * kShStride + k];
+        const float lr0 = (k == 0) ? A.lr_sh_dc : A.lr[4];
+        adam_update(pq[u].x, gq.x, mq[u].x, vq[u].x, lr0, A.c);
+        adam_update(pq[u].y, gq.y, mq[u].y, vq[u].y, lr0, A.c);
+        adam_update(pq[u].z, gq.z, mq[u].z, vq[u].z, lr0, A.c);
+        adam_update(pq[u].w, gq.w, mq[u].w, vq[u].w, A.lr[4], A.c);
+        shp[f] = pq[u];
+        m4[f] = mq[u];
+        v4[f] = vq[u];
+      }
+      if (kProject) s_dsh[j * kShStride + k] = pq[u];   // the element's new value replaces its gradient
+    }
+  }
+  if (kProject) {
+    __syncthreads();
+    if (tid < nb) {
+      const float4 q = s_grot[tid];
+      const float4* row = s_dsh + tid * kShStride;
+      project_gaussian(s_gmean[3 * tid + 0], s_gmean[3 * tid + 1], s_gmean[3 * tid + 2], q, s_glogs[3 * tid + 0],
+                       s_glogs[3 * tid + 1], s_glogs[3 * tid + 2], s_gop[tid], [&](int k) { return row[k]; },
+                       next.cam, next.degree, next.out, g);
     }
   }
 }
@@ -508,15 +547,26 @@ preprocess_bwd_adam_kernel(gs_params_t p, DevCamera cam, int degree, const float
 }  // namespace
 }  // namespace gs
 
-extern "C" int gs_preprocess_backward_adam_guarded(const gs_params_t* params, const gs_camera_t* camera,
-                                                   int32_t active_sh_degree, const gs_splats_t* splats,
-                                                   const float* grads2d, const gs_adam_group_t* groups, double beta1,
-                                                   double beta2, double eps, double bias1, double bias2,
-                                                   const gs_stats_t* stats, const gs_grads_t* grads_out,
-                                                   const int32_t* skip, void* stream) {
+namespace {
+// shared by the guarded entry and the one that also projects the next view
+int launch_backward_adam(const gs_params_t* params, const gs_camera_t* camera, int32_t active_sh_degree,
+                         const gs_splats_t* splats, const float* grads2d, const gs_adam_group_t* groups, double beta1,
+                         double beta2, double eps, double bias1, double bias2, const gs_stats_t* stats,
+                         const gs_grads_t* grads_out, const int32_t* skip, const gs_camera_t* next_camera,
+                         int32_t next_degree, gs_splats_t* next_splats, cudaStream_t s) {
   if (!params || !camera || !splats || !grads2d || !groups) return GS_ERR_INVALID_ARG;
   if (active_sh_degree < 0 || active_sh_degree > 3) return GS_ERR_INVALID_ARG;
   if (splats->n != params->n || !(bias1 > 0) || !(bias2 > 0)) return GS_ERR_INVALID_ARG;
+  const bool project = next_splats != nullptr;
+  if (project) {
+    if (!next_camera || next_degree < 0 || next_degree > 3 || next_splats->n != params->n) return GS_ERR_INVALID_ARG;
+    if (next_camera->width <= 0 || next_camera->height <= 0 || !(next_camera->fx > 0) || !(next_camera->fy > 0) ||
+        !(next_camera->near_plane > 0))
+      return GS_ERR_INVALID_ARG;
+    if (next_splats->rec == splats->rec) return GS_ERR_INVALID_ARG;   // the kernel still reads this step's records
+    cudaError_t e = cudaMemsetAsync(next_splats->status, 0, sizeof(int32_t), s);
+    if (e != cudaSuccess) return gs::record_cuda_error(e);
+  }
   if (params->n == 0) return GS_OK;
   for (int i = 0; i < 5; ++i)
     if (!groups[i].exp_avg || !groups[i].exp_avg_sq) return GS_ERR_INVALID_ARG;
@@ -536,19 +586,55 @@ extern "C" int gs_preprocess_backward_adam_guarded(const gs_params_t* params, co
   const size_t smem = (128 * gs::kShStride + 128) * sizeof(float4) + 128 * 7 * sizeof(float);
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(gs::preprocess_bwd_adam_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         int(smem));
-    if (e != cudaSuccess) return gs::record_cuda_error(e);
+    for (const void* fn : {reinterpret_cast<const void*>(gs::preprocess_bwd_adam_kernel<false>),
+                           reinterpret_cast<const void*>(gs::preprocess_bwd_adam_kernel<true>)}) {
+      cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+      if (e != cudaSuccess) return gs::record_cuda_error(e);
+    }
     configured = true;
   }
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
   const gs::DevCamera cam = gs::make_dev_camera(*camera);
+  gs::NextView next{};
+  if (project) {
+    next.cam = gs::make_dev_camera(*next_camera);
+    next.degree = next_degree;
+    next.out = *next_splats;
+  }
   const unsigned grid = unsigned((params->n + 127) / 128);
-  gs::preprocess_bwd_adam_kernel<<<grid, 128, smem, s>>>(*params, cam, active_sh_degree,
-                                                         reinterpret_cast<const float4*>(splats->rec),
-                                                         splats->radii, reinterpret_cast<const float4*>(grads2d),
-                                                         go, st, A, skip);
+  const float4* rec = reinterpret_cast<const float4*>(splats->rec);
+  const float4* g2 = reinterpret_cast<const float4*>(grads2d);
+  if (project)
+    gs::preprocess_bwd_adam_kernel<true><<<grid, 128, smem, s>>>(*params, cam, active_sh_degree, rec, splats->radii,
+                                                                 g2, go, st, A, skip, next);
+  else
+    gs::preprocess_bwd_adam_kernel<false><<<grid, 128, smem, s>>>(*params, cam, active_sh_degree, rec, splats->radii,
+                                                                  g2, go, st, A, skip, next);
   return gs::check_launch();
+}
+}  // namespace
+
+extern "C" int gs_preprocess_backward_adam_guarded(const gs_params_t* params, const gs_camera_t* camera,
+                                                   int32_t active_sh_degree, const gs_splats_t* splats,
+                                                   const float* grads2d, const gs_adam_group_t* groups, double beta1,
+                                                   double beta2, double eps, double bias1, double bias2,
+                                                   const gs_stats_t* stats, const gs_grads_t* grads_out,
+                                                   const int32_t* skip, void* stream) {
+  return launch_backward_adam(params, camera, active_sh_degree, splats, grads2d, groups, beta1, beta2, eps, bias1,
+                              bias2, stats, grads_out, skip, nullptr, 0, nullptr, static_cast<cudaStream_t>(stream));
+}
+
+extern "C" int gs_preprocess_backward_adam_project(const gs_params_t* params, const gs_camera_t* camera,
+                                                   int32_t active_sh_degree, const gs_splats_t* splats,
+                                                   const float* grads2d, const gs_adam_group_t* groups, double beta1,
+                                                   double beta2, double eps, double bias1, double bias2,
+                                                   const gs_stats_t* stats, const gs_grads_t* grads_out,
+                                                   const int32_t* skip, const gs_camera_t* next_camera,
+                                                   int32_t next_active_sh_degree, gs_splats_t* next_splats,
+                                                   void* stream) {
+  if (!next_splats) return GS_ERR_INVALID_ARG;
+  return launch_backward_adam(params, camera, active_sh_degree, splats, grads2d, groups, beta1, beta2, eps, bias1,
+                              bias2, stats, grads_out, skip, next_camera, next_active_sh_degree, next_splats,
+                              static_cast<cudaStream_t>(stream));
 }
 
 extern "C" int gs_preprocess_backward_adam(const gs_params_t* params, const gs_camera_t* camera,

@@ -157,13 +157,19 @@ class DeviceAdam:
 
     def backward_step(self, cloud: GaussianCloud, camera, splats, grads2d, active_sh_degree: int, iteration: int,
                       config: TrainConfig, stats=None, grads_out: GaussianGrads | None = None,
-                      skip: torch.Tensor | None = None) -> None:
+                      skip: torch.Tensor | None = None, project_next=None):
         """backward_project + densify statistics + Adam fused in one kernel
         (gs_preprocess_backward_adam): parameters are updated in place, the
         raw gradients never round-trip through HBM unless `grads_out` is given.
         `skip` (device int32 from `step_guard`): when set on the device, the
-        launch applies nothing."""
-        from .rasterizer import _camera
+        launch applies nothing.
+
+        project_next = (camera, active_sh_degree): the same launch also
+        projects the updated parameters for the next iteration's view
+        (gs_preprocess_backward_adam_project) and returns those splats
+        (bit-identical to rasterizer.project after this call; pass them to
+        render_view_async(..., splats=...)); otherwise returns None."""
+        from .rasterizer import DeviceSplats, _camera
         if not 0 <= active_sh_degree <= 3:
             raise ValueError(f"SH degree must be in 0..3, got {active_sh_degree}")
         t = int(iteration)
@@ -173,12 +179,23 @@ class DeviceAdam:
         cs = splats.c_struct()
         cst = stats.c_struct() if stats is not None else None
         cg = grads_out.c_struct() if grads_out is not None else None
-        _lib.check(_lib.load().gs_preprocess_backward_adam_guarded(
-            ctypes.byref(cloud.c_params()), ctypes.byref(_camera(camera).to_c()), int(active_sh_degree),
-            ctypes.byref(cs), grads2d.packed.data_ptr(), groups, beta1, beta2, config.adam_eps, bias1, bias2,
-            ctypes.byref(cst) if cst is not None else None, ctypes.byref(cg) if cg is not None else None,
-            skip.data_ptr() if skip is not None else None, torch.cuda.current_stream().cuda_stream),
-            "backward_adam")
+        common = (ctypes.byref(cloud.c_params()), ctypes.byref(_camera(camera).to_c()), int(active_sh_degree),
+                  ctypes.byref(cs), grads2d.packed.data_ptr(), groups, beta1, beta2, config.adam_eps, bias1, bias2,
+                  ctypes.byref(cst) if cst is not None else None, ctypes.byref(cg) if cg is not None else None,
+                  skip.data_ptr() if skip is not None else None)
+        stream = torch.cuda.current_stream().cuda_stream
+        if project_next is None:
+            _lib.check(_lib.load().gs_preprocess_backward_adam_guarded(*common, stream), "backward_adam")
+            return None
+        next_camera, next_degree = project_next
+        if not 0 <= next_degree <= 3:
+            raise ValueError(f"SH degree must be in 0..3, got {next_degree}")
+        nxt = DeviceSplats.empty(len(cloud), cloud.device)
+        cn = nxt.c_struct()
+        _lib.check(_lib.load().gs_preprocess_backward_adam_project(
+            *common, ctypes.byref(_camera(next_camera).to_c()), int(next_degree), ctypes.byref(cn), stream),
+            "backward_adam_project")
+        return nxt
 
 
 def step_guard(loss: torch.Tensor, k_info: torch.Tensor, out: torch.Tensor | None = None,

@@ -30,7 +30,8 @@ import torch
 # scatter, window count, window prefix, tile ranges, instance write)
 KERNELS_PER_STEP = {"preprocess_fwd": 1, "bin_and_sort": 14, "blend_fwd": 2, "loss": 3, "blend_bwd": 1,
                     "blend_bwd_setup": 3,
-                    "preprocess_bwd": 1, "adam": 1, "preprocess_bwd_adam": 1, "sharded_adam": 1}
+                    "preprocess_bwd": 1, "adam": 1, "preprocess_bwd_adam": 1, "preprocess_bwd_adam_project": 1,
+                    "sharded_adam": 1}
 
 
 class StageTimer:
@@ -97,6 +98,8 @@ class StageTimer:
             "adam": 1652 * n,
             # fused K8+K9: the 236 B/Gaussian gradient write and re-read are gone
             "preprocess_bwd_adam": 276 * V + 260 * n + 1652 * n - 472 * n,
+            # ... plus K1 for the next view on the updated parameters: only its record write is new
+            "preprocess_bwd_adam_project": 276 * V + 260 * n + 1652 * n - 472 * n + 48 * V,
             "loss": 132 * P,
         }
         hbm = float(peaks.get("hbm_gbs", 6650.0))

@@ -693,14 +693,20 @@ def render_view(cloud: GaussianCloud, camera, background, active_sh_degree: int 
 
 def render_view_async(cloud: GaussianCloud, camera, background, active_sh_degree: int = 3, training: bool = False,
                       capacity: int | None = None, tile_order: torch.Tensor | None = None,
-                      schedule: "TileSchedule | None" = None):
+                      schedule: "TileSchedule | None" = None, splats: "DeviceSplats | None" = None):
     """render_view with the sync-free binning: no host synchronisation, so
     the whole forward can be captured in a CUDA graph.  Errors (zero
     quaternion, capacity overflow) surface through binning.check().
     tile_order: see render_forward.  schedule: a TileSchedule for repeated
-    renders of one view (its order, when present, overrides tile_order)."""
+    renders of one view (its order, when present, overrides tile_order).
+    splats: this view's projection when already made (the previous step's
+    DeviceAdam.backward_step(..., project_next=(camera, degree))): K1 is
+    skipped."""
     camera = _camera(camera)
-    splats = _project_tensors(cloud.c_params(), len(cloud), cloud.device, camera, active_sh_degree)
+    if splats is None:
+        splats = _project_tensors(cloud.c_params(), len(cloud), cloud.device, camera, active_sh_degree)
+    elif len(splats) != len(cloud):
+        raise ValueError(f"splats hold {len(splats)} Gaussians, the cloud {len(cloud)}")
     binning = bin_and_sort_async(splats, camera.width, camera.height, capacity)
     work = None
     if schedule is not None:

@@ -253,12 +253,14 @@ def _ground_truth(state: TrainState, view: TrainView, camera: Camera, fresh: boo
     return downscale_image(image, camera.height, camera.width), consumed
 
 
-def _enqueue_forward(state: TrainState, fw: _Forward, config: TrainConfig) -> _Forward:
+def _enqueue_forward(state: TrainState, fw: _Forward, config: TrainConfig, splats=None) -> _Forward:
+    """splats: the view's projection when the previous step's fused
+    backward + Adam already made it (DeviceAdam.backward_step project_next)."""
     # the view's last backward schedule (heavy tiles first) orders this forward's tiles
     orders = getattr(state, "_tile_orders", None)
     order = orders.get((fw.view_idx, fw.camera.width, fw.camera.height)) if orders else None
     fw.out, fw.splats, fw.binning = R.render_view_async(state.cloud, fw.camera, config.background, fw.degree,
-                                                        training=True, tile_order=order)
+                                                        training=True, tile_order=order, splats=splats)
     # the backward's tile schedule and row clearing run on a side stream, beside the loss
     fw.prep = None if config.deterministic else R.prepare_backward(fw.out, fw.splats, fw.binning, fw.camera.width,
                                                                   fw.camera.height)
@@ -282,7 +284,8 @@ def train_step(state: TrainState, views: Sequence[TrainView], config: TrainConfi
     the NEXT iteration's view is
     drawn and its forward + loss enqueued behind this step's Adam (stream
     order: it sees the updated parameters), so the GPU never idles while the
-    host reads the loss.  The next train_step call consumes it when the
+    host reads the loss; the fused backward + Adam launch also projects the
+    updated parameters for that view (gs_preprocess_backward_adam_project).  The next train_step call consumes it when the
     iteration, views, config and cloud still match; otherwise (and in
     densify_and_prune) `TrainState.discard_lookahead` restores the view
     sampling state, so the sampled sequence is exactly the reference's.
@@ -321,11 +324,14 @@ def train_step(state: TrainState, views: Sequence[TrainView], config: TrainConfi
             if not hasattr(state, "_tile_orders"):
                 state._tile_orders = {}
             state._tile_orders[(fw.view_idx, fw.camera.width, fw.camera.height)] = g2.tile_order
-        state.adam.backward_step(state.cloud, fw.camera, fw.splats, g2, fw.degree, it, config, stats=state.stats,
-                                 skip=skip)
-        if lookahead:
-            nxt = _enqueue_forward(state, _sample_view(state, views, config, it + 1,
-                                                       _degree_for(degree, it + 1, config)), config)
+        # lookahead: the next view is drawn first, so the fused backward + Adam
+        # also projects the updated parameters for it (no separate K1 launch)
+        nxt = _sample_view(state, views, config, it + 1, _degree_for(degree, it + 1, config)) if lookahead else None
+        nsplats = state.adam.backward_step(state.cloud, fw.camera, fw.splats, g2, fw.degree, it, config,
+                                           stats=state.stats, skip=skip,
+                                           project_next=None if nxt is None else (nxt.camera, nxt.degree))
+        if nxt is not None:
+            nxt = _enqueue_forward(state, nxt, config, splats=nsplats)
         done.synchronize()
         lvals, kvals = host.report_values()
         try:

@@ -330,6 +330,49 @@ def test_fused_backward_adam_matches_unfused(cuda_device):
     torch.testing.assert_close(st_b.accum_pos_grad, st_a.accum_pos_grad, rtol=1e-6, atol=0)
 
 
+@pytest.mark.parametrize("skipped", [False, True])
+def test_fused_next_view_projection_bit_identical(cuda_device, skipped):
+    """gs_preprocess_backward_adam_project == the guarded backward + Adam
+    followed by gs_preprocess_forward for the next view: parameters, moments
+    and the next view's splats bit for bit (next view: another pose and
+    resolution, with culled and guard-band Gaussians); with the step guard
+    set, nothing is updated and the next view is projected from the
+    unchanged parameters."""
+    from paper_2308_04079_b200.camera import look_at
+    g, cloud_np, cam = golden_scenes.load("scene_c")
+    degree, bg = int(g["degree"]), g["background"]
+    d_image = torch.from_numpy(golden_scenes.d_image_for(17, cam.width, cam.height).astype(np.float32)).cuda()
+    centre = cloud_np["means"].mean(axis=0)
+    # from inside the cloud: Gaussians behind the near plane and outside the guard band are culled
+    nxt_cam = look_at(centre, centre + np.array([1.0, 0.3, 0.2]), width=97, height=61, fx=60.0, near=0.05)
+    cfg = TrainConfig(total_iters=1000)
+    a, b = GaussianCloud.from_numpy(**cloud_np), GaussianCloud.from_numpy(**cloud_np)
+    opt_a, opt_b = DeviceAdam(a), DeviceAdam(b)
+    st_a, st_b = R.DensifyStats.zeros(len(a), "cuda"), R.DensifyStats.zeros(len(b), "cuda")
+    skip = torch.full((1,), int(skipped), dtype=torch.int32, device="cuda")
+    before = {k: getattr(a, k).clone() for k in ("means", "log_scales", "rotations", "opacity_logits", "sh")}
+    out, splats, binning = R.render_view(a, cam, bg, degree, training=True)
+    g2 = R.render_backward(d_image, out, splats, binning, cam.width, cam.height, bg)
+    opt_a.backward_step(a, cam, splats, g2, degree, 1, cfg, stats=st_a, skip=skip)
+    ref = R.project(a, nxt_cam, 2)
+    got = opt_b.backward_step(b, cam, splats, g2, degree, 1, cfg, stats=st_b, skip=skip, project_next=(nxt_cam, 2))
+    torch.cuda.synchronize()
+    for k in ("means", "log_scales", "rotations", "opacity_logits", "sh"):
+        assert torch.equal(getattr(b, k), getattr(a, k)), k
+        assert torch.equal(opt_b.exp_avg[k], opt_a.exp_avg[k]), k
+        assert torch.equal(opt_b.exp_avg_sq[k], opt_a.exp_avg_sq[k]), k
+        if skipped:
+            assert torch.equal(getattr(b, k), before[k]), k
+    assert torch.equal(st_a.accum_count, st_b.accum_count)
+    assert torch.equal(st_a.accum_pos_grad, st_b.accum_pos_grad)
+    vis = ref.radii > 0
+    assert 0 < int(vis.sum()) < len(a)   # the next view culls some Gaussians
+    for f in ("radii", "tiles_touched", "status"):
+        assert torch.equal(getattr(got, f), getattr(ref, f)), f
+    for f in ("rec", "depth", "rect"):
+        assert torch.equal(getattr(got, f)[vis], getattr(ref, f)[vis]), f
+
+
 def _fuzz_scene(seed: int):
     """Adversarial mixes: random look-at camera, Gaussians behind / at / beyond
     the near plane and the guard band, extreme anisotropy and scales,

@@ -63,10 +63,20 @@ def main() -> None:
         it[0] += 1
         adam.backward_step(cloud, cam, splats, g2, 3, it[0], TrainConfig(), stats=stats)
 
+    def bwd_adam_project():
+        it[0] += 1
+        adam.backward_step(cloud, cam, splats, g2, 3, it[0], TrainConfig(), stats=stats, project_next=(cam, 3))
+
+    def bwd_adam_then_project():
+        bwd_adam()
+        R._project_tensors(cloud.c_params(), len(cloud), "cuda", cam, 3)
+
     res = {
         "lib": str(_lib.LIB_PATH), "n": args.n, "width": W, "height": H,
         "instances": binning.num_instances,
         "bwd_adam_ms": timeit(bwd_adam),
+        "bwd_adam_project_ms": timeit(bwd_adam_project),
+        "bwd_adam_then_project_ms": timeit(bwd_adam_then_project),
         "blend_fwd_ms": timeit(lambda: R.render_forward(splats, binning, W, H, bg, training=True)),
         "blend_bwd_ms": timeit(lambda: R.render_backward(d, out, splats, binning, W, H, bg)),
         "bin_async_ms": timeit(lambda: R.bin_and_sort_async(splats, W, H)),
@@ -124,6 +134,14 @@ def main() -> None:
                                              torch.cuda.current_stream().cuda_stream)
             res[f"blend_fwd_order_{name}_ms"] = timeit(runf)
             res[f"fwd_order_{name}_same"] = bool(torch.equal(img, out.image) and torch.equal(ls, out.last_contributor))
+    # the fused projection is bit-identical to projecting after the update
+    nxt = adam.backward_step(cloud, cam, splats, g2, 3, it[0] + 1, TrainConfig(), project_next=(cam, 3))
+    ref = R._project_tensors(cloud.c_params(), len(cloud), "cuda", cam, 3)
+    vis = ref.radii > 0
+    res["project_fused_identical"] = (all(torch.equal(getattr(nxt, f), getattr(ref, f))
+                                          for f in ("radii", "tiles_touched", "status"))
+                                      and all(torch.equal(getattr(nxt, f)[vis], getattr(ref, f)[vis])
+                                              for f in ("rec", "depth", "rect")))
     g_ref = R.render_backward(d, out, splats, binning, W, H, bg).packed
     res["bwd_checksum"] = float(g_ref.double().abs().sum())
     print(json.dumps(res))
