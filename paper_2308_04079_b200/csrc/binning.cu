@@ -197,6 +197,7 @@ constexpr int kHistItems = 8;
 __global__ void __launch_bounds__(kThreads) depth_hist_kernel(const float* __restrict__ depth,
                                                              const int32_t* __restrict__ tiles, int64_t n,
                                                              uint32_t* __restrict__ hist, int64_t* __restrict__ kinfo) {
+  pdl_begin();
   __shared__ uint32_t s_h[kPasses * kRadix];
   for (int i = threadIdx.x; i < kPasses * kRadix; i += kThreads) s_h[i] = 0;
   __syncthreads();
@@ -257,6 +258,7 @@ __global__ void __launch_bounds__(1024) sort_setup_kernel(const uint32_t* __rest
                                                           uint32_t* __restrict__ digit_base,
                                                           const int32_t* __restrict__ status, int64_t capacity,
                                                           int64_t* __restrict__ kinfo) {
+  pdl_begin();
   __shared__ uint32_t s_w[32];
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;   // pass = t / 256 = warp / 8
   const uint32_t v = hist[t];
@@ -298,6 +300,7 @@ __global__ void __launch_bounds__(kThreads, GS_SORT_MIN_BLOCKS) onesweep_kernel(
     const uint32_t* __restrict__ keys_in, const uint32_t* __restrict__ ids_in, uint32_t* __restrict__ keys_out,
     uint32_t* __restrict__ ids_out, int4* __restrict__ drect_out, const uint32_t* __restrict__ digit_base,
     uint64_t* status, uint32_t* ticket, int shift, int64_t n, const int64_t* __restrict__ kinfo) {
+  pdl_begin();
   __shared__ uint32_t s_cnt[kWarps][kRadix];
   __shared__ uint32_t s_local[kRadix];
   __shared__ uint32_t s_delta[kRadix];
@@ -432,6 +435,7 @@ __global__ void __launch_bounds__(kThreads) bucket_count_kernel(const int4* __re
                                                                int64_t n, Grid g, uint32_t* __restrict__ M,
                                                                uint16_t* __restrict__ Mw, int64_t chunks,
                                                                const int64_t* __restrict__ kinfo) {
+  pdl_begin();
   extern __shared__ uint32_t s_h[];   // [kWarps][S]
   if (kinfo[1] != 0) return;
   for (int s = threadIdx.x; s < kWarps * g.S; s += kThreads) s_h[s] = 0u;
@@ -473,6 +477,7 @@ __global__ void __launch_bounds__(kThreads) bucket_count_kernel(const int4* __re
 // of one value per block).  *total_out = the sum.
 __global__ void __launch_bounds__(kThreads) scan_kernel(uint32_t* data, int64_t len, uint64_t* status, uint32_t* ticket,
                                                         uint32_t* total_out, const int64_t* __restrict__ kinfo) {
+  pdl_begin();
   __shared__ uint32_t s_w[33];
   __shared__ uint32_t s_block, s_excl;
   if (kinfo[1] != 0) return;
@@ -541,6 +546,7 @@ __global__ void __launch_bounds__(1024) window_setup_kernel(const uint32_t* __re
                                                             uint32_t* __restrict__ bstart, uint32_t* __restrict__ wstart,
                                                             uint32_t* __restrict__ wmap,
                                                             const int64_t* __restrict__ kinfo) {
+  pdl_begin();
   __shared__ uint32_t s_w[33];
   if (kinfo[1] != 0) return;
   constexpr int kPer = kMaxSuper / 1024;
@@ -595,6 +601,7 @@ __global__ void __launch_bounds__(kThreads) bucket_scatter_kernel(const int4* __
                                                                  const uint16_t* __restrict__ Mw, int64_t chunks,
                                                                  uint2* __restrict__ entries, int64_t capacity,
                                                                  const int64_t* __restrict__ kinfo) {
+  pdl_begin();
   extern __shared__ uint32_t s_cur[];   // [kWarps][S] cursors, then [kWarps][S] bytes of bucket stamps
   if (kinfo[1] != 0) return;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -776,6 +783,7 @@ __global__ void __launch_bounds__(kThreads) window_count_kernel(const uint2* __r
                                                                const uint32_t* __restrict__ wstart, Grid g,
                                                                uint32_t* __restrict__ cnt,
                                                                const int64_t* __restrict__ kinfo) {
+  pdl_begin();
   if (kinfo[1] != 0) return;
   const int lane = threadIdx.x & 31;
   const uint32_t nwin = wstart[g.S];
@@ -815,6 +823,7 @@ __global__ void __launch_bounds__(kThreads) window_prefix_kernel(const uint32_t*
                                                                 uint32_t* __restrict__ cnt,
                                                                 uint32_t* __restrict__ tile_total,
                                                                 const int64_t* __restrict__ kinfo) {
+  pdl_begin();
   if (kinfo[1] != 0) return;
   const uint32_t s = blockIdx.x * kWarps + (threadIdx.x >> 5);
   if (s >= uint32_t(g.S)) return;
@@ -855,6 +864,7 @@ __global__ void __launch_bounds__(kThreads) window_prefix_kernel(const uint32_t*
 __global__ void __launch_bounds__(1024) tile_ranges_kernel(const uint32_t* __restrict__ tile_total, int64_t tiles,
                                                            int2* __restrict__ ranges,
                                                            const int64_t* __restrict__ kinfo) {
+  pdl_begin();
   __shared__ uint32_t s_w[33];
   const bool flagged = kinfo[1] != 0;
   uint32_t carry = 0;
@@ -883,6 +893,7 @@ __global__ void __launch_bounds__(kThreads) instance_write_kernel(
     const uint32_t* __restrict__ wstart, Grid g, const uint32_t* __restrict__ cnt, const int2* __restrict__ ranges,
     const float* __restrict__ depth, uint32_t* __restrict__ ids, unsigned long long* __restrict__ keys,
     const int64_t* __restrict__ kinfo) {
+  pdl_begin();
   if (kinfo[1] != 0) return;
   const int lane = threadIdx.x & 31;
   const uint32_t nwin = wstart[g.S];
@@ -955,6 +966,7 @@ __global__ void __launch_bounds__(kThreads) instance_write_staged_kernel(
     const uint32_t* __restrict__ wstart, Grid g, const uint32_t* __restrict__ cnt, const int2* __restrict__ ranges,
     const float* __restrict__ depth, uint32_t* __restrict__ ids, unsigned long long* __restrict__ keys,
     const int64_t* __restrict__ kinfo) {
+  pdl_begin();
   extern __shared__ uint32_t s_ring[];
   __shared__ uint32_t s_eid[kWarps][32];
   if (kinfo[1] != 0) return;
@@ -1120,15 +1132,15 @@ int walk(const Layout& L, char* ws, const float* depth, uint32_t* ids, int2* ran
          const int64_t* kinfo, cudaStream_t s) {
   const Grid g = L.g;
   const int persistent = 148 * 8;   // 8 resident warps-blocks per SM x 148 SMs
-  window_count_kernel<Q><<<persistent, kThreads, 0, s>>>(at<uint2>(ws, L.entries), at<uint32_t>(ws, L.wmap),
+  launch_pdl(window_count_kernel<Q>, persistent, kThreads, 0, s, at<uint2>(ws, L.entries), at<uint32_t>(ws, L.wmap),
                                                         at<uint32_t>(ws, L.bstart), at<uint32_t>(ws, L.wstart), g,
                                                         at<uint32_t>(ws, L.cnt), kinfo);
   int st = check_launch();
   if (st != GS_OK) return st;
-  window_prefix_kernel<Q><<<unsigned((g.S + kWarps - 1) / kWarps), kThreads, 0, s>>>(
+  launch_pdl(window_prefix_kernel<Q>, unsigned((g.S + kWarps - 1) / kWarps), kThreads, 0, s, 
       at<uint32_t>(ws, L.wstart), g, at<uint32_t>(ws, L.cnt), at<uint32_t>(ws, L.tile_total), kinfo);
   if ((st = check_launch()) != GS_OK) return st;
-  tile_ranges_kernel<<<1, 1024, 0, s>>>(at<uint32_t>(ws, L.tile_total), L.tiles, ranges, kinfo);
+  launch_pdl(tile_ranges_kernel, 1, 1024, 0, s, at<uint32_t>(ws, L.tile_total), L.tiles, ranges, kinfo);
   if ((st = check_launch()) != GS_OK) return st;
   if (Q == 1) {
     const void* fn = keys ? reinterpret_cast<const void*>(instance_write_staged_kernel<true>)
@@ -1136,15 +1148,15 @@ int walk(const Layout& L, char* ws, const float* depth, uint32_t* ids, int2* ran
     cudaError_t e = smem_opt_in(fn, kStagedSmem);
     if (e != cudaSuccess) return record_cuda_error(e);
     if (keys)
-      instance_write_staged_kernel<true><<<148 * 3, kThreads, kStagedSmem, s>>>(
+      launch_pdl(instance_write_staged_kernel<true>, 148 * 3, kThreads, kStagedSmem, s, 
           at<uint2>(ws, L.entries), at<uint32_t>(ws, L.wmap), at<uint32_t>(ws, L.bstart), at<uint32_t>(ws, L.wstart),
           g, at<uint32_t>(ws, L.cnt), ranges, depth, ids, keys, kinfo);
     else
-      instance_write_staged_kernel<false><<<148 * 3, kThreads, kStagedSmem, s>>>(
+      launch_pdl(instance_write_staged_kernel<false>, 148 * 3, kThreads, kStagedSmem, s, 
         at<uint2>(ws, L.entries), at<uint32_t>(ws, L.wmap), at<uint32_t>(ws, L.bstart), at<uint32_t>(ws, L.wstart),
         g, at<uint32_t>(ws, L.cnt), ranges, depth, ids, keys, kinfo);
   } else {
-    instance_write_kernel<Q><<<persistent, kThreads, 0, s>>>(at<uint2>(ws, L.entries), at<uint32_t>(ws, L.wmap),
+    launch_pdl(instance_write_kernel<Q>, persistent, kThreads, 0, s, at<uint2>(ws, L.entries), at<uint32_t>(ws, L.wmap),
                                                             at<uint32_t>(ws, L.bstart), at<uint32_t>(ws, L.wstart), g,
                                                             at<uint32_t>(ws, L.cnt), ranges, depth, ids, keys, kinfo);
   }
@@ -1178,10 +1190,9 @@ int bin_enqueue(const gs_splats_t* splats, int32_t width, int32_t height, void* 
   uint32_t* digit_base = at<uint32_t>(ws, L.digit_base);
   uint64_t* sort_status = at<uint64_t>(ws, L.sort_status);
   const unsigned blocks = unsigned(L.blocks);
-  depth_hist_kernel<<<unsigned((n + int64_t(kThreads) * kHistItems - 1) / (int64_t(kThreads) * kHistItems)), kThreads, 0,
-                      s>>>(splats->depth, splats->tiles_touched, n, hist, kinfo);
+  launch_pdl(depth_hist_kernel, unsigned((n + int64_t(kThreads) * kHistItems - 1) / (int64_t(kThreads) * kHistItems)), kThreads, 0, s, splats->depth, splats->tiles_touched, n, hist, kinfo);
   if ((st = check_launch()) != GS_OK) return st;
-  sort_setup_kernel<<<1, 1024, 0, s>>>(hist, digit_base, splats->status, cap, kinfo);
+  launch_pdl(sort_setup_kernel, 1, 1024, 0, s, hist, digit_base, splats->status, cap, kinfo);
   if ((st = check_launch()) != GS_OK) return st;
   if (cap == 0) {   // K and the flags only
     if (ranges) e = cudaMemsetAsync(ranges, 0, size_t(L.tiles) * sizeof(int2), s);
@@ -1194,19 +1205,19 @@ int bin_enqueue(const gs_splats_t* splats, int32_t width, int32_t height, void* 
   uint32_t* order = at<uint32_t>(ws, L.order);
   int4* drect = at<int4>(ws, L.drect);
   const size_t pass_status = size_t(kRadix) * L.blocks;
-  onesweep_kernel<true, false><<<blocks, kThreads, 0, s>>>(splats->depth, splats->tiles_touched, rect, nullptr,
+  launch_pdl(onesweep_kernel<true, false>, blocks, kThreads, 0, s, splats->depth, splats->tiles_touched, rect, nullptr,
                                                            nullptr, ka, ia, nullptr, digit_base, sort_status,
                                                            tickets + 0, 0, n, kinfo);
   if ((st = check_launch()) != GS_OK) return st;
-  onesweep_kernel<false, false><<<blocks, kThreads, 0, s>>>(nullptr, nullptr, nullptr, ka, ia, kb, ib, nullptr,
+  launch_pdl(onesweep_kernel<false, false>, blocks, kThreads, 0, s, nullptr, nullptr, nullptr, ka, ia, kb, ib, nullptr,
                                                             digit_base + kRadix, sort_status + pass_status,
                                                             tickets + 1, 8, n, kinfo);
   if ((st = check_launch()) != GS_OK) return st;
-  onesweep_kernel<false, false><<<blocks, kThreads, 0, s>>>(nullptr, nullptr, nullptr, kb, ib, ka, ia, nullptr,
+  launch_pdl(onesweep_kernel<false, false>, blocks, kThreads, 0, s, nullptr, nullptr, nullptr, kb, ib, ka, ia, nullptr,
                                                             digit_base + 2 * kRadix, sort_status + 2 * pass_status,
                                                             tickets + 2, 16, n, kinfo);
   if ((st = check_launch()) != GS_OK) return st;
-  onesweep_kernel<false, true><<<blocks, kThreads, 0, s>>>(nullptr, splats->tiles_touched, rect, ka, ia, nullptr,
+  launch_pdl(onesweep_kernel<false, true>, blocks, kThreads, 0, s, nullptr, splats->tiles_touched, rect, ka, ia, nullptr,
                                                            order, drect, digit_base + 3 * kRadix,
                                                            sort_status + 3 * pass_status, tickets + 3, 24, n, kinfo);
   if ((st = check_launch()) != GS_OK) return st;
@@ -1216,14 +1227,14 @@ int bin_enqueue(const gs_splats_t* splats, int32_t width, int32_t height, void* 
   uint16_t* Mw = at<uint16_t>(ws, L.mw);
   if ((e = smem_opt_in(reinterpret_cast<const void*>(bucket_count_kernel), smem_count)) != cudaSuccess)
     return record_cuda_error(e);
-  bucket_count_kernel<<<unsigned(L.chunks), kThreads, smem_count, s>>>(rect, order, hist, drect, n, g, M, Mw, L.chunks,
+  launch_pdl(bucket_count_kernel, unsigned(L.chunks), kThreads, smem_count, s, rect, order, hist, drect, n, g, M, Mw, L.chunks,
                                                                        kinfo);
   if ((st = check_launch()) != GS_OK) return st;
   uint32_t* mtotal = at<uint32_t>(ws, L.mtotal);
-  scan_kernel<<<unsigned((L.mlen + kScanTile - 1) / kScanTile), kThreads, 0, s>>>(
+  launch_pdl(scan_kernel, unsigned((L.mlen + kScanTile - 1) / kScanTile), kThreads, 0, s, 
       M, L.mlen, at<uint64_t>(ws, L.scan_status), tickets + 4, mtotal, kinfo);
   if ((st = check_launch()) != GS_OK) return st;
-  window_setup_kernel<<<1, 1024, 0, s>>>(M, L.chunks, mtotal, g, at<uint32_t>(ws, L.bstart),
+  launch_pdl(window_setup_kernel, 1, 1024, 0, s, M, L.chunks, mtotal, g, at<uint32_t>(ws, L.bstart),
                                          at<uint32_t>(ws, L.wstart), at<uint32_t>(ws, L.wmap), kinfo);
   if ((st = check_launch()) != GS_OK) return st;
   // cursors + OR bins (<= 2048 super-tiles) or cursors + byte stamps
@@ -1233,10 +1244,10 @@ int bin_enqueue(const gs_splats_t* splats, int32_t width, int32_t height, void* 
                                    : reinterpret_cast<const void*>(bucket_scatter_kernel<false>);
   if ((e = smem_opt_in(scatter_fn, smem_scatter)) != cudaSuccess) return record_cuda_error(e);
   if (or_bins)
-    bucket_scatter_kernel<true><<<unsigned(L.chunks), kThreads, smem_scatter, s>>>(drect, order, n, g, M, Mw, L.chunks,
+    launch_pdl(bucket_scatter_kernel<true>, unsigned(L.chunks), kThreads, smem_scatter, s, drect, order, n, g, M, Mw, L.chunks,
                                                                       at<uint2>(ws, L.entries), cap, kinfo);
   else
-    bucket_scatter_kernel<false><<<unsigned(L.chunks), kThreads, smem_scatter, s>>>(drect, order, n, g, M, Mw, L.chunks,
+    launch_pdl(bucket_scatter_kernel<false>, unsigned(L.chunks), kThreads, smem_scatter, s, drect, order, n, g, M, Mw, L.chunks,
                                                                        at<uint2>(ws, L.entries), cap, kinfo);
   if ((st = check_launch()) != GS_OK) return st;
   // 3-5. windows, ranges, instance lists

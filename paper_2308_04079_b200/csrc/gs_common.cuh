@@ -8,7 +8,8 @@
 #pragma once
 
 #include <cstdint>
-#include <cuda.h>   // CUtensorMap (the TMA descriptor type; the encoder is fetched at run time)
+#include <cuda.h>
+#include <utility>   // CUtensorMap (the TMA descriptor type; the encoder is fetched at run time)
 #include <cuda_runtime.h>
 
 #include "../../include/gs_rasterizer.h"
@@ -619,5 +620,41 @@ __device__ __forceinline__ void sh_basis_vjp(float x, float y, float z, int degr
 // Status plumbing shared by the C-ABI entry points.
 int record_cuda_error(cudaError_t err);
 int check_launch();
+
+// ---------------------------------------------------------------------------
+// Programmatic dependent launch.  A kernel launched with launch_pdl may be
+// scheduled while its stream predecessor's last blocks still run (its blocks
+// take the SM slots the predecessor's tail frees); every such kernel begins
+// with pdl_begin(): griddepcontrol.wait blocks until the predecessor grid has
+// completed and its memory is visible (so no read or write of this kernel can
+// race it), then launch_dependents lets the successor do the same.  After a
+// kernel that never triggers (a library kernel, a memset) the wait returns
+// at once and the launch is an ordinary stream-ordered one.
+#ifndef GS_PDL
+#define GS_PDL 1
+#endif
+
+__device__ __forceinline__ void pdl_begin() {
+#if GS_PDL
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+}
+
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                       Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = GS_PDL ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);   // errors surface through check_launch()
+}
 
 }  // namespace gs
