@@ -25,6 +25,7 @@ __device__ __forceinline__ void adam_elem(float& p, float gr, float& m, float& v
 }
 
 __global__ void __launch_bounds__(256) adam_kernel(AdamArgs a, const int32_t* __restrict__ skip) {
+  pdl_begin();
   const int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (q >= a.quad_start[a.num_groups]) return;
   if (skip != nullptr && *skip != 0) return;   // the step guard (gs_step_guard) vetoed this step
@@ -97,7 +98,7 @@ int adam_step(const gs_adam_group_t* groups, int32_t num_groups, double beta1, d
   const int64_t quads = a.quad_start[num_groups];
   if (quads == 0) return GS_OK;
   const int block = 256;
-  adam_kernel<<<unsigned((quads + block - 1) / block), block, 0, static_cast<cudaStream_t>(stream)>>>(a, skip);
+  launch_pdl(adam_kernel, unsigned((quads + block - 1) / block), block, 0, static_cast<cudaStream_t>(stream), a, skip);
   return check_launch();
 }
 }  // namespace

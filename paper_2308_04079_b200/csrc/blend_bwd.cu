@@ -169,6 +169,7 @@ blend_bwd_kernel(const float* __restrict__ d_image, const float4* __restrict__ r
                  const int2* __restrict__ ranges, const float* __restrict__ t_final, const int32_t* __restrict__ last,
                  int width, int height, int tiles_x, int tile0, float3 bg, float4* __restrict__ grads2d,
                  const int32_t* __restrict__ tile_order, float* __restrict__ part_out, int32_t* __restrict__ top_out) {
+  pdl_begin();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   BwdStage* stages = reinterpret_cast<BwdStage*>(smem_raw);
   RawRec* raw = reinterpret_cast<RawRec*>(smem_raw + sizeof(BwdStage) * kStages);
@@ -413,12 +414,12 @@ int blend_backward_rows(const float* d_image, const gs_splats_t* splats, const u
   const float3 bg = make_float3(background[0], background[1], background[2]);
   const int64_t ntiles = int64_t(row_end - row_begin) * tiles_x;
   if (part_out)
-    blend_bwd_kernel<true><<<unsigned(ntiles * kParts), kThreads, kSmemBytesDet, static_cast<cudaStream_t>(stream)>>>(
+    launch_pdl(blend_bwd_kernel<true>, unsigned(ntiles * kParts), kThreads, kSmemBytesDet, static_cast<cudaStream_t>(stream), 
         d_image, reinterpret_cast<const float4*>(splats->rec), sorted_ids, reinterpret_cast<const int2*>(ranges),
         t_final, last, width, height, tiles_x, row_begin * tiles_x, bg, reinterpret_cast<float4*>(grads2d),
         tile_order, part_out, top_out);
   else
-    blend_bwd_kernel<false><<<unsigned(ntiles * kParts), kThreads, kSmemBytes, static_cast<cudaStream_t>(stream)>>>(
+    launch_pdl(blend_bwd_kernel<false>, unsigned(ntiles * kParts), kThreads, kSmemBytes, static_cast<cudaStream_t>(stream), 
         d_image, reinterpret_cast<const float4*>(splats->rec), sorted_ids, reinterpret_cast<const int2*>(ranges),
         t_final, last, width, height, tiles_x, row_begin * tiles_x, bg, reinterpret_cast<float4*>(grads2d),
         tile_order, nullptr, nullptr);
@@ -474,6 +475,7 @@ __device__ __forceinline__ int need_bucket(int need) {
 __global__ void tile_need_kernel(const int32_t* __restrict__ last, const int2* __restrict__ ranges, int width,
                                  int height, int tiles_x, int tiles, int32_t* __restrict__ bucket_of,
                                  int32_t* __restrict__ hist) {
+  pdl_begin();
   const int tile = int((int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5);
   const int lane = threadIdx.x & 31;
   if (tile >= tiles) return;
@@ -497,6 +499,7 @@ __global__ void tile_need_kernel(const int32_t* __restrict__ last, const int2* _
 // bucket of a given per-tile work (gs_tile_schedule)
 __global__ void tile_bucket_kernel(const int32_t* __restrict__ work, int tiles, int32_t* __restrict__ bucket_of,
                                    int32_t* __restrict__ hist) {
+  pdl_begin();
   const int t = int(int64_t(blockIdx.x) * blockDim.x + threadIdx.x);
   if (t >= tiles) return;
   const int b = need_bucket(work[t]);
@@ -508,6 +511,7 @@ __global__ void tile_bucket_kernel(const int32_t* __restrict__ work, int tiles, 
 // kSchedBuckets threads; thread i owns bucket kSchedBuckets - 1 - i)
 __global__ void __launch_bounds__(kSchedBuckets) tile_sched_scan_kernel(const int32_t* __restrict__ hist,
                                                                         int32_t* __restrict__ cursor) {
+  pdl_begin();
   __shared__ int warp_tot[kSchedBuckets / 32];
   const int i = threadIdx.x, lane = i & 31, w = i >> 5;
   const int b = kSchedBuckets - 1 - i;
@@ -535,6 +539,7 @@ __global__ void __launch_bounds__(kSchedBuckets) tile_sched_scan_kernel(const in
 
 __global__ void tile_sched_scatter_kernel(const int32_t* __restrict__ bucket_of, int32_t* __restrict__ cursor,
                                           int tiles, int32_t* __restrict__ order) {
+  pdl_begin();
   const int t = int(int64_t(blockIdx.x) * blockDim.x + threadIdx.x);
   if (t < tiles) order[atomicAdd(&cursor[bucket_of[t]], 1)] = t;
 }
@@ -557,10 +562,10 @@ extern "C" int gs_blend_backward_schedule(const int32_t* ranges, const int32_t* 
   int32_t* cursor = hist + kSchedBuckets;
   cudaError_t e = cudaMemsetAsync(hist, 0, kSchedBuckets * sizeof(int32_t), s);
   if (e != cudaSuccess) return record_cuda_error(e);
-  tile_need_kernel<<<unsigned((int64_t(tiles) * 32 + 255) / 256), 256, 0, s>>>(
+  launch_pdl(tile_need_kernel, unsigned((int64_t(tiles) * 32 + 255) / 256), 256, 0, s, 
       last, reinterpret_cast<const int2*>(ranges), width, height, tiles_x, tiles, bucket_of, hist);
-  tile_sched_scan_kernel<<<1, kSchedBuckets, 0, s>>>(hist, cursor);
-  tile_sched_scatter_kernel<<<unsigned((tiles + 255) / 256), 256, 0, s>>>(bucket_of, cursor, tiles, order);
+  launch_pdl(tile_sched_scan_kernel, 1, kSchedBuckets, 0, s, hist, cursor);
+  launch_pdl(tile_sched_scatter_kernel, unsigned((tiles + 255) / 256), 256, 0, s, bucket_of, cursor, tiles, order);
   return check_launch();
 }
 
@@ -602,9 +607,9 @@ extern "C" int gs_tile_schedule(const int32_t* work, int32_t tiles, int32_t* scr
   int32_t* cursor = hist + kSchedBuckets;
   cudaError_t e = cudaMemsetAsync(hist, 0, kSchedBuckets * sizeof(int32_t), s);
   if (e != cudaSuccess) return record_cuda_error(e);
-  tile_bucket_kernel<<<unsigned((tiles + 255) / 256), 256, 0, s>>>(work, tiles, bucket_of, hist);
-  tile_sched_scan_kernel<<<1, kSchedBuckets, 0, s>>>(hist, cursor);
-  tile_sched_scatter_kernel<<<unsigned((tiles + 255) / 256), 256, 0, s>>>(bucket_of, cursor, tiles, order);
+  launch_pdl(tile_bucket_kernel, unsigned((tiles + 255) / 256), 256, 0, s, work, tiles, bucket_of, hist);
+  launch_pdl(tile_sched_scan_kernel, 1, kSchedBuckets, 0, s, hist, cursor);
+  launch_pdl(tile_sched_scatter_kernel, unsigned((tiles + 255) / 256), 256, 0, s, bucket_of, cursor, tiles, order);
   return check_launch();
 }
 
@@ -626,6 +631,7 @@ constexpr int kScanBlock = 1024;
 // single-block scan of the sums, then the per-block add
 __global__ void __launch_bounds__(kScanBlock) det_count_kernel(const int32_t* __restrict__ tiles, int64_t n,
                                                                uint32_t* __restrict__ off, uint32_t* __restrict__ sums) {
+  pdl_begin();
   __shared__ uint32_t s_w[32];
   const int64_t g = int64_t(blockIdx.x) * kScanBlock + threadIdx.x;
   const uint32_t v = g < n ? uint32_t(max(tiles[g], 0)) : 0u;
@@ -654,6 +660,7 @@ __global__ void __launch_bounds__(kScanBlock) det_count_kernel(const int32_t* __
 }
 
 __global__ void __launch_bounds__(kScanBlock) det_sums_kernel(uint32_t* __restrict__ sums, int64_t blocks) {
+  pdl_begin();
   __shared__ uint32_t s_run;
   if (threadIdx.x == 0) s_run = 0u;
   __syncthreads();
@@ -691,6 +698,7 @@ __global__ void __launch_bounds__(kScanBlock) det_sums_kernel(uint32_t* __restri
 }
 
 __global__ void det_add_kernel(uint32_t* __restrict__ off, const uint32_t* __restrict__ sums, int64_t n) {
+  pdl_begin();
   const int64_t g = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (g < n) off[g] += sums[g / kScanBlock];
 }
@@ -699,6 +707,7 @@ __global__ void det_add_kernel(uint32_t* __restrict__ off, const uint32_t* __res
 __global__ void det_inverse_kernel(const uint32_t* __restrict__ ids, const int2* __restrict__ ranges,
                                    const int4* __restrict__ rect, const uint32_t* __restrict__ off, int tiles_x,
                                    int64_t tiles, uint32_t* __restrict__ inv) {
+  pdl_begin();
   const int64_t tile = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   if (tile >= tiles) return;
   const int tx = int(tile % tiles_x), ty = int(tile / tiles_x);
@@ -715,6 +724,7 @@ __global__ void det_reduce_kernel(const int32_t* __restrict__ tiles, const int4*
                                   const uint32_t* __restrict__ off, const uint32_t* __restrict__ inv,
                                   const float* __restrict__ part_rows, const int32_t* __restrict__ top,
                                   int tiles_x, int64_t n, float* __restrict__ grads2d) {
+  pdl_begin();
   const int64_t g = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (g >= n) return;
   float acc[kC];
@@ -802,13 +812,13 @@ extern "C" int gs_blend_backward_deterministic(const float* d_image, const gs_sp
                            grads2d, stream, tile_order, part_rows, top);
   if (st != GS_OK) return st;
   const int64_t blocks = (n + kScanBlock - 1) / kScanBlock;
-  det_count_kernel<<<unsigned(blocks), kScanBlock, 0, s>>>(splats->tiles_touched, n, off, sums);
-  det_sums_kernel<<<1, kScanBlock, 0, s>>>(sums, blocks);
-  det_add_kernel<<<unsigned((n + 255) / 256), 256, 0, s>>>(off, sums, n);
+  launch_pdl(det_count_kernel, unsigned(blocks), kScanBlock, 0, s, splats->tiles_touched, n, off, sums);
+  launch_pdl(det_sums_kernel, 1, kScanBlock, 0, s, sums, blocks);
+  launch_pdl(det_add_kernel, unsigned((n + 255) / 256), 256, 0, s, off, sums, n);
   const int4* rect = reinterpret_cast<const int4*>(splats->rect);
-  det_inverse_kernel<<<unsigned((tiles * 32 + 255) / 256), 256, 0, s>>>(
+  launch_pdl(det_inverse_kernel, unsigned((tiles * 32 + 255) / 256), 256, 0, s, 
       sorted_ids, reinterpret_cast<const int2*>(ranges), rect, off, tiles_x, tiles, inv);
-  det_reduce_kernel<<<unsigned((n + 255) / 256), 256, 0, s>>>(splats->tiles_touched, rect, off, inv, part_rows, top,
+  launch_pdl(det_reduce_kernel, unsigned((n + 255) / 256), 256, 0, s, splats->tiles_touched, rect, off, inv, part_rows, top,
                                                               tiles_x, n, grads2d);
   return check_launch();
 }

@@ -326,6 +326,7 @@ __global__ void __launch_bounds__(kFixThreads, 6) blend_exact_kernel(const float
                                                                  int tiles_x, float3 bg, float* __restrict__ image,
                                                                  float* __restrict__ t_final,
                                                                  int32_t* __restrict__ last, int32_t* fix) {
+  pdl_begin();
   __shared__ FixShared sh;
   const int count = *reinterpret_cast<volatile int32_t*>(fix);
   for (;;) {
@@ -352,6 +353,7 @@ blend_fwd_kernel(const float4* __restrict__ rec, const uint32_t* __restrict__ id
                  int width, int height, int tiles_x, int tile0, float3 bg, float* __restrict__ image,
                  float* __restrict__ t_final, int32_t* __restrict__ last, const int32_t* __restrict__ tile_order,
                  int32_t* __restrict__ tile_work, int32_t* __restrict__ fix, const __grid_constant__ CUtensorMap tmap) {
+  pdl_begin();
   extern __shared__ __align__(128) unsigned char smem_raw[];
 #if GS_FWD_TMA
   FwdStage* stages = reinterpret_cast<FwdStage*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
@@ -548,12 +550,12 @@ int launch(const int32_t* order, int32_t* work, const float4* rec, int64_t n, co
     cudaError_t e = cudaMemsetAsync(fix, 0, 2 * sizeof(int32_t), s);
     if (e != cudaSuccess) return record_cuda_error(e);
   }
-  blend_fwd_kernel<kTraining><<<unsigned(ntiles * kParts), kThreads, kSmemBytes, s>>>(rec, ids, rg, width, height, tiles_x,
+  launch_pdl(blend_fwd_kernel<kTraining>, unsigned(ntiles * kParts), kThreads, kSmemBytes, s, rec, ids, rg, width, height, tiles_x,
                                                                              tile0, bg, image, t_final, last,
                                                                              order, work, fix, tmap);
   int st = check_launch();
   if (st != GS_OK || !kTraining) return st;
-  blend_exact_kernel<<<148 * 6, kFixThreads, 0, s>>>(rec, ids, rg, width, tiles_x, bg, image, t_final, last, fix);
+  launch_pdl(blend_exact_kernel, 148 * 6, kFixThreads, 0, s, rec, ids, rg, width, tiles_x, bg, image, t_final, last, fix);
   return check_launch();
 }
 

@@ -104,6 +104,7 @@ __device__ __forceinline__ double block_sum384(double v, double* red) {
 __global__ void __launch_bounds__(kLossThreads)
 ssim_forward_kernel(const float* __restrict__ img, const float* __restrict__ gt, int W, int H, Window win,
                     double d_map, float* __restrict__ src, double* __restrict__ sums) {
+  pdl_begin();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   FwdSmem& sm = *reinterpret_cast<FwdSmem*>(smem_raw);
   const int t = threadIdx.x;
@@ -234,6 +235,7 @@ ssim_forward_kernel(const float* __restrict__ img, const float* __restrict__ gt,
 __global__ void __launch_bounds__(kLossThreads)
 ssim_backward_kernel(const float* __restrict__ img, const float* __restrict__ gt, const float* __restrict__ src,
                      int W, int H, Window win, float l1_scale, float* __restrict__ d_image) {
+  pdl_begin();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   BwdSmem& sm = *reinterpret_cast<BwdSmem*>(smem_raw);
   const int t = threadIdx.x;
@@ -308,6 +310,7 @@ constexpr int kFinThreads = 1024;
 __global__ void __launch_bounds__(kFinThreads) loss_finalize_kernel(const double* __restrict__ part, int64_t blocks,
                                                                     double count, double lambda,
                                                                     float* __restrict__ loss) {
+  pdl_begin();
   __shared__ double red[3][kFinThreads];
   // strided per thread with four loads in flight, then a fixed tree: the
   // summation order depends only on the block count (deterministic)
@@ -382,13 +385,13 @@ extern "C" int gs_l1_dssim_loss(const float* image, const float* target, int32_t
   }
   const dim3 grid((width + kTW - 1) / kTW, (height + kTH - 1) / kTH);
   // d_map = -lambda / (2 count) everywhere (optimizer.py:159)
-  ssim_forward_kernel<<<grid, kLossThreads, sizeof(FwdSmem), s>>>(image, target, width, height, win,
+  launch_pdl(ssim_forward_kernel, grid, kLossThreads, sizeof(FwdSmem), s, image, target, width, height, win,
                                                                    -lambda / (2.0 * count), src, sums);
   int st = check_launch();
   if (st != GS_OK) return st;
-  ssim_backward_kernel<<<grid, kLossThreads, sizeof(BwdSmem), s>>>(image, target, src, width, height, win,
+  launch_pdl(ssim_backward_kernel, grid, kLossThreads, sizeof(BwdSmem), s, image, target, src, width, height, win,
                                                                     float((1.0 - lambda) / count), d_image);
   if ((st = check_launch()) != GS_OK) return st;
-  loss_finalize_kernel<<<1, kFinThreads, 0, s>>>(sums, int64_t(loss_blocks(width, height)), count, lambda, loss_out);
+  launch_pdl(loss_finalize_kernel, 1, kFinThreads, 0, s, sums, int64_t(loss_blocks(width, height)), count, lambda, loss_out);
   return check_launch();
 }

@@ -308,6 +308,7 @@ __global__ void __launch_bounds__(128, 4)
 preprocess_bwd_kernel(gs_params_t p, DevCamera cam, int degree, const float4* __restrict__ rec,
                       const int32_t* __restrict__ radii, const float4* __restrict__ g2d, gs_grads_t out,
                       int accumulate, gs_stats_t stats, const int32_t* __restrict__ stats_skip) {
+  pdl_begin();
   __shared__ float4 s_sh[128 * kShStride];
   if (stats_skip != nullptr && *stats_skip != 0) stats = gs_stats_t{nullptr, nullptr, nullptr};
   const int64_t g0 = int64_t(blockIdx.x) * blockDim.x;
@@ -389,6 +390,7 @@ __global__ void __launch_bounds__(128, GS_BWDADAM_MINB)
 preprocess_bwd_adam_kernel(gs_params_t p, DevCamera cam, int degree, const float4* __restrict__ rec,
                            const int32_t* __restrict__ radii, const float4* __restrict__ g2d, gs_grads_t out,
                            gs_stats_t stats, FusedAdam A, const int32_t* __restrict__ skip, NextView next) {
+  pdl_begin();
   // device-side step guard (gs_step_guard): a step whose loss is not finite
   // or whose binning overflowed applies nothing — parameters, moments and
   // statistics stay untouched, as the reference raises before updating (the
@@ -604,10 +606,10 @@ int launch_backward_adam(const gs_params_t* params, const gs_camera_t* camera, i
   const float4* rec = reinterpret_cast<const float4*>(splats->rec);
   const float4* g2 = reinterpret_cast<const float4*>(grads2d);
   if (project)
-    gs::preprocess_bwd_adam_kernel<true><<<grid, 128, smem, s>>>(*params, cam, active_sh_degree, rec, splats->radii,
+    gs::launch_pdl(gs::preprocess_bwd_adam_kernel<true>, grid, 128, smem, s, *params, cam, active_sh_degree, rec, splats->radii,
                                                                  g2, go, st, A, skip, next);
   else
-    gs::preprocess_bwd_adam_kernel<false><<<grid, 128, smem, s>>>(*params, cam, active_sh_degree, rec, splats->radii,
+    gs::launch_pdl(gs::preprocess_bwd_adam_kernel<false>, grid, 128, smem, s, *params, cam, active_sh_degree, rec, splats->radii,
                                                                   g2, go, st, A, skip, next);
   return gs::check_launch();
 }
@@ -649,6 +651,7 @@ extern "C" int gs_preprocess_backward_adam(const gs_params_t* params, const gs_c
 namespace gs {
 namespace {
 __global__ void step_guard_kernel(const float* loss, const int64_t* k_info, int32_t* skip, double* report) {
+  pdl_begin();
   const float v = loss[0];
   const int32_t sk = (k_info[1] != 0 || !isfinite(v)) ? 1 : 0;
   skip[0] = sk;
@@ -665,7 +668,7 @@ __global__ void step_guard_kernel(const float* loss, const int64_t* k_info, int3
 extern "C" int gs_step_guard(const float* loss, const int64_t* k_info, int32_t* skip, double* report,
                              void* stream) {
   if (!loss || !k_info || !skip) return GS_ERR_INVALID_ARG;
-  gs::step_guard_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(loss, k_info, skip, report);
+  gs::launch_pdl(gs::step_guard_kernel, 1, 1, 0, static_cast<cudaStream_t>(stream), loss, k_info, skip, report);
   return gs::check_launch();
 }
 
@@ -684,7 +687,7 @@ int preprocess_backward(const gs_params_t* params, const gs_camera_t* camera, in
   const DevCamera cam = make_dev_camera(*camera);
   const int block = 128;
   const unsigned grid = unsigned((params->n + block - 1) / block);
-  preprocess_bwd_kernel<<<grid, block, 0, s>>>(*params, cam, active_sh_degree,
+  launch_pdl(preprocess_bwd_kernel, grid, block, 0, s, *params, cam, active_sh_degree,
                                                reinterpret_cast<const float4*>(splats->rec), splats->radii,
                                                reinterpret_cast<const float4*>(grads2d), *grads, accumulate, st,
                                                skip);

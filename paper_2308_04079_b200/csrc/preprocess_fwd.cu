@@ -18,6 +18,7 @@ namespace {
 #endif
 __global__ void __launch_bounds__(128, GS_PREFWD_MINB)
 preprocess_fwd_kernel(gs_params_t p, DevCamera cam, int degree, gs_splats_t out) {
+  pdl_begin();
   const int64_t g0 = int64_t(blockIdx.x) * blockDim.x;
   const int64_t g = g0 + threadIdx.x;
   // The block's SH rows (one contiguous 192 B x 128 span) are bulk-prefetched
@@ -64,6 +65,6 @@ extern "C" int gs_preprocess_forward(const gs_params_t* params, const gs_camera_
   const gs::DevCamera cam = gs::make_dev_camera(*camera);
   const int block = 128;
   const unsigned grid = unsigned((params->n + block - 1) / block);
-  gs::preprocess_fwd_kernel<<<grid, block, 0, s>>>(*params, cam, active_sh_degree, *splats);
+  gs::launch_pdl(gs::preprocess_fwd_kernel, grid, block, 0, s, *params, cam, active_sh_degree, *splats);
   return gs::check_launch();
 }
