@@ -197,7 +197,7 @@ constexpr int kHistItems = 8;
 __global__ void __launch_bounds__(kThreads) depth_hist_kernel(const float* __restrict__ depth,
                                                              const int32_t* __restrict__ tiles, int64_t n,
                                                              uint32_t* __restrict__ hist, int64_t* __restrict__ kinfo) {
-  pdl_begin();
+  pdl_wait();
   __shared__ uint32_t s_h[kPasses * kRadix];
   for (int i = threadIdx.x; i < kPasses * kRadix; i += kThreads) s_h[i] = 0;
   __syncthreads();
@@ -258,7 +258,7 @@ __global__ void __launch_bounds__(1024) sort_setup_kernel(const uint32_t* __rest
                                                           uint32_t* __restrict__ digit_base,
                                                           const int32_t* __restrict__ status, int64_t capacity,
                                                           int64_t* __restrict__ kinfo) {
-  pdl_begin();
+  pdl_wait();
   __shared__ uint32_t s_w[32];
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;   // pass = t / 256 = warp / 8
   const uint32_t v = hist[t];
@@ -300,7 +300,7 @@ __global__ void __launch_bounds__(kThreads, GS_SORT_MIN_BLOCKS) onesweep_kernel(
     const uint32_t* __restrict__ keys_in, const uint32_t* __restrict__ ids_in, uint32_t* __restrict__ keys_out,
     uint32_t* __restrict__ ids_out, int4* __restrict__ drect_out, const uint32_t* __restrict__ digit_base,
     uint64_t* status, uint32_t* ticket, int shift, int64_t n, const int64_t* __restrict__ kinfo) {
-  pdl_begin();
+  pdl_wait();
   __shared__ uint32_t s_cnt[kWarps][kRadix];
   __shared__ uint32_t s_local[kRadix];
   __shared__ uint32_t s_delta[kRadix];
@@ -435,7 +435,7 @@ __global__ void __launch_bounds__(kThreads) bucket_count_kernel(const int4* __re
                                                                int64_t n, Grid g, uint32_t* __restrict__ M,
                                                                uint16_t* __restrict__ Mw, int64_t chunks,
                                                                const int64_t* __restrict__ kinfo) {
-  pdl_begin();
+  pdl_wait();
   extern __shared__ uint32_t s_h[];   // [kWarps][S]
   if (kinfo[1] != 0) return;
   for (int s = threadIdx.x; s < kWarps * g.S; s += kThreads) s_h[s] = 0u;
@@ -477,7 +477,7 @@ __global__ void __launch_bounds__(kThreads) bucket_count_kernel(const int4* __re
 // of one value per block).  *total_out = the sum.
 __global__ void __launch_bounds__(kThreads) scan_kernel(uint32_t* data, int64_t len, uint64_t* status, uint32_t* ticket,
                                                         uint32_t* total_out, const int64_t* __restrict__ kinfo) {
-  pdl_begin();
+  pdl_wait();
   __shared__ uint32_t s_w[33];
   __shared__ uint32_t s_block, s_excl;
   if (kinfo[1] != 0) return;
@@ -546,7 +546,7 @@ __global__ void __launch_bounds__(1024) window_setup_kernel(const uint32_t* __re
                                                             uint32_t* __restrict__ bstart, uint32_t* __restrict__ wstart,
                                                             uint32_t* __restrict__ wmap,
                                                             const int64_t* __restrict__ kinfo) {
-  pdl_begin();
+  pdl_wait();
   __shared__ uint32_t s_w[33];
   if (kinfo[1] != 0) return;
   constexpr int kPer = kMaxSuper / 1024;
@@ -601,7 +601,7 @@ __global__ void __launch_bounds__(kThreads) bucket_scatter_kernel(const int4* __
                                                                  const uint16_t* __restrict__ Mw, int64_t chunks,
                                                                  uint2* __restrict__ entries, int64_t capacity,
                                                                  const int64_t* __restrict__ kinfo) {
-  pdl_begin();
+  pdl_wait();
   extern __shared__ uint32_t s_cur[];   // [kWarps][S] cursors, then [kWarps][S] bytes of bucket stamps
   if (kinfo[1] != 0) return;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -783,7 +783,7 @@ __global__ void __launch_bounds__(kThreads) window_count_kernel(const uint2* __r
                                                                const uint32_t* __restrict__ wstart, Grid g,
                                                                uint32_t* __restrict__ cnt,
                                                                const int64_t* __restrict__ kinfo) {
-  pdl_begin();
+  pdl_wait();
   if (kinfo[1] != 0) return;
   const int lane = threadIdx.x & 31;
   const uint32_t nwin = wstart[g.S];
@@ -823,7 +823,7 @@ __global__ void __launch_bounds__(kThreads) window_prefix_kernel(const uint32_t*
                                                                 uint32_t* __restrict__ cnt,
                                                                 uint32_t* __restrict__ tile_total,
                                                                 const int64_t* __restrict__ kinfo) {
-  pdl_begin();
+  pdl_wait();
   if (kinfo[1] != 0) return;
   const uint32_t s = blockIdx.x * kWarps + (threadIdx.x >> 5);
   if (s >= uint32_t(g.S)) return;
@@ -864,7 +864,7 @@ __global__ void __launch_bounds__(kThreads) window_prefix_kernel(const uint32_t*
 __global__ void __launch_bounds__(1024) tile_ranges_kernel(const uint32_t* __restrict__ tile_total, int64_t tiles,
                                                            int2* __restrict__ ranges,
                                                            const int64_t* __restrict__ kinfo) {
-  pdl_begin();
+  pdl_wait();
   __shared__ uint32_t s_w[33];
   const bool flagged = kinfo[1] != 0;
   uint32_t carry = 0;
@@ -893,7 +893,7 @@ __global__ void __launch_bounds__(kThreads) instance_write_kernel(
     const uint32_t* __restrict__ wstart, Grid g, const uint32_t* __restrict__ cnt, const int2* __restrict__ ranges,
     const float* __restrict__ depth, uint32_t* __restrict__ ids, unsigned long long* __restrict__ keys,
     const int64_t* __restrict__ kinfo) {
-  pdl_begin();
+  pdl_wait();
   if (kinfo[1] != 0) return;
   const int lane = threadIdx.x & 31;
   const uint32_t nwin = wstart[g.S];
@@ -966,7 +966,7 @@ __global__ void __launch_bounds__(kThreads) instance_write_staged_kernel(
     const uint32_t* __restrict__ wstart, Grid g, const uint32_t* __restrict__ cnt, const int2* __restrict__ ranges,
     const float* __restrict__ depth, uint32_t* __restrict__ ids, unsigned long long* __restrict__ keys,
     const int64_t* __restrict__ kinfo) {
-  pdl_begin();
+  pdl_wait();
   extern __shared__ uint32_t s_ring[];
   __shared__ uint32_t s_eid[kWarps][32];
   if (kinfo[1] != 0) return;

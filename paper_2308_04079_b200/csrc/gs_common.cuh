@@ -9,6 +9,7 @@
 
 #include <cstdint>
 #include <cuda.h>
+#include <cstdlib>
 #include <utility>   // CUtensorMap (the TMA descriptor type; the encoder is fetched at run time)
 #include <cuda_runtime.h>
 
@@ -634,11 +635,37 @@ int check_launch();
 #define GS_PDL 1
 #endif
 
+#ifndef GS_PDL_TRIGGER
+#define GS_PDL_TRIGGER 1
+#endif
 __device__ __forceinline__ void pdl_begin() {
 #if GS_PDL
   asm volatile("griddepcontrol.wait;" ::: "memory");
+#if GS_PDL_TRIGGER
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 #endif
+#endif
+}
+
+// wait only: the successor launches when this grid's blocks exit (implicit
+// trigger).  The binning's kernels use it: an early trigger puts the next
+// kernel's waiting blocks beside the tail of the look-back passes (bin_and_sort
+// 0.485 ms with it, 0.471 without); the loss kernels gain from it (0.211 ->
+// 0.203 ms); the blends and the per-Gaussian kernels are indifferent.
+__device__ __forceinline__ void pdl_wait() {
+#if GS_PDL
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+}
+
+// GS_PDL_LAUNCH=0 in the environment launches every kernel without the
+// programmatic attribute (A/B measurements; read once)
+inline int pdl_launch_enabled() {
+  static const int on = [] {
+    const char* v = std::getenv("GS_PDL_LAUNCH");
+    return (v && v[0] == '0') ? 0 : 1;
+  }();
+  return on;
 }
 
 template <typename... KArgs, typename... Args>
@@ -651,7 +678,7 @@ inline void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t s
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = GS_PDL ? 1 : 0;
+  attr[0].val.programmaticStreamSerializationAllowed = (GS_PDL && pdl_launch_enabled()) ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);   // errors surface through check_launch()
