@@ -1177,8 +1177,7 @@ int bin_enqueue(const gs_splats_t* splats, int32_t width, int32_t height, void* 
   if (cap > 0 && (!sorted_ids || !ranges_raw)) return GS_ERR_INVALID_ARG;
   char* ws = static_cast<char*>(workspace);
   int2* ranges = reinterpret_cast<int2*>(ranges_raw);
-  cudaError_t e = cudaMemsetAsync(kinfo, 0, 3 * sizeof(int64_t), s);
-  if (e == cudaSuccess) e = cudaMemsetAsync(ws + L.zero, 0, L.zero_bytes, s);
+  cudaError_t e = zero_async(kinfo, 3 * sizeof(int64_t), ws + L.zero, L.zero_bytes, s);
   if (e != cudaSuccess) return record_cuda_error(e);
   if (n == 0) {
     if (ranges) e = cudaMemsetAsync(ranges, 0, size_t(L.tiles) * sizeof(int2), s);

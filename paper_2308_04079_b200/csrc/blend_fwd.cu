@@ -547,7 +547,7 @@ int launch(const int32_t* order, int32_t* work, const float4* rec, int64_t n, co
   }
   if (ntiles <= 0) return GS_OK;
   if (kTraining) {
-    cudaError_t e = cudaMemsetAsync(fix, 0, 2 * sizeof(int32_t), s);
+    cudaError_t e = zero_async(fix, 2 * sizeof(int32_t), nullptr, 0, s);
     if (e != cudaSuccess) return record_cuda_error(e);
   }
   launch_pdl(blend_fwd_kernel<kTraining>, unsigned(ntiles * kParts), kThreads, kSmemBytes, s, rec, ids, rg, width, height, tiles_x,

@@ -684,4 +684,30 @@ inline void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t s
   cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);   // errors surface through check_launch()
 }
 
+// Zero up to two word ranges as a programmatically launched kernel (a
+// cudaMemsetAsync node between two kernels would break the launch chain).
+static __global__ void zero_words_kernel(uint32_t* a, int64_t na, uint32_t* b, int64_t nb) {
+  pdl_begin();
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < na + nb; i += stride) {
+    if (i < na) a[i] = 0u;
+    else b[i - na] = 0u;
+  }
+}
+
+// bytes must be multiples of 4 (else a memset); returns the launch status
+inline cudaError_t zero_async(void* a, size_t a_bytes, void* b, size_t b_bytes, cudaStream_t s) {
+  if ((a_bytes | b_bytes) & 3u) {
+    cudaError_t e = a_bytes ? cudaMemsetAsync(a, 0, a_bytes, s) : cudaSuccess;
+    if (e == cudaSuccess && b_bytes) e = cudaMemsetAsync(b, 0, b_bytes, s);
+    return e;
+  }
+  const int64_t words = int64_t((a_bytes + b_bytes) / 4);
+  if (words == 0) return cudaSuccess;
+  const int64_t blocks = (words + 1023) / 1024;
+  launch_pdl(zero_words_kernel, unsigned(blocks < 148 * 8 ? blocks : 148 * 8), 256, 0, s,
+             static_cast<uint32_t*>(a), int64_t(a_bytes / 4), static_cast<uint32_t*>(b), int64_t(b_bytes / 4));
+  return cudaGetLastError();
+}
+
 }  // namespace gs

@@ -566,7 +566,7 @@ int launch_backward_adam(const gs_params_t* params, const gs_camera_t* camera, i
         !(next_camera->near_plane > 0))
       return GS_ERR_INVALID_ARG;
     if (next_splats->rec == splats->rec) return GS_ERR_INVALID_ARG;   // the kernel still reads this step's records
-    cudaError_t e = cudaMemsetAsync(next_splats->status, 0, sizeof(int32_t), s);
+    cudaError_t e = gs::zero_async(next_splats->status, sizeof(int32_t), nullptr, 0, s);
     if (e != cudaSuccess) return gs::record_cuda_error(e);
   }
   if (params->n == 0) return GS_OK;

@@ -59,7 +59,7 @@ extern "C" int gs_preprocess_forward(const gs_params_t* params, const gs_camera_
     return GS_ERR_INVALID_ARG;
   if (params->n < 0 || splats->n != params->n) return GS_ERR_INVALID_ARG;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  cudaError_t e = cudaMemsetAsync(splats->status, 0, sizeof(int32_t), s);
+  cudaError_t e = gs::zero_async(splats->status, sizeof(int32_t), nullptr, 0, s);
   if (e != cudaSuccess) return gs::record_cuda_error(e);
   if (params->n == 0) return GS_OK;
   const gs::DevCamera cam = gs::make_dev_camera(*camera);

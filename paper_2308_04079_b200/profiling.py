@@ -24,13 +24,15 @@ from collections import defaultdict
 import torch
 
 # our own __global__ kernels launched per training step (every one hand-written;
+# the buffers a stage must clear first are zeroed by a programmatically
+# launched kernel, counted with the stage;
 # blend_fwd: the blend + the exact re-blend of undecidable stops; blend_bwd:
 # the blend (its three tile-schedule kernels: blend_bwd_setup); bin_and_sort: depth histogram,
 # sort setup, 4 onesweep passes, bucket count, scan, window setup, bucket
 # scatter, window count, window prefix, tile ranges, instance write)
-KERNELS_PER_STEP = {"preprocess_fwd": 1, "bin_and_sort": 14, "blend_fwd": 2, "loss": 3, "blend_bwd": 1,
+KERNELS_PER_STEP = {"preprocess_fwd": 2, "bin_and_sort": 15, "blend_fwd": 3, "loss": 3, "blend_bwd": 1,
                     "blend_bwd_setup": 3,
-                    "preprocess_bwd": 1, "adam": 1, "preprocess_bwd_adam": 1, "preprocess_bwd_adam_project": 1,
+                    "preprocess_bwd": 1, "adam": 1, "preprocess_bwd_adam": 1, "preprocess_bwd_adam_project": 2,
                     "sharded_adam": 1}
 
 
