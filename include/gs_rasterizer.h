@@ -392,6 +392,14 @@ int gs_backward(const float* d_image, const gs_params_t* params, const gs_camera
                 const int32_t* ranges, const float* t_final, const int32_t* last, const float background[3],
                 int32_t* sched_scratch, float* grads2d, const gs_grads_t* grads, const gs_stats_t* stats,
                 void* stream);
+/* gs_backward after its setup was enqueued ahead (gs_blend_backward_schedule
+ * into sched_scratch and grads2d cleared, e.g. on a side stream while the
+ * loss runs): gs_blend_backward_accumulate + gs_preprocess_backward. */
+int gs_backward_prepared(const float* d_image, const gs_params_t* params, const gs_camera_t* camera,
+                         int32_t active_sh_degree, const gs_splats_t* splats, const uint32_t* sorted_ids,
+                         const int32_t* ranges, const float* t_final, const int32_t* last,
+                         const float background[3], const int32_t* sched_scratch, float* grads2d,
+                         const gs_grads_t* grads, const gs_stats_t* stats, void* stream);
 
 /* ---- adaptive density control: replaces
  * optimizer.densify_and_prune (optimizer.py:304-374).

@@ -133,6 +133,9 @@ SIGNATURES = [
     ("gs_backward", c_int32, [c_void_p, POINTER(GsParams), POINTER(GsCamera), c_int32, POINTER(GsSplats), c_void_p,
                               c_void_p, c_void_p, c_void_p, POINTER(c_float), c_void_p, c_void_p, POINTER(GsGrads),
                               POINTER(GsStats), c_void_p]),
+    ("gs_backward_prepared", c_int32, [c_void_p, POINTER(GsParams), POINTER(GsCamera), c_int32, POINTER(GsSplats),
+                                       c_void_p, c_void_p, c_void_p, c_void_p, POINTER(c_float), c_void_p, c_void_p,
+                                       POINTER(GsGrads), POINTER(GsStats), c_void_p]),
     ("gs_densify_workspace_size", c_int32, [c_int64, POINTER(c_size_t)]),
     ("gs_densify_classify", c_int32, [POINTER(GsCloudState), POINTER(GsStats), POINTER(GsDensifyConfig), c_void_p,
                                       c_size_t, POINTER(c_int64), POINTER(c_int64), c_void_p]),

@@ -35,3 +35,15 @@ extern "C" int gs_backward(const float* d_image, const gs_params_t* params, cons
   if (st != GS_OK) return st;
   return gs_preprocess_backward(params, camera, active_sh_degree, splats, grads2d, grads, 0, stats, stream);
 }
+
+extern "C" int gs_backward_prepared(const float* d_image, const gs_params_t* params, const gs_camera_t* camera,
+                                    int32_t active_sh_degree, const gs_splats_t* splats, const uint32_t* sorted_ids,
+                                    const int32_t* ranges, const float* t_final, const int32_t* last,
+                                    const float background[3], const int32_t* sched_scratch, float* grads2d,
+                                    const gs_grads_t* grads, const gs_stats_t* stats, void* stream) {
+  if (!camera || !splats || !grads || !sched_scratch) return GS_ERR_INVALID_ARG;
+  int st = gs_blend_backward_accumulate(d_image, splats, sorted_ids, ranges, t_final, last, camera->width,
+                                        camera->height, background, sched_scratch, grads2d, stream);
+  if (st != GS_OK) return st;
+  return gs_preprocess_backward(params, camera, active_sh_degree, splats, grads2d, grads, 0, stats, stream);
+}

@@ -794,9 +794,12 @@ class GaussianRasterizer(torch.autograd.Function):
     ResourceLimitError past 2^31 instances (rasterizer.py:99-101) — or
     CapacityError when the frame outgrew the instance-buffer hint (the hint is
     raised; re-run the step).  The first frame of a frame size bins
-    synchronously to learn its instance count.  Backward: one gs_backward
-    call (scheduled backward blend + backward_project, densify statistics when
-    `stats` is given), or the deterministic blend when deterministic=True."""
+    synchronously to learn its instance count.  The backward's tile schedule
+    and gradient-row clearing are enqueued on a side stream at the end of the
+    forward (prepare_backward), beside the caller's loss.  Backward: one
+    gs_backward_prepared call (scheduled backward blend + backward_project,
+    densify statistics when `stats` is given), or the deterministic blend when
+    deterministic=True."""
 
     @staticmethod
     def forward(ctx, means, log_scales, rotations, opacity_logits, sh, camera, background, active_sh_degree=3,
@@ -842,6 +845,9 @@ class GaussianRasterizer(torch.autograd.Function):
             k_report.copy_(binning.k_info, non_blocking=True)
             k_event = torch.cuda.Event()
             k_event.record(torch.cuda.current_stream(device))
+        # the backward's tile schedule and row clearing on a side stream, beside
+        # the caller's loss (gs_backward_prepared consumes them)
+        ctx.prep = None if deterministic else prepare_backward(out, splats, binning, W, H)
         ctx.save_for_backward(*tensors, splats.rec, splats.depth, splats.radii, splats.rect, splats.tiles_touched,
                               splats.status, binning.splat_ids, binning.ranges, out.final_transmittance,
                               out.last_contributor)
@@ -873,16 +879,16 @@ class GaussianRasterizer(torch.autograd.Function):
             _backward_project_tensors(params, n, device, camera, splats, g2, ctx.degree, ctx.stats, grads, False)
         else:
             tx, ty = ctx.tiles
-            sched = torch.empty(2 * tx * ty + 2048, dtype=torch.int32, device=device)
-            packed = torch.empty((n, _lib.GRAD2D_FLOATS), **z)
+            prep, ctx.prep = ctx.prep, None
             cs, cg = splats.c_struct(), grads.c_struct()
             cst = ctx.stats.c_struct() if ctx.stats is not None else None
-            _lib.check(_lib.load().gs_backward(
+            torch.cuda.current_stream(device).wait_event(prep.done)
+            _lib.check(_lib.load().gs_backward_prepared(
                 d_image.data_ptr(), ctypes.byref(params), ctypes.byref(camera.to_c()), ctx.degree, ctypes.byref(cs),
                 ids.data_ptr(), ranges.data_ptr(), t_final.data_ptr(), last.data_ptr(), _bg(ctx.background),
-                sched.data_ptr(), packed.data_ptr(), ctypes.byref(cg), ctypes.byref(cst) if cst is not None else None,
-                _stream()), "render_backward")
-            _tile_orders.put(ctx.okey, sched[:tx * ty])
+                prep.scratch.data_ptr(), prep.packed.data_ptr(), ctypes.byref(cg),
+                ctypes.byref(cst) if cst is not None else None, _stream()), "render_backward")
+            _tile_orders.put(ctx.okey, prep.scratch[:tx * ty])
         ctx.view_pos_grad_norm = grads.view_pos_grad_norm
         return (grads.d_means, grads.d_log_scales, grads.d_rotations, grads.d_opacity_logits, grads.d_sh,
                 None, None, None, None, None)

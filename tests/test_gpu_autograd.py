@@ -1,6 +1,7 @@
 """The drop-in torch.autograd.Function: GaussianRasterizer /
-rasterize_gaussians through the fused, sync-free gs_forward / gs_backward
-entry points, against the stage functions and the oracle."""
+rasterize_gaussians through the fused, sync-free gs_forward /
+gs_backward_prepared entry points, against the stage functions and the
+oracle; gs_backward (the single call with its own setup) against them."""
 import numpy as np
 import pytest
 import torch
@@ -50,6 +51,44 @@ def test_autograd_async_path_matches_stages_and_oracle(cuda_device):
     assert np.abs(image.detach().cpu().numpy() - fwd["image"]).max() <= 1e-4
     for leaf, key in zip(leaves, ("d_means", "d_log_scales", "d_rotations", "d_opacity_logits", "d_sh")):
         assert rel(leaf.grad.cpu().numpy(), og[key]) < 1e-3, key
+
+
+def test_gs_backward_matches_prepared_path(cuda_device):
+    """gs_backward (schedule + clearing + blend + backward_project in one call)
+    == prepare_backward + gs_backward_prepared (the autograd path)."""
+    import ctypes
+
+    from paper_2308_04079_b200 import _lib
+    w, h, bg = 240, 136, (0.2, 0.1, 0.0)
+    cloud_np, cam = synthetic.frustum_scene(15_000, w, h, seed=83)
+    cloud = GaussianCloud.from_numpy(**cloud_np)
+    d = torch.from_numpy(np.random.default_rng(4).uniform(-1, 1, (h, w, 3)).astype(np.float32) / (h * w)).cuda()
+    out, splats, binning = R.render_view(cloud, cam, bg, 3, training=True)
+    n, lib = len(cloud), _lib.load()
+    results = []
+    for prepared in (False, True):
+        z = dict(dtype=torch.float32, device="cuda")
+        grads = R.GaussianGrads(torch.empty((n, 3), **z), torch.empty((n, 4), **z), torch.empty((n, 3), **z),
+                                torch.empty(n, **z), torch.empty((n, 16, 3), **z), torch.empty(n, **z))
+        args = (d.data_ptr(), ctypes.byref(cloud.c_params()), ctypes.byref(cam.to_c()), 3,
+                ctypes.byref(splats.c_struct()), binning.splat_ids.data_ptr(), binning.ranges.data_ptr(),
+                out.final_transmittance.data_ptr(), out.last_contributor.data_ptr(), R._bg(bg))
+        if prepared:
+            prep = R.prepare_backward(out, splats, binning, w, h)
+            torch.cuda.current_stream().wait_event(prep.done)
+            _lib.check(lib.gs_backward_prepared(*args, prep.scratch.data_ptr(), prep.packed.data_ptr(),
+                                                ctypes.byref(grads.c_struct()), None, R._stream()), "bwd")
+        else:
+            tx, ty = R.tile_extent(w, h)
+            sched = torch.empty(2 * tx * ty + 2048, dtype=torch.int32, device="cuda")
+            packed = torch.empty((n, _lib.GRAD2D_FLOATS), **z)
+            _lib.check(lib.gs_backward(*args, sched.data_ptr(), packed.data_ptr(), ctypes.byref(grads.c_struct()),
+                                       None, R._stream()), "bwd")
+        torch.cuda.synchronize()
+        results.append(grads)
+    for key in ("d_means", "d_log_scales", "d_rotations", "d_opacity_logits", "d_sh"):
+        # same kernels and schedule; float REDs make the order nondeterministic
+        assert rel(getattr(results[1], key).cpu().numpy(), getattr(results[0], key).cpu().numpy()) < 1e-5, key
 
 
 def test_autograd_capacity_overflow_raises_then_recovers(cuda_device):
