@@ -125,7 +125,33 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
 ALLOC_EVENTS: list = []   # caching-allocator cudaMalloc / cudaFree / retry counts per timed loop
 
 
-def _time_loop(step, steps: int, world: int, dev) -> float:
+def _reserve_pool(dev, gib: float = 4.0) -> None:
+    """Allocate and free one large block: torch's caching allocator keeps it
+    as a splittable free segment, so later allocations are carved from it
+    instead of calling cudaMalloc (which can stall the stream)."""
+    import torch
+    t = torch.empty(int(gib * 2 ** 30), dtype=torch.uint8, device=dev)
+    del t
+
+
+def _paced(step, steps: int) -> None:
+    """steps untimed calls of step(i) with _time_loop's host pacing (the
+    warm-up: the caching allocator then already holds the blocks the timed
+    loop's in-flight steps need)."""
+    import torch
+    from collections import deque
+    inflight = deque()
+    for i in range(steps):
+        if len(inflight) >= 3:
+            inflight.popleft().synchronize()
+        step(i)
+        ev = torch.cuda.Event()
+        ev.record()
+        inflight.append(ev)
+    torch.cuda.synchronize()
+
+
+def _time_loop(step, steps: int, world: int, dev, prime=None) -> float:
     """Device milliseconds of `steps` calls of step(), max over ranks.  The
     device loop is enqueued without host synchronisation, so the GPU idles
     whenever the host falls behind; Python's cyclic garbage collector (a
@@ -142,7 +168,6 @@ def _time_loop(step, steps: int, world: int, dev) -> float:
     gc_was_enabled = gc.isenabled()
     if os.environ.get("GS_BENCH_GC") != "1":
         gc.disable()
-    m0 = torch.cuda.memory_stats(dev)
     # host pacing: before enqueuing step i the host waits for step i-3 to
     # finish on the device.  The GPU still has two steps queued (no bubble),
     # but the host no longer runs tens of steps ahead, each holding its
@@ -153,6 +178,12 @@ def _time_loop(step, steps: int, world: int, dev) -> float:
     inflight = deque()
     try:
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if prime is not None:
+            # one untimed step enqueued ahead of the start event, so the device
+            # is busy while the host enqueues timed step 0 (the start event
+            # completes when it does: the timed region holds exactly `steps`)
+            prime()
+        m0 = torch.cuda.memory_stats(dev)   # allocator events of the timed steps only
         s.record()
         for i in range(steps):
             if len(inflight) >= 3:
@@ -273,9 +304,12 @@ def run_single(args, local_rank: int) -> None:
     # the warm-up runs the timed path itself (it keeps the last step's
     # buffers alive like the timed steps do), so the caching allocator has
     # every block it needs before the timed region (no cudaMalloc inside it)
-    for _ in range(args.warmup):
-        train_step(target, True)
-    torch.cuda.synchronize()
+    _paced(lambda i: train_step(target, True), args.warmup)
+    # a cached free segment the timed loops can carve an odd extra buffer
+    # from: one cudaMalloc inside the timed region (the in-flight pattern of
+    # the paced loop differs slightly from the warm-up's) was measured to stall
+    # a step by up to 26 ms
+    _reserve_pool(dev)
     timer.events.clear()
     check_binned(binnings)
     clocks = ClockSampler(local_rank)
@@ -284,7 +318,8 @@ def run_single(args, local_rank: int) -> None:
     # rooflines); measured against the same loop without the stage events
     # (which serialise the programmatic launches at the six stage boundaries):
     # 315.6 vs 314.7 it/s, so the events cost nothing
-    ms = _time_loop(lambda i: train_step(target, True), args.steps, 1, dev)
+    ms = _time_loop(lambda i: train_step(target, True), args.steps, 1, dev,
+                    prime=lambda: train_step(target, True, stages=False))
     clock_info = clocks.stop()
     check_binned(binnings)   # every timed step binned within capacity (else the step is invalid)
     # evaluated (pixel, splat) pairs E, visible Gaussians and bucket entries of
@@ -389,11 +424,13 @@ def run_single(args, local_rank: int) -> None:
     # reference-shaped render_view (one host read of K per frame)
     fps_steps = max(args.steps, 10)
     sched = R.TileSchedule()
-    for _ in range(3):
-        R.render_view_async(cloud, cam, bg, DEGREE, schedule=sched)[2].check()
+    R.render_view_async(cloud, cam, bg, DEGREE, schedule=sched)[2].check()
     kinfos = []
+    _paced(lambda i: kinfos.append(R.render_view_async(cloud, cam, bg, DEGREE, schedule=sched)[2].k_info), 5)
     render_ms = _time_loop(lambda i: kinfos.append(R.render_view_async(cloud, cam, bg, DEGREE, schedule=sched)[2]
-                                                   .k_info), fps_steps, 1, dev) / fps_steps
+                                                   .k_info), fps_steps, 1, dev,
+                           prime=lambda: kinfos.append(R.render_view_async(cloud, cam, bg, DEGREE,
+                                                                           schedule=sched)[2].k_info)) / fps_steps
     check_binned(kinfos)
     for _ in range(3):
         R.render_view(cloud, cam, bg, DEGREE)
@@ -426,6 +463,7 @@ def run_single(args, local_rank: int) -> None:
         "render_fps": round(1e3 / render_ms, 2), "render_ms": round(render_ms, 4),
         "render_fps_sync": round(1e3 / render_sync_ms, 2),
         "stage_ms": {k: round(v, 4) for k, v in stage_ms.items()},
+        "stage_ms_min_median_max": timer.spread_ms(),
         "instances_per_view": k_last, "evaluated_pairs_per_view": e_pairs, "visible_gaussians": visible,
         "bucket_entries_per_view": entries,
         "e2e": {"value": round(args.steps / (e2e_ms / 1e3), 3), "unit": UNIT,
@@ -530,9 +568,8 @@ def c4_batches(args, rank: int, world: int, dev, steps: int, warmup: int) -> dic
     # the first view of each camera sizes its instance buffers synchronously
     for cam in cams:
         R.bin_and_sort(R._project_tensors(cloud.c_params(), n, dev, cam, DEGREE), WIDTH, HEIGHT)
-    for i in range(warmup):
-        step(i)
-    torch.cuda.synchronize()
+    _paced(step, warmup)
+    _reserve_pool(dev)
     check_binned(k_infos)
     ms = _time_loop(step, steps, world, dev)
     check_binned(k_infos)

@@ -80,6 +80,16 @@ class StageTimer:
         torch.cuda.synchronize()
         return {k: sum(s.elapsed_time(e) for s, e in v) / len(v) for k, v in self.events.items() if v}
 
+    def spread_ms(self) -> dict:
+        """Per stage (min, median, max) over the timed steps."""
+        torch.cuda.synchronize()
+        out = {}
+        for k, v in self.events.items():
+            if v:
+                t = sorted(s.elapsed_time(e) for s, e in v)
+                out[k] = [round(t[0], 4), round(t[len(t) // 2], 4), round(t[-1], 4)]
+        return out
+
     def launches_per_step(self) -> int:
         return sum(KERNELS_PER_STEP.get(k, 0) for k in self.events)
 

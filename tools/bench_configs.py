@@ -36,20 +36,34 @@ sys.path.insert(0, str(ROOT))
 
 def timed(fn, steps: int, warmup: int):
     """CUDA-event milliseconds per call; Python's cyclic GC is held off during
-    the timed calls (the loops are enqueued without host synchronisation)."""
+    the timed calls (the loops are enqueued without host synchronisation),
+    the host runs at most three calls ahead, and an 8 GiB block is allocated
+    and freed first so the caching allocator carves any new buffer from it."""
     import gc
+
+    from collections import deque
 
     import torch
     for _ in range(warmup):
         fn()
     gc.collect()
     torch.cuda.synchronize()
+    # a cached free segment for any buffer the timed steps add (a cudaMalloc
+    # inside the timed region can stall the stream); host paced two steps ahead
+    t = torch.empty(8 * 2 ** 30, dtype=torch.uint8, device="cuda")
+    del t
     gc.disable()
+    inflight = deque()
     try:
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.record()
         for _ in range(steps):
+            if len(inflight) >= 3:
+                inflight.popleft().synchronize()
             fn()
+            ev = torch.cuda.Event()
+            ev.record()
+            inflight.append(ev)
         e.record()
         torch.cuda.synchronize()
     finally:
