@@ -216,8 +216,8 @@ def run_single(args, local_rank: int) -> None:
     from paper_2308_04079_b200.cloud import GaussianCloud
     from paper_2308_04079_b200.loss import l1_dssim_loss
     from paper_2308_04079_b200.optimizer import DeviceAdam, TrainConfig
-    from paper_2308_04079_b200.profiling import (StageTimer, bucket_entries, evaluated_pairs, fp32_nominal_tflops,
-                                                  measure_fp32_peak)
+    from paper_2308_04079_b200.profiling import (KERNELS_PER_STEP, StageTimer, bucket_entries, evaluated_pairs,
+                                                  fp32_nominal_tflops, measure_fp32_peak)
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
@@ -482,7 +482,9 @@ def run_single(args, local_rank: int) -> None:
                                  "target H2D (on a copy stream beside the forward) and loss.item() every step"},
         alt_key: alt,
         "c4_1gpu": c4,
-        "gpu_launches": timer.launches_per_step() * args.steps,
+        # the stages' kernels plus the backward's three tile-schedule kernels
+        # that prepare_backward enqueues on the side stream (outside the stages)
+        "gpu_launches": (timer.launches_per_step() + KERNELS_PER_STEP["blend_bwd_setup"]) * args.steps,
         "roofline": roof["primary"], "roofline_hbm": roof["hbm"], "roofline_fp32": roof["fp32"],
         "roofline_stages": roof["stages"],
         "allocator_during_timed_loops": ALLOC_EVENTS[:4],
