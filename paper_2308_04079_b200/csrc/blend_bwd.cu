@@ -46,7 +46,7 @@ namespace {
 #define GS_WAIT_NS 2000
 #endif
 #ifndef GS_BWD_MIN_BLOCKS
-#define GS_BWD_MIN_BLOCKS 6  // half-tile CTAs: 64 registers, 6 CTAs (24 warps) per SM
+#define GS_BWD_MIN_BLOCKS 7  // half-tile CTAs: <= 56 registers (no spills), 7 CTAs (35 warps) per SM: 0.926 -> 0.907 ms (8: spills, 0.944)
 #endif
 #ifndef GS_BWD_EXACT_MASK
 #define GS_BWD_EXACT_MASK 0   // 1: exact ellipse-vs-block masks (slower since the ball test: 1.031 vs 0.994 ms)
