@@ -65,7 +65,12 @@ constexpr uint64_t kStAgg = uint64_t(1) << 32, kStPre = uint64_t(2) << 32;
 
 // super-tile buckets and walk windows
 constexpr int kMaxSuper = 4096;                 // bucket scatter keeps kWarps x S cursors in smem
-constexpr int kChunk = 4096;                    // Gaussians per bucketing block (512 per warp)
+// Gaussians per bucketing block, chosen per frame: small chunks give the
+// count / scatter more blocks, but M and Mw grow with S x chunks, so 1024 for
+// up to 512 super-tiles (1080p: 0.466 -> 0.456 ms) and 2048 above (4K, S =
+// 1020: 1.335 -> 1.304 ms with 2048 vs 4096; 1.446 with 1024)
+constexpr int kChunkSmall = 1024, kChunkLarge = 2048, kChunkSmallMaxS = 512;
+inline int chunk_for(int S) { return S <= kChunkSmallMaxS ? kChunkSmall : kChunkLarge; }
 #ifndef GS_BIN_WINDOW
 #define GS_BIN_WINDOW 1024
 #endif
@@ -429,6 +434,7 @@ __device__ __forceinline__ SuperRect super_rect(int4 rc, const Grid& g) {
 // ranges bucket_scatter's warps own): M[s * chunks + chunk] = their sum and
 // Mw[(chunk * kWarps + w) * S + s] (u16) the warp range's own count, from
 // which the scatter's warps take their cursor bases without recounting.
+template <int kChunk>
 __global__ void __launch_bounds__(kThreads) bucket_count_kernel(const int4* __restrict__ rect,
                                                                const uint32_t* __restrict__ order,
                                                                const uint32_t* __restrict__ hist, int4* __restrict__ drect,
@@ -594,7 +600,7 @@ __global__ void __launch_bounds__(1024) window_setup_kernel(const uint32_t* __re
 // rectangle clipped to the super-tile, local tile coordinates packed
 // x0 | y0 << 8 | x1 << 16 | y1 << 24).  (Staging the block's entries in
 // shared memory for coalesced writes measured slower: 116-133 vs 96 us at c3.)
-template <bool kOrBins>
+template <bool kOrBins, int kChunk>
 __global__ void __launch_bounds__(kThreads) bucket_scatter_kernel(const int4* __restrict__ drect,
                                                                  const uint32_t* __restrict__ order, int64_t n, Grid g,
                                                                  const uint32_t* __restrict__ M,
@@ -1063,7 +1069,7 @@ int make_grid(int width, int height, Grid* g) {
 
 struct Layout {
   Grid g;
-  int64_t n, cap, tiles, blocks, chunks, mlen, wmax;
+  int64_t n, cap, tiles, blocks, chunk, chunks, mlen, wmax;
   size_t zero, zero_bytes;                              // memset region
   size_t hist, tickets, mtotal, sort_status, scan_status;  // inside it
   size_t digit_base, keys_a, keys_b, ids_a, ids_b, order, drect, m, mw, bstart, wstart, wmap, entries, cnt, tile_total,
@@ -1079,7 +1085,8 @@ int layout(int64_t n, int width, int height, int64_t cap, Layout* L) {
   L->cap = cap;
   L->tiles = int64_t(L->g.tiles_x) * L->g.tiles_y;
   L->blocks = (n + kSortTile - 1) / kSortTile;
-  L->chunks = (n + kChunk - 1) / kChunk;
+  L->chunk = chunk_for(L->g.S);
+  L->chunks = (n + L->chunk - 1) / L->chunk;
   L->mlen = int64_t(L->g.S) * L->chunks;
   L->wmax = (cap + kWindow - 1) / kWindow + L->g.S;
   const size_t un = size_t(n > 0 ? n : 1), ub = size_t(L->blocks > 0 ? L->blocks : 1);
@@ -1163,6 +1170,45 @@ int walk(const Layout& L, char* ws, const float* depth, uint32_t* ids, int2* ran
   return check_launch();
 }
 
+// Step 2 of the binning (bucket counts, their scan, the window setup and the
+// ordered bucket scatter) for a chunk size.
+template <int kChunk>
+int bucket(const Layout& L, char* ws, const gs_splats_t* splats, const uint32_t* order, int4* drect,
+           const uint32_t* hist, uint32_t* tickets, int64_t cap, int64_t* kinfo, cudaStream_t s) {
+  const Grid g = L.g;
+  const int64_t n = L.n;
+  const int4* rect = reinterpret_cast<const int4*>(splats->rect);
+  uint32_t* M = at<uint32_t>(ws, L.m);
+  const size_t smem_count = sizeof(uint32_t) * kWarps * size_t(g.S);
+  uint16_t* Mw = at<uint16_t>(ws, L.mw);
+  cudaError_t e = smem_opt_in(reinterpret_cast<const void*>(bucket_count_kernel<kChunk>), smem_count);
+  if (e != cudaSuccess) return record_cuda_error(e);
+  launch_pdl(bucket_count_kernel<kChunk>, unsigned(L.chunks), kThreads, smem_count, s, rect, order, hist, drect, n, g,
+             M, Mw, L.chunks, kinfo);
+  int st = check_launch();
+  if (st != GS_OK) return st;
+  uint32_t* mtotal = at<uint32_t>(ws, L.mtotal);
+  launch_pdl(scan_kernel, unsigned((L.mlen + kScanTile - 1) / kScanTile), kThreads, 0, s, M, L.mlen,
+             at<uint64_t>(ws, L.scan_status), tickets + 4, mtotal, kinfo);
+  if ((st = check_launch()) != GS_OK) return st;
+  launch_pdl(window_setup_kernel, 1, 1024, 0, s, M, L.chunks, mtotal, g, at<uint32_t>(ws, L.bstart),
+             at<uint32_t>(ws, L.wstart), at<uint32_t>(ws, L.wmap), kinfo);
+  if ((st = check_launch()) != GS_OK) return st;
+  // cursors + OR bins (<= 2048 super-tiles) or cursors + byte stamps
+  const bool or_bins = g.S <= 2048;
+  const size_t smem_scatter = (sizeof(uint32_t) + (or_bins ? sizeof(uint32_t) : 1)) * kWarps * size_t(g.S);
+  const void* scatter_fn = or_bins ? reinterpret_cast<const void*>(bucket_scatter_kernel<true, kChunk>)
+                                   : reinterpret_cast<const void*>(bucket_scatter_kernel<false, kChunk>);
+  if ((e = smem_opt_in(scatter_fn, smem_scatter)) != cudaSuccess) return record_cuda_error(e);
+  if (or_bins)
+    launch_pdl(bucket_scatter_kernel<true, kChunk>, unsigned(L.chunks), kThreads, smem_scatter, s, drect, order, n, g,
+               M, Mw, L.chunks, at<uint2>(ws, L.entries), cap, kinfo);
+  else
+    launch_pdl(bucket_scatter_kernel<false, kChunk>, unsigned(L.chunks), kThreads, smem_scatter, s, drect, order, n,
+               g, M, Mw, L.chunks, at<uint2>(ws, L.entries), cap, kinfo);
+  return check_launch();
+}
+
 // The whole binning, enqueued on `s` without synchronising.  ranges /
 // sorted_ids may be NULL only with capacity 0 (K and the flags only).
 int bin_enqueue(const gs_splats_t* splats, int32_t width, int32_t height, void* workspace, size_t workspace_bytes,
@@ -1221,34 +1267,9 @@ int bin_enqueue(const gs_splats_t* splats, int32_t width, int32_t height, void* 
                                                            sort_status + 3 * pass_status, tickets + 3, 24, n, kinfo);
   if ((st = check_launch()) != GS_OK) return st;
   // 2. super-tile buckets
-  uint32_t* M = at<uint32_t>(ws, L.m);
-  const size_t smem_count = sizeof(uint32_t) * kWarps * size_t(g.S);
-  uint16_t* Mw = at<uint16_t>(ws, L.mw);
-  if ((e = smem_opt_in(reinterpret_cast<const void*>(bucket_count_kernel), smem_count)) != cudaSuccess)
-    return record_cuda_error(e);
-  launch_pdl(bucket_count_kernel, unsigned(L.chunks), kThreads, smem_count, s, rect, order, hist, drect, n, g, M, Mw, L.chunks,
-                                                                       kinfo);
-  if ((st = check_launch()) != GS_OK) return st;
-  uint32_t* mtotal = at<uint32_t>(ws, L.mtotal);
-  launch_pdl(scan_kernel, unsigned((L.mlen + kScanTile - 1) / kScanTile), kThreads, 0, s, 
-      M, L.mlen, at<uint64_t>(ws, L.scan_status), tickets + 4, mtotal, kinfo);
-  if ((st = check_launch()) != GS_OK) return st;
-  launch_pdl(window_setup_kernel, 1, 1024, 0, s, M, L.chunks, mtotal, g, at<uint32_t>(ws, L.bstart),
-                                         at<uint32_t>(ws, L.wstart), at<uint32_t>(ws, L.wmap), kinfo);
-  if ((st = check_launch()) != GS_OK) return st;
-  // cursors + OR bins (<= 2048 super-tiles) or cursors + byte stamps
-  const bool or_bins = g.S <= 2048;
-  const size_t smem_scatter = (sizeof(uint32_t) + (or_bins ? sizeof(uint32_t) : 1)) * kWarps * size_t(g.S);
-  const void* scatter_fn = or_bins ? reinterpret_cast<const void*>(bucket_scatter_kernel<true>)
-                                   : reinterpret_cast<const void*>(bucket_scatter_kernel<false>);
-  if ((e = smem_opt_in(scatter_fn, smem_scatter)) != cudaSuccess) return record_cuda_error(e);
-  if (or_bins)
-    launch_pdl(bucket_scatter_kernel<true>, unsigned(L.chunks), kThreads, smem_scatter, s, drect, order, n, g, M, Mw, L.chunks,
-                                                                      at<uint2>(ws, L.entries), cap, kinfo);
-  else
-    launch_pdl(bucket_scatter_kernel<false>, unsigned(L.chunks), kThreads, smem_scatter, s, drect, order, n, g, M, Mw, L.chunks,
-                                                                       at<uint2>(ws, L.entries), cap, kinfo);
-  if ((st = check_launch()) != GS_OK) return st;
+  st = L.chunk == kChunkSmall ? bucket<kChunkSmall>(L, ws, splats, order, drect, hist, tickets, cap, kinfo, s)
+                              : bucket<kChunkLarge>(L, ws, splats, order, drect, hist, tickets, cap, kinfo, s);
+  if (st != GS_OK) return st;
   // 3-5. windows, ranges, instance lists
   unsigned long long* k64 = reinterpret_cast<unsigned long long*>(keys);
   switch (g.lq) {
