@@ -103,7 +103,7 @@ __device__ __forceinline__ void st_status(uint64_t* p, uint64_t v) {
 // (base + p * stride) GS_LOOKBACK at a time (one memory round trip each)
 // until an inclusive prefix is met.
 #ifndef GS_LOOKBACK
-#define GS_LOOKBACK 8
+#define GS_LOOKBACK 4   // predecessors per round trip: 2 / 3 / 4 / 6 / 8 -> 0.457 / 0.453 / 0.454 / 0.457 / 0.462 ms at c3
 #endif
 __device__ __forceinline__ uint32_t look_back(const uint64_t* base, int64_t stride, int64_t b) {
   constexpr int kW = GS_LOOKBACK;   // predecessors read per memory round trip
