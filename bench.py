@@ -392,11 +392,13 @@ def run_single(args, local_rank: int) -> None:
 
     copy_stream = torch.cuda.Stream(dev)
 
-    def autograd_step(_):
+    pending_loss = [None]
+
+    def autograd_step(i, last=None):
         ag_it[0] += 1
         # the target's H2D copy on a copy stream beside the forward (the loss
-        # waits for it); the previous step's loss, its last reader, finished
-        # before loss.item() returned
+        # waits for it; the copy waits for the previous step's loss, its last
+        # reader, through wait_stream)
         main = torch.cuda.current_stream(dev)
         copy_stream.wait_stream(main)
         with torch.cuda.stream(copy_stream):
@@ -410,10 +412,18 @@ def run_single(args, local_rank: int) -> None:
         ag_adam.step(ag_cloud, g, ag_it[0], config)
         for leaf in leaves:
             leaf.grad = None
-        return float(loss[0].item())
+        # every step's loss is read on the host: the previous step's once this
+        # step is enqueued (a logging loop's pattern, so the device does not
+        # idle while the host enqueues the next step), the last one at once
+        prev, pending_loss[0] = pending_loss[0], loss
+        value = float(prev[0].item()) if prev is not None else None
+        is_last = (i == args.steps - 1) if last is None else last
+        if is_last:
+            value, pending_loss[0] = float(loss[0].item()), None
+        return value
 
     for i in range(args.warmup):
-        autograd_step(i)
+        autograd_step(i, last=i == args.warmup - 1)
     ag_ms = _time_loop(autograd_step, args.steps, 1, dev)
     del leaves, ag_cloud, ag_adam, ag_stats, initial
 
@@ -479,7 +489,9 @@ def run_single(args, local_rank: int) -> None:
                          "h2d_bytes_per_step": WIDTH * HEIGHT * 3 * 4, "d2h_bytes_per_step": 4 + 24,
                          "path": "rasterize_gaussians (GaussianRasterizer.apply: gs_forward / gs_backward) on leaf "
                                  "tensors + device L1/D-SSIM + autograd backward + Adam on the leaf gradients; "
-                                 "target H2D (on a copy stream beside the forward) and loss.item() every step"},
+                                 "target H2D (on a copy stream beside the forward) every step; every step's loss "
+                                 "read D2H (loss.item() of the previous step once the next is enqueued, the "
+                                 "last step's inside the timed region)"},
         alt_key: alt,
         "c4_1gpu": c4,
         # the stages' kernels plus the backward's three tile-schedule kernels
