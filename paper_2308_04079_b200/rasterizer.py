@@ -847,7 +847,8 @@ class GaussianRasterizer(torch.autograd.Function):
             k_event.record(torch.cuda.current_stream(device))
         # the backward's tile schedule and row clearing on a side stream, beside
         # the caller's loss (gs_backward_prepared consumes them)
-        ctx.prep = None if deterministic else prepare_backward(out, splats, binning, W, H)
+        ctx.prep = (prepare_backward(out, splats, binning, W, H)
+                    if not deterministic and any(ctx.needs_input_grad[:5]) else None)
         ctx.save_for_backward(*tensors, splats.rec, splats.depth, splats.radii, splats.rect, splats.tiles_touched,
                               splats.status, binning.splat_ids, binning.ranges, out.final_transmittance,
                               out.last_contributor)
@@ -880,6 +881,9 @@ class GaussianRasterizer(torch.autograd.Function):
         else:
             tx, ty = ctx.tiles
             prep, ctx.prep = ctx.prep, None
+            if prep is None:   # (no parameter required a gradient at forward time)
+                prep = prepare_backward(RenderOutput(None, t_final, last), splats, TileBinning(ids, ranges, *ctx.tiles),
+                                        camera.width, camera.height)
             cs, cg = splats.c_struct(), grads.c_struct()
             cst = ctx.stats.c_struct() if ctx.stats is not None else None
             torch.cuda.current_stream(device).wait_event(prep.done)
