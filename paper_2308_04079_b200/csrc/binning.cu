@@ -1007,19 +1007,24 @@ __global__ void __launch_bounds__(kThreads) instance_write_staged_kernel(
       // lane t: the entries (bit k = entry eb + k) covering tile t, in depth order
       uint32_t col = transpose32(cover_mask(ent.y), lane);
       __syncwarp();
-      const int rounds = __reduce_max_sync(0xffffffffu, uint32_t(__popc(col)));
-      // branch-free rounds on raw shared addresses: a lane whose column is
-      // exhausted rewrites its current ring slot with the entry-0 id (the slot
-      // is past its staged ids and is overwritten before it is flushed)
+      const uint32_t cnt = uint32_t(__popc(col));
+      const int rounds = __reduce_max_sync(0xffffffffu, cnt);
+      // branch-free rounds on raw shared addresses.  The column is bit-reversed
+      // once, so the leading one (one CLZ) is the next entry in depth order;
+      // round r writes ring slot wp + r: a lane whose column is exhausted
+      // writes past its staged ids (slots < fp + 64, since wp - fp < 32 before
+      // and rounds <= 32), which are overwritten before they are flushed
+      uint32_t colr = __brev(col);
+      uint32_t wb = 4u * (wp & (kRing - 1));
       for (int r = 0; r < rounds; ++r) {
-        const uint32_t live = col != 0u ? 1u : 0u;
-        const uint32_t bit = uint32_t(__ffs(col) - 1) & 31u;
+        const uint32_t k = uint32_t(__clz(colr)) & 31u;   // 32 (exhausted) -> 0
         uint32_t id;
-        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(id) : "r"(eid_s + 4u * bit) : "memory");
-        asm volatile("st.shared.u32 [%0], %1;" ::"r"(mine_s + 4u * (wp & (kRing - 1))), "r"(id) : "memory");
-        wp += live;
-        col &= col - 1u;
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(id) : "r"(eid_s + 4u * k) : "memory");
+        asm volatile("st.shared.u32 [%0], %1;" ::"r"(mine_s + wb), "r"(id) : "memory");
+        wb = (wb + 4u) & (4u * kRing - 1u);
+        colr &= 0x7FFFFFFFu >> k;   // clears the leading one (no-op on an exhausted column)
       }
+      wp += cnt;
       __syncwarp();
       // at most 32 ids were staged since the last flush, so a lane holds < 64
       uint32_t full = __ballot_sync(0xffffffffu, wp - fp >= 32u);
