@@ -1028,9 +1028,9 @@ __global__ void __launch_bounds__(kThreads) instance_write_staged_kernel(
       __syncwarp();
       // at most 32 ids were staged since the last flush, so a lane holds < 64
       uint32_t full = __ballot_sync(0xffffffffu, wp - fp >= 32u);
-      while (full) {
-        const int f = __ffs(full) - 1;
-        full &= full - 1;
+      while (full) {   // any order (distinct destinations): highest lane first, one FLO per pick
+        const int f = 31 - __clz(full);
+        full ^= 1u << f;
         flush(f, __shfl_sync(0xffffffffu, fp, f), __shfl_sync(0xffffffffu, cur, f), 32u,
               kKeys ? __shfl_sync(0xffffffffu, tile, f) : int64_t(0));
         if (lane == f) {
@@ -1042,8 +1042,8 @@ __global__ void __launch_bounds__(kThreads) instance_write_staged_kernel(
     }
     uint32_t rest = __ballot_sync(0xffffffffu, wp != fp);
     while (rest) {
-      const int f = __ffs(rest) - 1;
-      rest &= rest - 1;
+      const int f = 31 - __clz(rest);
+      rest ^= 1u << f;
       flush(f, __shfl_sync(0xffffffffu, fp, f), __shfl_sync(0xffffffffu, cur, f),
             __shfl_sync(0xffffffffu, wp - fp, f), kKeys ? __shfl_sync(0xffffffffu, tile, f) : int64_t(0));
     }
