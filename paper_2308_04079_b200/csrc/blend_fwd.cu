@@ -166,6 +166,9 @@ __device__ __forceinline__ void produce_batch(FwdStage& st, RawRec& raw, const f
 // reference's).  Their product and colour are block prefix products over the
 // list prefix; then the candidates after L are visited in order until the
 // exact stop (1 - T_new > 0.9999), as the reference's sequential rule.
+#ifndef GS_FIX_CTAS_PER_SM
+#define GS_FIX_CTAS_PER_SM 6
+#endif
 constexpr int kFixThreads = 256, kFixItems = 2, kFixPass = kFixThreads * kFixItems;
 
 struct FixShared {
@@ -320,7 +323,7 @@ __device__ void exact_pixel(const float4* __restrict__ rec, const uint32_t* __re
 
 // Persistent CTAs take the listed pixels one at a time (fix[0] = count,
 // fix[1] = work counter, fix[2 + i] = pixel index).
-__global__ void __launch_bounds__(kFixThreads, 6) blend_exact_kernel(const float4* __restrict__ rec,
+__global__ void __launch_bounds__(kFixThreads, GS_FIX_CTAS_PER_SM) blend_exact_kernel(const float4* __restrict__ rec,
                                                                  const uint32_t* __restrict__ ids,
                                                                  const int2* __restrict__ ranges, int width,
                                                                  int tiles_x, float3 bg, float* __restrict__ image,
@@ -555,7 +558,7 @@ int launch(const int32_t* order, int32_t* work, const float4* rec, int64_t n, co
                                                                              order, work, fix, tmap);
   int st = check_launch();
   if (st != GS_OK || !kTraining) return st;
-  launch_pdl(blend_exact_kernel, 148 * 6, kFixThreads, 0, s, rec, ids, rg, width, tiles_x, bg, image, t_final, last, fix);
+  launch_pdl(blend_exact_kernel, 148 * GS_FIX_CTAS_PER_SM, kFixThreads, 0, s, rec, ids, rg, width, tiles_x, bg, image, t_final, last, fix);
   return check_launch();
 }
 
