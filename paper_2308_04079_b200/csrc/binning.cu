@@ -52,7 +52,10 @@ constexpr int64_t kFlagZeroQuat = 1, kFlagCapacity = 2, kFlagLimit = 4;
 // depth sort
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
-constexpr int kItems = 16;                     // scan items per thread
+#ifndef GS_SCAN_ITEMS
+#define GS_SCAN_ITEMS 16
+#endif
+constexpr int kItems = GS_SCAN_ITEMS;          // scan items per thread
 constexpr int kScanTile = kThreads * kItems;   // 4096 values per scan block
 #ifndef GS_SORT_ITEMS
 #define GS_SORT_ITEMS 12   // 3072 keys per block: 8 / 12 / 16 -> 0.454 / 0.446 / 0.457 ms at c3 (1.299 / 1.274 / 1.289 at 6M/4K)
